@@ -1,0 +1,320 @@
+"""Thin ctypes binding of libcppp.so (include/cppp.h) — argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only converts
+numpy arrays / torch tensors to pointers, allocates the device workspace through PyTorch
+(device memory and streams are PyTorch's; the library never owns a torch object), and turns
+status codes into exceptions.  There is no CPU fallback: if the library or a CUDA device is
+missing, every call raises.
+
+Function names mirror the C ABI: cp_init, cp_set_factors, cp_get_factors, mttkrp_dt,
+pp_build_operators, pp_get_operator, pp_get_single, pp_update, als_sweep,
+cp_set_phase_override, fitness, cppp_generate, cp_destroy.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcppp.so")
+
+PHASE_AUTO, PHASE_DT, PHASE_PP_BUILD, PHASE_PP = -1, 0, 1, 2
+PHASE_NAMES = {PHASE_DT: "dt", PHASE_PP_BUILD: "pp-build", PHASE_PP: "pp-approx"}
+PHASE_BY_NAME = {v: k for k, v in PHASE_NAMES.items()}
+FLAG_BORROW_TENSOR, FLAG_SIMT_TTM, FLAG_PROFILE, FLAG_NO_FUSED_TTV = 1, 2, 4, 8
+K_TTM, K_TTV, K_PPUPDATE, K_SOLVE, K_OTHER = range(5)
+KCLASS_NAMES = ["ttm", "ttv", "pp_update", "solve", "other"]
+
+
+class CpppError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"cppp status {status}: {msg}")
+        self.status = status
+
+
+class Opts(C.Structure):
+    _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t), ("flags", C.c_uint), ("shard_mode", C.c_int),
+                ("shard_offset", C.c_int64), ("shard_extent", C.c_int64),
+                ("nccl_unique_id", C.c_void_p), ("rank", C.c_int), ("world", C.c_int)]
+
+
+class SweepInfo(C.Structure):
+    _fields_ = [("sweep", C.c_int), ("phase", C.c_int), ("fitness", C.c_double),
+                ("residual_sq", C.c_double), ("grad_norm_sum", C.c_double),
+                ("max_rel_dA", C.c_double), ("next_phase", C.c_int), ("restarts", C.c_int),
+                ("converged", C.c_int), ("seconds", C.c_double)]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["phase"] = PHASE_NAMES.get(self.phase, str(self.phase))
+        d["next_phase"] = PHASE_NAMES.get(self.next_phase, str(self.next_phase))
+        return d
+
+
+class KernelStat(C.Structure):
+    _fields_ = [("launches", C.c_int64), ("total_ms", C.c_double), ("flops", C.c_double),
+                ("bytes", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libcppp.so (raises if it was not built — there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1811_10573_b200.build`")
+    L = C.CDLL(LIB_PATH)
+    P, I, D, V = C.c_void_p, C.c_int, C.c_double, None
+    sig = {
+        "cppp_default_opts": (V, [C.POINTER(Opts)]),
+        "cppp_workspace_bytes": (C.c_size_t, [I, C.POINTER(C.c_int64), I, C.POINTER(Opts)]),
+        "cp_init": (I, [C.POINTER(P), P, I, C.POINTER(C.c_int64), I, C.POINTER(Opts)]),
+        "cp_set_factors": (I, [P, C.POINTER(P)]),
+        "cp_get_factors": (I, [P, C.POINTER(P)]),
+        "cp_update_factors": (I, [P, C.POINTER(P)]),
+        "mttkrp_dt": (I, [P, C.POINTER(P)]),
+        "pp_build_operators": (I, [P]),
+        "pp_get_operator": (I, [P, I, I, P]),
+        "pp_get_single": (I, [P, I, P]),
+        "pp_update": (I, [P, I, P]),
+        "als_sweep": (I, [P, D, D, C.POINTER(SweepInfo)]),
+        "cp_set_phase_override": (I, [P, I]),
+        "fitness": (I, [P, C.POINTER(D)]),
+        "cppp_kernel_stats": (I, [P, I, C.POINTER(KernelStat)]),
+        "cppp_reset_kernel_stats": (I, [P]),
+        "cppp_generate": (I, [P, P, I, C.POINTER(C.c_int64), I, C.POINTER(P), I, D, C.c_uint64,
+                              C.c_int64, C.c_int64, P]),
+        "cppp_nccl_unique_id": (I, [P]),
+        "cppp_plan_describe": (C.c_size_t, [I, I, C.c_char_p, C.c_size_t]),
+        "cp_destroy": (V, [P]),
+        "cp_last_error": (C.c_char_p, [P]),
+        "cppp_status_string": (C.c_char_p, [I]),
+        "cppp_version": (C.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+EXPORTED = ["cppp_default_opts", "cppp_workspace_bytes", "cp_init", "cp_set_factors",
+            "cp_update_factors",
+            "cp_get_factors", "mttkrp_dt", "pp_build_operators", "pp_get_operator",
+            "pp_get_single", "pp_update", "als_sweep", "cp_set_phase_override", "fitness",
+            "cppp_kernel_stats", "cppp_reset_kernel_stats", "cppp_generate",
+            "cppp_nccl_unique_id", "cppp_plan_describe", "cp_destroy", "cp_last_error",
+            "cppp_status_string", "cppp_version"]
+
+
+# ------------------------------------------------------------------ marshalling helpers
+def _ptr(a) -> int:
+    """Data pointer of a C-contiguous float64 numpy array or torch tensor."""
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr()
+    if not (isinstance(a, np.ndarray) and a.flags.c_contiguous and a.dtype == np.float64):
+        raise ValueError("expected a C-contiguous float64 numpy array or torch tensor")
+    return a.ctypes.data
+
+
+def _ptrs(arrs) -> C.Array:
+    return (C.c_void_p * len(arrs))(*[_ptr(a) for a in arrs])
+
+
+def _check(ctx, status: int):
+    if status != 0:
+        msg = lib().cp_last_error(ctx.h if ctx is not None else None)
+        raise CpppError(status, (msg or b"").decode() or lib().cppp_status_string(status).decode())
+
+
+class Ctx:
+    """Handle returned by cp_init: owns the C context and keeps the torch workspace alive."""
+
+    def __init__(self):
+        self.h = C.c_void_p()
+        self.N = 0
+        self.K = 0
+        self.s: List[int] = []
+        self.local_rows: List[int] = []
+        self.keep = []
+
+    def __del__(self):
+        try:
+            cp_destroy(self)
+        except Exception:
+            pass
+
+
+def _torch_workspace(nbytes: int, device: int):
+    import torch
+    return torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+
+
+def cp_init(X, N: int, s: Sequence[int], K: int, *, device: int = 0, stream=None,
+            flags: int = 0, shard_offset: Optional[int] = None, shard_extent: Optional[int] = None,
+            nccl_unique_id: Optional[bytes] = None, rank: int = 0, world: int = 1,
+            torch_workspace: bool = True) -> Ctx:
+    """cp_init (include/cppp.h).  X: numpy array (host) or torch CUDA tensor (device; borrowed
+    with FLAG_BORROW_TENSOR).  The device workspace is a torch uint8 tensor unless
+    torch_workspace=False (then the library cudaMallocs it).  stream: a torch.cuda.Stream or
+    None (library-owned stream)."""
+    L = lib()
+    ctx = Ctx()
+    ctx.N, ctx.K, ctx.s = N, K, list(s)
+    o = Opts()
+    L.cppp_default_opts(C.byref(o))
+    o.device = device
+    o.flags = flags
+    if stream is not None:
+        o.stream = stream.cuda_stream
+    if shard_extent is not None:
+        o.shard_mode = 0
+        o.shard_offset = int(shard_offset)
+        o.shard_extent = int(shard_extent)
+    o.rank, o.world = rank, world
+    if nccl_unique_id is not None:
+        idbuf = C.create_string_buffer(bytes(nccl_unique_id), 128)
+        ctx.keep.append(idbuf)
+        o.nccl_unique_id = C.cast(idbuf, C.c_void_p)
+    dims = (C.c_int64 * N)(*s)
+    if torch_workspace:
+        nbytes = L.cppp_workspace_bytes(N, dims, K, C.byref(o))
+        if nbytes == 0:
+            raise CpppError(-1, "invalid problem for cppp_workspace_bytes")
+        ws = _torch_workspace(nbytes, device)
+        ctx.keep.append(ws)
+        o.workspace = ws.data_ptr()
+        o.workspace_bytes = nbytes
+    if hasattr(X, "data_ptr"):
+        ctx.keep.append(X)
+    st = L.cp_init(C.byref(ctx.h), _ptr(X), N, dims, K, C.byref(o))
+    _check(ctx, st)
+    ctx.local_rows = list(s)
+    if shard_extent is not None:
+        ctx.local_rows[0] = int(shard_extent)
+    return ctx
+
+
+def cp_set_factors(ctx: Ctx, A: Sequence) -> None:
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) if isinstance(a, np.ndarray) else a for a in A]
+    _check(ctx, lib().cp_set_factors(ctx.h, _ptrs(arrs)))
+
+
+def cp_update_factors(ctx: Ctx, A: Sequence) -> None:
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) if isinstance(a, np.ndarray) else a for a in A]
+    _check(ctx, lib().cp_update_factors(ctx.h, _ptrs(arrs)))
+
+
+def cp_get_factors(ctx: Ctx) -> List[np.ndarray]:
+    out = [np.empty((ctx.s[n], ctx.K)) for n in range(ctx.N)]
+    _check(ctx, lib().cp_get_factors(ctx.h, _ptrs(out)))
+    return out
+
+
+def mttkrp_dt(ctx: Ctx) -> List[np.ndarray]:
+    out = [np.empty((ctx.local_rows[n], ctx.K)) for n in range(ctx.N)]
+    _check(ctx, lib().mttkrp_dt(ctx.h, _ptrs(out)))
+    return out
+
+
+def pp_build_operators(ctx: Ctx) -> None:
+    _check(ctx, lib().pp_build_operators(ctx.h))
+
+
+def pp_get_operator(ctx: Ctx, i: int, j: int, out=None) -> np.ndarray:
+    if out is None:
+        out = np.empty((ctx.local_rows[i], ctx.local_rows[j], ctx.K))
+    _check(ctx, lib().pp_get_operator(ctx.h, i, j, _ptr(out)))
+    return out
+
+
+def pp_get_single(ctx: Ctx, n: int) -> np.ndarray:
+    out = np.empty((ctx.local_rows[n], ctx.K))
+    _check(ctx, lib().pp_get_single(ctx.h, n, _ptr(out)))
+    return out
+
+
+def pp_update(ctx: Ctx, n: int, out=None) -> np.ndarray:
+    if out is None:
+        out = np.empty((ctx.local_rows[n], ctx.K))
+    _check(ctx, lib().pp_update(ctx.h, n, _ptr(out)))
+    return out
+
+
+def als_sweep(ctx: Ctx, eps: float, eps_pp: float) -> dict:
+    info = SweepInfo()
+    _check(ctx, lib().als_sweep(ctx.h, eps, eps_pp, C.byref(info)))
+    return info.as_dict()
+
+
+def cp_set_phase_override(ctx: Ctx, phase) -> None:
+    if isinstance(phase, str):
+        phase = PHASE_BY_NAME[phase]
+    _check(ctx, lib().cp_set_phase_override(ctx.h, int(phase)))
+
+
+def fitness(ctx: Ctx) -> float:
+    f = C.c_double()
+    _check(ctx, lib().fitness(ctx.h, C.byref(f)))
+    return f.value
+
+
+def kernel_stats(ctx: Ctx) -> dict:
+    out = {}
+    for k, name in enumerate(KCLASS_NAMES):
+        st = KernelStat()
+        _check(ctx, lib().cppp_kernel_stats(ctx.h, k, C.byref(st)))
+        out[name] = dict(launches=st.launches, total_ms=st.total_ms, flops=st.flops, bytes=st.bytes)
+    return out
+
+
+def reset_kernel_stats(ctx: Ctx) -> None:
+    _check(ctx, lib().cppp_reset_kernel_stats(ctx.h))
+
+
+def cppp_generate(X_dev, s: Sequence[int], K: int, A_true: Sequence, noise_kind: int, noise: float,
+                  seed: int = 0, row_lo: int = 0, row_hi: Optional[int] = None, stream=None,
+                  ctx: Optional[Ctx] = None) -> None:
+    """Device twin of synthgen.make_tensor: X_dev (torch CUDA tensor) := rows [row_lo,row_hi)."""
+    N = len(s)
+    row_hi = s[0] if row_hi is None else row_hi
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) if isinstance(a, np.ndarray) else a for a in A_true]
+    dims = (C.c_int64 * N)(*s)
+    st = lib().cppp_generate(ctx.h if ctx else None, _ptr(X_dev), N, dims, K, _ptrs(arrs), noise_kind,
+                             noise, seed, row_lo, row_hi, stream.cuda_stream if stream is not None else None)
+    _check(ctx, st)
+
+
+def cppp_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = lib().cppp_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if st != 0:
+        raise CpppError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def cppp_plan_describe(N: int, shard_mode: int = -1) -> str:
+    need = lib().cppp_plan_describe(N, shard_mode, None, 0)
+    buf = C.create_string_buffer(need)
+    lib().cppp_plan_describe(N, shard_mode, buf, need)
+    return buf.value.decode()
+
+
+def cp_destroy(ctx: Ctx) -> None:
+    if ctx is not None and ctx.h:
+        lib().cp_destroy(ctx.h)
+        ctx.h = C.c_void_p()
+
+
+def cppp_version() -> str:
+    return lib().cppp_version().decode()

@@ -1,0 +1,1231 @@
+// engine.cu — the host-side engine behind the C ABI (include/cppp.h): workspace planning, the
+// regular dimension tree, the PP construction tree (Def. pptree), the Alg. 3 phase machine,
+// slab sharding with NCCL all-reduce, kernel-class profiling.
+//
+// Citations: P:n = PAPER.md line n; Lnn = SURVEY.md §8(c) / DESIGN.md reading nn.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cppp.h"
+#include "internal.h"
+
+using namespace cppp;
+
+namespace {
+
+constexpr size_t ALIGN = 256;
+inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
+inline int popc(uint32_t m) { return __builtin_popcount(m); }
+
+// ---------------------------------------------------------------- NCCL (dlopen'ed on demand)
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+    return getUniqueId && commInitRank && allReduce && commDestroy && getErrorString;
+  }
+};
+Nccl g_nccl;
+
+// ---------------------------------------------------------------- bump/stack allocator
+struct Stack {
+  char* base = nullptr;
+  size_t top = 0, peak = 0, cap = 0;
+  bool dry = true;
+  double* push(size_t doubles) {
+    size_t off = top;
+    top = align_up(top + doubles * sizeof(double));
+    peak = std::max(peak, top);
+    return dry ? reinterpret_cast<double*>(ALIGN) : reinterpret_cast<double*>(base + off);
+  }
+  size_t mark() const { return top; }
+  void release(size_t m) { top = m; }
+};
+
+struct Node {
+  uint32_t mask;   // kept modes
+  double* data;    // kept modes ascending, then K; root: X (no K)
+  bool root;
+};
+
+struct ProfPending {
+  int cls;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+
+}  // namespace
+
+struct cppp_ctx {
+  // problem
+  int N = 0, K = 0;
+  int64_t s[CPPP_MAX_ORDER] = {};    // global sizes
+  int64_t dl[CPPP_MAX_ORDER] = {};   // local sizes
+  int q = -1;                        // sharded mode (-1 none)
+  int64_t qoff = 0, qext = 0;
+  unsigned flags = 0;
+  int device = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  // memory
+  char* ws = nullptr;
+  char* ws_alloc = nullptr;
+  size_t ws_bytes = 0;
+  bool own_ws = false;
+  double* X = nullptr;
+  int64_t numel_local = 0;
+  double *A[CPPP_MAX_ORDER] = {}, *Ap[CPPP_MAX_ORDER] = {}, *dA[CPPP_MAX_ORDER] = {};
+  double *M[CPPP_MAX_ORDER] = {}, *Mp[CPPP_MAX_ORDER] = {}, *T[CPPP_MAX_ORDER] = {};
+  double* S_all = nullptr;   // N x K x K
+  double* Gamma = nullptr;   // K x K (of the last solved mode)
+  double* L = nullptr;       // 2 K x K
+  int* lmode = nullptr;
+  double* rowstat = nullptr; // max local rows x 3
+  double* stats = nullptr;   // N x 3 norms, then fitness terms [2], then ||X||² [1]
+  double* Fpad = nullptr;    // max s x 128
+  double* ops[CPPP_MAX_ORDER][CPPP_MAX_ORDER] = {};   // i<j
+  double* pp_partial = nullptr;
+  double* sq_partial = nullptr;
+  double* gath = nullptr;    // gather scratch (max s x K)
+  double* gen_scratch = nullptr;
+  Stack stack;
+  // state
+  double normX_sq = 0.0;
+  bool ops_valid = false;
+  bool factors_set = false;
+  int next_phase = CPPP_PHASE_DT;
+  int override_phase = CPPP_PHASE_AUTO;
+  int sweep = 0, restarts = 0;
+  double last_fitness = NAN;
+  double* host_stats = nullptr;  // pinned
+  // comm
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  // profiling
+  std::vector<ProfPending> pending;
+  std::vector<cudaEvent_t> evpool;
+  cppp_kernel_stat kstat[CPPP_K_COUNT] = {};
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  std::string err;
+  bool dry = false;   // planning pass: no launches
+};
+
+namespace {
+
+// ---------------------------------------------------------------- error plumbing
+cppp_status fail(cppp_ctx* c, cppp_status s, const char* fmt, ...) {
+  if (c) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return s;
+}
+
+#define CUCHK(c, expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail((c), CPPP_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+#define STCHK(expr)                    \
+  do {                                 \
+    cppp_status s_ = (expr);           \
+    if (s_ != CPPP_OK) return s_;      \
+  } while (0)
+
+// ---------------------------------------------------------------- profiling
+cudaEvent_t get_event(cppp_ctx* c) {
+  if (!c->evpool.empty()) {
+    cudaEvent_t e = c->evpool.back();
+    c->evpool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct Prof {
+  cppp_ctx* c;
+  int cls;
+  double flops, bytes;
+  cudaEvent_t a = nullptr;
+  Prof(cppp_ctx* c_, int cls_, double f, double b) : c(c_), cls(cls_), flops(f), bytes(b) {
+    if (!c->dry && (c->flags & CPPP_FLAG_PROFILE)) {
+      a = get_event(c);
+      cudaEventRecord(a, c->st);
+    }
+  }
+  ~Prof() {
+    if (a) {
+      cudaEvent_t b = get_event(c);
+      cudaEventRecord(b, c->st);
+      c->pending.push_back({cls, a, b, flops, bytes});
+    }
+  }
+};
+void prof_collect(cppp_ctx* c) {
+  if (c->pending.empty()) return;
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(p.b);
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    auto& k = c->kstat[p.cls];
+    k.launches += 1;
+    k.total_ms += ms;
+    k.flops += p.flops;
+    k.bytes += p.bytes;
+    c->evpool.push_back(p.a);
+    c->evpool.push_back(p.b);
+  }
+  c->pending.clear();
+}
+
+// ---------------------------------------------------------------- comm
+cppp_status allreduce(cppp_ctx* c, double* buf, size_t count) {
+  if (c->world <= 1 || c->dry || count == 0) return CPPP_OK;
+  ncclResult_t r = g_nccl.allReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, c->st);
+  if (r != ncclSuccess) return fail(c, CPPP_ENCCL, "ncclAllReduce: %s", g_nccl.getErrorString(r));
+  return CPPP_OK;
+}
+
+// ---------------------------------------------------------------- geometry helpers
+const double* fac_local(cppp_ctx* c, double* const* F, int u) {
+  return F[u] + (u == c->q ? c->qoff * c->K : 0);
+}
+double* fac_local_mut(cppp_ctx* c, double* const* F, int u) {
+  return F[u] + (u == c->q ? c->qoff * c->K : 0);
+}
+int64_t node_elems(cppp_ctx* c, uint32_t mask) {
+  int64_t e = c->K;
+  for (int v = 0; v < c->N; ++v)
+    if (mask & (1u << v)) e *= c->dl[v];
+  return e;
+}
+
+// out = contraction of `src` along mode u with factor F (local rows)
+cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, double* out) {
+  int64_t B = 1, R = 1;
+  for (int v = 0; v < c->N; ++v) {
+    if (!(src.mask & (1u << v)) || v == u) continue;
+    if (v < u) B *= c->dl[v];
+    else R *= c->dl[v];
+  }
+  const int64_t S = c->dl[u];
+  if (c->dry) return CPPP_OK;
+  const int K = c->K;
+  if (src.root) {
+    const double flops = 2.0 * B * S * R * K;
+    const double bytes = 8.0 * (B * S * R + B * R * K);
+    Prof p(c, CPPP_K_TTM, flops, bytes);
+    CUCHK(c, launch_ttm(src.data, B, S, R, F, K, out, c->Fpad,
+                        (c->flags & CPPP_FLAG_SIMT_TTM) != 0, c->st));
+  } else {
+    const double flops = 2.0 * B * S * R * K;
+    const double bytes = 8.0 * (B * S * R * K + B * R * K);
+    Prof p(c, CPPP_K_TTV, flops, bytes);
+    CUCHK(c, launch_ttv(src.data, B, S, R, K, F, out, c->st));
+  }
+  return CPPP_OK;
+}
+
+// ---------------------------------------------------------------- small solve of one mode
+// A_new = M Γ^†, G, dA = A_new - ref, S^(n), norms (Alg. 1 P:393-399 / Alg. 3).
+cppp_status finish_mode(cppp_ctx* c, int n, const double* Mn, bool pp_phase) {
+  if (c->dry) return CPPP_OK;
+  const int K = c->K;
+  const int64_t rows = c->dl[n];
+  const int64_t off = (n == c->q) ? c->qoff : 0;
+  SolveWS ws{c->Gamma, c->L, c->lmode, c->rowstat};
+  {
+    Prof p(c, CPPP_K_SOLVE, 2.0 * rows * K * K * 2 + K * K * K / 3.0, 8.0 * rows * K * 4);
+    CUCHK(c, launch_gamma_factor(c->S_all, c->N, n, K, ws, c->st));
+    double* An = c->A[n] + off * K;
+    const double* ref = pp_phase ? (c->Ap[n] + off * K) : An;
+    CUCHK(c, launch_solve_rows(Mn, An, ref, c->dA[n] + off * K, rows, K, ws, c->st));
+    CUCHK(c, launch_gram_norms(An, rows, K, c->S_all + (int64_t)n * K * K, c->rowstat,
+                               c->stats + 3 * n, c->st));
+  }
+  if (n == c->q) {
+    STCHK(allreduce(c, c->S_all + (int64_t)n * K * K, (size_t)K * K));
+    STCHK(allreduce(c, c->stats + 3 * n, 3));
+  }
+  if (n == c->N - 1) {
+    Prof p(c, CPPP_K_OTHER, 0, 0);
+    CUCHK(c, launch_fitness_terms(Mn, c->A[n] + off * K, rows, K, c->Gamma,
+                                  c->S_all + (int64_t)n * K * K, c->stats + 3 * c->N, c->st));
+  }
+  return CPPP_OK;
+}
+
+// ---------------------------------------------------------------- regular dimension tree
+// DT sweep (Alg. 1 with a binary dimension tree; leading cost 4 s^N R).  Node `nd`
+// keeps exactly modes [lo, hi].  Left half first (Gauss-Seidel order n = 0..N-1): its modes
+// are reached by contracting the right half with the not-yet-updated factors; the right half
+// is then reached by contracting the (now updated) left half.
+struct DT {
+  cppp_ctx* c;
+  bool update;
+  double* const* Mout;   // where M^(n) goes (c->M or caller buffers)
+
+  std::vector<int> chain_order(const Node& nd, int lo, int hi) {
+    std::vector<int> m;
+    for (int v = lo; v <= hi; ++v) m.push_back(v);
+    // keep the natural GEMM orientation for the first-level TTM: contract the last mode first
+    // when it is in the chain, else the first; never contract the sharded mode first (SURVEY
+    // §8(e)): it goes last so every big intermediate stays exact for the local rows.
+    bool has_last = false;
+    int last_kept = -1;
+    for (int v = 0; v < c->N; ++v)
+      if (nd.mask & (1u << v)) last_kept = v;
+    for (int v : m) has_last |= (v == last_kept);
+    if (has_last) std::reverse(m.begin(), m.end());
+    auto it = std::find(m.begin(), m.end(), c->q);
+    if (it != m.end()) {
+      m.erase(it);
+      m.push_back(c->q);
+    }
+    return m;
+  }
+
+  // contract `modes` (in order) out of nd; the final node goes to `final_dst` if given
+  cppp_status chain(const Node& nd, const std::vector<int>& modes, double* final_dst, Node* out) {
+    Node cur = nd;
+    for (size_t i = 0; i < modes.size(); ++i) {
+      const int u = modes[i];
+      const uint32_t nm = cur.mask & ~(1u << u);
+      double* dst = (i + 1 == modes.size() && final_dst) ? final_dst
+                                                         : c->stack.push(node_elems(c, nm));
+      STCHK(contract(c, cur, u, fac_local(c, c->A, u), dst));
+      cur = Node{nm, dst, false};
+    }
+    *out = cur;
+    return CPPP_OK;
+  }
+
+  cppp_status leaf(int n, const double* Mn) {
+    if (Mout != c->M && !c->dry) {
+      CUCHK(c, cudaMemcpyAsync(Mout[n], Mn, sizeof(double) * c->dl[n] * c->K,
+                               cudaMemcpyDeviceToDevice, c->st));
+    }
+    if (n != c->q) STCHK(allreduce(c, Mout[n], (size_t)c->dl[n] * c->K));
+    if (update) STCHK(finish_mode(c, n, Mout[n], false));
+    return CPPP_OK;
+  }
+
+  cppp_status range(const Node& nd, int lo, int hi) {
+    const int mid = lo + (hi - lo + 1 + 1) / 2 - 1;  // left half has ceil(len/2) modes
+    // ---- left: modes [lo, mid]
+    {
+      const size_t mk = c->stack.mark();
+      std::vector<int> ord = chain_order(nd, mid + 1, hi);
+      Node L;
+      if (lo == mid) {
+        STCHK(chain(nd, ord, c->M[lo], &L));
+        STCHK(leaf(lo, c->M[lo]));
+      } else {
+        STCHK(chain(nd, ord, nullptr, &L));
+        STCHK(range(L, lo, mid));
+      }
+      c->stack.release(mk);
+    }
+    // ---- right: modes [mid+1, hi]
+    {
+      const size_t mk = c->stack.mark();
+      std::vector<int> ord = chain_order(nd, lo, mid);
+      Node R;
+      if (mid + 1 == hi) {
+        STCHK(chain(nd, ord, c->M[hi], &R));
+        STCHK(leaf(hi, c->M[hi]));
+      } else {
+        STCHK(chain(nd, ord, nullptr, &R));
+        STCHK(range(R, mid + 1, hi));
+      }
+      c->stack.release(mk);
+    }
+    return CPPP_OK;
+  }
+};
+
+cppp_status run_dt(cppp_ctx* c, bool update, double* const* Mout) {
+  DT dt{c, update, Mout};
+  Node root{(1u << c->N) - 1, c->X, true};
+  return dt.range(root, 0, c->N - 1);
+}
+
+// ---------------------------------------------------------------- PP construction tree
+// Def. pptree over tree modes 0..N-1 mapped to physical modes by tau (tree mode N-1
+// is the sharded mode when sharded, so it is contracted only at the leaves).  A node at level
+// l has contracted set mu ⊂ {0..l+1}, |mu| = l; its children are mu ∪ {w}, w ∈ (max mu, l+2],
+// each computed from it by contracting tau[w] (Tree_Map_PP P:77-91: i = max mu(t)).
+struct PPTree {
+  cppp_ctx* c;
+  int tau[CPPP_MAX_ORDER];
+
+  void init() {
+    const int N = c->N;
+    int k = 0;
+    for (int v = 0; v < N; ++v)
+      if (v != c->q) tau[k++] = v;
+    // largest dimensions contracted first: stable sort by decreasing global size
+    std::stable_sort(tau, tau + k, [&](int a, int b) { return c->s[a] > c->s[b]; });
+    if (c->q >= 0) tau[k++] = c->q;
+  }
+
+  uint32_t kept_of(uint32_t mu_tree) {
+    uint32_t kept = (1u << c->N) - 1;
+    for (int t = 0; t < c->N; ++t)
+      if (mu_tree & (1u << t)) kept &= ~(1u << tau[t]);
+    return kept;
+  }
+
+  double* op_ptr(uint32_t kept) {
+    int i = -1, j = -1;
+    for (int v = 0; v < c->N; ++v)
+      if (kept & (1u << v)) {
+        if (i < 0) i = v;
+        else j = v;
+      }
+    return c->ops[i][j];
+  }
+
+  cppp_status visit(const Node& nd, uint32_t mu, int level) {
+    const int N = c->N;
+    if (level == N - 2) return CPPP_OK;  // leaf
+    int maxmu = -1;
+    for (int t = 0; t < N; ++t)
+      if (mu & (1u << t)) maxmu = t;
+    const bool child_leaf = (level + 1 == N - 2);
+    if (nd.root) {
+      // level-1 nodes are full-size TTMs: one at a time, depth first
+      for (int w = maxmu + 1; w <= level + 2; ++w) {
+        const uint32_t cmu = mu | (1u << w);
+        const uint32_t kept = kept_of(cmu);
+        const size_t mk = c->stack.mark();
+        double* dst = child_leaf ? op_ptr(kept) : c->stack.push(node_elems(c, kept));
+        STCHK(contract(c, nd, tau[w], fac_local(c, c->Ap, tau[w]), dst));
+        STCHK(visit(Node{kept, dst, false}, cmu, level + 1));
+        c->stack.release(mk);
+      }
+      return CPPP_OK;
+    }
+    // deeper: all children of this parent together (one pass over the parent when fused)
+    const size_t mk = c->stack.mark();
+    std::vector<Node> kids;
+    std::vector<uint32_t> kmu;
+    for (int w = maxmu + 1; w <= level + 2; ++w) {
+      const uint32_t cmu = mu | (1u << w);
+      const uint32_t kept = kept_of(cmu);
+      double* dst = child_leaf ? op_ptr(kept) : c->stack.push(node_elems(c, kept));
+      kids.push_back(Node{kept, dst, false});
+      kmu.push_back(cmu);
+    }
+    STCHK(emit_children(nd, mu, maxmu, level, kids));
+    for (size_t i = 0; i < kids.size(); ++i) STCHK(visit(kids[i], kmu[i], level + 1));
+    c->stack.release(mk);
+    return CPPP_OK;
+  }
+
+  cppp_status emit_children(const Node& nd, uint32_t mu, int maxmu, int level,
+                            const std::vector<Node>& kids) {
+    size_t i = 0;
+    for (int w = maxmu + 1; w <= level + 2; ++w, ++i)
+      STCHK(contract(c, nd, tau[w], fac_local(c, c->Ap, tau[w]), kids[i].data));
+    (void)mu;
+    return CPPP_OK;
+  }
+
+  cppp_status run() {
+    init();
+    Node root{(1u << c->N) - 1, c->X, true};
+    return visit(root, 0u, 0);
+  }
+};
+
+// M_p^(n) = M_p^(j,n) ×_j A_p^(j), j = min{j ∉ {n, q}}
+cppp_status build_singles(cppp_ctx* c) {
+  const int N = c->N, K = c->K;
+  for (int n = 0; n < N; ++n) {
+    int j = -1;
+    for (int v = 0; v < N; ++v)
+      if (v != n && v != c->q) {
+        j = v;
+        break;
+      }
+    const int a = std::min(j, n), b = std::max(j, n);
+    Node op{(1u << a) | (1u << b), c->ops[a][b], false};
+    STCHK(contract(c, op, j, fac_local(c, c->Ap, j), c->Mp[n]));
+  }
+  (void)K;
+  return CPPP_OK;
+}
+
+cppp_status run_pp_build(cppp_ctx* c) {
+  const int N = c->N, K = c->K;
+  if (!c->dry) {
+    for (int n = 0; n < N; ++n) {
+      CUCHK(c, cudaMemcpyAsync(c->Ap[n], c->A[n], sizeof(double) * c->s[n] * K,
+                               cudaMemcpyDeviceToDevice, c->st));
+      CUCHK(c, cudaMemsetAsync(c->dA[n], 0, sizeof(double) * c->s[n] * K, c->st));
+    }
+  }
+  PPTree t{c};
+  STCHK(t.run());
+  // leaves that contracted the sharded mode hold partial sums: all-reduce them (SURVEY C-b)
+  if (c->q >= 0)
+    for (int i = 0; i < N; ++i)
+      for (int j = i + 1; j < N; ++j)
+        if (i != c->q && j != c->q)
+          STCHK(allreduce(c, c->ops[i][j], (size_t)c->dl[i] * c->dl[j] * K));
+  STCHK(build_singles(c));
+  if (!c->dry) c->ops_valid = true;
+  return CPPP_OK;
+}
+
+// One PP term list for mode n (operator reads per L5: (i,n) is the transpose of (n,i)).
+void pp_terms(cppp_ctx* c, int n, bool skip_q, PPUpdateArgs* a) {
+  const int K = c->K;
+  a->nterms = 0;
+  for (int i = 0; i < c->N; ++i) {
+    if (i == n || (skip_q && i == c->q)) continue;
+    PPTerm t;
+    const int lo = std::min(i, n), hi = std::max(i, n);
+    t.op = c->ops[lo][hi];
+    t.dA = fac_local(c, c->dA, i);
+    t.nx = c->dl[i];
+    if (i < n) {  // stored [x_i][y][k]
+      t.sx = c->dl[n] * K;
+      t.sy = K;
+    } else {      // stored [y][x_i][k]
+      t.sx = K;
+      t.sy = c->dl[i] * K;
+    }
+    a->t[a->nterms++] = t;
+  }
+}
+
+cppp_status pp_update_mode(cppp_ctx* c, int n, double* out, const double* extra, bool skip_q,
+                           const double* Mp) {
+  if (c->dry) return CPPP_OK;
+  PPUpdateArgs a;
+  a.Mp = Mp;
+  a.extra = extra;
+  a.ny = c->dl[n];
+  a.K = c->K;
+  a.out = out;
+  a.partial = c->pp_partial;
+  pp_terms(c, n, skip_q, &a);
+  double bytes = 8.0 * (2.0 * a.ny * a.K);
+  double flops = 0.0;
+  for (int i = 0; i < a.nterms; ++i) {
+    bytes += 8.0 * (a.t[i].nx * a.ny * a.K + a.t[i].nx * a.K);
+    flops += 2.0 * a.t[i].nx * a.ny * a.K;
+  }
+  Prof p(c, CPPP_K_PPUPDATE, flops, bytes);
+  CUCHK(c, launch_pp_update(a, c->st));
+  return CPPP_OK;
+}
+
+// PP sweep (Alg. 3).  Sharded: the mode-q terms of the other modes depend only on
+// dA^(q) (mode q is updated first), so they are formed once and all-reduced once (SURVEY C-c).
+cppp_status run_pp_sweep(cppp_ctx* c) {
+  const int N = c->N;
+  const bool sh = c->q >= 0 && c->world > 1;
+  for (int n = 0; n < N; ++n) {
+    const double* extra = nullptr;
+    if (sh && n != c->q) extra = c->T[n];
+    STCHK(pp_update_mode(c, n, c->M[n], extra, sh && n != c->q, c->Mp[n]));
+    STCHK(finish_mode(c, n, c->M[n], true));
+    if (sh && n == c->q) {
+      // T_m = M_p^(q,m) ×_q dA^(q) (partial over local rows) for every m != q
+      for (int m = 0; m < N; ++m) {
+        if (m == c->q) continue;
+        if (!c->dry) {
+          PPUpdateArgs a;
+          a.Mp = nullptr;
+          a.extra = nullptr;
+          a.ny = c->dl[m];
+          a.K = c->K;
+          a.out = c->T[m];
+          a.partial = c->pp_partial;
+          a.nterms = 1;
+          const int lo = std::min(c->q, m), hi = std::max(c->q, m);
+          PPTerm t;
+          t.op = c->ops[lo][hi];
+          t.dA = fac_local(c, c->dA, c->q);
+          t.nx = c->dl[c->q];
+          if (c->q < m) { t.sx = c->dl[m] * c->K; t.sy = c->K; }
+          else { t.sx = c->K; t.sy = c->dl[c->q] * c->K; }
+          a.t[0] = t;
+          CUCHK(c, launch_pp_update(a, c->st));
+        }
+        STCHK(allreduce(c, c->T[m], (size_t)c->dl[m] * c->K));
+      }
+    }
+  }
+  return CPPP_OK;
+}
+
+// ---------------------------------------------------------------- workspace plan
+struct Plan {
+  size_t total = 0;
+  size_t off_X = 0, off_fac = 0, off_small = 0, off_ops = 0, off_stack = 0;
+  size_t stack_bytes = 0;
+};
+
+size_t factor_block_doubles(const cppp_ctx* c) {
+  size_t d = 0;
+  for (int n = 0; n < c->N; ++n) d += align_up(sizeof(double) * c->s[n] * c->K) / 8 * 3;   // A, Ap, dA
+  for (int n = 0; n < c->N; ++n) d += align_up(sizeof(double) * c->dl[n] * c->K) / 8 * 3;  // M, Mp, T
+  return d;
+}
+
+cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
+  // sizes (bytes)
+  const int N = c->N, K = c->K;
+  int64_t smax = 0;
+  for (int n = 0; n < N; ++n) smax = std::max(smax, c->s[n]);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes);
+    return o;
+  };
+  size_t oX = borrow ? 0 : take(sizeof(double) * c->numel_local);
+  size_t oA[CPPP_MAX_ORDER], oAp[CPPP_MAX_ORDER], odA[CPPP_MAX_ORDER], oM[CPPP_MAX_ORDER],
+      oMp[CPPP_MAX_ORDER], oT[CPPP_MAX_ORDER];
+  for (int n = 0; n < N; ++n) {
+    oA[n] = take(sizeof(double) * c->s[n] * K);
+    oAp[n] = take(sizeof(double) * c->s[n] * K);
+    odA[n] = take(sizeof(double) * c->s[n] * K);
+    oM[n] = take(sizeof(double) * c->dl[n] * K);
+    oMp[n] = take(sizeof(double) * c->dl[n] * K);
+    oT[n] = take(sizeof(double) * c->dl[n] * K);
+  }
+  size_t oS = take(sizeof(double) * N * K * K);
+  size_t oG = take(sizeof(double) * K * K);
+  size_t oL = take(sizeof(double) * 2 * K * K);
+  size_t oLm = take(sizeof(int) * 4);
+  size_t oRow = take(sizeof(double) * smax * 3);
+  size_t oStats = take(sizeof(double) * (3 * N + 8));
+  size_t oFpad = take(sizeof(double) * smax * 128);
+  size_t oOps[CPPP_MAX_ORDER][CPPP_MAX_ORDER];
+  for (int i = 0; i < N; ++i)
+    for (int j = i + 1; j < N; ++j) oOps[i][j] = take(sizeof(double) * c->dl[i] * c->dl[j] * K);
+  size_t oPP = take(sizeof(double) * pp_update_scratch_doubles(smax, K, smax));
+  size_t oSq = take(sizeof(double) * 2048);
+  size_t oGath = take(sizeof(double) * smax * K);
+  size_t oStack = off;
+  plan->off_stack = oStack;
+  // dry-run the DT sweep and the PP build to size the stack
+  c->dry = true;
+  c->stack = Stack{};
+  c->stack.dry = true;
+  cppp_status s1 = run_dt(c, true, c->M);
+  cppp_status s2 = run_pp_build(c);
+  c->dry = false;
+  if (s1 != CPPP_OK) return s1;
+  if (s2 != CPPP_OK) return s2;
+  plan->stack_bytes = c->stack.peak;
+  plan->total = oStack + align_up(c->stack.peak) + ALIGN;
+  if (!c->ws) return CPPP_OK;  // sizing only
+  char* b = c->ws;
+  c->X = borrow ? c->X : reinterpret_cast<double*>(b + oX);
+  for (int n = 0; n < N; ++n) {
+    c->A[n] = reinterpret_cast<double*>(b + oA[n]);
+    c->Ap[n] = reinterpret_cast<double*>(b + oAp[n]);
+    c->dA[n] = reinterpret_cast<double*>(b + odA[n]);
+    c->M[n] = reinterpret_cast<double*>(b + oM[n]);
+    c->Mp[n] = reinterpret_cast<double*>(b + oMp[n]);
+    c->T[n] = reinterpret_cast<double*>(b + oT[n]);
+  }
+  c->S_all = reinterpret_cast<double*>(b + oS);
+  c->Gamma = reinterpret_cast<double*>(b + oG);
+  c->L = reinterpret_cast<double*>(b + oL);
+  c->lmode = reinterpret_cast<int*>(b + oLm);
+  c->rowstat = reinterpret_cast<double*>(b + oRow);
+  c->stats = reinterpret_cast<double*>(b + oStats);
+  c->Fpad = reinterpret_cast<double*>(b + oFpad);
+  for (int i = 0; i < N; ++i)
+    for (int j = i + 1; j < N; ++j) c->ops[i][j] = reinterpret_cast<double*>(b + oOps[i][j]);
+  c->pp_partial = reinterpret_cast<double*>(b + oPP);
+  c->sq_partial = reinterpret_cast<double*>(b + oSq);
+  c->gath = reinterpret_cast<double*>(b + oGath);
+  c->stack = Stack{};
+  c->stack.base = b + oStack;
+  c->stack.cap = c->ws_bytes - oStack;
+  c->stack.dry = false;
+  return CPPP_OK;
+}
+
+cppp_status validate(cppp_ctx* c, int N, const int64_t* s, int K, const cppp_opts* o) {
+  if (N < 3 || N > CPPP_MAX_ORDER)
+    return fail(c, CPPP_EINVAL, "order N=%d out of range [3, %d]", N, CPPP_MAX_ORDER);
+  if (K < 1 || K > CPPP_MAX_RANK)
+    return fail(c, CPPP_EINVAL, "rank K=%d out of range [1, %d]", K, CPPP_MAX_RANK);
+  if (!s) return fail(c, CPPP_EINVAL, "null sizes");
+  for (int n = 0; n < N; ++n)
+    if (s[n] < 1) return fail(c, CPPP_EINVAL, "dimension mismatch: s[%d]=%lld < 1", n, (long long)s[n]);
+  if (o && o->shard_mode != -1) {
+    if (o->shard_mode != 0)
+      return fail(c, CPPP_EINVAL, "slab sharding is along mode 0 only (got mode %d)", o->shard_mode);
+    if (o->shard_offset < 0 || o->shard_extent < 1 || o->shard_offset + o->shard_extent > s[0])
+      return fail(c, CPPP_EINVAL, "shard [%lld, +%lld) outside mode 0 of size %lld",
+                  (long long)o->shard_offset, (long long)o->shard_extent, (long long)s[0]);
+  }
+  return CPPP_OK;
+}
+
+void setup_dims(cppp_ctx* c, int N, const int64_t* s, int K, const cppp_opts* o) {
+  c->N = N;
+  c->K = K;
+  for (int n = 0; n < N; ++n) c->s[n] = c->dl[n] = s[n];
+  c->q = -1;
+  if (o && o->shard_mode == 0) {
+    c->q = 0;
+    c->qoff = o->shard_offset;
+    c->qext = o->shard_extent;
+    c->dl[0] = o->shard_extent;
+  }
+  c->numel_local = 1;
+  for (int n = 0; n < N; ++n) c->numel_local *= c->dl[n];
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+cppp_status copy_in(cppp_ctx* c, double* dst, const double* src, size_t n) {
+  CUCHK(c, cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDefault, c->st));
+  return CPPP_OK;
+}
+cppp_status copy_out(cppp_ctx* c, double* dst, const double* src, size_t n) {
+  CUCHK(c, cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDefault, c->st));
+  if (!is_device_ptr(dst)) CUCHK(c, cudaStreamSynchronize(c->st));
+  return CPPP_OK;
+}
+
+// gather the sharded factor's rows: zero everything but the local rows, all-reduce
+cppp_status gather_rows(cppp_ctx* c, double* buf) {
+  if (c->q < 0 || c->world <= 1) return CPPP_OK;
+  const int K = c->K;
+  CUCHK(c, cudaMemsetAsync(c->gath, 0, sizeof(double) * c->s[c->q] * K, c->st));
+  CUCHK(c, cudaMemcpyAsync(c->gath + c->qoff * K, buf + c->qoff * K, sizeof(double) * c->qext * K,
+                           cudaMemcpyDeviceToDevice, c->st));
+  STCHK(allreduce(c, c->gath, (size_t)c->s[c->q] * K));
+  CUCHK(c, cudaMemcpyAsync(buf, c->gath, sizeof(double) * c->s[c->q] * K, cudaMemcpyDeviceToDevice,
+                           c->st));
+  return CPPP_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+extern "C" {
+
+void cppp_default_opts(cppp_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->device = 0;
+  o->shard_mode = -1;
+  o->rank = 0;
+  o->world = 1;
+}
+
+const char* cppp_status_string(int s) {
+  switch (s) {
+    case CPPP_OK: return "ok";
+    case CPPP_EINVAL: return "invalid argument";
+    case CPPP_ENOMEM: return "out of memory / workspace too small";
+    case CPPP_ECUDA: return "CUDA error";
+    case CPPP_ENCCL: return "NCCL error";
+    case CPPP_ESTATE: return "call out of order";
+    case CPPP_ENODEV: return "no CUDA device";
+  }
+  return "unknown status";
+}
+
+const char* cppp_version(void) { return "cppp 0.1 sm_100a"; }
+
+const char* cp_last_error(const cppp_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+size_t cppp_workspace_bytes(int N, const int64_t* s, int K, const cppp_opts* o) {
+  cppp_ctx tmp;
+  if (validate(&tmp, N, s, K, o) != CPPP_OK) return 0;
+  setup_dims(&tmp, N, s, K, o);
+  Plan p;
+  const bool borrow = o && (o->flags & CPPP_FLAG_BORROW_TENSOR);
+  if (assign_buffers(&tmp, borrow, &p) != CPPP_OK) return 0;
+  return p.total;
+}
+
+cppp_status cppp_nccl_unique_id(void* out128) {
+  if (!out128) return CPPP_EINVAL;
+  if (!g_nccl.load()) return CPPP_ENCCL;
+  ncclUniqueId id;
+  if (g_nccl.getUniqueId(&id) != ncclSuccess) return CPPP_ENCCL;
+  std::memcpy(out128, &id, sizeof(id));
+  return CPPP_OK;
+}
+
+cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, int K,
+                    const cppp_opts* o_in) {
+  if (!out) return CPPP_EINVAL;
+  *out = nullptr;
+  cppp_opts o;
+  if (o_in) o = *o_in;
+  else cppp_default_opts(&o);
+  cppp_ctx* c = new cppp_ctx();
+  *out = c;
+  STCHK(validate(c, N, s, K, &o));
+  if (!X) return fail(c, CPPP_EINVAL, "null tensor");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(c, CPPP_ENODEV, "no CUDA device visible");
+  }
+  if (o.device < 0 || o.device >= ndev) return fail(c, CPPP_EINVAL, "device %d of %d", o.device, ndev);
+  c->device = o.device;
+  CUCHK(c, cudaSetDevice(c->device));
+  c->flags = o.flags;
+  setup_dims(c, N, s, K, &o);
+  if (o.stream) c->st = static_cast<cudaStream_t>(o.stream);
+  else {
+    CUCHK(c, cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  // comm
+  c->rank = o.rank;
+  c->world = o.world < 1 ? 1 : o.world;
+  if (c->world > 1) {
+    if (!o.nccl_unique_id) return fail(c, CPPP_EINVAL, "world > 1 needs nccl_unique_id");
+    if (!g_nccl.load()) return fail(c, CPPP_ENCCL, "cannot dlopen libnccl.so.2");
+    ncclUniqueId id;
+    std::memcpy(&id, o.nccl_unique_id, sizeof(id));
+    ncclResult_t r = g_nccl.commInitRank(&c->comm, c->world, id, c->rank);
+    if (r != ncclSuccess) return fail(c, CPPP_ENCCL, "ncclCommInitRank: %s", g_nccl.getErrorString(r));
+  }
+  const bool x_dev = is_device_ptr(X);
+  const bool borrow = (o.flags & CPPP_FLAG_BORROW_TENSOR) && x_dev;
+  if ((o.flags & CPPP_FLAG_BORROW_TENSOR) && !x_dev)
+    return fail(c, CPPP_EINVAL, "CPPP_FLAG_BORROW_TENSOR needs a device pointer");
+  if (borrow) c->X = const_cast<double*>(X);
+  Plan p;
+  STCHK(assign_buffers(c, borrow, &p));
+  if (o.workspace) {
+    if (o.workspace_bytes < p.total)
+      return fail(c, CPPP_ENOMEM, "workspace of %zu bytes < required %zu bytes", o.workspace_bytes,
+                  p.total);
+    c->ws = static_cast<char*>(o.workspace);
+    c->ws_bytes = o.workspace_bytes;
+  } else {
+    void* m = nullptr;
+    if (cudaMalloc(&m, p.total) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, CPPP_ENOMEM, "cudaMalloc(%zu) failed", p.total);
+    }
+    c->ws = static_cast<char*>(m);
+    c->ws_alloc = c->ws;
+    c->ws_bytes = p.total;
+    c->own_ws = true;
+  }
+  c->ws = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(c->ws)));
+  c->ws_bytes -= ALIGN;
+  if (borrow) c->X = const_cast<double*>(X);
+  STCHK(assign_buffers(c, borrow, &p));
+  if (!borrow) STCHK(copy_in(c, c->X, X, (size_t)c->numel_local));
+  CUCHK(c, cudaMemsetAsync(c->ws + (borrow ? 0 : align_up(sizeof(double) * c->numel_local)), 0,
+                           p.off_stack - (borrow ? 0 : align_up(sizeof(double) * c->numel_local)),
+                           c->st));
+  CUCHK(c, cudaMallocHost(&c->host_stats, sizeof(double) * (3 * N + 8)));
+  CUCHK(c, cudaEventCreate(&c->ev_a));
+  CUCHK(c, cudaEventCreate(&c->ev_b));
+  // ||X||² (all-reduced)
+  {
+    Prof pr(c, CPPP_K_OTHER, 2.0 * c->numel_local, 8.0 * c->numel_local);
+    const int nb = sqnorm_blocks(c->numel_local);
+    CUCHK(c, launch_sqnorm(c->X, c->numel_local, c->sq_partial, nb, c->stats + 3 * N + 2, c->st));
+  }
+  STCHK(allreduce(c, c->stats + 3 * N + 2, 1));
+  CUCHK(c, cudaMemcpyAsync(c->host_stats, c->stats + 3 * N + 2, sizeof(double),
+                           cudaMemcpyDeviceToHost, c->st));
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  c->normX_sq = c->host_stats[0];
+  return CPPP_OK;
+}
+
+cppp_status cp_set_factors(cppp_ctx* c, const double* const* A) {
+  if (!c) return CPPP_EINVAL;
+  if (!A) return fail(c, CPPP_EINVAL, "null factor list");
+  for (int n = 0; n < c->N; ++n) {
+    if (!A[n]) return fail(c, CPPP_EINVAL, "null factor %d", n);
+    STCHK(copy_in(c, c->A[n], A[n], (size_t)c->s[n] * c->K));
+  }
+  for (int n = 0; n < c->N; ++n) {
+    const int64_t off = (n == c->q) ? c->qoff : 0;
+    CUCHK(c, launch_gram(c->A[n] + off * c->K, c->dl[n], c->K, c->S_all + (int64_t)n * c->K * c->K,
+                         c->st));
+    if (n == c->q) STCHK(allreduce(c, c->S_all + (int64_t)n * c->K * c->K, (size_t)c->K * c->K));
+    CUCHK(c, cudaMemsetAsync(c->dA[n], 0, sizeof(double) * c->s[n] * c->K, c->st));
+  }
+  c->factors_set = true;
+  c->ops_valid = false;
+  c->next_phase = CPPP_PHASE_DT;
+  c->sweep = 0;
+  c->restarts = 0;
+  c->last_fitness = NAN;
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  return CPPP_OK;
+}
+
+cppp_status cp_update_factors(cppp_ctx* c, const double* const* A) {
+  if (!c) return CPPP_EINVAL;
+  if (!A) return fail(c, CPPP_EINVAL, "null factor list");
+  if (!c->factors_set) return fail(c, CPPP_ESTATE, "cp_update_factors before cp_set_factors");
+  for (int n = 0; n < c->N; ++n) {
+    if (!A[n]) return fail(c, CPPP_EINVAL, "null factor %d", n);
+    STCHK(copy_in(c, c->A[n], A[n], (size_t)c->s[n] * c->K));
+    const int64_t off = (n == c->q) ? c->qoff : 0;
+    CUCHK(c, launch_gram(c->A[n] + off * c->K, c->dl[n], c->K, c->S_all + (int64_t)n * c->K * c->K,
+                         c->st));
+    if (n == c->q) STCHK(allreduce(c, c->S_all + (int64_t)n * c->K * c->K, (size_t)c->K * c->K));
+  }
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  return CPPP_OK;
+}
+
+cppp_status cp_get_factors(cppp_ctx* c, double* const* A) {
+  if (!c) return CPPP_EINVAL;
+  if (!A) return fail(c, CPPP_EINVAL, "null output list");
+  for (int n = 0; n < c->N; ++n) {
+    if (n == c->q) STCHK(gather_rows(c, c->A[n]));
+    STCHK(copy_out(c, A[n], c->A[n], (size_t)c->s[n] * c->K));
+  }
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  return CPPP_OK;
+}
+
+cppp_status mttkrp_dt(cppp_ctx* c, double* const* M) {
+  if (!c) return CPPP_EINVAL;
+  if (!c->factors_set) return fail(c, CPPP_ESTATE, "mttkrp_dt before cp_set_factors");
+  STCHK(run_dt(c, false, c->M));
+  if (M) {
+    for (int n = 0; n < c->N; ++n) {
+      if (!M[n]) continue;
+      STCHK(copy_out(c, M[n], c->M[n], (size_t)c->dl[n] * c->K));
+    }
+  }
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  prof_collect(c);
+  return CPPP_OK;
+}
+
+cppp_status pp_build_operators(cppp_ctx* c) {
+  if (!c) return CPPP_EINVAL;
+  if (!c->factors_set) return fail(c, CPPP_ESTATE, "pp_build_operators before cp_set_factors");
+  STCHK(run_pp_build(c));
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  prof_collect(c);
+  return CPPP_OK;
+}
+
+cppp_status pp_get_operator(cppp_ctx* c, int i, int j, double* out) {
+  if (!c) return CPPP_EINVAL;
+  if (i < 0 || j >= c->N || i >= j) return fail(c, CPPP_EINVAL, "operator (%d,%d): need 0<=i<j<N", i, j);
+  if (!c->ops_valid) return fail(c, CPPP_ESTATE, "no PP operators (call pp_build_operators)");
+  if (!out) return fail(c, CPPP_EINVAL, "null output");
+  return copy_out(c, out, c->ops[i][j], (size_t)c->dl[i] * c->dl[j] * c->K);
+}
+
+cppp_status pp_get_single(cppp_ctx* c, int n, double* out) {
+  if (!c) return CPPP_EINVAL;
+  if (n < 0 || n >= c->N) return fail(c, CPPP_EINVAL, "mode %d out of range", n);
+  if (!c->ops_valid) return fail(c, CPPP_ESTATE, "no PP operators (call pp_build_operators)");
+  if (!out) return fail(c, CPPP_EINVAL, "null output");
+  return copy_out(c, out, c->Mp[n], (size_t)c->dl[n] * c->K);
+}
+
+cppp_status pp_update(cppp_ctx* c, int n, double* M_tilde) {
+  if (!c) return CPPP_EINVAL;
+  if (n < 0 || n >= c->N) return fail(c, CPPP_EINVAL, "mode %d out of range", n);
+  if (!c->ops_valid) return fail(c, CPPP_ESTATE, "pp_update before pp_build_operators");
+  // dA = A - A_p for every mode (the caller may have moved the factors)
+  for (int i = 0; i < c->N; ++i)
+    CUCHK(c, launch_sub(c->A[i], c->Ap[i], c->dA[i], c->s[i] * c->K, c->st));
+  const bool sh = c->q >= 0 && c->world > 1;
+  if (sh && n != c->q) {
+    // partial term over the local rows of the sharded mode, then all-reduce
+    PPUpdateArgs a;
+    a.Mp = nullptr;
+    a.extra = nullptr;
+    a.ny = c->dl[n];
+    a.K = c->K;
+    a.out = c->T[n];
+    a.partial = c->pp_partial;
+    a.nterms = 1;
+    PPTerm t;
+    t.op = c->ops[std::min(c->q, n)][std::max(c->q, n)];
+    t.dA = fac_local(c, c->dA, c->q);
+    t.nx = c->dl[c->q];
+    if (c->q < n) { t.sx = c->dl[n] * c->K; t.sy = c->K; }
+    else { t.sx = c->K; t.sy = c->dl[c->q] * c->K; }
+    a.t[0] = t;
+    CUCHK(c, launch_pp_update(a, c->st));
+    STCHK(allreduce(c, c->T[n], (size_t)c->dl[n] * c->K));
+    STCHK(pp_update_mode(c, n, c->M[n], c->T[n], true, c->Mp[n]));
+  } else {
+    STCHK(pp_update_mode(c, n, c->M[n], nullptr, false, c->Mp[n]));
+  }
+  if (M_tilde) STCHK(copy_out(c, M_tilde, c->M[n], (size_t)c->dl[n] * c->K));
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  prof_collect(c);
+  return CPPP_OK;
+}
+
+cppp_status cp_set_phase_override(cppp_ctx* c, int phase) {
+  if (!c) return CPPP_EINVAL;
+  if (phase < CPPP_PHASE_AUTO || phase > CPPP_PHASE_PP) return fail(c, CPPP_EINVAL, "bad phase %d", phase);
+  c->override_phase = phase;
+  return CPPP_OK;
+}
+
+cppp_status als_sweep(cppp_ctx* c, double eps, double eps_pp, cppp_sweep_info* info) {
+  if (!c) return CPPP_EINVAL;
+  if (!c->factors_set) return fail(c, CPPP_ESTATE, "als_sweep before cp_set_factors");
+  if (!(eps_pp >= 0.0)) return fail(c, CPPP_EINVAL, "eps_pp must be >= 0");
+  const int phase = c->override_phase != CPPP_PHASE_AUTO ? c->override_phase : c->next_phase;
+  if (phase == CPPP_PHASE_PP && !c->ops_valid)
+    return fail(c, CPPP_ESTATE, "PP sweep requested without operators");
+  CUCHK(c, cudaEventRecord(c->ev_a, c->st));
+  if (phase == CPPP_PHASE_DT) {
+    STCHK(run_dt(c, true, c->M));
+  } else {
+    if (phase == CPPP_PHASE_PP_BUILD) {
+      STCHK(run_pp_build(c));
+      c->restarts++;
+    }
+    STCHK(run_pp_sweep(c));
+  }
+  CUCHK(c, cudaEventRecord(c->ev_b, c->st));
+  const int N = c->N;
+  CUCHK(c, cudaMemcpyAsync(c->host_stats, c->stats, sizeof(double) * (3 * N + 2),
+                           cudaMemcpyDeviceToHost, c->st));
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  prof_collect(c);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev_a, c->ev_b);
+  const double* hs = c->host_stats;
+  double maxrel = 0.0, gsum = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double na = hs[3 * n], nd = hs[3 * n + 1], ng = hs[3 * n + 2];
+    const double rel = na > 0.0 ? std::sqrt(nd) / std::sqrt(na) : (nd > 0.0 ? INFINITY : 0.0);
+    maxrel = std::max(maxrel, rel);
+    gsum += std::sqrt(ng);
+  }
+  const double inner = hs[3 * N], model = hs[3 * N + 1];
+  const double r2 = c->normX_sq - 2.0 * inner + model;
+  const double fit = 1.0 - std::sqrt(std::max(0.0, r2)) / std::sqrt(c->normX_sq);
+  const bool small = maxrel < eps_pp;
+  if (phase == CPPP_PHASE_DT) c->next_phase = small ? CPPP_PHASE_PP_BUILD : CPPP_PHASE_DT;
+  else c->next_phase = small ? CPPP_PHASE_PP : CPPP_PHASE_DT;
+  c->sweep++;
+  c->last_fitness = fit;
+  if (info) {
+    info->sweep = c->sweep;
+    info->phase = phase;
+    info->fitness = fit;
+    info->residual_sq = r2;
+    info->grad_norm_sum = gsum;
+    info->max_rel_dA = maxrel;
+    info->next_phase = c->next_phase;
+    info->restarts = c->restarts;
+    info->converged = gsum <= eps;
+    info->seconds = ms * 1e-3;
+  }
+  return CPPP_OK;
+}
+
+cppp_status fitness(cppp_ctx* c, double* f) {
+  if (!c) return CPPP_EINVAL;
+  if (!f) return fail(c, CPPP_EINVAL, "null output");
+  if (c->sweep == 0) return fail(c, CPPP_ESTATE, "fitness before any sweep");
+  *f = c->last_fitness;
+  return CPPP_OK;
+}
+
+cppp_status cppp_kernel_stats(cppp_ctx* c, int kclass, cppp_kernel_stat* out) {
+  if (!c) return CPPP_EINVAL;
+  if (kclass < 0 || kclass >= CPPP_K_COUNT || !out) return fail(c, CPPP_EINVAL, "bad kernel class");
+  prof_collect(c);
+  *out = c->kstat[kclass];
+  return CPPP_OK;
+}
+
+cppp_status cppp_reset_kernel_stats(cppp_ctx* c) {
+  if (!c) return CPPP_EINVAL;
+  prof_collect(c);
+  std::memset(c->kstat, 0, sizeof(c->kstat));
+  return CPPP_OK;
+}
+
+cppp_status cppp_generate(cppp_ctx* c, double* X_dev, int N, const int64_t* s, int K,
+                          const double* const* A_true, int noise_kind, double noise, uint64_t seed,
+                          int64_t row_lo, int64_t row_hi, void* stream) {
+  if (!X_dev || !s || !A_true || N < 2 || N > CPPP_MAX_ORDER || K < 1 || K > CPPP_MAX_RANK)
+    return c ? fail(c, CPPP_EINVAL, "cppp_generate: bad arguments") : CPPP_EINVAL;
+  if (row_lo < 0 || row_hi > s[0] || row_lo > row_hi)
+    return c ? fail(c, CPPP_EINVAL, "cppp_generate: bad row range") : CPPP_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // stage factors on device
+  std::vector<double*> Ad(N, nullptr);
+  size_t tot = 0;
+  for (int n = 0; n < N; ++n) tot += s[n] * K;
+  const int64_t nrows = row_hi - row_lo;
+  const size_t part = gen_partials_doubles(nrows);
+  double* buf = nullptr;
+  if (cudaMalloc(&buf, sizeof(double) * (tot + 2 * s[0] + part + 1)) != cudaSuccess)
+    return c ? fail(c, CPPP_ENOMEM, "cppp_generate: cudaMalloc") : CPPP_ENOMEM;
+  cppp_status rc = CPPP_OK;
+  double* p = buf;
+  for (int n = 0; n < N && rc == CPPP_OK; ++n) {
+    Ad[n] = p;
+    if (cudaMemcpyAsync(p, A_true[n], sizeof(double) * s[n] * K, cudaMemcpyDefault, st) != cudaSuccess)
+      rc = CPPP_ECUDA;
+    p += s[n] * K;
+  }
+  double* rowsq_x = p;
+  double* rowsq_z = p + s[0];
+  double* partials = p + 2 * s[0];
+  double* scale = partials + part;
+  if (rc == CPPP_OK && launch_gen_kruskal(X_dev, N, s, K, Ad.data(), row_lo, row_hi, st) != cudaSuccess)
+    rc = CPPP_ECUDA;
+  if (rc == CPPP_OK && noise_kind == 1 && noise != 0.0) {
+    if (launch_gen_noise_add(X_dev, s, N, seed, row_lo, row_hi, nullptr, noise, st) != cudaSuccess)
+      rc = CPPP_ECUDA;
+  } else if (rc == CPPP_OK && noise_kind == 2 && noise != 0.0) {
+    cudaMemsetAsync(rowsq_x, 0, sizeof(double) * 2 * s[0], st);
+    if (launch_gen_noise_rowsq(X_dev, s, N, seed, row_lo, row_hi, rowsq_x, rowsq_z, partials, st) !=
+        cudaSuccess)
+      rc = CPPP_ECUDA;
+    if (rc == CPPP_OK && c && c->world > 1) {
+      cudaStream_t save = c->st;
+      c->st = st;
+      rc = allreduce(c, rowsq_x, 2 * (size_t)s[0]);
+      c->st = save;
+    }
+    if (rc == CPPP_OK && launch_gen_scale(rowsq_x, rowsq_z, s[0], noise, scale, st) != cudaSuccess)
+      rc = CPPP_ECUDA;
+    if (rc == CPPP_OK &&
+        launch_gen_noise_add(X_dev, s, N, seed, row_lo, row_hi, scale, 0.0, st) != cudaSuccess)
+      rc = CPPP_ECUDA;
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(buf);
+  if (rc == CPPP_OK && e != cudaSuccess) rc = CPPP_ECUDA;
+  if (rc != CPPP_OK && c && c->err.empty()) c->err = "cppp_generate: CUDA error";
+  return rc;
+}
+
+size_t cppp_plan_describe(int N, int shard_mode, char* buf, size_t buflen) {
+  // host-only listing of the two trees (no device needed)
+  std::string out;
+  if (N < 3 || N > CPPP_MAX_ORDER) return 0;
+  int64_t s[CPPP_MAX_ORDER];
+  for (int n = 0; n < N; ++n) s[n] = 4;
+  cppp_opts o;
+  cppp_default_opts(&o);
+  if (shard_mode == 0) {
+    o.shard_mode = 0;
+    o.shard_offset = 0;
+    o.shard_extent = 2;
+  }
+  // PP tree listing (Def. pptree) in tree-mode terms and physical kept sets
+  cppp_ctx tmp;
+  setup_dims(&tmp, N, s, 1, &o);
+  PPTree t{&tmp};
+  t.init();
+  out += "pptree tau:";
+  for (int i = 0; i < N; ++i) out += " " + std::to_string(t.tau[i]);
+  out += "\n";
+  // BFS over levels
+  std::vector<uint32_t> level{0u};
+  for (int l = 1; l <= N - 2; ++l) {
+    std::vector<uint32_t> next;
+    for (uint32_t mu : level) {
+      int maxmu = -1;
+      for (int q = 0; q < N; ++q)
+        if (mu & (1u << q)) maxmu = q;
+      for (int w = maxmu + 1; w <= l + 1; ++w) {
+        const uint32_t cmu = mu | (1u << w);
+        next.push_back(cmu);
+        const uint32_t kept = t.kept_of(cmu);
+        out += "L" + std::to_string(l) + " kept:";
+        for (int v = 0; v < N; ++v)
+          if (kept & (1u << v)) out += " " + std::to_string(v);
+        out += " contract:" + std::to_string(t.tau[w]) + (l == 1 ? " ttm" : " ttv");
+        out += (l == N - 2) ? " leaf\n" : "\n";
+      }
+    }
+    level.swap(next);
+  }
+  const size_t need = out.size() + 1;
+  if (buf && buflen) {
+    const size_t n = std::min(buflen - 1, out.size());
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return need;
+}
+
+void cp_destroy(cppp_ctx* c) {
+  if (!c) return;
+  if (c->st) cudaStreamSynchronize(c->st);
+  prof_collect(c);
+  for (auto e : c->evpool) cudaEventDestroy(e);
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
+  if (c->host_stats) cudaFreeHost(c->host_stats);
+  if (c->own_ws && c->ws_alloc) cudaFree(c->ws_alloc);
+  if (c->comm) g_nccl.commDestroy(c->comm);
+  if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+}  // extern "C"

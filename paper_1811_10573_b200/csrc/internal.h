@@ -1,0 +1,116 @@
+// internal.h — shared declarations of the libcppp.so translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#define CPPP_MAX_TERMS_ 8
+
+namespace cppp {
+
+struct Dims {
+  int64_t s[8];
+};
+
+// ---------------------------------------------------------------- kernel launchers
+// All launchers enqueue on `st` and return the launch's cudaError_t.
+
+// TTM (first tree level, P:78-80 / P:408-414): out[b][r][n] = Σ_x X[b][x][r] * F[x][n]
+// X viewed as [B][S][R] (row-major), F is S x K (ld K), out is [B][R][K].
+// R == 1 is the natural mode-(N-1) unfolding X(BxS)·F; R > 1 contracts a middle/first mode.
+// Uses the DMMA (FP64 tensor core) kernel with TMA staging when the shape allows it (even
+// S and R, K <= 128), else the SIMT FP64 kernel.  `Fpad` is scratch of >= S*128 doubles.
+cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R,
+                       const double* F, int K, double* out, double* Fpad,
+                       bool force_simt, cudaStream_t st);
+cudaError_t launch_ttm_simt(const double* X, int64_t B, int64_t S, int64_t R,
+                            const double* F, int K, double* out, cudaStream_t st);
+bool ttm_dmma_supported(int64_t B, int64_t S, int64_t R, int K);
+
+// Multi-TTV: rank-diagonal contraction of one mode of a parent intermediate,
+// out[b][r][k] = Σ_x P[b][x][r][k] * F[x][k];  parent viewed as [B][S][R][K].
+cudaError_t launch_ttv(const double* P, int64_t B, int64_t S, int64_t R, int K,
+                       const double* F, double* out, cudaStream_t st);
+
+// Fused multi-output TTV: up to 3 children of one parent in one pass.  The parent is viewed
+// as [B][S0]...[S_{m-1}][T][K] where the children contract axis c of the m middle axes.
+struct TtvMulti {
+  const double* P;
+  int64_t B, T;             // outer block count, tail size
+  int m;                    // number of middle axes (1..3), each contracted by one child
+  int64_t S[3];
+  const double* F[3];       // factor for the contracted axis (S[c] x K)
+  double* out[3];           // child outputs: parent layout with axis c removed
+  int K;
+};
+cudaError_t launch_ttv_multi(const TtvMulti& p, cudaStream_t st);
+
+// PP update (Alg. 3): Mt[y][k] = Mp[y][k] + extra[y][k]
+//   + Σ_t Σ_x Op_t(x, y, k) * dA_t[x][k], Op_t(x,y,k) at Op_t + x*sx_t + y*sy_t + k.
+struct PPTerm {
+  const double* op;
+  const double* dA;
+  int64_t sx, sy;   // strides (doubles) of the contracted index x and of the output row y
+  int64_t nx;       // extent of x
+};
+struct PPUpdateArgs {
+  const double* Mp;       // s_n x K
+  const double* extra;    // optional additive s_n x K term (sharded runs), may be null
+  int nterms;
+  PPTerm t[CPPP_MAX_TERMS_];
+  int64_t ny;             // s_n (local)
+  int K;
+  double* out;            // s_n x K
+  double* partial;        // scratch for split-x partial sums (>= xsplit * ny * K doubles)
+};
+cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st);
+size_t pp_update_scratch_doubles(int64_t ny, int K, int64_t max_nx);
+
+// ---------------------------------------------------------------- small dense ops (K <= 128)
+// Gamma^(n) = Hadamard of S[m], m != n; Cholesky with the L13 pivot rule, else the
+// eigen pseudo-inverse (cyclic Jacobi).  Writes Gamma, L (or pinv P) and *mode (0 chol, 1 pinv).
+struct SolveWS {
+  double* Gamma;    // K x K
+  double* L;        // 2 K x K: Cholesky factor (lower) or the pseudo-inverse, then Jacobi scratch
+  int* mode;        // 0 = Cholesky, 1 = pinv
+  double* rowstat;  // per-row partial norms: s x 3  (||a_new||², ||dA||², ||g||²)
+};
+cudaError_t launch_gamma_factor(const double* S_all /* N x K x K */, int N, int n, int K, SolveWS ws,
+                                cudaStream_t st);
+// Row solves: A_new = M Gamma^† ; G = (A_old - A_new) Gamma ; dA = A_new - ref.
+// A is updated in place; ref may alias A (DT: dA = A_new - A_old).
+cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, double* dA,
+                              int64_t rows, int K, SolveWS ws, cudaStream_t st);
+// S = A^T A (K x K) and the per-mode norm triple reduced from rowstat -> nrm[0..2].
+cudaError_t launch_gram_norms(const double* A, int64_t rows, int K, double* S,
+                              const double* rowstat, double* nrm, cudaStream_t st);
+// plain Gram (no norms)
+cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, cudaStream_t st);
+// fitness pieces: out[0] = Σ M∘A (inner), out[1] = Σ Gamma∘S (model)
+cudaError_t launch_fitness_terms(const double* M, const double* A, int64_t rows, int K,
+                                 const double* Gamma, const double* S, double* out,
+                                 cudaStream_t st);
+// ||x||² with a fixed reduction tree: partial[nblk] then out[0]
+cudaError_t launch_sqnorm(const double* x, int64_t n, double* partial, int nblk, double* out,
+                          cudaStream_t st);
+int sqnorm_blocks(int64_t n);
+// y = a - b (elementwise)
+cudaError_t launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st);
+// Fp[x][n] = F[x][n] for n < K, 0 for K <= n < ld (TMA-aligned copy of a factor)
+cudaError_t launch_pad_rows(const double* F, int64_t S, int K, double* Fp, int ld, cudaStream_t st);
+
+// ---------------------------------------------------------------- generator (twin of synthgen)
+cudaError_t launch_gen_kruskal(double* X, int N, const int64_t* s, int K, const double* const* A_dev,
+                               int64_t row_lo, int64_t row_hi, cudaStream_t st);
+// per-row Σ X_true² and Σ Z² into rowsq_x/z[row_lo..row_hi) (partials: gen_partials_doubles)
+cudaError_t launch_gen_noise_rowsq(double* X, const int64_t* s, int N, uint64_t seed,
+                                   int64_t row_lo, int64_t row_hi, double* rowsq_x, double* rowsq_z,
+                                   double* partials, cudaStream_t st);
+size_t gen_partials_doubles(int64_t nrows);
+cudaError_t launch_gen_noise_add(double* X, const int64_t* s, int N, uint64_t seed, int64_t row_lo,
+                                 int64_t row_hi, const double* scale_dev, double abs_scale,
+                                 cudaStream_t st);
+cudaError_t launch_gen_scale(const double* rowsq_x, const double* rowsq_z, int64_t s0, double eta,
+                             double* scale_dev, cudaStream_t st);
+
+}  // namespace cppp

@@ -1,0 +1,109 @@
+// ppupdate.cu — the pairwise-perturbation update (Alg. 3):
+//
+//   M~^(n)(y,k) = M_p^(n)(y,k) + Σ_{i≠n} Σ_x M_p^(i,n)(x,y,k) · dA^(i)(x,k)
+//
+// All N-1 operator terms of one mode in ONE launch (plus a tiny deterministic combine).  The
+// operators are stored once per unordered pair as [x_min][x_max][k] (L5), so a term reads its
+// operator either as [x][y][k] (i < n: stride of x = s_n K) or [y][x][k] (i > n: stride K).
+// HBM-bound: 8 bytes read per 2 flops; the operator bytes dominate (N(N-1) s² K per sweep).
+//
+// Work split: CTA (y, part) reduces a contiguous x-range of every term for one output row y.
+// Threads are laid out as [G][K] (G = 256 / K x-groups), so each thread keeps one k and walks
+// x with stride G: every load instruction of the CTA touches G contiguous K-runs.  The G
+// partial sums of each k are reduced in shared memory in a fixed order, the `part` partials in
+// the combine kernel in a fixed order: bit-reproducible run to run.
+#include "internal.h"
+
+namespace cppp {
+namespace {
+
+constexpr int NT = 256;
+
+__global__ void __launch_bounds__(NT)
+    pp_update_partial(PPUpdateArgs a, int xsplit) {
+  const int64_t y = blockIdx.x;
+  const int part = blockIdx.y;
+  const int K = a.K;
+  const int G = NT / K;
+  const int tid = threadIdx.x;
+  const int k = tid % K;
+  const int xg = tid / K;
+  double acc = 0.0;
+  if (xg < G) {
+    for (int ti = 0; ti < a.nterms; ++ti) {
+      const PPTerm t = a.t[ti];
+      const int64_t x0 = (t.nx * part) / xsplit;
+      const int64_t x1 = (t.nx * (part + 1)) / xsplit;
+      const double* op = t.op + y * t.sy + k;
+      const double* d = t.dA + k;
+      int64_t x = x0 + xg;
+      for (; x + 3 * G < x1; x += 4 * G) {
+        const double o0 = __ldcs(op + x * t.sx), o1 = __ldcs(op + (x + G) * t.sx);
+        const double o2 = __ldcs(op + (x + 2 * G) * t.sx), o3 = __ldcs(op + (x + 3 * G) * t.sx);
+        const double d0 = __ldg(d + x * K), d1 = __ldg(d + (x + G) * K);
+        const double d2 = __ldg(d + (x + 2 * G) * K), d3 = __ldg(d + (x + 3 * G) * K);
+        acc = fma(o0, d0, acc);
+        acc = fma(o1, d1, acc);
+        acc = fma(o2, d2, acc);
+        acc = fma(o3, d3, acc);
+      }
+      for (; x < x1; x += G) acc = fma(__ldcs(op + x * t.sx), __ldg(d + x * K), acc);
+    }
+  }
+  __shared__ double red[NT];
+  red[tid] = acc;
+  __syncthreads();
+  if (tid < K) {
+    double s = 0.0;
+    for (int j = 0; j < G; ++j) s += red[j * K + tid];
+    a.partial[(static_cast<int64_t>(part) * a.ny + y) * K + tid] = s;
+  }
+}
+
+__global__ void pp_update_combine(PPUpdateArgs a, int xsplit) {
+  const int64_t total = a.ny * a.K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int p = 0; p < xsplit; ++p) v += a.partial[p * total + e];
+    double m = a.Mp[e];
+    if (a.extra) m += a.extra[e];
+    a.out[e] = m + v;
+  }
+}
+
+int choose_xsplit(int64_t ny, int64_t max_nx) {
+  // aim for >= ~4 CTAs per SM, keep >= 8 x per part
+  int64_t want = (148 * 4 + ny - 1) / ny;
+  int64_t cap = max_nx / 8;
+  if (want > cap) want = cap;
+  if (want > 16) want = 16;
+  if (want < 1) want = 1;
+  return static_cast<int>(want);
+}
+
+}  // namespace
+
+size_t pp_update_scratch_doubles(int64_t ny, int K, int64_t max_nx) {
+  (void)max_nx;
+  return static_cast<size_t>(16) * ny * K;
+}
+
+cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st) {
+  if (a.ny == 0) return cudaSuccess;
+  if (a.K > NT) return cudaErrorInvalidValue;
+  int64_t max_nx = 1;
+  for (int i = 0; i < a.nterms; ++i) max_nx = a.t[i].nx > max_nx ? a.t[i].nx : max_nx;
+  const int xsplit = choose_xsplit(a.ny, max_nx);
+  dim3 grid((unsigned)a.ny, (unsigned)xsplit);
+  pp_update_partial<<<grid, NT, 0, st>>>(a, xsplit);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int64_t total = a.ny * a.K;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  pp_update_combine<<<blocks, 256, 0, st>>>(a, xsplit);
+  return cudaGetLastError();
+}
+
+}  // namespace cppp

@@ -1,0 +1,365 @@
+// ttm.cu — first-level TTM T = X ×_m A^(m) (PAPER.md P:78-80 Tree_Map_PP level 1; P:405-414
+// the dimension-tree MTTKRP whose leading 4 s^N R cost is exactly these TTMs).
+//
+//   out[b][r][n] = Σ_x X[b][x][r] · F[x][n]      X viewed as [B][S][R], F = A^(m) (S x K)
+//
+// Contracting mode m of a row-major tensor: B = Π_{v<m} s_v, S = s_m, R = Π_{v>m} s_v.  The
+// rank index n lands last (Def. 3.1).  Two orientations of the same GEMM:
+//   R == 1  ("k-contiguous"): the natural unfolding X(B x S) · F — X rows are contiguous in x.
+//   R  > 1  ("m-contiguous"): per batch b, X_b(S x R)^T · F — X rows are contiguous in r.
+//
+// sm_100a design:
+//   * FP64 tensor cores: tcgen05 has no f64 kind, so the FP64 tensor path on sm_100a is the
+//     warp-level DMMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4).
+//   * One CTA = 128 output rows x BN (= K rounded up to 16) columns, so X is streamed from HBM
+//     exactly once.  8 consumer warps each own 16 rows x BN; 1 producer warp issues TMA.
+//   * TMA (cp.async.bulk.tensor) stages 16-deep k slices of X and of a zero-padded copy of F
+//     through a STAGES-deep mbarrier ring with 128-byte swizzle.
+//   * Fragment loads are 16-byte LDS (two doubles) with a k-slot permutation and a row
+//     permutation chosen so that every quarter-warp hits 8 distinct 16-byte bank groups under
+//     the 128B swizzle (derivation in DESIGN.md): thread (g = lane/4, t = lane%4) uses
+//     k = 8q + 2t + kk for MMA k-slot t in sub-step (q, kk).
+#include "internal.h"
+
+#include <cuda.h>
+
+#include <mutex>
+
+namespace cppp {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 16;
+constexpr int NWARP = 8;
+constexpr int NTHREADS = (NWARP + 1) * 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                       uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                       int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void lds2(double& x, double& y, uint32_t addr) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr));
+}
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Stage depth per BN so that STAGES * (16 KiB + 2 KiB * BN/16) stays within ~200 KiB.
+template <int BN>
+struct Cfg {
+  static constexpr int XBYTES = BM * BK * 8;           // 16 KiB
+  static constexpr int FBYTES = BK * BN * 8;           // 2 KiB per 16 columns
+  static constexpr int STAGE = XBYTES + FBYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+  static constexpr int SMEM = STAGES * STAGE + 2 * STAGES * 8 + 1024;
+};
+
+template <int BN, bool MC>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    ttm_dmma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
+                    double* __restrict__ out, int64_t Mrows, int64_t mtiles, int S, int K) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tile = blockIdx.x;
+  const int64_t b = MC ? tile / mtiles : 0;
+  const int64_t m0 = (tile - b * mtiles) * BM;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  const int nk = (S + BK - 1) / BK;
+
+  if (warp == NWARP) {  // ---------------- TMA producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmF)) : "memory");
+      for (int kt = 0; kt < nk; ++kt) {
+        const int st = kt % C::STAGES;
+        const uint32_t ph = (kt / C::STAGES) & 1;
+        if (kt >= C::STAGES) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+        const uint32_t fb = smem_u32(&full[st]);
+        mbar_expect_tx(fb, C::STAGE);
+        const uint32_t sx = smem_u32(base + st * C::STAGE);
+        const uint32_t sf = sx + C::XBYTES;
+        if (!MC) {
+          tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb);
+        } else {
+#pragma unroll
+          for (int c = 0; c < BM / 16; ++c)
+            tma_3d(sx + c * 2048, &tmX, static_cast<int>(m0 + 16 * c), kt * BK,
+                   static_cast<int>(b), fb);
+        }
+#pragma unroll
+        for (int c = 0; c < BN / 16; ++c) tma_2d(sf + c * 2048, &tmF, 16 * c, kt * BK, fb);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: warp owns rows [16*warp, 16*warp+16) x all BN columns
+  const int g = lane >> 2, t = lane & 3;
+  double acc[2][BN / 8][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < BN / 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // k-contiguous A rows: tile i, fragment row g -> box row 16w + 8i + fm(g), fm(g) = (g>>1)|((g&1)<<2)
+  const int fm = (g >> 1) | ((g & 1) << 2);
+
+  for (int kt = 0; kt < nk; ++kt) {
+    const int st = kt % C::STAGES;
+    const uint32_t ph = (kt / C::STAGES) & 1;
+    mbar_wait(smem_u32(&full[st]), ph);
+    const uint32_t sx = smem_u32(base + st * C::STAGE);
+    const uint32_t sf = sx + C::XBYTES;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      double a[2][2];  // [m-tile i][kk]
+      if (!MC) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int row = 16 * warp + 8 * i + fm;
+          const int chunk = 4 * q + t;
+          lds2(a[i][0], a[i][1], sx + row * 128 + ((chunk ^ (row & 7)) << 4));
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int row = 8 * q + 2 * t + kk;
+          lds2(a[0][kk], a[1][kk], sx + warp * 2048 + row * 128 + ((g ^ (row & 7)) << 4));
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const int row = 8 * q + 2 * t + kk;
+        const uint32_t frow = sf + row * 128 + ((g ^ (row & 7)) << 4);
+#pragma unroll
+        for (int c = 0; c < BN / 16; ++c) {
+          double b0, b1;
+          lds2(b0, b1, frow + c * 2048);
+          dmma(acc[0][2 * c], a[0][kk], b0);
+          dmma(acc[1][2 * c], a[1][kk], b0);
+          dmma(acc[0][2 * c + 1], a[0][kk], b1);
+          dmma(acc[1][2 * c + 1], a[1][kk], b1);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
+  }
+
+  // ---------------- epilogue: thread holds rows {r_i} x columns 16c + 4t + {0,1,2,3}
+  const bool pairs = (K % 2) == 0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int mloc = MC ? (16 * warp + 2 * g + i) : (16 * warp + 8 * i + fm);
+    const int64_t m = m0 + mloc;
+    if (m >= Mrows) continue;
+    double* orow = out + (b * Mrows + m) * static_cast<int64_t>(K);
+#pragma unroll
+    for (int c = 0; c < BN / 16; ++c) {
+      const int n0 = 16 * c + 4 * t;
+      const double v0 = acc[i][2 * c][0], v1 = acc[i][2 * c + 1][0];
+      const double v2 = acc[i][2 * c][1], v3 = acc[i][2 * c + 1][1];
+      if (pairs && n0 + 3 < K) {
+        *reinterpret_cast<double2*>(orow + n0) = make_double2(v0, v1);
+        *reinterpret_cast<double2*>(orow + n0 + 2) = make_double2(v2, v3);
+      } else {
+        if (n0 < K) orow[n0] = v0;
+        if (n0 + 1 < K) orow[n0 + 1] = v1;
+        if (n0 + 2 < K) orow[n0 + 2] = v2;
+        if (n0 + 3 < K) orow[n0 + 3] = v3;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- SIMT fallback
+// One thread per output (b, r, n); X read with r fastest across the warp.
+__global__ void ttm_simt_kernel(const double* __restrict__ X, int64_t B, int64_t S, int64_t R,
+                                const double* __restrict__ F, int K, double* __restrict__ out) {
+  const int64_t total = B * R * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = e / (B * R);
+    const int64_t br = e - n * (B * R);
+    const int64_t b = br / R, r = br - b * R;
+    const double* xp = X + b * S * R + r;
+    double acc = 0.0;
+    for (int64_t x = 0; x < S; ++x) acc = fma(xp[x * R], F[x * K + n], acc);
+    out[br * K + n] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims,
+              const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(ptr), dims,
+                   strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool MC>
+cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
+                     double* out, cudaStream_t st) {
+  using C = Cfg<BN>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(ttm_dmma_kernel<BN, MC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  CUtensorMap tmX, tmF;
+  const int64_t Mrows = MC ? R : B;
+  if (!MC) {
+    cuuint64_t dims[2] = {(cuuint64_t)S, (cuuint64_t)B};
+    cuuint64_t str[1] = {(cuuint64_t)S * 8};
+    cuuint32_t box[2] = {16, BM};
+    if (!make_map(&tmX, X, 2, dims, str, box)) return cudaErrorInvalidValue;
+  } else {
+    cuuint64_t dims[3] = {(cuuint64_t)R, (cuuint64_t)S, (cuuint64_t)B};
+    cuuint64_t str[2] = {(cuuint64_t)R * 8, (cuuint64_t)(S * R) * 8};
+    cuuint32_t box[3] = {16, 16, 1};
+    if (!make_map(&tmX, X, 3, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)BN, (cuuint64_t)S};
+    cuuint64_t str[1] = {(cuuint64_t)BN * 8};
+    cuuint32_t box[2] = {16, 16};
+    if (!make_map(&tmF, Fp, 2, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  const int64_t mtiles = (Mrows + BM - 1) / BM;
+  const int64_t grid = mtiles * (MC ? B : 1);
+  ttm_dmma_kernel<BN, MC><<<(unsigned)grid, NTHREADS, C::SMEM, st>>>(tmX, tmF, out, Mrows, mtiles,
+                                                                     (int)S, K);
+  return cudaGetLastError();
+}
+
+template <bool MC>
+cudaError_t dispatch_bn(int BN, const double* X, int64_t B, int64_t S, int64_t R, const double* Fp,
+                        int K, double* out, cudaStream_t st) {
+  switch (BN) {
+    case 16: return run_dmma<16, MC>(X, B, S, R, Fp, K, out, st);
+    case 32: return run_dmma<32, MC>(X, B, S, R, Fp, K, out, st);
+    case 48: return run_dmma<48, MC>(X, B, S, R, Fp, K, out, st);
+    case 64: return run_dmma<64, MC>(X, B, S, R, Fp, K, out, st);
+    case 80: return run_dmma<80, MC>(X, B, S, R, Fp, K, out, st);
+    case 96: return run_dmma<96, MC>(X, B, S, R, Fp, K, out, st);
+    case 112: return run_dmma<112, MC>(X, B, S, R, Fp, K, out, st);
+    case 128: return run_dmma<128, MC>(X, B, S, R, Fp, K, out, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+bool ttm_dmma_supported(int64_t B, int64_t S, int64_t R, int K) {
+  if (K < 1 || K > 128) return false;
+  if (S % 2 != 0) return false;                 // TMA: row strides multiple of 16 bytes
+  if (R > 1 && R % 2 != 0) return false;
+  if (S >= (1ll << 31) || B >= (1ll << 31) || R >= (1ll << 31)) return false;
+  if (get_encode() == nullptr) return false;
+  return true;
+}
+
+cudaError_t launch_ttm_simt(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
+                            int K, double* out, cudaStream_t st) {
+  const int64_t total = B * R * K;
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  ttm_simt_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, B, S, R, F, K, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R, const double* F, int K,
+                       double* out, double* Fpad, bool force_simt, cudaStream_t st) {
+  if (B * R * K == 0) return cudaSuccess;
+  if (force_simt || !ttm_dmma_supported(B, S, R, K))
+    return launch_ttm_simt(X, B, S, R, F, K, out, st);
+  const int BN = ((K + 15) / 16) * 16;
+  cudaError_t e = launch_pad_rows(F, S, K, Fpad, BN, st);
+  if (e != cudaSuccess) return e;
+  if (R == 1) return dispatch_bn<false>(BN, X, B, S, R, Fpad, K, out, st);
+  return dispatch_bn<true>(BN, X, B, S, R, Fpad, K, out, st);
+}
+
+}  // namespace cppp

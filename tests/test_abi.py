@@ -1,0 +1,65 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/cppp.h
+declares, host-only helpers work, and device calls fail loudly (no CPU fallback)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1811_10573_b200.cppp as cp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "cppp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*([a-z_0-9]+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for want in ["cp_init", "mttkrp_dt", "pp_build_operators", "pp_update", "als_sweep", "fitness"]:
+        assert want in names
+
+
+def test_library_exports_every_declared_symbol():
+    L = cp.lib()
+    for name in declared_functions():
+        assert hasattr(L, name), name
+    assert set(declared_functions()) <= set(cp.EXPORTED)
+
+
+def test_version_and_status_strings():
+    assert cp.cppp_version().endswith("sm_100a")
+    assert cp.lib().cppp_status_string(-5) == b"call out of order"
+
+
+def test_workspace_sizing_matches_survey_estimate():
+    L = cp.lib()
+    import ctypes as C
+    dims = (C.c_int64 * 4)(256, 256, 256, 256)
+    b = L.cppp_workspace_bytes(4, dims, 128, None)
+    # X (32 GiB) + one level-1 node (16 GiB) + 6 operators (384 MiB) ≈ 48.4 GiB
+    assert 48.0 * 2**30 < b < 49.0 * 2**30
+    assert L.cppp_workspace_bytes(2, dims, 4, None) == 0          # N < 3 rejected
+    assert L.cppp_workspace_bytes(4, dims, 129, None) == 0        # K > 128 rejected
+
+
+def test_plan_describe_lists_def_pptree():
+    txt = cp.cppp_plan_describe(6)
+    lines = [l for l in txt.splitlines() if l.startswith("L")]
+    per_level = [sum(l.startswith(f"L{k} ") for l in lines) for k in range(1, 5)]
+    assert per_level == [3, 6, 10, 15]          # C(l+2, 2), Lemma cost
+    assert sum("leaf" in l for l in lines) == 15
+    sh = cp.cppp_plan_describe(4, 0)
+    assert sh.splitlines()[0] == "pptree tau: 1 2 3 0"   # sharded mode contracted only at leaves
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="CPU-only behaviour")
+def test_device_calls_fail_loudly_without_gpu():
+    X = np.zeros((4, 4, 4))
+    with pytest.raises(cp.CpppError) as e:
+        cp.cp_init(X, 3, (4, 4, 4), 2, torch_workspace=False)
+    assert e.value.status == -6   # CPPP_ENODEV

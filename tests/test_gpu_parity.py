@@ -1,0 +1,164 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on identical seeded inputs.
+
+Tolerances (BASELINE.json north_star): MTTKRP, PP operators and PP updates within relative
+Frobenius 1e-11 given identical factors; per-sweep fitness traces within 1e-8 over 20 sweeps
+(phase schedule replayed, L12), applied while the relative residual ρ >= 1e-6 (L27).
+"""
+import numpy as np
+import pytest
+
+import oracle.cp_oracle as O
+import synthgen as G
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1811_10573_b200.cppp as cp  # noqa: E402
+
+TOL = 1e-11
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def problem(cfg_name, seed=0):
+    cfg = G.CONFIGS[cfg_name]
+    X = G.make_tensor(cfg, seed)
+    A0 = G.initial_factors(cfg, seed)
+    return cfg, X, A0
+
+
+def random_problem(dims, K, seed):
+    r = np.random.default_rng(seed)
+    X = r.standard_normal(dims)
+    A = [r.standard_normal((d, K)) for d in dims]
+    return X, A
+
+
+SMALL = ["C1", "C2mini", "C3mini", "C4mini", "C5mini"]
+RAGGED = [((7, 9, 5), 3), ((6, 10, 12), 17), ((130, 4, 6), 5), ((8, 6, 4, 10), 7),
+          ((3, 4, 2, 3, 2), 2), ((40, 36, 34), 128), ((34, 18, 10, 6), 100)]
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("simt", [False, True])
+def test_mttkrp_dt_matches_oracle(name, simt):
+    cfg, X, A0 = problem(name)
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K, flags=cp.FLAG_SIMT_TTM if simt else 0)
+    cp.cp_set_factors(ctx, A0)
+    M = cp.mttkrp_dt(ctx)
+    for n in range(cfg.N):
+        assert rel(M[n], O.mttkrp(X, A0, n)) < TOL, (name, n)
+
+
+@pytest.mark.parametrize("dims,K", RAGGED)
+def test_mttkrp_ragged_and_general_dims(dims, K):
+    X, A = random_problem(dims, K, 1)
+    ctx = cp.cp_init(X, len(dims), dims, K)
+    cp.cp_set_factors(ctx, A)
+    M = cp.mttkrp_dt(ctx)
+    for n in range(len(dims)):
+        assert rel(M[n], O.mttkrp(X, A, n)) < TOL, (dims, K, n)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_pp_operators_and_singles_match_oracle(name):
+    cfg, X, A0 = problem(name)
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    cp.cp_set_factors(ctx, A0)
+    cp.pp_build_operators(ctx)
+    ops = O.pp_operators(X, A0)
+    for (i, j), ref in ops.items():
+        assert rel(cp.pp_get_operator(ctx, i, j), ref) < TOL, (name, i, j)
+    for n in range(cfg.N):
+        assert rel(cp.pp_get_single(ctx, n), O.mttkrp(X, A0, n)) < TOL, (name, n)
+
+
+@pytest.mark.parametrize("dims,K", RAGGED)
+def test_pp_operators_ragged(dims, K):
+    X, A = random_problem(dims, K, 2)
+    ctx = cp.cp_init(X, len(dims), dims, K)
+    cp.cp_set_factors(ctx, A)
+    cp.pp_build_operators(ctx)
+    for (i, j), ref in O.pp_operators(X, A).items():
+        assert rel(cp.pp_get_operator(ctx, i, j), ref) < TOL, (dims, K, i, j)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_pp_update_matches_oracle(name):
+    cfg, X, Ap = problem(name)
+    r = np.random.default_rng(3)
+    dA = [0.01 * r.standard_normal(a.shape) for a in Ap]
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    cp.cp_set_factors(ctx, Ap)
+    cp.pp_build_operators(ctx)
+    ops = O.pp_operators(X, Ap)
+    Mp = [O.pp_single(ops, Ap, n, cfg.N) for n in range(cfg.N)]
+    # move the factors without dropping the operators: pp_update reads dA = A - A_p
+    cp.cp_update_factors(ctx, [a + d for a, d in zip(Ap, dA)])
+    for n in range(cfg.N):
+        ref = O.pp_update(Mp[n], ops, dA, n)
+        assert rel(cp.pp_update(ctx, n), ref) < TOL, (name, n)
+
+
+@pytest.mark.parametrize("name,sweeps", [("C1", 20), ("C2mini", 20), ("C3mini", 20), ("C4mini", 20),
+                                         ("C5mini", 20)])
+def test_sweep_trace_matches_oracle(name, sweeps):
+    cfg, X, A0 = problem(name)
+    _, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, sweeps)
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    cp.cp_set_factors(ctx, A0)
+    phases = []
+    for t in tr:
+        cp.cp_set_phase_override(ctx, t["phase"])
+        info = cp.als_sweep(ctx, 0.0, cfg.eps_pp)
+        phases.append(info["phase"])
+        rho = 1.0 - t["fitness"]
+        if rho >= 1e-6:
+            assert abs(info["fitness"] - t["fitness"]) < 1e-8, (name, t, info)
+        assert info["phase"] == t["phase"]
+    assert any(p != "dt" for p in phases) or cfg.name == "C4mini"
+
+
+def test_free_running_phase_machine_matches_oracle_schedule():
+    cfg, X, A0 = problem("C1")
+    _, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, 20)
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    cp.cp_set_factors(ctx, A0)
+    for t in tr:
+        info = cp.als_sweep(ctx, 0.0, cfg.eps_pp)
+        if t["margin"] > 1e-6:
+            assert info["phase"] == t["phase"]
+
+
+def test_device_generator_matches_synthgen():
+    for name in ["C1", "C2mini", "C5mini", "C4mini"]:
+        cfg = G.CONFIGS[name]
+        A = G.true_factors(cfg)
+        Xh = G.make_tensor(cfg, A_true=A)
+        Xd = torch.empty(cfg.numel, dtype=torch.float64, device="cuda")
+        kind = {"none": 0, "abs": 1, "rel": 2}[cfg.noise_kind]
+        cp.cppp_generate(Xd, cfg.dims, cfg.K, A, kind, cfg.noise)
+        Xg = Xd.cpu().numpy().reshape(cfg.dims)
+        assert np.max(np.abs(Xg - Xh)) <= 1e-13 * np.max(np.abs(Xh)), name
+
+
+def test_error_paths():
+    cfg, X, A0 = problem("C1")
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    with pytest.raises(cp.CpppError) as e:
+        cp.als_sweep(ctx, 0.0, 0.1)
+    assert e.value.status == -5
+    cp.cp_set_factors(ctx, A0)
+    with pytest.raises(cp.CpppError) as e:
+        cp.pp_update(ctx, 0)
+    assert e.value.status == -5
+    with pytest.raises(cp.CpppError) as e:
+        cp.pp_get_operator(ctx, 2, 1)
+    assert e.value.status == -1
+    with pytest.raises(cp.CpppError):
+        cp.cp_init(X, 3, (40, 40, 40), 129)
