@@ -1,0 +1,351 @@
+#!/usr/bin/env python3
+"""bench.py — CP-ALS-PP sweeps/s on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+A "step" is one CP-ALS-PP run of the workload (default C2 = BASELINE configs[1]: N=3, s=400,
+K=100, collinear + 1% noise): cp_set_factors(seeded initial factors) followed by 20 als_sweep
+calls with eps_pp = 0.1 — every §8(a) row of the hot path (first-level TTM, multi-TTV levels,
+PP construction tree, PP update, small solves, fitness, Alg. 3 phase machine).  value = sweeps
+per second over the timed steps (inputs resident in HBM; the 512 MB tensor is larger than L2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU): the tensor is sharded in mode-0 slabs; the ranks
+cooperate on the same run through NCCL all-reduce (strong scaling).  --impl reference times
+the CPU oracle (the deliberately slow, plain FP64 program of oracle/) on the same workload.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synthgen as G  # noqa: E402
+
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default="C2")
+    p.add_argument("--sweeps", type=int, default=None)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ clocks (during timed region)
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        med = float(np.median(sm)) if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def oracle_run(cfg, X, A0, sweeps):
+    import oracle.cp_oracle as O
+    t = time.perf_counter()
+    _, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, sweeps)
+    return time.perf_counter() - t, tr
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] or [os.cpu_count() or 1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = G.CONFIGS[args.config]
+    sweeps = args.sweeps or cfg.sweeps
+    if cfg.numel > 2e8:
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle needs the full {args.config} tensor on the host"}))
+        return
+    X = G.make_tensor(cfg)
+    A0 = G.initial_factors(cfg)
+    for _ in range(args.warmup):
+        oracle_run(cfg, X, A0, sweeps)
+    total = 0.0
+    for _ in range(args.steps):
+        dt, tr = oracle_run(cfg, X, A0, sweeps)
+        total += dt
+    value = sweeps * args.steps / total
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": "CP-ALS-PP sweeps/s", "value": value, "unit": "sweeps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded synthgen, host)",
+        "config": {"workload": cfg.name, "N": cfg.N, "s": cfg.s, "K": cfg.K, "sweeps": sweeps,
+                   "eps_pp": cfg.eps_pp},
+        "cpu_baseline": {"value": value, "unit": "sweeps/s", "cores": cores, "kind": "oracle",
+                         "sample": f"the full {sweeps}-sweep {cfg.name} run per step (oracle/cp_oracle.py, numpy FP64)"},
+        "e2e": {"value": value, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "phases": [t["phase"] for t in tr],
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_1811_10573_b200.cppp as cp
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world if world > 1 else args.gpus
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    cfg = G.CONFIGS[args.config]
+    sweeps = args.sweeps or cfg.sweeps
+    s0 = cfg.s
+    row_lo, row_hi = rank * s0 // world, (rank + 1) * s0 // world
+    dims = cfg.dims
+    stream = torch.cuda.current_stream()
+
+    # ---- inputs: generated on device by the seeded generator (untimed), resident in HBM
+    A_true = G.true_factors(cfg)
+    A0 = G.initial_factors(cfg)
+    local_numel = (row_hi - row_lo) * (cfg.s ** (cfg.N - 1))
+    X_dev = torch.empty(local_numel, dtype=torch.float64, device="cuda")
+    nccl_id = None
+    if world > 1:
+        obj = [cp.cppp_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    shard = dict(shard_offset=row_lo, shard_extent=row_hi - row_lo) if world > 1 else {}
+    kind = {"none": 0, "abs": 1, "rel": 2}[cfg.noise_kind]
+    # generate first (the context's ||X||² is taken at cp_init)
+    gen_ctx = None
+    if world > 1:
+        # a throw-away context provides the communicator for the shard-invariant noise scale
+        tmp = torch.zeros((row_hi - row_lo) * cfg.s ** (cfg.N - 1), dtype=torch.float64, device="cuda")
+        gen_ctx = cp.cp_init(tmp, cfg.N, dims, cfg.K, stream=stream, flags=cp.FLAG_BORROW_TENSOR,
+                             nccl_unique_id=nccl_id, rank=rank, world=world, torch_workspace=False, **shard)
+        del tmp
+    cp.cppp_generate(X_dev, dims, cfg.K, A_true, kind, cfg.noise, 0, row_lo, row_hi, stream=stream, ctx=gen_ctx)
+    if gen_ctx is not None:
+        cp.cp_destroy(gen_ctx)
+        obj = [cp.cppp_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ctx = cp.cp_init(X_dev, cfg.N, dims, cfg.K, stream=stream,
+                     flags=cp.FLAG_BORROW_TENSOR | cp.FLAG_PROFILE,
+                     nccl_unique_id=nccl_id, rank=rank, world=world, **shard)
+    A0_dev = [torch.from_numpy(a).cuda() for a in A0]
+
+    def step():
+        cp.cp_set_factors(ctx, A0_dev)
+        return [cp.als_sweep(ctx, 0.0, cfg.eps_pp) for _ in range(sweeps)]
+
+    for _ in range(max(args.warmup, 0)):
+        infos = step()
+    cp.reset_kernel_stats(ctx)
+    launches0 = cp.cppp_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    clk.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        infos = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    launches = (cp.cppp_launch_count() - launches0) / max(args.steps, 1)
+    kstats = cp.kernel_stats(ctx)
+    value = sweeps * args.steps / (ms * 1e-3)
+    phases = [i["phase"] for i in infos]
+
+    # ---- roofline of the dominant kernel class
+    peaks = {}
+    if os.path.exists(MEASURED_PEAKS):
+        peaks = json.load(open(MEASURED_PEAKS))
+    fp64 = {}
+    if os.path.exists(FP64_PEAK_FILE):
+        fp64 = json.load(open(FP64_PEAK_FILE))
+    dmma_peak = fp64.get("dmma_tflops_sustained", 37.0)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    roof_all = {}
+    for name, k in kstats.items():
+        if k["launches"] == 0 or k["total_ms"] <= 0:
+            continue
+        sec = k["total_ms"] * 1e-3
+        entry = {"launches_per_step": k["launches"] / args.steps, "ms_per_step": k["total_ms"] / args.steps,
+                 "share_of_step": k["total_ms"] / ms}
+        if name == "ttm":
+            entry.update(bound="tensor", achieved=k["flops"] / sec / 1e12, peak=dmma_peak, unit="TFLOP/s")
+        else:
+            entry.update(bound="hbm", achieved=k["bytes"] / sec / 1e9, peak=hbm_peak, unit="GB/s")
+        entry["frac"] = entry["achieved"] / entry["peak"]
+        roof_all[name] = entry
+    dom = max(roof_all, key=lambda n: roof_all[n]["ms_per_step"]) if roof_all else None
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
+    if dom and os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(dom)
+    roofline = None
+    if dom:
+        r = roof_all[dom]
+        roofline = {"kernel": dom, "bound": r["bound"], "achieved": r["achieved"], "peak": r["peak"],
+                    "unit": r["unit"], "frac": r["frac"], "traffic": traffic,
+                    "peak_source": ("tools/fp64_peak (register-resident DMMA.8x8x4, sustained) -> profiles/fp64_peak_r01.json"
+                                    if r["bound"] == "tensor" else "MEASURED_PEAKS.json hbm_gbs")}
+
+    # ---- e2e through the public API with host buffers (pinned), H2D/D2H inside the region
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.empty(local_numel, dtype=torch.float64, pin_memory=True)
+        Xh.copy_(X_dev.cpu())
+        A0h = [torch.from_numpy(a.copy()).pin_memory() for a in A0]
+        outh = [torch.empty(a.shape, dtype=torch.float64).pin_memory() for a in A0]
+
+        def e2e_step():
+            # N = 1: a fresh context from the pinned host tensor (H2D of X inside cp_init).
+            # N > 1: the sharded context is reused (a new one would need a new communicator).
+            c2 = cp.cp_init(Xh, cfg.N, dims, cfg.K, stream=stream) if world == 1 else ctx
+            cp.cp_set_factors(c2, A0h)
+            for _ in range(sweeps):
+                cp.als_sweep(c2, 0.0, cfg.eps_pp)
+            cp.cp_get_factors(c2, out=outh)
+            f = cp.fitness(c2)
+            if c2 is not ctx:
+                cp.cp_destroy(c2)
+            return f
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        h2d = (local_numel * 8 if world == 1 else 0) + sum(a.nbytes for a in A0)
+        e2e = {"value": sweeps * args.steps / dt, "unit": "sweeps/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(sum(a.nbytes for a in A0) + 8)}
+
+    # ---- CPU baseline: the oracle on the same workload (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.numel <= 2e8:
+        Xo = G.make_tensor(cfg)
+        dt, tr = oracle_run(cfg, Xo, A0, sweeps)
+        cpu = {"value": sweeps / dt, "unit": "sweeps/s", "cores": blas_threads(), "kind": "oracle",
+               "sample": f"one full {sweeps}-sweep {cfg.name} run (oracle/cp_oracle.py, numpy FP64 + BLAS)",
+               "phases": [t["phase"] for t in tr]}
+
+    if rank == 0:
+        line = {
+            "metric": "CP-ALS-PP sweeps/s", "value": value, "unit": "sweeps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded on-device generator, twin of synthgen)",
+            "config": {"workload": cfg.name, "N": cfg.N, "s": cfg.s, "K": cfg.K, "sweeps_per_step": sweeps,
+                       "eps_pp": cfg.eps_pp, "family": cfg.family, "noise": [cfg.noise_kind, cfg.noise],
+                       "parallelism": f"mode-0 slabs x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (X = %.0f MiB)" % (cfg.numel * 8 / 2**20)},
+            "phases": phases, "final_fitness": infos[-1]["fitness"],
+            "roofline": roofline, "roofline_all": roof_all, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line))
+    cp.cp_destroy(ctx)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -117,7 +117,7 @@ size_t cppp_workspace_bytes(int N, const int64_t *s, int K, const cppp_opts *o);
 /* Create a context for tensor X (order N, GLOBAL sizes s[0..N-1], rank K).
  *   X: host or device pointer to this rank's slab (whole tensor when unsharded), row-major.
  *   Computes ||X||_F^2 (all-reduced when sharded).  Factors start at zero: call
- *   cp_set_factors before any sweep.  2 <= N <= CPPP_MAX_ORDER, 1 <= K <= CPPP_MAX_RANK. */
+ *   cp_set_factors before any sweep.  3 <= N <= CPPP_MAX_ORDER, 1 <= K <= CPPP_MAX_RANK. */
 cppp_status cp_init(cppp_ctx **ctx, const double *X, int N, const int64_t *s, int K,
                     const cppp_opts *o);
 
@@ -184,6 +184,8 @@ size_t cppp_plan_describe(int N, int shard_mode, char *buf, size_t buflen);
 void cp_destroy(cppp_ctx *ctx);
 const char *cp_last_error(const cppp_ctx *ctx);
 const char *cppp_status_string(int status);
+/* Total kernel launches issued by this library in this process (all contexts). */
+uint64_t cppp_launch_count(void);
 /* Library build id "cppp <version> sm_100a". */
 const char *cppp_version(void);
 

@@ -97,6 +97,7 @@ def lib():
         "cp_last_error": (C.c_char_p, [P]),
         "cppp_status_string": (C.c_char_p, [I]),
         "cppp_version": (C.c_char_p, []),
+        "cppp_launch_count": (C.c_uint64, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -112,7 +113,7 @@ EXPORTED = ["cppp_default_opts", "cppp_workspace_bytes", "cp_init", "cp_set_fact
             "pp_get_single", "pp_update", "als_sweep", "cp_set_phase_override", "fitness",
             "cppp_kernel_stats", "cppp_reset_kernel_stats", "cppp_generate",
             "cppp_nccl_unique_id", "cppp_plan_describe", "cp_destroy", "cp_last_error",
-            "cppp_status_string", "cppp_version"]
+            "cppp_status_string", "cppp_version", "cppp_launch_count"]
 
 
 # ------------------------------------------------------------------ marshalling helpers
@@ -215,8 +216,9 @@ def cp_update_factors(ctx: Ctx, A: Sequence) -> None:
     _check(ctx, lib().cp_update_factors(ctx.h, _ptrs(arrs)))
 
 
-def cp_get_factors(ctx: Ctx) -> List[np.ndarray]:
-    out = [np.empty((ctx.s[n], ctx.K)) for n in range(ctx.N)]
+def cp_get_factors(ctx: Ctx, out=None) -> List:
+    if out is None:
+        out = [np.empty((ctx.s[n], ctx.K)) for n in range(ctx.N)]
     _check(ctx, lib().cp_get_factors(ctx.h, _ptrs(out)))
     return out
 
@@ -314,6 +316,10 @@ def cp_destroy(ctx: Ctx) -> None:
     if ctx is not None and ctx.h:
         lib().cp_destroy(ctx.h)
         ctx.h = C.c_void_p()
+
+
+def cppp_launch_count() -> int:
+    return int(lib().cppp_launch_count())
 
 
 def cppp_version() -> str:

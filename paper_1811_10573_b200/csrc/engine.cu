@@ -24,7 +24,6 @@ namespace {
 
 constexpr size_t ALIGN = 256;
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
-inline int popc(uint32_t m) { return __builtin_popcount(m); }
 
 // ---------------------------------------------------------------- NCCL (dlopen'ed on demand)
 struct Nccl {
@@ -223,9 +222,6 @@ cppp_status allreduce(cppp_ctx* c, double* buf, size_t count) {
 const double* fac_local(cppp_ctx* c, double* const* F, int u) {
   return F[u] + (u == c->q ? c->qoff * c->K : 0);
 }
-double* fac_local_mut(cppp_ctx* c, double* const* F, int u) {
-  return F[u] + (u == c->q ? c->qoff * c->K : 0);
-}
 int64_t node_elems(cppp_ctx* c, uint32_t mask) {
   int64_t e = c->K;
   for (int v = 0; v < c->N; ++v)
@@ -247,9 +243,10 @@ cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, doubl
   if (src.root) {
     const double flops = 2.0 * B * S * R * K;
     const double bytes = 8.0 * (B * S * R + B * R * K);
+    const bool simt = (c->flags & CPPP_FLAG_SIMT_TTM) != 0;
+    if (ttm_uses_dmma(B, S, R, K, simt)) CUCHK(c, ttm_prepare(S, F, K, c->Fpad, c->st));
     Prof p(c, CPPP_K_TTM, flops, bytes);
-    CUCHK(c, launch_ttm(src.data, B, S, R, F, K, out, c->Fpad,
-                        (c->flags & CPPP_FLAG_SIMT_TTM) != 0, c->st));
+    CUCHK(c, launch_ttm_core(src.data, B, S, R, F, K, out, c->Fpad, simt, c->st));
   } else {
     const double flops = 2.0 * B * S * R * K;
     const double bytes = 8.0 * (B * S * R * K + B * R * K);
@@ -603,13 +600,6 @@ struct Plan {
   size_t stack_bytes = 0;
 };
 
-size_t factor_block_doubles(const cppp_ctx* c) {
-  size_t d = 0;
-  for (int n = 0; n < c->N; ++n) d += align_up(sizeof(double) * c->s[n] * c->K) / 8 * 3;   // A, Ap, dA
-  for (int n = 0; n < c->N; ++n) d += align_up(sizeof(double) * c->dl[n] * c->K) / 8 * 3;  // M, Mp, T
-  return d;
-}
-
 cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   // sizes (bytes)
   const int N = c->N, K = c->K;
@@ -783,6 +773,8 @@ const char* cppp_status_string(int s) {
 }
 
 const char* cppp_version(void) { return "cppp 0.1 sm_100a"; }
+
+uint64_t cppp_launch_count(void) { return launch_count(); }
 
 const char* cp_last_error(const cppp_ctx* c) { return c ? c->err.c_str() : "null context"; }
 

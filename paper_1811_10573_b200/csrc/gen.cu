@@ -162,6 +162,7 @@ cudaError_t launch_gen_kruskal(double* X, int N, const int64_t* s, int K, const 
   if (nfib == 0) return cudaSuccess;
   int64_t blocks = nfib < 148 * 32 ? nfib : 148 * 32;
   gen_kruskal_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, N, d, K, f, row_lo, nfib);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -174,10 +175,12 @@ cudaError_t launch_gen_noise_rowsq(double* X, const int64_t* s, int N, uint64_t 
   if (nrows == 0) return cudaSuccess;
   gen_rowsq_kernel<<<(unsigned)(nrows * CHUNKS), 256, 0, st>>>(X, rowlen, (uint32_t)N, seed, row_lo,
                                                                 partials);
+  note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   gen_rowsq_final<<<(unsigned)((nrows + 127) / 128), 128, 0, st>>>(partials, nrows, row_lo,
                                                                      rowsq_x, rowsq_z);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -186,6 +189,7 @@ size_t gen_partials_doubles(int64_t nrows) { return static_cast<size_t>(nrows) *
 cudaError_t launch_gen_scale(const double* rowsq_x, const double* rowsq_z, int64_t s0, double eta,
                              double* scale_dev, cudaStream_t st) {
   gen_scale_kernel<<<1, 1, 0, st>>>(rowsq_x, rowsq_z, s0, eta, scale_dev);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -200,6 +204,7 @@ cudaError_t launch_gen_noise_add(double* X, const int64_t* s, int N, uint64_t se
   if (blocks > 148 * 64) blocks = 148 * 64;
   gen_noise_add_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, n, static_cast<uint64_t>(row_lo) * rowlen,
                                                           (uint32_t)N, seed, scale_dev, abs_scale);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -12,6 +12,11 @@ struct Dims {
   int64_t s[8];
 };
 
+// Count of kernel launches issued by this library (all contexts), for the bench's
+// gpu_launches claim.  note_launch() follows every <<<>>> in the library.
+void note_launch();
+uint64_t launch_count();
+
 // ---------------------------------------------------------------- kernel launchers
 // All launchers enqueue on `st` and return the launch's cudaError_t.
 
@@ -23,6 +28,13 @@ struct Dims {
 cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R,
                        const double* F, int K, double* out, double* Fpad,
                        bool force_simt, cudaStream_t st);
+// The two halves of launch_ttm, so the engine can time the GEMM alone: ttm_prepare pads F
+// into Fpad (no-op for the SIMT path); launch_ttm_core runs the GEMM.
+bool ttm_uses_dmma(int64_t B, int64_t S, int64_t R, int K, bool force_simt);
+cudaError_t ttm_prepare(int64_t S, const double* F, int K, double* Fpad, cudaStream_t st);
+cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
+                            int K, double* out, const double* Fpad, bool force_simt,
+                            cudaStream_t st);
 cudaError_t launch_ttm_simt(const double* X, int64_t B, int64_t S, int64_t R,
                             const double* F, int K, double* out, cudaStream_t st);
 bool ttm_dmma_supported(int64_t B, int64_t S, int64_t R, int K);

@@ -97,12 +97,14 @@ cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st) {
   const int xsplit = choose_xsplit(a.ny, max_nx);
   dim3 grid((unsigned)a.ny, (unsigned)xsplit);
   pp_update_partial<<<grid, NT, 0, st>>>(a, xsplit);
+  note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int64_t total = a.ny * a.K;
   int blocks = (int)((total + 255) / 256);
   if (blocks > 1184) blocks = 1184;
   pp_update_combine<<<blocks, 256, 0, st>>>(a, xsplit);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -414,6 +414,10 @@ int grid_for(int64_t n, int threads, int cap) {
 
 }  // namespace
 
+static unsigned long long g_launches = 0;
+void note_launch() { __atomic_add_fetch(&g_launches, 1ull, __ATOMIC_RELAXED); }
+uint64_t launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
 cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, SolveWS ws,
                                 cudaStream_t st) {
   const size_t smem = static_cast<size_t>(K) * (K + 1) * sizeof(double);
@@ -428,6 +432,7 @@ cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, SolveW
   // ws.L holds 2 K*K doubles: the factor / pseudo-inverse, then the Jacobi V scratch
   gamma_factor_kernel<<<1, GF_THREADS, smem, st>>>(S_all, N, n, K, ws.Gamma, ws.L, ws.mode,
                                                    ws.L + K * K);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -446,6 +451,7 @@ cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, dou
   const int blocks = grid_for(rows, SR_WARPS, 148);
   solve_rows_kernel<<<blocks, SR_WARPS * 32, smem, st>>>(M, A, ref, dA, rows, K, ws.Gamma, ws.L,
                                                          ws.mode, ws.rowstat);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -453,6 +459,7 @@ cudaError_t launch_gram_norms(const double* A, int64_t rows, int K, double* S,
                               const double* rowstat, double* nrm, cudaStream_t st) {
   const int blocks = grid_for((int64_t)K * K, 256, 1 << 20);
   gram_norms_kernel<<<blocks, 256, 0, st>>>(A, rows, K, S, rowstat, nrm);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -464,6 +471,7 @@ cudaError_t launch_fitness_terms(const double* M, const double* A, int64_t rows,
                                  const double* Gamma, const double* S, double* out,
                                  cudaStream_t st) {
   fitness_terms_kernel<<<1, 1024, 0, st>>>(M, A, rows * K, Gamma, S, (int64_t)K * K, out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -472,21 +480,25 @@ int sqnorm_blocks(int64_t n) { return grid_for(n, 256, 1184); }
 cudaError_t launch_sqnorm(const double* x, int64_t n, double* partial, int nblk, double* out,
                           cudaStream_t st) {
   sqnorm_partial<<<nblk, 256, 0, st>>>(x, n, partial);
+  note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   sum_final<<<1, 1024, 0, st>>>(partial, nblk, out);
+  note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   sub_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(a, b, y, n);
+  note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_pad_rows(const double* F, int64_t S, int K, double* Fp, int ld,
                             cudaStream_t st) {
   pad_rows_kernel<<<grid_for(S * ld, 256, 1184), 256, 0, st>>>(F, S, K, Fp, ld);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -310,6 +310,7 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
   const int64_t grid = mtiles * (MC ? B : 1);
   ttm_dmma_kernel<BN, MC><<<(unsigned)grid, NTHREADS, C::SMEM, st>>>(tmX, tmF, out, Mrows, mtiles,
                                                                      (int)S, K);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -347,19 +348,37 @@ cudaError_t launch_ttm_simt(const double* X, int64_t B, int64_t S, int64_t R, co
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
   ttm_simt_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, B, S, R, F, K, out);
+  note_launch();
   return cudaGetLastError();
+}
+
+bool ttm_uses_dmma(int64_t B, int64_t S, int64_t R, int K, bool force_simt) {
+  return !force_simt && ttm_dmma_supported(B, S, R, K);
+}
+
+cudaError_t ttm_prepare(int64_t S, const double* F, int K, double* Fpad, cudaStream_t st) {
+  const int BN = ((K + 15) / 16) * 16;
+  return launch_pad_rows(F, S, K, Fpad, BN, st);
+}
+
+cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
+                            int K, double* out, const double* Fpad, bool force_simt,
+                            cudaStream_t st) {
+  if (B * R * K == 0) return cudaSuccess;
+  if (!ttm_uses_dmma(B, S, R, K, force_simt)) return launch_ttm_simt(X, B, S, R, F, K, out, st);
+  const int BN = ((K + 15) / 16) * 16;
+  if (R == 1) return dispatch_bn<false>(BN, X, B, S, R, Fpad, K, out, st);
+  return dispatch_bn<true>(BN, X, B, S, R, Fpad, K, out, st);
 }
 
 cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R, const double* F, int K,
                        double* out, double* Fpad, bool force_simt, cudaStream_t st) {
   if (B * R * K == 0) return cudaSuccess;
-  if (force_simt || !ttm_dmma_supported(B, S, R, K))
-    return launch_ttm_simt(X, B, S, R, F, K, out, st);
-  const int BN = ((K + 15) / 16) * 16;
-  cudaError_t e = launch_pad_rows(F, S, K, Fpad, BN, st);
-  if (e != cudaSuccess) return e;
-  if (R == 1) return dispatch_bn<false>(BN, X, B, S, R, Fpad, K, out, st);
-  return dispatch_bn<true>(BN, X, B, S, R, Fpad, K, out, st);
+  if (ttm_uses_dmma(B, S, R, K, force_simt)) {
+    cudaError_t e = ttm_prepare(S, F, K, Fpad, st);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_ttm_core(X, B, S, R, F, K, out, Fpad, force_simt, st);
 }
 
 }  // namespace cppp

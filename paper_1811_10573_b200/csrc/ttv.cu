@@ -55,6 +55,7 @@ cudaError_t launch_ttv(const double* P, int64_t B, int64_t S, int64_t R, int K, 
   const int64_t cap = 148LL * 16;
   if (blocks > cap) blocks = cap;
   ttv_kernel<8><<<(unsigned)blocks, 256, 0, st>>>(P, B, S, RK, K, F, out);
+  note_launch();
   return cudaGetLastError();
 }
 
