@@ -102,9 +102,13 @@ struct cppp_ctx {
   double *A[CPPP_MAX_ORDER] = {}, *Ap[CPPP_MAX_ORDER] = {}, *dA[CPPP_MAX_ORDER] = {};
   double *M[CPPP_MAX_ORDER] = {}, *Mp[CPPP_MAX_ORDER] = {}, *T[CPPP_MAX_ORDER] = {};
   double* S_all = nullptr;   // N x K x K
-  double* Gamma = nullptr;   // K x K (of the last solved mode)
-  double* L = nullptr;       // 2 K x K
+  double* Gamma = nullptr;   // K x K (of the mode being solved)
+  double* L = nullptr;       // 2 K x K: Γ^(-1) or Γ^†, then Jacobi scratch
   int* lmode = nullptr;
+  double* gpart = nullptr;   // per-CTA partial Grams (solve_row_blocks(max s) x K x K)
+  cudaStream_t st2 = nullptr;           // side stream: Γ^(n) inverse overlapped with M^(n)
+  cudaEvent_t ev_S = nullptr, ev_P = nullptr;
+  int prefetched = -1;                  // mode whose Γ inverse is issued on st2
   double* rowstat = nullptr; // max local rows x 3
   double* stats = nullptr;   // N x 3 norms, then fitness terms [2], then ||X||² [1]
   double* Fpad = nullptr;    // max s x 128
@@ -112,6 +116,7 @@ struct cppp_ctx {
   double* pp_partial = nullptr;
   double* sq_partial = nullptr;
   double* gath = nullptr;    // gather scratch (max s x K)
+  double* ttv_scratch = nullptr;
   double* gen_scratch = nullptr;
   Stack stack;
   // state
@@ -251,27 +256,48 @@ cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, doubl
     const double flops = 2.0 * B * S * R * K;
     const double bytes = 8.0 * (B * S * R * K + B * R * K);
     Prof p(c, CPPP_K_TTV, flops, bytes);
-    CUCHK(c, launch_ttv(src.data, B, S, R, K, F, out, c->st));
+    CUCHK(c, launch_ttv(src.data, B, S, R, K, F, out, c->ttv_scratch, c->st));
   }
   return CPPP_OK;
 }
 
 // ---------------------------------------------------------------- small solve of one mode
 // A_new = M Γ^†, G, dA = A_new - ref, S^(n), norms (Alg. 1 P:393-399 / Alg. 3).
+// Issue Γ^(n) and its inverse on the side stream once every S^(m), m != n, is final (ev_S).
+cppp_status prefetch_inverse(cppp_ctx* c, int n) {
+  if (c->dry || c->prefetched == n) return CPPP_OK;
+  CUCHK(c, cudaStreamWaitEvent(c->st2, c->ev_S, 0));
+  CUCHK(c, launch_gamma_inverse(c->S_all, c->N, n, c->K, c->Gamma, c->L, c->lmode, c->L + c->K * c->K,
+                                c->st2));
+  CUCHK(c, cudaEventRecord(c->ev_P, c->st2));
+  c->prefetched = n;
+  return CPPP_OK;
+}
+
+// Drop a pending prefetch before the Grams are rewritten outside a sweep.
+cppp_status drain_prefetch(cppp_ctx* c) {
+  if (c->prefetched >= 0) CUCHK(c, cudaStreamWaitEvent(c->st, c->ev_P, 0));
+  c->prefetched = -1;
+  return CPPP_OK;
+}
+
+// A_new = M Γ^†, G, dA = A_new - ref, S^(n), norms (Alg. 1 P:393-399 / Alg. 3).
 cppp_status finish_mode(cppp_ctx* c, int n, const double* Mn, bool pp_phase) {
   if (c->dry) return CPPP_OK;
   const int K = c->K;
   const int64_t rows = c->dl[n];
   const int64_t off = (n == c->q) ? c->qoff : 0;
-  SolveWS ws{c->Gamma, c->L, c->lmode, c->rowstat};
+  STCHK(prefetch_inverse(c, n));
+  CUCHK(c, cudaStreamWaitEvent(c->st, c->ev_P, 0));
+  c->prefetched = -1;
   {
-    Prof p(c, CPPP_K_SOLVE, 2.0 * rows * K * K * 2 + K * K * K / 3.0, 8.0 * rows * K * 4);
-    CUCHK(c, launch_gamma_factor(c->S_all, c->N, n, K, ws, c->st));
+    Prof p(c, CPPP_K_SOLVE, 4.0 * rows * K * K, 8.0 * rows * K * 5);
     double* An = c->A[n] + off * K;
     const double* ref = pp_phase ? (c->Ap[n] + off * K) : An;
-    CUCHK(c, launch_solve_rows(Mn, An, ref, c->dA[n] + off * K, rows, K, ws, c->st));
-    CUCHK(c, launch_gram_norms(An, rows, K, c->S_all + (int64_t)n * K * K, c->rowstat,
-                               c->stats + 3 * n, c->st));
+    CUCHK(c, launch_solve_rows(Mn, An, ref, c->dA[n] + off * K, rows, K, c->Gamma, c->L, c->rowstat,
+                               c->gpart, c->st));
+    CUCHK(c, launch_gram_reduce(c->gpart, solve_row_blocks(rows), K, c->S_all + (int64_t)n * K * K,
+                                c->rowstat, rows, c->stats + 3 * n, c->st));
   }
   if (n == c->q) {
     STCHK(allreduce(c, c->S_all + (int64_t)n * K * K, (size_t)K * K));
@@ -282,7 +308,8 @@ cppp_status finish_mode(cppp_ctx* c, int n, const double* Mn, bool pp_phase) {
     CUCHK(c, launch_fitness_terms(Mn, c->A[n] + off * K, rows, K, c->Gamma,
                                   c->S_all + (int64_t)n * K * K, c->stats + 3 * c->N, c->st));
   }
-  return CPPP_OK;
+  CUCHK(c, cudaEventRecord(c->ev_S, c->st));
+  return prefetch_inverse(c, (n + 1) % c->N);
 }
 
 // ---------------------------------------------------------------- regular dimension tree
@@ -625,6 +652,7 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   size_t oS = take(sizeof(double) * N * K * K);
   size_t oG = take(sizeof(double) * K * K);
   size_t oL = take(sizeof(double) * 2 * K * K);
+  size_t oGp = take(sizeof(double) * (size_t)solve_row_blocks(smax) * K * K);
   size_t oLm = take(sizeof(int) * 4);
   size_t oRow = take(sizeof(double) * smax * 3);
   size_t oStats = take(sizeof(double) * (3 * N + 8));
@@ -635,6 +663,7 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   size_t oPP = take(sizeof(double) * pp_update_scratch_doubles(smax, K, smax));
   size_t oSq = take(sizeof(double) * 2048);
   size_t oGath = take(sizeof(double) * smax * K);
+  size_t oTtv = take(sizeof(double) * ttv_scratch_doubles());
   size_t oStack = off;
   plan->off_stack = oStack;
   // dry-run the DT sweep and the PP build to size the stack
@@ -662,6 +691,7 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   c->S_all = reinterpret_cast<double*>(b + oS);
   c->Gamma = reinterpret_cast<double*>(b + oG);
   c->L = reinterpret_cast<double*>(b + oL);
+  c->gpart = reinterpret_cast<double*>(b + oGp);
   c->lmode = reinterpret_cast<int*>(b + oLm);
   c->rowstat = reinterpret_cast<double*>(b + oRow);
   c->stats = reinterpret_cast<double*>(b + oStats);
@@ -671,6 +701,7 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   c->pp_partial = reinterpret_cast<double*>(b + oPP);
   c->sq_partial = reinterpret_cast<double*>(b + oSq);
   c->gath = reinterpret_cast<double*>(b + oGath);
+  c->ttv_scratch = reinterpret_cast<double*>(b + oTtv);
   c->stack = Stack{};
   c->stack.base = b + oStack;
   c->stack.cap = c->ws_bytes - oStack;
@@ -869,6 +900,9 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
   CUCHK(c, cudaMallocHost(&c->host_stats, sizeof(double) * (3 * N + 8)));
   CUCHK(c, cudaEventCreate(&c->ev_a));
   CUCHK(c, cudaEventCreate(&c->ev_b));
+  CUCHK(c, cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+  CUCHK(c, cudaEventCreateWithFlags(&c->ev_S, cudaEventDisableTiming));
+  CUCHK(c, cudaEventCreateWithFlags(&c->ev_P, cudaEventDisableTiming));
   // ||X||² (all-reduced)
   {
     Prof pr(c, CPPP_K_OTHER, 2.0 * c->numel_local, 8.0 * c->numel_local);
@@ -886,6 +920,7 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
 cppp_status cp_set_factors(cppp_ctx* c, const double* const* A) {
   if (!c) return CPPP_EINVAL;
   if (!A) return fail(c, CPPP_EINVAL, "null factor list");
+  STCHK(drain_prefetch(c));
   for (int n = 0; n < c->N; ++n) {
     if (!A[n]) return fail(c, CPPP_EINVAL, "null factor %d", n);
     STCHK(copy_in(c, c->A[n], A[n], (size_t)c->s[n] * c->K));
@@ -893,10 +928,11 @@ cppp_status cp_set_factors(cppp_ctx* c, const double* const* A) {
   for (int n = 0; n < c->N; ++n) {
     const int64_t off = (n == c->q) ? c->qoff : 0;
     CUCHK(c, launch_gram(c->A[n] + off * c->K, c->dl[n], c->K, c->S_all + (int64_t)n * c->K * c->K,
-                         c->st));
+                         c->gpart, c->st));
     if (n == c->q) STCHK(allreduce(c, c->S_all + (int64_t)n * c->K * c->K, (size_t)c->K * c->K));
     CUCHK(c, cudaMemsetAsync(c->dA[n], 0, sizeof(double) * c->s[n] * c->K, c->st));
   }
+  CUCHK(c, cudaEventRecord(c->ev_S, c->st));
   c->factors_set = true;
   c->ops_valid = false;
   c->next_phase = CPPP_PHASE_DT;
@@ -911,14 +947,16 @@ cppp_status cp_update_factors(cppp_ctx* c, const double* const* A) {
   if (!c) return CPPP_EINVAL;
   if (!A) return fail(c, CPPP_EINVAL, "null factor list");
   if (!c->factors_set) return fail(c, CPPP_ESTATE, "cp_update_factors before cp_set_factors");
+  STCHK(drain_prefetch(c));
   for (int n = 0; n < c->N; ++n) {
     if (!A[n]) return fail(c, CPPP_EINVAL, "null factor %d", n);
     STCHK(copy_in(c, c->A[n], A[n], (size_t)c->s[n] * c->K));
     const int64_t off = (n == c->q) ? c->qoff : 0;
     CUCHK(c, launch_gram(c->A[n] + off * c->K, c->dl[n], c->K, c->S_all + (int64_t)n * c->K * c->K,
-                         c->st));
+                         c->gpart, c->st));
     if (n == c->q) STCHK(allreduce(c, c->S_all + (int64_t)n * c->K * c->K, (size_t)c->K * c->K));
   }
+  CUCHK(c, cudaEventRecord(c->ev_S, c->st));
   CUCHK(c, cudaStreamSynchronize(c->st));
   return CPPP_OK;
 }
@@ -1026,6 +1064,7 @@ cppp_status als_sweep(cppp_ctx* c, double eps, double eps_pp, cppp_sweep_info* i
   if (phase == CPPP_PHASE_PP && !c->ops_valid)
     return fail(c, CPPP_ESTATE, "PP sweep requested without operators");
   CUCHK(c, cudaEventRecord(c->ev_a, c->st));
+  STCHK(prefetch_inverse(c, 0));
   if (phase == CPPP_PHASE_DT) {
     STCHK(run_dt(c, true, c->M));
   } else {
@@ -1209,6 +1248,7 @@ size_t cppp_plan_describe(int N, int shard_mode, char* buf, size_t buflen) {
 void cp_destroy(cppp_ctx* c) {
   if (!c) return;
   if (c->st) cudaStreamSynchronize(c->st);
+  if (c->st2) cudaStreamSynchronize(c->st2);
   prof_collect(c);
   for (auto e : c->evpool) cudaEventDestroy(e);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
@@ -1216,6 +1256,9 @@ void cp_destroy(cppp_ctx* c) {
   if (c->host_stats) cudaFreeHost(c->host_stats);
   if (c->own_ws && c->ws_alloc) cudaFree(c->ws_alloc);
   if (c->comm) g_nccl.commDestroy(c->comm);
+  if (c->ev_S) cudaEventDestroy(c->ev_S);
+  if (c->ev_P) cudaEventDestroy(c->ev_P);
+  if (c->st2) cudaStreamDestroy(c->st2);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
 }

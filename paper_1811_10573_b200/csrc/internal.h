@@ -41,8 +41,10 @@ bool ttm_dmma_supported(int64_t B, int64_t S, int64_t R, int K);
 
 // Multi-TTV: rank-diagonal contraction of one mode of a parent intermediate,
 // out[b][r][k] = Σ_x P[b][x][r][k] * F[x][k];  parent viewed as [B][S][R][K].
+// `scratch` (>= ttv_scratch_doubles(), may be null) enables the split-x path for small outputs.
 cudaError_t launch_ttv(const double* P, int64_t B, int64_t S, int64_t R, int K,
-                       const double* F, double* out, cudaStream_t st);
+                       const double* F, double* out, double* scratch, cudaStream_t st);
+size_t ttv_scratch_doubles();
 
 // Fused multi-output TTV: up to 3 children of one parent in one pass.  The parent is viewed
 // as [B][S0]...[S_{m-1}][T][K] where the children contract axis c of the m middle axes.
@@ -79,25 +81,24 @@ cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st);
 size_t pp_update_scratch_doubles(int64_t ny, int K, int64_t max_nx);
 
 // ---------------------------------------------------------------- small dense ops (K <= 128)
-// Gamma^(n) = Hadamard of S[m], m != n; Cholesky with the L13 pivot rule, else the
-// eigen pseudo-inverse (cyclic Jacobi).  Writes Gamma, L (or pinv P) and *mode (0 chol, 1 pinv).
-struct SolveWS {
-  double* Gamma;    // K x K
-  double* L;        // 2 K x K: Cholesky factor (lower) or the pseudo-inverse, then Jacobi scratch
-  int* mode;        // 0 = Cholesky, 1 = pinv
-  double* rowstat;  // per-row partial norms: s x 3  (||a_new||², ||dA||², ||g||²)
-};
-cudaError_t launch_gamma_factor(const double* S_all /* N x K x K */, int N, int n, int K, SolveWS ws,
-                                cudaStream_t st);
-// Row solves: A_new = M Gamma^† ; G = (A_old - A_new) Gamma ; dA = A_new - ref.
+// Γ^(n) = Hadamard of S[m], m != n -> Gamma; its inverse (Gauss-Jordan, L13 pivot rule)
+// or eigen pseudo-inverse -> P; *mode = 0 (inverse) / 1 (pinv).  One CTA.  Vscratch: K*K doubles.
+cudaError_t launch_gamma_inverse(const double* S_all /* N x K x K */, int N, int n, int K,
+                                 double* Gamma, double* P, int* mode, double* Vscratch,
+                                 cudaStream_t st);
+// Row solves: A_new = M P ; G = (A_old - A_new) Γ ; dA = A_new - ref ; per-row norms -> rowstat
+// (rows x 3: ||a_new||², ||dA||², ||g||²); per-CTA partial Grams -> gpart (solve_row_blocks x K*K).
 // A is updated in place; ref may alias A (DT: dA = A_new - A_old).
+int solve_row_blocks(int64_t rows);
 cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, double* dA,
-                              int64_t rows, int K, SolveWS ws, cudaStream_t st);
-// S = A^T A (K x K) and the per-mode norm triple reduced from rowstat -> nrm[0..2].
-cudaError_t launch_gram_norms(const double* A, int64_t rows, int K, double* S,
-                              const double* rowstat, double* nrm, cudaStream_t st);
-// plain Gram (no norms)
-cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, cudaStream_t st);
+                              int64_t rows, int K, const double* Gamma, const double* P,
+                              double* rowstat, double* gpart, cudaStream_t st);
+// S = Σ_b gpart[b]; if rowstat: nrm[0..2] = Σ_rows rowstat (fixed order)
+cudaError_t launch_gram_reduce(const double* gpart, int nb, int K, double* S,
+                               const double* rowstat, int64_t rows, double* nrm, cudaStream_t st);
+// S = AᵀA (partial Grams over 16-row blocks, then the reduction)
+cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, double* gpart,
+                        cudaStream_t st);
 // fitness pieces: out[0] = Σ M∘A (inner), out[1] = Σ Gamma∘S (model)
 cudaError_t launch_fitness_terms(const double* M, const double* A, int64_t rows, int K,
                                  const double* Gamma, const double* S, double* out,

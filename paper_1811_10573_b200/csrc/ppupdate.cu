@@ -37,15 +37,15 @@ __global__ void __launch_bounds__(NT)
       const double* op = t.op + y * t.sy + k;
       const double* d = t.dA + k;
       int64_t x = x0 + xg;
-      for (; x + 3 * G < x1; x += 4 * G) {
-        const double o0 = __ldcs(op + x * t.sx), o1 = __ldcs(op + (x + G) * t.sx);
-        const double o2 = __ldcs(op + (x + 2 * G) * t.sx), o3 = __ldcs(op + (x + 3 * G) * t.sx);
-        const double d0 = __ldg(d + x * K), d1 = __ldg(d + (x + G) * K);
-        const double d2 = __ldg(d + (x + 2 * G) * K), d3 = __ldg(d + (x + 3 * G) * K);
-        acc = fma(o0, d0, acc);
-        acc = fma(o1, d1, acc);
-        acc = fma(o2, d2, acc);
-        acc = fma(o3, d3, acc);
+      for (; x + 7 * G < x1; x += 8 * G) {
+        double o[8], dd[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          o[u] = __ldcs(op + (x + u * G) * t.sx);
+          dd[u] = __ldg(d + (x + u * G) * K);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = fma(o[u], dd[u], acc);
       }
       for (; x < x1; x += G) acc = fma(__ldcs(op + x * t.sx), __ldg(d + x * K), acc);
     }
@@ -73,8 +73,8 @@ __global__ void pp_update_combine(PPUpdateArgs a, int xsplit) {
 }
 
 int choose_xsplit(int64_t ny, int64_t max_nx) {
-  // aim for >= ~4 CTAs per SM, keep >= 8 x per part
-  int64_t want = (148 * 4 + ny - 1) / ny;
+  // aim for >= ~8 CTAs per SM, keep >= 8 x per part
+  int64_t want = (148 * 8 + ny - 1) / ny;
   int64_t cap = max_nx / 8;
   if (want > cap) want = cap;
   if (want > 16) want = 16;

@@ -6,6 +6,11 @@
 //   S^(n) = A_newᵀ A_new
 // plus ‖A‖², ‖dA‖², ‖G‖² per mode (the ε_pp test L7 and the stop metric) and the fitness
 // expansion terms.  K <= 128.  Every reduction has a fixed order (deterministic).
+//
+// Latency design: Γ^(n) only depends on the Grams, so its inverse is computed by
+// ONE CTA (register-resident Gauss-Jordan, one barrier per pivot) on a side stream while the main
+// stream computes M^(n); the main stream then runs one row kernel (A_new = M P, G, dA, norms and
+// a per-block partial Gram, all from shared memory) and one tiny reduction.
 #include "internal.h"
 
 namespace cppp {
@@ -36,82 +41,98 @@ __device__ double block_sum(double v, double* sh) {
   return r;
 }
 
-constexpr int GF_THREADS = 512;
 constexpr double PIVOT_TAU = 1e-12;  // L13 / S:201
 constexpr double PINV_TAU = 1e-12;
+constexpr int GI_THREADS = 1024;
+constexpr int GI_MAXE = 16;          // K*K <= 16384 = 16 * 1024 register-resident elements
 
-// Γ, Cholesky (right-looking, in shared memory) with the L13 pivot rule; on failure the
-// cyclic-Jacobi eigen pseudo-inverse (Brent-Luk parallel ordering).  One CTA.
-__global__ void __launch_bounds__(GF_THREADS)
-    gamma_factor_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
-                        double* Lout, int* mode, double* Vscratch) {
-  extern __shared__ double W[];  // K x (K+1)
+// ---------------------------------------------------------------- Γ and its (pseudo-)inverse
+// Gauss-Jordan on the SPD Γ without pivoting: the pivot of step j is the Schur complement
+// diagonal, i.e. exactly the Cholesky pivot d_j of the L13 rule (accept iff every d_j >
+// τ·max diag Γ).  Each thread keeps up to 16 entries of W in registers; row j and column j are
+// broadcast through double-buffered shared memory, so one barrier per pivot.  On a rejected
+// pivot the eigen pseudo-inverse (cyclic Jacobi, Brent-Luk parallel ordering) takes over.
+__global__ void __launch_bounds__(GI_THREADS, 1)
+    gamma_inverse_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
+                         double* Pout, int* mode, double* Vscratch) {
+  extern __shared__ double W[];  // K x (K+1), Jacobi fallback only
+  __shared__ double rowb[2][128], colb[2][128];
   __shared__ double sh[32];
-  __shared__ int s_ok;
-  const int P = K + 1;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  double dmax_local = 0.0;
-  for (int e = tid; e < K * K; e += nt) {
-    double v = 0.0;
-    bool first = true;
-    for (int m = 0; m < N; ++m) {
-      if (m == n) continue;
-      const double sv = S_all[(int64_t)m * K * K + e];
-      v = first ? sv : v * sv;
-      first = false;
-    }
-    Gamma[e] = v;
-    const int i = e / K, j = e - i * K;
-    W[i * P + j] = v;
-    if (i == j) dmax_local = fmax(dmax_local, v);
-  }
-  // max diag (fixed order reduction via max is order independent)
-  double dm = dmax_local;
+  const int tid = threadIdx.x, KK = K * K;
+  double w[GI_MAXE];
+  int wi[GI_MAXE], wl[GI_MAXE];
+  double dmax = 0.0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
-  if ((tid & 31) == 0) sh[tid >> 5] = dm;
+  for (int u = 0; u < GI_MAXE; ++u) {
+    const int e = tid + u * GI_THREADS;
+    w[u] = 0.0;
+    wi[u] = -1;
+    wl[u] = -1;
+    if (e < KK) {
+      double v = 0.0;
+      bool first = true;
+      for (int m = 0; m < N; ++m) {
+        if (m == n) continue;
+        const double sv = S_all[(int64_t)m * KK + e];
+        v = first ? sv : v * sv;
+        first = false;
+      }
+      Gamma[e] = v;
+      w[u] = v;
+      wi[u] = e / K;
+      wl[u] = e - wi[u] * K;
+      if (wi[u] == wl[u]) dmax = fmax(dmax, v);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  if ((tid & 31) == 0) sh[tid >> 5] = dmax;
   __syncthreads();
   if (tid == 0) {
     double m = 0.0;
-    for (int w = 0; w < (nt + 31) / 32; ++w) m = fmax(m, sh[w]);
+    for (int i = 0; i < GI_THREADS / 32; ++i) m = fmax(m, sh[i]);
     sh[0] = m;
-    s_ok = 1;
   }
   __syncthreads();
   const double thresh = PIVOT_TAU * sh[0];
-  // ---- Cholesky, right-looking
+  bool ok = true;
   for (int j = 0; j < K; ++j) {
-    if (tid == 0) {
-      const double d = W[j * P + j];
-      if (!(d > thresh)) s_ok = 0;
-      else W[j * P + j] = sqrt(d);
+    const int b = j & 1;
+#pragma unroll
+    for (int u = 0; u < GI_MAXE; ++u) {
+      if (wi[u] == j) rowb[b][wl[u]] = w[u];
+      if (wl[u] == j) colb[b][wi[u]] = w[u];
     }
     __syncthreads();
-    if (!s_ok) break;
-    const double ljj = W[j * P + j];
-    for (int i = j + 1 + tid; i < K; i += nt) W[i * P + j] /= ljj;
-    __syncthreads();
-    const int m = K - j - 1;
-    // trailing lower triangle (j < l <= i < K) as an m x m square, lower half only
-    for (int e = tid; e < m * m; e += nt) {
-      const int ii = e / m, ll = e - ii * m;
-      if (ll <= ii) {
-        const int i = j + 1 + ii, l = j + 1 + ll;
-        W[i * P + l] -= W[i * P + j] * W[l * P + j];
-      }
+    const double p = rowb[b][j];
+    if (!(p > thresh)) {
+      ok = false;
+      break;
     }
-    __syncthreads();
+    const double inv = 1.0 / p;
+#pragma unroll
+    for (int u = 0; u < GI_MAXE; ++u) {
+      const int i = wi[u], l = wl[u];
+      if (i < 0) continue;
+      if (i == j) w[u] = (l == j) ? inv : w[u] * inv;
+      else if (l == j) w[u] = -w[u] * inv;
+      else w[u] = fma(-colb[b][i] * inv, rowb[b][l], w[u]);
+    }
   }
-  if (s_ok) {
-    for (int e = tid; e < K * K; e += nt) {
-      const int i = e / K, j = e - i * K;
-      Lout[e] = (j <= i) ? W[i * P + j] : 0.0;
+  if (ok) {
+#pragma unroll
+    for (int u = 0; u < GI_MAXE; ++u) {
+      const int e = tid + u * GI_THREADS;
+      if (e < KK) Pout[e] = w[u];
     }
     if (tid == 0) *mode = 0;
     return;
   }
-  // ---- eigen pseudo-inverse: two-sided cyclic Jacobi on W (reloaded), V in global scratch
-  for (int e = tid; e < K * K; e += nt) {
+  __syncthreads();
+  // ---- eigen pseudo-inverse: two-sided cyclic Jacobi on W (from Γ), V in global scratch
+  const int P = K + 1;
+  const int nt = GI_THREADS;
+  for (int e = tid; e < KK; e += nt) {
     const int i = e / K, j = e - i * K;
     W[i * P + j] = Gamma[e];
     Vscratch[e] = (i == j) ? 1.0 : 0.0;
@@ -121,12 +142,12 @@ __global__ void __launch_bounds__(GF_THREADS)
   __shared__ double cs[64], sn[64];
   __shared__ int pp_[64], qq_[64];
   for (int sweep = 0; sweep < 40; ++sweep) {
-    // convergence: off-diagonal mass relative to the diagonal
     double off = 0.0, dia = 0.0;
-    for (int e = tid; e < K * K; e += nt) {
+    for (int e = tid; e < KK; e += nt) {
       const int i = e / K, j = e - i * K;
       const double v = W[i * P + j];
-      if (i == j) dia += v * v; else off += v * v;
+      if (i == j) dia += v * v;
+      else off += v * v;
     }
     off = block_sum(off, sh);
     dia = block_sum(dia, sh);
@@ -134,9 +155,18 @@ __global__ void __launch_bounds__(GF_THREADS)
     for (int r = 0; r < Ke - 1; ++r) {
       if (tid < Ke / 2) {
         int p, q;
-        if (tid == 0) { p = Ke - 1; q = r; }
-        else { p = (r + tid) % (Ke - 1); q = (r - tid + Ke - 1) % (Ke - 1); }
-        if (p > q) { int tmp = p; p = q; q = tmp; }
+        if (tid == 0) {
+          p = Ke - 1;
+          q = r;
+        } else {
+          p = (r + tid) % (Ke - 1);
+          q = (r - tid + Ke - 1) % (Ke - 1);
+        }
+        if (p > q) {
+          const int tmp = p;
+          p = q;
+          q = tmp;
+        }
         double c = 1.0, s = 0.0;
         if (q < K) {
           const double apq = W[p * P + q];
@@ -147,11 +177,13 @@ __global__ void __launch_bounds__(GF_THREADS)
             s = t * c;
           }
         }
-        cs[tid] = c; sn[tid] = s; pp_[tid] = p; qq_[tid] = q;
+        cs[tid] = c;
+        sn[tid] = s;
+        pp_[tid] = p;
+        qq_[tid] = q;
       }
       __syncthreads();
-      // rows: W <- J^T W
-      for (int e = tid; e < (Ke / 2) * K; e += nt) {
+      for (int e = tid; e < (Ke / 2) * K; e += nt) {  // rows: W <- Jᵀ W
         const int pr = e / K, l = e - pr * K;
         const int p = pp_[pr], q = qq_[pr];
         if (q >= K) continue;
@@ -161,8 +193,7 @@ __global__ void __launch_bounds__(GF_THREADS)
         W[q * P + l] = s * wp + c * wq;
       }
       __syncthreads();
-      // columns: W <- W J, V <- V J
-      for (int e = tid; e < (Ke / 2) * K; e += nt) {
+      for (int e = tid; e < (Ke / 2) * K; e += nt) {  // columns: W <- W J, V <- V J
         const int pr = e / K, l = e - pr * K;
         const int p = pp_[pr], q = qq_[pr];
         if (q >= K) continue;
@@ -177,7 +208,6 @@ __global__ void __launch_bounds__(GF_THREADS)
       __syncthreads();
     }
   }
-  // eigenvalues on the diagonal; λ⁺ with cutoff PINV_TAU * λmax
   __shared__ double lam[128];
   for (int i = tid; i < K; i += nt) lam[i] = W[i * P + i];
   __syncthreads();
@@ -193,145 +223,140 @@ __global__ void __launch_bounds__(GF_THREADS)
     lam[i] = (lmax > 0.0 && l > PINV_TAU * lmax) ? 1.0 / l : 0.0;
   }
   __syncthreads();
-  for (int e = tid; e < K * K; e += nt) {
+  for (int e = tid; e < KK; e += nt) {
     const int i = e / K, j = e - i * K;
     double v = 0.0;
     for (int l = 0; l < K; ++l) v += Vscratch[i * K + l] * lam[l] * Vscratch[j * K + l];
-    Lout[e] = v;
+    Pout[e] = v;
   }
   if (tid == 0) *mode = 1;
 }
 
-// One warp per row y.  Lane c owns columns c, c+32, c+64, c+96.  Cholesky path: forward then
-// back substitution with L staged in shared memory (pitch K+1, conflict-free columns);
-// pinv path: a = m P.  Then g = (a_old - a_new) Γ, dA = a_new - ref, row norm partials.
+// ---------------------------------------------------------------- row solves + partial Gram
+// One warp per row (16 rows per CTA).  Shared memory: W (K x K: P, then Γ) and the CTA's rows of
+// M, A_new and A_old - A_new.  Lane c owns columns c + 32u.
 constexpr int SR_WARPS = 16;
 
 __global__ void __launch_bounds__(SR_WARPS * 32)
     solve_rows_kernel(const double* __restrict__ M, double* A, const double* ref, double* dA,
                       int64_t rows, int K, const double* __restrict__ Gamma,
-                      const double* __restrict__ L, const int* __restrict__ mode_p,
-                      double* __restrict__ rowstat) {
-  extern __shared__ double Ls[];  // K x (K+1) when mode == 0
-  const int P = K + 1;
-  const int mode = *mode_p;
-  if (mode == 0) {
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-      const int i = e / K, j = e - i * K;
-      Ls[i * P + j] = L[e];
+                      const double* __restrict__ Pm, double* __restrict__ rowstat,
+                      double* __restrict__ gpart) {
+  extern __shared__ double sm[];
+  const int KK = K * K;
+  double* Ws = sm;                     // K*K
+  double* Ms = Ws + KK;                // SR_WARPS*K
+  double* As = Ms + SR_WARPS * K;      // SR_WARPS*K
+  double* Ds = As + SR_WARPS * K;      // SR_WARPS*K
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t y = blockIdx.x * (int64_t)SR_WARPS + w;
+  const bool valid = y < rows;
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) Ws[e] = Pm[e];
+  double aold[4], rf[4], a[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int c = lane + 32 * u;
+    const bool in = valid && c < K;
+    aold[u] = in ? A[y * K + c] : 0.0;
+    rf[u] = in ? ref[y * K + c] : 0.0;
+    if (c < K) Ms[w * K + c] = in ? M[y * K + c] : 0.0;
+  }
+  __syncthreads();
+  // A_new = m P
+#pragma unroll
+  for (int u = 0; u < 4; ++u) a[u] = 0.0;
+  for (int p = 0; p < K; ++p) {
+    const double mp = Ms[w * K + p];
+    const double* wr = Ws + p * K;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = lane + 32 * u;
+      if (c < K) a[u] = fma(mp, wr[c], a[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int c = lane + 32 * u;
+    if (c < K) {
+      As[w * K + c] = valid ? a[u] : 0.0;
+      Ds[w * K + c] = valid ? aold[u] - a[u] : 0.0;
     }
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t y = blockIdx.x * (int64_t)SR_WARPS + w; y < rows; y += (int64_t)gridDim.x * SR_WARPS) {
-    double m[4], a[4], aold[4], rf[4];
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) Ws[e] = Gamma[e];
+  __syncthreads();
+  // G row = (a_old - a_new) Γ
+  double g[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int p = 0; p < K; ++p) {
+    const double dp = Ds[w * K + p];
+    const double* wr = Ws + p * K;
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int c = lane + 32 * s;
-      m[s] = c < K ? M[y * K + c] : 0.0;
-      aold[s] = c < K ? A[y * K + c] : 0.0;
-      rf[s] = c < K ? ref[y * K + c] : 0.0;
+    for (int u = 0; u < 4; ++u) {
+      const int c = lane + 32 * u;
+      if (c < K) g[u] = fma(dp, wr[c], g[u]);
     }
-    if (mode == 0) {
-      // forward: L z = m  (z overwrites m)
-      for (int j = 0; j < K; ++j) {
-        const int owner = j & 31, slot = j >> 5;
-        double zj = 0.0;
-        if (lane == owner) {
-          double v = (slot == 0) ? m[0] : (slot == 1) ? m[1] : (slot == 2) ? m[2] : m[3];
-          zj = v / Ls[j * P + j];
-        }
-        zj = __shfl_sync(0xffffffffu, zj, owner);
+  }
+  double na = 0.0, nd = 0.0, ng = 0.0;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const int c = lane + 32 * s;
-          if (c == j) m[s] = zj;
-          else if (c > j && c < K) m[s] -= Ls[c * P + j] * zj;
-        }
-      }
-      // back: L^T a = z
-      for (int j = K - 1; j >= 0; --j) {
-        const int owner = j & 31, slot = j >> 5;
-        double aj = 0.0;
-        if (lane == owner) {
-          double v = (slot == 0) ? m[0] : (slot == 1) ? m[1] : (slot == 2) ? m[2] : m[3];
-          aj = v / Ls[j * P + j];
-        }
-        aj = __shfl_sync(0xffffffffu, aj, owner);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const int c = lane + 32 * s;
-          if (c == j) m[s] = aj;
-          else if (c < j) m[s] -= Ls[j * P + c] * aj;
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < 4; ++s) a[s] = (lane + 32 * s < K) ? m[s] : 0.0;
-    } else {
-#pragma unroll
-      for (int s = 0; s < 4; ++s) a[s] = 0.0;
-      for (int p = 0; p < K; ++p) {
-        const int owner = p & 31, slot = p >> 5;
-        double mp = (slot == 0) ? m[0] : (slot == 1) ? m[1] : (slot == 2) ? m[2] : m[3];
-        mp = __shfl_sync(0xffffffffu, mp, owner);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const int c = lane + 32 * s;
-          if (c < K) a[s] = fma(mp, L[p * K + c], a[s]);
-        }
-      }
+  for (int u = 0; u < 4; ++u) {
+    const int c = lane + 32 * u;
+    if (valid && c < K) {
+      const double d = a[u] - rf[u];
+      A[y * K + c] = a[u];
+      dA[y * K + c] = d;
+      na = fma(a[u], a[u], na);
+      nd = fma(d, d, nd);
+      ng = fma(g[u], g[u], ng);
     }
-    // gradient g = (a_old - a_new) Γ
-    double g[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int p = 0; p < K; ++p) {
-      const int owner = p & 31, slot = p >> 5;
-      double dp = (slot == 0) ? aold[0] - a[0] : (slot == 1) ? aold[1] - a[1]
-                : (slot == 2) ? aold[2] - a[2] : aold[3] - a[3];
-      dp = __shfl_sync(0xffffffffu, dp, owner);
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const int c = lane + 32 * s;
-        if (c < K) g[s] = fma(dp, Gamma[p * K + c], g[s]);
-      }
-    }
-    double na = 0.0, nd = 0.0, ng = 0.0;
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int c = lane + 32 * s;
-      if (c < K) {
-        const double d = a[s] - rf[s];
-        A[y * K + c] = a[s];
-        dA[y * K + c] = d;
-        na += a[s] * a[s];
-        nd += d * d;
-        ng += g[s] * g[s];
-      }
-    }
-    na = warp_sum(na);
-    nd = warp_sum(nd);
-    ng = warp_sum(ng);
-    if (lane == 0) {
-      rowstat[y * 3 + 0] = na;
-      rowstat[y * 3 + 1] = nd;
-      rowstat[y * 3 + 2] = ng;
-    }
+  }
+  na = warp_sum(na);
+  nd = warp_sum(nd);
+  ng = warp_sum(ng);
+  if (valid && lane == 0) {
+    rowstat[y * 3 + 0] = na;
+    rowstat[y * 3 + 1] = nd;
+    rowstat[y * 3 + 2] = ng;
+  }
+  // partial Gram of this CTA's rows (rows in ascending order)
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    const int k1 = e / K, k2 = e - k1 * K;
+    double s = 0.0;
+#pragma unroll 4
+    for (int r = 0; r < SR_WARPS; ++r) s = fma(As[r * K + k1], As[r * K + k2], s);
+    gpart[(int64_t)blockIdx.x * KK + e] = s;
   }
 }
 
-// S = AᵀA: thread per (k1 <= k2), sum over rows ascending, mirrored (exactly symmetric).
-// Block 0 also reduces the per-row norm partials in row order -> nrm[0..2].
-__global__ void gram_norms_kernel(const double* __restrict__ A, int64_t rows, int K, double* S,
-                                  const double* __restrict__ rowstat, double* nrm) {
-  const int64_t pairs = (int64_t)K * K;
-  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e < pairs) {
-    const int k1 = static_cast<int>(e / K), k2 = static_cast<int>(e % K);
-    if (k1 <= k2) {
-      double acc = 0.0;
-      for (int64_t y = 0; y < rows; ++y) acc = fma(A[y * K + k1], A[y * K + k2], acc);
-      S[k1 * K + k2] = acc;
-      S[k2 * K + k1] = acc;
-    }
+// partial Gram only (rows staged in shared memory), same partial layout as solve_rows
+__global__ void __launch_bounds__(SR_WARPS * 32)
+    gram_partial_kernel(const double* __restrict__ A, int64_t rows, int K,
+                        double* __restrict__ gpart) {
+  extern __shared__ double As[];  // SR_WARPS x K
+  const int KK = K * K;
+  const int64_t y0 = blockIdx.x * (int64_t)SR_WARPS;
+  for (int e = threadIdx.x; e < SR_WARPS * K; e += blockDim.x) {
+    const int64_t y = y0 + e / K;
+    As[e] = y < rows ? A[y0 * K + e] : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    const int k1 = e / K, k2 = e - k1 * K;
+    double s = 0.0;
+#pragma unroll 4
+    for (int r = 0; r < SR_WARPS; ++r) s = fma(As[r * K + k1], As[r * K + k2], s);
+    gpart[(int64_t)blockIdx.x * KK + e] = s;
+  }
+}
+
+// S = Σ_b gpart[b] (ascending b); block 0 also reduces the row norms in row order.
+__global__ void gram_reduce_kernel(const double* __restrict__ gpart, int nb, int K, double* S,
+                                   const double* __restrict__ rowstat, int64_t rows, double* nrm) {
+  const int KK = K * K;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < KK) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += gpart[(int64_t)b * KK + e];
+    S[e] = s;
   }
   if (rowstat != nullptr && blockIdx.x == 0) {
     __shared__ double sh[32];
@@ -418,53 +443,58 @@ static unsigned long long g_launches = 0;
 void note_launch() { __atomic_add_fetch(&g_launches, 1ull, __ATOMIC_RELAXED); }
 uint64_t launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
-cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, SolveWS ws,
-                                cudaStream_t st) {
+int solve_row_blocks(int64_t rows) { return static_cast<int>((rows + SR_WARPS - 1) / SR_WARPS); }
+
+cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int K, double* Gamma, double* P,
+                                 int* mode, double* Vscratch, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(K) * (K + 1) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gamma_factor_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         128 * 129 * 8);
+    cudaError_t e = cudaFuncSetAttribute(gamma_inverse_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 129 * 8);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  // ws.L holds 2 K*K doubles: the factor / pseudo-inverse, then the Jacobi V scratch
-  gamma_factor_kernel<<<1, GF_THREADS, smem, st>>>(S_all, N, n, K, ws.Gamma, ws.L, ws.mode,
-                                                   ws.L + K * K);
+  gamma_inverse_kernel<<<1, GI_THREADS, smem, st>>>(S_all, N, n, K, Gamma, P, mode, Vscratch);
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, double* dA,
-                              int64_t rows, int K, SolveWS ws, cudaStream_t st) {
+                              int64_t rows, int K, const double* Gamma, const double* P,
+                              double* rowstat, double* gpart, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  const size_t smem = static_cast<size_t>(K) * (K + 1) * sizeof(double);
+  const size_t smem = (static_cast<size_t>(K) * K + 3 * SR_WARPS * K) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(solve_rows_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         128 * 129 * 8);
+                                         (128 * 128 + 3 * SR_WARPS * 128) * 8);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int blocks = grid_for(rows, SR_WARPS, 148);
-  solve_rows_kernel<<<blocks, SR_WARPS * 32, smem, st>>>(M, A, ref, dA, rows, K, ws.Gamma, ws.L,
-                                                         ws.mode, ws.rowstat);
+  solve_rows_kernel<<<solve_row_blocks(rows), SR_WARPS * 32, smem, st>>>(M, A, ref, dA, rows, K,
+                                                                         Gamma, P, rowstat, gpart);
   note_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_gram_norms(const double* A, int64_t rows, int K, double* S,
-                              const double* rowstat, double* nrm, cudaStream_t st) {
-  const int blocks = grid_for((int64_t)K * K, 256, 1 << 20);
-  gram_norms_kernel<<<blocks, 256, 0, st>>>(A, rows, K, S, rowstat, nrm);
+cudaError_t launch_gram_reduce(const double* gpart, int nb, int K, double* S,
+                               const double* rowstat, int64_t rows, double* nrm, cudaStream_t st) {
+  gram_reduce_kernel<<<grid_for((int64_t)K * K, 256, 1 << 20), 256, 0, st>>>(gpart, nb, K, S, rowstat,
+                                                                            rows, nrm);
   note_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, cudaStream_t st) {
-  return launch_gram_norms(A, rows, K, S, nullptr, nullptr, st);
+cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, double* gpart,
+                        cudaStream_t st) {
+  const int nb = solve_row_blocks(rows);
+  gram_partial_kernel<<<nb, SR_WARPS * 32, SR_WARPS * K * sizeof(double), st>>>(A, rows, K, gpart);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_gram_reduce(gpart, nb, K, S, nullptr, 0, nullptr, st);
 }
 
 cudaError_t launch_fitness_terms(const double* M, const double* A, int64_t rows, int K,

@@ -44,13 +44,72 @@ __global__ void ttv_kernel(const double* __restrict__ P, int64_t B, int64_t S, i
   }
 }
 
+// Small outputs (the lower tree levels of an order-3 tensor: s²K -> sK): split the x range
+// over `xsplit` independent partial sums, then add them in a fixed order.
+__global__ void ttv_split_kernel(const double* __restrict__ P, int64_t S, int64_t RK, int K,
+                                 int64_t total, int xsplit, const double* __restrict__ F,
+                                 double* __restrict__ part) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int p = blockIdx.y;
+  if (e >= total) return;
+  const int64_t b = e / RK;
+  const int64_t rk = e - b * RK;
+  const int k = static_cast<int>(rk % K);
+  const int64_t x0 = S * p / xsplit, x1 = S * (p + 1) / xsplit;
+  const double* pp = P + b * S * RK + rk;
+  const double* f = F + k;
+  double acc = 0.0;
+  int64_t x = x0;
+  for (; x + 4 <= x1; x += 4) {
+    const double p0 = __ldcs(pp + x * RK), p1 = __ldcs(pp + (x + 1) * RK);
+    const double p2 = __ldcs(pp + (x + 2) * RK), p3 = __ldcs(pp + (x + 3) * RK);
+    acc = fma(p0, __ldg(f + x * K), acc);
+    acc = fma(p1, __ldg(f + (x + 1) * K), acc);
+    acc = fma(p2, __ldg(f + (x + 2) * K), acc);
+    acc = fma(p3, __ldg(f + (x + 3) * K), acc);
+  }
+  for (; x < x1; ++x) acc = fma(__ldcs(pp + x * RK), __ldg(f + x * K), acc);
+  part[p * total + e] = acc;
+}
+
+__global__ void ttv_combine_kernel(const double* __restrict__ part, int64_t total, int xsplit,
+                                   double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < xsplit; ++p) s += part[p * total + e];
+    out[e] = s;
+  }
+}
+
 }  // namespace
 
+size_t ttv_scratch_doubles() { return static_cast<size_t>(148) * 2048 * 16; }
+
 cudaError_t launch_ttv(const double* P, int64_t B, int64_t S, int64_t R, int K, const double* F,
-                       double* out, cudaStream_t st) {
+                       double* out, double* scratch, cudaStream_t st) {
   const int64_t RK = R * K;
   const int64_t total = B * RK;
   if (total == 0) return cudaSuccess;
+  const int64_t target = 148LL * 2048;
+  if (scratch != nullptr && total < target && S >= 32) {
+    int64_t xs = (target + total - 1) / total;
+    xs = xs > S / 8 ? S / 8 : xs;
+    xs = xs > 64 ? 64 : xs;
+    const int64_t cap = static_cast<int64_t>(ttv_scratch_doubles()) / total;
+    xs = xs > cap ? cap : xs;
+    if (xs >= 2) {
+      dim3 grid((unsigned)((total + 255) / 256), (unsigned)xs);
+      ttv_split_kernel<<<grid, 256, 0, st>>>(P, S, RK, K, total, (int)xs, F, scratch);
+      note_launch();
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      int blocks = (int)((total + 255) / 256);
+      ttv_combine_kernel<<<blocks, 256, 0, st>>>(scratch, total, (int)xs, out);
+      note_launch();
+      return cudaGetLastError();
+    }
+  }
   int64_t blocks = (total + 255) / 256;
   const int64_t cap = 148LL * 16;
   if (blocks > cap) blocks = cap;
@@ -66,7 +125,7 @@ cudaError_t launch_ttv_multi(const TtvMulti& p, cudaStream_t st) {
     int64_t Bc = p.B, Rc = p.T;
     for (int a = 0; a < c; ++a) Bc *= p.S[a];
     for (int a = c + 1; a < p.m; ++a) Rc *= p.S[a];
-    cudaError_t e = launch_ttv(p.P, Bc, p.S[c], Rc, p.K, p.F[c], p.out[c], st);
+    cudaError_t e = launch_ttv(p.P, Bc, p.S[c], Rc, p.K, p.F[c], p.out[c], nullptr, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -162,3 +162,35 @@ def test_error_paths():
     assert e.value.status == -1
     with pytest.raises(cp.CpppError):
         cp.cp_init(X, 3, (40, 40, 40), 129)
+
+
+def test_singular_gamma_uses_pseudo_inverse():
+    """Duplicate factor columns make every Γ singular: both sides must take the eigen
+    pseudo-inverse branch of L13 and agree on the minimum-norm solution."""
+    cfg, X, A0 = problem("C1")
+    A = [a.copy() for a in A0]
+    for a in A:
+        a[:, 1] = a[:, 0]
+    st = O.State(X, A)
+    st.dt_sweep()
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    cp.cp_set_factors(ctx, A)
+    cp.cp_set_phase_override(ctx, "dt")
+    cp.als_sweep(ctx, 0.0, cfg.eps_pp)
+    got = cp.cp_get_factors(ctx)
+    for n in range(cfg.N):
+        assert rel(got[n], st.A[n]) < 1e-8, n
+
+
+@pytest.mark.parametrize("dims,K", [((160, 150, 140), 128), ((30, 28, 26, 24), 64)])
+def test_sweeps_large_rank(dims, K):
+    X, _ = random_problem(dims, K, 5)
+    r = np.random.default_rng(6)
+    A0 = [r.random((d, K)) for d in dims]
+    _, tr = O.pp_cp_als(X, A0, 0.0, 0.5, 6)
+    ctx = cp.cp_init(X, len(dims), dims, K)
+    cp.cp_set_factors(ctx, A0)
+    for t in tr:
+        cp.cp_set_phase_override(ctx, t["phase"])
+        info = cp.als_sweep(ctx, 0.0, 0.5)
+        assert abs(info["fitness"] - t["fitness"]) < 1e-8, (t, info)
