@@ -59,29 +59,29 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
   __shared__ double rowb[2][128], colb[2][128];
   __shared__ double sh[32];
   const int tid = threadIdx.x, KK = K * K;
+  // thread owns column l = tid % 128 and rows i = rg + 8v, v = 0..15 (rg = tid / 128):
+  // the row indices are compile-time, so W stays in 16 registers
+  const int l = tid & 127, rg = tid >> 7;
+  const bool col_ok = l < K;
   double w[GI_MAXE];
-  int wi[GI_MAXE], wl[GI_MAXE];
   double dmax = 0.0;
 #pragma unroll
-  for (int u = 0; u < GI_MAXE; ++u) {
-    const int e = tid + u * GI_THREADS;
-    w[u] = 0.0;
-    wi[u] = -1;
-    wl[u] = -1;
-    if (e < KK) {
-      double v = 0.0;
+  for (int v = 0; v < GI_MAXE; ++v) {
+    const int i = rg + 8 * v;
+    w[v] = 0.0;
+    if (col_ok && i < K) {
+      const int e = i * K + l;
+      double x = 0.0;
       bool first = true;
       for (int m = 0; m < N; ++m) {
         if (m == n) continue;
         const double sv = S_all[(int64_t)m * KK + e];
-        v = first ? sv : v * sv;
+        x = first ? sv : x * sv;
         first = false;
       }
-      Gamma[e] = v;
-      w[u] = v;
-      wi[u] = e / K;
-      wl[u] = e - wi[u] * K;
-      if (wi[u] == wl[u]) dmax = fmax(dmax, v);
+      Gamma[e] = x;
+      w[v] = x;
+      if (i == l) dmax = fmax(dmax, x);
     }
   }
 #pragma unroll
@@ -98,10 +98,13 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
   bool ok = true;
   for (int j = 0; j < K; ++j) {
     const int b = j & 1;
+    if (col_ok) {
 #pragma unroll
-    for (int u = 0; u < GI_MAXE; ++u) {
-      if (wi[u] == j) rowb[b][wl[u]] = w[u];
-      if (wl[u] == j) colb[b][wi[u]] = w[u];
+      for (int v = 0; v < GI_MAXE; ++v) {
+        const int i = rg + 8 * v;
+        if (i == j) rowb[b][l] = w[v];
+        if (l == j && i < K) colb[b][i] = w[v];
+      }
     }
     __syncthreads();
     const double p = rowb[b][j];
@@ -110,20 +113,31 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
       break;
     }
     const double inv = 1.0 / p;
+    if (col_ok) {
+      const double rl = rowb[b][l] * inv;
+      if (l == j) {
 #pragma unroll
-    for (int u = 0; u < GI_MAXE; ++u) {
-      const int i = wi[u], l = wl[u];
-      if (i < 0) continue;
-      if (i == j) w[u] = (l == j) ? inv : w[u] * inv;
-      else if (l == j) w[u] = -w[u] * inv;
-      else w[u] = fma(-colb[b][i] * inv, rowb[b][l], w[u]);
+        for (int v = 0; v < GI_MAXE; ++v) {
+          const int i = rg + 8 * v;
+          w[v] = (i == j) ? inv : -w[v] * inv;
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < GI_MAXE; ++v) {
+          const int i = rg + 8 * v;
+          if (i >= K) continue;
+          w[v] = (i == j) ? rl : fma(-colb[b][i], rl, w[v]);
+        }
+      }
     }
   }
   if (ok) {
+    if (col_ok) {
 #pragma unroll
-    for (int u = 0; u < GI_MAXE; ++u) {
-      const int e = tid + u * GI_THREADS;
-      if (e < KK) Pout[e] = w[u];
+      for (int v = 0; v < GI_MAXE; ++v) {
+        const int i = rg + 8 * v;
+        if (i < K) Pout[i * K + l] = w[v];
+      }
     }
     if (tid == 0) *mode = 0;
     return;

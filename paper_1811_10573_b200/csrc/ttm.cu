@@ -85,33 +85,36 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// Stage depth per BN so that STAGES * (16 KiB + 2 KiB * BN/16) stays within ~200 KiB.
-template <int BN>
+// NT = number of 8-wide n-tiles (BN = 8 NT >= K); the factor is staged 16 columns per TMA box,
+// so smem holds BNP = round_up(BN, 16) columns and the odd last tile (if any) is skipped.
+template <int NT>
 struct Cfg {
+  static constexpr int BN = 8 * NT;
+  static constexpr int BNP = ((BN + 15) / 16) * 16;
   static constexpr int XBYTES = BM * BK * 8;           // 16 KiB
-  static constexpr int FBYTES = BK * BN * 8;           // 2 KiB per 16 columns
+  static constexpr int FBYTES = BK * BNP * 8;          // 2 KiB per 16 columns
   static constexpr int STAGE = XBYTES + FBYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
-  static constexpr int SMEM = STAGES * STAGE + 2 * STAGES * 8 + 1024;
+  static constexpr int MAX_STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+  static int smem(int stages) { return stages * STAGE + 2 * stages * 8 + 1024; }
 };
 
-template <int BN, bool MC>
-__global__ void __launch_bounds__(NTHREADS, 1)
+// Persistent: CTA b processes tiles b, b + gridDim.x, ...; the producer warp runs ahead across
+// tile boundaries (bounded by the ring), so the next tile's loads overlap this tile's epilogue.
+template <int NT, bool MC>
+__global__ void __launch_bounds__(NTHREADS)
     ttm_dmma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
-                    double* __restrict__ out, int64_t Mrows, int64_t mtiles, int S, int K) {
-  using C = Cfg<BN>;
+                    double* __restrict__ out, int64_t Mrows, int64_t mtiles, int64_t ntiles, int S,
+                    int K, int stages) {
+  using C = Cfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + C::STAGES * C::STAGE);
-  uint64_t* empty = full + C::STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + stages * C::STAGE);
+  uint64_t* empty = full + stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tile = blockIdx.x;
-  const int64_t b = MC ? tile / mtiles : 0;
-  const int64_t m0 = (tile - b * mtiles) * BM;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < stages; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), NWARP);
     }
@@ -125,24 +128,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmF)) : "memory");
-      for (int kt = 0; kt < nk; ++kt) {
-        const int st = kt % C::STAGES;
-        const uint32_t ph = (kt / C::STAGES) & 1;
-        if (kt >= C::STAGES) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
-        const uint32_t fb = smem_u32(&full[st]);
-        mbar_expect_tx(fb, C::STAGE);
-        const uint32_t sx = smem_u32(base + st * C::STAGE);
-        const uint32_t sf = sx + C::XBYTES;
-        if (!MC) {
-          tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb);
-        } else {
+      int64_t it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t b = MC ? tile / mtiles : 0;
+        const int64_t m0 = (tile - b * mtiles) * BM;
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int st = static_cast<int>(it % stages);
+          const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+          if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+          const uint32_t fb = smem_u32(&full[st]);
+          mbar_expect_tx(fb, C::STAGE);
+          const uint32_t sx = smem_u32(base + st * C::STAGE);
+          const uint32_t sf = sx + C::XBYTES;
+          if (!MC) {
+            tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb);
+          } else {
 #pragma unroll
-          for (int c = 0; c < BM / 16; ++c)
-            tma_3d(sx + c * 2048, &tmX, static_cast<int>(m0 + 16 * c), kt * BK,
-                   static_cast<int>(b), fb);
+            for (int c = 0; c < BM / 16; ++c)
+              tma_3d(sx + c * 2048, &tmX, static_cast<int>(m0 + 16 * c), kt * BK,
+                     static_cast<int>(b), fb);
+          }
+#pragma unroll
+          for (int c = 0; c < C::BNP / 16; ++c) tma_2d(sf + c * 2048, &tmF, 16 * c, kt * BK, fb);
         }
-#pragma unroll
-        for (int c = 0; c < BN / 16; ++c) tma_2d(sf + c * 2048, &tmF, 16 * c, kt * BK, fb);
       }
     }
     return;
@@ -150,78 +158,88 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   // ---------------- consumers: warp owns rows [16*warp, 16*warp+16) x all BN columns
   const int g = lane >> 2, t = lane & 3;
-  double acc[2][BN / 8][2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < BN / 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
   // k-contiguous A rows: tile i, fragment row g -> box row 16w + 8i + fm(g), fm(g) = (g>>1)|((g&1)<<2)
   const int fm = (g >> 1) | ((g & 1) << 2);
+  const bool pairs = (K % 2) == 0;
+  int64_t it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t b = MC ? tile / mtiles : 0;
+    const int64_t m0 = (tile - b * mtiles) * BM;
+    double acc[2][NT][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  for (int kt = 0; kt < nk; ++kt) {
-    const int st = kt % C::STAGES;
-    const uint32_t ph = (kt / C::STAGES) & 1;
-    mbar_wait(smem_u32(&full[st]), ph);
-    const uint32_t sx = smem_u32(base + st * C::STAGE);
-    const uint32_t sf = sx + C::XBYTES;
+    for (int kt = 0; kt < nk; ++kt, ++it) {
+      const int st = static_cast<int>(it % stages);
+      const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+      mbar_wait(smem_u32(&full[st]), ph);
+      const uint32_t sx = smem_u32(base + st * C::STAGE);
+      const uint32_t sf = sx + C::XBYTES;
+      const int qmax = (S - kt * BK) > 8 ? 2 : 1;   // skip an all-zero k tail
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      double a[2][2];  // [m-tile i][kk]
-      if (!MC) {
+      for (int q = 0; q < 2; ++q) {
+        if (q >= qmax) break;
+        double a[2][2];  // [m-tile i][kk]
+        if (!MC) {
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int row = 16 * warp + 8 * i + fm;
-          const int chunk = 4 * q + t;
-          lds2(a[i][0], a[i][1], sx + row * 128 + ((chunk ^ (row & 7)) << 4));
+          for (int i = 0; i < 2; ++i) {
+            const int row = 16 * warp + 8 * i + fm;
+            const int chunk = 4 * q + t;
+            lds2(a[i][0], a[i][1], sx + row * 128 + ((chunk ^ (row & 7)) << 4));
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int row = 8 * q + 2 * t + kk;
+            lds2(a[0][kk], a[1][kk], sx + warp * 2048 + row * 128 + ((g ^ (row & 7)) << 4));
+          }
         }
-      } else {
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
           const int row = 8 * q + 2 * t + kk;
-          lds2(a[0][kk], a[1][kk], sx + warp * 2048 + row * 128 + ((g ^ (row & 7)) << 4));
+          const uint32_t frow = sf + row * 128 + ((g ^ (row & 7)) << 4);
+#pragma unroll
+          for (int c = 0; c < C::BNP / 16; ++c) {
+            double b0, b1;
+            lds2(b0, b1, frow + c * 2048);
+            dmma(acc[0][2 * c], a[0][kk], b0);
+            dmma(acc[1][2 * c], a[1][kk], b0);
+            if (2 * c + 1 < NT) {
+              dmma(acc[0][2 * c + 1], a[0][kk], b1);
+              dmma(acc[1][2 * c + 1], a[1][kk], b1);
+            }
+          }
         }
       }
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-        const int row = 8 * q + 2 * t + kk;
-        const uint32_t frow = sf + row * 128 + ((g ^ (row & 7)) << 4);
-#pragma unroll
-        for (int c = 0; c < BN / 16; ++c) {
-          double b0, b1;
-          lds2(b0, b1, frow + c * 2048);
-          dmma(acc[0][2 * c], a[0][kk], b0);
-          dmma(acc[1][2 * c], a[1][kk], b0);
-          dmma(acc[0][2 * c + 1], a[0][kk], b1);
-          dmma(acc[1][2 * c + 1], a[1][kk], b1);
-        }
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
-  }
 
-  // ---------------- epilogue: thread holds rows {r_i} x columns 16c + 4t + {0,1,2,3}
-  const bool pairs = (K % 2) == 0;
+    // ---------------- epilogue: thread holds rows {r_i} x columns 16c + 4t + {0,1,2,3}
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int mloc = MC ? (16 * warp + 2 * g + i) : (16 * warp + 8 * i + fm);
-    const int64_t m = m0 + mloc;
-    if (m >= Mrows) continue;
-    double* orow = out + (b * Mrows + m) * static_cast<int64_t>(K);
+    for (int i = 0; i < 2; ++i) {
+      const int mloc = MC ? (16 * warp + 2 * g + i) : (16 * warp + 8 * i + fm);
+      const int64_t m = m0 + mloc;
+      if (m >= Mrows) continue;
+      double* orow = out + (b * Mrows + m) * static_cast<int64_t>(K);
 #pragma unroll
-    for (int c = 0; c < BN / 16; ++c) {
-      const int n0 = 16 * c + 4 * t;
-      const double v0 = acc[i][2 * c][0], v1 = acc[i][2 * c + 1][0];
-      const double v2 = acc[i][2 * c][1], v3 = acc[i][2 * c + 1][1];
-      if (pairs && n0 + 3 < K) {
-        *reinterpret_cast<double2*>(orow + n0) = make_double2(v0, v1);
-        *reinterpret_cast<double2*>(orow + n0 + 2) = make_double2(v2, v3);
-      } else {
-        if (n0 < K) orow[n0] = v0;
-        if (n0 + 1 < K) orow[n0 + 1] = v1;
-        if (n0 + 2 < K) orow[n0 + 2] = v2;
-        if (n0 + 3 < K) orow[n0 + 3] = v3;
+      for (int c = 0; c < C::BNP / 16; ++c) {
+        const int n0 = 16 * c + 4 * t;
+        const double v0 = acc[i][2 * c][0];
+        const double v2 = acc[i][2 * c][1];
+        const double v1 = (2 * c + 1 < NT) ? acc[i][2 * c + 1 < NT ? 2 * c + 1 : 0][0] : 0.0;
+        const double v3 = (2 * c + 1 < NT) ? acc[i][2 * c + 1 < NT ? 2 * c + 1 : 0][1] : 0.0;
+        if (pairs && n0 + 3 < K) {
+          *reinterpret_cast<double2*>(orow + n0) = make_double2(v0, v1);
+          *reinterpret_cast<double2*>(orow + n0 + 2) = make_double2(v2, v3);
+        } else {
+          if (n0 < K) orow[n0] = v0;
+          if (n0 + 1 < K) orow[n0 + 1] = v1;
+          if (n0 + 2 < K) orow[n0 + 2] = v2;
+          if (n0 + 3 < K) orow[n0 + 3] = v3;
+        }
       }
     }
   }
@@ -276,14 +294,15 @@ bool make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims,
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool MC>
+template <int NT, bool MC>
 cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
                      double* out, cudaStream_t st) {
-  using C = Cfg<BN>;
+  using C = Cfg<NT>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(ttm_dmma_kernel<BN, MC>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(ttm_dmma_kernel<NT, MC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::smem(C::MAX_STAGES));
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -301,33 +320,42 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
     if (!make_map(&tmX, X, 3, dims, str, box)) return cudaErrorInvalidValue;
   }
   {
-    cuuint64_t dims[2] = {(cuuint64_t)BN, (cuuint64_t)S};
-    cuuint64_t str[1] = {(cuuint64_t)BN * 8};
+    cuuint64_t dims[2] = {(cuuint64_t)C::BNP, (cuuint64_t)S};
+    cuuint64_t str[1] = {(cuuint64_t)C::BNP * 8};
     cuuint32_t box[2] = {16, 16};
     if (!make_map(&tmF, Fp, 2, dims, str, box)) return cudaErrorInvalidValue;
   }
+  const int nk = static_cast<int>((S + BK - 1) / BK);
+  const int stages = nk < C::MAX_STAGES ? (nk < 2 ? 2 : nk) : C::MAX_STAGES;
+  const int smem = C::smem(stages);
   const int64_t mtiles = (Mrows + BM - 1) / BM;
-  const int64_t grid = mtiles * (MC ? B : 1);
-  ttm_dmma_kernel<BN, MC><<<(unsigned)grid, NTHREADS, C::SMEM, st>>>(tmX, tmF, out, Mrows, mtiles,
-                                                                     (int)S, K);
+  const int64_t ntiles = mtiles * (MC ? B : 1);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ttm_dmma_kernel<NT, MC>, NTHREADS, smem);
+  if (occ < 1) occ = 1;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int64_t grid = static_cast<int64_t>(sms) * occ;
+  if (grid > ntiles) grid = ntiles;
+  ttm_dmma_kernel<NT, MC><<<(unsigned)grid, NTHREADS, smem, st>>>(tmX, tmF, out, Mrows, mtiles, ntiles,
+                                                                   (int)S, K, stages);
   note_launch();
   return cudaGetLastError();
 }
 
-template <bool MC>
-cudaError_t dispatch_bn(int BN, const double* X, int64_t B, int64_t S, int64_t R, const double* Fp,
+template <bool MC, int NT = 1>
+cudaError_t dispatch_nt(int nt, const double* X, int64_t B, int64_t S, int64_t R, const double* Fp,
                         int K, double* out, cudaStream_t st) {
-  switch (BN) {
-    case 16: return run_dmma<16, MC>(X, B, S, R, Fp, K, out, st);
-    case 32: return run_dmma<32, MC>(X, B, S, R, Fp, K, out, st);
-    case 48: return run_dmma<48, MC>(X, B, S, R, Fp, K, out, st);
-    case 64: return run_dmma<64, MC>(X, B, S, R, Fp, K, out, st);
-    case 80: return run_dmma<80, MC>(X, B, S, R, Fp, K, out, st);
-    case 96: return run_dmma<96, MC>(X, B, S, R, Fp, K, out, st);
-    case 112: return run_dmma<112, MC>(X, B, S, R, Fp, K, out, st);
-    case 128: return run_dmma<128, MC>(X, B, S, R, Fp, K, out, st);
+  if constexpr (NT > 16) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (nt == NT) return run_dmma<NT, MC>(X, B, S, R, Fp, K, out, st);
+    return dispatch_nt<MC, NT + 1>(nt, X, B, S, R, Fp, K, out, st);
   }
-  return cudaErrorInvalidValue;
 }
 
 }  // namespace
@@ -356,9 +384,11 @@ bool ttm_uses_dmma(int64_t B, int64_t S, int64_t R, int K, bool force_simt) {
   return !force_simt && ttm_dmma_supported(B, S, R, K);
 }
 
+// padded factor width for K: 16-column TMA boxes
+int ttm_ld(int K) { return ((((K + 7) / 8) * 8 + 15) / 16) * 16; }
+
 cudaError_t ttm_prepare(int64_t S, const double* F, int K, double* Fpad, cudaStream_t st) {
-  const int BN = ((K + 15) / 16) * 16;
-  return launch_pad_rows(F, S, K, Fpad, BN, st);
+  return launch_pad_rows(F, S, K, Fpad, ttm_ld(K), st);
 }
 
 cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
@@ -366,9 +396,9 @@ cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, co
                             cudaStream_t st) {
   if (B * R * K == 0) return cudaSuccess;
   if (!ttm_uses_dmma(B, S, R, K, force_simt)) return launch_ttm_simt(X, B, S, R, F, K, out, st);
-  const int BN = ((K + 15) / 16) * 16;
-  if (R == 1) return dispatch_bn<false>(BN, X, B, S, R, Fpad, K, out, st);
-  return dispatch_bn<true>(BN, X, B, S, R, Fpad, K, out, st);
+  const int nt = (K + 7) / 8;
+  if (R == 1) return dispatch_nt<false>(nt, X, B, S, R, Fpad, K, out, st);
+  return dispatch_nt<true>(nt, X, B, S, R, Fpad, K, out, st);
 }
 
 cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R, const double* F, int K,
