@@ -201,15 +201,22 @@ __global__ void __launch_bounds__(NTHREADS)
           const int row = 8 * q + 2 * t + kk;
           const uint32_t frow = sf + row * 128 + ((g ^ (row & 7)) << 4);
 #pragma unroll
-          for (int c = 0; c < C::BNP / 16; ++c) {
+          for (int c = 0; c < NT / 2; ++c) {   // tile pair: columns 16c + 2g (+1), interleaved
             double b0, b1;
             lds2(b0, b1, frow + c * 2048);
             dmma(acc[0][2 * c], a[0][kk], b0);
             dmma(acc[1][2 * c], a[1][kk], b0);
-            if (2 * c + 1 < NT) {
-              dmma(acc[0][2 * c + 1], a[0][kk], b1);
-              dmma(acc[1][2 * c + 1], a[1][kk], b1);
-            }
+            dmma(acc[0][2 * c + 1], a[0][kk], b1);
+            dmma(acc[1][2 * c + 1], a[1][kk], b1);
+          }
+          if (NT & 1) {  // unpaired last tile: contiguous columns 16c + g, 8-byte loads
+            constexpr int c = NT / 2;
+            double b0;
+            asm volatile("ld.shared.f64 %0, [%1];"
+                         : "=d"(b0)
+                         : "r"(sf + c * 2048 + row * 128 + (((g >> 1) ^ (row & 7)) << 4) + ((g & 1) << 3)));
+            dmma(acc[0][NT - 1], a[0][kk], b0);
+            dmma(acc[1][NT - 1], a[1][kk], b0);
           }
         }
       }
@@ -225,12 +232,10 @@ __global__ void __launch_bounds__(NTHREADS)
       if (m >= Mrows) continue;
       double* orow = out + (b * Mrows + m) * static_cast<int64_t>(K);
 #pragma unroll
-      for (int c = 0; c < C::BNP / 16; ++c) {
+      for (int c = 0; c < NT / 2; ++c) {
         const int n0 = 16 * c + 4 * t;
-        const double v0 = acc[i][2 * c][0];
-        const double v2 = acc[i][2 * c][1];
-        const double v1 = (2 * c + 1 < NT) ? acc[i][2 * c + 1 < NT ? 2 * c + 1 : 0][0] : 0.0;
-        const double v3 = (2 * c + 1 < NT) ? acc[i][2 * c + 1 < NT ? 2 * c + 1 : 0][1] : 0.0;
+        const double v0 = acc[i][2 * c][0], v1 = acc[i][2 * c + 1][0];
+        const double v2 = acc[i][2 * c][1], v3 = acc[i][2 * c + 1][1];
         if (pairs && n0 + 3 < K) {
           *reinterpret_cast<double2*>(orow + n0) = make_double2(v0, v1);
           *reinterpret_cast<double2*>(orow + n0 + 2) = make_double2(v2, v3);
@@ -239,6 +244,16 @@ __global__ void __launch_bounds__(NTHREADS)
           if (n0 + 1 < K) orow[n0 + 1] = v1;
           if (n0 + 2 < K) orow[n0 + 2] = v2;
           if (n0 + 3 < K) orow[n0 + 3] = v3;
+        }
+      }
+      if (NT & 1) {
+        const int n0 = 16 * (NT / 2) + 2 * t;
+        const double v0 = acc[i][NT - 1][0], v1 = acc[i][NT - 1][1];
+        if (pairs && n0 + 1 < K) {
+          *reinterpret_cast<double2*>(orow + n0) = make_double2(v0, v1);
+        } else {
+          if (n0 < K) orow[n0] = v0;
+          if (n0 + 1 < K) orow[n0 + 1] = v1;
         }
       }
     }
