@@ -24,7 +24,8 @@ uint64_t launch_count();
 // X viewed as [B][S][R] (row-major), F is S x K (ld K), out is [B][R][K].
 // R == 1 is the natural mode-(N-1) unfolding X(BxS)·F; R > 1 contracts a middle/first mode.
 // Uses the DMMA (FP64 tensor core) kernel with TMA staging when the shape allows it (even
-// S and R, K <= 128), else the SIMT FP64 kernel.  `Fpad` is scratch of >= S*128 doubles.
+// S and R, K <= 128), else the SIMT FP64 kernel.  `Fpad` is scratch of >= S*128 + 32 doubles
+// (padded factor, then the persistent kernel's tile counter).
 cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R,
                        const double* F, int K, double* out, double* Fpad,
                        bool force_simt, cudaStream_t st);

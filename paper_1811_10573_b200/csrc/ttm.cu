@@ -104,13 +104,14 @@ template <int NT, bool MC>
 __global__ void __launch_bounds__(NTHREADS)
     ttm_dmma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
                     double* __restrict__ out, int64_t Mrows, int64_t mtiles, int64_t ntiles, int S,
-                    int K, int stages) {
+                    int K, int stages, unsigned long long* __restrict__ tile_counter) {
   using C = Cfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(base + stages * C::STAGE);
   uint64_t* empty = full + stages;
+  __shared__ long long stage_tile[16];   // tile id carried by the first k-stage of each tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -129,31 +130,20 @@ __global__ void __launch_bounds__(NTHREADS)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmF)) : "memory");
       int64_t it = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t b = MC ? tile / mtiles : 0;
-        const int64_t m0 = (tile - b * mtiles) * BM;
-        for (int kt = 0; kt < nk; ++kt, ++it) {
+      while (true) {
+        // dynamic tile scheduler: robust to SMs that are busy with other streams' work
+        const long long tile = static_cast<long long>(atomicAdd(tile_counter, 1ull));
+        if (tile >= ntiles) {
           const int st = static_cast<int>(it % stages);
           const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
           if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
-          const uint32_t fb = smem_u32(&full[st]);
-          mbar_expect_tx(fb, C::STAGE);
-          const uint32_t sx = smem_u32(base + st * C::STAGE);
-          const uint32_t sf = sx + C::XBYTES;
-          if (!MC) {
-            tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BM / 16; ++c)
-              tma_3d(sx + c * 2048, &tmX, static_cast<int>(m0 + 16 * c), kt * BK,
-                     static_cast<int>(b), fb);
-          }
-#pragma unroll
-          for (int c = 0; c < C::BNP / 16; ++c) tma_2d(sf + c * 2048, &tmF, 16 * c, kt * BK, fb);
+          stage_tile[st] = -1;
+          mbar_arrive(smem_u32(&full[st]));   // wake the consumers with the sentinel
+          break;
         }
-      }
-    }
-    return;
+        const int64_t b = MC ? tile / mtiles : 0;
+        const int64_t m0 = (tile - b * mtiles) * BM;
+        for (int kt = 0; kt < nk; ++kt, ++it) {    return;
   }
 
   // ---------------- consumers: warp owns rows [16*warp, 16*warp+16) x all BN columns
@@ -162,7 +152,13 @@ __global__ void __launch_bounds__(NTHREADS)
   const int fm = (g >> 1) | ((g & 1) << 2);
   const bool pairs = (K % 2) == 0;
   int64_t it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  while (true) {
+    {
+      const int st = static_cast<int>(it % stages);
+      mbar_wait(smem_u32(&full[st]), static_cast<uint32_t>((it / stages) & 1));
+    }
+    const long long tile = stage_tile[static_cast<int>(it % stages)];
+    if (tile < 0) break;
     const int64_t b = MC ? tile / mtiles : 0;
     const int64_t m0 = (tile - b * mtiles) * BM;
     double acc[2][NT][2];
@@ -174,7 +170,7 @@ __global__ void __launch_bounds__(NTHREADS)
     for (int kt = 0; kt < nk; ++kt, ++it) {
       const int st = static_cast<int>(it % stages);
       const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
-      mbar_wait(smem_u32(&full[st]), ph);
+      if (kt > 0) mbar_wait(smem_u32(&full[st]), ph);
       const uint32_t sx = smem_u32(base + st * C::STAGE);
       const uint32_t sf = sx + C::XBYTES;
       const int qmax = (S - kt * BK) > 8 ? 2 : 1;   // skip an all-zero k tail
@@ -311,7 +307,7 @@ bool make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims,
 
 template <int NT, bool MC>
 cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
-                     double* out, cudaStream_t st) {
+                     double* out, unsigned long long* counter, cudaStream_t st) {
   using C = Cfg<NT>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -356,20 +352,22 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
   }
   int64_t grid = static_cast<int64_t>(sms) * occ;
   if (grid > ntiles) grid = ntiles;
+  cudaError_t e0 = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+  if (e0 != cudaSuccess) return e0;
   ttm_dmma_kernel<NT, MC><<<(unsigned)grid, NTHREADS, smem, st>>>(tmX, tmF, out, Mrows, mtiles, ntiles,
-                                                                   (int)S, K, stages);
+                                                                   (int)S, K, stages, counter);
   note_launch();
   return cudaGetLastError();
 }
 
 template <bool MC, int NT = 1>
 cudaError_t dispatch_nt(int nt, const double* X, int64_t B, int64_t S, int64_t R, const double* Fp,
-                        int K, double* out, cudaStream_t st) {
+                        int K, double* out, unsigned long long* counter, cudaStream_t st) {
   if constexpr (NT > 16) {
     return cudaErrorInvalidValue;
   } else {
-    if (nt == NT) return run_dmma<NT, MC>(X, B, S, R, Fp, K, out, st);
-    return dispatch_nt<MC, NT + 1>(nt, X, B, S, R, Fp, K, out, st);
+    if (nt == NT) return run_dmma<NT, MC>(X, B, S, R, Fp, K, out, counter, st);
+    return dispatch_nt<MC, NT + 1>(nt, X, B, S, R, Fp, K, out, counter, st);
   }
 }
 
@@ -411,9 +409,12 @@ cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, co
                             cudaStream_t st) {
   if (B * R * K == 0) return cudaSuccess;
   if (!ttm_uses_dmma(B, S, R, K, force_simt)) return launch_ttm_simt(X, B, S, R, F, K, out, st);
+  // the tile counter lives right after the padded factor (see ttm_fpad_doubles)
+  unsigned long long* counter =
+      reinterpret_cast<unsigned long long*>(const_cast<double*>(Fpad) + S * ttm_ld(K));
   const int nt = (K + 7) / 8;
-  if (R == 1) return dispatch_nt<false>(nt, X, B, S, R, Fpad, K, out, st);
-  return dispatch_nt<true>(nt, X, B, S, R, Fpad, K, out, st);
+  if (R == 1) return dispatch_nt<false>(nt, X, B, S, R, Fpad, K, out, counter, st);
+  return dispatch_nt<true>(nt, X, B, S, R, Fpad, K, out, counter, st);
 }
 
 cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R, const double* F, int K,
