@@ -143,7 +143,29 @@ __global__ void __launch_bounds__(NTHREADS)
         }
         const int64_t b = MC ? tile / mtiles : 0;
         const int64_t m0 = (tile - b * mtiles) * BM;
-        for (int kt = 0; kt < nk; ++kt, ++it) {    return;
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+          const int st = static_cast<int>(it % stages);
+          const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+          if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+          if (kt == 0) stage_tile[st] = tile;
+          const uint32_t fb = smem_u32(&full[st]);
+          mbar_expect_tx(fb, C::STAGE);
+          const uint32_t sx = smem_u32(base + st * C::STAGE);
+          const uint32_t sf = sx + C::XBYTES;
+          if (!MC) {
+            tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 16; ++c)
+              tma_3d(sx + c * 2048, &tmX, static_cast<int>(m0 + 16 * c), kt * BK,
+                     static_cast<int>(b), fb);
+          }
+#pragma unroll
+          for (int c = 0; c < C::BNP / 16; ++c) tma_2d(sf + c * 2048, &tmF, 16 * c, kt * BK, fb);
+        }
+      }
+    }
+    return;
   }
 
   // ---------------- consumers: warp owns rows [16*warp, 16*warp+16) x all BN columns

@@ -7,8 +7,20 @@
 #include <vector>
 #include "../paper_1811_10573_b200/csrc/solve.cu"
 
+__global__ void spin(double* o, int n) {
+  double a = threadIdx.x;
+  for (int i = 0; i < n; ++i) a = fma(a, 1.0000001, 1e-9);
+  if (a == 0.5) o[0] = a;
+}
+
 int main() {
   using namespace cppp;
+  {
+    double* o;
+    cudaMalloc(&o, 8);
+    for (int r = 0; r < 40; ++r) spin<<<148 * 8, 256>>>(o, 1 << 16);   // ramp the SM clock
+    cudaDeviceSynchronize();
+  }
   for (int K : {10, 30, 50, 100, 128}) {
     const int N = 3, s = 400;
     std::vector<double> A(s * K), S(N * K * K);
