@@ -43,8 +43,8 @@ __device__ double block_sum(double v, double* sh) {
 
 constexpr double PIVOT_TAU = 1e-12;  // L13 / S:201
 constexpr double PINV_TAU = 1e-12;
-constexpr int GI_THREADS = 1024;
-constexpr int GI_MAXE = 16;          // K*K <= 16384 = 16 * 1024 register-resident elements
+constexpr int GI_THREADS = 512;
+constexpr int GI_MAXE = 32;          // K*K <= 16384 = 32 * 512 register-resident elements
 
 // ---------------------------------------------------------------- Γ and its (pseudo-)inverse
 // Gauss-Jordan on the SPD Γ without pivoting: the pivot of step j is the Schur complement
@@ -56,18 +56,18 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
     gamma_inverse_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
                          double* Pout, int* mode, double* Vscratch) {
   extern __shared__ double W[];  // K x (K+1), Jacobi fallback only
-  __shared__ double rowb[2][128], colb[2][128];
+  __shared__ __align__(16) double rowb[2][128], colb[2][128];
   __shared__ double sh[32];
   const int tid = threadIdx.x, KK = K * K;
-  // thread owns column l = tid % 128 and rows i = rg + 8v, v = 0..15 (rg = tid / 128):
-  // the row indices are compile-time, so W stays in 16 registers
+  // thread owns column l = tid % 128 and the 32 contiguous rows i = 32 rg + v (rg = tid / 128):
+  // row indices are compile-time, so W stays in 32 registers.
   const int l = tid & 127, rg = tid >> 7;
   const bool col_ok = l < K;
   double w[GI_MAXE];
   double dmax = 0.0;
 #pragma unroll
   for (int v = 0; v < GI_MAXE; ++v) {
-    const int i = rg + 8 * v;
+    const int i = 32 * rg + v;
     w[v] = 0.0;
     if (col_ok && i < K) {
       const int e = i * K + l;
@@ -84,6 +84,10 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
       if (i == l) dmax = fmax(dmax, x);
     }
   }
+  for (int i = tid; i < 2 * 128; i += GI_THREADS) {
+    (&colb[0][0])[i] = 0.0;
+    (&rowb[0][0])[i] = 0.0;
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   if ((tid & 31) == 0) sh[tid >> 5] = dmax;
@@ -98,13 +102,22 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
   bool ok = true;
   for (int j = 0; j < K; ++j) {
     const int b = j & 1;
-    if (col_ok) {
+    // publish row j (owners: rg == j/16; warp-uniform) and column j (owners: l == j)
+    if (col_ok && rg == (j >> 5)) {
+      const int jj = j & 31;
+      double* dst = &rowb[b][l];
 #pragma unroll
       for (int v = 0; v < GI_MAXE; ++v) {
-        const int i = rg + 8 * v;
-        if (i == j) rowb[b][l] = w[v];
-        if (l == j && i < K) colb[b][i] = w[v];
+        // predicated shared store per v (a select chain would be folded into a dynamically
+        // indexed local-memory array by the compiler)
+        asm volatile("{\n .reg .pred q;\n setp.eq.s32 q, %0, %1;\n @q st.shared.f64 [%2], %3;\n}\n"
+                     :: "r"(jj), "r"(v), "r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "d"(w[v])
+                     : "memory");
       }
+    }
+    if (l == j) {
+#pragma unroll
+      for (int v = 0; v < GI_MAXE; ++v) colb[b][32 * rg + v] = w[v];
     }
     __syncthreads();
     const double p = rowb[b][j];
@@ -113,21 +126,23 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
       break;
     }
     const double inv = 1.0 / p;
-    if (col_ok) {
+    if (l == j) {
+      // pivot column: W[i][j] <- -W[i][j]/p, W[j][j] <- 1/p
+#pragma unroll
+      for (int v = 0; v < GI_MAXE; ++v) w[v] = (32 * rg + v == j) ? inv : -w[v] * inv;
+    } else if (col_ok) {
+      // uniform rank-1 update W[i][l] -= W[i][j] W[j][l]/p; for the pivot row the column
+      // entry is read as p - 1 so the same FMA yields W[j][l]/p.
       const double rl = rowb[b][l] * inv;
-      if (l == j) {
+      const bool prow = rg == (j >> 5);
+      const int jj = j & 31;
 #pragma unroll
-        for (int v = 0; v < GI_MAXE; ++v) {
-          const int i = rg + 8 * v;
-          w[v] = (i == j) ? inv : -w[v] * inv;
-        }
-      } else {
-#pragma unroll
-        for (int v = 0; v < GI_MAXE; ++v) {
-          const int i = rg + 8 * v;
-          if (i >= K) continue;
-          w[v] = (i == j) ? rl : fma(-colb[b][i], rl, w[v]);
-        }
+      for (int v = 0; v < GI_MAXE; v += 2) {
+        const double2 cc = *reinterpret_cast<const double2*>(&colb[b][32 * rg + v]);
+        const double c0 = (prow && v == jj) ? p - 1.0 : cc.x;
+        const double c1 = (prow && v + 1 == jj) ? p - 1.0 : cc.y;
+        w[v] = fma(-c0, rl, w[v]);
+        w[v + 1] = fma(-c1, rl, w[v + 1]);
       }
     }
   }
@@ -135,7 +150,7 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
     if (col_ok) {
 #pragma unroll
       for (int v = 0; v < GI_MAXE; ++v) {
-        const int i = rg + 8 * v;
+        const int i = 32 * rg + v;
         if (i < K) Pout[i * K + l] = w[v];
       }
     }
