@@ -55,33 +55,35 @@ constexpr int GI_MAXE = 32;          // K*K <= 16384 = 32 * 512 register-residen
 __global__ void __launch_bounds__(GI_THREADS, 1)
     gamma_inverse_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
                          double* Pout, int* mode, double* Vscratch) {
-  extern __shared__ double W[];  // K x (K+1), Jacobi fallback only
   __shared__ __align__(16) double rowb[2][128], colb[2][128];
   __shared__ double sh[32];
+  (void)Vscratch;
   const int tid = threadIdx.x, KK = K * K;
   // thread owns column l = tid % 128 and the 32 contiguous rows i = 32 rg + v (rg = tid / 128):
   // row indices are compile-time, so W stays in 32 registers.
   const int l = tid & 127, rg = tid >> 7;
   const bool col_ok = l < K;
   double w[GI_MAXE];
+#pragma unroll
+  for (int v = 0; v < GI_MAXE; ++v) w[v] = 1.0;   // 1.0 * S^(first) is exactly S^(first)
+  const int rows_here = min(GI_MAXE, max(0, K - 32 * rg));
+  if (col_ok) {
+    for (int m = 0; m < N; ++m) {
+      if (m == n) continue;
+      const double* Sm = S_all + (int64_t)m * KK + (32 * rg) * K + l;
+#pragma unroll
+      for (int v = 0; v < GI_MAXE; ++v)
+        if (v < rows_here) w[v] *= __ldg(Sm + v * K);
+    }
+  }
   double dmax = 0.0;
 #pragma unroll
   for (int v = 0; v < GI_MAXE; ++v) {
     const int i = 32 * rg + v;
-    w[v] = 0.0;
-    if (col_ok && i < K) {
-      const int e = i * K + l;
-      double x = 0.0;
-      bool first = true;
-      for (int m = 0; m < N; ++m) {
-        if (m == n) continue;
-        const double sv = S_all[(int64_t)m * KK + e];
-        x = first ? sv : x * sv;
-        first = false;
-      }
-      Gamma[e] = x;
-      w[v] = x;
-      if (i == l) dmax = fmax(dmax, x);
+    if (!(col_ok && v < rows_here)) w[v] = 0.0;
+    else {
+      Gamma[i * K + l] = w[v];
+      if (i == l) dmax = fmax(dmax, w[v]);
     }
   }
   for (int i = tid; i < 2 * 128; i += GI_THREADS) {
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
       ok = false;
       break;
     }
-    const double inv = 1.0 / p;
+    const double inv = __drcp_rn(p);
     if (l == j) {
       // pivot column: W[i][j] <- -W[i][j]/p, W[j][j] <- 1/p
 #pragma unroll
@@ -155,9 +157,20 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
       }
     }
     if (tid == 0) *mode = 0;
-    return;
+  } else if (tid == 0) {
+    *mode = 1;   // gamma_pinv_kernel takes over
   }
-  __syncthreads();
+}
+
+// Eigen pseudo-inverse fallback (L13): runs after gamma_inverse_kernel and exits at once unless
+// the Gauss-Jordan pivot test failed.  Two-sided cyclic Jacobi, Brent-Luk parallel ordering.
+__global__ void __launch_bounds__(GI_THREADS, 1)
+    gamma_pinv_kernel(int K, const double* __restrict__ Gamma, double* Pout, const int* mode,
+                      double* Vscratch) {
+  if (*mode == 0) return;
+  extern __shared__ double W[];  // K x (K+1)
+  __shared__ double sh[32];
+  const int tid = threadIdx.x, KK = K * K;
   // ---- eigen pseudo-inverse: two-sided cyclic Jacobi on W (from Γ), V in global scratch
   const int P = K + 1;
   const int nt = GI_THREADS;
@@ -258,7 +271,6 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
     for (int l = 0; l < K; ++l) v += Vscratch[i * K + l] * lam[l] * Vscratch[j * K + l];
     Pout[e] = v;
   }
-  if (tid == 0) *mode = 1;
 }
 
 // ---------------------------------------------------------------- row solves + partial Gram
@@ -479,12 +491,16 @@ cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int K, doubl
   const size_t smem = static_cast<size_t>(K) * (K + 1) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gamma_inverse_kernel,
+    cudaError_t e = cudaFuncSetAttribute(gamma_pinv_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 129 * 8);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  gamma_inverse_kernel<<<1, GI_THREADS, smem, st>>>(S_all, N, n, K, Gamma, P, mode, Vscratch);
+  gamma_inverse_kernel<<<1, GI_THREADS, 0, st>>>(S_all, N, n, K, Gamma, P, mode, Vscratch);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  gamma_pinv_kernel<<<1, GI_THREADS, smem, st>>>(K, Gamma, P, mode, Vscratch);
   note_launch();
   return cudaGetLastError();
 }
