@@ -267,8 +267,8 @@ cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, doubl
 cppp_status prefetch_inverse(cppp_ctx* c, int n) {
   if (c->dry || c->prefetched == n) return CPPP_OK;
   CUCHK(c, cudaStreamWaitEvent(c->st2, c->ev_S, 0));
-  CUCHK(c, launch_gamma_inverse(c->S_all, c->N, n, c->K, c->Gamma, c->L, c->lmode, c->L + c->K * c->K,
-                                c->st2));
+  CUCHK(c, launch_gamma_factor(c->S_all, c->N, n, c->K, c->Gamma, c->L, c->lmode, c->L + c->K * c->K,
+                               c->st2));
   CUCHK(c, cudaEventRecord(c->ev_P, c->st2));
   c->prefetched = n;
   return CPPP_OK;
@@ -294,8 +294,8 @@ cppp_status finish_mode(cppp_ctx* c, int n, const double* Mn, bool pp_phase) {
     Prof p(c, CPPP_K_SOLVE, 4.0 * rows * K * K, 8.0 * rows * K * 5);
     double* An = c->A[n] + off * K;
     const double* ref = pp_phase ? (c->Ap[n] + off * K) : An;
-    CUCHK(c, launch_solve_rows(Mn, An, ref, c->dA[n] + off * K, rows, K, c->Gamma, c->L, c->rowstat,
-                               c->gpart, c->st));
+    CUCHK(c, launch_solve_rows(Mn, An, ref, c->dA[n] + off * K, rows, K, c->Gamma, c->L, c->lmode,
+                               c->rowstat, c->gpart, c->st));
     CUCHK(c, launch_gram_reduce(c->gpart, solve_row_blocks(rows), K, c->S_all + (int64_t)n * K * K,
                                 c->rowstat, rows, c->stats + 3 * n, c->st));
   }

@@ -82,18 +82,19 @@ cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st);
 size_t pp_update_scratch_doubles(int64_t ny, int K, int64_t max_nx);
 
 // ---------------------------------------------------------------- small dense ops (K <= 128)
-// Γ^(n) = Hadamard of S[m], m != n -> Gamma; its inverse (Gauss-Jordan, L13 pivot rule)
-// or eigen pseudo-inverse -> P; *mode = 0 (inverse) / 1 (pinv).  One CTA.  Vscratch: K*K doubles.
-cudaError_t launch_gamma_inverse(const double* S_all /* N x K x K */, int N, int n, int K,
-                                 double* Gamma, double* P, int* mode, double* Vscratch,
-                                 cudaStream_t st);
-// Row solves: A_new = M P ; G = (A_old - A_new) Γ ; dA = A_new - ref ; per-row norms -> rowstat
-// (rows x 3: ||a_new||², ||dA||², ||g||²); per-CTA partial Grams -> gpart (solve_row_blocks x K*K).
-// A is updated in place; ref may alias A (DT: dA = A_new - A_old).
+// Γ^(n) = Hadamard of S[m], m != n -> Gamma; Cholesky factor (L13 pivot rule) -> L
+// with *mode = 0, else the eigen pseudo-inverse -> L with *mode = 1.  One CTA per kernel.
+// Vscratch: K*K doubles (Jacobi V).
+cudaError_t launch_gamma_factor(const double* S_all /* N x K x K */, int N, int n, int K,
+                                double* Gamma, double* L, int* mode, double* Vscratch,
+                                cudaStream_t st);
+// Row solves: A_new = M Γ^† (substitution with L, or M P) ; G = (A_old - A_new) Γ ;
+// dA = A_new - ref ; per-row norms -> rowstat (rows x 3: ||a_new||², ||dA||², ||g||²);
+// per-CTA partial Grams -> gpart (solve_row_blocks x K*K).  A is updated in place; ref may alias A.
 int solve_row_blocks(int64_t rows);
 cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, double* dA,
-                              int64_t rows, int K, const double* Gamma, const double* P,
-                              double* rowstat, double* gpart, cudaStream_t st);
+                              int64_t rows, int K, const double* Gamma, const double* L,
+                              const int* mode, double* rowstat, double* gpart, cudaStream_t st);
 // S = Σ_b gpart[b]; if rowstat: nrm[0..2] = Σ_rows rowstat (fixed order)
 cudaError_t launch_gram_reduce(const double* gpart, int nb, int K, double* S,
                                const double* rowstat, int64_t rows, double* nrm, cudaStream_t st);

@@ -46,21 +46,17 @@ constexpr double PINV_TAU = 1e-12;
 constexpr int GI_THREADS = 512;
 constexpr int GI_MAXE = 32;          // K*K <= 16384 = 32 * 512 register-resident elements
 
-// ---------------------------------------------------------------- Γ and its (pseudo-)inverse
-// Gauss-Jordan on the SPD Γ without pivoting: the pivot of step j is the Schur complement
-// diagonal, i.e. exactly the Cholesky pivot d_j of the L13 rule (accept iff every d_j >
-// τ·max diag Γ).  Each thread keeps up to 16 entries of W in registers; row j and column j are
-// broadcast through double-buffered shared memory, so one barrier per pivot.  On a rejected
-// pivot the eigen pseudo-inverse (cyclic Jacobi, Brent-Luk parallel ordering) takes over.
+// ---------------------------------------------------------------- Γ and its Cholesky factor
+// Right-looking Cholesky Γ = L Lᵀ with the L13 pivot rule (accept iff every pivot d_j >
+// τ·max diag Γ), the same factorization the oracle uses.  Thread (l = tid % 128, rg = tid / 128)
+// keeps column l, rows 32 rg + v (v < 32) in registers.  Column j+1 is published (unscaled) at the
+// end of step j, so step j+1 reads its pivot and scales on the fly: one barrier per pivot.
 __global__ void __launch_bounds__(GI_THREADS, 1)
-    gamma_inverse_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
-                         double* Pout, int* mode, double* Vscratch) {
-  __shared__ __align__(16) double rowb[2][128], colb[2][128];
+    gamma_chol_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
+                      double* Lout, int* mode) {
+  __shared__ __align__(16) double colb[2][128];
   __shared__ double sh[32];
-  (void)Vscratch;
   const int tid = threadIdx.x, KK = K * K;
-  // thread owns column l = tid % 128 and the 32 contiguous rows i = 32 rg + v (rg = tid / 128):
-  // row indices are compile-time, so W stays in 32 registers.
   const int l = tid & 127, rg = tid >> 7;
   const bool col_ok = l < K;
   double w[GI_MAXE];
@@ -86,10 +82,7 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
       if (i == l) dmax = fmax(dmax, w[v]);
     }
   }
-  for (int i = tid; i < 2 * 128; i += GI_THREADS) {
-    (&colb[0][0])[i] = 0.0;
-    (&rowb[0][0])[i] = 0.0;
-  }
+  for (int i = tid; i < 2 * 128; i += GI_THREADS) (&colb[0][0])[i] = 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   if ((tid & 31) == 0) sh[tid >> 5] = dmax;
@@ -99,61 +92,49 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
     for (int i = 0; i < GI_THREADS / 32; ++i) m = fmax(m, sh[i]);
     sh[0] = m;
   }
+  if (l == 0) {
+#pragma unroll
+    for (int v = 0; v < GI_MAXE; ++v) colb[0][32 * rg + v] = w[v];
+  }
   __syncthreads();
   const double thresh = PIVOT_TAU * sh[0];
   bool ok = true;
   for (int j = 0; j < K; ++j) {
     const int b = j & 1;
-    // publish row j (owners: rg == j/16; warp-uniform) and column j (owners: l == j)
-    if (col_ok && rg == (j >> 5)) {
-      const int jj = j & 31;
-      double* dst = &rowb[b][l];
-#pragma unroll
-      for (int v = 0; v < GI_MAXE; ++v) {
-        // predicated shared store per v (a select chain would be folded into a dynamically
-        // indexed local-memory array by the compiler)
-        asm volatile("{\n .reg .pred q;\n setp.eq.s32 q, %0, %1;\n @q st.shared.f64 [%2], %3;\n}\n"
-                     :: "r"(jj), "r"(v), "r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "d"(w[v])
-                     : "memory");
-      }
-    }
-    if (l == j) {
-#pragma unroll
-      for (int v = 0; v < GI_MAXE; ++v) colb[b][32 * rg + v] = w[v];
-    }
-    __syncthreads();
-    const double p = rowb[b][j];
-    if (!(p > thresh)) {
+    const double piv = colb[b][j];
+    if (!(piv > thresh)) {
       ok = false;
       break;
     }
-    const double inv = __drcp_rn(p);
+    const double ljj = sqrt(piv);
+    const double inv = 1.0 / ljj;
     if (l == j) {
-      // pivot column: W[i][j] <- -W[i][j]/p, W[j][j] <- 1/p
 #pragma unroll
-      for (int v = 0; v < GI_MAXE; ++v) w[v] = (32 * rg + v == j) ? inv : -w[v] * inv;
-    } else if (col_ok) {
-      // uniform rank-1 update W[i][l] -= W[i][j] W[j][l]/p; for the pivot row the column
-      // entry is read as p - 1 so the same FMA yields W[j][l]/p.
-      const double rl = rowb[b][l] * inv;
-      const bool prow = rg == (j >> 5);
-      const int jj = j & 31;
+      for (int v = 0; v < GI_MAXE; ++v) {
+        const int i = 32 * rg + v;
+        w[v] = (i == j) ? ljj : (i > j ? w[v] * inv : 0.0);
+      }
+    } else if (col_ok && l > j) {
+      const double cl = colb[b][l] * inv * inv;   // L[l][j] / L[j][j]... times L[i][j] below
 #pragma unroll
       for (int v = 0; v < GI_MAXE; v += 2) {
         const double2 cc = *reinterpret_cast<const double2*>(&colb[b][32 * rg + v]);
-        const double c0 = (prow && v == jj) ? p - 1.0 : cc.x;
-        const double c1 = (prow && v + 1 == jj) ? p - 1.0 : cc.y;
-        w[v] = fma(-c0, rl, w[v]);
-        w[v + 1] = fma(-c1, rl, w[v + 1]);
+        w[v] = fma(-cc.x, cl, w[v]);
+        w[v + 1] = fma(-cc.y, cl, w[v + 1]);
       }
     }
+    if (l == j + 1) {
+#pragma unroll
+      for (int v = 0; v < GI_MAXE; ++v) colb[b ^ 1][32 * rg + v] = w[v];
+    }
+    __syncthreads();
   }
   if (ok) {
     if (col_ok) {
 #pragma unroll
       for (int v = 0; v < GI_MAXE; ++v) {
         const int i = 32 * rg + v;
-        if (i < K) Pout[i * K + l] = w[v];
+        if (i < K) Lout[i * K + l] = (i >= l) ? w[v] : 0.0;
       }
     }
     if (tid == 0) *mode = 0;
@@ -162,7 +143,7 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
   }
 }
 
-// Eigen pseudo-inverse fallback (L13): runs after gamma_inverse_kernel and exits at once unless
+// Eigen pseudo-inverse fallback (L13): runs after gamma_chol_kernel and exits at once unless
 // the Gauss-Jordan pivot test failed.  Two-sided cyclic Jacobi, Brent-Luk parallel ordering.
 __global__ void __launch_bounds__(GI_THREADS, 1)
     gamma_pinv_kernel(int K, const double* __restrict__ Gamma, double* Pout, const int* mode,
@@ -274,59 +255,113 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
 }
 
 // ---------------------------------------------------------------- row solves + partial Gram
-// One warp per row (16 rows per CTA).  Shared memory: W (K x K: P, then Γ) and the CTA's rows of
-// M, A_new and A_old - A_new.  Lane c owns columns c + 32u.
+// One warp per row (16 rows per CTA).  Cholesky path (mode 0): forward then back substitution
+// with L staged in shared memory (pitch K+1: column reads are conflict-free), as the oracle does;
+// pinv path (mode 1): a = m P.  Then G = (a_old - a_new) Γ with Γ staged, dA, row norms and the
+// CTA's partial Gram.  Lane c owns columns c + 32u.
 constexpr int SR_WARPS = 16;
+
+// stage a K x K row-major matrix into shared memory with row pitch `pitch` (8 loads in flight)
+__device__ __forceinline__ void stage_matrix(double* dst, int pitch, const double* __restrict__ src,
+                                             int K) {
+  const int KK = K * K;
+  for (int e0 = threadIdx.x; e0 < KK; e0 += 8 * blockDim.x) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      v[u] = e < KK ? __ldg(src + e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < KK) {
+        const int i = e / K, j = e - i * K;
+        dst[i * pitch + j] = v[u];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ double pick4(const double (&m)[4], int slot) {
+  return slot == 0 ? m[0] : slot == 1 ? m[1] : slot == 2 ? m[2] : m[3];
+}
 
 __global__ void __launch_bounds__(SR_WARPS * 32)
     solve_rows_kernel(const double* __restrict__ M, double* A, const double* ref, double* dA,
                       int64_t rows, int K, const double* __restrict__ Gamma,
-                      const double* __restrict__ Pm, double* __restrict__ rowstat,
-                      double* __restrict__ gpart) {
+                      const double* __restrict__ Lm, const int* __restrict__ mode_p,
+                      double* __restrict__ rowstat, double* __restrict__ gpart) {
   extern __shared__ double sm[];
   const int KK = K * K;
-  double* Ws = sm;                     // K*K
-  double* Ms = Ws + KK;                // SR_WARPS*K
-  double* As = Ms + SR_WARPS * K;      // SR_WARPS*K
-  double* Ds = As + SR_WARPS * K;      // SR_WARPS*K
+  const int P = K + 1;
+  double* Ws = sm;                         // K*(K+1)
+  double* dinv = Ws + K * P;               // K
+  double* As = dinv + K;                   // SR_WARPS*K
+  double* Ds = As + SR_WARPS * K;          // SR_WARPS*K
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t y = blockIdx.x * (int64_t)SR_WARPS + w;
   const bool valid = y < rows;
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) Ws[e] = Pm[e];
-  double aold[4], rf[4], a[4];
+  const int mode = *mode_p;
+  stage_matrix(Ws, mode == 0 ? P : K, Lm, K);
+  double m[4], aold[4], rf[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int c = lane + 32 * u;
     const bool in = valid && c < K;
     aold[u] = in ? A[y * K + c] : 0.0;
     rf[u] = in ? ref[y * K + c] : 0.0;
-    if (c < K) Ms[w * K + c] = in ? M[y * K + c] : 0.0;
+    m[u] = in ? M[y * K + c] : 0.0;
   }
   __syncthreads();
-  // A_new = m P
+  if (mode == 0) {
+    for (int j = threadIdx.x; j < K; j += blockDim.x) dinv[j] = 1.0 / Ws[j * P + j];
+    __syncthreads();
+    // forward: L z = m
+    for (int j = 0; j < K; ++j) {
+      const double zj = __shfl_sync(0xffffffffu, pick4(m, j >> 5), j & 31) * dinv[j];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) a[u] = 0.0;
-  for (int p = 0; p < K; ++p) {
-    const double mp = Ms[w * K + p];
-    const double* wr = Ws + p * K;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = lane + 32 * u;
-      if (c < K) a[u] = fma(mp, wr[c], a[u]);
+      for (int u = 0; u < 4; ++u) {
+        const int c = lane + 32 * u;
+        if (c == j) m[u] = zj;
+        else if (c > j && c < K) m[u] = fma(-Ws[c * P + j], zj, m[u]);
+      }
     }
+    // back: Lᵀ a = z
+    for (int j = K - 1; j >= 0; --j) {
+      const double aj = __shfl_sync(0xffffffffu, pick4(m, j >> 5), j & 31) * dinv[j];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = lane + 32 * u;
+        if (c == j) m[u] = aj;
+        else if (c < j) m[u] = fma(-Ws[j * P + c], aj, m[u]);
+      }
+    }
+  } else {
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int p = 0; p < K; ++p) {
+      const double mp = __shfl_sync(0xffffffffu, pick4(m, p >> 5), p & 31);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = lane + 32 * u;
+        if (c < K) a[u] = fma(mp, Ws[p * K + c], a[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) m[u] = a[u];
   }
+  // m now holds a_new
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int c = lane + 32 * u;
     if (c < K) {
-      As[w * K + c] = valid ? a[u] : 0.0;
-      Ds[w * K + c] = valid ? aold[u] - a[u] : 0.0;
+      As[w * K + c] = valid ? m[u] : 0.0;
+      Ds[w * K + c] = valid ? aold[u] - m[u] : 0.0;
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) Ws[e] = Gamma[e];
+  stage_matrix(Ws, K, Gamma, K);
   __syncthreads();
-  // G row = (a_old - a_new) Γ
   double g[4] = {0.0, 0.0, 0.0, 0.0};
   for (int p = 0; p < K; ++p) {
     const double dp = Ds[w * K + p];
@@ -342,10 +377,10 @@ __global__ void __launch_bounds__(SR_WARPS * 32)
   for (int u = 0; u < 4; ++u) {
     const int c = lane + 32 * u;
     if (valid && c < K) {
-      const double d = a[u] - rf[u];
-      A[y * K + c] = a[u];
+      const double d = m[u] - rf[u];
+      A[y * K + c] = m[u];
       dA[y * K + c] = d;
-      na = fma(a[u], a[u], na);
+      na = fma(m[u], m[u], na);
       nd = fma(d, d, nd);
       ng = fma(g[u], g[u], ng);
     }
@@ -358,11 +393,11 @@ __global__ void __launch_bounds__(SR_WARPS * 32)
     rowstat[y * 3 + 1] = nd;
     rowstat[y * 3 + 2] = ng;
   }
-  // partial Gram of this CTA's rows (rows in ascending order)
+  // partial Gram of this CTA's rows (rows in ascending order), 2 outputs per thread per pass
   for (int e = threadIdx.x; e < KK; e += blockDim.x) {
     const int k1 = e / K, k2 = e - k1 * K;
     double s = 0.0;
-#pragma unroll 4
+#pragma unroll
     for (int r = 0; r < SR_WARPS; ++r) s = fma(As[r * K + k1], As[r * K + k2], s);
     gpart[(int64_t)blockIdx.x * KK + e] = s;
   }
@@ -486,8 +521,8 @@ uint64_t launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED);
 
 int solve_row_blocks(int64_t rows) { return static_cast<int>((rows + SR_WARPS - 1) / SR_WARPS); }
 
-cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int K, double* Gamma, double* P,
-                                 int* mode, double* Vscratch, cudaStream_t st) {
+cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double* Gamma, double* L,
+                                int* mode, double* Vscratch, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(K) * (K + 1) * sizeof(double);
   static bool attr = false;
   if (!attr) {
@@ -496,30 +531,31 @@ cudaError_t launch_gamma_inverse(const double* S_all, int N, int n, int K, doubl
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  gamma_inverse_kernel<<<1, GI_THREADS, 0, st>>>(S_all, N, n, K, Gamma, P, mode, Vscratch);
+  gamma_chol_kernel<<<1, GI_THREADS, 0, st>>>(S_all, N, n, K, Gamma, L, mode);
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  gamma_pinv_kernel<<<1, GI_THREADS, smem, st>>>(K, Gamma, P, mode, Vscratch);
+  gamma_pinv_kernel<<<1, GI_THREADS, smem, st>>>(K, Gamma, L, mode, Vscratch);
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, double* dA,
-                              int64_t rows, int K, const double* Gamma, const double* P,
-                              double* rowstat, double* gpart, cudaStream_t st) {
+                              int64_t rows, int K, const double* Gamma, const double* L,
+                              const int* mode, double* rowstat, double* gpart, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  const size_t smem = (static_cast<size_t>(K) * K + 3 * SR_WARPS * K) * sizeof(double);
+  const size_t smem = (static_cast<size_t>(K) * (K + 1) + K + 2 * SR_WARPS * K) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(solve_rows_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (128 * 128 + 3 * SR_WARPS * 128) * 8);
+                                         (128 * 129 + 128 + 2 * SR_WARPS * 128) * 8);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   solve_rows_kernel<<<solve_row_blocks(rows), SR_WARPS * 32, smem, st>>>(M, A, ref, dA, rows, K,
-                                                                         Gamma, P, rowstat, gpart);
+                                                                         Gamma, L, mode, rowstat,
+                                                                         gpart);
   note_launch();
   return cudaGetLastError();
 }

@@ -44,15 +44,15 @@ int main() {
     cudaMemcpy(dA, A.data(), 8 * s * K, cudaMemcpyHostToDevice);
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
-    launch_gamma_inverse(dS, N, 0, K, dG, dP, dmode, dV, 0);
+    launch_gamma_factor(dS, N, 0, K, dG, dP, dmode, dV, 0);
     cudaDeviceSynchronize();
     cudaEventRecord(a);
-    for (int r = 0; r < 20; ++r) launch_gamma_inverse(dS, N, 0, K, dG, dP, dmode, dV, 0);
+    for (int r = 0; r < 20; ++r) launch_gamma_factor(dS, N, 0, K, dG, dP, dmode, dV, 0);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms_inv; cudaEventElapsedTime(&ms_inv, a, b);
     cudaEventRecord(a);
     for (int r = 0; r < 20; ++r) {
-      launch_solve_rows(dM, dA, dA, dD, s, K, dG, dP, drs, dgp, 0);
+      launch_solve_rows(dM, dA, dA, dD, s, K, dG, dP, dmode, drs, dgp, 0);
       launch_gram_reduce(dgp, solve_row_blocks(s), K, dSn, drs, s, dn, 0);
     }
     cudaEventRecord(b); cudaEventSynchronize(b);
@@ -66,10 +66,10 @@ int main() {
     for (int i = 0; i < K; ++i)
       for (int j = 0; j < K; ++j) {
         double acc = 0;
-        for (int l = 0; l < K; ++l) acc += P[i * K + l] * G[l * K + j];
-        err = fmax(err, fabs(acc - (i == j)));
+        for (int l = 0; l < K; ++l) acc += P[i * K + l] * P[j * K + l];
+        err = fmax(err, fabs(acc - G[i * K + j]) / fabs(G[i * K + i]));
       }
-    printf("{\"K\": %d, \"mode\": %d, \"inv_err\": %.3e, \"gamma_inverse_us\": %.2f, \"rows_plus_reduce_us\": %.2f, \"cuda\": \"%s\"}\n",
+    printf("{\"K\": %d, \"mode\": %d, \"inv_err\": %.3e, \"gamma_factor_us\": %.2f, \"rows_plus_reduce_us\": %.2f, \"cuda\": \"%s\"}\n",
            K, mode, err, ms_inv * 1e3 / 20, ms_rows * 1e3 / 20, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
