@@ -55,9 +55,14 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
     gamma_chol_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
                       double* Lout, int* mode) {
   __shared__ __align__(16) double colb[2][128];
+  __shared__ double piv_s[2][2];    // [buffer][sqrt(pivot), 1/sqrt(pivot)]
+  __shared__ int bad_s[2];
   __shared__ double sh[32];
   const int tid = threadIdx.x, KK = K * K;
-  const int l = tid & 127, rg = tid >> 7;
+  const int lane = tid & 31, wid = tid >> 5;
+  // column l = 4 lane + (warp mod 4): every SM sub-partition owns every 4th column, so the
+  // shrinking trailing matrix stays balanced; rg = warp / 4 selects rows 32 rg .. 32 rg + 31.
+  const int l = 4 * lane + (wid & 3), rg = wid >> 2;
   const bool col_ok = l < K;
   double w[GI_MAXE];
 #pragma unroll
@@ -85,37 +90,44 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
   for (int i = tid; i < 2 * 128; i += GI_THREADS) (&colb[0][0])[i] = 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-  if ((tid & 31) == 0) sh[tid >> 5] = dmax;
+  if (lane == 0) sh[wid] = dmax;
   __syncthreads();
   if (tid == 0) {
     double m = 0.0;
     for (int i = 0; i < GI_THREADS / 32; ++i) m = fmax(m, sh[i]);
     sh[0] = m;
   }
+  __syncthreads();
+  const double thresh = PIVOT_TAU * sh[0];
+  // publish column 0 and its pivot
   if (l == 0) {
 #pragma unroll
     for (int v = 0; v < GI_MAXE; ++v) colb[0][32 * rg + v] = w[v];
+    if (rg == 0) {
+      const double p = w[0];
+      bad_s[0] = !(p > thresh);
+      const double r = sqrt(p);
+      piv_s[0][0] = r;
+      piv_s[0][1] = 1.0 / r;
+    }
   }
   __syncthreads();
-  const double thresh = PIVOT_TAU * sh[0];
   bool ok = true;
   for (int j = 0; j < K; ++j) {
     const int b = j & 1;
-    const double piv = colb[b][j];
-    if (!(piv > thresh)) {
+    if (bad_s[b]) {
       ok = false;
       break;
     }
-    const double ljj = sqrt(piv);
-    const double inv = 1.0 / ljj;
+    const double ljj = piv_s[b][0], inv = piv_s[b][1];
     if (l == j) {
 #pragma unroll
       for (int v = 0; v < GI_MAXE; ++v) {
         const int i = 32 * rg + v;
         w[v] = (i == j) ? ljj : (i > j ? w[v] * inv : 0.0);
       }
-    } else if (col_ok && l > j) {
-      const double cl = colb[b][l] * inv * inv;   // L[l][j] / L[j][j]... times L[i][j] below
+    } else if (col_ok && l > j && 32 * rg + 31 > j) {
+      const double cl = colb[b][l] * inv * inv;
 #pragma unroll
       for (int v = 0; v < GI_MAXE; v += 2) {
         const double2 cc = *reinterpret_cast<const double2*>(&colb[b][32 * rg + v]);
@@ -123,9 +135,16 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
         w[v + 1] = fma(-cc.y, cl, w[v + 1]);
       }
     }
-    if (l == j + 1) {
+    if (l == j + 1) {   // publish the next column (and, from its diagonal owner, the pivot)
 #pragma unroll
       for (int v = 0; v < GI_MAXE; ++v) colb[b ^ 1][32 * rg + v] = w[v];
+      if (rg == ((j + 1) >> 5)) {
+        const double p = colb[b ^ 1][j + 1];   // this thread just wrote it
+        bad_s[b ^ 1] = !(p > thresh);
+        const double r = sqrt(p);
+        piv_s[b ^ 1][0] = r;
+        piv_s[b ^ 1][1] = 1.0 / r;
+      }
     }
     __syncthreads();
   }
