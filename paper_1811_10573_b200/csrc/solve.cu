@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
     gamma_chol_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
                       double* Lout, int* mode) {
   __shared__ __align__(16) double colb[2][128];
-  __shared__ double piv_s[2][2];    // [buffer][sqrt(pivot), 1/sqrt(pivot)]
+  __shared__ double piv_s[2][2];    // [buffer][-, 1/pivot]
   __shared__ int bad_s[2];
   __shared__ double sh[32];
   const int tid = threadIdx.x, KK = K * K;
@@ -99,16 +99,18 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
   }
   __syncthreads();
   const double thresh = PIVOT_TAU * sh[0];
-  // publish column 0 and its pivot
+  // Unscaled (LDLᵀ-form) elimination: column j keeps W[i][j] with d_j = W[j][j] the pivot, the
+  // trailing update is W[i][l] -= W[i][j] W[l][j] / d_j, and L = W diag(d)^(-1/2) is applied at
+  // the end, so only one reciprocal (no sqrt) sits on the per-pivot critical path.
+  __shared__ double dpiv[128];
   if (l == 0) {
 #pragma unroll
     for (int v = 0; v < GI_MAXE; ++v) colb[0][32 * rg + v] = w[v];
     if (rg == 0) {
       const double p = w[0];
       bad_s[0] = !(p > thresh);
-      const double r = sqrt(p);
-      piv_s[0][0] = r;
-      piv_s[0][1] = 1.0 / r;
+      dpiv[0] = p;
+      piv_s[0][1] = __drcp_rn(p);
     }
   }
   __syncthreads();
@@ -119,15 +121,8 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
       ok = false;
       break;
     }
-    const double ljj = piv_s[b][0], inv = piv_s[b][1];
-    if (l == j) {
-#pragma unroll
-      for (int v = 0; v < GI_MAXE; ++v) {
-        const int i = 32 * rg + v;
-        w[v] = (i == j) ? ljj : (i > j ? w[v] * inv : 0.0);
-      }
-    } else if (col_ok && l > j && 32 * rg + 31 > j) {
-      const double cl = colb[b][l] * inv * inv;
+    if (col_ok && l > j && 32 * rg + 31 > j) {
+      const double cl = colb[b][l] * piv_s[b][1];
 #pragma unroll
       for (int v = 0; v < GI_MAXE; v += 2) {
         const double2 cc = *reinterpret_cast<const double2*>(&colb[b][32 * rg + v]);
@@ -141,19 +136,21 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
       if (rg == ((j + 1) >> 5)) {
         const double p = colb[b ^ 1][j + 1];   // this thread just wrote it
         bad_s[b ^ 1] = !(p > thresh);
-        const double r = sqrt(p);
-        piv_s[b ^ 1][0] = r;
-        piv_s[b ^ 1][1] = 1.0 / r;
+        dpiv[j + 1] = p;
+        piv_s[b ^ 1][1] = __drcp_rn(p);
       }
     }
     __syncthreads();
   }
   if (ok) {
     if (col_ok) {
+      const double d = dpiv[l];
+      const double r = sqrt(d);
+      const double ri = 1.0 / r;
 #pragma unroll
       for (int v = 0; v < GI_MAXE; ++v) {
         const int i = 32 * rg + v;
-        if (i < K) Lout[i * K + l] = (i >= l) ? w[v] : 0.0;
+        if (i < K) Lout[i * K + l] = (i > l) ? w[v] * ri : (i == l ? r : 0.0);
       }
     }
     if (tid == 0) *mode = 0;

@@ -1,0 +1,3 @@
+./tools/probe_solve
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "Error|assert|FAILED|passed|failed" | head -20
+./tools/probe_solve > /dev/null && ncu --set full --clock-control none --import-source on -k regex:"solve_rows|gamma_chol" -s 82 -c 2 -o gpurun_out/prof_rows2 ./tools/probe_solve > gpurun_out/ncu_rows.log 2>&1; tail -1 gpurun_out/ncu_rows.log
