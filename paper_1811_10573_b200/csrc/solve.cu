@@ -333,24 +333,52 @@ __global__ void __launch_bounds__(SR_WARPS * 32)
   if (mode == 0) {
     for (int j = threadIdx.x; j < K; j += blockDim.x) dinv[j] = 1.0 / Ws[j * P + j];
     __syncthreads();
-    // forward: L z = m
-    for (int j = 0; j < K; ++j) {
-      const double zj = __shfl_sync(0xffffffffu, pick4(m, j >> 5), j & 31) * dinv[j];
+    // forward L z = m, blocked by 32 columns: in-block substitution (lane = column), then a
+    // dependency-free update of the later column blocks
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = lane + 32 * u;
-        if (c == j) m[u] = zj;
-        else if (c > j && c < K) m[u] = fma(-Ws[c * P + j], zj, m[u]);
+    for (int b = 0; b < 4; ++b) {
+      if (32 * b >= K) break;
+      const int c = 32 * b + lane;
+      for (int jj = 0; jj < 32; ++jj) {
+        const int j = 32 * b + jj;
+        if (j >= K) break;
+        const double zj = __shfl_sync(0xffffffffu, m[b], jj) * dinv[j];
+        if (lane == jj) m[b] = zj;
+        else if (lane > jj && c < K) m[b] = fma(-Ws[c * P + j], zj, m[b]);
+      }
+#pragma unroll
+      for (int u = b + 1; u < 4; ++u) {
+        const int cu = lane + 32 * u;
+        if (32 * u >= K) break;
+        double acc = m[u];
+        for (int jj = 0; jj < 32 && 32 * b + jj < K; ++jj) {
+          const double zj = __shfl_sync(0xffffffffu, m[b], jj);
+          if (cu < K) acc = fma(-Ws[cu * P + 32 * b + jj], zj, acc);
+        }
+        m[u] = acc;
       }
     }
-    // back: Lᵀ a = z
-    for (int j = K - 1; j >= 0; --j) {
-      const double aj = __shfl_sync(0xffffffffu, pick4(m, j >> 5), j & 31) * dinv[j];
+    // back Lᵀ a = z, blocks in reverse
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = lane + 32 * u;
-        if (c == j) m[u] = aj;
-        else if (c < j) m[u] = fma(-Ws[j * P + c], aj, m[u]);
+    for (int b = 3; b >= 0; --b) {
+      if (32 * b >= K) continue;
+      const int c = 32 * b + lane;
+      const int jtop = min(31, K - 1 - 32 * b);
+      for (int jj = jtop; jj >= 0; --jj) {
+        const int j = 32 * b + jj;
+        const double aj = __shfl_sync(0xffffffffu, m[b], jj) * dinv[j];
+        if (lane == jj) m[b] = aj;
+        else if (lane < jj) m[b] = fma(-Ws[j * P + c], aj, m[b]);
+      }
+#pragma unroll
+      for (int u = 0; u < b; ++u) {
+        const int cu = lane + 32 * u;
+        double acc = m[u];
+        for (int jj = 0; jj <= jtop; ++jj) {
+          const double aj = __shfl_sync(0xffffffffu, m[b], jj);
+          acc = fma(-Ws[(32 * b + jj) * P + cu], aj, acc);
+        }
+        m[u] = acc;
       }
     }
   } else {
