@@ -74,6 +74,12 @@ typedef struct {
    * and broadcast by the caller, e.g. through torch.distributed. */
   const void *nccl_unique_id;
   int rank, world;
+  /* Optional host-side all-reduce (sum) used INSTEAD of NCCL when world > 1: the library copies
+   * the device buffer to pinned host memory, calls host_allreduce(buf, count, user) (which must
+   * leave the element-wise sum over all ranks in buf and return 0), and copies it back.  Lets
+   * several contexts on ONE device (one host thread each) run the sharded algebra in tests. */
+  int (*host_allreduce)(double *buf, size_t count, void *user);
+  void *host_allreduce_user;
 } cppp_opts;
 
 /* Per-sweep record (S:505 trace schema). */

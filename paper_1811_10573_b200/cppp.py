@@ -35,11 +35,15 @@ class CpppError(RuntimeError):
         self.status = status
 
 
+HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_size_t, C.c_void_p)
+
+
 class Opts(C.Structure):
     _fields_ = [("device", C.c_int), ("stream", C.c_void_p), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("flags", C.c_uint), ("shard_mode", C.c_int),
                 ("shard_offset", C.c_int64), ("shard_extent", C.c_int64),
-                ("nccl_unique_id", C.c_void_p), ("rank", C.c_int), ("world", C.c_int)]
+                ("nccl_unique_id", C.c_void_p), ("rank", C.c_int), ("world", C.c_int),
+                ("host_allreduce", HOST_ALLREDUCE), ("host_allreduce_user", C.c_void_p)]
 
 
 class SweepInfo(C.Structure):
@@ -164,7 +168,7 @@ def _torch_workspace(nbytes: int, device: int):
 def cp_init(X, N: int, s: Sequence[int], K: int, *, device: int = 0, stream=None,
             flags: int = 0, shard_offset: Optional[int] = None, shard_extent: Optional[int] = None,
             nccl_unique_id: Optional[bytes] = None, rank: int = 0, world: int = 1,
-            torch_workspace: bool = True) -> Ctx:
+            torch_workspace: bool = True, host_allreduce=None) -> Ctx:
     """cp_init (include/cppp.h).  X: numpy array (host) or torch CUDA tensor (device; borrowed
     with FLAG_BORROW_TENSOR).  The device workspace is a torch uint8 tensor unless
     torch_workspace=False (then the library cudaMallocs it).  stream: a torch.cuda.Stream or
@@ -183,6 +187,17 @@ def cp_init(X, N: int, s: Sequence[int], K: int, *, device: int = 0, stream=None
         o.shard_offset = int(shard_offset)
         o.shard_extent = int(shard_extent)
     o.rank, o.world = rank, world
+    if host_allreduce is not None:
+        # host_allreduce(np.ndarray view of the staged buffer) -> None, sums in place
+        def _cb(buf, count, _user, _fn=host_allreduce):
+            try:
+                _fn(np.ctypeslib.as_array(buf, shape=(count,)))
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a status by the library
+                return 1
+        cb = HOST_ALLREDUCE(_cb)
+        ctx.keep.append(cb)
+        o.host_allreduce = cb
     if nccl_unique_id is not None:
         idbuf = C.create_string_buffer(bytes(nccl_unique_id), 128)
         ctx.keep.append(idbuf)

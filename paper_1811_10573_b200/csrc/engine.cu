@@ -131,6 +131,10 @@ struct cppp_ctx {
   // comm
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  int (*host_ar)(double*, size_t, void*) = nullptr;
+  void* host_ar_user = nullptr;
+  double* host_ar_buf = nullptr;   // pinned staging
+  size_t host_ar_cap = 0;
   // profiling
   std::vector<ProfPending> pending;
   std::vector<cudaEvent_t> evpool;
@@ -218,6 +222,22 @@ void prof_collect(cppp_ctx* c) {
 // ---------------------------------------------------------------- comm
 cppp_status allreduce(cppp_ctx* c, double* buf, size_t count) {
   if (c->world <= 1 || c->dry || count == 0) return CPPP_OK;
+  if (c->host_ar) {
+    if (count > c->host_ar_cap) {
+      if (c->host_ar_buf) cudaFreeHost(c->host_ar_buf);
+      c->host_ar_buf = nullptr;
+      if (cudaMallocHost(&c->host_ar_buf, count * sizeof(double)) != cudaSuccess)
+        return fail(c, CPPP_ENOMEM, "host all-reduce staging of %zu doubles", count);
+      c->host_ar_cap = count;
+    }
+    CUCHK(c, cudaMemcpyAsync(c->host_ar_buf, buf, count * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CUCHK(c, cudaStreamSynchronize(c->st));
+    if (c->host_ar(c->host_ar_buf, count, c->host_ar_user) != 0)
+      return fail(c, CPPP_ENCCL, "host all-reduce callback failed");
+    CUCHK(c, cudaMemcpyAsync(buf, c->host_ar_buf, count * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CUCHK(c, cudaStreamSynchronize(c->st));
+    return CPPP_OK;
+  }
   ncclResult_t r = g_nccl.allReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, c->st);
   if (r != ncclSuccess) return fail(c, CPPP_ENCCL, "ncclAllReduce: %s", g_nccl.getErrorString(r));
   return CPPP_OK;
@@ -857,8 +877,10 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
   // comm
   c->rank = o.rank;
   c->world = o.world < 1 ? 1 : o.world;
-  if (c->world > 1) {
-    if (!o.nccl_unique_id) return fail(c, CPPP_EINVAL, "world > 1 needs nccl_unique_id");
+  c->host_ar = o.host_allreduce;
+  c->host_ar_user = o.host_allreduce_user;
+  if (c->world > 1 && !c->host_ar) {
+    if (!o.nccl_unique_id) return fail(c, CPPP_EINVAL, "world > 1 needs nccl_unique_id or host_allreduce");
     if (!g_nccl.load()) return fail(c, CPPP_ENCCL, "cannot dlopen libnccl.so.2");
     ncclUniqueId id;
     std::memcpy(&id, o.nccl_unique_id, sizeof(id));
@@ -1256,6 +1278,7 @@ void cp_destroy(cppp_ctx* c) {
   if (c->host_stats) cudaFreeHost(c->host_stats);
   if (c->own_ws && c->ws_alloc) cudaFree(c->ws_alloc);
   if (c->comm) g_nccl.commDestroy(c->comm);
+  if (c->host_ar_buf) cudaFreeHost(c->host_ar_buf);
   if (c->ev_S) cudaEventDestroy(c->ev_S);
   if (c->ev_P) cudaEventDestroy(c->ev_P);
   if (c->st2) cudaStreamDestroy(c->st2);

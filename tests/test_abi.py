@@ -14,7 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared_functions():
     src = open(os.path.join(ROOT, "include", "cppp.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*([a-z_0-9]+)\s*\(", src, flags=re.M)
+    names = re.findall(r"^[ \t]*(?:const[ \t]+)?[a-z_0-9]+(?:[ \t]+|[ \t]*\*[ \t]*)([a-z_0-9]+)[ \t]*\(",
+                       src, flags=re.M)
     return sorted(set(names))
 
 

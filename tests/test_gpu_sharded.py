@@ -1,0 +1,152 @@
+"""The sharded (multi-GPU) code path of libcppp on ONE device: P contexts, one host thread each,
+each holding a mode-0 slab, with the library's all-reduce routed through a host-side reducer
+(cppp_opts.host_allreduce) instead of NCCL.  No kernel waits on another context, so this is safe
+on a single GPU; it exercises every sharded branch of the engine (partial leaves, local solves of
+the sharded mode, the PP-sweep exchange) against the unsharded oracle."""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle.cp_oracle as O
+import synthgen as G
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1811_10573_b200.cppp as cp  # noqa: E402
+
+
+class HostReducer:
+    """Sum over P participants in rank order (deterministic)."""
+
+    def __init__(self, P):
+        self.P = P
+        self.bar = threading.Barrier(P)
+        self.slots = [None] * P
+        self.total = None
+
+    def fn(self, rank):
+        def reduce(buf):
+            self.slots[rank] = buf.copy()
+            self.bar.wait()
+            if rank == 0:
+                tot = self.slots[0].copy()
+                for r in range(1, self.P):
+                    tot += self.slots[r]
+                self.total = tot
+            self.bar.wait()
+            buf[:] = self.total
+            self.bar.wait()
+        return reduce
+
+
+def slab(s0, rank, world):
+    return rank * s0 // world, (rank + 1) * s0 // world
+
+
+def run_sharded(P, X, dims, K, body):
+    """Run body(rank, ctx, lo, hi) on P threads with sharded contexts; returns per-rank results."""
+    red = HostReducer(P)
+    out = [None] * P
+    err = [None] * P
+
+    def work(rank):
+        try:
+            lo, hi = slab(dims[0], rank, P)
+            Xs = np.ascontiguousarray(X[lo:hi])
+            ctx = cp.cp_init(Xs, len(dims), dims, K, shard_offset=lo, shard_extent=hi - lo, rank=rank,
+                             world=P, torch_workspace=False, host_allreduce=red.fn(rank))
+            out[rank] = body(rank, ctx, lo, hi)
+            cp.cp_destroy(ctx)
+        except Exception as e:  # noqa: BLE001
+            err[rank] = e
+            try:
+                red.bar.abort()
+            except Exception:
+                pass
+
+    ths = [threading.Thread(target=work, args=(r,)) for r in range(P)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=600)
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("name", ["C1", "C3mini", "C5mini"])
+def test_sharded_kernels_match_oracle(P, name):
+    cfg = G.CONFIGS[name]
+    X = G.make_tensor(cfg)
+    A0 = G.initial_factors(cfg)
+    r = np.random.default_rng(4)
+    dA = [0.01 * r.standard_normal(a.shape) for a in A0]
+
+    def body(rank, ctx, lo, hi):
+        cp.cp_set_factors(ctx, A0)
+        M = cp.mttkrp_dt(ctx)
+        cp.pp_build_operators(ctx)
+        ops = {(i, j): cp.pp_get_operator(ctx, i, j) for i in range(cfg.N) for j in range(i + 1, cfg.N)}
+        singles = [cp.pp_get_single(ctx, n) for n in range(cfg.N)]
+        cp.cp_update_factors(ctx, [a + d for a, d in zip(A0, dA)])
+        upd = [cp.pp_update(ctx, n) for n in range(cfg.N)]
+        return M, ops, singles, upd
+
+    res = run_sharded(P, X, cfg.dims, cfg.K, body)
+    ops_ref = O.pp_operators(X, A0)
+    Mp_ref = [O.pp_single(ops_ref, A0, n, cfg.N) for n in range(cfg.N)]
+    for rank, (M, ops, singles, upd) in enumerate(res):
+        lo, hi = slab(cfg.s, rank, P)
+        for n in range(cfg.N):
+            ref = O.mttkrp(X, A0, n)
+            ref = ref[lo:hi] if n == 0 else ref
+            assert rel(M[n], ref) < 1e-11, (rank, n)
+            sref = Mp_ref[n][lo:hi] if n == 0 else Mp_ref[n]
+            assert rel(singles[n], sref) < 1e-11, (rank, n)
+            uref = O.pp_update(Mp_ref[n], ops_ref, dA, n)
+            uref = uref[lo:hi] if n == 0 else uref
+            assert rel(upd[n], uref) < 1e-11, (rank, n)
+        for (i, j), ref in ops_ref.items():
+            ref = ref[lo:hi] if i == 0 else ref
+            assert rel(ops[(i, j)], ref) < 1e-11, (rank, i, j)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("name", ["C1", "C3mini", "C5mini", "C4mini"])
+def test_sharded_trace_matches_oracle(P, name):
+    cfg = G.CONFIGS[name]
+    X = G.make_tensor(cfg)
+    A0 = G.initial_factors(cfg)
+    A_fin, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, 20)
+
+    def body(rank, ctx, lo, hi):
+        cp.cp_set_factors(ctx, A0)
+        infos = []
+        for t in tr:
+            cp.cp_set_phase_override(ctx, t["phase"])
+            infos.append(cp.als_sweep(ctx, 0.0, cfg.eps_pp))
+        return infos, cp.cp_get_factors(ctx)
+
+    res = run_sharded(P, X, cfg.dims, cfg.K, body)
+    for rank, (infos, A) in enumerate(res):
+        for t, info in zip(tr, infos):
+            assert info["phase"] == t["phase"]
+            if 1.0 - t["fitness"] >= 1e-6:
+                assert abs(info["fitness"] - t["fitness"]) < 1e-8, (rank, t, info)
+        if 1.0 - tr[-1]["fitness"] >= 1e-6:
+            for n in range(cfg.N):
+                assert rel(A[n], A_fin[n]) < 1e-6, (rank, n)
+    # replicas agree bit for bit on the replicated factors (deterministic reductions)
+    for n in range(1, cfg.N):
+        for rank in range(1, P):
+            assert np.array_equal(res[rank][1][n], res[0][1][n])
