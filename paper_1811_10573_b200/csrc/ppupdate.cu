@@ -66,7 +66,7 @@ __global__ void pp_update_combine(PPUpdateArgs a, int xsplit) {
        e += (int64_t)gridDim.x * blockDim.x) {
     double v = 0.0;
     for (int p = 0; p < xsplit; ++p) v += a.partial[p * total + e];
-    double m = a.Mp[e];
+    double m = a.Mp ? a.Mp[e] : 0.0;   // Mp may be null (sharded exchange terms)
     if (a.extra) m += a.extra[e];
     a.out[e] = m + v;
   }
