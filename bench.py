@@ -262,8 +262,12 @@ def main():
         sec = k["total_ms"] * 1e-3
         entry = {"launches_per_step": k["launches"] / args.steps, "ms_per_step": k["total_ms"] / args.steps,
                  "share_of_step": k["total_ms"] / ms}
-        if name == "ttm":
+        ridge = dmma_peak * 1e12 / (hbm_peak * 1e9)          # flop/byte where the two roofs meet
+        if name == "ttm" and k["flops"] / max(k["bytes"], 1.0) >= ridge:
             entry.update(bound="tensor", achieved=k["flops"] / sec / 1e12, peak=dmma_peak, unit="TFLOP/s")
+        elif name == "ttm":   # low arithmetic intensity (e.g. C4: K=30, s=20): HBM-bound GEMM
+            entry.update(bound="hbm", achieved=k["bytes"] / sec / 1e9, peak=hbm_peak, unit="GB/s",
+                         tflops=k["flops"] / sec / 1e12, arithmetic_intensity=k["flops"] / k["bytes"])
         else:
             entry.update(bound="hbm", achieved=k["bytes"] / sec / 1e9, peak=hbm_peak, unit="GB/s")
         entry["frac"] = entry["achieved"] / entry["peak"]

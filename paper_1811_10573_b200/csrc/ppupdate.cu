@@ -60,6 +60,82 @@ __global__ void __launch_bounds__(NT)
   }
 }
 
+// Even K: every (x, y) pair of a term is a contiguous K-run op(x, y, 0..K).  A warp streams whole
+// runs with 16-byte loads (lane owns k-pairs 2l and 64 + 2l) for x = x0 + warp, x0 + warp + 8, ...,
+// four runs in flight per lane; the 8 warps' partial sums are reduced in shared memory in a fixed
+// order.  Works for both operator orientations (only the run's base address differs).
+constexpr int V2_WARPS = 8;
+
+__global__ void __launch_bounds__(V2_WARPS * 32)
+    pp_update_partial_v2(PPUpdateArgs a, int xsplit) {
+  const int64_t y = blockIdx.x;
+  const int part = blockIdx.y;
+  const int K = a.K;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int k0 = 2 * lane, k1 = 64 + 2 * lane;
+  const bool h0 = k0 < K, h1 = k1 < K;
+  double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+  for (int ti = 0; ti < a.nterms; ++ti) {
+    const PPTerm t = a.t[ti];
+    const int64_t x0 = (t.nx * part) / xsplit;
+    const int64_t x1 = (t.nx * (part + 1)) / xsplit;
+    const double* opy = t.op + y * t.sy;
+    int64_t x = x0 + w;
+    for (; x + 3 * V2_WARPS < x1; x += 4 * V2_WARPS) {
+      double2 o0[4], o1[4], d0[4], d1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t xx = x + u * V2_WARPS;
+        const double* run = opy + xx * t.sx;
+        const double* dr = t.dA + xx * K;
+        o0[u] = h0 ? __ldcs(reinterpret_cast<const double2*>(run + k0)) : make_double2(0.0, 0.0);
+        o1[u] = h1 ? __ldcs(reinterpret_cast<const double2*>(run + k1)) : make_double2(0.0, 0.0);
+        d0[u] = h0 ? __ldg(reinterpret_cast<const double2*>(dr + k0)) : make_double2(0.0, 0.0);
+        d1[u] = h1 ? __ldg(reinterpret_cast<const double2*>(dr + k1)) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc0.x = fma(o0[u].x, d0[u].x, acc0.x);
+        acc0.y = fma(o0[u].y, d0[u].y, acc0.y);
+        acc1.x = fma(o1[u].x, d1[u].x, acc1.x);
+        acc1.y = fma(o1[u].y, d1[u].y, acc1.y);
+      }
+    }
+    for (; x < x1; x += V2_WARPS) {
+      const double* run = opy + x * t.sx;
+      const double* dr = t.dA + x * K;
+      if (h0) {
+        const double2 o = __ldcs(reinterpret_cast<const double2*>(run + k0));
+        const double2 d = __ldg(reinterpret_cast<const double2*>(dr + k0));
+        acc0.x = fma(o.x, d.x, acc0.x);
+        acc0.y = fma(o.y, d.y, acc0.y);
+      }
+      if (h1) {
+        const double2 o = __ldcs(reinterpret_cast<const double2*>(run + k1));
+        const double2 d = __ldg(reinterpret_cast<const double2*>(dr + k1));
+        acc1.x = fma(o.x, d.x, acc1.x);
+        acc1.y = fma(o.y, d.y, acc1.y);
+      }
+    }
+  }
+  __shared__ double red[V2_WARPS][128];
+  if (h0) {
+    red[w][k0] = acc0.x;
+    red[w][k0 + 1] = acc0.y;
+  }
+  if (h1) {
+    red[w][k1] = acc1.x;
+    red[w][k1 + 1] = acc1.y;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < V2_WARPS; ++j) s += red[j][k];
+    a.partial[(static_cast<int64_t>(part) * a.ny + y) * K + k] = s;
+  }
+}
+
 __global__ void pp_update_combine(PPUpdateArgs a, int xsplit) {
   const int64_t total = a.ny * a.K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -96,7 +172,13 @@ cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st) {
   for (int i = 0; i < a.nterms; ++i) max_nx = a.t[i].nx > max_nx ? a.t[i].nx : max_nx;
   const int xsplit = choose_xsplit(a.ny, max_nx);
   dim3 grid((unsigned)a.ny, (unsigned)xsplit);
-  pp_update_partial<<<grid, NT, 0, st>>>(a, xsplit);
+  bool aligned = (a.K % 2) == 0;
+  for (int i = 0; i < a.nterms; ++i)
+    aligned = aligned && (a.t[i].sx % 2 == 0) && (a.t[i].sy % 2 == 0) &&
+              (reinterpret_cast<uintptr_t>(a.t[i].op) % 16 == 0) &&
+              (reinterpret_cast<uintptr_t>(a.t[i].dA) % 16 == 0);
+  if (aligned) pp_update_partial_v2<<<grid, V2_WARPS * 32, 0, st>>>(a, xsplit);
+  else pp_update_partial<<<grid, NT, 0, st>>>(a, xsplit);
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
