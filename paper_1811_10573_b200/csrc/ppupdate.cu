@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(NT)
 // order.  Works for both operator orientations (only the run's base address differs).
 constexpr int V2_WARPS = 8;
 
-__global__ void __launch_bounds__(V2_WARPS * 32)
+__global__ void __launch_bounds__(V2_WARPS * 32, 6)
     pp_update_partial_v2(PPUpdateArgs a, int xsplit) {
   const int64_t y = blockIdx.x;
   const int part = blockIdx.y;
@@ -149,10 +149,12 @@ __global__ void pp_update_combine(PPUpdateArgs a, int xsplit) {
 }
 
 int choose_xsplit(int64_t ny, int64_t max_nx) {
-  // aim for >= ~8 CTAs per SM, keep >= 8 x per part
-  int64_t want = (148 * 8 + ny - 1) / ny;
-  int64_t cap = max_nx / 8;
-  if (want > cap) want = cap;
+  // one full wave of resident CTAs (148 SMs x 6 CTAs) when ny allows it (no tail wave);
+  // keep >= 8 x per part
+  const int64_t cap = 148 * 6;
+  int64_t want = ny >= cap ? 1 : cap / ny;
+  const int64_t lim = max_nx / 8;
+  if (want > lim) want = lim;
   if (want > 16) want = 16;
   if (want < 1) want = 1;
   return static_cast<int>(want);
