@@ -66,10 +66,13 @@ __global__ void __launch_bounds__(NT)
 // order.  Works for both operator orientations (only the run's base address differs).
 constexpr int V2_WARPS = 8;
 
-__global__ void __launch_bounds__(V2_WARPS * 32, 6)
+__global__ void __launch_bounds__(V2_WARPS * 32, 4)
     pp_update_partial_v2(PPUpdateArgs a, int xsplit) {
-  const int64_t y = blockIdx.x;
-  const int part = blockIdx.y;
+  __shared__ double red[V2_WARPS][128];
+  const int64_t items = a.ny * xsplit;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+  const int part = static_cast<int>(item / a.ny);
+  const int64_t y = item - static_cast<int64_t>(part) * a.ny;
   const int K = a.K;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int k0 = 2 * lane, k1 = 64 + 2 * lane;
@@ -118,7 +121,6 @@ __global__ void __launch_bounds__(V2_WARPS * 32, 6)
       }
     }
   }
-  __shared__ double red[V2_WARPS][128];
   if (h0) {
     red[w][k0] = acc0.x;
     red[w][k0 + 1] = acc0.y;
@@ -134,86 +136,7 @@ __global__ void __launch_bounds__(V2_WARPS * 32, 6)
     for (int j = 0; j < V2_WARPS; ++j) s += red[j][k];
     a.partial[(static_cast<int64_t>(part) * a.ny + y) * K + k] = s;
   }
-}
-
-// v3 (even K, 16-byte aligned runs): the same warp-per-run walk as v2, but every lane streams its
-// own 16-byte chunks (k-pairs 2l and 64 + 2l) of op and dA through a private 6-stage cp.async
-// ring in shared memory, so the bytes in flight live in smem instead of registers.
-constexpr int V3_WARPS = 8;
-constexpr int V3_STAGES = 6;
-
-__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool pred) {
-  const int n = pred ? 16 : 0;   // src-size 0 fills zeros
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
-}
-
-__global__ void __launch_bounds__(V3_WARPS * 32)
-    pp_update_partial_v3(PPUpdateArgs a, int xsplit) {
-  // per lane and stage: op pair 0, op pair 1, dA pair 0, dA pair 1 (4 x 16 B) — dynamic smem
-  extern __shared__ __align__(16) double v3_smem[];
-  double (*ring)[V3_WARPS * 32][8] = reinterpret_cast<double (*)[V3_WARPS * 32][8]>(v3_smem);
-  __shared__ double red[V3_WARPS][128];
-  const int64_t y = blockIdx.x;
-  const int part = blockIdx.y;
-  const int K = a.K;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int k0 = 2 * lane, k1 = 64 + 2 * lane;
-  const bool h0 = k0 < K, h1 = k1 < K;
-  double acc0x = 0.0, acc0y = 0.0, acc1x = 0.0, acc1y = 0.0;
-  for (int ti = 0; ti < a.nterms; ++ti) {
-    const double* op = a.t[ti].op;
-    const double* dA = a.t[ti].dA;
-    const int64_t sx = a.t[ti].sx, nx = a.t[ti].nx;
-    const int64_t x0 = (nx * part) / xsplit, x1 = (nx * (part + 1)) / xsplit;
-    const double* opy = op + y * a.t[ti].sy;
-    // runs of this warp: x = x0 + w + V3_WARPS * r, r = 0 .. nr-1
-    const int64_t nr = (x1 - x0 - w + V3_WARPS - 1) / V3_WARPS;
-    auto issue = [&](int64_t r) {
-      const int s = static_cast<int>(r % V3_STAGES);
-      const int64_t x = x0 + w + V3_WARPS * r;
-      const double* run = opy + x * sx;
-      const double* dr = dA + x * K;
-      const uint32_t base =
-          static_cast<uint32_t>(__cvta_generic_to_shared(&ring[s][threadIdx.x][0]));
-      cp16(base, run + (h0 ? k0 : 0), h0);
-      cp16(base + 16, run + (h1 ? k1 : 0), h1);
-      cp16(base + 32, dr + (h0 ? k0 : 0), h0);
-      cp16(base + 48, dr + (h1 ? k1 : 0), h1);
-    };
-    for (int64_t r = 0; r < V3_STAGES - 1; ++r) {
-      if (r < nr) issue(r);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    for (int64_t r = 0; r < nr; ++r) {
-      if (r + V3_STAGES - 1 < nr) issue(r + V3_STAGES - 1);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group %0;" ::"n"(V3_STAGES - 1) : "memory");
-      const double* sl = &ring[r % V3_STAGES][threadIdx.x][0];
-      const double2 o0 = *reinterpret_cast<const double2*>(sl);
-      const double2 o1 = *reinterpret_cast<const double2*>(sl + 2);
-      const double2 d0 = *reinterpret_cast<const double2*>(sl + 4);
-      const double2 d1 = *reinterpret_cast<const double2*>(sl + 6);
-      acc0x = fma(o0.x, d0.x, acc0x);
-      acc0y = fma(o0.y, d0.y, acc0y);
-      acc1x = fma(o1.x, d1.x, acc1x);
-      acc1y = fma(o1.y, d1.y, acc1y);
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-  }
-  if (h0) {
-    red[w][k0] = acc0x;
-    red[w][k0 + 1] = acc0y;
-  }
-  if (h1) {
-    red[w][k1] = acc1x;
-    red[w][k1 + 1] = acc1y;
-  }
   __syncthreads();
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < V3_WARPS; ++j) s += red[j][k];
-    a.partial[(static_cast<int64_t>(part) * a.ny + y) * K + k] = s;
   }
 }
 
@@ -230,10 +153,10 @@ __global__ void pp_update_combine(PPUpdateArgs a, int xsplit) {
 }
 
 int choose_xsplit(int64_t ny, int64_t max_nx) {
-  // one full wave of resident CTAs (148 SMs x 2 CTAs of the 96 KB cp.async ring) when ny
-  // allows it (no tail wave); keep >= 8 x per part
-  const int64_t cap = 148 * 2;
-  int64_t want = ny >= cap ? 1 : cap / ny;
+  // the aligned kernel walks (y, part) items grid-stride with 4 CTAs/SM: make ~4 items per CTA
+  // slot; keep >= 8 x per part
+  const int64_t cap = 148 * 4 * 4;
+  int64_t want = (cap + ny - 1) / ny;
   const int64_t lim = max_nx / 8;
   if (want > lim) want = lim;
   if (want > 16) want = 16;
@@ -260,15 +183,12 @@ cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st) {
     aligned = aligned && (a.t[i].sx % 2 == 0) && (a.t[i].sy % 2 == 0) &&
               (reinterpret_cast<uintptr_t>(a.t[i].op) % 16 == 0) &&
               (reinterpret_cast<uintptr_t>(a.t[i].dA) % 16 == 0);
-  constexpr int v3_smem = V3_STAGES * V3_WARPS * 32 * 8 * sizeof(double);
-  static bool v3_attr = false;
-  if (aligned && !v3_attr) {
-    cudaError_t e = cudaFuncSetAttribute(pp_update_partial_v3,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, v3_smem);
-    if (e != cudaSuccess) return e;
-    v3_attr = true;
+  if (aligned) {
+    const int64_t items = a.ny * xsplit;
+    int64_t g2 = 148LL * 4;
+    if (g2 > items) g2 = items;
+    pp_update_partial_v2<<<(unsigned)g2, V2_WARPS * 32, 0, st>>>(a, xsplit);
   }
-  if (aligned) pp_update_partial_v3<<<grid, V3_WARPS * 32, v3_smem, st>>>(a, xsplit);
   else pp_update_partial<<<grid, NT, 0, st>>>(a, xsplit);
   note_launch();
   cudaError_t e = cudaGetLastError();
