@@ -164,7 +164,30 @@ int choose_xsplit(int64_t ny, int64_t max_nx) {
   return static_cast<int>(want);
 }
 
+__global__ void swap_runs_kernel(const double* __restrict__ in, int64_t di, int64_t dj, int K,
+                                 double* __restrict__ out) {
+  const int64_t total = di * dj * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t run = e / K;
+    const int k = static_cast<int>(e - run * K);
+    const int64_t j = run / di, i = run - j * di;   // output run (j, i)
+    out[e] = __ldcs(in + (i * dj + j) * K + k);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_swap_runs(const double* in, int64_t di, int64_t dj, int K, double* out,
+                             cudaStream_t st) {
+  const int64_t total = di * dj * K;
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  swap_runs_kernel<<<(unsigned)blocks, 256, 0, st>>>(in, di, dj, K, out);
+  note_launch();
+  return cudaGetLastError();
+}
 
 size_t pp_update_scratch_doubles(int64_t ny, int K, int64_t max_nx) {
   (void)max_nx;
