@@ -140,6 +140,98 @@ __global__ void __launch_bounds__(V2_WARPS * 32, 4)
   }
 }
 
+// v4 (even K, all terms read as [y][x][k]): an item is (group of YG output rows, x-part).  For
+// each x the warp loads the dA row pair once and the YG operator runs op(y, x, :) of its rows,
+// U x-steps at a time, so YG*U 16-byte loads of operator data are in flight per lane.
+template <int YG, int U>
+__global__ void __launch_bounds__(256, (YG * U > 8) ? 2 : 3)
+    pp_update_partial_v4(PPUpdateArgs a, int xsplit) {
+  __shared__ double red[8][YG][128];
+  const int64_t ngroups = (a.ny + YG - 1) / YG;
+  const int64_t items = ngroups * xsplit;
+  const int K = a.K;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int k0 = 2 * lane, k1 = 64 + 2 * lane;
+  const bool h0 = k0 < K, h1 = k1 < K;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int part = static_cast<int>(item / ngroups);
+    const int64_t y0 = (item - static_cast<int64_t>(part) * ngroups) * YG;
+    double acc[YG][4];
+#pragma unroll
+    for (int g = 0; g < YG; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.0;
+    for (int ti = 0; ti < a.nterms; ++ti) {
+      const PPTerm t = a.t[ti];
+      const int64_t x0 = (t.nx * part) / xsplit, x1 = (t.nx * (part + 1)) / xsplit;
+      const double* opb[YG];
+#pragma unroll
+      for (int g = 0; g < YG; ++g) opb[g] = t.op + min(y0 + g, a.ny - 1) * t.sy;
+      int64_t x = x0 + w;
+      for (; x + (U - 1) * 8 < x1; x += U * 8) {
+        double2 o[U][YG][2], d[U][2];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t xx = x + u * 8;
+          const double* dr = t.dA + xx * K;
+          d[u][0] = h0 ? __ldg(reinterpret_cast<const double2*>(dr + k0)) : make_double2(0.0, 0.0);
+          d[u][1] = h1 ? __ldg(reinterpret_cast<const double2*>(dr + k1)) : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int g = 0; g < YG; ++g) {
+            const double* run = opb[g] + xx * t.sx;
+            o[u][g][0] = h0 ? __ldcs(reinterpret_cast<const double2*>(run + k0)) : make_double2(0.0, 0.0);
+            o[u][g][1] = h1 ? __ldcs(reinterpret_cast<const double2*>(run + k1)) : make_double2(0.0, 0.0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int g = 0; g < YG; ++g) {
+            acc[g][0] = fma(o[u][g][0].x, d[u][0].x, acc[g][0]);
+            acc[g][1] = fma(o[u][g][0].y, d[u][0].y, acc[g][1]);
+            acc[g][2] = fma(o[u][g][1].x, d[u][1].x, acc[g][2]);
+            acc[g][3] = fma(o[u][g][1].y, d[u][1].y, acc[g][3]);
+          }
+      }
+      for (; x < x1; x += 8) {
+        const double* dr = t.dA + x * K;
+        const double2 d0 = h0 ? __ldg(reinterpret_cast<const double2*>(dr + k0)) : make_double2(0.0, 0.0);
+        const double2 d1 = h1 ? __ldg(reinterpret_cast<const double2*>(dr + k1)) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int g = 0; g < YG; ++g) {
+          const double* run = opb[g] + x * t.sx;
+          const double2 o0 = h0 ? __ldcs(reinterpret_cast<const double2*>(run + k0)) : make_double2(0.0, 0.0);
+          const double2 o1 = h1 ? __ldcs(reinterpret_cast<const double2*>(run + k1)) : make_double2(0.0, 0.0);
+          acc[g][0] = fma(o0.x, d0.x, acc[g][0]);
+          acc[g][1] = fma(o0.y, d0.y, acc[g][1]);
+          acc[g][2] = fma(o1.x, d1.x, acc[g][2]);
+          acc[g][3] = fma(o1.y, d1.y, acc[g][3]);
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < YG; ++g) {
+      if (h0) {
+        red[w][g][k0] = acc[g][0];
+        red[w][g][k0 + 1] = acc[g][1];
+      }
+      if (h1) {
+        red[w][g][k1] = acc[g][2];
+        red[w][g][k1 + 1] = acc[g][3];
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < YG * K; e += blockDim.x) {
+      const int g = e / K, k = e - g * K;
+      if (y0 + g < a.ny) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += red[j][g][k];
+        a.partial[(static_cast<int64_t>(part) * a.ny + y0 + g) * K + k] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void pp_update_combine(PPUpdateArgs a, int xsplit) {
   const int64_t total = a.ny * a.K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -200,26 +292,35 @@ cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st) {
   int64_t max_nx = 1;
   for (int i = 0; i < a.nterms; ++i) max_nx = a.t[i].nx > max_nx ? a.t[i].nx : max_nx;
   const int xsplit = choose_xsplit(a.ny, max_nx);
-  dim3 grid((unsigned)a.ny, (unsigned)xsplit);
   bool aligned = (a.K % 2) == 0;
   for (int i = 0; i < a.nterms; ++i)
     aligned = aligned && (a.t[i].sx % 2 == 0) && (a.t[i].sy % 2 == 0) &&
               (reinterpret_cast<uintptr_t>(a.t[i].op) % 16 == 0) &&
               (reinterpret_cast<uintptr_t>(a.t[i].dA) % 16 == 0);
+  int xs_used = xsplit;
   if (aligned) {
-    const int64_t items = a.ny * xsplit;
-    int64_t g2 = 148LL * 4;
-    if (g2 > items) g2 = items;
-    pp_update_partial_v2<<<(unsigned)g2, V2_WARPS * 32, 0, st>>>(a, xsplit);
+    // v4 sizing (tools/probe_pp, C2 shape): ~3 items of (2 rows, x-part) per SM, one per CTA
+    const int64_t ngroups = (a.ny + 1) / 2;
+    int64_t xs = (148 * 3 + ngroups / 2) / ngroups;
+    const int64_t lim = max_nx / 16;
+    if (xs > lim) xs = lim;
+    if (xs > 16) xs = 16;
+    if (xs < 1) xs = 1;
+    xs_used = static_cast<int>(xs);
+    const int64_t items = ngroups * xs;
+    const int64_t grid = items < 148 * 3 ? items : 148 * 3;
+    pp_update_partial_v4<2, 2><<<(unsigned)grid, 256, 0, st>>>(a, xs_used);
+  } else {
+    dim3 grid((unsigned)a.ny, (unsigned)xsplit);
+    pp_update_partial<<<grid, NT, 0, st>>>(a, xsplit);
   }
-  else pp_update_partial<<<grid, NT, 0, st>>>(a, xsplit);
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int64_t total = a.ny * a.K;
   int blocks = (int)((total + 255) / 256);
   if (blocks > 1184) blocks = 1184;
-  pp_update_combine<<<blocks, 256, 0, st>>>(a, xsplit);
+  pp_update_combine<<<blocks, 256, 0, st>>>(a, xs_used);
   note_launch();
   return cudaGetLastError();
 }
