@@ -113,7 +113,6 @@ struct cppp_ctx {
   double* stats = nullptr;   // N x 3 norms, then fitness terms [2], then ||X||² [1]
   double* Fpad = nullptr;    // max s x 128
   double* ops[CPPP_MAX_ORDER][CPPP_MAX_ORDER] = {};   // i<j: [x_i][x_j][k]
-  double* opsT[CPPP_MAX_ORDER][CPPP_MAX_ORDER] = {};  // i<j: [x_j][x_i][k] (PP-update streaming)
   double* pp_partial = nullptr;
   double* sq_partial = nullptr;
   double* gath = nullptr;    // gather scratch (max s x K)
@@ -552,14 +551,6 @@ cppp_status run_pp_build(cppp_ctx* c) {
       for (int j = i + 1; j < N; ++j)
         if (i != c->q && j != c->q)
           STCHK(allreduce(c, c->ops[i][j], (size_t)c->dl[i] * c->dl[j] * K));
-  // second orientation of every operator so each PP-update term streams contiguous
-  // [x-range][K] blocks per output row
-  if (!c->dry) {
-    Prof p(c, CPPP_K_OTHER, 0.0, 0.0);
-    for (int i = 0; i < N; ++i)
-      for (int j = i + 1; j < N; ++j)
-        CUCHK(c, launch_swap_runs(c->ops[i][j], c->dl[i], c->dl[j], K, c->opsT[i][j], c->st));
-  }
   STCHK(build_singles(c));
   if (!c->dry) c->ops_valid = true;
   return CPPP_OK;
@@ -572,13 +563,17 @@ void pp_terms(cppp_ctx* c, int n, bool skip_q, PPUpdateArgs* a) {
   for (int i = 0; i < c->N; ++i) {
     if (i == n || (skip_q && i == c->q)) continue;
     PPTerm t;
-    // M_p^(i,n)(x, y, k) read as [y][x][k]: the stored [x_n][x_i][k] of (n,i) when n < i, the
-    // transposed copy of (i,n) when i < n (P:711 symmetry, L5)
-    t.op = (n < i) ? c->ops[n][i] : c->opsT[i][n];
+    const int lo = std::min(i, n), hi = std::max(i, n);
+    t.op = c->ops[lo][hi];
     t.dA = fac_local(c, c->dA, i);
     t.nx = c->dl[i];
-    t.sx = K;
-    t.sy = c->dl[i] * K;
+    if (i < n) {  // stored [x_i][y][k]
+      t.sx = c->dl[n] * K;
+      t.sy = K;
+    } else {      // stored [y][x_i][k]
+      t.sx = K;
+      t.sy = c->dl[i] * K;
+    }
     a->t[a->nterms++] = t;
   }
 }
@@ -628,12 +623,13 @@ cppp_status run_pp_sweep(cppp_ctx* c) {
           a.out = c->T[m];
           a.partial = c->pp_partial;
           a.nterms = 1;
+          const int lo = std::min(c->q, m), hi = std::max(c->q, m);
           PPTerm t;
-          t.op = (m < c->q) ? c->ops[m][c->q] : c->opsT[c->q][m];   // [x_m][x_q][k]
+          t.op = c->ops[lo][hi];
           t.dA = fac_local(c, c->dA, c->q);
           t.nx = c->dl[c->q];
-          t.sx = c->K;
-          t.sy = c->dl[c->q] * c->K;
+          if (c->q < m) { t.sx = c->dl[m] * c->K; t.sy = c->K; }
+          else { t.sx = c->K; t.sy = c->dl[c->q] * c->K; }
           a.t[0] = t;
           CUCHK(c, launch_pp_update(a, c->st));
         }
@@ -682,12 +678,8 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   size_t oStats = take(sizeof(double) * (3 * N + 8));
   size_t oFpad = take(sizeof(double) * (smax * 128 + 32));   // + TTM tile counter
   size_t oOps[CPPP_MAX_ORDER][CPPP_MAX_ORDER];
-  size_t oOpsT[CPPP_MAX_ORDER][CPPP_MAX_ORDER];
   for (int i = 0; i < N; ++i)
-    for (int j = i + 1; j < N; ++j) {
-      oOps[i][j] = take(sizeof(double) * c->dl[i] * c->dl[j] * K);
-      oOpsT[i][j] = take(sizeof(double) * c->dl[i] * c->dl[j] * K);
-    }
+    for (int j = i + 1; j < N; ++j) oOps[i][j] = take(sizeof(double) * c->dl[i] * c->dl[j] * K);
   size_t oPP = take(sizeof(double) * pp_update_scratch_doubles(smax, K, smax));
   size_t oSq = take(sizeof(double) * 2048);
   size_t oGath = take(sizeof(double) * smax * K);
@@ -725,10 +717,7 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   c->stats = reinterpret_cast<double*>(b + oStats);
   c->Fpad = reinterpret_cast<double*>(b + oFpad);
   for (int i = 0; i < N; ++i)
-    for (int j = i + 1; j < N; ++j) {
-      c->ops[i][j] = reinterpret_cast<double*>(b + oOps[i][j]);
-      c->opsT[i][j] = reinterpret_cast<double*>(b + oOpsT[i][j]);
-    }
+    for (int j = i + 1; j < N; ++j) c->ops[i][j] = reinterpret_cast<double*>(b + oOps[i][j]);
   c->pp_partial = reinterpret_cast<double*>(b + oPP);
   c->sq_partial = reinterpret_cast<double*>(b + oSq);
   c->gath = reinterpret_cast<double*>(b + oGath);
@@ -1064,11 +1053,11 @@ cppp_status pp_update(cppp_ctx* c, int n, double* M_tilde) {
     a.partial = c->pp_partial;
     a.nterms = 1;
     PPTerm t;
-    t.op = (n < c->q) ? c->ops[n][c->q] : c->opsT[c->q][n];   // [x_n][x_q][k]
+    t.op = c->ops[std::min(c->q, n)][std::max(c->q, n)];
     t.dA = fac_local(c, c->dA, c->q);
     t.nx = c->dl[c->q];
-    t.sx = c->K;
-    t.sy = c->dl[c->q] * c->K;
+    if (c->q < n) { t.sx = c->dl[n] * c->K; t.sy = c->K; }
+    else { t.sx = c->K; t.sy = c->dl[c->q] * c->K; }
     a.t[0] = t;
     CUCHK(c, launch_pp_update(a, c->st));
     STCHK(allreduce(c, c->T[n], (size_t)c->dl[n] * c->K));

@@ -80,9 +80,7 @@ struct PPUpdateArgs {
 };
 cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st);
 size_t pp_update_scratch_doubles(int64_t ny, int K, int64_t max_nx);
-// out[j][i][k] = in[i][j][k] (swap the two leading indices, K-runs kept contiguous)
-cudaError_t launch_swap_runs(const double* in, int64_t di, int64_t dj, int K, double* out,
-                             cudaStream_t st);
+
 
 // ---------------------------------------------------------------- small dense ops (K <= 128)
 // Γ^(n) = Hadamard of S[m], m != n -> Gamma; Cholesky factor (L13 pivot rule) -> L

@@ -60,87 +60,7 @@ __global__ void __launch_bounds__(NT)
   }
 }
 
-// Even K: every (x, y) pair of a term is a contiguous K-run op(x, y, 0..K).  A warp streams whole
-// runs with 16-byte loads (lane owns k-pairs 2l and 64 + 2l) for x = x0 + warp, x0 + warp + 8, ...,
-// four runs in flight per lane; the 8 warps' partial sums are reduced in shared memory in a fixed
-// order.  Works for both operator orientations (only the run's base address differs).
-constexpr int V2_WARPS = 8;
-
-__global__ void __launch_bounds__(V2_WARPS * 32, 4)
-    pp_update_partial_v2(PPUpdateArgs a, int xsplit) {
-  __shared__ double red[V2_WARPS][128];
-  const int64_t items = a.ny * xsplit;
-  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-  const int part = static_cast<int>(item / a.ny);
-  const int64_t y = item - static_cast<int64_t>(part) * a.ny;
-  const int K = a.K;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int k0 = 2 * lane, k1 = 64 + 2 * lane;
-  const bool h0 = k0 < K, h1 = k1 < K;
-  double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-  for (int ti = 0; ti < a.nterms; ++ti) {
-    const PPTerm t = a.t[ti];
-    const int64_t x0 = (t.nx * part) / xsplit;
-    const int64_t x1 = (t.nx * (part + 1)) / xsplit;
-    const double* opy = t.op + y * t.sy;
-    int64_t x = x0 + w;
-    for (; x + 3 * V2_WARPS < x1; x += 4 * V2_WARPS) {
-      double2 o0[4], o1[4], d0[4], d1[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t xx = x + u * V2_WARPS;
-        const double* run = opy + xx * t.sx;
-        const double* dr = t.dA + xx * K;
-        o0[u] = h0 ? __ldcs(reinterpret_cast<const double2*>(run + k0)) : make_double2(0.0, 0.0);
-        o1[u] = h1 ? __ldcs(reinterpret_cast<const double2*>(run + k1)) : make_double2(0.0, 0.0);
-        d0[u] = h0 ? __ldg(reinterpret_cast<const double2*>(dr + k0)) : make_double2(0.0, 0.0);
-        d1[u] = h1 ? __ldg(reinterpret_cast<const double2*>(dr + k1)) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        acc0.x = fma(o0[u].x, d0[u].x, acc0.x);
-        acc0.y = fma(o0[u].y, d0[u].y, acc0.y);
-        acc1.x = fma(o1[u].x, d1[u].x, acc1.x);
-        acc1.y = fma(o1[u].y, d1[u].y, acc1.y);
-      }
-    }
-    for (; x < x1; x += V2_WARPS) {
-      const double* run = opy + x * t.sx;
-      const double* dr = t.dA + x * K;
-      if (h0) {
-        const double2 o = __ldcs(reinterpret_cast<const double2*>(run + k0));
-        const double2 d = __ldg(reinterpret_cast<const double2*>(dr + k0));
-        acc0.x = fma(o.x, d.x, acc0.x);
-        acc0.y = fma(o.y, d.y, acc0.y);
-      }
-      if (h1) {
-        const double2 o = __ldcs(reinterpret_cast<const double2*>(run + k1));
-        const double2 d = __ldg(reinterpret_cast<const double2*>(dr + k1));
-        acc1.x = fma(o.x, d.x, acc1.x);
-        acc1.y = fma(o.y, d.y, acc1.y);
-      }
-    }
-  }
-  if (h0) {
-    red[w][k0] = acc0.x;
-    red[w][k0 + 1] = acc0.y;
-  }
-  if (h1) {
-    red[w][k1] = acc1.x;
-    red[w][k1 + 1] = acc1.y;
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < K; k += blockDim.x) {
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < V2_WARPS; ++j) s += red[j][k];
-    a.partial[(static_cast<int64_t>(part) * a.ny + y) * K + k] = s;
-  }
-  __syncthreads();
-  }
-}
-
-// v4 (even K, all terms read as [y][x][k]): an item is (group of YG output rows, x-part).  For
+// v4 (even K, 16-byte aligned K-runs; both operator orientations): an item is (group of YG output rows, x-part).  For
 // each x the warp loads the dA row pair once and the YG operator runs op(y, x, :) of its rows,
 // U x-steps at a time, so YG*U 16-byte loads of operator data are in flight per lane.
 template <int YG, int U>
@@ -256,30 +176,7 @@ int choose_xsplit(int64_t ny, int64_t max_nx) {
   return static_cast<int>(want);
 }
 
-__global__ void swap_runs_kernel(const double* __restrict__ in, int64_t di, int64_t dj, int K,
-                                 double* __restrict__ out) {
-  const int64_t total = di * dj * K;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t run = e / K;
-    const int k = static_cast<int>(e - run * K);
-    const int64_t j = run / di, i = run - j * di;   // output run (j, i)
-    out[e] = __ldcs(in + (i * dj + j) * K + k);
-  }
-}
-
 }  // namespace
-
-cudaError_t launch_swap_runs(const double* in, int64_t di, int64_t dj, int K, double* out,
-                             cudaStream_t st) {
-  const int64_t total = di * dj * K;
-  if (total == 0) return cudaSuccess;
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 32) blocks = 148 * 32;
-  swap_runs_kernel<<<(unsigned)blocks, 256, 0, st>>>(in, di, dj, K, out);
-  note_launch();
-  return cudaGetLastError();
-}
 
 size_t pp_update_scratch_doubles(int64_t ny, int K, int64_t max_nx) {
   (void)max_nx;

@@ -57,17 +57,6 @@ int main() {
   for (int t = 0; t < 2; ++t) { a.t[t].op = t ? op2 : op1; a.t[t].dA = dA; a.t[t].sx = K; a.t[t].sy = s * K; a.t[t].nx = s; }
   float ms = timeit([&] { launch_pp_update(a, 0); });
   printf("{\"kernel\": \"launch_pp_update (partial+combine)\", \"GBps\": %.0f, \"us\": %.1f}\n", bytes / (ms * 1e-3) / 1e9, ms * 1e3);
-  for (int xs : {1, 2, 4, 6, 8, 12, 16}) {
-    const int64_t items = s * xs;
-    for (int g : {148 * 2, 148 * 4, 148 * 8}) {
-      int gg = items < g ? (int)items : g;
-      ms = timeit([&] { pp_update_partial_v2<<<gg, V2_WARPS * 32>>>(a, xs); });
-      printf("{\"kernel\": \"partial_v2\", \"xsplit\": %d, \"grid\": %d, \"GBps\": %.0f, \"us\": %.1f}\n", xs, gg, bytes / (ms * 1e-3) / 1e9, ms * 1e3);
-    }
-    dim3 grid(s, xs);
-    ms = timeit([&] { pp_update_partial<<<grid, 256>>>(a, xs); });
-    printf("{\"kernel\": \"partial_v1\", \"xsplit\": %d, \"GBps\": %.0f}\n", xs, bytes / (ms * 1e-3) / 1e9);
-  }
   auto v4 = [&](auto kern, const char* name, int yg) {
     for (int xs : {2, 4, 6, 8}) {
       const int64_t items = ((s + yg - 1) / yg) * xs;
@@ -79,6 +68,10 @@ int main() {
     }
   };
   v4(pp_update_partial_v4<2, 2>, "v4 YG2 U2", 2);
+  for (int t = 0; t < 2; ++t) { a.t[t].sx = s * K; a.t[t].sy = K; }   // native [x][y][k] orientation
+  v4(pp_update_partial_v4<2, 2>, "v4 YG2 U2 strided", 2);
+  v4(pp_update_partial_v4<4, 1>, "v4 YG4 U1 strided", 4);
+  for (int t = 0; t < 2; ++t) { a.t[t].sx = K; a.t[t].sy = s * K; }
   v4(pp_update_partial_v4<4, 2>, "v4 YG4 U2", 4);
   v4(pp_update_partial_v4<2, 4>, "v4 YG2 U4", 2);
   v4(pp_update_partial_v4<4, 1>, "v4 YG4 U1", 4);
