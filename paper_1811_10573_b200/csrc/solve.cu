@@ -275,28 +275,26 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
 // with L staged in shared memory (pitch K+1: column reads are conflict-free), as the oracle does;
 // pinv path (mode 1): a = m P.  Then G = (a_old - a_new) Γ with Γ staged, dA, row norms and the
 // CTA's partial Gram.  Lane c owns columns c + 32u.
-constexpr int SR_WARPS = 16;
+constexpr int SR_WARPS = 8;
 
-// stage a K x K row-major matrix into shared memory with row pitch `pitch` (8 loads in flight)
+// stage a K x K row-major matrix into shared memory with row pitch `pitch`: 8-byte cp.async
+// (LDGSTS) for every element, all in flight, no register round trip; the caller syncs.
 __device__ __forceinline__ void stage_matrix(double* dst, int pitch, const double* __restrict__ src,
                                              int K) {
   const int KK = K * K;
-  for (int e0 = threadIdx.x; e0 < KK; e0 += 8 * blockDim.x) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * blockDim.x;
-      v[u] = e < KK ? __ldg(src + e) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * blockDim.x;
-      if (e < KK) {
-        const int i = e / K, j = e - i * K;
-        dst[i * pitch + j] = v[u];
-      }
+  int i = threadIdx.x / K, j = threadIdx.x - (threadIdx.x / K) * K;
+  const int di = blockDim.x / K, dj = blockDim.x - di * K;
+  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + i * pitch + j));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src + e) : "memory");
+    i += di;
+    j += dj;
+    if (j >= K) {
+      j -= K;
+      ++i;
     }
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
 __device__ __forceinline__ double pick4(const double (&m)[4], int slot) {

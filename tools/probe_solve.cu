@@ -38,7 +38,7 @@ int main() {
     cudaMalloc(&dS, 8 * N * K * K); cudaMalloc(&dG, 8 * K * K); cudaMalloc(&dP, 8 * K * K);
     cudaMalloc(&dV, 8 * K * K); cudaMalloc(&dmode, 4); cudaMalloc(&dM, 8 * s * K);
     cudaMalloc(&dA, 8 * s * K); cudaMalloc(&dD, 8 * s * K); cudaMalloc(&drs, 8 * s * 3);
-    cudaMalloc(&dgp, 8 * 32 * K * K); cudaMalloc(&dSn, 8 * K * K); cudaMalloc(&dn, 8 * 3);
+    cudaMalloc(&dgp, 8 * 64 * K * K); cudaMalloc(&dSn, 8 * K * K); cudaMalloc(&dn, 8 * 3);
     cudaMemcpy(dS, S.data(), 8 * N * K * K, cudaMemcpyHostToDevice);
     cudaMemcpy(dM, A.data(), 8 * s * K, cudaMemcpyHostToDevice);
     cudaMemcpy(dA, A.data(), 8 * s * K, cudaMemcpyHostToDevice);
