@@ -58,6 +58,7 @@ typedef enum {
 #define CPPP_FLAG_SIMT_TTM      2u  /* force the SIMT (non-tensor-core) TTM kernel (testing) */
 #define CPPP_FLAG_PROFILE       4u  /* time each kernel class with CUDA events (cppp_kernel_stats) */
 #define CPPP_FLAG_NO_FUSED_TTV  8u  /* one multi-TTV launch per child instead of per parent */
+#define CPPP_FLAG_NO_GRAPH     16u  /* run sweeps eagerly instead of replaying captured CUDA graphs */
 
 typedef struct {
   int device;               /* CUDA ordinal (default 0) */

@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(_HERE, "libcppp.so")
 PHASE_AUTO, PHASE_DT, PHASE_PP_BUILD, PHASE_PP = -1, 0, 1, 2
 PHASE_NAMES = {PHASE_DT: "dt", PHASE_PP_BUILD: "pp-build", PHASE_PP: "pp-approx"}
 PHASE_BY_NAME = {v: k for k, v in PHASE_NAMES.items()}
-FLAG_BORROW_TENSOR, FLAG_SIMT_TTM, FLAG_PROFILE, FLAG_NO_FUSED_TTV = 1, 2, 4, 8
+FLAG_BORROW_TENSOR, FLAG_SIMT_TTM, FLAG_PROFILE, FLAG_NO_FUSED_TTV, FLAG_NO_GRAPH = 1, 2, 4, 8, 16
 K_TTM, K_TTV, K_PPUPDATE, K_SOLVE, K_OTHER = range(5)
 KCLASS_NAMES = ["ttm", "ttv", "pp_update", "solve", "other"]
 

@@ -137,11 +137,20 @@ struct cppp_ctx {
   size_t host_ar_cap = 0;
   // profiling
   std::vector<ProfPending> pending;
+  std::vector<ProfPending> pending_graph;     // graph-owned events to read after a replay
   std::vector<cudaEvent_t> evpool;
   cppp_kernel_stat kstat[CPPP_K_COUNT] = {};
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   std::string err;
   bool dry = false;   // planning pass: no launches
+  // CUDA graphs of whole sweeps, one per phase (captured on the phase's second use)
+  bool capturing = false;
+  std::vector<ProfPending> capture_prof;       // external event-record nodes of the capture
+  struct SweepGraph {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<ProfPending> prof;
+    int uses = 0;
+  } graphs[3];
 };
 
 namespace {
@@ -190,12 +199,23 @@ struct Prof {
   cudaEvent_t a = nullptr;
   Prof(cppp_ctx* c_, int cls_, double f, double b) : c(c_), cls(cls_), flops(f), bytes(b) {
     if (!c->dry && (c->flags & CPPP_FLAG_PROFILE)) {
-      a = get_event(c);
-      cudaEventRecord(a, c->st);
+      if (c->capturing) {   // graph-owned event, recorded by an event-record node on every replay
+        cudaEventCreate(&a);
+        cudaEventRecordWithFlags(a, c->st, cudaEventRecordExternal);
+      } else {
+        a = get_event(c);
+        cudaEventRecord(a, c->st);
+      }
     }
   }
   ~Prof() {
-    if (a) {
+    if (!a) return;
+    if (c->capturing) {
+      cudaEvent_t b;
+      cudaEventCreate(&b);
+      cudaEventRecordWithFlags(b, c->st, cudaEventRecordExternal);
+      c->capture_prof.push_back({cls, a, b, flops, bytes});
+    } else {
       cudaEvent_t b = get_event(c);
       cudaEventRecord(b, c->st);
       c->pending.push_back({cls, a, b, flops, bytes});
@@ -203,6 +223,17 @@ struct Prof {
   }
 };
 void prof_collect(cppp_ctx* c) {
+  for (auto& p : c->pending_graph) {
+    float ms = 0.f;
+    cudaEventSynchronize(p.b);
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    auto& k = c->kstat[p.cls];
+    k.launches += 1;
+    k.total_ms += ms;
+    k.flops += p.flops;
+    k.bytes += p.bytes;
+  }
+  c->pending_graph.clear();
   if (c->pending.empty()) return;
   for (auto& p : c->pending) {
     float ms = 0.f;
@@ -329,6 +360,9 @@ cppp_status finish_mode(cppp_ctx* c, int n, const double* Mn, bool pp_phase) {
                                   c->S_all + (int64_t)n * K * K, c->stats + 3 * c->N, c->st));
   }
   CUCHK(c, cudaEventRecord(c->ev_S, c->st));
+  // the next mode's factorization starts right away on the side stream; inside a captured sweep
+  // the wrap-around to mode 0 of the next sweep is left out (every fork must join in the graph)
+  if (c->capturing && n == c->N - 1) return CPPP_OK;
   return prefetch_inverse(c, (n + 1) % c->N);
 }
 
@@ -637,6 +671,61 @@ cppp_status run_pp_sweep(cppp_ctx* c) {
       }
     }
   }
+  return CPPP_OK;
+}
+
+// ---------------------------------------------------------------- one sweep of a phase
+cppp_status run_phase_eager(cppp_ctx* c, int phase) {
+  // inside a capture the side stream must fork from an event recorded in the capture
+  if (c->capturing) CUCHK(c, cudaEventRecord(c->ev_S, c->st));
+  STCHK(prefetch_inverse(c, 0));
+  if (phase == CPPP_PHASE_DT) {
+    STCHK(run_dt(c, true, c->M));
+  } else {
+    if (phase == CPPP_PHASE_PP_BUILD) STCHK(run_pp_build(c));
+    STCHK(run_pp_sweep(c));
+  }
+  return CPPP_OK;
+}
+
+// Whole sweeps replay as CUDA graphs (captured on a phase's second use, so the first use sets
+// every kernel attribute eagerly).  Not used with several ranks (collectives stay eager).
+cppp_status run_phase(cppp_ctx* c, int phase) {
+  const bool graphs = !(c->flags & CPPP_FLAG_NO_GRAPH) && c->world == 1;
+  auto& g = c->graphs[phase];
+  g.uses++;
+  if (!graphs || g.uses < 2) {
+    STCHK(run_phase_eager(c, phase));
+  } else {
+    if (!g.exec) {
+      // a pending prefetch on the side stream belongs to the previous sweep: join it first
+      STCHK(drain_prefetch(c));
+      cudaGraph_t graph = nullptr;
+      CUCHK(c, cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
+      c->capturing = true;
+      c->capture_prof.clear();
+      cppp_status s = run_phase_eager(c, phase);
+      c->capturing = false;
+      cudaError_t e = cudaStreamEndCapture(c->st, &graph);
+      if (s != CPPP_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return s;
+      }
+      if (e != cudaSuccess) return fail(c, CPPP_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+      e = cudaGraphInstantiate(&g.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return fail(c, CPPP_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+      g.prof = c->capture_prof;
+      c->capture_prof.clear();
+      c->prefetched = -1;   // the graph starts with its own mode-0 factorization
+    } else {
+      STCHK(drain_prefetch(c));
+    }
+    CUCHK(c, cudaGraphLaunch(g.exec, c->st));
+    c->prefetched = -1;
+    for (auto& p : g.prof) c->pending_graph.push_back(p);
+  }
+  if (phase == CPPP_PHASE_PP_BUILD) c->ops_valid = true;
   return CPPP_OK;
 }
 
@@ -1086,16 +1175,8 @@ cppp_status als_sweep(cppp_ctx* c, double eps, double eps_pp, cppp_sweep_info* i
   if (phase == CPPP_PHASE_PP && !c->ops_valid)
     return fail(c, CPPP_ESTATE, "PP sweep requested without operators");
   CUCHK(c, cudaEventRecord(c->ev_a, c->st));
-  STCHK(prefetch_inverse(c, 0));
-  if (phase == CPPP_PHASE_DT) {
-    STCHK(run_dt(c, true, c->M));
-  } else {
-    if (phase == CPPP_PHASE_PP_BUILD) {
-      STCHK(run_pp_build(c));
-      c->restarts++;
-    }
-    STCHK(run_pp_sweep(c));
-  }
+  STCHK(run_phase(c, phase));
+  if (phase == CPPP_PHASE_PP_BUILD) c->restarts++;
   CUCHK(c, cudaEventRecord(c->ev_b, c->st));
   const int N = c->N;
   CUCHK(c, cudaMemcpyAsync(c->host_stats, c->stats, sizeof(double) * (3 * N + 2),
@@ -1279,6 +1360,13 @@ void cp_destroy(cppp_ctx* c) {
   if (c->own_ws && c->ws_alloc) cudaFree(c->ws_alloc);
   if (c->comm) g_nccl.commDestroy(c->comm);
   if (c->host_ar_buf) cudaFreeHost(c->host_ar_buf);
+  for (auto& g : c->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (auto& p : g.prof) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+  }
   if (c->ev_S) cudaEventDestroy(c->ev_S);
   if (c->ev_P) cudaEventDestroy(c->ev_P);
   if (c->st2) cudaStreamDestroy(c->st2);
