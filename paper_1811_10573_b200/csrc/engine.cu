@@ -722,6 +722,10 @@ cppp_status run_phase(cppp_ctx* c, int phase) {
       STCHK(drain_prefetch(c));
     }
     CUCHK(c, cudaGraphLaunch(g.exec, c->st));
+    // events recorded inside a capture cannot be waited on outside it: re-arm them eagerly
+    // (after the replay the Grams are final and no factorization is pending)
+    CUCHK(c, cudaEventRecord(c->ev_S, c->st));
+    CUCHK(c, cudaEventRecord(c->ev_P, c->st));
     c->prefetched = -1;
     for (auto& p : g.prof) c->pending_graph.push_back(p);
   }
