@@ -150,6 +150,7 @@ struct cppp_ctx {
     cudaGraphExec_t exec = nullptr;
     std::vector<ProfPending> prof;
     int uses = 0;
+    uint64_t launches = 0;   // kernel nodes captured (credited to cppp_launch_count per replay)
   } graphs[3];
 };
 
@@ -704,7 +705,10 @@ cppp_status run_phase(cppp_ctx* c, int phase) {
       CUCHK(c, cudaStreamBeginCapture(c->st, cudaStreamCaptureModeRelaxed));
       c->capturing = true;
       c->capture_prof.clear();
+      const uint64_t l0 = launch_count();
       cppp_status s = run_phase_eager(c, phase);
+      g.launches = launch_count() - l0;
+      note_launches(0ull - g.launches);   // captured, not executed
       c->capturing = false;
       cudaError_t e = cudaStreamEndCapture(c->st, &graph);
       if (s != CPPP_OK) {
@@ -722,6 +726,7 @@ cppp_status run_phase(cppp_ctx* c, int phase) {
       STCHK(drain_prefetch(c));
     }
     CUCHK(c, cudaGraphLaunch(g.exec, c->st));
+    note_launches(g.launches);
     // events recorded inside a capture cannot be waited on outside it: re-arm them eagerly
     // (after the replay the Grams are final and no factorization is pending)
     CUCHK(c, cudaEventRecord(c->ev_S, c->st));

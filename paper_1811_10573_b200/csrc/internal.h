@@ -15,6 +15,7 @@ struct Dims {
 // Count of kernel launches issued by this library (all contexts), for the bench's
 // gpu_launches claim.  note_launch() follows every <<<>>> in the library.
 void note_launch();
+void note_launches(uint64_t n);   // n may be a wrapped negative (two's complement)
 uint64_t launch_count();
 
 // ---------------------------------------------------------------- kernel launchers

@@ -559,6 +559,7 @@ int grid_for(int64_t n, int threads, int cap) {
 
 static unsigned long long g_launches = 0;
 void note_launch() { __atomic_add_fetch(&g_launches, 1ull, __ATOMIC_RELAXED); }
+void note_launches(uint64_t n) { __atomic_add_fetch(&g_launches, n, __ATOMIC_RELAXED); }
 uint64_t launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
 int solve_row_blocks(int64_t rows) { return static_cast<int>((rows + SR_WARPS - 1) / SR_WARPS); }

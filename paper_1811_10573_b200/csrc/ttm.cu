@@ -30,7 +30,7 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 16;
-constexpr int NWARP = 8;
+constexpr int NWARP = 16;   // consumer warps, 8 output rows each (4 per SM sub-partition)
 constexpr int NTHREADS = (NWARP + 1) * 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -101,7 +101,7 @@ struct Cfg {
 // Persistent: CTA b processes tiles b, b + gridDim.x, ...; the producer warp runs ahead across
 // tile boundaries (bounded by the ring), so the next tile's loads overlap this tile's epilogue.
 template <int NT, bool MC>
-__global__ void __launch_bounds__(NTHREADS)
+__global__ void __launch_bounds__(NTHREADS, 1)
     ttm_dmma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
                     double* __restrict__ out, int64_t Mrows, int64_t mtiles, int64_t ntiles, int S,
                     int K, int stages, unsigned long long* __restrict__ tile_counter) {
@@ -168,10 +168,12 @@ __global__ void __launch_bounds__(NTHREADS)
     return;
   }
 
-  // ---------------- consumers: warp owns rows [16*warp, 16*warp+16) x all BN columns
+  // ---------------- consumers: warp owns 8 output rows x all BN columns (one 8-row m-tile)
   const int g = lane >> 2, t = lane & 3;
-  // k-contiguous A rows: tile i, fragment row g -> box row 16w + 8i + fm(g), fm(g) = (g>>1)|((g&1)<<2)
+  // k-contiguous A: fragment row g -> box row 8 warp + fm(g), fm(g) = (g>>1)|((g&1)<<2)
   const int fm = (g >> 1) | ((g & 1) << 2);
+  // m-contiguous A: 16-row box (warp >> 1), rows 8 (warp & 1) + g within it
+  const int mbox = warp >> 1, mrow = 8 * (warp & 1) + g;
   const bool pairs = (K % 2) == 0;
   int64_t it = 0;
   while (true) {
@@ -183,11 +185,9 @@ __global__ void __launch_bounds__(NTHREADS)
     if (tile < 0) break;
     const int64_t b = MC ? tile / mtiles : 0;
     const int64_t m0 = (tile - b * mtiles) * BM;
-    double acc[2][NT][2];
+    double acc[NT][2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
 
     for (int kt = 0; kt < nk; ++kt, ++it) {
       const int st = static_cast<int>(it % stages);
@@ -199,19 +199,19 @@ __global__ void __launch_bounds__(NTHREADS)
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         if (q >= qmax) break;
-        double a[2][2];  // [m-tile i][kk]
+        double a[2];  // [kk]
         if (!MC) {
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int row = 16 * warp + 8 * i + fm;
-            const int chunk = 4 * q + t;
-            lds2(a[i][0], a[i][1], sx + row * 128 + ((chunk ^ (row & 7)) << 4));
-          }
+          const int row = 8 * warp + fm;
+          const int chunk = 4 * q + t;
+          lds2(a[0], a[1], sx + row * 128 + ((chunk ^ (row & 7)) << 4));
         } else {
 #pragma unroll
           for (int kk = 0; kk < 2; ++kk) {
             const int row = 8 * q + 2 * t + kk;
-            lds2(a[0][kk], a[1][kk], sx + warp * 2048 + row * 128 + ((g ^ (row & 7)) << 4));
+            asm volatile("ld.shared.f64 %0, [%1];"
+                         : "=d"(a[kk])
+                         : "r"(sx + mbox * 2048 + row * 128 + (((mrow >> 1) ^ (row & 7)) << 4) +
+                               ((mrow & 1) << 3)));
           }
         }
 #pragma unroll
@@ -222,10 +222,8 @@ __global__ void __launch_bounds__(NTHREADS)
           for (int c = 0; c < NT / 2; ++c) {   // tile pair: columns 16c + 2g (+1), interleaved
             double b0, b1;
             lds2(b0, b1, frow + c * 2048);
-            dmma(acc[0][2 * c], a[0][kk], b0);
-            dmma(acc[1][2 * c], a[1][kk], b0);
-            dmma(acc[0][2 * c + 1], a[0][kk], b1);
-            dmma(acc[1][2 * c + 1], a[1][kk], b1);
+            dmma(acc[2 * c], a[kk], b0);
+            dmma(acc[2 * c + 1], a[kk], b1);
           }
           if (NT & 1) {  // unpaired last tile: contiguous columns 16c + g, 8-byte loads
             constexpr int c = NT / 2;
@@ -233,8 +231,7 @@ __global__ void __launch_bounds__(NTHREADS)
             asm volatile("ld.shared.f64 %0, [%1];"
                          : "=d"(b0)
                          : "r"(sf + c * 2048 + row * 128 + (((g >> 1) ^ (row & 7)) << 4) + ((g & 1) << 3)));
-            dmma(acc[0][NT - 1], a[0][kk], b0);
-            dmma(acc[1][NT - 1], a[1][kk], b0);
+            dmma(acc[NT - 1], a[kk], b0);
           }
         }
       }
@@ -242,36 +239,36 @@ __global__ void __launch_bounds__(NTHREADS)
       if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
     }
 
-    // ---------------- epilogue: thread holds rows {r_i} x columns 16c + 4t + {0,1,2,3}
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int mloc = MC ? (16 * warp + 2 * g + i) : (16 * warp + 8 * i + fm);
+    // ---------------- epilogue: thread holds row r x columns 16c + 4t + {0,1,2,3}
+    {
+      const int mloc = MC ? (16 * mbox + mrow) : (8 * warp + fm);
       const int64_t m = m0 + mloc;
-      if (m >= Mrows) continue;
-      double* orow = out + (b * Mrows + m) * static_cast<int64_t>(K);
+      if (m < Mrows) {
+        double* orow = out + (b * Mrows + m) * static_cast<int64_t>(K);
 #pragma unroll
-      for (int c = 0; c < NT / 2; ++c) {
-        const int n0 = 16 * c + 4 * t;
-        const double v0 = acc[i][2 * c][0], v1 = acc[i][2 * c + 1][0];
-        const double v2 = acc[i][2 * c][1], v3 = acc[i][2 * c + 1][1];
-        if (pairs && n0 + 3 < K) {
-          *reinterpret_cast<double2*>(orow + n0) = make_double2(v0, v1);
-          *reinterpret_cast<double2*>(orow + n0 + 2) = make_double2(v2, v3);
-        } else {
-          if (n0 < K) orow[n0] = v0;
-          if (n0 + 1 < K) orow[n0 + 1] = v1;
-          if (n0 + 2 < K) orow[n0 + 2] = v2;
-          if (n0 + 3 < K) orow[n0 + 3] = v3;
+        for (int c = 0; c < NT / 2; ++c) {
+          const int n0 = 16 * c + 4 * t;
+          const double v0 = acc[2 * c][0], v1 = acc[2 * c + 1][0];
+          const double v2 = acc[2 * c][1], v3 = acc[2 * c + 1][1];
+          if (pairs && n0 + 3 < K) {
+            *reinterpret_cast<double2*>(orow + n0) = make_double2(v0, v1);
+            *reinterpret_cast<double2*>(orow + n0 + 2) = make_double2(v2, v3);
+          } else {
+            if (n0 < K) orow[n0] = v0;
+            if (n0 + 1 < K) orow[n0 + 1] = v1;
+            if (n0 + 2 < K) orow[n0 + 2] = v2;
+            if (n0 + 3 < K) orow[n0 + 3] = v3;
+          }
         }
-      }
-      if (NT & 1) {
-        const int n0 = 16 * (NT / 2) + 2 * t;
-        const double v0 = acc[i][NT - 1][0], v1 = acc[i][NT - 1][1];
-        if (pairs && n0 + 1 < K) {
-          *reinterpret_cast<double2*>(orow + n0) = make_double2(v0, v1);
-        } else {
-          if (n0 < K) orow[n0] = v0;
-          if (n0 + 1 < K) orow[n0 + 1] = v1;
+        if (NT & 1) {
+          const int n0 = 16 * (NT / 2) + 2 * t;
+          const double v0 = acc[NT - 1][0], v1 = acc[NT - 1][1];
+          if (pairs && n0 + 1 < K) {
+            *reinterpret_cast<double2*>(orow + n0) = make_double2(v0, v1);
+          } else {
+            if (n0 < K) orow[n0] = v0;
+            if (n0 + 1 < K) orow[n0 + 1] = v1;
+          }
         }
       }
     }
