@@ -104,7 +104,8 @@ typedef enum {
   CPPP_K_PPUPDATE = 2,  /* fused PP update over all pairs */
   CPPP_K_SOLVE = 3,     /* Gram / Hadamard / Cholesky / row solves / gradient */
   CPPP_K_OTHER = 4,
-  CPPP_K_COUNT = 5
+  CPPP_K_FACTOR = 5,    /* Γ^(n) and its Cholesky factor (side stream, overlapped with M^(n)) */
+  CPPP_K_COUNT = 6
 } cppp_kernel_class;
 
 typedef struct {

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -105,11 +106,12 @@ struct cppp_ctx {
   double* Gamma = nullptr;   // K x K (of the mode being solved)
   double* L = nullptr;       // 2 K x K: Γ^(-1) or Γ^†, then Jacobi scratch
   int* lmode = nullptr;
-  double* gpart = nullptr;   // per-CTA partial Grams (solve_row_blocks(max s) x K x K)
+  double* gram_scratch = nullptr;   // Gram split partials + per-tile Σ Γ∘S partials
+  unsigned int* gram_counters = nullptr;
   cudaStream_t st2 = nullptr;           // side stream: Γ^(n) inverse overlapped with M^(n)
   cudaEvent_t ev_S = nullptr, ev_P = nullptr;
   int prefetched = -1;                  // mode whose Γ inverse is issued on st2
-  double* rowstat = nullptr; // max local rows x 3
+  double* rowstat = nullptr; // max local rows x 4
   double* stats = nullptr;   // N x 3 norms, then fitness terms [2], then ||X||² [1]
   double* Fpad = nullptr;    // max s x 128
   double* ops[CPPP_MAX_ORDER][CPPP_MAX_ORDER] = {};   // i<j: [x_i][x_j][k]
@@ -197,15 +199,17 @@ struct Prof {
   cppp_ctx* c;
   int cls;
   double flops, bytes;
+  cudaStream_t st;
   cudaEvent_t a = nullptr;
-  Prof(cppp_ctx* c_, int cls_, double f, double b) : c(c_), cls(cls_), flops(f), bytes(b) {
+  Prof(cppp_ctx* c_, int cls_, double f, double b, cudaStream_t s = nullptr)
+      : c(c_), cls(cls_), flops(f), bytes(b), st(s ? s : c_->st) {
     if (!c->dry && (c->flags & CPPP_FLAG_PROFILE)) {
       if (c->capturing) {   // graph-owned event, recorded by an event-record node on every replay
         cudaEventCreate(&a);
-        cudaEventRecordWithFlags(a, c->st, cudaEventRecordExternal);
+        cudaEventRecordWithFlags(a, st, cudaEventRecordExternal);
       } else {
         a = get_event(c);
-        cudaEventRecord(a, c->st);
+        cudaEventRecord(a, st);
       }
     }
   }
@@ -214,20 +218,32 @@ struct Prof {
     if (c->capturing) {
       cudaEvent_t b;
       cudaEventCreate(&b);
-      cudaEventRecordWithFlags(b, c->st, cudaEventRecordExternal);
+      cudaEventRecordWithFlags(b, st, cudaEventRecordExternal);
       c->capture_prof.push_back({cls, a, b, flops, bytes});
     } else {
       cudaEvent_t b = get_event(c);
-      cudaEventRecord(b, c->st);
+      cudaEventRecord(b, st);
       c->pending.push_back({cls, a, b, flops, bytes});
     }
   }
 };
+// CPPP_TRACE=1 (debugging aid): every profiled scope of a sweep is printed to stderr as
+// "trace <class> <start us> <end us>" relative to the sweep's first event.
+void prof_trace(cppp_ctx* c, const char* tag, cudaEvent_t a, cudaEvent_t b, int cls) {
+  static const bool on = getenv("CPPP_TRACE") != nullptr;
+  if (!on) return;
+  float t0 = 0.f, t1 = 0.f;
+  cudaEventElapsedTime(&t0, c->ev_a, a);
+  cudaEventElapsedTime(&t1, c->ev_a, b);
+  fprintf(stderr, "trace %s %d %.1f %.1f\n", tag, cls, t0 * 1e3f, t1 * 1e3f);
+}
+
 void prof_collect(cppp_ctx* c) {
   for (auto& p : c->pending_graph) {
     float ms = 0.f;
     cudaEventSynchronize(p.b);
     cudaEventElapsedTime(&ms, p.a, p.b);
+    prof_trace(c, "g", p.a, p.b, p.cls);
     auto& k = c->kstat[p.cls];
     k.launches += 1;
     k.total_ms += ms;
@@ -240,6 +256,7 @@ void prof_collect(cppp_ctx* c) {
     float ms = 0.f;
     cudaEventSynchronize(p.b);
     cudaEventElapsedTime(&ms, p.a, p.b);
+    prof_trace(c, "e", p.a, p.b, p.cls);
     auto& k = c->kstat[p.cls];
     k.launches += 1;
     k.total_ms += ms;
@@ -319,8 +336,12 @@ cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, doubl
 cppp_status prefetch_inverse(cppp_ctx* c, int n) {
   if (c->dry || c->prefetched == n) return CPPP_OK;
   CUCHK(c, cudaStreamWaitEvent(c->st2, c->ev_S, 0));
-  CUCHK(c, launch_gamma_factor(c->S_all, c->N, n, c->K, c->Gamma, c->L, c->lmode, c->L + c->K * c->K,
-                               c->st2));
+  {   // (the scope closes before ev_P: every side-stream node must be joined)
+    Prof p(c, CPPP_K_FACTOR, (double)c->K * c->K * c->K / 3.0, 8.0 * c->K * c->K * c->N, c->st2);
+    CUCHK(c, launch_gamma_factor(c->S_all, c->N, n, c->K, c->Gamma, c->L, c->lmode,
+                                 c->L + (int64_t)solve_ld(c->K) * solve_ld(c->K),
+                                 c->st2));
+  }
   CUCHK(c, cudaEventRecord(c->ev_P, c->st2));
   c->prefetched = n;
   return CPPP_OK;
@@ -347,18 +368,17 @@ cppp_status finish_mode(cppp_ctx* c, int n, const double* Mn, bool pp_phase) {
     double* An = c->A[n] + off * K;
     const double* ref = pp_phase ? (c->Ap[n] + off * K) : An;
     CUCHK(c, launch_solve_rows(Mn, An, ref, c->dA[n] + off * K, rows, K, c->Gamma, c->L, c->lmode,
-                               c->rowstat, c->gpart, c->st));
-    CUCHK(c, launch_gram_reduce(c->gpart, solve_row_blocks(rows), K, c->S_all + (int64_t)n * K * K,
-                                c->rowstat, rows, c->stats + 3 * n, c->st));
+                               c->rowstat, c->st));
+    // S^(n), the norms and (last mode) the fitness terms in one kernel; Γ^(n) is still in place
+    // (the next factorization starts after ev_S below)
+    const bool last = (n == c->N - 1);
+    CUCHK(c, launch_gram(An, rows, K, c->S_all + (int64_t)n * K * K, c->rowstat, c->stats + 3 * n,
+                         last ? c->Gamma : nullptr, last ? c->stats + 3 * c->N : nullptr,
+                         c->gram_scratch, c->gram_counters, c->st));
   }
   if (n == c->q) {
     STCHK(allreduce(c, c->S_all + (int64_t)n * K * K, (size_t)K * K));
     STCHK(allreduce(c, c->stats + 3 * n, 3));
-  }
-  if (n == c->N - 1) {
-    Prof p(c, CPPP_K_OTHER, 0, 0);
-    CUCHK(c, launch_fitness_terms(Mn, c->A[n] + off * K, rows, K, c->Gamma,
-                                  c->S_all + (int64_t)n * K * K, c->stats + 3 * c->N, c->st));
   }
   CUCHK(c, cudaEventRecord(c->ev_S, c->st));
   // the next mode's factorization starts right away on the side stream; inside a captured sweep
@@ -768,11 +788,11 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
     oT[n] = take(sizeof(double) * c->dl[n] * K);
   }
   size_t oS = take(sizeof(double) * N * K * K);
-  size_t oG = take(sizeof(double) * K * K);
-  size_t oL = take(sizeof(double) * 2 * K * K);
-  size_t oGp = take(sizeof(double) * (size_t)solve_row_blocks(smax) * K * K);
+  size_t oG = take(sizeof(double) * solve_ld(K) * solve_ld(K));
+  size_t oL = take(sizeof(double) * (solve_ld(K) * solve_ld(K) + K * K));   // packed factor + Jacobi V
+  size_t oGp = take(sizeof(double) * gram_scratch_doubles() + 64 * sizeof(unsigned int));
   size_t oLm = take(sizeof(int) * 4);
-  size_t oRow = take(sizeof(double) * smax * 3);
+  size_t oRow = take(sizeof(double) * smax * 4);
   size_t oStats = take(sizeof(double) * (3 * N + 8));
   size_t oFpad = take(sizeof(double) * (smax * 128 + 32));   // + TTM tile counter
   size_t oOps[CPPP_MAX_ORDER][CPPP_MAX_ORDER];
@@ -809,7 +829,8 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   c->S_all = reinterpret_cast<double*>(b + oS);
   c->Gamma = reinterpret_cast<double*>(b + oG);
   c->L = reinterpret_cast<double*>(b + oL);
-  c->gpart = reinterpret_cast<double*>(b + oGp);
+  c->gram_scratch = reinterpret_cast<double*>(b + oGp);
+  c->gram_counters = reinterpret_cast<unsigned int*>(b + oGp + sizeof(double) * gram_scratch_doubles());
   c->lmode = reinterpret_cast<int*>(b + oLm);
   c->rowstat = reinterpret_cast<double*>(b + oRow);
   c->stats = reinterpret_cast<double*>(b + oStats);
@@ -1048,7 +1069,8 @@ cppp_status cp_set_factors(cppp_ctx* c, const double* const* A) {
   for (int n = 0; n < c->N; ++n) {
     const int64_t off = (n == c->q) ? c->qoff : 0;
     CUCHK(c, launch_gram(c->A[n] + off * c->K, c->dl[n], c->K, c->S_all + (int64_t)n * c->K * c->K,
-                         c->gpart, c->st));
+                         nullptr, nullptr, nullptr, nullptr, c->gram_scratch, c->gram_counters,
+                         c->st));
     if (n == c->q) STCHK(allreduce(c, c->S_all + (int64_t)n * c->K * c->K, (size_t)c->K * c->K));
     CUCHK(c, cudaMemsetAsync(c->dA[n], 0, sizeof(double) * c->s[n] * c->K, c->st));
   }
@@ -1073,7 +1095,8 @@ cppp_status cp_update_factors(cppp_ctx* c, const double* const* A) {
     STCHK(copy_in(c, c->A[n], A[n], (size_t)c->s[n] * c->K));
     const int64_t off = (n == c->q) ? c->qoff : 0;
     CUCHK(c, launch_gram(c->A[n] + off * c->K, c->dl[n], c->K, c->S_all + (int64_t)n * c->K * c->K,
-                         c->gpart, c->st));
+                         nullptr, nullptr, nullptr, nullptr, c->gram_scratch, c->gram_counters,
+                         c->st));
     if (n == c->q) STCHK(allreduce(c, c->S_all + (int64_t)n * c->K * c->K, (size_t)c->K * c->K));
   }
   CUCHK(c, cudaEventRecord(c->ev_S, c->st));

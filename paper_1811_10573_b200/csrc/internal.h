@@ -84,29 +84,29 @@ size_t pp_update_scratch_doubles(int64_t ny, int K, int64_t max_nx);
 
 
 // ---------------------------------------------------------------- small dense ops (K <= 128)
-// Γ^(n) = Hadamard of S[m], m != n -> Gamma; Cholesky factor (L13 pivot rule) -> L
-// with *mode = 0, else the eigen pseudo-inverse -> L with *mode = 1.  One CTA per kernel.
+// Γ^(n) = Hadamard of S[m], m != n -> Gamma (ld x ld, ld = solve_ld(K), zero padding);
+// Cholesky factor (L13 pivot rule) packed into Tp (ld x ld: diag 1/L[j][j], upper = Lᵀ,
+// lower = L, zero padding with a unit diagonal) with
+// *mode = 0, else the eigen pseudo-inverse P -> Tp with *mode = 1.  One CTA per kernel.
 // Vscratch: K*K doubles (Jacobi V).
+int solve_ld(int K);
 cudaError_t launch_gamma_factor(const double* S_all /* N x K x K */, int N, int n, int K,
-                                double* Gamma, double* L, int* mode, double* Vscratch,
+                                double* Gamma, double* Tp, int* mode, double* Vscratch,
                                 cudaStream_t st);
-// Row solves: A_new = M Γ^† (substitution with L, or M P) ; G = (A_old - A_new) Γ ;
-// dA = A_new - ref ; per-row norms -> rowstat (rows x 3: ||a_new||², ||dA||², ||g||²);
-// per-CTA partial Grams -> gpart (solve_row_blocks x K*K).  A is updated in place; ref may alias A.
-int solve_row_blocks(int64_t rows);
+// Row solves: A_new = M Γ^† (substitution with the packed factor, or M P) ; G = (A_old - A_new) Γ ;
+// dA = A_new - ref ; per-row statistics -> rowstat (rows x 4: ‖a_new‖², ‖dA‖², ‖g‖², Σ m∘a_new).
+// A is updated in place; ref may alias A.
 cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, double* dA,
-                              int64_t rows, int K, const double* Gamma, const double* L,
-                              const int* mode, double* rowstat, double* gpart, cudaStream_t st);
-// S = Σ_b gpart[b]; if rowstat: nrm[0..2] = Σ_rows rowstat (fixed order)
-cudaError_t launch_gram_reduce(const double* gpart, int nb, int K, double* S,
-                               const double* rowstat, int64_t rows, double* nrm, cudaStream_t st);
-// S = AᵀA (partial Grams over 16-row blocks, then the reduction)
-cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, double* gpart,
-                        cudaStream_t st);
-// fitness pieces: out[0] = Σ M∘A (inner), out[1] = Σ Gamma∘S (model)
-cudaError_t launch_fitness_terms(const double* M, const double* A, int64_t rows, int K,
-                                 const double* Gamma, const double* S, double* out,
-                                 cudaStream_t st);
+                              int64_t rows, int K, const double* Gamma, const double* Tp,
+                              const int* mode, double* rowstat, cudaStream_t st);
+// S = AᵀA (fixed order).  With nrm: nrm[0..2] = Σ_rows rowstat[.][0..2]; with Gamma_model also
+// fit[0] = Σ_rows rowstat[.][3] and fit[1] = Σ Γ∘S.  scratch: gram_scratch_doubles() doubles;
+// counters: 64 zeroed device words the kernel leaves zeroed (K <= 128).
+int gram_tiles(int K);
+size_t gram_scratch_doubles();
+cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, const double* rowstat,
+                        double* nrm, const double* Gamma_model, double* fit, double* scratch,
+                        unsigned int* counters, cudaStream_t st);
 // ||x||² with a fixed reduction tree: partial[nblk] then out[0]
 cudaError_t launch_sqnorm(const double* x, int64_t n, double* partial, int nblk, double* out,
                           cudaStream_t st);

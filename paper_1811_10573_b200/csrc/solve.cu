@@ -7,13 +7,22 @@
 // plus ‖A‖², ‖dA‖², ‖G‖² per mode (the ε_pp test L7 and the stop metric) and the fitness
 // expansion terms.  K <= 128.  Every reduction has a fixed order (deterministic).
 //
-// Latency design: Γ^(n) only depends on the Grams, so its inverse is computed by
-// ONE CTA (register-resident Gauss-Jordan, one barrier per pivot) on a side stream while the main
-// stream computes M^(n); the main stream then runs one row kernel (A_new = M P, G, dA, norms and
-// a per-block partial Gram, all from shared memory) and one tiny reduction.
+// Latency design: Γ^(n) only depends on the Grams, so its Cholesky factor is
+// computed by ONE CTA (register-resident, one barrier per pivot) on a side stream while the main
+// stream computes M^(n); the main stream then runs one row kernel (substitution solves, G, dA,
+// per-row statistics; one warp per row) and one Gram kernel (S^(n), the fixed-order sums).
 #include "internal.h"
 
 namespace cppp {
+#ifdef CPPP_PROBE_CYCLES   // tools/probe_solve only: per-phase clock64 deltas of CTA 0, thread 0
+__device__ long long g_probe_cycles[16];
+#define PROBE_T0() const long long probe_t0_ = clock64()
+#define PROBE_T(slot) \
+  if (threadIdx.x == 0 && blockIdx.x == 0) g_probe_cycles[slot] = clock64() - probe_t0_
+#else
+#define PROBE_T0() (void)0
+#define PROBE_T(slot) (void)0
+#endif
 namespace {
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -43,137 +52,170 @@ __device__ double block_sum(double v, double* sh) {
 
 constexpr double PIVOT_TAU = 1e-12;  // L13 / S:201
 constexpr double PINV_TAU = 1e-12;
-constexpr int GI_THREADS = 512;
-constexpr int GI_MAXE = 32;          // K*K <= 16384 = 32 * 512 register-resident elements
+constexpr int GF_THREADS = 640;      // factorization: 20 warps = the lower-triangle 16x32 blocks
+constexpr int GP_THREADS = 512;      // Jacobi fallback
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 
 // ---------------------------------------------------------------- Γ and its Cholesky factor
-// Right-looking Cholesky Γ = L Lᵀ with the L13 pivot rule (accept iff every pivot d_j >
-// τ·max diag Γ), the same factorization the oracle uses.  Thread (l = tid % 128, rg = tid / 128)
-// keeps column l, rows 32 rg + v (v < 32) in registers.  Column j+1 is published (unscaled) at the
-// end of step j, so step j+1 reads its pivot and scales on the fly: one barrier per pivot.
-__global__ void __launch_bounds__(GI_THREADS, 1)
+// Right-looking Cholesky Γ = L Lᵀ in unscaled (LDLᵀ) form with the L13 pivot rule (accept iff
+// every pivot d_j > τ·max diag Γ), the factorization the oracle uses.  Step j updates
+// W[i][l] -= W[i][j] · (W[l][j] / d_j) for i, l > j, then L = W diag(d)^(-1/2).
+//
+// Layout: a 128 x 128 Γ is cut into 16-row x 32-column blocks; the 20 blocks that touch the
+// lower triangle get one warp each, and thread (block, lane) keeps W[16 rg + v][32 cg + lane],
+// v < 16, in registers.  Blocks are dealt to warps in order of how long they stay active (a
+// block retires once j passes its last row or column), so the four SM sub-partitions stay
+// balanced while the trailing matrix shrinks; a retired warp skips the step.  Column j+1 and
+// 1/d_(j+1) are published through a double-buffered shared column: one barrier per pivot.
+//
+// Γ is stored with row pitch ldt (K rounded up to 8; zero padding).  Output Tp (ldt x ldt, the
+// row solves' packed factor; zero padding with a unit diagonal past K):
+// Tp[j][j] = 1 / L[j][j];
+// Tp[j][c] = L[c][j] for c > j (column j of L: the forward substitution reads row j);
+// Tp[j][c] = L[j][c] for c < j (row j of L: the back substitution reads row j).
+// warp -> lower block (rg | cg << 4), sorted by decreasing lifetime min(16 rg + 15, 32 cg + 31)
+// (ties: ascending cg, then rg), dealt round-robin over the SM sub-partitions (wid % 4)
+__constant__ unsigned char kCholBlock[20] = {
+    7 | 3 << 4, 6 | 3 << 4, 5 | 2 << 4, 6 | 2 << 4, 7 | 2 << 4, 4 | 2 << 4, 3 | 1 << 4,
+    4 | 1 << 4, 5 | 1 << 4, 6 | 1 << 4, 7 | 1 << 4, 2 | 1 << 4, 1,          2,
+    3,          4,          5,          6,          7,          0};
+
+__global__ void __launch_bounds__(GF_THREADS, 1)
     gamma_chol_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
-                      double* Lout, int* mode) {
+                      double* Tp, int ldt, int* mode) {
+  PROBE_T0();
   __shared__ __align__(16) double colb[2][128];
-  __shared__ double piv_s[2][2];    // [buffer][-, 1/pivot]
-  __shared__ int bad_s[2];
+  __shared__ double rdv[2];
+  __shared__ int bad_s;
+  __shared__ double dpiv[128];
   __shared__ double sh[32];
-  const int tid = threadIdx.x, KK = K * K;
-  const int lane = tid & 31, wid = tid >> 5;
-  // column l = 4 lane + (warp mod 4): every SM sub-partition owns every 4th column, so the
-  // shrinking trailing matrix stays balanced; rg = warp / 4 selects rows 32 rg .. 32 rg + 31.
-  const int l = 4 * lane + (wid & 3), rg = wid >> 2;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int rg = kCholBlock[wid] & 15, cg = kCholBlock[wid] >> 4;
+  const int r0 = 16 * rg, l = 32 * cg + lane;
   const bool col_ok = l < K;
-  double w[GI_MAXE];
+  const bool lowerw = (r0 < K) && (32 * cg < K);   // every allocated block touches the lower part
+  const bool has_diag = col_ok && l >= r0 && l < r0 + 16;   // this thread holds W[l][l]
+  double w[16];
 #pragma unroll
-  for (int v = 0; v < GI_MAXE; ++v) w[v] = 1.0;   // 1.0 * S^(first) is exactly S^(first)
-  const int rows_here = min(GI_MAXE, max(0, K - 32 * rg));
+  for (int v = 0; v < 16; ++v) w[v] = 1.0;   // 1.0 * S^(first) is exactly S^(first)
+  double diag = 1.0;                          // a second copy of W[l][l] (same operations)
+  const int rows_here = min(16, max(0, K - r0));
   if (col_ok) {
     for (int m = 0; m < N; ++m) {
       if (m == n) continue;
-      const double* Sm = S_all + (int64_t)m * KK + (32 * rg) * K + l;
+      const double* Sm = S_all + (int64_t)m * K * K + r0 * K + l;
 #pragma unroll
-      for (int v = 0; v < GI_MAXE; ++v)
+      for (int v = 0; v < 16; ++v)
         if (v < rows_here) w[v] *= __ldg(Sm + v * K);
+      diag *= __ldg(S_all + (int64_t)m * K * K + l * K + l);
     }
   }
-  double dmax = 0.0;
 #pragma unroll
-  for (int v = 0; v < GI_MAXE; ++v) {
-    const int i = 32 * rg + v;
-    if (!(col_ok && v < rows_here)) w[v] = 0.0;
-    else {
-      Gamma[i * K + l] = w[v];
-      if (i == l) dmax = fmax(dmax, w[v]);
+  for (int v = 0; v < 16; ++v) {
+    const int i = r0 + v;
+    if (!(col_ok && v < rows_here)) {
+      w[v] = 0.0;
+    } else {
+      Gamma[i * ldt + l] = w[v];   // Γ is exactly symmetric (Grams are written mirrored):
+      Gamma[l * ldt + i] = w[v];   // the lower blocks also fill the upper triangle
     }
   }
-  for (int i = tid; i < 2 * 128; i += GI_THREADS) (&colb[0][0])[i] = 0.0;
+  double dmax = has_diag ? diag : 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   if (lane == 0) sh[wid] = dmax;
+  if (tid == 0) bad_s = 0;
   __syncthreads();
   if (tid == 0) {
-    double m = 0.0;
-    for (int i = 0; i < GI_THREADS / 32; ++i) m = fmax(m, sh[i]);
-    sh[0] = m;
+    double mx = 0.0;
+    for (int i = 0; i < GF_THREADS / 32; ++i) mx = fmax(mx, sh[i]);
+    sh[0] = mx;
   }
   __syncthreads();
   const double thresh = PIVOT_TAU * sh[0];
-  // Unscaled (LDLᵀ-form) elimination: column j keeps W[i][j] with d_j = W[j][j] the pivot, the
-  // trailing update is W[i][l] -= W[i][j] W[l][j] / d_j, and L = W diag(d)^(-1/2) is applied at
-  // the end, so only one reciprocal (no sqrt) sits on the per-pivot critical path.
-  __shared__ double dpiv[128];
-  if (l == 0) {
+  if (tid < ldt - K) Tp[(K + tid) * ldt + K + tid] = 1.0;   // unit diagonal of the padding
+  if (l == 0) {   // publish column 0 and its pivot
 #pragma unroll
-    for (int v = 0; v < GI_MAXE; ++v) colb[0][32 * rg + v] = w[v];
+    for (int v = 0; v < 16; ++v) colb[0][r0 + v] = w[v];
     if (rg == 0) {
-      const double p = w[0];
-      bad_s[0] = !(p > thresh);
-      dpiv[0] = p;
-      piv_s[0][1] = __drcp_rn(p);
+      if (!(diag > thresh)) bad_s = 1;
+      dpiv[0] = diag;
+      rdv[0] = __drcp_rn(diag);
     }
   }
   __syncthreads();
-  bool ok = true;
+  PROBE_T(0);
+  // One pivot per step.  The diagonal owner of column j+1 updates its copy of W[j+1][j+1]
+  // first, so the reciprocal overlaps the rest of the update.  A failed pivot test is recorded
+  // (sticky) and acted on after the loop.
   for (int j = 0; j < K; ++j) {
     const int b = j & 1;
-    if (bad_s[b]) {
-      ok = false;
-      break;
-    }
-    if (col_ok && l > j && 32 * rg + 31 > j) {
-      const double cl = colb[b][l] * piv_s[b][1];
+    if (lowerw && r0 + 15 > j && 32 * cg + 31 > j && l > j) {
+      const double cl = colb[b][l] * rdv[b];
+      if (has_diag) {
+        diag = fma(-colb[b][l], cl, diag);
+        if (l == j + 1) {
+          if (!(diag > thresh)) bad_s = 1;
+          dpiv[j + 1] = diag;
+          rdv[b ^ 1] = __drcp_rn(diag);
+        }
+      }
 #pragma unroll
-      for (int v = 0; v < GI_MAXE; v += 2) {
-        const double2 cc = *reinterpret_cast<const double2*>(&colb[b][32 * rg + v]);
+      for (int v = 0; v < 16; v += 2) {
+        const double2 cc = *reinterpret_cast<const double2*>(&colb[b][r0 + v]);
         w[v] = fma(-cc.x, cl, w[v]);
         w[v + 1] = fma(-cc.y, cl, w[v + 1]);
       }
-    }
-    if (l == j + 1) {   // publish the next column (and, from its diagonal owner, the pivot)
+      if (l == j + 1) {   // publish column j+1
 #pragma unroll
-      for (int v = 0; v < GI_MAXE; ++v) colb[b ^ 1][32 * rg + v] = w[v];
-      if (rg == ((j + 1) >> 5)) {
-        const double p = colb[b ^ 1][j + 1];   // this thread just wrote it
-        bad_s[b ^ 1] = !(p > thresh);
-        dpiv[j + 1] = p;
-        piv_s[b ^ 1][1] = __drcp_rn(p);
+        for (int v = 0; v < 16; v += 2)
+          *reinterpret_cast<double2*>(&colb[b ^ 1][r0 + v]) = make_double2(w[v], w[v + 1]);
       }
     }
     __syncthreads();
   }
-  if (ok) {
+  if (!bad_s) {
     if (col_ok) {
       const double d = dpiv[l];
       const double r = sqrt(d);
       const double ri = 1.0 / r;
 #pragma unroll
-      for (int v = 0; v < GI_MAXE; ++v) {
-        const int i = 32 * rg + v;
-        if (i < K) Lout[i * K + l] = (i > l) ? w[v] * ri : (i == l ? r : 0.0);
+      for (int v = 0; v < 16; ++v) {
+        const int i = r0 + v;
+        if (i < K && i > l) {
+          const double x = w[v] * ri;
+          Tp[i * ldt + l] = x;   // row i of L
+          Tp[l * ldt + i] = x;   // column l of L
+        } else if (i == l) {
+          Tp[l * ldt + l] = 1.0 / r;
+        }
       }
     }
     if (tid == 0) *mode = 0;
   } else if (tid == 0) {
     *mode = 1;   // gamma_pinv_kernel takes over
   }
+  PROBE_T(1);
 }
 
 // Eigen pseudo-inverse fallback (L13): runs after gamma_chol_kernel and exits at once unless
-// the Gauss-Jordan pivot test failed.  Two-sided cyclic Jacobi, Brent-Luk parallel ordering.
-__global__ void __launch_bounds__(GI_THREADS, 1)
-    gamma_pinv_kernel(int K, const double* __restrict__ Gamma, double* Pout, const int* mode,
-                      double* Vscratch) {
+// the pivot test failed.  Two-sided cyclic Jacobi, Brent-Luk parallel ordering; the
+// pseudo-inverse P goes to Tp (pitch ldt).
+__global__ void __launch_bounds__(GP_THREADS, 1)
+    gamma_pinv_kernel(int K, const double* __restrict__ Gamma, double* Pout, int ldt,
+                      const int* mode, double* Vscratch) {
   if (*mode == 0) return;
   extern __shared__ double W[];  // K x (K+1)
   __shared__ double sh[32];
   const int tid = threadIdx.x, KK = K * K;
-  // ---- eigen pseudo-inverse: two-sided cyclic Jacobi on W (from Γ), V in global scratch
   const int P = K + 1;
-  const int nt = GI_THREADS;
+  const int nt = GP_THREADS;
   for (int e = tid; e < KK; e += nt) {
     const int i = e / K, j = e - i * K;
-    W[i * P + j] = Gamma[e];
+    W[i * P + j] = Gamma[i * ldt + j];
     Vscratch[e] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
@@ -266,59 +308,74 @@ __global__ void __launch_bounds__(GI_THREADS, 1)
     const int i = e / K, j = e - i * K;
     double v = 0.0;
     for (int l = 0; l < K; ++l) v += Vscratch[i * K + l] * lam[l] * Vscratch[j * K + l];
-    Pout[e] = v;
+    Pout[i * ldt + j] = v;
   }
 }
 
-// ---------------------------------------------------------------- row solves + partial Gram
-// One warp per row (16 rows per CTA).  Cholesky path (mode 0): forward then back substitution
-// with L staged in shared memory (pitch K+1: column reads are conflict-free), as the oracle does;
-// pinv path (mode 1): a = m P.  Then G = (a_old - a_new) Γ with Γ staged, dA, row norms and the
-// CTA's partial Gram.  Lane c owns columns c + 32u.
-constexpr int SR_WARPS = 8;
+// ---------------------------------------------------------------- row solves
+// One warp per row, SR_WARPS rows per CTA (one CTA per SM: every row of a B200-sized mode runs
+// at once).  The packed factor Tp (and Γ when it fits) arrive in shared memory by one bulk copy
+// (cp.async.bulk + mbarrier) while the warps load their rows.  Lane c owns columns c + 32u.
+//   Cholesky path (mode 0): forward L z = m, then back Lᵀ a = z, right-looking, one pivot per
+//   step: z_j is broadcast by shuffle and every later column takes its fma (the oracle's
+//   substitution, P:395 via L13).  pinv path (mode 1): a = m P.
+//   Then G = (a_old - a_new) Γ, dA = a_new - ref, and the per-row statistics
+//   rowstat[y] = (‖a_new‖², ‖dA‖², ‖g‖², Σ m∘a_new) for the norms and the fitness.
+constexpr int SR_WARPS = 4;
 
-// stage a K x K row-major matrix into shared memory with row pitch `pitch`: 8-byte cp.async
-// (LDGSTS) for every element, all in flight, no register round trip; the caller syncs.
-__device__ __forceinline__ void stage_matrix(double* dst, int pitch, const double* __restrict__ src,
-                                             int K) {
-  const int KK = K * K;
-  int i = threadIdx.x / K, j = threadIdx.x - (threadIdx.x / K) * K;
-  const int di = blockDim.x / K, dj = blockDim.x - di * K;
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + i * pitch + j));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src + e) : "memory");
-    i += di;
-    j += dj;
-    if (j >= K) {
-      j -= K;
-      ++i;
-    }
+__device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+// one bulk copy global -> shared, completing on `bar` (the caller arms it with bar_expect)
+__device__ __forceinline__ void bulk_to_smem(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
   }
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
-__device__ __forceinline__ double pick4(const double (&m)[4], int slot) {
-  return slot == 0 ? m[0] : slot == 1 ? m[1] : slot == 2 ? m[2] : m[3];
-}
-
-__global__ void __launch_bounds__(SR_WARPS * 32)
+__global__ void __launch_bounds__(SR_WARPS * 32, 1)
     solve_rows_kernel(const double* __restrict__ M, double* A, const double* ref, double* dA,
                       int64_t rows, int K, const double* __restrict__ Gamma,
-                      const double* __restrict__ Lm, const int* __restrict__ mode_p,
-                      double* __restrict__ rowstat, double* __restrict__ gpart) {
-  extern __shared__ double sm[];
-  const int KK = K * K;
-  const int P = K + 1;
-  double* Ws = sm;                         // K*(K+1)
-  double* dinv = Ws + K * P;               // K
-  double* As = dinv + K;                   // SR_WARPS*K
-  double* Ds = As + SR_WARPS * K;          // SR_WARPS*K
+                      const double* __restrict__ Tp, int ldt, int gamma_in_smem,
+                      const int* __restrict__ mode_p, double* __restrict__ rowstat) {
+  PROBE_T0();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t bar;
+  double* Ts = sm + 128;                                // ldt x ldt (+ 128 pad on each side)
+  double* Gs = Ts + (int64_t)ldt * ldt + 256;           // ldt x ldt (+ 128 pad), if staged
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t tbytes = static_cast<uint32_t>(ldt) * ldt * 8;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bar_expect(&bar, gamma_in_smem ? 2 * tbytes : tbytes);
+    bulk_to_smem(Ts, Tp, tbytes, &bar);
+    if (gamma_in_smem) bulk_to_smem(Gs, Gamma, tbytes, &bar);
+  }
   const int64_t y = blockIdx.x * (int64_t)SR_WARPS + w;
   const bool valid = y < rows;
-  const int mode = *mode_p;
-  stage_matrix(Ws, mode == 0 ? P : K, Lm, K);
-  double m[4], aold[4], rf[4];
+  double m[4], m0[4], aold[4], rf[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int c = lane + 32 * u;
@@ -326,180 +383,285 @@ __global__ void __launch_bounds__(SR_WARPS * 32)
     aold[u] = in ? A[y * K + c] : 0.0;
     rf[u] = in ? ref[y * K + c] : 0.0;
     m[u] = in ? M[y * K + c] : 0.0;
+    m0[u] = m[u];
   }
-  __syncthreads();
+  const int mode = *mode_p;
+  bar_wait(&bar, 0);
+  PROBE_T(2);
+  // Tp / Γ are ldt x ldt (ldt = K rounded up to 8) with zero padding and a unit diagonal past K,
+  // so every loop below runs ldt (a multiple of 8) steps: 8-step bodies with compile-time trip
+  // counts; the padded steps change nothing (their m and factor entries are zero).
+  const int kp = ldt;
   if (mode == 0) {
-    for (int j = threadIdx.x; j < K; j += blockDim.x) dinv[j] = 1.0 / Ws[j * P + j];
-    __syncthreads();
-    // forward L z = m, blocked by 32 columns: in-block substitution (lane = column), then a
-    // dependency-free update of the later column blocks
+    // forward: L z = m.  Step j reads row j of Tp (1/L[j][j] and column j of L); the row of
+    // step j+1 is loaded during step j, and the next shuffle reads this step's fma result
+    // directly (lane j+1 > j always takes it), so the chain per pivot is shfl -> mul -> fma.
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      if (32 * b >= K) break;
-      const int c = 32 * b + lane;
-      for (int jj = 0; jj < 32; ++jj) {
-        const int j = 32 * b + jj;
-        if (j >= K) break;
-        const double zj = __shfl_sync(0xffffffffu, m[b], jj) * dinv[j];
-        if (lane == jj) m[b] = zj;
-        else if (lane > jj && c < K) m[b] = fma(-Ws[c * P + j], zj, m[b]);
-      }
+    for (int u = 0; u < 4; ++u) {
+      if (32 * u >= kp) break;
+      const int nb = min(32, kp - 32 * u);
+      const double* row = Ts + (32 * u) * ldt;
+      double dn = row[32 * u], tn[4];
 #pragma unroll
-      for (int u = b + 1; u < 4; ++u) {
-        const int cu = lane + 32 * u;
-        if (32 * u >= K) break;
-        double acc = m[u];
-        for (int jj = 0; jj < 32 && 32 * b + jj < K; ++jj) {
-          const double zj = __shfl_sync(0xffffffffu, m[b], jj);
-          if (cu < K) acc = fma(-Ws[cu * P + 32 * b + jj], zj, acc);
+      for (int v = u; v < 4; ++v) tn[v] = row[32 * v + lane];
+      double src = m[u];
+      for (int j8 = 0; j8 < nb; j8 += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int jj = j8 + k;
+          const double dj = dn;
+          double tj[4];
+#pragma unroll
+          for (int v = u; v < 4; ++v) tj[v] = tn[v];
+          row += ldt;   // prefetch the next row (one row past the end is inside the pad)
+          dn = row[32 * u + jj + 1];
+#pragma unroll
+          for (int v = u; v < 4; ++v) tn[v] = row[32 * v + lane];
+          const double zj = __shfl_sync(0xffffffffu, src, jj) * dj;
+          const double t = fma(-tj[u], zj, m[u]);
+          src = t;
+          m[u] = lane == jj ? zj : (lane > jj ? t : m[u]);
+#pragma unroll
+          for (int v = u + 1; v < 4; ++v) m[v] = fma(-tj[v], zj, m[v]);
         }
-        m[u] = acc;
       }
     }
-    // back Lᵀ a = z, blocks in reverse
+    // back: Lᵀ a = z (row j of Tp holds row j of L), same pipeline, pivots descending
 #pragma unroll
-    for (int b = 3; b >= 0; --b) {
-      if (32 * b >= K) continue;
-      const int c = 32 * b + lane;
-      const int jtop = min(31, K - 1 - 32 * b);
-      for (int jj = jtop; jj >= 0; --jj) {
-        const int j = 32 * b + jj;
-        const double aj = __shfl_sync(0xffffffffu, m[b], jj) * dinv[j];
-        if (lane == jj) m[b] = aj;
-        else if (lane < jj) m[b] = fma(-Ws[j * P + c], aj, m[b]);
-      }
+    for (int u = 3; u >= 0; --u) {
+      if (32 * u >= kp) continue;
+      const int nb = min(32, kp - 32 * u);
+      const double* row = Ts + (32 * u + nb - 1) * ldt;
+      double dn = row[32 * u + nb - 1], tn[4];
 #pragma unroll
-      for (int u = 0; u < b; ++u) {
-        const int cu = lane + 32 * u;
-        double acc = m[u];
-        for (int jj = 0; jj <= jtop; ++jj) {
-          const double aj = __shfl_sync(0xffffffffu, m[b], jj);
-          acc = fma(-Ws[(32 * b + jj) * P + cu], aj, acc);
+      for (int v = 0; v <= u; ++v) tn[v] = row[32 * v + lane];
+      double src = m[u];
+      for (int j8 = nb - 8; j8 >= 0; j8 -= 8) {
+#pragma unroll
+        for (int k = 7; k >= 0; --k) {
+          const int jj = j8 + k;
+          const double dj = dn;
+          double tj[4];
+#pragma unroll
+          for (int v = 0; v <= u; ++v) tj[v] = tn[v];
+          row -= ldt;   // (one row before the start is the Γ area or the pad: never used)
+          dn = row[32 * u + jj - 1];
+#pragma unroll
+          for (int v = 0; v <= u; ++v) tn[v] = row[32 * v + lane];
+          const double aj = __shfl_sync(0xffffffffu, src, jj) * dj;
+          const double t = fma(-tj[u], aj, m[u]);
+          src = t;
+          m[u] = lane == jj ? aj : (lane < jj ? t : m[u]);
+#pragma unroll
+          for (int v = 0; v < u; ++v) m[v] = fma(-tj[v], aj, m[v]);
         }
-        m[u] = acc;
       }
     }
   } else {
     double a[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int p = 0; p < K; ++p) {
-      const double mp = __shfl_sync(0xffffffffu, pick4(m, p >> 5), p & 31);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = lane + 32 * u;
-        if (c < K) a[u] = fma(mp, Ws[p * K + c], a[u]);
+    for (int u = 0; u < 4; ++u) {
+      if (32 * u >= kp) break;
+      const int nb = min(32, kp - 32 * u);
+      for (int j8 = 0; j8 < nb; j8 += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int p = 32 * u + j8 + k;
+          const double mp = __shfl_sync(0xffffffffu, m[u], j8 + k);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) a[v] = fma(mp, Ts[p * ldt + 32 * v + lane], a[v]);
+        }
       }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) m[u] = a[u];
   }
-  // m now holds a_new
+  PROBE_T(3);
+  // m now holds a_new (garbage in lanes c >= K)
+  double d[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) d[u] = (lane + 32 * u < K) ? aold[u] - m[u] : 0.0;
+  if (!gamma_in_smem) {   // K > 112: Γ replaces the factor in shared memory
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bar_expect(&bar, tbytes);
+      bulk_to_smem(Ts, Gamma, tbytes, &bar);
+    }
+    bar_wait(&bar, 1);
+  }
+  const double* Gm = gamma_in_smem ? Gs : Ts;
+  double g[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    const int c = lane + 32 * u;
-    if (c < K) {
-      As[w * K + c] = valid ? m[u] : 0.0;
-      Ds[w * K + c] = valid ? aold[u] - m[u] : 0.0;
-    }
-  }
-  __syncthreads();
-  stage_matrix(Ws, K, Gamma, K);
-  __syncthreads();
-  double g[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int p = 0; p < K; ++p) {
-    const double dp = Ds[w * K + p];
-    const double* wr = Ws + p * K;
+    if (32 * u >= kp) break;
+    const int nb = min(32, kp - 32 * u);
+    for (int j8 = 0; j8 < nb; j8 += 8) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int c = lane + 32 * u;
-      if (c < K) g[u] = fma(dp, wr[c], g[u]);
+      for (int k = 0; k < 8; ++k) {
+        const int p = 32 * u + j8 + k;
+        const double dp = __shfl_sync(0xffffffffu, d[u], j8 + k);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) g[v] = fma(dp, Gm[p * ldt + 32 * v + lane], g[v]);
+      }
     }
   }
-  double na = 0.0, nd = 0.0, ng = 0.0;
+  double na = 0.0, nd = 0.0, ng = 0.0, in = 0.0;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int c = lane + 32 * u;
     if (valid && c < K) {
-      const double d = m[u] - rf[u];
+      const double e = m[u] - rf[u];
       A[y * K + c] = m[u];
-      dA[y * K + c] = d;
+      dA[y * K + c] = e;
       na = fma(m[u], m[u], na);
-      nd = fma(d, d, nd);
+      nd = fma(e, e, nd);
       ng = fma(g[u], g[u], ng);
+      in = fma(m0[u], m[u], in);
     }
   }
   na = warp_sum(na);
   nd = warp_sum(nd);
   ng = warp_sum(ng);
-  if (valid && lane == 0) {
-    rowstat[y * 3 + 0] = na;
-    rowstat[y * 3 + 1] = nd;
-    rowstat[y * 3 + 2] = ng;
-  }
-  // partial Gram of this CTA's rows (rows in ascending order), 2 outputs per thread per pass
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    const int k1 = e / K, k2 = e - k1 * K;
-    double s = 0.0;
-#pragma unroll
-    for (int r = 0; r < SR_WARPS; ++r) s = fma(As[r * K + k1], As[r * K + k2], s);
-    gpart[(int64_t)blockIdx.x * KK + e] = s;
-  }
+  in = warp_sum(in);
+  if (valid && lane == 0)
+    *reinterpret_cast<double4*>(rowstat + y * 4) = make_double4(na, nd, ng, in);
+  PROBE_T(4);
 }
 
-// partial Gram only (rows staged in shared memory), same partial layout as solve_rows
-__global__ void __launch_bounds__(SR_WARPS * 32)
-    gram_partial_kernel(const double* __restrict__ A, int64_t rows, int K,
-                        double* __restrict__ gpart) {
-  extern __shared__ double As[];  // SR_WARPS x K
-  const int KK = K * K;
-  const int64_t y0 = blockIdx.x * (int64_t)SR_WARPS;
-  for (int e = threadIdx.x; e < SR_WARPS * K; e += blockDim.x) {
-    const int64_t y = y0 + e / K;
-    As[e] = y < rows ? A[y0 * K + e] : 0.0;
+// ---------------------------------------------------------------- Gram S = AᵀA (+ statistics)
+// CTA (tile pair t, split q): tile pair (ti <= tj) of S, rows [q R/ns, (q+1) R/ns) of A;
+// thread (i, j) owns S[16ti+i][16tj+j] (and its mirror).  The two 16-column strips stream
+// through shared memory GR_ROWS rows at a time: every thread issues its coalesced loads of the
+// next chunk (all in flight) while the current chunk is consumed; rows are stored in pairs so
+// one 16-byte load serves two rows; 4 accumulators (row mod 4) are combined in a fixed order.
+// With ns > 1 the splits leave partial tiles and the last split to finish (per-tile ticket)
+// sums them in split order.  With stats, the last tile to finish (global ticket) sums the
+// per-row statistics in row order and the per-tile Σ Γ∘S partials in tile order
+// (nrm[0..2] = Σ ‖a‖², ‖dA‖², ‖g‖²; fit[0] = Σ M∘A, fit[1] = 1ᵀ(Γ∗S)1).
+// Every sum has a fixed order; the tickets only decide which CTA performs it.
+constexpr int GR_ROWS = 128;
+constexpr int GR_THREADS = 256;
+constexpr int GR_LOADS = 2 * GR_ROWS * 16 / GR_THREADS;   // 16 per thread
+constexpr size_t GR_SMEM = 2 * GR_ROWS * 16 * sizeof(double);   // 32 KiB
+constexpr int GR_MAX_CTAS = 148;
+
+__global__ void __launch_bounds__(GR_THREADS)
+    gram_kernel(const double* __restrict__ A, int64_t rows, int K, int nsplit,
+                double* __restrict__ S, const double* __restrict__ rowstat, double* nrm,
+                const double* __restrict__ Gm, int ldt, double* fit, double* scratch,
+                unsigned int* counters) {
+  PROBE_T0();
+  extern __shared__ __align__(16) double gsm[];   // [2 strips][GR_ROWS / 2][16][2]
+  __shared__ double sh[32];
+  __shared__ int last_s;
+  const int T = (K + 15) >> 4;
+  const int ntiles = T * (T + 1) / 2;
+  const int tile = blockIdx.x % ntiles, split = blockIdx.x / ntiles;
+  int t = tile, ti = 0;   // tile pair -> (ti, tj), ti <= tj, row-major over the upper triangle
+  while (t >= T - ti) {
+    t -= T - ti;
+    ++ti;
+  }
+  const int tj = ti + t;
+  const int tid = threadIdx.x, i = tid >> 4, j = tid & 15;
+  const int64_t rlo = rows * split / nsplit, rhi = rows * (split + 1) / nsplit;
+  // loader: element e = tid + 256 q (q < GR_LOADS): strip = q >= GR_LOADS / 2,
+  // row = (e >> 4) % GR_ROWS, column = e % 16  (a warp reads two 128-byte row segments)
+  double pre[GR_LOADS];
+  auto load = [&](int64_t r0) {
+#pragma unroll
+    for (int q = 0; q < GR_LOADS; ++q) {
+      const int e = tid + GR_THREADS * q;
+      const int strip = q >= GR_LOADS / 2;
+      const int rr = (e >> 4) & (GR_ROWS - 1), cc = e & 15;
+      const int col = 16 * (strip ? tj : ti) + cc;
+      const int64_t r = r0 + rr;
+      pre[q] = (r < rhi && col < K) ? __ldcg(A + r * K + col) : 0.0;
+    }
+  };
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (rlo < rhi) load(rlo);
+  for (int64_t r0 = rlo; r0 < rhi; r0 += GR_ROWS) {
+#pragma unroll
+    for (int q = 0; q < GR_LOADS; ++q) {
+      const int e = tid + GR_THREADS * q;
+      const int strip = q >= GR_LOADS / 2;
+      const int rr = (e >> 4) & (GR_ROWS - 1), cc = e & 15;
+      gsm[strip * GR_ROWS * 16 + ((rr >> 1) * 16 + cc) * 2 + (rr & 1)] = pre[q];
+    }
+    __syncthreads();
+    if (r0 + GR_ROWS < rhi) load(r0 + GR_ROWS);
+    const int nr = static_cast<int>(rhi - r0 < GR_ROWS ? rhi - r0 : GR_ROWS);
+    const double2* sa = reinterpret_cast<const double2*>(gsm);
+    const double2* sb = reinterpret_cast<const double2*>(gsm + GR_ROWS * 16);
+    for (int p = 0; p < (nr + 1) / 2; p += 2) {   // row pairs; rows past the end are zero
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double2 x = sa[(p + k) * 16 + i], y = sb[(p + k) * 16 + j];
+        acc[2 * k] = fma(x.x, y.x, acc[2 * k]);
+        acc[2 * k + 1] = fma(x.y, y.y, acc[2 * k + 1]);
+      }
+    }
+    __syncthreads();
+  }
+  PROBE_T(5);
+  double s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  if (nsplit > 1) {   // partial tiles: the last split of this tile sums them in split order
+    scratch[(int64_t)blockIdx.x * GR_THREADS + tid] = s;
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      last_s = atomicAdd(counters + tile, 1u) == static_cast<unsigned>(nsplit - 1);
+    }
+    __syncthreads();
+    if (!last_s) return;
+    __threadfence();
+    s = 0.0;
+    for (int q = 0; q < nsplit; ++q)
+      s += __ldcg(scratch + (int64_t)(q * ntiles + tile) * GR_THREADS + tid);
+    if (tid == 0) counters[tile] = 0u;
+  }
+  const int gi = 16 * ti + i, gj = 16 * tj + j;
+  const bool ok = gi < K && gj < K;
+  if (ok) {
+    S[gi * K + gj] = s;
+    S[gj * K + gi] = s;
+  }
+  if (nrm == nullptr) return;
+  double* tilepart = scratch + (int64_t)GR_MAX_CTAS * GR_THREADS;
+  if (Gm != nullptr) {
+    double v = ok ? Gm[gi * ldt + gj] * s : 0.0;
+    if (ti != tj) v *= 2.0;   // the mirrored tile
+    v = block_sum(v, sh);
+    if (tid == 0) tilepart[tile] = v;
+  }
+  // last tile: fixed-order sums of the row statistics and of the tile partials
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    last_s = atomicAdd(counters + ntiles, 1u) == static_cast<unsigned>(ntiles - 1);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < KK; e += blockDim.x) {
-    const int k1 = e / K, k2 = e - k1 * K;
-    double s = 0.0;
-#pragma unroll 4
-    for (int r = 0; r < SR_WARPS; ++r) s = fma(As[r * K + k1], As[r * K + k2], s);
-    gpart[(int64_t)blockIdx.x * KK + e] = s;
-  }
-}
-
-// S = Σ_b gpart[b] (ascending b); block 0 also reduces the row norms in row order.
-__global__ void gram_reduce_kernel(const double* __restrict__ gpart, int nb, int K, double* S,
-                                   const double* __restrict__ rowstat, int64_t rows, double* nrm) {
-  const int KK = K * K;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < KK) {
-    double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += gpart[(int64_t)b * KK + e];
-    S[e] = s;
-  }
-  if (rowstat != nullptr && blockIdx.x == 0) {
-    __shared__ double sh[32];
-    for (int c = 0; c < 3; ++c) {
-      double v = 0.0;
-      for (int64_t y = threadIdx.x; y < rows; y += blockDim.x) v += rowstat[y * 3 + c];
-      v = block_sum(v, sh);
-      if (threadIdx.x == 0) nrm[c] = v;
+  if (!last_s) return;
+  __threadfence();
+  const int nst = Gm != nullptr ? 4 : 3;
+  for (int c = 0; c < nst; ++c) {
+    double v = 0.0;
+    for (int64_t y = tid; y < rows; y += GR_THREADS) v += __ldcg(rowstat + y * 4 + c);
+    v = block_sum(v, sh);
+    if (tid == 0) {
+      if (c < 3) nrm[c] = v;
+      else fit[0] = v;
     }
   }
-}
-
-__global__ void fitness_terms_kernel(const double* __restrict__ M, const double* __restrict__ A,
-                                     int64_t n, const double* __restrict__ Gm,
-                                     const double* __restrict__ S, int64_t kk, double* out) {
-  __shared__ double sh[32];
-  double v = 0.0;
-  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) v = fma(M[e], A[e], v);
-  v = block_sum(v, sh);
-  double w = 0.0;
-  for (int64_t e = threadIdx.x; e < kk; e += blockDim.x) w = fma(Gm[e], S[e], w);
-  w = block_sum(w, sh);
-  if (threadIdx.x == 0) {
-    out[0] = v;
-    out[1] = w;
+  if (tid == 0) {
+    if (Gm != nullptr) {
+      double v = 0.0;
+      for (int b = 0; b < ntiles; ++b) v += __ldcg(tilepart + b);
+      fit[1] = v;
+    }
+    counters[ntiles] = 0u;
   }
 }
 
@@ -562,10 +724,11 @@ void note_launch() { __atomic_add_fetch(&g_launches, 1ull, __ATOMIC_RELAXED); }
 void note_launches(uint64_t n) { __atomic_add_fetch(&g_launches, n, __ATOMIC_RELAXED); }
 uint64_t launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
-int solve_row_blocks(int64_t rows) { return static_cast<int>((rows + SR_WARPS - 1) / SR_WARPS); }
+int solve_ld(int K) { return (K + 7) & ~7; }
 
-cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double* Gamma, double* L,
+cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double* Gamma, double* Tp,
                                 int* mode, double* Vscratch, cudaStream_t st) {
+  const int ldt = solve_ld(K);
   const size_t smem = static_cast<size_t>(K) * (K + 1) * sizeof(double);
   static bool attr = false;
   if (!attr) {
@@ -574,57 +737,65 @@ cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  gamma_chol_kernel<<<1, GI_THREADS, 0, st>>>(S_all, N, n, K, Gamma, L, mode);
+  gamma_chol_kernel<<<1, GF_THREADS, 0, st>>>(S_all, N, n, K, Gamma, Tp, ldt, mode);
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  gamma_pinv_kernel<<<1, GI_THREADS, smem, st>>>(K, Gamma, L, mode, Vscratch);
+  gamma_pinv_kernel<<<1, GP_THREADS, smem, st>>>(K, Gamma, Tp, ldt, mode, Vscratch);
   note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, double* dA,
-                              int64_t rows, int K, const double* Gamma, const double* L,
-                              const int* mode, double* rowstat, double* gpart, cudaStream_t st) {
+                              int64_t rows, int K, const double* Gamma, const double* Tp,
+                              const int* mode, double* rowstat, cudaStream_t st) {
   if (rows == 0) return cudaSuccess;
-  const size_t smem = (static_cast<size_t>(K) * (K + 1) + K + 2 * SR_WARPS * K) * sizeof(double);
+  const int ldt = solve_ld(K);
+  const size_t one = static_cast<size_t>(ldt) * ldt * sizeof(double);
+  // layout: 128 pad | Tp | 256 pad | Γ | 128 pad   (reads run up to one row past either end)
+  const bool both = 2 * one + 512 * sizeof(double) <= 220 * 1024;   // Γ staged too (K <= 112)
+  const size_t smem = (both ? 2 * one : one) + 512 * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(solve_rows_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (128 * 129 + 128 + 2 * SR_WARPS * 128) * 8);
+                                         220 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  solve_rows_kernel<<<solve_row_blocks(rows), SR_WARPS * 32, smem, st>>>(M, A, ref, dA, rows, K,
-                                                                         Gamma, L, mode, rowstat,
-                                                                         gpart);
+  const int64_t blocks = (rows + SR_WARPS - 1) / SR_WARPS;
+  solve_rows_kernel<<<(unsigned)blocks, SR_WARPS * 32, smem, st>>>(M, A, ref, dA, rows, K, Gamma,
+                                                                   Tp, ldt, both ? 1 : 0, mode,
+                                                                   rowstat);
   note_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_gram_reduce(const double* gpart, int nb, int K, double* S,
-                               const double* rowstat, int64_t rows, double* nrm, cudaStream_t st) {
-  gram_reduce_kernel<<<grid_for((int64_t)K * K, 256, 1 << 20), 256, 0, st>>>(gpart, nb, K, S, rowstat,
-                                                                            rows, nrm);
-  note_launch();
-  return cudaGetLastError();
+int gram_tiles(int K) {
+  const int T = (K + 15) / 16;
+  return T * (T + 1) / 2;
 }
 
-cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, double* gpart,
-                        cudaStream_t st) {
-  const int nb = solve_row_blocks(rows);
-  gram_partial_kernel<<<nb, SR_WARPS * 32, SR_WARPS * K * sizeof(double), st>>>(A, rows, K, gpart);
-  note_launch();
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  return launch_gram_reduce(gpart, nb, K, S, nullptr, 0, nullptr, st);
-}
+size_t gram_scratch_doubles() { return (size_t)GR_MAX_CTAS * GR_THREADS + 64; }
 
-cudaError_t launch_fitness_terms(const double* M, const double* A, int64_t rows, int K,
-                                 const double* Gamma, const double* S, double* out,
-                                 cudaStream_t st) {
-  fitness_terms_kernel<<<1, 1024, 0, st>>>(M, A, rows * K, Gamma, S, (int64_t)K * K, out);
+cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, const double* rowstat,
+                        double* nrm, const double* Gamma_model, double* fit, double* scratch,
+                        unsigned int* counters, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(GR_SMEM));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int nt = gram_tiles(K);
+  int64_t ns = (rows + GR_ROWS - 1) / GR_ROWS;
+  const int64_t cap = GR_MAX_CTAS / nt;
+  if (ns > cap) ns = cap;
+  if (ns < 1) ns = 1;
+  gram_kernel<<<(unsigned)(nt * ns), GR_THREADS, GR_SMEM, st>>>(A, rows, K, (int)ns, S, rowstat,
+                                                                nrm, Gamma_model, solve_ld(K), fit,
+                                                                scratch, counters);
   note_launch();
   return cudaGetLastError();
 }

@@ -355,8 +355,9 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
     cuuint32_t box[2] = {16, 16};
     if (!make_map(&tmF, Fp, 2, dims, str, box)) return cudaErrorInvalidValue;
   }
-  const int nk = static_cast<int>((S + BK - 1) / BK);
-  const int stages = nk < C::MAX_STAGES ? (nk < 2 ? 2 : nk) : C::MAX_STAGES;
+  // the ring spans several tiles when S is short (C4: s = 20 -> 2 slices per tile), so the
+  // producer keeps loading the next tiles while the consumers finish this one
+  const int stages = C::MAX_STAGES;
   const int smem = C::smem(stages);
   const int64_t mtiles = (Mrows + BM - 1) / BM;
   const int64_t ntiles = mtiles * (MC ? B : 1);

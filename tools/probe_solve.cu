@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <vector>
+#define CPPP_PROBE_CYCLES 1
 #include "../paper_1811_10573_b200/csrc/solve.cu"
 
 __global__ void spin(double* o, int n) {
@@ -33,12 +34,16 @@ int main() {
           for (int y = 0; y < s; ++y) acc += A[y * K + i] * A[y * K + j] * (1.0 + 0.1 * m);
           S[m * K * K + i * K + j] = acc;
         }
-    double *dS, *dG, *dP, *dV, *dM, *dA, *dD, *drs, *dgp, *dSn, *dn;
+    const int ldt = solve_ld(K);
+    double *dS, *dG, *dP, *dV, *dM, *dA, *dD, *drs, *dtp, *dSn, *dn, *dfit;
+    unsigned* dcnt;
     int* dmode;
-    cudaMalloc(&dS, 8 * N * K * K); cudaMalloc(&dG, 8 * K * K); cudaMalloc(&dP, 8 * K * K);
+    cudaMalloc(&dS, 8 * N * K * K); cudaMalloc(&dG, 8 * ldt * ldt); cudaMalloc(&dP, 8 * ldt * ldt);
+    cudaMemset(dG, 0, 8 * ldt * ldt); cudaMemset(dP, 0, 8 * ldt * ldt);
     cudaMalloc(&dV, 8 * K * K); cudaMalloc(&dmode, 4); cudaMalloc(&dM, 8 * s * K);
-    cudaMalloc(&dA, 8 * s * K); cudaMalloc(&dD, 8 * s * K); cudaMalloc(&drs, 8 * s * 3);
-    cudaMalloc(&dgp, 8 * 64 * K * K); cudaMalloc(&dSn, 8 * K * K); cudaMalloc(&dn, 8 * 3);
+    cudaMalloc(&dA, 8 * s * K); cudaMalloc(&dD, 8 * s * K); cudaMalloc(&drs, 8 * s * 4);
+    cudaMalloc(&dtp, 8 * gram_scratch_doubles()); cudaMalloc(&dSn, 8 * K * K); cudaMalloc(&dn, 8 * 3);
+    cudaMalloc(&dfit, 8 * 2); cudaMalloc(&dcnt, 256); cudaMemset(dcnt, 0, 256);
     cudaMemcpy(dS, S.data(), 8 * N * K * K, cudaMemcpyHostToDevice);
     cudaMemcpy(dM, A.data(), 8 * s * K, cudaMemcpyHostToDevice);
     cudaMemcpy(dA, A.data(), 8 * s * K, cudaMemcpyHostToDevice);
@@ -51,26 +56,54 @@ int main() {
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms_inv; cudaEventElapsedTime(&ms_inv, a, b);
     cudaEventRecord(a);
-    for (int r = 0; r < 20; ++r) {
-      launch_solve_rows(dM, dA, dA, dD, s, K, dG, dP, dmode, drs, dgp, 0);
-      launch_gram_reduce(dgp, solve_row_blocks(s), K, dSn, drs, s, dn, 0);
-    }
+    for (int r = 0; r < 20; ++r) launch_solve_rows(dM, dA, dA, dD, s, K, dG, dP, dmode, drs, 0);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms_rows; cudaEventElapsedTime(&ms_rows, a, b);
-    std::vector<double> G(K * K), P(K * K);
-    int mode = -1;
-    cudaMemcpy(G.data(), dG, 8 * K * K, cudaMemcpyDeviceToHost);
-    cudaMemcpy(P.data(), dP, 8 * K * K, cudaMemcpyDeviceToHost);
-    cudaMemcpy(&mode, dmode, 4, cudaMemcpyDeviceToHost);
-    double err = 0;
+    cudaEventRecord(a);
+    for (int r = 0; r < 20; ++r) launch_gram(dA, s, K, dSn, drs, dn, dG, dfit, dtp, dcnt, 0);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms_gram; cudaEventElapsedTime(&ms_gram, a, b);
+    // one solve from the original M to check A_new Γ = M
+    cudaMemcpy(dA, A.data(), 8 * s * K, cudaMemcpyHostToDevice);
+    launch_solve_rows(dM, dA, dA, dD, s, K, dG, dP, dmode, drs, 0);
+    std::vector<double> An(s * K);
+    cudaMemcpy(An.data(), dA, 8 * s * K, cudaMemcpyDeviceToHost);
+    launch_gamma_factor(dS, N, 0, K, dG, dP, dmode, dV, 0);
+    cudaDeviceSynchronize();
+    long long cyc[16];
+    cudaMemcpyFromSymbol(cyc, g_probe_cycles, sizeof(cyc));
+    std::vector<double> Tp(K * ldt), Gh(K * ldt);
+    cudaMemcpy(Tp.data(), dP, 8 * K * ldt, cudaMemcpyDeviceToHost);
+    cudaMemcpy(Gh.data(), dG, 8 * K * ldt, cudaMemcpyDeviceToHost);
+    // L from the packed factor: lower part = L, diag = 1/Tp[j][j]; check L Lᵀ = Γ and Tp upper = Lᵀ
+    double lerr = 0, terr = 0;
     for (int i = 0; i < K; ++i)
-      for (int j = 0; j < K; ++j) {
+      for (int j = 0; j <= i; ++j) {
         double acc = 0;
-        for (int l = 0; l < K; ++l) acc += P[i * K + l] * P[j * K + l];
-        err = fmax(err, fabs(acc - G[i * K + j]) / fabs(G[i * K + i]));
+        for (int p = 0; p <= j; ++p) {
+          const double li = p == i ? 1.0 / Tp[i * ldt + i] : Tp[i * ldt + p];
+          const double lj = p == j ? 1.0 / Tp[j * ldt + j] : Tp[j * ldt + p];
+          acc += li * lj;
+        }
+        lerr = fmax(lerr, fabs(acc - Gh[i * ldt + j]) / Gh[i * ldt + i]);
+        if (j < i) terr = fmax(terr, fabs(Tp[j * ldt + i] - Tp[i * ldt + j]));
       }
-    printf("{\"K\": %d, \"mode\": %d, \"inv_err\": %.3e, \"gamma_factor_us\": %.2f, \"rows_plus_reduce_us\": %.2f, \"cuda\": \"%s\"}\n",
-           K, mode, err, ms_inv * 1e3 / 20, ms_rows * 1e3 / 20, cudaGetErrorString(cudaGetLastError()));
+    printf("K %d: LLt err %.3e, upper-vs-lower %.3e; cycles chol setup %lld total %lld; rows staged %lld subst %lld total %lld; gram loop %lld\n",
+           K, lerr, terr, cyc[0], cyc[1], cyc[2], cyc[3], cyc[4], cyc[5]);
+    std::vector<double> G(K * ldt);
+    int mode = -1;
+    cudaMemcpy(G.data(), dG, 8 * K * ldt, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&mode, dmode, 4, cudaMemcpyDeviceToHost);
+    double err = 0, nrm = 0;
+    for (int y = 0; y < s; ++y)
+      for (int c = 0; c < K; ++c) {
+        double acc = 0;
+        for (int l = 0; l < K; ++l) acc += An[y * K + l] * G[l * ldt + c];
+        err = fmax(err, fabs(acc - A[y * K + c]));
+        nrm = fmax(nrm, fabs(A[y * K + c]));
+      }
+    printf("{\"K\": %d, \"mode\": %d, \"resid\": %.3e, \"gamma_factor_us\": %.2f, \"rows_us\": %.2f, \"gram_us\": %.2f, \"cuda\": \"%s\"}\n",
+           K, mode, err / nrm, ms_inv * 1e3 / 20, ms_rows * 1e3 / 20, ms_gram * 1e3 / 20, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
