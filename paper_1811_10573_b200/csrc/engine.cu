@@ -794,7 +794,7 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   size_t oLm = take(sizeof(int) * 4);
   size_t oRow = take(sizeof(double) * smax * 4);
   size_t oStats = take(sizeof(double) * (3 * N + 8));
-  size_t oFpad = take(sizeof(double) * (smax * 128 + 32));   // + TTM tile counter
+  size_t oFpad = take(sizeof(double) * ttm_scratch_doubles(smax));   // TTM factor + scheduler
   size_t oOps[CPPP_MAX_ORDER][CPPP_MAX_ORDER];
   for (int i = 0; i < N; ++i)
     for (int j = i + 1; j < N; ++j) oOps[i][j] = take(sizeof(double) * c->dl[i] * c->dl[j] * K);

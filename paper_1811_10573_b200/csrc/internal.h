@@ -25,8 +25,9 @@ uint64_t launch_count();
 // X viewed as [B][S][R] (row-major), F is S x K (ld K), out is [B][R][K].
 // R == 1 is the natural mode-(N-1) unfolding X(BxS)·F; R > 1 contracts a middle/first mode.
 // Uses the DMMA (FP64 tensor core) kernel with TMA staging when the shape allows it (even
-// S and R, K <= 128), else the SIMT FP64 kernel.  `Fpad` is scratch of >= S*128 + 32 doubles
-// (padded factor, then the persistent kernel's tile counter).
+// S and R, K <= 128), else the SIMT FP64 kernel.  `Fpad` is scratch of ttm_scratch_doubles(S)
+// doubles (padded factor, the persistent kernel's tile counter and tail tickets, tail partials;
+// zeroed once, left zeroed).
 cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R,
                        const double* F, int K, double* out, double* Fpad,
                        bool force_simt, cudaStream_t st);
@@ -34,6 +35,8 @@ cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R,
 // into Fpad (no-op for the SIMT path); launch_ttm_core runs the GEMM.
 bool ttm_uses_dmma(int64_t B, int64_t S, int64_t R, int K, bool force_simt);
 cudaError_t ttm_prepare(int64_t S, const double* F, int K, double* Fpad, cudaStream_t st);
+// doubles of TTM scratch (`Fpad`) for a contracted extent S (padded factor + scheduler + tail)
+size_t ttm_scratch_doubles(int64_t S);
 cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
                             int K, double* out, const double* Fpad, bool force_simt,
                             cudaStream_t st);
@@ -43,10 +46,12 @@ bool ttm_dmma_supported(int64_t B, int64_t S, int64_t R, int K);
 
 // Multi-TTV: rank-diagonal contraction of one mode of a parent intermediate,
 // out[b][r][k] = Σ_x P[b][x][r][k] * F[x][k];  parent viewed as [B][S][R][K].
-// `scratch` (>= ttv_scratch_doubles(), may be null) enables the split-x path for small outputs.
+// Small outputs split x over a (1, xs, 1) cluster reduced over DSMEM; `scratch` is unused.
 cudaError_t launch_ttv(const double* P, int64_t B, int64_t S, int64_t R, int K,
                        const double* F, double* out, double* scratch, cudaStream_t st);
 size_t ttv_scratch_doubles();
+cudaError_t launch_ttv_cfg(const double* P, int64_t B, int64_t S, int64_t R, int K,
+                           const double* F, double* out, int V, int U, int xs, cudaStream_t st);
 
 // Fused multi-output TTV: up to 3 children of one parent in one pass.  The parent is viewed
 // as [B][S0]...[S_{m-1}][T][K] where the children contract axis c of the m middle axes.

@@ -26,12 +26,38 @@
 #include <mutex>
 
 namespace cppp {
+#ifdef CPPP_PROBE_TTM   // tools/probe_ttm only: per-unit (sm, start, end) global-timer stamps
+__device__ unsigned long long g_ttm_trace[1 << 16][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+#define TTM_STAMP_START(u)                                      \
+  unsigned long long ttm_t0_ = 0;                               \
+  if (threadIdx.x == 0) ttm_t0_ = gtimer()
+#define TTM_STAMP_END(u)                                                     \
+  if (threadIdx.x == 0 && (u) < (1 << 16)) {                                 \
+    g_ttm_trace[u][0] = smid();                                              \
+    g_ttm_trace[u][1] = ttm_t0_;                                             \
+    g_ttm_trace[u][2] = gtimer();                                            \
+  }
+#else
+#define TTM_STAMP_START(u) (void)0
+#define TTM_STAMP_END(u) (void)0
+#endif
 namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 16;
 constexpr int NWARP = 16;   // consumer warps, 8 output rows each (4 per SM sub-partition)
 constexpr int NTHREADS = (NWARP + 1) * 32;
+constexpr int TTM_MAX_TAIL = 74;   // split tail tiles per launch (<= 148 / 2 half-tile units)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -100,18 +126,37 @@ struct Cfg {
 
 // Persistent: CTA b processes tiles b, b + gridDim.x, ...; the producer warp runs ahead across
 // tile boundaries (bounded by the ring), so the next tile's loads overlap this tile's epilogue.
+// Work units: tiles [0, nfull) are whole; each of the ntail tiles after them is split into two
+// k halves (units nfull + 2v + h), so the last, partial wave of a launch whose tile count is
+// just above a multiple of the grid costs half a tile instead of a whole one.  The two halves of
+// a tail tile leave partial sums in `part`; the second to finish (ticket) adds them in a fixed
+// order (half 0 + half 1) and writes the tile.
+struct Unit {
+  long long tile;
+  int k0, k1, half;   // half = -1 for a whole tile
+};
+__device__ __forceinline__ Unit decode_unit(long long u, long long nfull, int nk, int khalf) {
+  if (u < nfull) return Unit{u, 0, nk, -1};
+  const long long v = u - nfull;
+  const int h = static_cast<int>(v & 1);
+  return Unit{nfull + (v >> 1), h ? khalf : 0, h ? nk : khalf, h};
+}
+
 template <int NT, bool MC>
 __global__ void __launch_bounds__(NTHREADS, 1)
     ttm_dmma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
-                    double* __restrict__ out, int64_t Mrows, int64_t mtiles, int64_t ntiles, int S,
-                    int K, int stages, unsigned long long* __restrict__ tile_counter) {
+                    double* __restrict__ out, int64_t Mrows, int64_t mtiles, int64_t nfull,
+                    int64_t ntail, int S, int K, int stages,
+                    unsigned long long* __restrict__ tile_counter, unsigned int* __restrict__ tickets,
+                    double* __restrict__ part) {
   using C = Cfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(base + stages * C::STAGE);
   uint64_t* empty = full + stages;
-  __shared__ long long stage_tile[16];   // tile id carried by the first k-stage of each tile
+  __shared__ long long stage_tile[16];   // unit id carried by the first k-stage of each unit
+  __shared__ int ticket_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -124,6 +169,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   __syncthreads();
   const int nk = (S + BK - 1) / BK;
+  const int khalf = nk / 2;
+  const long long nunits = nfull + 2 * ntail;
 
   if (warp == NWARP) {  // ---------------- TMA producer
     if (lane == 0) {
@@ -132,8 +179,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       int64_t it = 0;
       while (true) {
         // dynamic tile scheduler: robust to SMs that are busy with other streams' work
-        const long long tile = static_cast<long long>(atomicAdd(tile_counter, 1ull));
-        if (tile >= ntiles) {
+        const long long unit = static_cast<long long>(atomicAdd(tile_counter, 1ull));
+        if (unit >= nunits) {
           const int st = static_cast<int>(it % stages);
           const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
           if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
@@ -141,13 +188,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_arrive(smem_u32(&full[st]));   // wake the consumers with the sentinel
           break;
         }
-        const int64_t b = MC ? tile / mtiles : 0;
-        const int64_t m0 = (tile - b * mtiles) * BM;
-        for (int kt = 0; kt < nk; ++kt, ++it) {
+        const Unit un = decode_unit(unit, nfull, nk, khalf);
+        const int64_t b = MC ? un.tile / mtiles : 0;
+        const int64_t m0 = (un.tile - b * mtiles) * BM;
+        for (int kt = un.k0; kt < un.k1; ++kt, ++it) {
           const int st = static_cast<int>(it % stages);
           const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
           if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
-          if (kt == 0) stage_tile[st] = tile;
+          if (kt == un.k0) stage_tile[st] = unit;
           const uint32_t fb = smem_u32(&full[st]);
           mbar_expect_tx(fb, C::STAGE);
           const uint32_t sx = smem_u32(base + st * C::STAGE);
@@ -181,18 +229,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int st = static_cast<int>(it % stages);
       mbar_wait(smem_u32(&full[st]), static_cast<uint32_t>((it / stages) & 1));
     }
-    const long long tile = stage_tile[static_cast<int>(it % stages)];
-    if (tile < 0) break;
-    const int64_t b = MC ? tile / mtiles : 0;
-    const int64_t m0 = (tile - b * mtiles) * BM;
+    const long long unit = stage_tile[static_cast<int>(it % stages)];
+    if (unit < 0) break;
+    const Unit un = decode_unit(unit, nfull, nk, khalf);
+    TTM_STAMP_START(unit);
+    const int64_t b = MC ? un.tile / mtiles : 0;
+    const int64_t m0 = (un.tile - b * mtiles) * BM;
     double acc[NT][2];
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
 
-    for (int kt = 0; kt < nk; ++kt, ++it) {
+    for (int kt = un.k0; kt < un.k1; ++kt, ++it) {
       const int st = static_cast<int>(it % stages);
       const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
-      if (kt > 0) mbar_wait(smem_u32(&full[st]), ph);
+      if (kt > un.k0) mbar_wait(smem_u32(&full[st]), ph);
       const uint32_t sx = smem_u32(base + st * C::STAGE);
       const uint32_t sf = sx + C::XBYTES;
       const int qmax = (S - kt * BK) > 8 ? 2 : 1;   // skip an all-zero k tail
@@ -239,6 +289,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
     }
 
+    // ---------------- split tail tile: park this half, the second half to finish combines
+    if (un.half >= 0) {
+      const int64_t v = un.tile - nfull;
+      double* mine = part + ((v * 2 + un.half) * (NT * 2)) * (NWARP * 32) + threadIdx.x;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        mine[(2 * j) * (NWARP * 32)] = acc[j][0];
+        mine[(2 * j + 1) * (NWARP * 32)] = acc[j][1];
+      }
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"r"(NWARP * 32) : "memory");   // consumer warps only
+      if (threadIdx.x == 0) ticket_s = atomicAdd(tickets + v, 1u);
+      asm volatile("bar.sync 1, %0;" ::"r"(NWARP * 32) : "memory");
+      if (ticket_s == 0) {   // the other half finishes the tile
+        TTM_STAMP_END(unit);
+        continue;
+      }
+      __threadfence();
+      const double* p0 = part + ((v * 2) * (NT * 2)) * (NWARP * 32) + threadIdx.x;
+      const double* p1 = p0 + (NT * 2) * (NWARP * 32);
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        acc[j][0] = __ldcg(p0 + (2 * j) * (NWARP * 32)) + __ldcg(p1 + (2 * j) * (NWARP * 32));
+        acc[j][1] = __ldcg(p0 + (2 * j + 1) * (NWARP * 32)) + __ldcg(p1 + (2 * j + 1) * (NWARP * 32));
+      }
+      if (threadIdx.x == 0) tickets[v] = 0u;
+    }
     // ---------------- epilogue: thread holds row r x columns 16c + 4t + {0,1,2,3}
     {
       const int mloc = MC ? (16 * mbox + mrow) : (8 * warp + fm);
@@ -272,6 +349,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
     }
+    TTM_STAMP_END(unit);
   }
 }
 
@@ -326,7 +404,8 @@ bool make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims,
 
 template <int NT, bool MC>
 cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
-                     double* out, unsigned long long* counter, cudaStream_t st) {
+                     double* out, unsigned long long* counter, unsigned int* tickets, double* part,
+                     cudaStream_t st) {
   using C = Cfg<NT>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -372,22 +451,29 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
   }
   int64_t grid = static_cast<int64_t>(sms) * occ;
   if (grid > ntiles) grid = ntiles;
+  // a last wave at most half full is split into k halves (one wave of half-tiles)
+  const int64_t tail = ntiles % grid;
+  const int nk = static_cast<int>((S + BK - 1) / BK);
+  const int64_t ntail = (ntiles > grid && tail > 0 && 2 * tail <= grid && tail <= TTM_MAX_TAIL &&
+                         nk >= 4) ? tail : 0;
+  const int64_t nfull = ntiles - ntail;
   cudaError_t e0 = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
   if (e0 != cudaSuccess) return e0;
-  ttm_dmma_kernel<NT, MC><<<(unsigned)grid, NTHREADS, smem, st>>>(tmX, tmF, out, Mrows, mtiles, ntiles,
-                                                                   (int)S, K, stages, counter);
+  ttm_dmma_kernel<NT, MC><<<(unsigned)grid, NTHREADS, smem, st>>>(
+      tmX, tmF, out, Mrows, mtiles, nfull, ntail, (int)S, K, stages, counter, tickets, part);
   note_launch();
   return cudaGetLastError();
 }
 
 template <bool MC, int NT = 1>
 cudaError_t dispatch_nt(int nt, const double* X, int64_t B, int64_t S, int64_t R, const double* Fp,
-                        int K, double* out, unsigned long long* counter, cudaStream_t st) {
+                        int K, double* out, unsigned long long* counter, unsigned int* tickets,
+                        double* part, cudaStream_t st) {
   if constexpr (NT > 16) {
     return cudaErrorInvalidValue;
   } else {
-    if (nt == NT) return run_dmma<NT, MC>(X, B, S, R, Fp, K, out, counter, st);
-    return dispatch_nt<MC, NT + 1>(nt, X, B, S, R, Fp, K, out, counter, st);
+    if (nt == NT) return run_dmma<NT, MC>(X, B, S, R, Fp, K, out, counter, tickets, part, st);
+    return dispatch_nt<MC, NT + 1>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st);
   }
 }
 
@@ -417,24 +503,35 @@ bool ttm_uses_dmma(int64_t B, int64_t S, int64_t R, int K, bool force_simt) {
   return !force_simt && ttm_dmma_supported(B, S, R, K);
 }
 
+
 // padded factor width for K: 16-column TMA boxes
 int ttm_ld(int K) { return ((((K + 7) / 8) * 8 + 15) / 16) * 16; }
 
+// scratch layout (ttm_scratch_doubles): tile counter + tail tickets (256 doubles) | tail partial
+// sums | padded factor (S x ttm_ld(K)) -- the control words sit at a fixed offset, so launches
+// with different S never overwrite each other's tickets
+constexpr size_t TTM_CTL = 256;
+constexpr size_t TTM_PART = static_cast<size_t>(TTM_MAX_TAIL) * 2 * BM * 128;
+
 cudaError_t ttm_prepare(int64_t S, const double* F, int K, double* Fpad, cudaStream_t st) {
-  return launch_pad_rows(F, S, K, Fpad, ttm_ld(K), st);
+  return launch_pad_rows(F, S, K, Fpad + TTM_CTL + TTM_PART, ttm_ld(K), st);
 }
+
+size_t ttm_scratch_doubles(int64_t S) { return TTM_CTL + TTM_PART + static_cast<size_t>(S) * 128; }
 
 cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
                             int K, double* out, const double* Fpad, bool force_simt,
                             cudaStream_t st) {
   if (B * R * K == 0) return cudaSuccess;
   if (!ttm_uses_dmma(B, S, R, K, force_simt)) return launch_ttm_simt(X, B, S, R, F, K, out, st);
-  // the tile counter lives right after the padded factor (see ttm_fpad_doubles)
-  unsigned long long* counter =
-      reinterpret_cast<unsigned long long*>(const_cast<double*>(Fpad) + S * ttm_ld(K));
+  double* ctl = const_cast<double*>(Fpad);
+  unsigned long long* counter = reinterpret_cast<unsigned long long*>(ctl);
+  unsigned int* tickets = reinterpret_cast<unsigned int*>(ctl + 8);
+  double* part = ctl + TTM_CTL;
+  const double* Fp = ctl + TTM_CTL + TTM_PART;
   const int nt = (K + 7) / 8;
-  if (R == 1) return dispatch_nt<false>(nt, X, B, S, R, Fpad, K, out, counter, st);
-  return dispatch_nt<true>(nt, X, B, S, R, Fpad, K, out, counter, st);
+  if (R == 1) return dispatch_nt<false>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st);
+  return dispatch_nt<true>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st);
 }
 
 cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R, const double* F, int K,
