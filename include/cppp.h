@@ -59,6 +59,8 @@ typedef enum {
 #define CPPP_FLAG_PROFILE       4u  /* time each kernel class with CUDA events (cppp_kernel_stats) */
 #define CPPP_FLAG_NO_FUSED_TTV  8u  /* one multi-TTV launch per child instead of per parent */
 #define CPPP_FLAG_NO_GRAPH     16u  /* run sweeps eagerly instead of replaying captured CUDA graphs */
+#define CPPP_FLAG_NO_KRP       32u  /* regular DT sweep: single-mode first-level TTMs instead of one
+                                        multi-mode (Khatri-Rao) GEMM per half (testing) */
 
 typedef struct {
   int device;               /* CUDA ordinal (default 0) */

@@ -330,6 +330,40 @@ cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, doubl
   return CPPP_OK;
 }
 
+// Multi-mode first level: contract the consecutive modes `modes` (ascending) of X in ONE GEMM
+// with their Khatri-Rao product (P:78-80 applied to a whole half of the tree at once; same
+// 2 s^N R flops as a single-mode TTM, but no s^(N-1) R intermediate and no multi-TTV pass over
+// it).  Returns false (nothing done) when the DMMA GEMM cannot take the shape.
+bool contract_multi(cppp_ctx* c, const Node& src, const std::vector<int>& modes, double* out,
+                    cppp_status* st) {
+  *st = CPPP_OK;
+  int64_t B = 1, S = 1, R = 1;
+  for (int v = 0; v < c->N; ++v) {
+    if (v < modes.front()) B *= c->dl[v];
+    else if (v > modes.back()) R *= c->dl[v];
+    else S *= c->dl[v];
+  }
+  const int K = c->K;
+  if (!ttm_uses_dmma(B, S, R, K, (c->flags & CPPP_FLAG_SIMT_TTM) != 0)) return false;
+  if (c->dry) return true;
+  KrpArgs a{};
+  a.nm = static_cast<int>(modes.size());
+  a.K = K;
+  for (int j = 0; j < a.nm; ++j) {
+    a.F[j] = fac_local(c, c->A, modes[j]);
+    a.dims[j] = c->dl[modes[j]];
+  }
+  cudaError_t e = ttm_prepare_krp(a, c->Fpad, c->st);
+  if (e != cudaSuccess) {
+    *st = fail(c, CPPP_ECUDA, "khatri-rao: %s", cudaGetErrorString(e));
+    return true;
+  }
+  Prof p(c, CPPP_K_TTM, 2.0 * B * S * R * K, 8.0 * (B * S * R + B * R * K));
+  e = launch_ttm_padded(src.data, B, S, R, K, out, c->Fpad, c->st);
+  if (e != cudaSuccess) *st = fail(c, CPPP_ECUDA, "multi-mode TTM: %s", cudaGetErrorString(e));
+  return true;
+}
+
 // ---------------------------------------------------------------- small solve of one mode
 // A_new = M Γ^†, G, dA = A_new - ref, S^(n), norms (Alg. 1 P:393-399 / Alg. 3).
 // Issue Γ^(n) and its inverse on the side stream once every S^(m), m != n, is final (ev_S).
@@ -417,8 +451,28 @@ struct DT {
     return m;
   }
 
-  // contract `modes` (in order) out of nd; the final node goes to `final_dst` if given
+  // contract `modes` (in order) out of nd; the final node goes to `final_dst` if given.  From
+  // the root of an order >= 4 tensor, a half of two or more modes (none of them sharded) is
+  // contracted in one multi-mode GEMM (contract_multi) unless CPPP_FLAG_NO_KRP.  (Order 3
+  // keeps the single-mode TTM: its level-1 node feeds two leaves, and the multi-mode GEMM
+  // would have only s/128 output tiles.)
   cppp_status chain(const Node& nd, const std::vector<int>& modes, double* final_dst, Node* out) {
+    if (nd.root && modes.size() >= 2 && c->N >= 4 && !(c->flags & CPPP_FLAG_NO_KRP) &&
+        std::find(modes.begin(), modes.end(), c->q) == modes.end()) {
+      std::vector<int> asc = modes;
+      std::sort(asc.begin(), asc.end());
+      uint32_t nm = nd.mask;
+      for (int v : asc) nm &= ~(1u << v);
+      const size_t mk = c->stack.mark();
+      double* dst = final_dst ? final_dst : c->stack.push(node_elems(c, nm));
+      cppp_status st;
+      if (contract_multi(c, nd, asc, dst, &st)) {
+        STCHK(st);
+        *out = Node{nm, dst, false};
+        return CPPP_OK;
+      }
+      c->stack.release(mk);
+    }
     Node cur = nd;
     for (size_t i = 0; i < modes.size(); ++i) {
       const int u = modes[i];
@@ -794,7 +848,17 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   size_t oLm = take(sizeof(int) * 4);
   size_t oRow = take(sizeof(double) * smax * 4);
   size_t oStats = take(sizeof(double) * (3 * N + 8));
-  size_t oFpad = take(sizeof(double) * ttm_scratch_doubles(smax));   // TTM factor + scheduler
+  // TTM scratch: the padded factor of the widest first-level GEMM (a single mode, or the
+  // Khatri-Rao product of a whole half: S = Π of its extents) + scheduler + split partials
+  int64_t maxS = smax;
+  {
+    const int mid = (c->N + 1) / 2 - 1;   // DT::range's split of [0, N-1]
+    int64_t sl = 1, sr = 1;
+    for (int v = 0; v <= mid; ++v) sl *= c->dl[v];
+    for (int v = mid + 1; v < c->N; ++v) sr *= c->dl[v];
+    maxS = std::max(maxS, std::max(sl, sr));
+  }
+  size_t oFpad = take(sizeof(double) * ttm_scratch_doubles(maxS));   // TTM factor + scheduler
   size_t oOps[CPPP_MAX_ORDER][CPPP_MAX_ORDER];
   for (int i = 0; i < N; ++i)
     for (int j = i + 1; j < N; ++j) oOps[i][j] = take(sizeof(double) * c->dl[i] * c->dl[j] * K);
@@ -869,6 +933,7 @@ cppp_status validate(cppp_ctx* c, int N, const int64_t* s, int K, const cppp_opt
 void setup_dims(cppp_ctx* c, int N, const int64_t* s, int K, const cppp_opts* o) {
   c->N = N;
   c->K = K;
+  c->flags = o ? o->flags : 0u;   // the plan (tree shapes) depends on the flags
   for (int n = 0; n < N; ++n) c->s[n] = c->dl[n] = s[n];
   c->q = -1;
   if (o && o->shard_mode == 0) {

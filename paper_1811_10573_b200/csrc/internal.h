@@ -5,6 +5,7 @@
 #include <stddef.h>
 
 #define CPPP_MAX_TERMS_ 8
+#define CPPP_MAX_ORDER_ 8
 
 namespace cppp {
 
@@ -37,6 +38,20 @@ bool ttm_uses_dmma(int64_t B, int64_t S, int64_t R, int K, bool force_simt);
 cudaError_t ttm_prepare(int64_t S, const double* F, int K, double* Fpad, cudaStream_t st);
 // doubles of TTM scratch (`Fpad`) for a contracted extent S (padded factor + scheduler + tail)
 size_t ttm_scratch_doubles(int64_t S);
+// Multi-mode first level: KR = A^(m_0) ⊙ ... ⊙ A^(m_{h-1}) (consecutive modes, row-major over
+// (x_0..x_{h-1})) into the padded-factor area of Fpad; then launch_ttm_padded contracts X viewed
+// as [B][S = Π s_{m_j}][R] with it (DMMA path only: ttm_uses_dmma must hold).
+struct KrpArgs {
+  const double* F[CPPP_MAX_ORDER_];
+  int64_t dims[CPPP_MAX_ORDER_];
+  int nm;
+  int K;
+  int ld;          // set by ttm_prepare_krp
+  int64_t rows;    // set by ttm_prepare_krp
+};
+cudaError_t ttm_prepare_krp(const KrpArgs& a, double* Fpad, cudaStream_t st);
+cudaError_t launch_ttm_padded(const double* X, int64_t B, int64_t S, int64_t R, int K, double* out,
+                              const double* Fpad, cudaStream_t st);
 cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
                             int K, double* out, const double* Fpad, bool force_simt,
                             cudaStream_t st);

@@ -23,6 +23,7 @@
 
 #include <cuda.h>
 
+#include <cmath>
 #include <mutex>
 
 namespace cppp {
@@ -57,7 +58,12 @@ constexpr int BM = 128;
 constexpr int BK = 16;
 constexpr int NWARP = 16;   // consumer warps, 8 output rows each (4 per SM sub-partition)
 constexpr int NTHREADS = (NWARP + 1) * 32;
-constexpr int TTM_MAX_TAIL = 74;   // split tail tiles per launch (<= 148 / 2 half-tile units)
+// scratch layout (ttm_scratch_doubles): tile counter + split tickets (TTM_CTL doubles) | split
+// partial sums (TTM_PART doubles) | padded factor (S x ttm_ld(K)) -- the control words sit at a
+// fixed offset, so launches with different S never overwrite each other's tickets
+constexpr int64_t TTM_CTL = 512;
+constexpr int64_t TTM_TICKETS = 2 * (TTM_CTL - 8);   // unsigned words after the 8-double counter
+constexpr int64_t TTM_PART = static_cast<int64_t>(8) << 20;   // 64 MiB of parked partial tiles
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -126,27 +132,28 @@ struct Cfg {
 
 // Persistent: CTA b processes tiles b, b + gridDim.x, ...; the producer warp runs ahead across
 // tile boundaries (bounded by the ring), so the next tile's loads overlap this tile's epilogue.
-// Work units: tiles [0, nfull) are whole; each of the ntail tiles after them is split into two
-// k halves (units nfull + 2v + h), so the last, partial wave of a launch whose tile count is
-// just above a multiple of the grid costs half a tile instead of a whole one.  The two halves of
-// a tail tile leave partial sums in `part`; the second to finish (ticket) adds them in a fixed
-// order (half 0 + half 1) and writes the tile.
+// Work units: tiles [0, nfull) are whole; each of the nsplit tiles after them is cut into ks
+// k chunks (units nfull + ks v + c).  Two uses: a last wave at most half full gets ks = 2 (it
+// then costs half a tile instead of a whole one), and a GEMM with few tiles and a long
+// reduction (the multi-mode first level, S = s^h) splits every tile.  The chunks of a split
+// tile leave partial sums in `part`; the last to finish (ticket) adds them in chunk order
+// (deterministic) and writes the tile.
 struct Unit {
   long long tile;
-  int k0, k1, half;   // half = -1 for a whole tile
+  int k0, k1, chunk;   // chunk = -1 for a whole tile
 };
-__device__ __forceinline__ Unit decode_unit(long long u, long long nfull, int nk, int khalf) {
+__device__ __forceinline__ Unit decode_unit(long long u, long long nfull, int nk, int ks) {
   if (u < nfull) return Unit{u, 0, nk, -1};
   const long long v = u - nfull;
-  const int h = static_cast<int>(v & 1);
-  return Unit{nfull + (v >> 1), h ? khalf : 0, h ? nk : khalf, h};
+  const int c = static_cast<int>(v % ks);
+  return Unit{nfull + v / ks, nk * c / ks, nk * (c + 1) / ks, c};
 }
 
 template <int NT, bool MC>
 __global__ void __launch_bounds__(NTHREADS, 1)
     ttm_dmma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
                     double* __restrict__ out, int64_t Mrows, int64_t mtiles, int64_t nfull,
-                    int64_t ntail, int S, int K, int stages,
+                    int64_t nsplit, int ks, int S, int K, int stages,
                     unsigned long long* __restrict__ tile_counter, unsigned int* __restrict__ tickets,
                     double* __restrict__ part) {
   using C = Cfg<NT>;
@@ -169,8 +176,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   __syncthreads();
   const int nk = (S + BK - 1) / BK;
-  const int khalf = nk / 2;
-  const long long nunits = nfull + 2 * ntail;
+  const long long nunits = nfull + static_cast<long long>(ks) * nsplit;
 
   if (warp == NWARP) {  // ---------------- TMA producer
     if (lane == 0) {
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_arrive(smem_u32(&full[st]));   // wake the consumers with the sentinel
           break;
         }
-        const Unit un = decode_unit(unit, nfull, nk, khalf);
+        const Unit un = decode_unit(unit, nfull, nk, ks);
         const int64_t b = MC ? un.tile / mtiles : 0;
         const int64_t m0 = (un.tile - b * mtiles) * BM;
         for (int kt = un.k0; kt < un.k1; ++kt, ++it) {
@@ -231,7 +237,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     const long long unit = stage_tile[static_cast<int>(it % stages)];
     if (unit < 0) break;
-    const Unit un = decode_unit(unit, nfull, nk, khalf);
+    const Unit un = decode_unit(unit, nfull, nk, ks);
     TTM_STAMP_START(unit);
     const int64_t b = MC ? un.tile / mtiles : 0;
     const int64_t m0 = (un.tile - b * mtiles) * BM;
@@ -289,10 +295,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
     }
 
-    // ---------------- split tail tile: park this half, the second half to finish combines
-    if (un.half >= 0) {
+    // ---------------- split tile: park this chunk; the last chunk to finish combines
+    if (un.chunk >= 0) {
       const int64_t v = un.tile - nfull;
-      double* mine = part + ((v * 2 + un.half) * (NT * 2)) * (NWARP * 32) + threadIdx.x;
+      double* mine = part + ((v * ks + un.chunk) * (NT * 2)) * (NWARP * 32) + threadIdx.x;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         mine[(2 * j) * (NWARP * 32)] = acc[j][0];
@@ -302,17 +308,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       asm volatile("bar.sync 1, %0;" ::"r"(NWARP * 32) : "memory");   // consumer warps only
       if (threadIdx.x == 0) ticket_s = atomicAdd(tickets + v, 1u);
       asm volatile("bar.sync 1, %0;" ::"r"(NWARP * 32) : "memory");
-      if (ticket_s == 0) {   // the other half finishes the tile
+      if (ticket_s != ks - 1) {   // another chunk finishes the tile
         TTM_STAMP_END(unit);
         continue;
       }
       __threadfence();
-      const double* p0 = part + ((v * 2) * (NT * 2)) * (NWARP * 32) + threadIdx.x;
-      const double* p1 = p0 + (NT * 2) * (NWARP * 32);
+      const double* p0 = part + ((v * ks) * (NT * 2)) * (NWARP * 32) + threadIdx.x;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
-        acc[j][0] = __ldcg(p0 + (2 * j) * (NWARP * 32)) + __ldcg(p1 + (2 * j) * (NWARP * 32));
-        acc[j][1] = __ldcg(p0 + (2 * j + 1) * (NWARP * 32)) + __ldcg(p1 + (2 * j + 1) * (NWARP * 32));
+        acc[j][0] = __ldcg(p0 + (2 * j) * (NWARP * 32));
+        acc[j][1] = __ldcg(p0 + (2 * j + 1) * (NWARP * 32));
+      }
+      for (int c = 1; c < ks; ++c) {
+        const double* pc = p0 + c * (NT * 2) * (NWARP * 32);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          acc[j][0] += __ldcg(pc + (2 * j) * (NWARP * 32));
+          acc[j][1] += __ldcg(pc + (2 * j + 1) * (NWARP * 32));
+        }
       }
       if (threadIdx.x == 0) tickets[v] = 0u;
     }
@@ -451,16 +464,45 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
   }
   int64_t grid = static_cast<int64_t>(sms) * occ;
   if (grid > ntiles) grid = ntiles;
-  // a last wave at most half full is split into k halves (one wave of half-tiles)
-  const int64_t tail = ntiles % grid;
   const int nk = static_cast<int>((S + BK - 1) / BK);
-  const int64_t ntail = (ntiles > grid && tail > 0 && 2 * tail <= grid && tail <= TTM_MAX_TAIL &&
-                         nk >= 4) ? tail : 0;
-  const int64_t nfull = ntiles - ntail;
+  const int64_t slot = static_cast<int64_t>(NT) * 2 * NWARP * 32;   // doubles per parked chunk
+  int64_t nsplit = 0;
+  int ks = 1;
+  const int64_t full_grid = static_cast<int64_t>(sms) * occ;
+  if (ntiles < full_grid && nk >= 32 && ntiles <= TTM_TICKETS) {
+    // few tiles, long reduction (the multi-mode first level): split every tile into ks k
+    // chunks, the smallest ks whose units fill their last wave to >= 90% (else the fullest)
+    int best = 1;
+    double best_eff = 0.0;
+    for (int k = 2; k <= 32 && k <= nk / 8 && ntiles * k * slot <= TTM_PART; ++k) {
+      const double waves = static_cast<double>(ntiles * k) / full_grid;
+      const double eff = waves / std::ceil(waves);
+      if (eff > best_eff + 1e-9) {
+        best = k;
+        best_eff = eff;
+      }
+      if (eff >= 0.9) break;
+    }
+    ks = best;
+    if (ks > 1) {
+      nsplit = ntiles;
+      grid = full_grid < ntiles * ks ? full_grid : ntiles * ks;
+    } else {
+      ks = 1;
+    }
+  } else {
+    // a last wave at most half full is split into k halves (one wave of half-tiles)
+    const int64_t tail = ntiles % grid;
+    if (ntiles > grid && tail > 0 && 2 * tail <= grid && tail * 2 * slot <= TTM_PART && nk >= 4) {
+      nsplit = tail;
+      ks = 2;
+    }
+  }
+  const int64_t nfull = ntiles - nsplit;
   cudaError_t e0 = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
   if (e0 != cudaSuccess) return e0;
   ttm_dmma_kernel<NT, MC><<<(unsigned)grid, NTHREADS, smem, st>>>(
-      tmX, tmF, out, Mrows, mtiles, nfull, ntail, (int)S, K, stages, counter, tickets, part);
+      tmX, tmF, out, Mrows, mtiles, nfull, nsplit, ks, (int)S, K, stages, counter, tickets, part);
   note_launch();
   return cudaGetLastError();
 }
@@ -507,17 +549,57 @@ bool ttm_uses_dmma(int64_t B, int64_t S, int64_t R, int K, bool force_simt) {
 // padded factor width for K: 16-column TMA boxes
 int ttm_ld(int K) { return ((((K + 7) / 8) * 8 + 15) / 16) * 16; }
 
-// scratch layout (ttm_scratch_doubles): tile counter + tail tickets (256 doubles) | tail partial
-// sums | padded factor (S x ttm_ld(K)) -- the control words sit at a fixed offset, so launches
-// with different S never overwrite each other's tickets
-constexpr size_t TTM_CTL = 256;
-constexpr size_t TTM_PART = static_cast<size_t>(TTM_MAX_TAIL) * 2 * BM * 128;
 
 cudaError_t ttm_prepare(int64_t S, const double* F, int K, double* Fpad, cudaStream_t st) {
   return launch_pad_rows(F, S, K, Fpad + TTM_CTL + TTM_PART, ttm_ld(K), st);
 }
 
+// Khatri-Rao product of the factors of consecutive modes m_0 < ... < m_{h-1} (row-major over
+// (x_0, ..., x_{h-1}), last fastest; product in ascending j), written straight into the padded
+// factor area (ld = ttm_ld(K), zero columns past K): the multi-mode first level of the
+// dimension tree contracts X_(m_0..m_{h-1}) with it in one GEMM (P:78-80 with the contracted
+// modes of a half taken together; the MTTKRP definition).
+__global__ void krp_kernel(KrpArgs a, double* __restrict__ out) {
+  const int64_t total = a.rows * a.ld;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / a.ld;
+    const int k = static_cast<int>(e - row * a.ld);
+    if (k >= a.K) {
+      out[e] = 0.0;
+      continue;
+    }
+    int64_t x[CPPP_MAX_ORDER_];
+    int64_t r = row;
+    for (int j = a.nm - 1; j >= 0; --j) {
+      x[j] = r % a.dims[j];
+      r /= a.dims[j];
+    }
+    double v = 1.0;
+    for (int j = 0; j < a.nm; ++j) v *= __ldg(a.F[j] + x[j] * a.K + k);
+    out[e] = v;
+  }
+}
+
+cudaError_t ttm_prepare_krp(const KrpArgs& args, double* Fpad, cudaStream_t st) {
+  KrpArgs a = args;
+  a.ld = ttm_ld(a.K);
+  a.rows = 1;
+  for (int j = 0; j < a.nm; ++j) a.rows *= a.dims[j];
+  const int64_t total = a.rows * a.ld;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  krp_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, Fpad + TTM_CTL + TTM_PART);
+  note_launch();
+  return cudaGetLastError();
+}
+
 size_t ttm_scratch_doubles(int64_t S) { return TTM_CTL + TTM_PART + static_cast<size_t>(S) * 128; }
+
+cudaError_t launch_ttm_padded(const double* X, int64_t B, int64_t S, int64_t R, int K, double* out,
+                              const double* Fpad, cudaStream_t st) {
+  return launch_ttm_core(X, B, S, R, nullptr, K, out, Fpad, false, st);
+}
 
 cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
                             int K, double* out, const double* Fpad, bool force_simt,

@@ -23,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--flags", type=int, default=0, help="extra CPPP_FLAG_* bits")
     a = ap.parse_args()
     cfg = G.CONFIGS[a.config]
     stream = torch.cuda.current_stream()
@@ -30,8 +31,8 @@ def main():
     kind = {"none": 0, "abs": 1, "rel": 2}[cfg.noise_kind]
     cp.cppp_generate(X, cfg.dims, cfg.K, G.true_factors(cfg), kind, cfg.noise, 0, stream=stream)
     A0 = [torch.from_numpy(x).cuda() for x in G.initial_factors(cfg)]
-    for flags, name in ((cp.FLAG_BORROW_TENSOR, "plain"),
-                        (cp.FLAG_BORROW_TENSOR | cp.FLAG_PROFILE, "profile")):
+    for flags, name in ((cp.FLAG_BORROW_TENSOR | a.flags, "plain"),
+                        (cp.FLAG_BORROW_TENSOR | cp.FLAG_PROFILE | a.flags, "profile")):
         ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K, stream=stream, flags=flags)
         for r in range(a.reps + 2):
             cp.cp_set_factors(ctx, A0)

@@ -24,6 +24,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
     ap.add_argument("--sweeps", default="1,7,8")
+    ap.add_argument("--flags", type=int, default=0, help="extra CPPP_FLAG_* bits")
     a = ap.parse_args()
     want = {int(x) for x in a.sweeps.split(",")}
     cfg = G.CONFIGS[a.config]
@@ -33,7 +34,7 @@ def main():
     cp.cppp_generate(X, cfg.dims, cfg.K, G.true_factors(cfg), kind, cfg.noise, 0, stream=stream)
     A0 = [torch.from_numpy(x).cuda() for x in G.initial_factors(cfg)]
     ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K, stream=stream,
-                     flags=cp.FLAG_BORROW_TENSOR | cp.FLAG_PROFILE)
+                     flags=cp.FLAG_BORROW_TENSOR | cp.FLAG_PROFILE | a.flags)
     for _ in range(2):   # warm (graphs captured)
         cp.cp_set_factors(ctx, A0)
         for _ in range(cfg.sweeps):
