@@ -24,6 +24,8 @@
 #include <cuda.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 namespace cppp {
@@ -499,6 +501,11 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
     }
   }
   const int64_t nfull = ntiles - nsplit;
+  static const bool dbg = getenv("CPPP_DEBUG_TTM") != nullptr;
+  if (dbg)
+    fprintf(stderr, "ttm B %lld S %lld R %lld K %d: tiles %lld grid %lld split %lld x %d\n",
+            (long long)B, (long long)S, (long long)R, K, (long long)ntiles, (long long)grid,
+            (long long)nsplit, ks);
   cudaError_t e0 = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
   if (e0 != cudaSuccess) return e0;
   ttm_dmma_kernel<NT, MC><<<(unsigned)grid, NTHREADS, smem, st>>>(

@@ -13,6 +13,9 @@
 // block of one (b, tail, k) fibre set in shared memory and reduces it along each axis.
 #include "internal.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace cppp {
 namespace {
 
@@ -168,6 +171,10 @@ cudaError_t launch_ttv(const double* P, int64_t B, int64_t S, int64_t R, int K, 
   const int64_t ctas = (total / V + TTV_THREADS - 1) / TTV_THREADS;
   int xs = 1;
   while (xs < 8 && ctas * xs < 148LL * 2 && S / (2 * xs) >= 16) xs *= 2;
+  static const bool dbg = getenv("CPPP_DEBUG_TTM") != nullptr;
+  if (dbg)
+    fprintf(stderr, "ttv B %lld S %lld R %lld K %d: V %d xs %d\n", (long long)B, (long long)S,
+            (long long)R, K, V, xs);
   return launch_ttv_cfg(P, B, S, R, K, F, out, V, 4, xs, st);
 }
 

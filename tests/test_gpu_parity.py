@@ -194,3 +194,50 @@ def test_sweeps_large_rank(dims, K):
         cp.cp_set_phase_override(ctx, t["phase"])
         info = cp.als_sweep(ctx, 0.0, 0.5)
         assert abs(info["fitness"] - t["fitness"]) < 1e-8, (t, info)
+
+
+# ---- scheduling paths of the GEMM / TTV kernels: each shape is chosen to hit one
+# ---- path; the values must not depend on the path (parity with the oracle either way)
+@pytest.mark.parametrize("krp", [True, False])
+@pytest.mark.parametrize("dims,K", [((6, 7, 40, 42), 30), ((8, 6, 5, 4, 6, 5), 16),
+                                    ((12, 10, 9, 11, 8), 33)])
+def test_multimode_first_level_matches_single_mode_chain(dims, K, krp):
+    """Order >= 4: each DT half is contracted from X in one Khatri-Rao GEMM (default) or by a
+    single-mode TTM followed by multi-TTVs (CPPP_FLAG_NO_KRP); both equal the oracle MTTKRP."""
+    X, A = random_problem(dims, K, 11)
+    ctx = cp.cp_init(X, len(dims), dims, K, flags=0 if krp else cp.FLAG_NO_KRP)
+    cp.cp_set_factors(ctx, A)
+    M = cp.mttkrp_dt(ctx)
+    for n in range(len(dims)):
+        assert rel(M[n], O.mttkrp(X, A, n)) < TOL, (dims, K, n, krp)
+
+
+@pytest.mark.parametrize("dims,K", [
+    ((120, 160, 64), 24),      # 19200 / 128 = 150 output tiles: half-empty last wave -> k halves
+    ((100, 190, 64), 8),       # 148 tiles + 1 -> tail split with NT = 1
+    ((4, 4, 60, 64), 16),      # multi-mode GEMM, 1 tile, S = 3840: every tile in k chunks
+    ((6, 6, 50, 50), 100),     # 1 tile of 36 rows, S = 2500, NT = 13
+])
+def test_ttm_split_units_match_oracle(dims, K):
+    X, A = random_problem(dims, K, 12)
+    ctx = cp.cp_init(X, len(dims), dims, K)
+    cp.cp_set_factors(ctx, A)
+    M = cp.mttkrp_dt(ctx)
+    for n in range(len(dims)):
+        assert rel(M[n], O.mttkrp(X, A, n)) < TOL, (dims, K, n)
+    # and the same factors twice: the split tickets must be left reset by the first run
+    M2 = cp.mttkrp_dt(ctx)
+    for n in range(len(dims)):
+        assert np.array_equal(M[n], M2[n]), n
+
+
+@pytest.mark.parametrize("dims,K", [((300, 64, 64), 2), ((64, 256, 3), 9), ((17, 33, 400), 11)])
+def test_ttv_cluster_split_matches_oracle(dims, K):
+    """Small level-2 outputs split the contracted range over a (1, xs, 1) cluster reduced over
+    DSMEM (odd K exercises the 8-byte path)."""
+    X, A = random_problem(dims, K, 13)
+    ctx = cp.cp_init(X, len(dims), dims, K)
+    cp.cp_set_factors(ctx, A)
+    M = cp.mttkrp_dt(ctx)
+    for n in range(len(dims)):
+        assert rel(M[n], O.mttkrp(X, A, n)) < TOL, (dims, K, n)
