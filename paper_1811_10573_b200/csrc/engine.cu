@@ -1106,7 +1106,13 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
   CUCHK(c, cudaMallocHost(&c->host_stats, sizeof(double) * (3 * N + 8)));
   CUCHK(c, cudaEventCreate(&c->ev_a));
   CUCHK(c, cudaEventCreate(&c->ev_b));
-  CUCHK(c, cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+  {  // the side stream of the Γ factorizations gets the highest priority: its one-CTA kernel is
+     // on the critical path whenever M^(n) is cheap (PP sweeps), and must not queue behind the
+     // CTAs of the main stream's next kernel
+    int lo = 0, hi = 0;
+    CUCHK(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUCHK(c, cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, hi));
+  }
   CUCHK(c, cudaEventCreateWithFlags(&c->ev_S, cudaEventDisableTiming));
   CUCHK(c, cudaEventCreateWithFlags(&c->ev_P, cudaEventDisableTiming));
   // ||X||² (all-reduced)

@@ -7,6 +7,33 @@
 #define CPPP_MAX_TERMS_ 8
 #define CPPP_MAX_ORDER_ 8
 
+#include <utility>
+
+// Programmatic dependent launch: kernels started with launch_pdl may be scheduled while the
+// previous kernel on the stream drains (its launch latency and prologue overlap the tail); each
+// of them calls pdl_wait() before touching anything an earlier kernel wrote.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
+namespace cppp {
+bool pdl_enabled();   // false when CPPP_NO_PDL is set (A/B measurements)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+}  // namespace cppp
+
 namespace cppp {
 
 struct Dims {

@@ -13,6 +13,8 @@
 // per-row statistics; one warp per row) and one Gram kernel (S^(n), the fixed-order sums).
 #include "internal.h"
 
+#include <cstdlib>
+
 namespace cppp {
 #ifdef CPPP_PROBE_CYCLES   // tools/probe_solve only: per-phase clock64 deltas of CTA 0, thread 0
 __device__ long long g_probe_cycles[16];
@@ -87,6 +89,7 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
     gamma_chol_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
                       double* Tp, int ldt, int* mode) {
   PROBE_T0();
+  pdl_wait();
   __shared__ __align__(16) double colb[2][128];
   __shared__ double rdv[2];
   __shared__ int bad_s;
@@ -207,6 +210,7 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
 __global__ void __launch_bounds__(GP_THREADS, 1)
     gamma_pinv_kernel(int K, const double* __restrict__ Gamma, double* Pout, int ldt,
                       const int* mode, double* Vscratch) {
+  pdl_wait();
   if (*mode == 0) return;
   extern __shared__ double W[];  // K x (K+1)
   __shared__ double sh[32];
@@ -368,6 +372,7 @@ __global__ void __launch_bounds__(SR_WARPS * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();
   if (threadIdx.x == 0) {
     bar_expect(&bar, gamma_in_smem ? 2 * tbytes : tbytes);
     bulk_to_smem(Ts, Tp, tbytes, &bar);
@@ -552,6 +557,7 @@ __global__ void __launch_bounds__(GR_THREADS)
                 const double* __restrict__ Gm, int ldt, double* fit, double* scratch,
                 unsigned int* counters) {
   PROBE_T0();
+  pdl_wait();
   extern __shared__ __align__(16) double gsm[];   // [2 strips][GR_ROWS / 2][16][2]
   __shared__ double sh[32];
   __shared__ int last_s;
@@ -701,6 +707,7 @@ __global__ void sub_kernel(const double* a, const double* b, double* y, int64_t 
 }
 
 __global__ void pad_rows_kernel(const double* F, int64_t S, int K, double* Fp, int ld) {
+  pdl_wait();
   const int64_t total = S * ld;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -718,6 +725,11 @@ int grid_for(int64_t n, int threads, int cap) {
 }
 
 }  // namespace
+
+bool pdl_enabled() {
+  static const bool on = getenv("CPPP_NO_PDL") == nullptr;
+  return on;
+}
 
 static unsigned long long g_launches = 0;
 void note_launch() { __atomic_add_fetch(&g_launches, 1ull, __ATOMIC_RELAXED); }
@@ -737,13 +749,14 @@ cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  gamma_chol_kernel<<<1, GF_THREADS, 0, st>>>(S_all, N, n, K, Gamma, Tp, ldt, mode);
+  cudaError_t e = launch_pdl(gamma_chol_kernel, dim3(1), dim3(GF_THREADS), 0, st, S_all, N, n, K,
+                             Gamma, Tp, ldt, mode);
   note_launch();
-  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  gamma_pinv_kernel<<<1, GP_THREADS, smem, st>>>(K, Gamma, Tp, ldt, mode, Vscratch);
+  e = launch_pdl(gamma_pinv_kernel, dim3(1), dim3(GP_THREADS), smem, st, K,
+                 static_cast<const double*>(Gamma), Tp, ldt, static_cast<const int*>(mode), Vscratch);
   note_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, double* dA,
@@ -764,11 +777,10 @@ cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, dou
     attr = true;
   }
   const int64_t blocks = (rows + SR_WARPS - 1) / SR_WARPS;
-  solve_rows_kernel<<<(unsigned)blocks, SR_WARPS * 32, smem, st>>>(M, A, ref, dA, rows, K, Gamma,
-                                                                   Tp, ldt, both ? 1 : 0, mode,
-                                                                   rowstat);
+  cudaError_t e = launch_pdl(solve_rows_kernel, dim3((unsigned)blocks), dim3(SR_WARPS * 32), smem,
+                             st, M, A, ref, dA, rows, K, Gamma, Tp, ldt, both ? 1 : 0, mode, rowstat);
   note_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 int gram_tiles(int K) {
@@ -793,11 +805,11 @@ cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, const d
   const int64_t cap = GR_MAX_CTAS / nt;
   if (ns > cap) ns = cap;
   if (ns < 1) ns = 1;
-  gram_kernel<<<(unsigned)(nt * ns), GR_THREADS, GR_SMEM, st>>>(A, rows, K, (int)ns, S, rowstat,
-                                                                nrm, Gamma_model, solve_ld(K), fit,
-                                                                scratch, counters);
+  cudaError_t e = launch_pdl(gram_kernel, dim3((unsigned)(nt * ns)), dim3(GR_THREADS), GR_SMEM, st,
+                             A, rows, K, (int)ns, S, rowstat, nrm, Gamma_model, solve_ld(K), fit,
+                             scratch, counters);
   note_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 int sqnorm_blocks(int64_t n) { return grid_for(n, 256, 1184); }
@@ -822,9 +834,10 @@ cudaError_t launch_sub(const double* a, const double* b, double* y, int64_t n, c
 
 cudaError_t launch_pad_rows(const double* F, int64_t S, int K, double* Fp, int ld,
                             cudaStream_t st) {
-  pad_rows_kernel<<<grid_for(S * ld, 256, 1184), 256, 0, st>>>(F, S, K, Fp, ld);
+  cudaError_t e = launch_pdl(pad_rows_kernel, dim3(grid_for(S * ld, 256, 1184)), dim3(256), 0, st,
+                             F, S, K, Fp, ld);
   note_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace cppp

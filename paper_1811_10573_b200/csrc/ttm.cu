@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();   // X, the padded factor and the scheduler words come from earlier kernels
   const int nk = (S + BK - 1) / BK;
   const long long nunits = nfull + static_cast<long long>(ks) * nsplit;
 
@@ -366,6 +367,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     TTM_STAMP_END(unit);
   }
+  // the last CTA out resets the scheduler words for the next launch (no memset node, so
+  // consecutive launches keep their programmatic dependency)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(tile_counter + 1, 1ull) == gridDim.x - 1) {
+      tile_counter[0] = 0ull;
+      tile_counter[1] = 0ull;
+      __threadfence();
+    }
+  }
 }
 
 // ---------------------------------------------------------------- SIMT fallback
@@ -506,12 +517,11 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
     fprintf(stderr, "ttm B %lld S %lld R %lld K %d: tiles %lld grid %lld split %lld x %d\n",
             (long long)B, (long long)S, (long long)R, K, (long long)ntiles, (long long)grid,
             (long long)nsplit, ks);
-  cudaError_t e0 = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
-  if (e0 != cudaSuccess) return e0;
-  ttm_dmma_kernel<NT, MC><<<(unsigned)grid, NTHREADS, smem, st>>>(
-      tmX, tmF, out, Mrows, mtiles, nfull, nsplit, ks, (int)S, K, stages, counter, tickets, part);
+  cudaError_t e = launch_pdl(ttm_dmma_kernel<NT, MC>, dim3((unsigned)grid), dim3(NTHREADS), smem, st,
+                             tmX, tmF, out, Mrows, mtiles, nfull, nsplit, ks, (int)S, K, stages,
+                             counter, tickets, part);
   note_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 template <bool MC, int NT = 1>
@@ -567,6 +577,7 @@ cudaError_t ttm_prepare(int64_t S, const double* F, int K, double* Fpad, cudaStr
 // dimension tree contracts X_(m_0..m_{h-1}) with it in one GEMM (P:78-80 with the contracted
 // modes of a half taken together; the MTTKRP definition).
 __global__ void krp_kernel(KrpArgs a, double* __restrict__ out) {
+  pdl_wait();
   const int64_t total = a.rows * a.ld;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -596,9 +607,10 @@ cudaError_t ttm_prepare_krp(const KrpArgs& args, double* Fpad, cudaStream_t st) 
   const int64_t total = a.rows * a.ld;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  krp_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, Fpad + TTM_CTL + TTM_PART);
+  cudaError_t e = launch_pdl(krp_kernel, dim3((unsigned)blocks), dim3(256), 0, st, a,
+                             Fpad + TTM_CTL + TTM_PART);
   note_launch();
-  return cudaGetLastError();
+  return e;
 }
 
 size_t ttm_scratch_doubles(int64_t S) { return TTM_CTL + TTM_PART + static_cast<size_t>(S) * 128; }

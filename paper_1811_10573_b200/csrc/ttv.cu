@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(TTV_THREADS)
     ttv_kernel(const double* __restrict__ P, int64_t S, int64_t RK, int K, int64_t nvec,
                const double* __restrict__ F, double* __restrict__ out) {
   using T = typename Vec<V>::T;
+  pdl_wait();
   __shared__ T red[TTV_THREADS];
   const int64_t e = blockIdx.x * (int64_t)TTV_THREADS + threadIdx.x;   // vector index
   const int p = blockIdx.y, xs = gridDim.y;
@@ -130,13 +131,15 @@ cudaError_t launch_v(const double* P, int64_t S, int64_t RK, int K, int64_t tota
   cfg.blockDim = dim3(TTV_THREADS, 1, 1);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = (unsigned)xs;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see launch_pdl
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, ttv_kernel<V, U>, P, S, RK, K, nvec, F, out);
   note_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
