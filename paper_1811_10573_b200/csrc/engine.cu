@@ -666,11 +666,12 @@ cppp_status run_pp_build(cppp_ctx* c) {
 }
 
 // One PP term list for mode n (operator reads per L5: (i,n) is the transpose of (n,i)).
-void pp_terms(cppp_ctx* c, int n, bool skip_q, PPUpdateArgs* a) {
+// terms i with dA^(i) known to be exactly zero (zero_mask bit i) are left out: they add +0.0
+void pp_terms(cppp_ctx* c, int n, bool skip_q, PPUpdateArgs* a, uint32_t zero_mask = 0u) {
   const int K = c->K;
   a->nterms = 0;
   for (int i = 0; i < c->N; ++i) {
-    if (i == n || (skip_q && i == c->q)) continue;
+    if (i == n || (skip_q && i == c->q) || (zero_mask & (1u << i))) continue;
     PPTerm t;
     const int lo = std::min(i, n), hi = std::max(i, n);
     t.op = c->ops[lo][hi];
@@ -688,7 +689,7 @@ void pp_terms(cppp_ctx* c, int n, bool skip_q, PPUpdateArgs* a) {
 }
 
 cppp_status pp_update_mode(cppp_ctx* c, int n, double* out, const double* extra, bool skip_q,
-                           const double* Mp) {
+                           const double* Mp, uint32_t zero_mask = 0u) {
   if (c->dry) return CPPP_OK;
   PPUpdateArgs a;
   a.Mp = Mp;
@@ -697,7 +698,7 @@ cppp_status pp_update_mode(cppp_ctx* c, int n, double* out, const double* extra,
   a.K = c->K;
   a.out = out;
   a.partial = c->pp_partial;
-  pp_terms(c, n, skip_q, &a);
+  pp_terms(c, n, skip_q, &a, zero_mask);
   double bytes = 8.0 * (2.0 * a.ny * a.K);
   double flops = 0.0;
   for (int i = 0; i < a.nterms; ++i) {
@@ -711,14 +712,24 @@ cppp_status pp_update_mode(cppp_ctx* c, int n, double* out, const double* extra,
 
 // PP sweep (Alg. 3).  Sharded: the mode-q terms of the other modes depend only on
 // dA^(q) (mode q is updated first), so they are formed once and all-reduced once (SURVEY C-c).
-cppp_status run_pp_sweep(cppp_ctx* c) {
+// after_build: the sweep that follows a PP build starts from A = A_p, so dA^(i) = 0 for every
+// mode not yet updated in this sweep (i > n); those terms are left out, and the first mode's
+// M~ is M_p itself (no launch).
+cppp_status run_pp_sweep(cppp_ctx* c, bool after_build) {
   const int N = c->N;
   const bool sh = c->q >= 0 && c->world > 1;
   for (int n = 0; n < N; ++n) {
     const double* extra = nullptr;
     if (sh && n != c->q) extra = c->T[n];
-    STCHK(pp_update_mode(c, n, c->M[n], extra, sh && n != c->q, c->Mp[n]));
-    STCHK(finish_mode(c, n, c->M[n], true));
+    uint32_t zero = 0u;
+    if (after_build)
+      for (int i = n + 1; i < N; ++i) zero |= 1u << i;
+    if (after_build && n == 0 && extra == nullptr) {   // every term is zero: M~^(0) = M_p^(0)
+      STCHK(finish_mode(c, n, c->Mp[n], true));
+    } else {
+      STCHK(pp_update_mode(c, n, c->M[n], extra, sh && n != c->q, c->Mp[n], zero));
+      STCHK(finish_mode(c, n, c->M[n], true));
+    }
     if (sh && n == c->q) {
       // T_m = M_p^(q,m) ×_q dA^(q) (partial over local rows) for every m != q
       for (int m = 0; m < N; ++m) {
@@ -758,7 +769,7 @@ cppp_status run_phase_eager(cppp_ctx* c, int phase) {
     STCHK(run_dt(c, true, c->M));
   } else {
     if (phase == CPPP_PHASE_PP_BUILD) STCHK(run_pp_build(c));
-    STCHK(run_pp_sweep(c));
+    STCHK(run_pp_sweep(c, phase == CPPP_PHASE_PP_BUILD));
   }
   return CPPP_OK;
 }

@@ -370,14 +370,14 @@ __global__ void __launch_bounds__(SR_WARPS * 32, 1)
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  pdl_wait();
-  if (threadIdx.x == 0) {
+    // Tp and Γ come from the factorization (a full, event dependency): stage them before the
+    // programmatic wait on the kernel that produced M
     bar_expect(&bar, gamma_in_smem ? 2 * tbytes : tbytes);
     bulk_to_smem(Ts, Tp, tbytes, &bar);
     if (gamma_in_smem) bulk_to_smem(Gs, Gamma, tbytes, &bar);
   }
+  __syncthreads();
+  pdl_wait();
   const int64_t y = blockIdx.x * (int64_t)SR_WARPS + w;
   const bool valid = y < rows;
   double m[4], m0[4], aold[4], rf[4];

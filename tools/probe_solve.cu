@@ -14,7 +14,8 @@ __global__ void spin(double* o, int n) {
   if (a == 0.5) o[0] = a;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int only_k = argc > 1 ? atoi(argv[1]) : 0;
   using namespace cppp;
   {
     double* o;
@@ -23,6 +24,7 @@ int main() {
     cudaDeviceSynchronize();
   }
   for (int K : {10, 30, 50, 100, 128}) {
+    if (only_k && K != only_k) continue;
     const int N = 3, s = 400;
     std::vector<double> A(s * K), S(N * K * K);
     srand(1);

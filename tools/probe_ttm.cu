@@ -17,18 +17,21 @@ __global__ void spin(double* o, int n) {
 
 int main(int argc, char** argv) {
   using namespace cppp;
-  const int64_t s = argc > 1 ? atoll(argv[1]) : 400;
-  const int K = argc > 2 ? atoi(argv[2]) : 100;
-  const int mc = argc > 3 ? atoi(argv[3]) : 0;   // 0: contract the last mode, 1: the first
-  const int64_t B = mc ? 1 : s * s, R = mc ? s * s : 1, S = s;
+  // probe_ttm B S R K   (X viewed as [B][S][R]; R == 1 contracts the last mode)
+  const int64_t B = argc > 1 ? atoll(argv[1]) : 160000;
+  const int64_t S = argc > 2 ? atoll(argv[2]) : 400;
+  const int64_t R = argc > 3 ? atoll(argv[3]) : 1;
+  const int K = argc > 4 ? atoi(argv[4]) : 100;
+  const int mc = R > 1;
+  const int64_t s = S;
   double *X, *F, *out, *scr, *o;
-  cudaMalloc(&X, 8 * s * s * s);
+  cudaMalloc(&X, 8 * B * S * R);
   cudaMalloc(&F, 8 * S * K);
   cudaMalloc(&out, 8 * B * R * K);
   const size_t nscr = ttm_scratch_doubles(S);
   cudaMalloc(&scr, 8 * nscr);
   cudaMemset(scr, 0, 8 * nscr);
-  cudaMemset(X, 0, 8 * s * s * s);
+  cudaMemset(X, 0, 8 * B * S * R);
   cudaMemset(F, 0, 8 * S * K);
   cudaMalloc(&o, 8);
   for (int r = 0; r < 20; ++r) spin<<<148 * 8, 256>>>(o, 1 << 16);
@@ -67,9 +70,10 @@ int main(int argc, char** argv) {
   std::vector<double> d2 = dur;
   std::sort(d2.begin(), d2.end());
   const double flops = 2.0 * B * R * S * K;
-  printf("s %lld K %d mc %d: %.1f us (event), span %.1f us, %.2f TF/s; tiles %lld units %d SMs %zu\n",
-         (long long)s, K, mc, ms * 1e3, (t1 - t0) * 1e-3, flops / (ms * 1e-3) / 1e12,
-         (long long)ntiles, nunits, ends.size());
+  const double bytes = 8.0 * (B * S * R + B * R * K);
+  printf("B %lld S %lld R %lld K %d: %.1f us (event), span %.1f us, %.2f TF/s, %.0f GB/s; tiles %lld units %d SMs %zu\n",
+         (long long)B, (long long)S, (long long)R, K, ms * 1e3, (t1 - t0) * 1e-3,
+         flops / (ms * 1e-3) / 1e12, bytes / (ms * 1e-3) / 1e9, (long long)ntiles, nunits, ends.size());
   printf("  SM end times: min %.1f p10 %.1f median %.1f p90 %.1f max %.1f us\n", ends.front(),
          ends[ends.size() / 10], ends[ends.size() / 2], ends[ends.size() * 9 / 10], ends.back());
   printf("  unit durations: min %.2f median %.2f p90 %.2f max %.2f us; first unit %.2f us\n", d2.front(),
