@@ -131,6 +131,14 @@ size_t cppp_workspace_bytes(int N, const int64_t *s, int K, const cppp_opts *o);
 cppp_status cp_init(cppp_ctx **ctx, const double *X, int N, const int64_t *s, int K,
                     const cppp_opts *o);
 
+/* Replace the tensor of an existing context with a new one of the same shape (host or device
+ * pointer, same slab), recompute ||X||_F^2, and drop the factors and the PP state (call
+ * cp_set_factors next).  Keeps the workspace and the captured sweep graphs, so a serving loop
+ * can alternate two contexts: the next tensor uploads on one context's stream while the other
+ * runs its sweeps.  A context created with CPPP_FLAG_BORROW_TENSOR accepts only its own
+ * borrowed pointer (after the caller rewrote that buffer); any other pointer -> CPPP_ESTATE. */
+cppp_status cp_load_tensor(cppp_ctx *ctx, const double *X);
+
 /* Set A^(n) for n = 0..N-1 (A[n] is s_n x K, GLOBAL rows even when sharded), reset the PP
  * state (no operators), the sweep counter and the phase machine (next sweep is DT, L9). */
 cppp_status cp_set_factors(cppp_ctx *ctx, const double *const *A);

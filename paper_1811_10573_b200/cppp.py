@@ -81,6 +81,7 @@ def lib():
         "cppp_default_opts": (V, [C.POINTER(Opts)]),
         "cppp_workspace_bytes": (C.c_size_t, [I, C.POINTER(C.c_int64), I, C.POINTER(Opts)]),
         "cp_init": (I, [C.POINTER(P), P, I, C.POINTER(C.c_int64), I, C.POINTER(Opts)]),
+        "cp_load_tensor": (I, [P, P]),
         "cp_set_factors": (I, [P, C.POINTER(P)]),
         "cp_get_factors": (I, [P, C.POINTER(P)]),
         "cp_update_factors": (I, [P, C.POINTER(P)]),
@@ -112,7 +113,7 @@ def lib():
     return L
 
 
-EXPORTED = ["cppp_default_opts", "cppp_workspace_bytes", "cp_init", "cp_set_factors",
+EXPORTED = ["cppp_default_opts", "cppp_workspace_bytes", "cp_init", "cp_load_tensor", "cp_set_factors",
             "cp_update_factors",
             "cp_get_factors", "mttkrp_dt", "pp_build_operators", "pp_get_operator",
             "pp_get_single", "pp_update", "als_sweep", "cp_set_phase_override", "fitness",
@@ -220,6 +221,14 @@ def cp_init(X, N: int, s: Sequence[int], K: int, *, device: int = 0, stream=None
     if shard_extent is not None:
         ctx.local_rows[0] = int(shard_extent)
     return ctx
+
+
+def cp_load_tensor(ctx: Ctx, X) -> None:
+    """cp_load_tensor (include/cppp.h): a new tensor of the same shape (numpy host array or torch
+    CUDA tensor) into an existing context; call cp_set_factors next."""
+    if hasattr(X, "data_ptr"):
+        ctx.keep.append(X)
+    _check(ctx, lib().cp_load_tensor(ctx.h, _ptr(X)))
 
 
 def cp_set_factors(ctx: Ctx, A: Sequence) -> None:
@@ -332,6 +341,7 @@ def cp_destroy(ctx: Ctx) -> None:
     if ctx is not None and ctx.h:
         lib().cp_destroy(ctx.h)
         ctx.h = C.c_void_p()
+        ctx.keep.clear()   # the borrowed tensor and the torch workspace can go now
 
 
 def cppp_launch_count() -> int:

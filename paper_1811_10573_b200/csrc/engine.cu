@@ -125,6 +125,7 @@ struct cppp_ctx {
   double normX_sq = 0.0;
   bool ops_valid = false;
   bool factors_set = false;
+  bool borrowed = false;        // X is the caller's device buffer (CPPP_FLAG_BORROW_TENSOR)
   int next_phase = CPPP_PHASE_DT;
   int override_phase = CPPP_PHASE_AUTO;
   int sweep = 0, restarts = 0;
@@ -823,6 +824,23 @@ cppp_status run_phase(cppp_ctx* c, int phase) {
   return CPPP_OK;
 }
 
+// ||X||² (all-reduced), kept on the host for the fitness (L17)
+cppp_status tensor_norm(cppp_ctx* c) {
+  const int N = c->N;
+  {
+    Prof pr(c, CPPP_K_OTHER, 2.0 * c->numel_local, 8.0 * c->numel_local);
+    const int nb = sqnorm_blocks(c->numel_local);
+    CUCHK(c, launch_sqnorm(c->X, c->numel_local, c->sq_partial, nb, c->stats + 3 * N + 2, c->st));
+  }
+  STCHK(allreduce(c, c->stats + 3 * N + 2, 1));
+  CUCHK(c, cudaMemcpyAsync(c->host_stats, c->stats + 3 * N + 2, sizeof(double),
+                           cudaMemcpyDeviceToHost, c->st));
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  prof_collect(c);
+  c->normX_sq = c->host_stats[0];
+  return CPPP_OK;
+}
+
 // ---------------------------------------------------------------- workspace plan
 struct Plan {
   size_t total = 0;
@@ -966,8 +984,15 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Host sources go up in 16 MiB pieces: the copy engine serves its queue in order, so a large
+// upload for one context (the next tensor of a serving loop) must not hold a small transfer of
+// another context (its factors) for the whole 0.5-32 GB copy.
 cppp_status copy_in(cppp_ctx* c, double* dst, const double* src, size_t n) {
-  CUCHK(c, cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDefault, c->st));
+  const size_t chunk = is_device_ptr(src) ? n : (size_t(16) << 20) / sizeof(double);
+  for (size_t o = 0; o < n; o += chunk) {
+    const size_t m = std::min(chunk, n - o);
+    CUCHK(c, cudaMemcpyAsync(dst + o, src + o, m * sizeof(double), cudaMemcpyDefault, c->st));
+  }
   return CPPP_OK;
 }
 cppp_status copy_out(cppp_ctx* c, double* dst, const double* src, size_t n) {
@@ -1110,6 +1135,7 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
   c->ws_bytes -= ALIGN;
   if (borrow) c->X = const_cast<double*>(X);
   STCHK(assign_buffers(c, borrow, &p));
+  c->borrowed = borrow;
   if (!borrow) STCHK(copy_in(c, c->X, X, (size_t)c->numel_local));
   CUCHK(c, cudaMemsetAsync(c->ws + (borrow ? 0 : align_up(sizeof(double) * c->numel_local)), 0,
                            p.off_stack - (borrow ? 0 : align_up(sizeof(double) * c->numel_local)),
@@ -1126,18 +1152,23 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
   }
   CUCHK(c, cudaEventCreateWithFlags(&c->ev_S, cudaEventDisableTiming));
   CUCHK(c, cudaEventCreateWithFlags(&c->ev_P, cudaEventDisableTiming));
-  // ||X||² (all-reduced)
-  {
-    Prof pr(c, CPPP_K_OTHER, 2.0 * c->numel_local, 8.0 * c->numel_local);
-    const int nb = sqnorm_blocks(c->numel_local);
-    CUCHK(c, launch_sqnorm(c->X, c->numel_local, c->sq_partial, nb, c->stats + 3 * N + 2, c->st));
+  return tensor_norm(c);
+}
+
+cppp_status cp_load_tensor(cppp_ctx* c, const double* X) {
+  if (!c) return CPPP_EINVAL;
+  if (!X) return fail(c, CPPP_EINVAL, "null tensor");
+  STCHK(drain_prefetch(c));
+  if (c->borrowed) {
+    if (X != c->X)
+      return fail(c, CPPP_ESTATE, "borrowed tensor: rewrite the borrowed buffer instead");
+  } else {
+    STCHK(copy_in(c, c->X, X, (size_t)c->numel_local));
   }
-  STCHK(allreduce(c, c->stats + 3 * N + 2, 1));
-  CUCHK(c, cudaMemcpyAsync(c->host_stats, c->stats + 3 * N + 2, sizeof(double),
-                           cudaMemcpyDeviceToHost, c->st));
-  CUCHK(c, cudaStreamSynchronize(c->st));
-  c->normX_sq = c->host_stats[0];
-  return CPPP_OK;
+  c->factors_set = false;
+  c->ops_valid = false;
+  c->next_phase = CPPP_PHASE_DT;
+  return tensor_norm(c);
 }
 
 cppp_status cp_set_factors(cppp_ctx* c, const double* const* A) {

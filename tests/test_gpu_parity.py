@@ -241,3 +241,32 @@ def test_ttv_cluster_split_matches_oracle(dims, K):
     M = cp.mttkrp_dt(ctx)
     for n in range(len(dims)):
         assert rel(M[n], O.mttkrp(X, A, n)) < TOL, (dims, K, n)
+
+
+def test_load_tensor_replaces_the_tensor():
+    """cp_load_tensor: a second tensor of the same shape in an existing context (host and device
+    sources) gives the oracle's MTTKRP and sweep trace for that tensor; the graphs captured for
+    the first tensor keep working."""
+    cfg = G.CONFIGS["C2mini"]
+    X1, A0 = G.make_tensor(cfg, 0), G.initial_factors(cfg, 0)
+    X2 = G.make_tensor(cfg, 1)
+    ctx = cp.cp_init(X1, cfg.N, cfg.dims, cfg.K)
+    cp.cp_set_factors(ctx, A0)
+    for _ in range(4):
+        cp.als_sweep(ctx, 0.0, cfg.eps_pp)
+    for src in (X2, torch.from_numpy(X2.ravel().copy()).cuda()):
+        cp.cp_load_tensor(ctx, src)
+        cp.cp_set_factors(ctx, A0)
+        M = cp.mttkrp_dt(ctx)
+        for n in range(cfg.N):
+            assert rel(M[n], O.mttkrp(X2, A0, n)) < TOL, n
+        cp.cp_set_factors(ctx, A0)
+        _, tr = O.pp_cp_als(X2, A0, 0.0, cfg.eps_pp, 8)
+        for t in tr:
+            cp.cp_set_phase_override(ctx, t["phase"])
+            info = cp.als_sweep(ctx, 0.0, cfg.eps_pp)
+            assert abs(info["fitness"] - t["fitness"]) < 1e-8, (t, info)
+    b = cp.cp_init(torch.from_numpy(X1.ravel().copy()).cuda(), cfg.N, cfg.dims, cfg.K,
+                   flags=cp.FLAG_BORROW_TENSOR)
+    with pytest.raises(cp.CpppError):
+        cp.cp_load_tensor(b, X2)
