@@ -217,9 +217,9 @@ def main():
                      nccl_unique_id=nccl_id, rank=rank, world=world, **shard)
     A0_dev = [torch.from_numpy(a).cuda() for a in A0]
 
-    def step():
+    def step():   # one CP-ALS-PP run: als_run = every sweep in one device launch (Alg. 3 on device)
         cp.cp_set_factors(ctx, A0_dev)
-        return [cp.als_sweep(ctx, 0.0, cfg.eps_pp) for _ in range(sweeps)]
+        return cp.als_run(ctx, 0.0, cfg.eps_pp, sweeps)
 
     for _ in range(max(args.warmup, 0)):
         infos = step()
@@ -348,8 +348,7 @@ def main():
         def run(c2, set_factors=False):
             if set_factors:
                 cp.cp_set_factors(c2, A0h)
-            for _ in range(sweeps):
-                cp.als_sweep(c2, 0.0, cfg.eps_pp)
+            cp.als_run(c2, 0.0, cfg.eps_pp, sweeps)
             cp.cp_get_factors(c2, out=outh)
             return cp.fitness(c2)
 

@@ -170,6 +170,15 @@ cppp_status pp_update(cppp_ctx *ctx, int n, double *M_tilde);
  * machine unless cp_set_phase_override forces it.  eps: global stop on Σ||G||;
  * eps_pp: PP tolerance on the relative factor change.  info may be NULL. */
 cppp_status als_sweep(cppp_ctx *ctx, double eps, double eps_pp, cppp_sweep_info *info);
+/* Up to max_sweeps (<= 1024) sweeps of Alg. 3 in ONE device launch: the phase decisions that
+ * als_sweep takes on the host after every sweep (L7-L11) are taken by a kernel on the device, and
+ * a CUDA graph with a WHILE node over a SWITCH of the three phase graphs runs the sweeps back to
+ * back.  Stops early once grad_norm_sum <= eps.  info[0..*done) (may be NULL) gets the per-sweep
+ * records (seconds = the run's device time / *done).  Same results as the same number of
+ * als_sweep calls; falls back to those calls with CPPP_FLAG_PROFILE, CPPP_FLAG_NO_GRAPH, several
+ * ranks, or a phase override. */
+cppp_status als_run(cppp_ctx *ctx, double eps, double eps_pp, int max_sweeps,
+                    cppp_sweep_info *info, int *done);
 /* Force the phase of the next sweeps (CPPP_PHASE_AUTO to release); used to replay the
  * oracle's phase schedule in parity runs (L12). */
 cppp_status cp_set_phase_override(cppp_ctx *ctx, int phase);

@@ -91,6 +91,7 @@ def lib():
         "pp_get_single": (I, [P, I, P]),
         "pp_update": (I, [P, I, P]),
         "als_sweep": (I, [P, D, D, C.POINTER(SweepInfo)]),
+        "als_run": (I, [P, D, D, I, C.POINTER(SweepInfo), C.POINTER(I)]),
         "cp_set_phase_override": (I, [P, I]),
         "fitness": (I, [P, C.POINTER(D)]),
         "cppp_kernel_stats": (I, [P, I, C.POINTER(KernelStat)]),
@@ -116,7 +117,7 @@ def lib():
 EXPORTED = ["cppp_default_opts", "cppp_workspace_bytes", "cp_init", "cp_load_tensor", "cp_set_factors",
             "cp_update_factors",
             "cp_get_factors", "mttkrp_dt", "pp_build_operators", "pp_get_operator",
-            "pp_get_single", "pp_update", "als_sweep", "cp_set_phase_override", "fitness",
+            "pp_get_single", "pp_update", "als_sweep", "als_run", "cp_set_phase_override", "fitness",
             "cppp_kernel_stats", "cppp_reset_kernel_stats", "cppp_generate",
             "cppp_nccl_unique_id", "cppp_plan_describe", "cp_destroy", "cp_last_error",
             "cppp_status_string", "cppp_version", "cppp_launch_count"]
@@ -282,6 +283,14 @@ def als_sweep(ctx: Ctx, eps: float, eps_pp: float) -> dict:
     info = SweepInfo()
     _check(ctx, lib().als_sweep(ctx.h, eps, eps_pp, C.byref(info)))
     return info.as_dict()
+
+
+def als_run(ctx: Ctx, eps: float, eps_pp: float, max_sweeps: int) -> list:
+    """als_run (include/cppp.h): up to max_sweeps sweeps in one device launch; per-sweep dicts."""
+    infos = (SweepInfo * max(max_sweeps, 1))()
+    done = C.c_int(0)
+    _check(ctx, lib().als_run(ctx.h, eps, eps_pp, max_sweeps, infos, C.byref(done)))
+    return [infos[i].as_dict() for i in range(done.value)]
 
 
 def cp_set_phase_override(ctx: Ctx, phase) -> None:

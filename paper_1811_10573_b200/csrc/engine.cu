@@ -155,6 +155,28 @@ struct cppp_ctx {
     int uses = 0;
     uint64_t launches = 0;   // kernel nodes captured (credited to cppp_launch_count per replay)
   } graphs[3];
+  // als_run: one graph for a whole run (a device-side WHILE over sweeps, a SWITCH over phases)
+  struct RunGraph {
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphConditionalHandle hw = 0, hs = 0;
+    uint64_t launches_per_sweep[3] = {0, 0, 0};
+    bool failed = false;   // capture not possible here: als_run falls back to als_sweep calls
+  } run;
+  struct RunState* run_dev = nullptr;   // device (workspace)
+  struct RunState* run_host = nullptr;  // pinned
+};
+
+// Device-side Alg. 3 phase machine state for als_run (the same decisions als_sweep takes on the
+// host, L7-L11, same IEEE operations in the same order).
+struct RunInfo {
+  double fitness, residual_sq, gsum, maxrel;
+  int phase, next_phase, restarts, converged;
+};
+constexpr int RUN_MAX = 1024;   // sweeps per als_run call
+struct RunState {
+  double eps, eps_pp, normX_sq;
+  int max_sweeps, done, phase, restarts, N, pad;
+  RunInfo info[RUN_MAX];
 };
 
 namespace {
@@ -841,6 +863,144 @@ cppp_status tensor_norm(cppp_ctx* c) {
   return CPPP_OK;
 }
 
+
+// ---------------------------------------------------------------- als_run: the device loop
+// A run of sweeps as ONE graph launch: run_prologue_kernel arms a WHILE node; its body is a
+// SWITCH over the three phase graphs (the same captured sweeps als_sweep replays) followed by
+// run_decide_kernel, which takes Alg. 3's decision on the device (the statistics als_sweep
+// reads back to the host) and sets both conditions.  No host round trip per sweep.
+__global__ void run_prologue_kernel(RunState* rs, cudaGraphConditionalHandle hw,
+                                    cudaGraphConditionalHandle hs) {
+  cudaGraphSetConditional(hs, static_cast<unsigned>(rs->phase));
+  cudaGraphSetConditional(hw, rs->max_sweeps > 0 ? 1u : 0u);
+}
+
+__global__ void run_decide_kernel(RunState* rs, const double* __restrict__ stats,
+                                  cudaGraphConditionalHandle hw, cudaGraphConditionalHandle hs) {
+  // the operations and their order are those of als_sweep (host), no contraction
+  const int N = rs->N;
+  double maxrel = 0.0, gsum = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double na = stats[3 * n], nd = stats[3 * n + 1], ng = stats[3 * n + 2];
+    const double rel = na > 0.0 ? __ddiv_rn(sqrt(nd), sqrt(na)) : (nd > 0.0 ? INFINITY : 0.0);
+    maxrel = fmax(maxrel, rel);
+    gsum = __dadd_rn(gsum, sqrt(ng));
+  }
+  const double inner = stats[3 * N], model = stats[3 * N + 1];
+  const double r2 = __dadd_rn(__dsub_rn(rs->normX_sq, __dmul_rn(2.0, inner)), model);
+  const double fit = __dsub_rn(1.0, __ddiv_rn(sqrt(fmax(0.0, r2)), sqrt(rs->normX_sq)));
+  const bool small = maxrel < rs->eps_pp;
+  const int phase = rs->phase;
+  const int next = phase == CPPP_PHASE_DT ? (small ? CPPP_PHASE_PP_BUILD : CPPP_PHASE_DT)
+                                          : (small ? CPPP_PHASE_PP : CPPP_PHASE_DT);
+  if (phase == CPPP_PHASE_PP_BUILD) rs->restarts++;
+  const int d = rs->done;
+  RunInfo& in = rs->info[d];
+  in.fitness = fit;
+  in.residual_sq = r2;
+  in.gsum = gsum;
+  in.maxrel = maxrel;
+  in.phase = phase;
+  in.next_phase = next;
+  in.restarts = rs->restarts;
+  in.converged = gsum <= rs->eps;
+  rs->done = d + 1;
+  rs->phase = next;
+  cudaGraphSetConditional(hs, static_cast<unsigned>(next));
+  cudaGraphSetConditional(hw, (d + 1 < rs->max_sweeps && !in.converged) ? 1u : 0u);
+}
+
+cppp_status build_run_graph(cppp_ctx* c) {
+  auto& R = c->run;
+  cudaGraph_t G = nullptr;
+  cudaGraphNode_t pro = nullptr, wn = nullptr, sn = nullptr, dn = nullptr;
+  auto bail = [&](const char* what, cudaError_t e) {
+    if (G) cudaGraphDestroy(G);
+    cudaGetLastError();
+    c->capturing = false;
+    R.failed = true;
+    return fail(c, CPPP_ECUDA, "als_run graph (%s): %s", what, cudaGetErrorString(e));
+  };
+  cudaError_t e = cudaGraphCreate(&G, 0);
+  if (e != cudaSuccess) return bail("create", e);
+  if ((e = cudaGraphConditionalHandleCreate(&R.hw, G, 0, 0)) != cudaSuccess) return bail("handle", e);
+  {
+    cudaKernelNodeParams kp = {};
+    void* args[3] = {&c->run_dev, &R.hw, &R.hs};
+    kp.func = reinterpret_cast<void*>(run_prologue_kernel);
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = args;
+    // R.hs is created below, inside the WHILE body; the prologue's copy of it is patched after
+    if ((e = cudaGraphAddKernelNode(&pro, G, nullptr, 0, &kp)) != cudaSuccess)
+      return bail("prologue", e);
+  }
+  cudaGraphNodeParams wp = {};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = R.hw;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  if ((e = cudaGraphAddNode(&wn, G, &pro, 1, &wp)) != cudaSuccess) return bail("while", e);
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+  if ((e = cudaGraphConditionalHandleCreate(&R.hs, body, 0, 0)) != cudaSuccess)
+    return bail("switch handle", e);
+  cudaGraphNodeParams sp = {};
+  sp.type = cudaGraphNodeTypeConditional;
+  sp.conditional.handle = R.hs;
+  sp.conditional.type = cudaGraphCondTypeSwitch;
+  sp.conditional.size = 3;
+  if ((e = cudaGraphAddNode(&sn, body, nullptr, 0, &sp)) != cudaSuccess) return bail("switch", e);
+  // the three phase bodies, captured from the eager sweep code (no profiling, no PDL edges)
+  for (int ph = 0; ph < 3; ++ph) {
+    STCHK(drain_prefetch(c));
+    e = cudaStreamBeginCaptureToGraph(c->st, sp.conditional.phGraph_out[ph], nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) return bail("capture", e);
+    c->capturing = true;
+    c->capture_prof.clear();
+    const uint64_t l0 = launch_count();
+    pdl_suppress(getenv("CPPP_RUN_NO_PDL") != nullptr);
+    cppp_status s = run_phase_eager(c, ph);
+    pdl_suppress(false);
+    R.launches_per_sweep[ph] = launch_count() - l0;
+    note_launches(0ull - R.launches_per_sweep[ph]);
+    c->capturing = false;
+    cudaGraph_t out = nullptr;
+    e = cudaStreamEndCapture(c->st, &out);
+    c->prefetched = -1;
+    if (s != CPPP_OK) {
+      if (G) cudaGraphDestroy(G);
+      R.failed = true;
+      return s;
+    }
+    if (e != cudaSuccess) return bail("end capture", e);
+  }
+  {
+    cudaKernelNodeParams kp = {};
+    void* args[4] = {&c->run_dev, &c->stats, &R.hw, &R.hs};
+    kp.func = reinterpret_cast<void*>(run_decide_kernel);
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = args;
+    if ((e = cudaGraphAddKernelNode(&dn, body, &sn, 1, &kp)) != cudaSuccess)
+      return bail("decide", e);
+  }
+  {  // the prologue node was added before hs existed: set its final arguments
+    cudaKernelNodeParams kp = {};
+    void* args[3] = {&c->run_dev, &R.hw, &R.hs};
+    kp.func = reinterpret_cast<void*>(run_prologue_kernel);
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.kernelParams = args;
+    if ((e = cudaGraphKernelNodeSetParams(pro, &kp)) != cudaSuccess) return bail("prologue args", e);
+  }
+  e = cudaGraphInstantiate(&R.exec, G, 0);
+  cudaGraphDestroy(G);
+  G = nullptr;
+  if (e != cudaSuccess) return bail("instantiate", e);
+  return CPPP_OK;
+}
+
 // ---------------------------------------------------------------- workspace plan
 struct Plan {
   size_t total = 0;
@@ -877,6 +1037,7 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   size_t oLm = take(sizeof(int) * 4);
   size_t oRow = take(sizeof(double) * smax * 4);
   size_t oStats = take(sizeof(double) * (3 * N + 8));
+  size_t oRun = take(sizeof(RunState));
   // TTM scratch: the padded factor of the widest first-level GEMM (a single mode, or the
   // Khatri-Rao product of a whole half: S = Π of its extents) + scheduler + split partials
   int64_t maxS = smax;
@@ -927,6 +1088,7 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   c->lmode = reinterpret_cast<int*>(b + oLm);
   c->rowstat = reinterpret_cast<double*>(b + oRow);
   c->stats = reinterpret_cast<double*>(b + oStats);
+  c->run_dev = reinterpret_cast<RunState*>(b + oRun);
   c->Fpad = reinterpret_cast<double*>(b + oFpad);
   for (int i = 0; i < N; ++i)
     for (int j = i + 1; j < N; ++j) c->ops[i][j] = reinterpret_cast<double*>(b + oOps[i][j]);
@@ -1141,6 +1303,7 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
                            p.off_stack - (borrow ? 0 : align_up(sizeof(double) * c->numel_local)),
                            c->st));
   CUCHK(c, cudaMallocHost(&c->host_stats, sizeof(double) * (3 * N + 8)));
+  CUCHK(c, cudaMallocHost(&c->run_host, sizeof(RunState)));
   CUCHK(c, cudaEventCreate(&c->ev_a));
   CUCHK(c, cudaEventCreate(&c->ev_b));
   {  // the side stream of the Γ factorizations gets the highest priority: its one-CTA kernel is
@@ -1361,6 +1524,89 @@ cppp_status als_sweep(cppp_ctx* c, double eps, double eps_pp, cppp_sweep_info* i
   return CPPP_OK;
 }
 
+cppp_status als_run(cppp_ctx* c, double eps, double eps_pp, int max_sweeps, cppp_sweep_info* info,
+                    int* done) {
+  if (!c) return CPPP_EINVAL;
+  if (!c->factors_set) return fail(c, CPPP_ESTATE, "als_run before cp_set_factors");
+  if (!(eps_pp >= 0.0)) return fail(c, CPPP_EINVAL, "eps_pp must be >= 0");
+  if (max_sweeps < 0 || max_sweeps > RUN_MAX)
+    return fail(c, CPPP_EINVAL, "max_sweeps must be in [0, %d]", RUN_MAX);
+  if (done) *done = 0;
+  if (max_sweeps == 0) return CPPP_OK;
+  // the host loop: profiling events, several ranks (collectives stay eager), no graphs, a
+  // forced phase, or a GPU/driver that cannot build the conditional graph
+  const bool host_loop = (c->flags & (CPPP_FLAG_PROFILE | CPPP_FLAG_NO_GRAPH)) || c->world > 1 ||
+                         c->override_phase != CPPP_PHASE_AUTO || c->run.failed ||
+                         (c->next_phase == CPPP_PHASE_PP && !c->ops_valid);
+  if (host_loop) {
+    for (int i = 0; i < max_sweeps; ++i) {
+      cppp_sweep_info one;
+      STCHK(als_sweep(c, eps, eps_pp, &one));
+      if (info) info[i] = one;
+      if (done) *done = i + 1;
+      if (one.converged) break;
+    }
+    return CPPP_OK;
+  }
+  if (!c->run.exec) {
+    cppp_status s = build_run_graph(c);
+    if (s != CPPP_OK) {   // fall back for good (recorded in cp_last_error)
+      c->run.failed = true;
+      return als_run(c, eps, eps_pp, max_sweeps, info, done);
+    }
+  }
+  STCHK(drain_prefetch(c));
+  RunState* h = c->run_host;
+  h->eps = eps;
+  h->eps_pp = eps_pp;
+  h->normX_sq = c->normX_sq;
+  h->max_sweeps = max_sweeps;
+  h->done = 0;
+  h->phase = c->next_phase;
+  h->restarts = c->restarts;
+  h->N = c->N;
+  const size_t head = offsetof(RunState, info);
+  CUCHK(c, cudaMemcpyAsync(c->run_dev, h, head, cudaMemcpyHostToDevice, c->st));
+  CUCHK(c, cudaEventRecord(c->ev_a, c->st));
+  CUCHK(c, cudaGraphLaunch(c->run.exec, c->st));
+  CUCHK(c, cudaEventRecord(c->ev_b, c->st));
+  CUCHK(c, cudaMemcpyAsync(h, c->run_dev, head + sizeof(RunInfo) * max_sweeps,
+                           cudaMemcpyDeviceToHost, c->st));
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  // events recorded inside a capture cannot be waited on outside it: re-arm them eagerly
+  CUCHK(c, cudaEventRecord(c->ev_S, c->st));
+  CUCHK(c, cudaEventRecord(c->ev_P, c->st));
+  c->prefetched = -1;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev_a, c->ev_b);
+  const int n = h->done;
+  for (int i = 0; i < n; ++i) {
+    const RunInfo& r = h->info[i];
+    note_launches(c->run.launches_per_sweep[r.phase] + 1);   // + the decision kernel
+    if (r.phase == CPPP_PHASE_PP_BUILD) c->ops_valid = true;
+    c->sweep++;
+    if (info) {
+      cppp_sweep_info& o = info[i];
+      o.sweep = c->sweep;
+      o.phase = r.phase;
+      o.fitness = r.fitness;
+      o.residual_sq = r.residual_sq;
+      o.grad_norm_sum = r.gsum;
+      o.max_rel_dA = r.maxrel;
+      o.next_phase = r.next_phase;
+      o.restarts = r.restarts;
+      o.converged = r.converged;
+      o.seconds = ms * 1e-3 / n;   // the run is one launch: its device time, shared evenly
+    }
+  }
+  note_launches(1);   // the prologue
+  c->next_phase = h->phase;
+  c->restarts = h->restarts;
+  if (n > 0) c->last_fitness = h->info[n - 1].fitness;
+  if (done) *done = n;
+  return CPPP_OK;
+}
+
 cppp_status fitness(cppp_ctx* c, double* f) {
   if (!c) return CPPP_EINVAL;
   if (!f) return fail(c, CPPP_EINVAL, "null output");
@@ -1502,6 +1748,8 @@ void cp_destroy(cppp_ctx* c) {
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
   if (c->host_stats) cudaFreeHost(c->host_stats);
+  if (c->run_host) cudaFreeHost(c->run_host);
+  if (c->run.exec) cudaGraphExecDestroy(c->run.exec);
   if (c->own_ws && c->ws_alloc) cudaFree(c->ws_alloc);
   if (c->comm) g_nccl.commDestroy(c->comm);
   if (c->host_ar_buf) cudaFreeHost(c->host_ar_buf);

@@ -16,7 +16,8 @@
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 #endif
 namespace cppp {
-bool pdl_enabled();   // false when CPPP_NO_PDL is set (A/B measurements)
+bool pdl_enabled();   // false when CPPP_NO_PDL is set (A/B measurements) or suppressed
+void pdl_suppress(bool on);   // this thread: plain launches (graph bodies that reject PDL edges)
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t st, Args&&... args) {

@@ -726,9 +726,11 @@ int grid_for(int64_t n, int threads, int cap) {
 
 }  // namespace
 
+static thread_local bool t_pdl_suppressed = false;
+void pdl_suppress(bool on) { t_pdl_suppressed = on; }
 bool pdl_enabled() {
   static const bool on = getenv("CPPP_NO_PDL") == nullptr;
-  return on;
+  return on && !t_pdl_suppressed;
 }
 
 static unsigned long long g_launches = 0;

@@ -270,3 +270,37 @@ def test_load_tensor_replaces_the_tensor():
                    flags=cp.FLAG_BORROW_TENSOR)
     with pytest.raises(cp.CpppError):
         cp.cp_load_tensor(b, X2)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2mini", "C4mini"])
+def test_als_run_device_loop_matches_host_loop(name):
+    """als_run (one launch: device-side Alg. 3 decisions, WHILE over a SWITCH of the phase
+    graphs) gives bit-identical sweeps to the same number of als_sweep calls, and follows the
+    oracle's free-running schedule."""
+    cfg, X, A0 = problem(name)
+    a = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    b = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    for rep in range(2):   # the second run replays the instantiated run graph
+        cp.cp_set_factors(a, A0)
+        cp.cp_set_factors(b, A0)
+        host = [cp.als_sweep(a, 0.0, cfg.eps_pp) for _ in range(20)]
+        dev = cp.als_run(b, 0.0, cfg.eps_pp, 20)
+        assert len(dev) == 20
+        # one launch for the whole run: the device time is shared evenly (the host loop would
+        # report per-sweep times) -- i.e. the device loop ran, not the fallback
+        assert len({d["seconds"] for d in dev}) == 1, cp.lib().cp_last_error(b.h)
+        for h, d in zip(host, dev):
+            for key in ("sweep", "phase", "next_phase", "restarts", "converged"):
+                assert h[key] == d[key], (rep, key, h, d)
+            for key in ("fitness", "residual_sq", "grad_norm_sum", "max_rel_dA"):
+                assert h[key] == d[key], (rep, key, h, d)
+        for x, y in zip(cp.cp_get_factors(a), cp.cp_get_factors(b)):
+            assert np.array_equal(x, y)
+    _, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, 20)
+    margin_ok = all(t["margin"] > 1e-6 for t in tr)
+    if margin_ok:
+        assert [t["phase"] for t in tr] == [d["phase"] for d in dev]
+    # a stop on the gradient norm ends the run early, like als_sweep's converged flag
+    cp.cp_set_factors(b, A0)
+    big = cp.als_run(b, 1e300, cfg.eps_pp, 20)
+    assert len(big) == 1 and big[0]["converged"] == 1

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--flags", type=int, default=0, help="extra CPPP_FLAG_* bits")
+    ap.add_argument("--run", action="store_true", help="also time als_run (one launch per run)")
     a = ap.parse_args()
     cfg = G.CONFIGS[a.config]
     stream = torch.cuda.current_stream()
@@ -63,6 +64,20 @@ def main():
             for ph, (n, d, w) in by.items():
                 print(f"    {ph:10s} x{n:2d}  device per sweep {1e3 * d / n:9.1f} us"
                       f"  wall per sweep {1e3 * w / n:9.1f} us")
+        cp.cp_destroy(ctx)
+    if a.run:
+        ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K, stream=stream, flags=cp.FLAG_BORROW_TENSOR | a.flags)
+        for r in range(a.reps + 2):
+            cp.cp_set_factors(ctx, A0)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            infos = cp.als_run(ctx, 0.0, cfg.eps_pp, cfg.sweeps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if r >= 2:
+                print(f"[als_run] {a.config} step {e0.elapsed_time(e1):.3f} ms "
+                      f"({len(infos)} sweeps, one launch)")
         cp.cp_destroy(ctx)
 
 
