@@ -61,6 +61,8 @@ typedef enum {
 #define CPPP_FLAG_NO_GRAPH     16u  /* run sweeps eagerly instead of replaying captured CUDA graphs */
 #define CPPP_FLAG_NO_KRP       32u  /* regular DT sweep: single-mode first-level TTMs instead of one
                                         multi-mode (Khatri-Rao) GEMM per half (testing) */
+#define CPPP_FLAG_NO_OVERLAP   64u  /* order-3 DT sweep: run the second first-level TTM after mode 1
+                                        instead of beside it (testing) */
 
 typedef struct {
   int device;               /* CUDA ordinal (default 0) */

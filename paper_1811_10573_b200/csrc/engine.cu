@@ -109,6 +109,8 @@ struct cppp_ctx {
   double* gram_scratch = nullptr;   // Gram split partials + per-tile Σ Γ∘S partials
   unsigned int* gram_counters = nullptr;
   cudaStream_t st2 = nullptr;           // side stream: Γ^(n) inverse overlapped with M^(n)
+  cudaStream_t st3 = nullptr;           // order-3 DT: the second first-level TTM, overlapped
+  cudaEvent_t ev_F = nullptr, ev_T = nullptr;   // st3 fork / join
   cudaEvent_t ev_S = nullptr, ev_P = nullptr;
   int prefetched = -1;                  // mode whose Γ inverse is issued on st2
   double* rowstat = nullptr; // max local rows x 4
@@ -327,7 +329,9 @@ int64_t node_elems(cppp_ctx* c, uint32_t mask) {
 }
 
 // out = contraction of `src` along mode u with factor F (local rows)
-cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, double* out) {
+cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, double* out,
+                     cudaStream_t st = nullptr) {
+  if (!st) st = c->st;
   int64_t B = 1, R = 1;
   for (int v = 0; v < c->N; ++v) {
     if (!(src.mask & (1u << v)) || v == u) continue;
@@ -341,14 +345,14 @@ cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, doubl
     const double flops = 2.0 * B * S * R * K;
     const double bytes = 8.0 * (B * S * R + B * R * K);
     const bool simt = (c->flags & CPPP_FLAG_SIMT_TTM) != 0;
-    if (ttm_uses_dmma(B, S, R, K, simt)) CUCHK(c, ttm_prepare(S, F, K, c->Fpad, c->st));
-    Prof p(c, CPPP_K_TTM, flops, bytes);
-    CUCHK(c, launch_ttm_core(src.data, B, S, R, F, K, out, c->Fpad, simt, c->st));
+    if (ttm_uses_dmma(B, S, R, K, simt)) CUCHK(c, ttm_prepare(S, F, K, c->Fpad, st));
+    Prof p(c, CPPP_K_TTM, flops, bytes, st);
+    CUCHK(c, launch_ttm_core(src.data, B, S, R, F, K, out, c->Fpad, simt, st));
   } else {
     const double flops = 2.0 * B * S * R * K;
     const double bytes = 8.0 * (B * S * R * K + B * R * K);
-    Prof p(c, CPPP_K_TTV, flops, bytes);
-    CUCHK(c, launch_ttv(src.data, B, S, R, K, F, out, c->ttv_scratch, c->st));
+    Prof p(c, CPPP_K_TTV, flops, bytes, st);
+    CUCHK(c, launch_ttv(src.data, B, S, R, K, F, out, c->ttv_scratch, st));
   }
   return CPPP_OK;
 }
@@ -519,7 +523,38 @@ struct DT {
     return CPPP_OK;
   }
 
+  // Order 3, unsharded: the right half's first-level TTM (X ×_0 A^(0)) needs only A^(0), so it
+  // runs on st3 beside mode 1's work (its multi-TTV, the Γ factorization and the row solves),
+  // which are latency-bound and leave the tensor cores idle.  Same contractions, same order of
+  // factor updates as range(); T01 and T12 are both live.
+  cppp_status range3_overlap(const Node& nd) {
+    const size_t mk = c->stack.mark();
+    double* T01 = c->stack.push(node_elems(c, 0x3u));
+    STCHK(contract(c, nd, 2, fac_local(c, c->A, 2), T01));
+    const Node L{0x3u, T01, false};
+    STCHK(contract(c, L, 1, fac_local(c, c->A, 1), c->M[0]));
+    STCHK(leaf(0, c->M[0]));
+    double* T12 = c->stack.push(node_elems(c, 0x6u));
+    if (!c->dry) {
+      CUCHK(c, cudaEventRecord(c->ev_F, c->st));
+      CUCHK(c, cudaStreamWaitEvent(c->st3, c->ev_F, 0));
+    }
+    STCHK(contract(c, nd, 0, fac_local(c, c->A, 0), T12, c->st3));
+    if (!c->dry) CUCHK(c, cudaEventRecord(c->ev_T, c->st3));
+    STCHK(contract(c, L, 0, fac_local(c, c->A, 0), c->M[1]));
+    STCHK(leaf(1, c->M[1]));
+    if (!c->dry) CUCHK(c, cudaStreamWaitEvent(c->st, c->ev_T, 0));
+    const Node Rn{0x6u, T12, false};
+    STCHK(contract(c, Rn, 1, fac_local(c, c->A, 1), c->M[2]));
+    STCHK(leaf(2, c->M[2]));
+    c->stack.release(mk);
+    return CPPP_OK;
+  }
+
   cppp_status range(const Node& nd, int lo, int hi) {
+    if (nd.root && c->N == 3 && lo == 0 && hi == 2 && c->q < 0 &&
+        !(c->flags & CPPP_FLAG_NO_OVERLAP))
+      return range3_overlap(nd);
     const int mid = lo + (hi - lo + 1 + 1) / 2 - 1;  // left half has ceil(len/2) modes
     // ---- left: modes [lo, mid]
     {
@@ -1313,6 +1348,9 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
     CUCHK(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CUCHK(c, cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, hi));
   }
+  CUCHK(c, cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
+  CUCHK(c, cudaEventCreateWithFlags(&c->ev_F, cudaEventDisableTiming));
+  CUCHK(c, cudaEventCreateWithFlags(&c->ev_T, cudaEventDisableTiming));
   CUCHK(c, cudaEventCreateWithFlags(&c->ev_S, cudaEventDisableTiming));
   CUCHK(c, cudaEventCreateWithFlags(&c->ev_P, cudaEventDisableTiming));
   return tensor_norm(c);
@@ -1742,6 +1780,7 @@ size_t cppp_plan_describe(int N, int shard_mode, char* buf, size_t buflen) {
 void cp_destroy(cppp_ctx* c) {
   if (!c) return;
   if (c->st) cudaStreamSynchronize(c->st);
+  if (c->st3) cudaStreamSynchronize(c->st3);
   if (c->st2) cudaStreamSynchronize(c->st2);
   prof_collect(c);
   for (auto e : c->evpool) cudaEventDestroy(e);
@@ -1763,6 +1802,9 @@ void cp_destroy(cppp_ctx* c) {
   if (c->ev_S) cudaEventDestroy(c->ev_S);
   if (c->ev_P) cudaEventDestroy(c->ev_P);
   if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->st3) cudaStreamDestroy(c->st3);
+  if (c->ev_F) cudaEventDestroy(c->ev_F);
+  if (c->ev_T) cudaEventDestroy(c->ev_T);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
 }

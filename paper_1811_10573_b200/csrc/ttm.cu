@@ -155,7 +155,7 @@ template <int NT, bool MC>
 __global__ void __launch_bounds__(NTHREADS, 1)
     ttm_dmma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
                     double* __restrict__ out, int64_t Mrows, int64_t mtiles, int64_t nfull,
-                    int64_t nsplit, int ks, int S, int K, int stages,
+                    int64_t nsplit, int ks, int S, int K, int stages, int64_t Rflat,
                     unsigned long long* __restrict__ tile_counter, unsigned int* __restrict__ tickets,
                     double* __restrict__ part) {
   using C = Cfg<NT>;
@@ -211,11 +211,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint32_t sf = sx + C::XBYTES;
           if (!MC) {
             tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb);
-          } else {
+          } else if (Rflat == 0) {
 #pragma unroll
             for (int c = 0; c < BM / 16; ++c)
               tma_3d(sx + c * 2048, &tmX, static_cast<int>(m0 + 16 * c), kt * BK,
                      static_cast<int>(b), fb);
+          } else {   // rows flattened over (b, r): each 16-row box has its own (b, r)
+#pragma unroll
+            for (int c = 0; c < BM / 16; ++c) {
+              const int64_t f = m0 + 16 * c;
+              const int64_t bc = f / Rflat;
+              tma_3d(sx + c * 2048, &tmX, static_cast<int>(f - bc * Rflat), kt * BK,
+                     static_cast<int>(bc), fb);
+            }
           }
 #pragma unroll
           for (int c = 0; c < C::BNP / 16; ++c) tma_2d(sf + c * 2048, &tmF, 16 * c, kt * BK, fb);
@@ -442,7 +450,11 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
     attr_done = true;
   }
   CUtensorMap tmX, tmF;
-  const int64_t Mrows = MC ? R : B;
+  // m-contiguous with several batches and R % 16 == 0: tiles run over the flattened (b, r) rows
+  // (16-row boxes never straddle a batch), so no batch leaves a partial tile (C2's middle mode:
+  // R = 400 = 3 x 128 + 16 wasted 22% of the tiles' rows)
+  const int64_t Rflat = (MC && B > 1 && R % 16 == 0) ? R : 0;
+  const int64_t Mrows = MC ? (Rflat ? B * R : R) : B;
   if (!MC) {
     cuuint64_t dims[2] = {(cuuint64_t)S, (cuuint64_t)B};
     cuuint64_t str[1] = {(cuuint64_t)S * 8};
@@ -465,7 +477,7 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
   const int stages = C::MAX_STAGES;
   const int smem = C::smem(stages);
   const int64_t mtiles = (Mrows + BM - 1) / BM;
-  const int64_t ntiles = mtiles * (MC ? B : 1);
+  const int64_t ntiles = mtiles * ((MC && !Rflat) ? B : 1);
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ttm_dmma_kernel<NT, MC>, NTHREADS, smem);
   if (occ < 1) occ = 1;
@@ -519,7 +531,7 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
             (long long)nsplit, ks);
   cudaError_t e = launch_pdl(ttm_dmma_kernel<NT, MC>, dim3((unsigned)grid), dim3(NTHREADS), smem, st,
                              tmX, tmF, out, Mrows, mtiles, nfull, nsplit, ks, (int)S, K, stages,
-                             counter, tickets, part);
+                             Rflat, counter, tickets, part);
   note_launch();
   return e;
 }

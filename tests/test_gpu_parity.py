@@ -78,8 +78,10 @@ def test_pp_operators_and_singles_match_oracle(name):
         assert rel(cp.pp_get_single(ctx, n), O.mttkrp(X, A0, n)) < TOL, (name, n)
 
 
-@pytest.mark.parametrize("dims,K", RAGGED)
+@pytest.mark.parametrize("dims,K", RAGGED + [((7, 30, 64), 20), ((3, 64, 5, 48), 24),
+                                            ((9, 400, 16), 8)])
 def test_pp_operators_ragged(dims, K):
+    # the last three contract a middle mode with R % 16 == 0: tiles over the flattened (b, r)
     X, A = random_problem(dims, K, 2)
     ctx = cp.cp_init(X, len(dims), dims, K)
     cp.cp_set_factors(ctx, A)
@@ -270,6 +272,22 @@ def test_load_tensor_replaces_the_tensor():
                    flags=cp.FLAG_BORROW_TENSOR)
     with pytest.raises(cp.CpppError):
         cp.cp_load_tensor(b, X2)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2mini"])
+def test_order3_overlapped_schedule_is_bit_identical(name):
+    """Order 3: the second first-level TTM runs beside mode 1's work (default) or after it
+    (CPPP_FLAG_NO_OVERLAP); same contractions in the same order -> identical sweeps."""
+    cfg, X, A0 = problem(name)
+    a = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    b = cp.cp_init(X, cfg.N, cfg.dims, cfg.K, flags=cp.FLAG_NO_OVERLAP)
+    for c in (a, b):
+        cp.cp_set_factors(c, A0)
+    for _ in range(12):
+        ia, ib = cp.als_sweep(a, 0.0, cfg.eps_pp), cp.als_sweep(b, 0.0, cfg.eps_pp)
+        assert ia["fitness"] == ib["fitness"] and ia["phase"] == ib["phase"], (ia, ib)
+    for x, y in zip(cp.cp_get_factors(a), cp.cp_get_factors(b)):
+        assert np.array_equal(x, y)
 
 
 @pytest.mark.parametrize("name", ["C1", "C2mini", "C4mini"])
