@@ -200,6 +200,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const Unit un = decode_unit(unit, nfull, nk, ks);
         const int64_t b = MC ? un.tile / mtiles : 0;
         const int64_t m0 = (un.tile - b * mtiles) * BM;
+        // flattened rows: (batch, row) of the tile's first row, one division per unit
+        const int64_t b_first = Rflat ? m0 / Rflat : 0;
+        const int64_t r_first = Rflat ? m0 - b_first * Rflat : 0;
         for (int kt = un.k0; kt < un.k1; ++kt, ++it) {
           const int st = static_cast<int>(it % stages);
           const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
@@ -217,12 +220,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               tma_3d(sx + c * 2048, &tmX, static_cast<int>(m0 + 16 * c), kt * BK,
                      static_cast<int>(b), fb);
           } else {   // rows flattened over (b, r): each 16-row box has its own (b, r)
+            int rc = static_cast<int>(r_first), bc = static_cast<int>(b_first);
 #pragma unroll
             for (int c = 0; c < BM / 16; ++c) {
-              const int64_t f = m0 + 16 * c;
-              const int64_t bc = f / Rflat;
-              tma_3d(sx + c * 2048, &tmX, static_cast<int>(f - bc * Rflat), kt * BK,
-                     static_cast<int>(bc), fb);
+              tma_3d(sx + c * 2048, &tmX, rc, kt * BK, bc, fb);
+              rc += 16;
+              if (rc >= Rflat) {   // R % 16 == 0: a box never straddles two batches
+                rc -= static_cast<int>(Rflat);
+                ++bc;
+              }
             }
           }
 #pragma unroll
