@@ -63,6 +63,9 @@ typedef enum {
                                         multi-mode (Khatri-Rao) GEMM per half (testing) */
 #define CPPP_FLAG_NO_OVERLAP   64u  /* order-3 DT sweep: run the second first-level TTM after mode 1
                                         instead of beside it (testing) */
+#define CPPP_FLAG_FORCE_COMM  128u  /* take the communicating (sharded) code paths even with one
+                                        rank: with a one-rank NCCL communicator this runs the
+                                        all-reduce transport on a single GPU (testing) */
 
 typedef struct {
   int device;               /* CUDA ordinal (default 0) */

@@ -174,6 +174,12 @@ struct RunInfo {
   double fitness, residual_sq, gsum, maxrel;
   int phase, next_phase, restarts, converged;
 };
+// the communicating (sharded) code paths run with several ranks, or with one rank under
+// CPPP_FLAG_FORCE_COMM (a one-rank NCCL communicator: the transport exercised on one GPU)
+inline bool comm_on(const cppp_ctx* c) {
+  return c->world > 1 || (c->flags & CPPP_FLAG_FORCE_COMM);
+}
+
 constexpr int RUN_MAX = 1024;   // sweeps per als_run call
 struct RunState {
   double eps, eps_pp, normX_sq;
@@ -295,7 +301,7 @@ void prof_collect(cppp_ctx* c) {
 
 // ---------------------------------------------------------------- comm
 cppp_status allreduce(cppp_ctx* c, double* buf, size_t count) {
-  if (c->world <= 1 || c->dry || count == 0) return CPPP_OK;
+  if (!comm_on(c) || c->dry || count == 0) return CPPP_OK;
   if (c->host_ar) {
     if (count > c->host_ar_cap) {
       if (c->host_ar_buf) cudaFreeHost(c->host_ar_buf);
@@ -775,7 +781,7 @@ cppp_status pp_update_mode(cppp_ctx* c, int n, double* out, const double* extra,
 // M~ is M_p itself (no launch).
 cppp_status run_pp_sweep(cppp_ctx* c, bool after_build) {
   const int N = c->N;
-  const bool sh = c->q >= 0 && c->world > 1;
+  const bool sh = c->q >= 0 && comm_on(c);
   for (int n = 0; n < N; ++n) {
     const double* extra = nullptr;
     if (sh && n != c->q) extra = c->T[n];
@@ -835,7 +841,7 @@ cppp_status run_phase_eager(cppp_ctx* c, int phase) {
 // Whole sweeps replay as CUDA graphs (captured on a phase's second use, so the first use sets
 // every kernel attribute eagerly).  Not used with several ranks (collectives stay eager).
 cppp_status run_phase(cppp_ctx* c, int phase) {
-  const bool graphs = !(c->flags & CPPP_FLAG_NO_GRAPH) && c->world == 1;
+  const bool graphs = !(c->flags & CPPP_FLAG_NO_GRAPH) && !comm_on(c);
   auto& g = c->graphs[phase];
   g.uses++;
   if (!graphs || g.uses < 2) {
@@ -1200,7 +1206,7 @@ cppp_status copy_out(cppp_ctx* c, double* dst, const double* src, size_t n) {
 
 // gather the sharded factor's rows: zero everything but the local rows, all-reduce
 cppp_status gather_rows(cppp_ctx* c, double* buf) {
-  if (c->q < 0 || c->world <= 1) return CPPP_OK;
+  if (c->q < 0 || !comm_on(c)) return CPPP_OK;
   const int K = c->K;
   CUCHK(c, cudaMemsetAsync(c->gath, 0, sizeof(double) * c->s[c->q] * K, c->st));
   CUCHK(c, cudaMemcpyAsync(c->gath + c->qoff * K, buf + c->qoff * K, sizeof(double) * c->qext * K,
@@ -1296,8 +1302,9 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
   c->world = o.world < 1 ? 1 : o.world;
   c->host_ar = o.host_allreduce;
   c->host_ar_user = o.host_allreduce_user;
-  if (c->world > 1 && !c->host_ar) {
-    if (!o.nccl_unique_id) return fail(c, CPPP_EINVAL, "world > 1 needs nccl_unique_id or host_allreduce");
+  if (comm_on(c) && !c->host_ar) {
+    if (!o.nccl_unique_id)
+      return fail(c, CPPP_EINVAL, "a communicating context needs nccl_unique_id or host_allreduce");
     if (!g_nccl.load()) return fail(c, CPPP_ENCCL, "cannot dlopen libnccl.so.2");
     ncclUniqueId id;
     std::memcpy(&id, o.nccl_unique_id, sizeof(id));
@@ -1476,7 +1483,7 @@ cppp_status pp_update(cppp_ctx* c, int n, double* M_tilde) {
   // dA = A - A_p for every mode (the caller may have moved the factors)
   for (int i = 0; i < c->N; ++i)
     CUCHK(c, launch_sub(c->A[i], c->Ap[i], c->dA[i], c->s[i] * c->K, c->st));
-  const bool sh = c->q >= 0 && c->world > 1;
+  const bool sh = c->q >= 0 && comm_on(c);
   if (sh && n != c->q) {
     // partial term over the local rows of the sharded mode, then all-reduce
     PPUpdateArgs a;
@@ -1573,7 +1580,7 @@ cppp_status als_run(cppp_ctx* c, double eps, double eps_pp, int max_sweeps, cppp
   if (max_sweeps == 0) return CPPP_OK;
   // the host loop: profiling events, several ranks (collectives stay eager), no graphs, a
   // forced phase, or a GPU/driver that cannot build the conditional graph
-  const bool host_loop = (c->flags & (CPPP_FLAG_PROFILE | CPPP_FLAG_NO_GRAPH)) || c->world > 1 ||
+  const bool host_loop = (c->flags & (CPPP_FLAG_PROFILE | CPPP_FLAG_NO_GRAPH)) || comm_on(c) ||
                          c->override_phase != CPPP_PHASE_AUTO || c->run.failed ||
                          (c->next_phase == CPPP_PHASE_PP && !c->ops_valid);
   if (host_loop) {
@@ -1707,7 +1714,7 @@ cppp_status cppp_generate(cppp_ctx* c, double* X_dev, int N, const int64_t* s, i
     if (launch_gen_noise_rowsq(X_dev, s, N, seed, row_lo, row_hi, rowsq_x, rowsq_z, partials, st) !=
         cudaSuccess)
       rc = CPPP_ECUDA;
-    if (rc == CPPP_OK && c && c->world > 1) {
+    if (rc == CPPP_OK && c && comm_on(c)) {
       cudaStream_t save = c->st;
       c->st = st;
       rc = allreduce(c, rowsq_x, 2 * (size_t)s[0]);

@@ -150,3 +150,35 @@ def test_sharded_trace_matches_oracle(P, name):
     for n in range(1, cfg.N):
         for rank in range(1, P):
             assert np.array_equal(res[rank][1][n], res[0][1][n])
+
+
+@pytest.mark.parametrize("name", ["C1", "C2mini", "C5mini"])
+def test_nccl_transport_single_rank(name):
+    """The NCCL transport itself on one GPU: a one-rank communicator (ncclCommInitRank with
+    nranks = 1) and CPPP_FLAG_FORCE_COMM, so every sharded branch runs and every all-reduce is a
+    real ncclAllReduce on the library stream.  The trace must match the oracle, and an unsharded
+    context to rounding (the sharded schedule keeps the slab mode out of the multi-mode first
+    level and contracts it last, so the operation order differs)."""
+    cfg = G.CONFIGS[name]
+    X = G.make_tensor(cfg)
+    A0 = G.initial_factors(cfg)
+    _, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, 12)
+    uid = cp.cppp_nccl_unique_id()
+    nc = cp.cp_init(X, cfg.N, cfg.dims, cfg.K, shard_offset=0, shard_extent=cfg.dims[0],
+                    rank=0, world=1, nccl_unique_id=uid, flags=cp.FLAG_FORCE_COMM)
+    plain = cp.cp_init(X, cfg.N, cfg.dims, cfg.K, flags=cp.FLAG_NO_OVERLAP)
+    for c in (nc, plain):
+        cp.cp_set_factors(c, A0)
+    for t in tr:
+        for c in (nc, plain):
+            cp.cp_set_phase_override(c, t["phase"])
+        a, b = cp.als_sweep(nc, 0.0, cfg.eps_pp), cp.als_sweep(plain, 0.0, cfg.eps_pp)
+        if 1.0 - t["fitness"] >= 1e-6:
+            assert abs(a["fitness"] - t["fitness"]) < 1e-8, (t, a)
+        assert abs(a["fitness"] - b["fitness"]) < 1e-9, (a, b)
+    M = cp.mttkrp_dt(nc)
+    A = cp.cp_get_factors(nc)
+    for n in range(cfg.N):
+        assert rel(M[n], O.mttkrp(X, A, n)) < 1e-11, n
+    cp.cp_destroy(nc)
+    cp.cp_destroy(plain)
