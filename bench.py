@@ -203,7 +203,7 @@ def main():
     if world > 1:
         # a throw-away context provides the communicator for the shard-invariant noise scale
         tmp = torch.zeros((row_hi - row_lo) * cfg.s ** (cfg.N - 1), dtype=torch.float64, device="cuda")
-        gen_ctx = cp.cp_init(tmp, cfg.N, dims, cfg.K, stream=stream, flags=cp.FLAG_BORROW_TENSOR,
+        gen_ctx = cp.cp_init(tmp, cfg.N, dims, cfg.K, stream=stream, device=local, flags=cp.FLAG_BORROW_TENSOR,
                              nccl_unique_id=nccl_id, rank=rank, world=world, torch_workspace=False, **shard)
         del tmp
     cp.cppp_generate(X_dev, dims, cfg.K, A_true, kind, cfg.noise, 0, row_lo, row_hi, stream=stream, ctx=gen_ctx)
@@ -213,7 +213,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     # timed pass: no profiling events inside the sweeps (they perturb a C2 step by ~8%)
-    ctx = cp.cp_init(X_dev, cfg.N, dims, cfg.K, stream=stream, flags=cp.FLAG_BORROW_TENSOR,
+    ctx = cp.cp_init(X_dev, cfg.N, dims, cfg.K, stream=stream, device=local, flags=cp.FLAG_BORROW_TENSOR,
                      nccl_unique_id=nccl_id, rank=rank, world=world, **shard)
     A0_dev = [torch.from_numpy(a).cuda() for a in A0]
 
@@ -257,7 +257,7 @@ def main():
         obj = [cp.cppp_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    ctx = cp.cp_init(X_dev, cfg.N, dims, cfg.K, stream=stream,
+    ctx = cp.cp_init(X_dev, cfg.N, dims, cfg.K, stream=stream, device=local,
                      flags=cp.FLAG_BORROW_TENSOR | cp.FLAG_PROFILE,
                      nccl_unique_id=nccl_id, rank=rank, world=world, **shard)
     step()
