@@ -406,7 +406,7 @@ cppp_status prefetch_inverse(cppp_ctx* c, int n) {
   {   // (the scope closes before ev_P: every side-stream node must be joined)
     Prof p(c, CPPP_K_FACTOR, (double)c->K * c->K * c->K / 3.0, 8.0 * c->K * c->K * c->N, c->st2);
     CUCHK(c, launch_gamma_factor(c->S_all, c->N, n, c->K, c->Gamma, c->L, c->lmode,
-                                 c->L + (int64_t)solve_ld(c->K) * solve_ld(c->K),
+                                 c->L + (int64_t)solve_ld(c->K) * solve_ld(c->K) + 4 * 32 * 33,
                                  c->st2));
   }
   CUCHK(c, cudaEventRecord(c->ev_P, c->st2));
@@ -1073,7 +1073,8 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   }
   size_t oS = take(sizeof(double) * N * K * K);
   size_t oG = take(sizeof(double) * solve_ld(K) * solve_ld(K));
-  size_t oL = take(sizeof(double) * (solve_ld(K) * solve_ld(K) + K * K));   // packed factor + Jacobi V
+  // packed factor, inverted 32 x 32 diagonal blocks, Jacobi V
+  size_t oL = take(sizeof(double) * (solve_ld(K) * solve_ld(K) + 4 * 32 * 33 + K * K));
   size_t oGp = take(sizeof(double) * gram_scratch_doubles() + 64 * sizeof(unsigned int));
   size_t oLm = take(sizeof(int) * 4);
   size_t oRow = take(sizeof(double) * smax * 4);

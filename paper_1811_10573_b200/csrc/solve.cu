@@ -204,6 +204,40 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
   PROBE_T(1);
 }
 
+// Inverses of the 32 x 32 diagonal blocks of L for the row solves (Q, right after Tp): warp b,
+// lane c computes column c of inv(L_bb) right-looking with compile-time indices; Q[b][c][j] =
+// inv(L_bb)[j][c] with row pitch 33.  Rows past ld are the identity.  Exits unless the Cholesky
+// path was taken.
+__global__ void __launch_bounds__(128)
+    block_inverse_kernel(double* Tp, int ldt, const int* mode) {
+  pdl_wait();
+  if (*mode != 0) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nblk = (ldt + 31) >> 5;
+  if (wid >= nblk) return;
+  const int b0 = 32 * wid, c = lane;
+  __shared__ double Ls[4][32][33];   // the diagonal block (coalesced rows), identity past ld
+#pragma unroll 4
+  for (int j = 0; j < 32; ++j) {
+    const int gj = b0 + j, gc = b0 + c;
+    Ls[wid][j][c] = (gj < ldt && gc < ldt) ? Tp[gj * ldt + gc] : (j == c ? 1.0 : 0.0);
+  }
+  __syncwarp();
+  double y[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) y[j] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const double dinv = Ls[wid][i][i];   // 1 / L[i][i]
+    y[i] = i == c ? dinv : (i > c ? -y[i] * dinv : 0.0);
+#pragma unroll
+    for (int j = i + 1; j < 32; ++j) y[j] = fma(Ls[wid][j][i], y[i], y[j]);   // L[j][i]
+  }
+  double* Q = Tp + ldt * ldt + wid * 32 * 33;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) Q[c * 33 + j] = y[j];
+}
+
 // Eigen pseudo-inverse fallback (L13): runs after gamma_chol_kernel and exits at once unless
 // the pivot test failed.  Two-sided cyclic Jacobi, Brent-Luk parallel ordering; the
 // pseudo-inverse P goes to Tp (pitch ldt).
@@ -364,7 +398,8 @@ __global__ void __launch_bounds__(SR_WARPS * 32, 1)
   extern __shared__ __align__(16) double sm[];
   __shared__ __align__(8) uint64_t bar;
   double* Ts = sm + 128;                                // ldt x ldt (+ 128 pad on each side)
-  double* Gs = Ts + (int64_t)ldt * ldt + 256;           // ldt x ldt (+ 128 pad), if staged
+  double* Qs = Ts + (int64_t)ldt * ldt + 256;           // 4 x 32 x 33 inverted diagonal blocks
+  double* Gs = Qs + 4 * 32 * 33;                        // ldt x ldt (+ 128 pad), if staged
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t tbytes = static_cast<uint32_t>(ldt) * ldt * 8;
   if (threadIdx.x == 0) {
@@ -372,8 +407,10 @@ __global__ void __launch_bounds__(SR_WARPS * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // Tp and Γ come from the factorization (a full, event dependency): stage them before the
     // programmatic wait on the kernel that produced M
-    bar_expect(&bar, gamma_in_smem ? 2 * tbytes : tbytes);
+    const uint32_t qbytes = static_cast<uint32_t>((ldt + 31) >> 5) * 32 * 33 * 8;
+    bar_expect(&bar, (gamma_in_smem ? 2 * tbytes : tbytes) + qbytes);
     bulk_to_smem(Ts, Tp, tbytes, &bar);
+    bulk_to_smem(Qs, Tp + (int64_t)ldt * ldt, qbytes, &bar);
     if (gamma_in_smem) bulk_to_smem(Gs, Gamma, tbytes, &bar);
   }
   __syncthreads();
@@ -398,67 +435,54 @@ __global__ void __launch_bounds__(SR_WARPS * 32, 1)
   // counts; the padded steps change nothing (their m and factor entries are zero).
   const int kp = ldt;
   if (mode == 0) {
-    // forward: L z = m.  Step j reads row j of Tp (1/L[j][j] and column j of L); the row of
-    // step j+1 is loaded during step j, and the next shuffle reads this step's fma result
-    // directly (lane j+1 > j always takes it), so the chain per pivot is shfl -> mul -> fma.
+    // Blocked substitution with the inverted 32 x 32 diagonal blocks (Q, from the factorization):
+    // forward L z = m block by block: z_u = inv(L_uu) m_u (32 independent shuffles and fmas,
+    // two accumulators added in a fixed order), then the later blocks take -L[.][u] z_u
+    // (rows of Tp's upper part, in ascending order).  Back Lᵀ a = z the same way, descending, with
+    // inv(L_uu)ᵀ and the rows of Tp's lower part.  No per-pivot dependency chain.
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (32 * u >= kp) break;
-      const int nb = min(32, kp - 32 * u);
-      const double* row = Ts + (32 * u) * ldt;
-      double dn = row[32 * u], tn[4];
+      const double* Qu = Qs + u * 32 * 33;
+      double z0 = 0.0, z1 = 0.0;
 #pragma unroll
-      for (int v = u; v < 4; ++v) tn[v] = row[32 * v + lane];
-      double src = m[u];
+      for (int jj = 0; jj < 32; jj += 2) {
+        z0 = fma(Qu[jj * 33 + lane], __shfl_sync(0xffffffffu, m[u], jj), z0);
+        z1 = fma(Qu[(jj + 1) * 33 + lane], __shfl_sync(0xffffffffu, m[u], jj + 1), z1);
+      }
+      m[u] = z0 + z1;
+      const int nb = min(32, kp - 32 * u);
       for (int j8 = 0; j8 < nb; j8 += 8) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int jj = j8 + k;
-          const double dj = dn;
-          double tj[4];
+          const double zj = __shfl_sync(0xffffffffu, m[u], jj);
+          const double* tr = Ts + (32 * u + jj) * ldt + lane;
 #pragma unroll
-          for (int v = u; v < 4; ++v) tj[v] = tn[v];
-          row += ldt;   // prefetch the next row (one row past the end is inside the pad)
-          dn = row[32 * u + jj + 1];
-#pragma unroll
-          for (int v = u; v < 4; ++v) tn[v] = row[32 * v + lane];
-          const double zj = __shfl_sync(0xffffffffu, src, jj) * dj;
-          const double t = fma(-tj[u], zj, m[u]);
-          src = t;
-          m[u] = lane == jj ? zj : (lane > jj ? t : m[u]);
-#pragma unroll
-          for (int v = u + 1; v < 4; ++v) m[v] = fma(-tj[v], zj, m[v]);
+          for (int v = u + 1; v < 4; ++v) m[v] = fma(-tr[32 * v], zj, m[v]);
         }
       }
     }
-    // back: Lᵀ a = z (row j of Tp holds row j of L), same pipeline, pivots descending
 #pragma unroll
     for (int u = 3; u >= 0; --u) {
       if (32 * u >= kp) continue;
+      const double* Qu = Qs + u * 32 * 33 + lane * 33;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 32; jj += 2) {
+        a0 = fma(Qu[jj], __shfl_sync(0xffffffffu, m[u], jj), a0);
+        a1 = fma(Qu[jj + 1], __shfl_sync(0xffffffffu, m[u], jj + 1), a1);
+      }
+      m[u] = a0 + a1;
       const int nb = min(32, kp - 32 * u);
-      const double* row = Ts + (32 * u + nb - 1) * ldt;
-      double dn = row[32 * u + nb - 1], tn[4];
+      for (int j8 = 0; j8 < nb; j8 += 8) {
 #pragma unroll
-      for (int v = 0; v <= u; ++v) tn[v] = row[32 * v + lane];
-      double src = m[u];
-      for (int j8 = nb - 8; j8 >= 0; j8 -= 8) {
-#pragma unroll
-        for (int k = 7; k >= 0; --k) {
+        for (int k = 0; k < 8; ++k) {
           const int jj = j8 + k;
-          const double dj = dn;
-          double tj[4];
+          const double aj = __shfl_sync(0xffffffffu, m[u], jj);
+          const double* tr = Ts + (32 * u + jj) * ldt + lane;
 #pragma unroll
-          for (int v = 0; v <= u; ++v) tj[v] = tn[v];
-          row -= ldt;   // (one row before the start is the Γ area or the pad: never used)
-          dn = row[32 * u + jj - 1];
-#pragma unroll
-          for (int v = 0; v <= u; ++v) tn[v] = row[32 * v + lane];
-          const double aj = __shfl_sync(0xffffffffu, src, jj) * dj;
-          const double t = fma(-tj[u], aj, m[u]);
-          src = t;
-          m[u] = lane == jj ? aj : (lane < jj ? t : m[u]);
-#pragma unroll
-          for (int v = 0; v < u; ++v) m[v] = fma(-tj[v], aj, m[v]);
+          for (int v = 0; v < u; ++v) m[v] = fma(-tr[32 * v], aj, m[v]);
         }
       }
     }
@@ -755,6 +779,10 @@ cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double
                              Gamma, Tp, ldt, mode);
   note_launch();
   if (e != cudaSuccess) return e;
+  e = launch_pdl(block_inverse_kernel, dim3(1), dim3(128), 0, st, Tp, ldt,
+                 static_cast<const int*>(mode));
+  note_launch();
+  if (e != cudaSuccess) return e;
   e = launch_pdl(gamma_pinv_kernel, dim3(1), dim3(GP_THREADS), smem, st, K,
                  static_cast<const double*>(Gamma), Tp, ldt, static_cast<const int*>(mode), Vscratch);
   note_launch();
@@ -767,9 +795,10 @@ cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, dou
   if (rows == 0) return cudaSuccess;
   const int ldt = solve_ld(K);
   const size_t one = static_cast<size_t>(ldt) * ldt * sizeof(double);
-  // layout: 128 pad | Tp | 256 pad | Γ | 128 pad   (reads run up to one row past either end)
-  const bool both = 2 * one + 512 * sizeof(double) <= 220 * 1024;   // Γ staged too (K <= 112)
-  const size_t smem = (both ? 2 * one : one) + 512 * sizeof(double);
+  // layout: 128 pad | Tp | 256 pad | Q (4 x 32 x 33) | Γ | 128 pad
+  const size_t qb = 4 * 32 * 33 * sizeof(double);
+  const bool both = 2 * one + qb + 512 * sizeof(double) <= 220 * 1024;   // Γ staged too
+  const size_t smem = (both ? 2 * one : one) + qb + 512 * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(solve_rows_kernel,

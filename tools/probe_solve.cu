@@ -40,8 +40,8 @@ int main(int argc, char** argv) {
     double *dS, *dG, *dP, *dV, *dM, *dA, *dD, *drs, *dtp, *dSn, *dn, *dfit;
     unsigned* dcnt;
     int* dmode;
-    cudaMalloc(&dS, 8 * N * K * K); cudaMalloc(&dG, 8 * ldt * ldt); cudaMalloc(&dP, 8 * ldt * ldt);
-    cudaMemset(dG, 0, 8 * ldt * ldt); cudaMemset(dP, 0, 8 * ldt * ldt);
+    cudaMalloc(&dS, 8 * N * K * K); cudaMalloc(&dG, 8 * ldt * ldt); cudaMalloc(&dP, 8 * (ldt * ldt + 4 * 32 * 33));
+    cudaMemset(dG, 0, 8 * ldt * ldt); cudaMemset(dP, 0, 8 * (ldt * ldt + 4 * 32 * 33));
     cudaMalloc(&dV, 8 * K * K); cudaMalloc(&dmode, 4); cudaMalloc(&dM, 8 * s * K);
     cudaMalloc(&dA, 8 * s * K); cudaMalloc(&dD, 8 * s * K); cudaMalloc(&drs, 8 * s * 4);
     cudaMalloc(&dtp, 8 * gram_scratch_doubles()); cudaMalloc(&dSn, 8 * K * K); cudaMalloc(&dn, 8 * 3);
