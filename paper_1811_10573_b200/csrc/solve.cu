@@ -53,6 +53,18 @@ __device__ double block_sum(double v, double* sh) {
 }
 
 constexpr double PIVOT_TAU = 1e-12;  // L13 / S:201
+
+// 1/d for the factorization's pivots: the hardware approximation (MUFU.RCP64H) refined by two
+// Newton steps -- within an ulp of the correctly rounded value, and off the slow path that
+// __drcp_rn takes on every call (the reciprocal sits on the per-pivot critical path)
+__device__ __forceinline__ double pivot_rcp(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
 constexpr double PINV_TAU = 1e-12;
 constexpr int GF_THREADS = 640;      // factorization: 20 warps = the lower-triangle 16x32 blocks
 constexpr int GP_THREADS = 512;      // Jacobi fallback
@@ -146,7 +158,7 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
     if (rg == 0) {
       if (!(diag > thresh)) bad_s = 1;
       dpiv[0] = diag;
-      rdv[0] = __drcp_rn(diag);
+      rdv[0] = pivot_rcp(diag);
     }
   }
   __syncthreads();
@@ -163,7 +175,7 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
         if (l == j + 1) {
           if (!(diag > thresh)) bad_s = 1;
           dpiv[j + 1] = diag;
-          rdv[b ^ 1] = __drcp_rn(diag);
+          rdv[b ^ 1] = pivot_rcp(diag);
         }
       }
 #pragma unroll
