@@ -267,12 +267,20 @@ def main():
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record(stream)
+    prof_infos = []
     for _ in range(args.steps):
-        step()
+        prof_infos += step()
     p1.record(stream)
     torch.cuda.synchronize()
     prof_ms = p0.elapsed_time(p1)
     kstats = cp.kernel_stats(ctx)
+    # per-phase device time (the profiled pass runs the host loop: one event pair per sweep)
+    phase_us = {}
+    for ph in ("dt", "pp-build", "pp-approx"):
+        v = sorted(i["seconds"] * 1e6 for i in prof_infos if i["phase"] == ph)
+        if v:
+            phase_us[ph] = {"median": v[len(v) // 2], "count_per_step": len(v) / args.steps}
+    algo_flops = sum(k["flops"] for k in kstats.values()) / max(args.steps, 1)
 
     # ---- roofline of the dominant kernel class
     peaks = {}
@@ -406,6 +414,8 @@ def main():
             "roofline": roofline, "roofline_all": roof_all, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
             "profiled_ms_per_step": prof_ms / args.steps,
+            "phase_us": phase_us,
+            "algorithmic_gflops": algo_flops / (ms / args.steps * 1e-3) / 1e9,
         }
         print(json.dumps(line))
     cp.cp_destroy(ctx)
