@@ -206,7 +206,7 @@ def main():
         gen_ctx = cp.cp_init(tmp, cfg.N, dims, cfg.K, stream=stream, device=local, flags=cp.FLAG_BORROW_TENSOR,
                              nccl_unique_id=nccl_id, rank=rank, world=world, torch_workspace=False, **shard)
         del tmp
-    cp.cppp_generate(X_dev, dims, cfg.K, A_true, kind, cfg.noise, 0, row_lo, row_hi, stream=stream, ctx=gen_ctx)
+    cp.cppp_generate(X_dev, dims, cfg.rank_true, A_true, kind, cfg.noise, 0, row_lo, row_hi, stream=stream, ctx=gen_ctx)
     if gen_ctx is not None:
         cp.cp_destroy(gen_ctx)
         obj = [cp.cppp_nccl_unique_id() if rank == 0 else None]

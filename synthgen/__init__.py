@@ -33,7 +33,7 @@ import numpy as np
 
 __all__ = [
     "philox4x32_10", "philox4x32_10_raw", "uniform", "normal", "Config", "CONFIGS", "get_config",
-    "true_factors", "initial_factors", "kruskal_slab", "make_tensor", "collinearity_c",
+    "true_factors", "initial_factors", "kruskal_slab", "make_tensor", "collinearity_c", "laplacian_1d",
 ]
 
 _M0 = np.uint64(0xD2511F53)
@@ -121,17 +121,22 @@ class Config:
     N: int
     s: int
     K: int
-    family: str                 # "uniform" | "collinear" | "gaussian"
+    family: str                 # "uniform" | "collinear" | "gaussian" | "laplacian"
     noise_kind: str             # "none" | "abs" (std) | "rel" (eta * ||X_true|| / ||noise||)
     noise: float = 0.0
     c_lo: float = 0.0
     c_hi: float = 0.0
     sweeps: int = 20
     eps_pp: float = 0.1
+    R_true: int = 0             # rank of the generating CP model (0: the decomposition rank K)
 
     @property
     def dims(self):
         return (self.s,) * self.N
+
+    @property
+    def rank_true(self):
+        return self.R_true if self.R_true > 0 else self.K
 
     @property
     def numel(self):
@@ -154,6 +159,16 @@ CONFIGS = {
     "C2mini": Config("C2mini", 3, 72, 24, "collinear", "rel", 0.01, 0.6, 0.8),
     "C3mini": Config("C3mini", 4, 20, 12, "uniform", "rel", 0.01),
     "C4mini": Config("C4mini", 6, 8, 10, "collinear", "none", 0.0, 0.5, 0.9),
+    # the paper's own workloads, synthetic:
+    # weak-scaling shape at p = 1 (N = 6, s = floor(32 p^(1/6)), R = floor(4 p^(1/6))); the paper
+    # does not say what those tensors hold: reading, Tensor 3 (U[0,1) factors, R = K) + 1% noise
+    "P6W": Config("P6W", 6, 32, 4, "uniform", "rel", 0.01),
+    # strong-scaling shape (N = 6, s = 50, R = 6): 1.56e10 entries, 125 GB -- fits one B200
+    "P6S": Config("P6S", 6, 50, 6, "uniform", "rel", 0.01),
+    # compact Laplacian tensor (Tensor 2) of order 6 with n = 5 (s = n^2 = 25),
+    # CP rank 6, approximated with rank 2 as in the paper
+    "LAP": Config("LAP", 6, 25, 2, "laplacian", "none", 0.0, R_true=6),
+    "LAPmini": Config("LAPmini", 4, 9, 2, "laplacian", "none", 0.0, R_true=4),
 }
 
 
@@ -167,10 +182,16 @@ def collinearity_c(cfg: Config, n: int, seed: int = 0) -> float:
     return cfg.c_lo + (cfg.c_hi - cfg.c_lo) * u
 
 
-def _factor_draw(cfg: Config, n: int, stream: int, kind: str, seed: int) -> np.ndarray:
-    idx = np.arange(cfg.s * cfg.K, dtype=np.uint64)
+def _factor_draw(cfg: Config, n: int, stream: int, kind: str, seed: int, R: int = 0) -> np.ndarray:
+    R = R or cfg.K
+    idx = np.arange(cfg.s * R, dtype=np.uint64)
     v = uniform(idx, stream, seed) if kind == "uniform" else normal(idx, stream, seed)
-    return v.reshape(cfg.s, cfg.K)
+    return v.reshape(cfg.s, R)
+
+
+def laplacian_1d(n: int) -> np.ndarray:
+    """The 1-D second-difference matrix tridiag(-1, 2, -1) (reading of the paper's D)."""
+    return 2.0 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)
 
 
 def true_factors(cfg: Config, seed: int = 0):
@@ -179,17 +200,28 @@ def true_factors(cfg: Config, seed: int = 0):
     uniform  : i.i.d. U[0,1)  (Tensor 3)
     gaussian : i.i.d. N(0,1)  (BASELINE configs[4])
     collinear: Cholesky mixing (L18): A = normalize_columns(G L^T), C_n = (1-c)I + c 11^T = L L^T
+    laplacian: Tensor 2, X = sum_k vec(I) o ... o vec(D) o ... o vec(I) (D in
+               position k): A^(n)[:, k] = vec(D) if k == n else vec(I); s = n_D^2, rank N.
+    Columns: cfg.rank_true.
     """
     out = []
+    R = cfg.rank_true
     for n in range(cfg.N):
         if cfg.family == "uniform":
-            out.append(_factor_draw(cfg, n, n, "uniform", seed))
+            out.append(_factor_draw(cfg, n, n, "uniform", seed, R))
         elif cfg.family == "gaussian":
-            out.append(_factor_draw(cfg, n, n, "normal", seed))
+            out.append(_factor_draw(cfg, n, n, "normal", seed, R))
+        elif cfg.family == "laplacian":
+            nd = int(round(math.sqrt(cfg.s)))
+            assert nd * nd == cfg.s and R == cfg.N, "laplacian: s = n^2 and rank N"
+            A = np.empty((cfg.s, R))
+            for k in range(R):
+                A[:, k] = (laplacian_1d(nd) if k == n else np.eye(nd)).ravel()
+            out.append(A)
         elif cfg.family == "collinear":
-            G = _factor_draw(cfg, n, n, "normal", seed)
+            G = _factor_draw(cfg, n, n, "normal", seed, R)
             c = collinearity_c(cfg, n, seed)
-            C = (1.0 - c) * np.eye(cfg.K) + c * np.ones((cfg.K, cfg.K))
+            C = (1.0 - c) * np.eye(R) + c * np.ones((R, R))
             L = np.linalg.cholesky(C)
             A = G @ L.T
             A = A / np.linalg.norm(A, axis=0, keepdims=True)

@@ -77,3 +77,31 @@ def test_relative_noise_level():
     Xt = G.kruskal_slab(A)
     X = G.make_tensor(cfg, A_true=A)
     assert abs(np.linalg.norm(X - Xt) / np.linalg.norm(Xt) - 0.01) < 1e-12
+
+
+def test_laplacian_tensor_is_the_papers_sum_of_outer_products():
+    """Tensor 2: X = sum_k vec(I) o ... o vec(D) o ... o vec(I), D in position k,
+    written out directly with the 1-D second-difference matrix D = tridiag(-1, 2, -1)."""
+    cfg = G.CONFIGS["LAPmini"]          # order 4, n = 3 (s = 9), CP rank 4
+    n = 3
+    D = 2.0 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)
+    vI, vD = np.eye(n).ravel(), D.ravel()
+    ref = np.zeros(cfg.dims)
+    for k in range(cfg.N):
+        vecs = [vD if m == k else vI for m in range(cfg.N)]
+        ref += np.einsum("a,b,c,d->abcd", *vecs)
+    X = G.make_tensor(cfg)
+    assert np.array_equal(X, ref) or np.allclose(X, ref, rtol=0, atol=1e-15)
+    # it is the d-dimensional Laplacian operator, entry (i, j) of sum_k I x .. x D x .. x I,
+    # with the row and column indices of each factor interleaved into one mode of size n^2
+    A = G.true_factors(cfg)
+    assert all(a.shape == (9, 4) for a in A)
+    assert cfg.rank_true == 4 and cfg.K == 2
+
+
+def test_paper_scaling_shapes():
+    """f4 shapes: weak scaling at p = 1 and the strong-scaling tensor."""
+    w, s = G.CONFIGS["P6W"], G.CONFIGS["P6S"]
+    assert (w.N, w.s, w.K) == (6, int(32 * 1 ** (1 / 6)), int(4 * 1 ** (1 / 6)))
+    assert (s.N, s.s, s.K) == (6, 50, 6)
+    assert s.numel * 8 == 125 * 10 ** 9

@@ -15,7 +15,7 @@ import paper_1811_10573_b200.cppp as cp  # noqa: E402
 cfg = G.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C4"]
 X = torch.empty(cfg.s ** cfg.N, dtype=torch.float64, device="cuda")
 kind = {"none": 0, "abs": 1, "rel": 2}[cfg.noise_kind]
-cp.cppp_generate(X, cfg.dims, cfg.K, G.true_factors(cfg), kind, cfg.noise, 0)
+cp.cppp_generate(X, cfg.dims, cfg.rank_true, G.true_factors(cfg), kind, cfg.noise, 0)
 Xh = torch.empty(X.numel(), dtype=torch.float64, pin_memory=True)
 Xh.copy_(X.cpu())
 A0 = [torch.from_numpy(a).pin_memory() for a in G.initial_factors(cfg)]

@@ -31,7 +31,7 @@ def main():
     stream = torch.cuda.current_stream()
     X = torch.empty(cfg.s ** cfg.N, dtype=torch.float64, device="cuda")
     kind = {"none": 0, "abs": 1, "rel": 2}[cfg.noise_kind]
-    cp.cppp_generate(X, cfg.dims, cfg.K, G.true_factors(cfg), kind, cfg.noise, 0, stream=stream)
+    cp.cppp_generate(X, cfg.dims, cfg.rank_true, G.true_factors(cfg), kind, cfg.noise, 0, stream=stream)
     A0 = [torch.from_numpy(x).cuda() for x in G.initial_factors(cfg)]
     ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K, stream=stream,
                      flags=cp.FLAG_BORROW_TENSOR | cp.FLAG_PROFILE | a.flags)
