@@ -500,11 +500,16 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
   int64_t nsplit = 0;
   int ks = 1;
   const int64_t full_grid = static_cast<int64_t>(sms) * occ;
-  if (ntiles < full_grid && nk >= 32 && ntiles <= TTM_TICKETS) {
-    // few tiles, long reduction (the multi-mode first level): split every tile into ks k
-    // chunks, the smallest ks whose units fill their last wave to >= 90% (else the fullest)
+  const double eff1 = [&] {
+    const double w = static_cast<double>(ntiles) / full_grid;
+    return w / std::ceil(w);
+  }();
+  if (eff1 < 0.9 && nk >= 32 && ntiles <= TTM_TICKETS) {
+    // few tiles or a badly filled last wave, and a long reduction (the multi-mode first level):
+    // split every tile into ks k chunks, the smallest ks whose units fill their last wave to
+    // >= 90% (else the fullest)
     int best = 1;
-    double best_eff = 0.0;
+    double best_eff = eff1;
     for (int k = 2; k <= 32 && k <= nk / 8 && ntiles * k * slot <= TTM_PART; ++k) {
       const double waves = static_cast<double>(ntiles * k) / full_grid;
       const double eff = waves / std::ceil(waves);
@@ -521,7 +526,8 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
     } else {
       ks = 1;
     }
-  } else {
+  }
+  if (ks == 1) {
     // a last wave at most half full is split into k halves (one wave of half-tiles)
     const int64_t tail = ntiles % grid;
     if (ntiles > grid && tail > 0 && 2 * tail <= grid && tail * 2 * slot <= TTM_PART && nk >= 4) {
