@@ -171,6 +171,19 @@ cppp_status pp_get_single(cppp_ctx *ctx, int n, double *out);
  * M_tilde (s_n x K).  Parity entry for hot-path part (c).  CPPP_ESTATE before a build. */
 cppp_status pp_update(cppp_ctx *ctx, int n, double *M_tilde);
 
+/* PP error monitor (Thm 4.1).  At the current factors A and
+ * the operators' A_p (dA = A - A_p), for every mode n and column k (outputs N x K, row n):
+ *   err[n][k]   = ||m~_k^(n) - m_k^(n)|| / ||m_k^(n)||      (M~ as pp_update, M the exact MTTKRP)
+ *   eps[n][k]   = ||da_k^(n)|| / ||a_k^(n)||                (the ε_k^(n) of Thm 4.1)
+ *   bound[n][k] = ||X||_F Σ_{S ⊆ modes≠n, |S|>=2} Π_{i∈S} ||da_k^(i)|| Π_{j∉S} ||a_p,k^(j)||
+ *                 / ||m_k^(n)||   — a certificate: err <= bound (the second-and-higher-order terms
+ *                 of the P:548 expansion, each bounded with ||X x_S v|| <= ||X||_F Π||v||).
+ * A ratio with a zero denominator is 0 when its numerator is 0, else +inf.  Any output may be
+ * NULL (host or device pointers).  Costs one DT pass (M is left holding the exact MTTKRPs) and N
+ * PP updates; factors, operators and the phase state are unchanged.  CPPP_ESTATE before
+ * cp_set_factors or pp_build_operators. */
+cppp_status pp_error(cppp_ctx *ctx, double *err, double *eps, double *bound);
+
 /* One CP-ALS-PP sweep (Alg. 3, readings L7-L12): phase chosen by the state
  * machine unless cp_set_phase_override forces it.  eps: global stop on Σ||G||;
  * eps_pp: PP tolerance on the relative factor change.  info may be NULL. */

@@ -23,6 +23,9 @@ What is the plain definition and what follows an algorithm
     and Alg. 3 follow the paper step by step in its order.
   * Fitness (not defined by the paper, L17) is the expansion of S:177.
 
+Error analysis: Alg. 5's pushed updates (cp_als_pushed) and the
+column-wise PP error monitor with its certificate (pp_error_monitor, Thm 4.1).
+
 Pins: every function here is pinned by tests in tests/test_oracle_*.py against closed
 forms, brute-force index loops, invariants and printed examples — see DESIGN.md
 "Oracle pins".  Parity unpinned: none of the functions below (the whole-trajectory
@@ -381,3 +384,88 @@ def pp_cp_als(X, A0, eps: float, eps_pp: float, max_sweeps: int,
         if gsum <= eps:
             break
     return st.A, trace
+
+
+# --------------------------------------------------------------------------------------
+# Error analysis (§4.1)
+# --------------------------------------------------------------------------------------
+def cp_als_pushed(X, A0, sweeps: int):
+    """Alg. 5, the reinterpreted ALS: every M^(n) formed once from the initial
+    factors; then, per mode n in order, Γ^(n), A_new = M^(n) Γ^(n)†,
+    δA^(n) = A_new - A^(n), A^(n) <- A_new, S^(n) <- A^T A, and the update
+    is pushed to every other right-hand side:
+        M^(m)(x,k) += Σ_y M^(m,n)(x,y,k) δA^(n)(y,k)   (= H^(m,n))
+    with M^(m,n) (Def. 3.1) at the current factors — the oracle-like use P:779 names.  Runs a
+    fixed number of sweeps (the while test of P:756 left to the caller); returns (factors,
+    fitness trace) like cp_als."""
+    X = np.asarray(X, dtype=np.float64)
+    N = X.ndim
+    A = [np.array(a, dtype=np.float64, copy=True) for a in A0]
+    S = [gram(a) for a in A]
+    M = [mttkrp(X, A, n) for n in range(N)]
+    normX_sq = float(np.dot(X.ravel(), X.ravel()))
+    trace = []
+    for _ in range(sweeps):
+        for n in range(N):
+            Gm = gamma(S, n)
+            A_new = solve_normal(M[n], Gm)
+            dA = A_new - A[n]
+            A[n] = A_new
+            S[n] = gram(A_new)
+            if n == N - 1:
+                M_last, Gamma_last = M[n], Gm
+            for m in range(N):
+                if m == n:
+                    continue
+                lo, hi = min(m, n), max(m, n)
+                Mmn = partial_mttkrp(X, A, [lo, hi])          # M^(lo,hi), current factors
+                Mmn = Mmn if m < n else np.transpose(Mmn, (1, 0, 2))   # index (x_m, y_n, k)
+                M[m] = M[m] + np.einsum("xyk,yk->xk", Mmn, dA)
+        trace.append(fitness_from(normX_sq, M_last, A[N - 1], Gamma_last, S[N - 1]))
+    return A, trace
+
+
+def pp_error_monitor(X, A, A_p):
+    """Column-wise error of the PP approximation at factors A with operators built at A_p.
+
+    For every mode n and column k, with dA = A - A_p:
+      err[n][k]   = ||m~_k - m_k|| / ||m_k||: M~ the first two terms of the P:548 expansion
+                    (P:553), M the exact MTTKRP at A (P:394);
+      eps[n][k]   = ||da_k^(n)|| / ||a_k^(n)|| (the ε_k^(n) of Thm 4.1, P:793);
+      bound[n][k] = ||X||_F Σ_{S ⊆ {i≠n}, |S| >= 2} Π_{i∈S} ||da_k^(i)|| Π_{j∉S} ||a_p,k^(j)||
+                    / ||m_k||: every dropped term of P:548 contracts X with the vectors da
+                    (i ∈ S) and a_p (j ∉ S), and ||X ×_S v|| <= ||X||_F Π ||v|| — the
+                    expansion of the proof of Thm 4.1 applied to M.
+    A ratio with zero denominator is 0 for a zero numerator, else inf.  Returns three N x K
+    arrays."""
+    X = np.asarray(X, dtype=np.float64)
+    N = X.ndim
+    K = A[0].shape[1]
+    ops = pp_operators(X, A_p)
+    dA = [a - ap for a, ap in zip(A, A_p)]
+    normX = math.sqrt(float(np.dot(X.ravel(), X.ravel())))
+
+    def ratio(num, den):
+        if num == 0.0:
+            return 0.0
+        return num / den if den > 0.0 else math.inf
+
+    err = np.zeros((N, K))
+    eps = np.zeros((N, K))
+    bound = np.zeros((N, K))
+    for n in range(N):
+        M = mttkrp(X, A, n)
+        Mt = pp_update(pp_single(ops, A_p, n, N), ops, dA, n)
+        others = [i for i in range(N) if i != n]
+        for k in range(K):
+            mk = float(np.linalg.norm(M[:, k]))
+            err[n, k] = ratio(float(np.linalg.norm(Mt[:, k] - M[:, k])), mk)
+            eps[n, k] = ratio(float(np.linalg.norm(dA[n][:, k])), float(np.linalg.norm(A[n][:, k])))
+            d = {i: float(np.linalg.norm(dA[i][:, k])) for i in others}
+            p = {i: float(np.linalg.norm(A_p[i][:, k])) for i in others}
+            tot = 0.0
+            for size in range(2, len(others) + 1):
+                for Sset in combinations(others, size):
+                    tot += math.prod(d[i] if i in Sset else p[i] for i in others)
+            bound[n, k] = ratio(normX * tot, mk)
+    return err, eps, bound

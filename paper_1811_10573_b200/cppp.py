@@ -7,7 +7,7 @@ status codes into exceptions.  There is no CPU fallback: if the library or a CUD
 missing, every call raises.
 
 Function names mirror the C ABI: cp_init, cp_set_factors, cp_get_factors, mttkrp_dt,
-pp_build_operators, pp_get_operator, pp_get_single, pp_update, als_sweep,
+pp_build_operators, pp_get_operator, pp_get_single, pp_update, pp_error, als_sweep,
 cp_set_phase_override, fitness, cppp_generate, cp_destroy.
 """
 from __future__ import annotations
@@ -92,6 +92,7 @@ def lib():
         "pp_get_operator": (I, [P, I, I, P]),
         "pp_get_single": (I, [P, I, P]),
         "pp_update": (I, [P, I, P]),
+        "pp_error": (I, [P, P, P, P]),
         "als_sweep": (I, [P, D, D, C.POINTER(SweepInfo)]),
         "als_run": (I, [P, D, D, I, C.POINTER(SweepInfo), C.POINTER(I)]),
         "cp_set_phase_override": (I, [P, I]),
@@ -119,7 +120,7 @@ def lib():
 EXPORTED = ["cppp_default_opts", "cppp_workspace_bytes", "cp_init", "cp_load_tensor", "cp_set_factors",
             "cp_update_factors",
             "cp_get_factors", "mttkrp_dt", "pp_build_operators", "pp_get_operator",
-            "pp_get_single", "pp_update", "als_sweep", "als_run", "cp_set_phase_override", "fitness",
+            "pp_get_single", "pp_update", "pp_error", "als_sweep", "als_run", "cp_set_phase_override", "fitness",
             "cppp_kernel_stats", "cppp_reset_kernel_stats", "cppp_generate",
             "cppp_nccl_unique_id", "cppp_plan_describe", "cp_destroy", "cp_last_error",
             "cppp_status_string", "cppp_version", "cppp_launch_count"]
@@ -279,6 +280,14 @@ def pp_update(ctx: Ctx, n: int, out=None) -> np.ndarray:
         out = np.empty((ctx.local_rows[n], ctx.K))
     _check(ctx, lib().pp_update(ctx.h, n, _ptr(out)))
     return out
+
+
+def pp_error(ctx: Ctx):
+    """pp_error (include/cppp.h): (err, eps, bound), each N x K — the column-wise relative error
+    of the PP approximation M~ against the exact MTTKRP, ε_k^(n), and the error certificate."""
+    err, eps, bound = (np.empty((ctx.N, ctx.K)) for _ in range(3))
+    _check(ctx, lib().pp_error(ctx.h, _ptr(err), _ptr(eps), _ptr(bound)))
+    return err, eps, bound
 
 
 def als_sweep(ctx: Ctx, eps: float, eps_pp: float) -> dict:

@@ -1,0 +1,104 @@
+// diag.cu — the pairwise-perturbation error monitor: column sums of squares of
+// two K-column matrices and the per-column error ratios and bound certificate built from them.
+//
+// P:548 writes M^(n) as M_p^(n) + the first-order terms (what PP keeps) + every term that
+// contracts X with two or more dA^(i) (what PP drops).  With p_i = ||a_p,k^(i)||, d_i =
+// ||da_k^(i)|| and ||X ×_S v|| <= ||X||_F Π ||v|| (the tensor spectral norm is at most the
+// Frobenius norm), the dropped part of column k is bounded by
+//     ||m~_k − m_k|| <= ||X||_F Σ_{S ⊆ others, |S| >= 2} Π_{i∈S} d_i Π_{j∉S} p_j
+// — the expansion in the proof of Thm 4.1 applied to M instead of H, with the
+// matrix 2-norms replaced by ||X||_F.  Every quantity here is computed on the device.
+#include <math_constants.h>
+
+#include "internal.h"
+
+namespace cppp {
+namespace {
+
+constexpr int CS_COLS = 32;   // columns per CTA (one per lane)
+constexpr int CS_ROWS = 8;    // row groups per CTA
+
+// sums[0][k] = Σ_y (a − b)², sums[1][k] = Σ_y b², sums[2][k] = Σ_y a²  (rows x K, row-major).
+// Rows are visited in ascending order per row group and the 8 groups added in order: the
+// result does not depend on the launch.
+__global__ void colsq_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                             int64_t rows, int K, double* __restrict__ sums) {
+  __shared__ double red[3][CS_ROWS][CS_COLS];
+  const int kx = threadIdx.x, ry = threadIdx.y;
+  const int k = blockIdx.x * CS_COLS + kx;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  if (k < K) {
+    for (int64_t y = ry; y < rows; y += CS_ROWS) {
+      const double av = a[y * K + k], bv = b[y * K + k], dv = av - bv;
+      s0 = fma(dv, dv, s0);
+      s1 = fma(bv, bv, s1);
+      s2 = fma(av, av, s2);
+    }
+  }
+  red[0][ry][kx] = s0;
+  red[1][ry][kx] = s1;
+  red[2][ry][kx] = s2;
+  __syncthreads();
+  if (ry < 3 && k < K) {
+    double t = 0.0;
+    for (int r = 0; r < CS_ROWS; ++r) t += red[ry][r][kx];
+    sums[ry * K + k] = t;
+  }
+}
+
+// One thread per (n, k).  msum[n] / asum[n]: the colsq sums of (M~^(n), M^(n)) and
+// (A_p^(n), A^(n)).  Outputs [N][K]: err = ||m~ − m|| / ||m||, eps = ||da|| / ||a||,
+// bound = the certificate above divided by ||m||.
+__global__ void pp_error_final_kernel(const double* __restrict__ msum, const double* __restrict__ asum,
+                                      int N, int K, double normX, double* __restrict__ err,
+                                      double* __restrict__ eps, double* __restrict__ bound) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= N * K) return;
+  const int n = idx / K, k = idx - n * K;
+  auto ratio = [](double num, double den) {
+    if (num == 0.0) return 0.0;
+    return den > 0.0 ? sqrt(num / den) : CUDART_INF;
+  };
+  const double* ms = msum + static_cast<int64_t>(n) * 3 * K;
+  const double* as = asum + static_cast<int64_t>(n) * 3 * K;
+  err[idx] = ratio(ms[k], ms[K + k]);
+  eps[idx] = ratio(as[k], as[K + k]);
+  double p[CPPP_MAX_ORDER_], d[CPPP_MAX_ORDER_];
+  int m = 0;
+  for (int i = 0; i < N; ++i) {
+    if (i == n) continue;
+    const double* ai = asum + static_cast<int64_t>(i) * 3 * K;
+    d[m] = sqrt(ai[k]);           // ||a_p − a|| = ||da||
+    p[m] = sqrt(ai[2 * K + k]);   // ||a_p||
+    ++m;
+  }
+  double tot = 0.0;
+  for (unsigned S = 0; S < (1u << m); ++S) {   // subsets in ascending bit order
+    if (__popc(S) < 2) continue;
+    double t = 1.0;
+    for (int i = 0; i < m; ++i) t *= (S >> i) & 1u ? d[i] : p[i];
+    tot += t;
+  }
+  const double mn = sqrt(ms[K + k]);
+  bound[idx] = tot == 0.0 ? 0.0 : (mn > 0.0 ? normX * tot / mn : CUDART_INF);
+}
+
+}  // namespace
+
+cudaError_t launch_colsq(const double* a, const double* b, int64_t rows, int K, double* sums,
+                         cudaStream_t st) {
+  colsq_kernel<<<(K + CS_COLS - 1) / CS_COLS, dim3(CS_COLS, CS_ROWS), 0, st>>>(a, b, rows, K, sums);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pp_error_final(const double* msum, const double* asum, int N, int K,
+                                  double normX, double* err, double* eps, double* bound,
+                                  cudaStream_t st) {
+  const int n = N * K;
+  pp_error_final_kernel<<<(n + 127) / 128, 128, 0, st>>>(msum, asum, N, K, normX, err, eps, bound);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace cppp

@@ -120,6 +120,7 @@ struct cppp_ctx {
   double* pp_partial = nullptr;
   double* sq_partial = nullptr;
   double* gath = nullptr;    // gather scratch (max s x K)
+  double* chk = nullptr;     // pp_error: M~ scratch (max s x K), [N][3][K] sums x 2, [3][N][K] out
   double* ttv_scratch = nullptr;
   double* gen_scratch = nullptr;
   Stack stack;
@@ -1097,6 +1098,7 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   size_t oPP = take(sizeof(double) * pp_update_scratch_doubles(smax, K, smax));
   size_t oSq = take(sizeof(double) * 2048);
   size_t oGath = take(sizeof(double) * smax * K);
+  size_t oChk = take(sizeof(double) * (smax * K + 9 * N * K));
   size_t oTtv = take(sizeof(double) * ttv_scratch_doubles());
   size_t oStack = off;
   plan->off_stack = oStack;
@@ -1137,6 +1139,7 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   c->pp_partial = reinterpret_cast<double*>(b + oPP);
   c->sq_partial = reinterpret_cast<double*>(b + oSq);
   c->gath = reinterpret_cast<double*>(b + oGath);
+  c->chk = reinterpret_cast<double*>(b + oChk);
   c->ttv_scratch = reinterpret_cast<double*>(b + oTtv);
   c->stack = Stack{};
   c->stack.base = b + oStack;
@@ -1477,13 +1480,8 @@ cppp_status pp_get_single(cppp_ctx* c, int n, double* out) {
   return copy_out(c, out, c->Mp[n], (size_t)c->dl[n] * c->K);
 }
 
-cppp_status pp_update(cppp_ctx* c, int n, double* M_tilde) {
-  if (!c) return CPPP_EINVAL;
-  if (n < 0 || n >= c->N) return fail(c, CPPP_EINVAL, "mode %d out of range", n);
-  if (!c->ops_valid) return fail(c, CPPP_ESTATE, "pp_update before pp_build_operators");
-  // dA = A - A_p for every mode (the caller may have moved the factors)
-  for (int i = 0; i < c->N; ++i)
-    CUCHK(c, launch_sub(c->A[i], c->Ap[i], c->dA[i], c->s[i] * c->K, c->st));
+// M~^(n) at the current factors into `out` (dA = A - A_p already formed)
+static cppp_status pp_approx_mode(cppp_ctx* c, int n, double* out) {
   const bool sh = c->q >= 0 && comm_on(c);
   if (sh && n != c->q) {
     // partial term over the local rows of the sharded mode, then all-reduce
@@ -1504,11 +1502,54 @@ cppp_status pp_update(cppp_ctx* c, int n, double* M_tilde) {
     a.t[0] = t;
     CUCHK(c, launch_pp_update(a, c->st));
     STCHK(allreduce(c, c->T[n], (size_t)c->dl[n] * c->K));
-    STCHK(pp_update_mode(c, n, c->M[n], c->T[n], true, c->Mp[n]));
-  } else {
-    STCHK(pp_update_mode(c, n, c->M[n], nullptr, false, c->Mp[n]));
+    return pp_update_mode(c, n, out, c->T[n], true, c->Mp[n]);
   }
+  return pp_update_mode(c, n, out, nullptr, false, c->Mp[n]);
+}
+
+cppp_status pp_update(cppp_ctx* c, int n, double* M_tilde) {
+  if (!c) return CPPP_EINVAL;
+  if (n < 0 || n >= c->N) return fail(c, CPPP_EINVAL, "mode %d out of range", n);
+  if (!c->ops_valid) return fail(c, CPPP_ESTATE, "pp_update before pp_build_operators");
+  // dA = A - A_p for every mode (the caller may have moved the factors)
+  for (int i = 0; i < c->N; ++i)
+    CUCHK(c, launch_sub(c->A[i], c->Ap[i], c->dA[i], c->s[i] * c->K, c->st));
+  STCHK(pp_approx_mode(c, n, c->M[n]));
   if (M_tilde) STCHK(copy_out(c, M_tilde, c->M[n], (size_t)c->dl[n] * c->K));
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  prof_collect(c);
+  return CPPP_OK;
+}
+
+// PP error monitor (Thm 4.1): exact MTTKRPs at the
+// current factors (one DT pass, M <- M), each mode's M~ into scratch, column sums of squares,
+// then the ratios and the bound certificate (diag.cu), all on the device.
+cppp_status pp_error(cppp_ctx* c, double* err, double* eps, double* bound) {
+  if (!c) return CPPP_EINVAL;
+  if (!c->factors_set) return fail(c, CPPP_ESTATE, "pp_error before cp_set_factors");
+  if (!c->ops_valid) return fail(c, CPPP_ESTATE, "pp_error before pp_build_operators");
+  const int N = c->N, K = c->K;
+  int64_t smax = 0;
+  for (int n = 0; n < N; ++n) smax = std::max(smax, c->s[n]);
+  double* Mt = c->chk;
+  double* msum = Mt + smax * K;          // [N][3][K]
+  double* asum = msum + 3 * N * K;       // [N][3][K]
+  double* out = asum + 3 * N * K;        // err | eps | bound, each [N][K]
+  STCHK(run_dt(c, false, c->M));
+  for (int i = 0; i < N; ++i)
+    CUCHK(c, launch_sub(c->A[i], c->Ap[i], c->dA[i], c->s[i] * K, c->st));
+  for (int n = 0; n < N; ++n) {
+    STCHK(pp_approx_mode(c, n, Mt));
+    CUCHK(c, launch_colsq(Mt, c->M[n], c->dl[n], K, msum + (int64_t)n * 3 * K, c->st));
+    CUCHK(c, launch_colsq(c->Ap[n], c->A[n], c->s[n], K, asum + (int64_t)n * 3 * K, c->st));
+  }
+  // the sharded mode's M rows are local: its sums are completed across ranks
+  if (c->q >= 0 && comm_on(c)) STCHK(allreduce(c, msum + (int64_t)c->q * 3 * K, (size_t)3 * K));
+  CUCHK(c, launch_pp_error_final(msum, asum, N, K, std::sqrt(c->normX_sq), out, out + N * K,
+                                 out + 2 * N * K, c->st));
+  double* dst[3] = {err, eps, bound};
+  for (int j = 0; j < 3; ++j)
+    if (dst[j]) STCHK(copy_out(c, dst[j], out + (int64_t)j * N * K, (size_t)N * K));
   CUCHK(c, cudaStreamSynchronize(c->st));
   prof_collect(c);
   return CPPP_OK;

@@ -161,6 +161,15 @@ cudaError_t launch_sqnorm(const double* x, int64_t n, double* partial, int nblk,
 int sqnorm_blocks(int64_t n);
 // y = a - b (elementwise)
 cudaError_t launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st);
+
+// PP error monitor (diag.cu).  colsq: sums[0..K) = Σ_y (a−b)², [K..2K) = Σ_y b², [2K..3K) = Σ_y a²
+// over a rows x K row-major pair.  pp_error_final: per (n, k) the error ratio, ε and bound
+// certificate from the [N][3][K] sums of (M~, M) and (A_p, A).
+cudaError_t launch_colsq(const double* a, const double* b, int64_t rows, int K, double* sums,
+                         cudaStream_t st);
+cudaError_t launch_pp_error_final(const double* msum, const double* asum, int N, int K,
+                                  double normX, double* err, double* eps, double* bound,
+                                  cudaStream_t st);
 // Fp[x][n] = F[x][n] for n < K, 0 for K <= n < ld (TMA-aligned copy of a factor)
 cudaError_t launch_pad_rows(const double* F, int64_t S, int K, double* Fp, int ld, cudaStream_t st);
 

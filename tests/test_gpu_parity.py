@@ -322,3 +322,70 @@ def test_als_run_device_loop_matches_host_loop(name):
     cp.cp_set_factors(b, A0)
     big = cp.als_run(b, 1e300, cfg.eps_pp, 20)
     assert len(big) == 1 and big[0]["converged"] == 1
+
+
+def moved_factors(Ap, t, seed):
+    """A = A_p + dA with ||da_k|| = t ||a_p,k|| per column."""
+    r = np.random.default_rng(seed)
+    out = []
+    for a in Ap:
+        d = r.standard_normal(a.shape)
+        d *= t * np.linalg.norm(a, axis=0) / np.linalg.norm(d, axis=0)
+        out.append(a + d)
+    return out
+
+
+@pytest.mark.parametrize("name", SMALL + ["LAPmini"])
+@pytest.mark.parametrize("t", [1e-1, 1e-2])
+def test_pp_error_monitor_matches_oracle(name, t):
+    """pp_error against oracle.pp_error_monitor at the same (A, A_p): ε and the
+    certificate to 1e-12 relative; err = ||M~ - M|| / ||M|| is a difference of two FP64
+    results of size ~t²||M||, so it carries their rounding (~1e-15 ||M||) amplified by 1/t²:
+    1e-8 relative plus 1e-13 absolute."""
+    cfg, X, Ap = problem(name)
+    A = moved_factors(Ap, t, 5)
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    cp.cp_set_factors(ctx, Ap)
+    cp.pp_build_operators(ctx)
+    cp.cp_update_factors(ctx, A)
+    err, eps, bound = cp.pp_error(ctx)
+    e_ref, eps_ref, b_ref = O.pp_error_monitor(X, A, Ap)
+    assert np.allclose(eps, eps_ref, rtol=1e-12, atol=0)
+    assert np.allclose(bound, b_ref, rtol=1e-12, atol=0)
+    assert np.all(np.abs(err - e_ref) <= 1e-8 * e_ref + 1e-13), (err, e_ref)
+    assert np.all(err <= bound * (1 + 1e-9))
+    cp.cp_destroy(ctx)
+
+
+def test_pp_error_quadratic_and_run_unchanged():
+    """Device monitor: err(t/10) ≈ err(t)/100, and calling it between sweeps leaves a
+    CP-ALS-PP run bit-identical."""
+    cfg, X, Ap = problem("C3mini")
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    e = []
+    for t in (1e-2, 1e-3):
+        cp.cp_set_factors(ctx, Ap)
+        cp.pp_build_operators(ctx)
+        cp.cp_update_factors(ctx, moved_factors(Ap, t, 6))
+        e.append(cp.pp_error(ctx)[0])
+    assert np.all(np.abs(e[0] / e[1] / 100 - 1) < 0.05)
+    cp.cp_destroy(ctx)
+    cfg, X, A0 = problem("C2mini")
+    _, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, 12)
+    a, b = (cp.cp_init(X, cfg.N, cfg.dims, cfg.K) for _ in range(2))
+    for c in (a, b):
+        cp.cp_set_factors(c, A0)
+    seen = 0
+    for t in tr:
+        for c in (a, b):
+            cp.cp_set_phase_override(c, t["phase"])
+        ia, ib = cp.als_sweep(a, 0.0, cfg.eps_pp), cp.als_sweep(b, 0.0, cfg.eps_pp)
+        assert ia["fitness"] == ib["fitness"], (t, ia, ib)
+        if t["phase"] != "dt":
+            err, eps, bound = cp.pp_error(b)
+            assert np.all(err <= bound * (1 + 1e-9))
+            seen += 1
+    assert seen > 0
+    assert all(np.array_equal(x, y) for x, y in zip(cp.cp_get_factors(a), cp.cp_get_factors(b)))
+    cp.cp_destroy(a)
+    cp.cp_destroy(b)

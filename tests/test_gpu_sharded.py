@@ -182,3 +182,26 @@ def test_nccl_transport_single_rank(name):
         assert rel(M[n], O.mttkrp(X, A, n)) < 1e-11, n
     cp.cp_destroy(nc)
     cp.cp_destroy(plain)
+
+
+def test_pp_error_sharded_single_rank():
+    """pp_error through the sharded branches (one-rank NCCL communicator, FORCE_COMM): the
+    slab mode's column sums go through the all-reduce; values match the oracle."""
+    cfg = G.CONFIGS["C3mini"]
+    X = G.make_tensor(cfg)
+    Ap = G.initial_factors(cfg)
+    r = np.random.default_rng(7)
+    A = [a + 0.02 * r.standard_normal(a.shape) * np.linalg.norm(a, axis=0) / np.sqrt(a.shape[0])
+         for a in Ap]
+    uid = cp.cppp_nccl_unique_id()
+    nc = cp.cp_init(X, cfg.N, cfg.dims, cfg.K, shard_offset=0, shard_extent=cfg.dims[0],
+                    rank=0, world=1, nccl_unique_id=uid, flags=cp.FLAG_FORCE_COMM)
+    cp.cp_set_factors(nc, Ap)
+    cp.pp_build_operators(nc)
+    cp.cp_update_factors(nc, A)
+    err, eps, bound = cp.pp_error(nc)
+    e_ref, eps_ref, b_ref = O.pp_error_monitor(X, A, Ap)
+    assert np.allclose(eps, eps_ref, rtol=1e-12, atol=0)
+    assert np.allclose(bound, b_ref, rtol=1e-12, atol=0)
+    assert np.all(np.abs(err - e_ref) <= 1e-8 * e_ref + 1e-13)
+    cp.cp_destroy(nc)
