@@ -66,6 +66,8 @@ typedef enum {
 #define CPPP_FLAG_FORCE_COMM  128u  /* take the communicating (sharded) code paths even with one
                                         rank: with a one-rank NCCL communicator this runs the
                                         all-reduce transport on a single GPU (testing) */
+#define CPPP_FLAG_NO_OP_REUSE 256u /* order 3: PP builds recompute M_p^(1,2) instead of taking the
+                                      preceding regular sweep's X x_0 A^(0) (A/B testing) */
 
 typedef struct {
   int device;               /* CUDA ordinal (default 0) */

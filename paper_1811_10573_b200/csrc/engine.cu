@@ -127,6 +127,9 @@ struct cppp_ctx {
   // state
   double normX_sq = 0.0;
   bool ops_valid = false;
+  // order 3: ops[1][2] holds X ×_0 A^(0) for the CURRENT factors (the last sweep was a regular
+  // one, which wrote it), so a PP build can take it instead of recomputing M_p^(1,2)
+  bool op12_fresh = false;
   bool factors_set = false;
   bool borrowed = false;        // X is the caller's device buffer (CPPP_FLAG_BORROW_TENSOR)
   int next_phase = CPPP_PHASE_DT;
@@ -328,6 +331,14 @@ cppp_status allreduce(cppp_ctx* c, double* buf, size_t count) {
 const double* fac_local(cppp_ctx* c, double* const* F, int u) {
   return F[u] + (u == c->q ? c->qoff * c->K : 0);
 }
+// Order 3, unsharded: a regular sweep's right-half TTM X ×_0 A^(0) (A^(0) already final for the
+// sweep) is written straight into the operator slot M_p^(1,2); the PP build that follows a
+// regular sweep (Alg. 3: always, unless a phase is forced) has A_p = A, so that TTM IS its
+// M_p^(1,2) = X ×_0 A_p^(0) — one of the build's three full-tensor TTMs is skipped.  Same kernel,
+// same shape: the operator is bit-identical to a recomputed one (tested).
+bool reuse12(const cppp_ctx* c) {
+  return c->N == 3 && c->q < 0 && !(c->flags & CPPP_FLAG_NO_OP_REUSE);
+}
 int64_t node_elems(cppp_ctx* c, uint32_t mask) {
   int64_t e = c->K;
   for (int v = 0; v < c->N; ++v)
@@ -513,6 +524,8 @@ struct DT {
       const uint32_t nm = cur.mask & ~(1u << u);
       double* dst = (i + 1 == modes.size() && final_dst) ? final_dst
                                                          : c->stack.push(node_elems(c, nm));
+      if (update && reuse12(c) && nd.root && i == 0 && u == 0 && modes.size() == 2)
+        dst = c->ops[1][2];   // (the stack slot stays pushed: sizing is the same either way)
       STCHK(contract(c, cur, u, fac_local(c, c->A, u), dst));
       cur = Node{nm, dst, false};
     }
@@ -542,6 +555,7 @@ struct DT {
     STCHK(contract(c, L, 1, fac_local(c, c->A, 1), c->M[0]));
     STCHK(leaf(0, c->M[0]));
     double* T12 = c->stack.push(node_elems(c, 0x6u));
+    if (update && reuse12(c)) T12 = c->ops[1][2];
     if (!c->dry) {
       CUCHK(c, cudaEventRecord(c->ev_F, c->st));
       CUCHK(c, cudaStreamWaitEvent(c->st3, c->ev_F, 0));
@@ -608,6 +622,7 @@ cppp_status run_dt(cppp_ctx* c, bool update, double* const* Mout) {
 // each computed from it by contracting tau[w] (Tree_Map_PP P:77-91: i = max mu(t)).
 struct PPTree {
   cppp_ctx* c;
+  bool have12 = false;   // ops[1][2] already holds X ×_0 A_p^(0) (reuse12)
   int tau[CPPP_MAX_ORDER];
 
   void init() {
@@ -651,7 +666,8 @@ struct PPTree {
         const uint32_t kept = kept_of(cmu);
         const size_t mk = c->stack.mark();
         double* dst = child_leaf ? op_ptr(kept) : c->stack.push(node_elems(c, kept));
-        STCHK(contract(c, nd, tau[w], fac_local(c, c->Ap, tau[w]), dst));
+        if (!(have12 && child_leaf && kept == 0x6u))
+          STCHK(contract(c, nd, tau[w], fac_local(c, c->Ap, tau[w]), dst));
         STCHK(visit(Node{kept, dst, false}, cmu, level + 1));
         c->stack.release(mk);
       }
@@ -708,7 +724,7 @@ cppp_status build_singles(cppp_ctx* c) {
   return CPPP_OK;
 }
 
-cppp_status run_pp_build(cppp_ctx* c) {
+cppp_status run_pp_build(cppp_ctx* c, bool have12 = false) {
   const int N = c->N, K = c->K;
   if (!c->dry) {
     for (int n = 0; n < N; ++n) {
@@ -718,6 +734,7 @@ cppp_status run_pp_build(cppp_ctx* c) {
     }
   }
   PPTree t{c};
+  t.have12 = have12 && reuse12(c);
   STCHK(t.run());
   // leaves that contracted the sharded mode hold partial sums: all-reduce them (SURVEY C-b)
   if (c->q >= 0)
@@ -826,14 +843,14 @@ cppp_status run_pp_sweep(cppp_ctx* c, bool after_build) {
 }
 
 // ---------------------------------------------------------------- one sweep of a phase
-cppp_status run_phase_eager(cppp_ctx* c, int phase) {
+cppp_status run_phase_eager(cppp_ctx* c, int phase, bool have12 = true) {
   // inside a capture the side stream must fork from an event recorded in the capture
   if (c->capturing) CUCHK(c, cudaEventRecord(c->ev_S, c->st));
   STCHK(prefetch_inverse(c, 0));
   if (phase == CPPP_PHASE_DT) {
     STCHK(run_dt(c, true, c->M));
   } else {
-    if (phase == CPPP_PHASE_PP_BUILD) STCHK(run_pp_build(c));
+    if (phase == CPPP_PHASE_PP_BUILD) STCHK(run_pp_build(c, have12));
     STCHK(run_pp_sweep(c, phase == CPPP_PHASE_PP_BUILD));
   }
   return CPPP_OK;
@@ -844,8 +861,13 @@ cppp_status run_phase_eager(cppp_ctx* c, int phase) {
 cppp_status run_phase(cppp_ctx* c, int phase) {
   const bool graphs = !(c->flags & CPPP_FLAG_NO_GRAPH) && !comm_on(c);
   auto& g = c->graphs[phase];
-  g.uses++;
-  if (!graphs || g.uses < 2) {
+  // the captured PP-build sweep takes M_p^(1,2) from the preceding regular sweep; a build
+  // forced anywhere else recomputes it, eagerly
+  const bool full_build = phase == CPPP_PHASE_PP_BUILD && reuse12(c) && !c->op12_fresh;
+  if (!full_build) g.uses++;
+  if (full_build) {
+    STCHK(run_phase_eager(c, phase, false));
+  } else if (!graphs || g.uses < 2) {
     STCHK(run_phase_eager(c, phase));
   } else {
     if (!g.exec) {
@@ -885,6 +907,10 @@ cppp_status run_phase(cppp_ctx* c, int phase) {
     for (auto& p : g.prof) c->pending_graph.push_back(p);
   }
   if (phase == CPPP_PHASE_PP_BUILD) c->ops_valid = true;
+  if (reuse12(c)) {
+    c->op12_fresh = phase == CPPP_PHASE_DT;
+    if (phase == CPPP_PHASE_DT) c->ops_valid = false;   // M_p^(1,2) was overwritten
+  }
   return CPPP_OK;
 }
 
@@ -1379,6 +1405,7 @@ cppp_status cp_load_tensor(cppp_ctx* c, const double* X) {
   }
   c->factors_set = false;
   c->ops_valid = false;
+  c->op12_fresh = false;
   c->next_phase = CPPP_PHASE_DT;
   return tensor_norm(c);
 }
@@ -1402,6 +1429,7 @@ cppp_status cp_set_factors(cppp_ctx* c, const double* const* A) {
   CUCHK(c, cudaEventRecord(c->ev_S, c->st));
   c->factors_set = true;
   c->ops_valid = false;
+  c->op12_fresh = false;
   c->next_phase = CPPP_PHASE_DT;
   c->sweep = 0;
   c->restarts = 0;
@@ -1426,6 +1454,7 @@ cppp_status cp_update_factors(cppp_ctx* c, const double* const* A) {
   }
   CUCHK(c, cudaEventRecord(c->ev_S, c->st));
   CUCHK(c, cudaStreamSynchronize(c->st));
+  c->op12_fresh = false;
   return CPPP_OK;
 }
 
@@ -1459,6 +1488,7 @@ cppp_status pp_build_operators(cppp_ctx* c) {
   if (!c) return CPPP_EINVAL;
   if (!c->factors_set) return fail(c, CPPP_ESTATE, "pp_build_operators before cp_set_factors");
   STCHK(run_pp_build(c));
+  c->op12_fresh = false;
   CUCHK(c, cudaStreamSynchronize(c->st));
   prof_collect(c);
   return CPPP_OK;
@@ -1624,7 +1654,8 @@ cppp_status als_run(cppp_ctx* c, double eps, double eps_pp, int max_sweeps, cppp
   // forced phase, or a GPU/driver that cannot build the conditional graph
   const bool host_loop = (c->flags & (CPPP_FLAG_PROFILE | CPPP_FLAG_NO_GRAPH)) || comm_on(c) ||
                          c->override_phase != CPPP_PHASE_AUTO || c->run.failed ||
-                         (c->next_phase == CPPP_PHASE_PP && !c->ops_valid);
+                         (c->next_phase == CPPP_PHASE_PP && !c->ops_valid) ||
+                         (c->next_phase == CPPP_PHASE_PP_BUILD && reuse12(c) && !c->op12_fresh);
   if (host_loop) {
     for (int i = 0; i < max_sweeps; ++i) {
       cppp_sweep_info one;
@@ -1671,6 +1702,10 @@ cppp_status als_run(cppp_ctx* c, double eps, double eps_pp, int max_sweeps, cppp
     const RunInfo& r = h->info[i];
     note_launches(c->run.launches_per_sweep[r.phase] + 1);   // + the decision kernel
     if (r.phase == CPPP_PHASE_PP_BUILD) c->ops_valid = true;
+    if (reuse12(c)) {
+      c->op12_fresh = r.phase == CPPP_PHASE_DT;
+      if (r.phase == CPPP_PHASE_DT) c->ops_valid = false;
+    }
     c->sweep++;
     if (info) {
       cppp_sweep_info& o = info[i];

@@ -389,3 +389,36 @@ def test_pp_error_quadratic_and_run_unchanged():
     assert all(np.array_equal(x, y) for x, y in zip(cp.cp_get_factors(a), cp.cp_get_factors(b)))
     cp.cp_destroy(a)
     cp.cp_destroy(b)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2mini"])
+def test_order3_operator_reuse_is_bit_identical(name):
+    """Order 3: the PP build takes M_p^(1,2) from the preceding regular sweep's X ×_0 A^(0)
+    (same kernel, same shape).  Replayed schedule, a forced second build in a row (recomputed),
+    and als_run all match a context that recomputes it (CPPP_FLAG_NO_OP_REUSE) bit for bit."""
+    cfg, X, A0 = problem(name)
+    _, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, 20)
+    assert any(t["phase"] == "pp-build" for t in tr)
+    a = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    b = cp.cp_init(X, cfg.N, cfg.dims, cfg.K, flags=cp.FLAG_NO_OP_REUSE)
+    for c in (a, b):
+        cp.cp_set_factors(c, A0)
+    sched = [t["phase"] for t in tr] + ["pp-build", "pp-build", "pp-approx", "dt", "pp-build"]
+    for ph in sched:
+        ia, ib = [], []
+        for c, out in ((a, ia), (b, ib)):
+            cp.cp_set_phase_override(c, ph)
+            out.append(cp.als_sweep(c, 0.0, cfg.eps_pp))
+        assert ia[0]["fitness"] == ib[0]["fitness"], (ph, ia, ib)
+    for n in range(cfg.N):
+        for i in range(n + 1, cfg.N):
+            assert np.array_equal(cp.pp_get_operator(a, n, i), cp.pp_get_operator(b, n, i))
+    for c in (a, b):
+        cp.cp_set_phase_override(c, cp.PHASE_AUTO)
+        cp.cp_set_factors(c, A0)
+    ra = cp.als_run(a, 0.0, cfg.eps_pp, 20)
+    rb = cp.als_run(b, 0.0, cfg.eps_pp, 20)
+    assert [r["fitness"] for r in ra] == [r["fitness"] for r in rb]
+    assert [r["phase"] for r in ra] == [t["phase"] for t in tr]
+    cp.cp_destroy(a)
+    cp.cp_destroy(b)
