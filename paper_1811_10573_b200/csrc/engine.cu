@@ -348,7 +348,7 @@ int64_t node_elems(cppp_ctx* c, uint32_t mask) {
 
 // out = contraction of `src` along mode u with factor F (local rows)
 cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, double* out,
-                     cudaStream_t st = nullptr) {
+                     cudaStream_t st = nullptr, int reserve_sms = 0) {
   if (!st) st = c->st;
   int64_t B = 1, R = 1;
   for (int v = 0; v < c->N; ++v) {
@@ -365,7 +365,7 @@ cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, doubl
     const bool simt = (c->flags & CPPP_FLAG_SIMT_TTM) != 0;
     if (ttm_uses_dmma(B, S, R, K, simt)) CUCHK(c, ttm_prepare(S, F, K, c->Fpad, st));
     Prof p(c, CPPP_K_TTM, flops, bytes, st);
-    CUCHK(c, launch_ttm_core(src.data, B, S, R, F, K, out, c->Fpad, simt, st));
+    CUCHK(c, launch_ttm_core(src.data, B, S, R, F, K, out, c->Fpad, simt, st, reserve_sms));
   } else {
     const double flops = 2.0 * B * S * R * K;
     const double bytes = 8.0 * (B * S * R * K + B * R * K);
@@ -560,7 +560,14 @@ struct DT {
       CUCHK(c, cudaEventRecord(c->ev_F, c->st));
       CUCHK(c, cudaStreamWaitEvent(c->st3, c->ev_F, 0));
     }
-    STCHK(contract(c, nd, 0, fac_local(c, c->A, 0), T12, c->st3));
+    // two SMs stay free of the GEMM's persistent CTAs: mode 1's factorization, row solves and
+    // Gram and mode 2's factorization (latency-bound, one CTA or a few rows at a time) run there
+    // meanwhile instead of waiting for the GEMM to end
+    static const int reserve = [] {
+      const char* e = getenv("CPPP_TTM_RESERVE");
+      return e ? atoi(e) : 2;
+    }();
+    STCHK(contract(c, nd, 0, fac_local(c, c->A, 0), T12, c->st3, reserve));
     if (!c->dry) CUCHK(c, cudaEventRecord(c->ev_T, c->st3));
     STCHK(contract(c, L, 0, fac_local(c, c->A, 0), c->M[1]));
     STCHK(leaf(1, c->M[1]));

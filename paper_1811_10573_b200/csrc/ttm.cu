@@ -23,6 +23,7 @@
 
 #include <cuda.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -445,7 +446,7 @@ bool make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims,
 template <int NT, bool MC>
 cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
                      double* out, unsigned long long* counter, unsigned int* tickets, double* part,
-                     cudaStream_t st) {
+                     cudaStream_t st, int reserve) {
   using C = Cfg<NT>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -493,13 +494,15 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  int64_t grid = static_cast<int64_t>(sms) * occ;
+  // `reserve` SMs get no CTA: the latency-bound kernels of other streams run there meanwhile
+  // (a persistent CTA holds its SM until the GEMM ends)
+  const int64_t full_grid = std::max<int64_t>(1, static_cast<int64_t>(sms) * occ - reserve);
+  int64_t grid = full_grid;
   if (grid > ntiles) grid = ntiles;
   const int nk = static_cast<int>((S + BK - 1) / BK);
   const int64_t slot = static_cast<int64_t>(NT) * 2 * NWARP * 32;   // doubles per parked chunk
   int64_t nsplit = 0;
   int ks = 1;
-  const int64_t full_grid = static_cast<int64_t>(sms) * occ;
   const double eff1 = [&] {
     const double w = static_cast<double>(ntiles) / full_grid;
     return w / std::ceil(w);
@@ -551,12 +554,12 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
 template <bool MC, int NT = 1>
 cudaError_t dispatch_nt(int nt, const double* X, int64_t B, int64_t S, int64_t R, const double* Fp,
                         int K, double* out, unsigned long long* counter, unsigned int* tickets,
-                        double* part, cudaStream_t st) {
+                        double* part, cudaStream_t st, int reserve) {
   if constexpr (NT > 16) {
     return cudaErrorInvalidValue;
   } else {
-    if (nt == NT) return run_dmma<NT, MC>(X, B, S, R, Fp, K, out, counter, tickets, part, st);
-    return dispatch_nt<MC, NT + 1>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st);
+    if (nt == NT) return run_dmma<NT, MC>(X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve);
+    return dispatch_nt<MC, NT + 1>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve);
   }
 }
 
@@ -646,7 +649,7 @@ cudaError_t launch_ttm_padded(const double* X, int64_t B, int64_t S, int64_t R, 
 
 cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
                             int K, double* out, const double* Fpad, bool force_simt,
-                            cudaStream_t st) {
+                            cudaStream_t st, int reserve_sms) {
   if (B * R * K == 0) return cudaSuccess;
   if (!ttm_uses_dmma(B, S, R, K, force_simt)) return launch_ttm_simt(X, B, S, R, F, K, out, st);
   double* ctl = const_cast<double*>(Fpad);
@@ -655,8 +658,9 @@ cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, co
   double* part = ctl + TTM_CTL;
   const double* Fp = ctl + TTM_CTL + TTM_PART;
   const int nt = (K + 7) / 8;
-  if (R == 1) return dispatch_nt<false>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st);
-  return dispatch_nt<true>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st);
+  if (R == 1)
+    return dispatch_nt<false>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve_sms);
+  return dispatch_nt<true>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve_sms);
 }
 
 cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R, const double* F, int K,
