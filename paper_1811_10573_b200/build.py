@@ -7,8 +7,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcppp.so")
-SOURCES = ["engine.cu", "ttm.cu", "ttv.cu", "ppupdate.cu", "solve.cu", "gen.cu", "diag.cu"]
-HEADERS = ["internal.h", os.path.join("..", "..", "include", "cppp.h")]
+SOURCES = ["engine.cu", "ttm.cu", "ttv.cu", "ppupdate.cu", "solve.cu", "gen.cu", "diag.cu", "tucker.cu"]
+HEADERS = ["internal.h", os.path.join("..", "..", "include", "cppp.h"),
+           os.path.join("..", "..", "include", "cppp_tucker.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
          "-gencode", "arch=compute_100a,code=sm_100a", "-I", os.path.join(ROOT, "include"),

@@ -109,6 +109,16 @@ def lib():
         "cppp_status_string": (C.c_char_p, [I]),
         "cppp_version": (C.c_char_p, []),
         "cppp_launch_count": (C.c_uint64, []),
+        "tk_init": (I, [C.POINTER(P), P, I, C.POINTER(C.c_int64), C.POINTER(I), P, C.c_uint]),
+        "tk_set_factors": (I, [P, C.POINTER(P)]),
+        "tk_update_factors": (I, [P, C.POINTER(P)]),
+        "tk_ttmc": (I, [P, C.POINTER(P)]),
+        "tk_pp_build": (I, [P]),
+        "tk_pp_get_operator": (I, [P, I, I, P]),
+        "tk_pp_get_single": (I, [P, I, P]),
+        "tk_pp_update": (I, [P, I, P]),
+        "tk_last_error": (C.c_char_p, [P]),
+        "tk_destroy": (V, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -124,7 +134,9 @@ EXPORTED = ["cppp_default_opts", "cppp_workspace_bytes", "cp_init", "cp_load_ten
             "pp_get_single", "pp_update", "pp_error", "als_sweep", "als_run", "cp_set_phase_override", "fitness",
             "cppp_kernel_stats", "cppp_reset_kernel_stats", "cppp_generate",
             "cppp_nccl_unique_id", "cppp_plan_describe", "cp_destroy", "cp_last_error",
-            "cppp_status_string", "cppp_version", "cppp_launch_count"]
+            "cppp_status_string", "cppp_version", "cppp_launch_count",
+            "tk_init", "tk_set_factors", "tk_update_factors", "tk_ttmc", "tk_pp_build",
+            "tk_pp_get_operator", "tk_pp_get_single", "tk_pp_update", "tk_last_error", "tk_destroy"]
 
 
 # ------------------------------------------------------------------ marshalling helpers
@@ -371,3 +383,85 @@ def cppp_launch_count() -> int:
 
 def cppp_version() -> str:
     return lib().cppp_version().decode()
+
+
+# ------------------------------------------------------------------ PP-Tucker (cppp_tucker.h)
+class TkCtx:
+    """Handle returned by tk_init (include/cppp_tucker.h)."""
+
+    def __init__(self, N, s, R):
+        self.h = C.c_void_p()
+        self.N, self.s, self.R = N, list(s), list(R)
+        self.keep = []
+
+    def canon_shape(self, kept):
+        return tuple(self.s[m] if m in kept else self.R[m] for m in range(self.N))
+
+    def __del__(self):
+        try:
+            tk_destroy(self)
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+def _tk_check(ctx, status: int):
+    if status != 0:
+        msg = lib().tk_last_error(ctx.h if ctx is not None else None)
+        raise CpppError(status, (msg or b"").decode() or lib().cppp_status_string(status).decode())
+
+
+def tk_init(X, s: Sequence[int], R: Sequence[int], *, stream=None, flags: int = 0) -> TkCtx:
+    """tk_init: X numpy (host) or torch CUDA tensor; ranks R[n] <= s[n]."""
+    N = len(s)
+    ctx = TkCtx(N, s, R)
+    dims = (C.c_int64 * N)(*s)
+    ranks = (C.c_int * N)(*R)
+    st = C.c_void_p(stream.cuda_stream) if stream is not None else None
+    if flags & FLAG_BORROW_TENSOR:
+        ctx.keep.append(X)
+    _tk_check(None, lib().tk_init(C.byref(ctx.h), _ptr(X), N, dims, ranks, st, flags))
+    return ctx
+
+
+def tk_set_factors(ctx: TkCtx, A) -> None:
+    _tk_check(ctx, lib().tk_set_factors(ctx.h, _ptrs([np.ascontiguousarray(a) if isinstance(a, np.ndarray) else a for a in A])))
+
+
+def tk_update_factors(ctx: TkCtx, A) -> None:
+    _tk_check(ctx, lib().tk_update_factors(ctx.h, _ptrs([np.ascontiguousarray(a) if isinstance(a, np.ndarray) else a for a in A])))
+
+
+def tk_ttmc(ctx: TkCtx):
+    """All N TTMcs Y^(n), canonical layout (numpy)."""
+    out = [np.empty(ctx.canon_shape({n})) for n in range(ctx.N)]
+    _tk_check(ctx, lib().tk_ttmc(ctx.h, _ptrs(out)))
+    return out
+
+
+def tk_pp_build(ctx: TkCtx) -> None:
+    _tk_check(ctx, lib().tk_pp_build(ctx.h))
+
+
+def tk_pp_get_operator(ctx: TkCtx, i: int, j: int) -> np.ndarray:
+    out = np.empty(ctx.canon_shape({i, j}))
+    _tk_check(ctx, lib().tk_pp_get_operator(ctx.h, i, j, _ptr(out)))
+    return out
+
+
+def tk_pp_get_single(ctx: TkCtx, n: int) -> np.ndarray:
+    out = np.empty(ctx.canon_shape({n}))
+    _tk_check(ctx, lib().tk_pp_get_single(ctx.h, n, _ptr(out)))
+    return out
+
+
+def tk_pp_update(ctx: TkCtx, n: int) -> np.ndarray:
+    out = np.empty(ctx.canon_shape({n}))
+    _tk_check(ctx, lib().tk_pp_update(ctx.h, n, _ptr(out)))
+    return out
+
+
+def tk_destroy(ctx: TkCtx) -> None:
+    if ctx is not None and ctx.h:
+        lib().tk_destroy(ctx.h)
+        ctx.h = C.c_void_p()
+        ctx.keep.clear()

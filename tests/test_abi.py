@@ -1,4 +1,4 @@
-"""C-ABI checks that need no GPU: the library loads, exports every symbol include/cppp.h
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/*.h
 declares, host-only helpers work, and device calls fail loudly (no CPU fallback)."""
 import os
 import re
@@ -12,7 +12,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def declared_functions():
-    src = open(os.path.join(ROOT, "include", "cppp.h")).read()
+    inc = os.path.join(ROOT, "include")
+    src = "\n".join(open(os.path.join(inc, f)).read() for f in sorted(os.listdir(inc)) if f.endswith(".h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     names = re.findall(r"^[ \t]*(?:const[ \t]+)?[a-z_0-9]+(?:[ \t]+|[ \t]*\*[ \t]*)([a-z_0-9]+)[ \t]*\(",
                        src, flags=re.M)

@@ -1,0 +1,87 @@
+"""GPU parity of the PP-Tucker contraction path (include/cppp_tucker.h) against
+oracle/tucker_oracle.py on identical seeded inputs: TTMc Y^(n) through the dimension tree, the
+Def. 3.2 operators Y_p^(i,j) through the construction tree, Y_p^(n), and the PP update
+Y~^(n) — relative Frobenius 1e-11 (the CP path's kernel tolerance; every result is a chain of
+FP64 GEMMs)."""
+import numpy as np
+import pytest
+
+import oracle.tucker_oracle as T
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1811_10573_b200.cppp as cp  # noqa: E402
+
+TOL = 1e-11
+SHAPES = [((40, 36, 34), (10, 8, 6)),           # DMMA path (even extents)
+          ((7, 9, 5), (3, 2, 4)),               # odd extents: SIMT path
+          ((20, 18, 16, 14), (4, 4, 3, 3)),
+          ((6, 5, 4, 6, 5), (2, 3, 2, 2, 3)),
+          ((12, 12, 12, 12, 12, 12), (3, 3, 3, 3, 3, 3))]   # the paper's N = 6 shape, reduced
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def problem(dims, ranks, seed):
+    r = np.random.default_rng(seed)
+    X = r.standard_normal(dims)
+    A = [np.linalg.qr(r.standard_normal((s, R)))[0].copy() for s, R in zip(dims, ranks)]
+    return X, A
+
+
+@pytest.mark.parametrize("dims,ranks", SHAPES)
+@pytest.mark.parametrize("simt", [False, True])
+def test_ttmc_matches_oracle(dims, ranks, simt):
+    X, A = problem(dims, ranks, 1)
+    ctx = cp.tk_init(X, dims, ranks, flags=cp.FLAG_SIMT_TTM if simt else 0)
+    cp.tk_set_factors(ctx, A)
+    Y = cp.tk_ttmc(ctx)
+    for n in range(len(dims)):
+        assert rel(Y[n], T.ttmc(X, A, n)) < TOL, n
+    cp.tk_destroy(ctx)
+
+
+@pytest.mark.parametrize("dims,ranks", SHAPES)
+def test_pp_operators_and_update_match_oracle(dims, ranks):
+    X, Ap = problem(dims, ranks, 2)
+    N = len(dims)
+    ctx = cp.tk_init(X, dims, ranks)
+    cp.tk_set_factors(ctx, Ap)
+    cp.tk_pp_build(ctx)
+    ops = T.pp_operators(X, Ap)
+    for (i, j), ref in ops.items():
+        assert rel(cp.tk_pp_get_operator(ctx, i, j), ref) < TOL, (i, j)
+    Yp = [T.pp_single(ops, Ap, n, N) for n in range(N)]
+    for n in range(N):
+        assert rel(cp.tk_pp_get_single(ctx, n), Yp[n]) < TOL, n
+    r = np.random.default_rng(3)
+    dA = [0.01 * r.standard_normal(a.shape) for a in Ap]
+    cp.tk_update_factors(ctx, [a + d for a, d in zip(Ap, dA)])
+    for n in range(N):
+        assert rel(cp.tk_pp_update(ctx, n), T.pp_update(Yp[n], ops, dA, n)) < TOL, n
+    cp.tk_destroy(ctx)
+
+
+def test_tucker_errors_and_device_tensor():
+    X, A = problem((8, 6, 4), (2, 3, 2), 4)
+    with pytest.raises(cp.CpppError):
+        cp.tk_init(X, (8, 6, 4), (9, 3, 2))          # R_0 > s_0
+    ctx = cp.tk_init(X, (8, 6, 4), (2, 3, 2))
+    with pytest.raises(cp.CpppError):
+        cp.tk_ttmc(ctx)                              # before tk_set_factors
+    cp.tk_set_factors(ctx, A)
+    with pytest.raises(cp.CpppError):
+        cp.tk_pp_update(ctx, 0)                      # before tk_pp_build
+    cp.tk_destroy(ctx)
+    Xd = torch.from_numpy(X).cuda()
+    ctx = cp.tk_init(Xd, (8, 6, 4), (2, 3, 2), flags=cp.FLAG_BORROW_TENSOR)
+    cp.tk_set_factors(ctx, A)
+    Y = cp.tk_ttmc(ctx)
+    assert rel(Y[1], T.ttmc(X, A, 1)) < TOL
+    cp.tk_destroy(ctx)
