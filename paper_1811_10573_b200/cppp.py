@@ -50,6 +50,17 @@ class Opts(C.Structure):
                 ("host_allreduce", HOST_ALLREDUCE), ("host_allreduce_user", C.c_void_p)]
 
 
+class TkSweepInfo(C.Structure):
+    _fields_ = [("sweep", C.c_int), ("phase", C.c_int), ("next_phase", C.c_int), ("converged", C.c_int),
+                ("core_change", C.c_double), ("core_norm", C.c_double), ("residual", C.c_double),
+                ("max_rel_dA", C.c_double)]
+
+    def as_dict(self):
+        return dict(sweep=self.sweep, phase=PHASE_NAMES[self.phase], next_phase=PHASE_NAMES[self.next_phase],
+                    converged=bool(self.converged), core_change=self.core_change, core_norm=self.core_norm,
+                    residual=self.residual, max_rel_dA=self.max_rel_dA)
+
+
 class SweepInfo(C.Structure):
     _fields_ = [("sweep", C.c_int), ("phase", C.c_int), ("fitness", C.c_double),
                 ("residual_sq", C.c_double), ("grad_norm_sum", C.c_double),
@@ -117,6 +128,11 @@ def lib():
         "tk_pp_get_operator": (I, [P, I, I, P]),
         "tk_pp_get_single": (I, [P, I, P]),
         "tk_pp_update": (I, [P, I, P]),
+        "tk_hosvd": (I, [P]),
+        "tk_sweep": (I, [P, D, D, C.POINTER(TkSweepInfo)]),
+        "tk_set_phase_override": (I, [P, I]),
+        "tk_get_factors": (I, [P, C.POINTER(P)]),
+        "tk_get_core": (I, [P, P]),
         "tk_last_error": (C.c_char_p, [P]),
         "tk_destroy": (V, [P]),
     }
@@ -136,7 +152,8 @@ EXPORTED = ["cppp_default_opts", "cppp_workspace_bytes", "cp_init", "cp_load_ten
             "cppp_nccl_unique_id", "cppp_plan_describe", "cp_destroy", "cp_last_error",
             "cppp_status_string", "cppp_version", "cppp_launch_count",
             "tk_init", "tk_set_factors", "tk_update_factors", "tk_ttmc", "tk_pp_build",
-            "tk_pp_get_operator", "tk_pp_get_single", "tk_pp_update", "tk_last_error", "tk_destroy"]
+            "tk_pp_get_operator", "tk_pp_get_single", "tk_pp_update", "tk_hosvd", "tk_sweep",
+            "tk_set_phase_override", "tk_get_factors", "tk_get_core", "tk_last_error", "tk_destroy"]
 
 
 # ------------------------------------------------------------------ marshalling helpers
@@ -457,6 +474,34 @@ def tk_pp_get_single(ctx: TkCtx, n: int) -> np.ndarray:
 def tk_pp_update(ctx: TkCtx, n: int) -> np.ndarray:
     out = np.empty(ctx.canon_shape({n}))
     _tk_check(ctx, lib().tk_pp_update(ctx.h, n, _ptr(out)))
+    return out
+
+
+def tk_hosvd(ctx: TkCtx) -> None:
+    _tk_check(ctx, lib().tk_hosvd(ctx.h))
+
+
+def tk_sweep(ctx: TkCtx, eps: float, eps_pp: float) -> dict:
+    info = TkSweepInfo()
+    _tk_check(ctx, lib().tk_sweep(ctx.h, eps, eps_pp, C.byref(info)))
+    return info.as_dict()
+
+
+def tk_set_phase_override(ctx: TkCtx, phase) -> None:
+    if isinstance(phase, str):
+        phase = PHASE_BY_NAME[phase]
+    _tk_check(ctx, lib().tk_set_phase_override(ctx.h, phase))
+
+
+def tk_get_factors(ctx: TkCtx):
+    out = [np.empty((ctx.s[n], ctx.R[n])) for n in range(ctx.N)]
+    _tk_check(ctx, lib().tk_get_factors(ctx.h, _ptrs(out)))
+    return out
+
+
+def tk_get_core(ctx: TkCtx) -> np.ndarray:
+    out = np.empty(tuple(ctx.R))
+    _tk_check(ctx, lib().tk_get_core(ctx.h, _ptr(out)))
     return out
 
 

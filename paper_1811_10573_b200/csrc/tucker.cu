@@ -54,6 +54,231 @@ __global__ void permute_kernel(const double* __restrict__ in, double* __restrict
   }
 }
 
+// ---------------------------------------------------------------- HOOI factor update kernels
+// (A^(n) = the R_n leading left singular vectors of Y_(n), from a Gram matrix)
+constexpr int EIG_MAX = 128;      // Gram matrices up to 128 x 128 (one CTA, shared memory)
+constexpr int EIG_THREADS = 512;
+
+__device__ double tk_warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ double tk_block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = tk_warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = lane < nw ? sh[lane] : 0.0;
+    r = tk_warp_sum(r);
+    if (lane == 0) sh[0] = r;
+  }
+  __syncthreads();
+  r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// Y viewed [P][S][Q] (mode n's unfolding Y_(n) has rows y and columns (p, q)).
+//   rows = true : W[a][b] = Σ_{p,q} Y[p][a][q] Y[p][b][q]        (S x S,  Y_(n) Y_(n)^T)
+//   rows = false: W[i][j] = Σ_y Y[p_i][y][q_i] Y[p_j][y][q_j]     (PQ x PQ, Y_(n)^T Y_(n))
+// one thread per upper-triangle entry, sums in a fixed order, mirrored
+__global__ void tk_gram_kernel(const double* __restrict__ Y, int64_t P, int64_t S, int64_t Q,
+                               bool rows, double* __restrict__ W) {
+  const int64_t n = rows ? S : P * Q;
+  const int64_t tot = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = e / n, b = e - a * n;
+    if (b < a) continue;
+    double acc = 0.0;
+    if (rows) {
+      for (int64_t p = 0; p < P; ++p) {
+        const double* ya = Y + (p * S + a) * Q;
+        const double* yb = Y + (p * S + b) * Q;
+        for (int64_t q = 0; q < Q; ++q) acc = fma(ya[q], yb[q], acc);
+      }
+    } else {
+      const int64_t pa = a / Q, qa = a - pa * Q, pb = b / Q, qb = b - pb * Q;
+      for (int64_t y = 0; y < S; ++y) acc = fma(Y[(pa * S + y) * Q + qa], Y[(pb * S + y) * Q + qb], acc);
+    }
+    W[a * n + b] = acc;
+    W[b * n + a] = acc;
+  }
+}
+
+// Symmetric eigendecomposition of W (n x n, n <= 128): two-sided cyclic Jacobi with the
+// Brent-Luk parallel ordering until the off-diagonal mass is below 1e-30 of the diagonal's
+// (accuracy ~ machine precision relative to ||W||).  lam = diag, V = accumulated rotations.
+__global__ void __launch_bounds__(EIG_THREADS, 1)
+    tk_eig_kernel(const double* __restrict__ Win, int n, double* __restrict__ V, double* __restrict__ lam) {
+  extern __shared__ double Wm[];   // n x (n + 1)
+  __shared__ double sh[32];
+  __shared__ double cs[64], sn[64];
+  __shared__ int pp_[64], qq_[64];
+  const int tid = threadIdx.x, nt = blockDim.x, P = n + 1, nn = n * n;
+  for (int e = tid; e < nn; e += nt) {
+    const int i = e / n, j = e - i * n;
+    Wm[i * P + j] = Win[e];
+    V[e] = i == j ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int ne = (n + 1) & ~1;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, dia = 0.0;
+    for (int e = tid; e < nn; e += nt) {
+      const int i = e / n, j = e - i * n;
+      const double v = Wm[i * P + j];
+      if (i == j) dia += v * v;
+      else off += v * v;
+    }
+    off = tk_block_sum(off, sh);
+    dia = tk_block_sum(dia, sh);
+    if (off <= 1e-30 * dia || dia == 0.0) break;
+    for (int r = 0; r < ne - 1; ++r) {
+      if (tid < ne / 2) {
+        int p = tid == 0 ? ne - 1 : (r + tid) % (ne - 1);
+        int q = tid == 0 ? r : (r - tid + ne - 1) % (ne - 1);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        double c = 1.0, sv = 0.0;
+        if (q < n) {
+          const double apq = Wm[p * P + q];
+          if (apq != 0.0) {
+            const double tau = (Wm[q * P + q] - Wm[p * P + p]) / (2.0 * apq);
+            const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            sv = t * c;
+          }
+        }
+        cs[tid] = c;
+        sn[tid] = sv;
+        pp_[tid] = p;
+        qq_[tid] = q;
+      }
+      __syncthreads();
+      for (int e = tid; e < (ne / 2) * n; e += nt) {   // rows: W <- J^T W
+        const int pr = e / n, l = e - pr * n;
+        const int p = pp_[pr], q = qq_[pr];
+        if (q >= n) continue;
+        const double c = cs[pr], sv = sn[pr];
+        const double wp = Wm[p * P + l], wq = Wm[q * P + l];
+        Wm[p * P + l] = c * wp - sv * wq;
+        Wm[q * P + l] = sv * wp + c * wq;
+      }
+      __syncthreads();
+      for (int e = tid; e < (ne / 2) * n; e += nt) {   // columns: W <- W J, V <- V J
+        const int pr = e / n, l = e - pr * n;
+        const int p = pp_[pr], q = qq_[pr];
+        if (q >= n) continue;
+        const double c = cs[pr], sv = sn[pr];
+        const double wp = Wm[l * P + p], wq = Wm[l * P + q];
+        Wm[l * P + p] = c * wp - sv * wq;
+        Wm[l * P + q] = sv * wp + c * wq;
+        const double vp = V[l * n + p], vq = V[l * n + q];
+        V[l * n + p] = c * vp - sv * vq;
+        V[l * n + q] = sv * vp + c * vq;
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < n; i += nt) lam[i] = Wm[i * P + i];
+}
+
+// A (S x R) = the R leading eigenvectors (eigenvalue descending, lower index first on a tie):
+// rows = true: columns of V; rows = false: Y_(n) v / sqrt(λ) (the left singular vector from the
+// right one).  Then each column's sign makes its largest-magnitude entry (first on a tie)
+// positive (reading T2).  One CTA.
+__global__ void __launch_bounds__(EIG_THREADS, 1)
+    tk_select_kernel(const double* __restrict__ V, const double* __restrict__ lam, int n, int R,
+                     const double* __restrict__ Y, int64_t P, int64_t S, int64_t Q, bool rows,
+                     double* __restrict__ A) {
+  __shared__ int idx[EIG_MAX];
+  __shared__ double sgn[EIG_MAX];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) {
+    bool used[EIG_MAX];
+    for (int i = 0; i < n; ++i) used[i] = false;
+    for (int j = 0; j < R; ++j) {
+      int best = -1;
+      for (int i = 0; i < n; ++i)
+        if (!used[i] && (best < 0 || lam[i] > lam[best])) best = i;
+      used[best] = true;
+      idx[j] = best;
+    }
+  }
+  __syncthreads();
+  for (int64_t e = tid; e < S * R; e += nt) {
+    const int64_t y = e / R;
+    const int j = static_cast<int>(e - y * R);
+    double v;
+    if (rows) {
+      v = V[y * n + idx[j]];
+    } else {
+      double acc = 0.0;
+      for (int64_t pq = 0; pq < P * Q; ++pq) {
+        const int64_t p = pq / Q, q = pq - p * Q;
+        acc = fma(Y[(p * S + y) * Q + q], V[pq * n + idx[j]], acc);
+      }
+      v = acc / sqrt(lam[idx[j]]);
+    }
+    A[e] = v;
+  }
+  __syncthreads();
+  const int w = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (int j = w; j < R; j += nw) {
+    double best = -1.0, val = 0.0;
+    int64_t bi = -1;
+    for (int64_t y = lane; y < S; y += 32) {
+      const double a = A[y * R + j];
+      if (fabs(a) > best) {
+        best = fabs(a);
+        bi = y;
+        val = a;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const double ov = __shfl_xor_sync(0xffffffffu, val, o);
+      if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) {
+        best = ob;
+        bi = oi;
+        val = ov;
+      }
+    }
+    if (lane == 0) sgn[j] = val < 0.0 ? -1.0 : 1.0;
+  }
+  __syncthreads();
+  for (int64_t e = tid; e < S * R; e += nt) A[e] *= sgn[e % R];
+}
+
+// out[0] = Σ (a - b)², out[1] = Σ a², out[2] = Σ b²  (one CTA, fixed order)
+__global__ void tk_sumsq_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                int64_t n, double* __restrict__ out) {
+  __shared__ double sh[32];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+    const double x = a[e], y = b ? b[e] : 0.0, d = x - y;
+    s0 = fma(d, d, s0);
+    s1 = fma(x, x, s1);
+    s2 = fma(y, y, s2);
+  }
+  s0 = tk_block_sum(s0, sh);
+  s1 = tk_block_sum(s1, sh);
+  s2 = tk_block_sum(s2, sh);
+  if (threadIdx.x == 0) {
+    out[0] = s0;
+    out[1] = s1;
+    out[2] = s2;
+  }
+}
+
 bool dev_ptr(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -84,6 +309,18 @@ struct tk_ctx {
   double* Fpad = nullptr;                              // TTM scratch (padded factor, scheduler)
   double* out = nullptr;                               // canonical result scratch (max Y^(n))
   bool factors_set = false, ops_valid = false;
+  // HOOI driver (tk_hosvd / tk_sweep)
+  double* W = nullptr;      // Gram matrix (<= 128 x 128)
+  double* V = nullptr;      // its eigenvectors
+  double* lam = nullptr;    // its eigenvalues
+  double* G = nullptr;      // core (canonical R_0 x .. x R_{N-1})
+  double* Gp = nullptr;     // previous core
+  double* Aold = nullptr;   // scratch: the factor before its update (regular sweeps)
+  double* stats = nullptr;  // device: per mode (Σ dA², Σ A², -), core (Σ F², Σ G², -), ||X||²
+  double* hstats = nullptr; // pinned host copy
+  double normX_sq = 0.0;
+  int next_phase = CPPP_PHASE_DT, override_phase = CPPP_PHASE_AUTO, sweeps = 0;
+  bool in_sweep = false;    // TDT leaves update factors
   std::string err;
   std::vector<void*> owned;
 };
@@ -213,8 +450,13 @@ cppp_status copy_out(tk_ctx* c, double* dst, const double* src, int64_t n) {
   return CPPP_OK;
 }
 
+cppp_status factor_update(tk_ctx* c, int n, const double* Yc, bool pp);
+cppp_status core_update(tk_ctx* c, const double* Yc);
+
 // Binary dimension tree: node keeps modes [lo, hi]; the left half is reached by
-// contracting the right half's modes and vice versa; a leaf is Y^(lo).
+// contracting the right half's modes and vice versa; a leaf is Y^(lo).  Inside a regular sweep
+// (c->in_sweep) each leaf updates A^(lo) before the tree moves on, so the right half contracts
+// the left half's new factors (Gauss-Seidel order of Alg. 2).
 struct TDT {
   tk_ctx* c;
   double* const* Y;
@@ -222,6 +464,10 @@ struct TDT {
   cppp_status leaf(const double* d, const Lay& l, int n) {
     TKST(to_canonical(c, d, l, c->out, false));
     if (Y && Y[n]) TKST(copy_out(c, Y[n], c->out, canon_elems(c, 1u << n)));
+    if (c->in_sweep) {
+      TKST(factor_update(c, n, c->out, false));
+      if (n == c->N - 1) TKST(core_update(c, c->out));
+    }
     return CPPP_OK;
   }
 
@@ -311,6 +557,89 @@ cppp_status load_factors(tk_ctx* c, const double* const* A) {
   return CPPP_OK;
 }
 
+// Y (canonical, mode n kept) viewed [P][s_n][Q]
+void unfold_dims(const tk_ctx* c, int n, int64_t* P, int64_t* Q, bool x_everywhere = false) {
+  *P = 1;
+  *Q = 1;
+  for (int m = 0; m < n; ++m) *P *= x_everywhere ? c->s[m] : c->R[m];
+  for (int m = n + 1; m < c->N; ++m) *Q *= x_everywhere ? c->s[m] : c->R[m];
+}
+
+// A^(n) <- the R_n leading left singular vectors of Y_(n) from the smaller Gram
+// matrix; dA^(n) = A_new - A_old (regular) or A_new - A_p (PP); per-mode norms into stats.
+cppp_status leading_vectors(tk_ctx* c, int n, const double* Y, int64_t P, int64_t Q) {
+  const int64_t S = c->s[n];
+  bool rows;
+  if (S <= cppp::EIG_MAX) rows = true;
+  else if (P * Q <= cppp::EIG_MAX) rows = false;
+  else return tfail(c, CPPP_EINVAL, "mode %d: Gram of %lld x %lld exceeds %d", n, (long long)S,
+                    (long long)(P * Q), cppp::EIG_MAX);
+  const int ne = static_cast<int>(rows ? S : P * Q);
+  static bool attr = false;
+  if (!attr) {
+    TKCU(c, cudaFuncSetAttribute(cppp::tk_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 cppp::EIG_MAX * (cppp::EIG_MAX + 1) * 8));
+    attr = true;
+  }
+  const int64_t tot = (int64_t)ne * ne;
+  const int64_t blocks = std::min<int64_t>((tot + 255) / 256, 148 * 8);
+  cppp::tk_gram_kernel<<<(unsigned)blocks, 256, 0, c->st>>>(Y, P, S, Q, rows, c->W);
+  cppp::tk_eig_kernel<<<1, cppp::EIG_THREADS, (size_t)ne * (ne + 1) * 8, c->st>>>(c->W, ne, c->V, c->lam);
+  cppp::tk_select_kernel<<<1, cppp::EIG_THREADS, 0, c->st>>>(c->V, c->lam, ne, c->R[n], Y, P, S, Q,
+                                                            rows, c->A[n]);
+  cppp::note_launches(3);
+  TKCU(c, cudaGetLastError());
+  return CPPP_OK;
+}
+
+cppp_status factor_update(tk_ctx* c, int n, const double* Yc, bool pp) {
+  const int64_t na = c->s[n] * c->R[n];
+  if (!pp) TKCU(c, cudaMemcpyAsync(c->Aold, c->A[n], sizeof(double) * na, cudaMemcpyDeviceToDevice, c->st));
+  int64_t P, Q;
+  unfold_dims(c, n, &P, &Q);
+  TKST(leading_vectors(c, n, Yc, P, Q));
+  TKCU(c, cppp::launch_sub(c->A[n], pp ? c->Ap[n] : c->Aold, c->dA[n], na, c->st));
+  cppp::tk_sumsq_kernel<<<1, 256, 0, c->st>>>(c->dA[n], c->A[n], na, c->stats + 3 * n);
+  cppp::note_launch();
+  TKCU(c, cudaGetLastError());
+  return CPPP_OK;
+}
+
+// G_new = Y^(N-1) ×_{N-1} A^(N-1)T (reading T1), ||G_new - G||², ||G_new||², then G <- G_new
+cppp_status core_update(tk_ctx* c, const double* Yc) {
+  const int N = c->N;
+  Lay nl;
+  TKST(contract(c, Yc, canon_lay(c, 1u << (N - 1)), N - 1, c->A[N - 1], c->G, &nl));
+  const int64_t ng = canon_elems(c, 0u);
+  cppp::tk_sumsq_kernel<<<1, 256, 0, c->st>>>(c->G, c->Gp, ng, c->stats + 3 * N);
+  cppp::note_launch();
+  TKCU(c, cudaGetLastError());
+  TKCU(c, cudaMemcpyAsync(c->Gp, c->G, sizeof(double) * ng, cudaMemcpyDeviceToDevice, c->st));
+  return CPPP_OK;
+}
+
+// G = X ×_0 A^(0)T ⋯ ×_{N-1} A^(N-1)T (contracted in ascending order: canonical) into Gp
+cppp_status full_core(tk_ctx* c) {
+  const double* cur = c->X;
+  Lay cl = root_lay(c);
+  for (int u = 0; u < c->N; ++u) {
+    double* o = nullptr;
+    TKST(talloc(c, &o, lay_elems(c, cl) / c->s[u] * c->R[u]));
+    Lay nl;
+    TKST(contract(c, cur, cl, u, c->A[u], o, &nl));
+    if (cur != c->X) TKST(tfree(c, const_cast<double*>(cur)));
+    cur = o;
+    cl = nl;
+  }
+  TKCU(c, cudaMemcpyAsync(c->Gp, cur, sizeof(double) * canon_elems(c, 0u), cudaMemcpyDeviceToDevice, c->st));
+  TKCU(c, cudaMemcpyAsync(c->G, cur, sizeof(double) * canon_elems(c, 0u), cudaMemcpyDeviceToDevice, c->st));
+  TKST(tfree(c, const_cast<double*>(cur)));
+  return CPPP_OK;
+}
+
+cppp_status pp_build_ops(tk_ctx* c);
+cppp_status pp_approx(tk_ctx* c, int n, double* out);
+
 }  // namespace
 
 extern "C" {
@@ -364,6 +693,21 @@ cppp_status tk_init(tk_ctx** out, const double* X, int N, const int64_t* s, cons
         return bail(CPPP_ENOMEM);
   }
   if (dalloc(c, &c->out, ymax) != CPPP_OK) return bail(CPPP_ENOMEM);
+  int64_t amax = 1;
+  for (int n = 0; n < N; ++n) amax = std::max<int64_t>(amax, s[n] * R[n]);
+  if (dalloc(c, &c->W, cppp::EIG_MAX * cppp::EIG_MAX) != CPPP_OK ||
+      dalloc(c, &c->V, cppp::EIG_MAX * cppp::EIG_MAX) != CPPP_OK ||
+      dalloc(c, &c->lam, cppp::EIG_MAX) != CPPP_OK || dalloc(c, &c->G, canon_elems(c, 0u)) != CPPP_OK ||
+      dalloc(c, &c->Gp, canon_elems(c, 0u)) != CPPP_OK || dalloc(c, &c->Aold, amax) != CPPP_OK ||
+      dalloc(c, &c->stats, 3 * N + 3) != CPPP_OK)
+    return bail(CPPP_ENOMEM);
+  if (cudaMallocHost(&c->hstats, sizeof(double) * (3 * N + 3)) != cudaSuccess) return bail(CPPP_ENOMEM);
+  cppp::tk_sumsq_kernel<<<1, 1024, 0, c->st>>>(c->X, nullptr, numel, c->stats);
+  cppp::note_launch();
+  if (cudaMemcpyAsync(c->hstats, c->stats, sizeof(double) * 3, cudaMemcpyDeviceToHost, c->st) != cudaSuccess ||
+      cudaStreamSynchronize(c->st) != cudaSuccess)
+    return bail(CPPP_ECUDA);
+  c->normX_sq = c->hstats[1];
   const size_t nscr = cppp::ttm_scratch_doubles(smax);
   if (dalloc(c, &c->Fpad, (int64_t)nscr) != CPPP_OK) return bail(CPPP_ENOMEM);
   if (cudaMemsetAsync(c->Fpad, 0, sizeof(double) * nscr, c->st) != cudaSuccess ||
@@ -376,8 +720,12 @@ cppp_status tk_init(tk_ctx** out, const double* X, int N, const int64_t* s, cons
 cppp_status tk_set_factors(tk_ctx* c, const double* const* A) {
   if (!c) return CPPP_EINVAL;
   TKST(load_factors(c, A));
+  TKST(full_core(c));
+  TKCU(c, cudaStreamSynchronize(c->st));
   c->factors_set = true;
   c->ops_valid = false;
+  c->next_phase = CPPP_PHASE_DT;
+  c->sweeps = 0;
   return CPPP_OK;
 }
 
@@ -399,30 +747,8 @@ cppp_status tk_ttmc(tk_ctx* c, double* const* Y) {
 cppp_status tk_pp_build(tk_ctx* c) {
   if (!c) return CPPP_EINVAL;
   if (!c->factors_set) return tfail(c, CPPP_ESTATE, "tk_pp_build before tk_set_factors");
-  const int N = c->N;
-  for (int n = 0; n < N; ++n) {
-    TKCU(c, cudaMemcpyAsync(c->Ap[n], c->A[n], sizeof(double) * c->s[n] * c->R[n],
-                            cudaMemcpyDeviceToDevice, c->st));
-    TKCU(c, cudaMemsetAsync(c->dA[n], 0, sizeof(double) * c->s[n] * c->R[n], c->st));
-  }
-  TTree t{c, {}};
-  for (int n = 0; n < N; ++n) t.tau[n] = n;
-  std::stable_sort(t.tau, t.tau + N, [&](int a, int b) { return c->s[a] > c->s[b]; });
-  TKST(t.visit(c->X, root_lay(c), 0u, 0));
-  // Y_p^(n) = Y_p^(j,n) ×_j A_p^(j)T, j = min{j != n}
-  for (int n = 0; n < N; ++n) {
-    const int j = n == 0 ? 1 : 0;
-    const int a = std::min(j, n), b = std::max(j, n);
-    const Lay l = canon_lay(c, (1u << a) | (1u << b));
-    double* o = nullptr;
-    TKST(talloc(c, &o, canon_elems(c, 1u << n)));
-    Lay nl;
-    TKST(contract(c, c->ops[a][b], l, j, c->Ap[j], o, &nl));
-    TKST(to_canonical(c, o, nl, c->Yp[n], false));
-    TKST(tfree(c, o));
-  }
+  TKST(pp_build_ops(c));
   TKCU(c, cudaStreamSynchronize(c->st));
-  c->ops_valid = true;
   return CPPP_OK;
 }
 
@@ -446,22 +772,10 @@ cppp_status tk_pp_update(tk_ctx* c, int n, double* Y_tilde) {
   if (!c) return CPPP_EINVAL;
   if (n < 0 || n >= c->N) return tfail(c, CPPP_EINVAL, "mode %d out of range", n);
   if (!c->ops_valid) return tfail(c, CPPP_ESTATE, "tk_pp_update before tk_pp_build");
-  const int N = c->N;
-  for (int i = 0; i < N; ++i)
+  for (int i = 0; i < c->N; ++i)
     TKCU(c, cppp::launch_sub(c->A[i], c->Ap[i], c->dA[i], c->s[i] * c->R[i], c->st));
-  const int64_t ne = canon_elems(c, 1u << n);
-  TKCU(c, cudaMemcpyAsync(c->out, c->Yp[n], sizeof(double) * ne, cudaMemcpyDeviceToDevice, c->st));
-  double* o = nullptr;
-  TKST(talloc(c, &o, ne));
-  for (int i = 0; i < N; ++i) {
-    if (i == n) continue;
-    const int a = std::min(i, n), b = std::max(i, n);
-    Lay nl;
-    TKST(contract(c, c->ops[a][b], canon_lay(c, (1u << a) | (1u << b)), i, c->dA[i], o, &nl));
-    TKST(to_canonical(c, o, nl, c->out, true));
-  }
-  TKST(tfree(c, o));
-  if (Y_tilde) TKST(copy_out(c, Y_tilde, c->out, ne));
+  TKST(pp_approx(c, n, c->out));
+  if (Y_tilde) TKST(copy_out(c, Y_tilde, c->out, canon_elems(c, 1u << n)));
   TKCU(c, cudaStreamSynchronize(c->st));
   return CPPP_OK;
 }
@@ -472,7 +786,152 @@ void tk_destroy(tk_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->st);
   for (void* p : c->owned) cudaFree(p);
+  if (c->hstats) cudaFreeHost(c->hstats);
   delete c;
+}
+
+}  // extern "C"
+
+namespace {
+
+// A_p := A, dA := 0, operators via the construction tree, Y_p^(n)
+cppp_status pp_build_ops(tk_ctx* c) {
+  const int N = c->N;
+  for (int n = 0; n < N; ++n) {
+    TKCU(c, cudaMemcpyAsync(c->Ap[n], c->A[n], sizeof(double) * c->s[n] * c->R[n],
+                            cudaMemcpyDeviceToDevice, c->st));
+    TKCU(c, cudaMemsetAsync(c->dA[n], 0, sizeof(double) * c->s[n] * c->R[n], c->st));
+  }
+  TTree t{c, {}};
+  for (int n = 0; n < N; ++n) t.tau[n] = n;
+  std::stable_sort(t.tau, t.tau + N, [&](int a, int b) { return c->s[a] > c->s[b]; });
+  TKST(t.visit(c->X, root_lay(c), 0u, 0));
+  // Y_p^(n) = Y_p^(j,n) ×_j A_p^(j)T, j = min{j != n}
+  for (int n = 0; n < N; ++n) {
+    const int j = n == 0 ? 1 : 0;
+    const int a = std::min(j, n), b = std::max(j, n);
+    double* o = nullptr;
+    TKST(talloc(c, &o, canon_elems(c, 1u << n)));
+    Lay nl;
+    TKST(contract(c, c->ops[a][b], canon_lay(c, (1u << a) | (1u << b)), j, c->Ap[j], o, &nl));
+    TKST(to_canonical(c, o, nl, c->Yp[n], false));
+    TKST(tfree(c, o));
+  }
+  c->ops_valid = true;
+  return CPPP_OK;
+}
+
+// out = Y~^(n) = Y_p^(n) + Σ_{i≠n} Y_p^(i,n) ×_i dA^(i)T (canonical; dA already formed)
+cppp_status pp_approx(tk_ctx* c, int n, double* out) {
+  const int N = c->N;
+  const int64_t ne = canon_elems(c, 1u << n);
+  TKCU(c, cudaMemcpyAsync(out, c->Yp[n], sizeof(double) * ne, cudaMemcpyDeviceToDevice, c->st));
+  double* o = nullptr;
+  TKST(talloc(c, &o, ne));
+  for (int i = 0; i < N; ++i) {
+    if (i == n) continue;
+    const int a = std::min(i, n), b = std::max(i, n);
+    Lay nl;
+    TKST(contract(c, c->ops[a][b], canon_lay(c, (1u << a) | (1u << b)), i, c->dA[i], o, &nl));
+    TKST(to_canonical(c, o, nl, out, true));
+  }
+  TKST(tfree(c, o));
+  return CPPP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+cppp_status tk_hosvd(tk_ctx* c) {
+  if (!c) return CPPP_EINVAL;
+  for (int n = 0; n < c->N; ++n) {
+    if (c->s[n] > cppp::EIG_MAX)
+      return tfail(c, CPPP_EINVAL, "tk_hosvd: s_%d = %lld > %d (set the factors instead)", n,
+                   (long long)c->s[n], cppp::EIG_MAX);
+    int64_t P, Q;
+    unfold_dims(c, n, &P, &Q, true);
+    TKST(leading_vectors(c, n, c->X, P, Q));
+  }
+  TKST(full_core(c));
+  TKCU(c, cudaStreamSynchronize(c->st));
+  c->factors_set = true;
+  c->ops_valid = false;
+  c->next_phase = CPPP_PHASE_DT;
+  c->sweeps = 0;
+  return CPPP_OK;
+}
+
+cppp_status tk_set_phase_override(tk_ctx* c, int phase) {
+  if (!c) return CPPP_EINVAL;
+  if (phase < CPPP_PHASE_AUTO || phase > CPPP_PHASE_PP) return tfail(c, CPPP_EINVAL, "bad phase %d", phase);
+  c->override_phase = phase;
+  return CPPP_OK;
+}
+
+cppp_status tk_sweep(tk_ctx* c, double eps, double eps_pp, tk_sweep_info* info) {
+  if (!c) return CPPP_EINVAL;
+  if (!c->factors_set) return tfail(c, CPPP_ESTATE, "tk_sweep before tk_set_factors / tk_hosvd");
+  if (!(eps_pp >= 0.0)) return tfail(c, CPPP_EINVAL, "eps_pp must be >= 0");
+  const int N = c->N;
+  const int phase = c->override_phase != CPPP_PHASE_AUTO ? c->override_phase : c->next_phase;
+  if (phase == CPPP_PHASE_PP && !c->ops_valid)
+    return tfail(c, CPPP_ESTATE, "PP sweep requested without operators");
+  if (phase == CPPP_PHASE_DT) {
+    c->in_sweep = true;
+    TDT t{c, nullptr};
+    cppp_status st = t.range(c->X, root_lay(c), 0, N - 1);
+    c->in_sweep = false;
+    TKST(st);
+  } else {
+    if (phase == CPPP_PHASE_PP_BUILD) TKST(pp_build_ops(c));
+    for (int n = 0; n < N; ++n) {
+      TKST(pp_approx(c, n, c->out));
+      TKST(factor_update(c, n, c->out, true));
+      if (n == N - 1) TKST(core_update(c, c->out));
+    }
+  }
+  TKCU(c, cudaMemcpyAsync(c->hstats, c->stats, sizeof(double) * (3 * N + 3), cudaMemcpyDeviceToHost, c->st));
+  TKCU(c, cudaStreamSynchronize(c->st));
+  const double* h = c->hstats;
+  double maxrel = 0.0;
+  for (int n = 0; n < N; ++n) {
+    const double d = h[3 * n + 1], a = h[3 * n + 2];
+    maxrel = std::max(maxrel, a > 0.0 ? std::sqrt(d) / std::sqrt(a) : (d > 0.0 ? INFINITY : 0.0));
+  }
+  const double F = std::sqrt(h[3 * N]), g2 = h[3 * N + 1];
+  const bool small = maxrel < eps_pp;
+  c->next_phase = phase == CPPP_PHASE_DT ? (small ? CPPP_PHASE_PP_BUILD : CPPP_PHASE_DT)
+                                         : (small ? CPPP_PHASE_PP : CPPP_PHASE_DT);
+  c->sweeps++;
+  if (info) {
+    info->sweep = c->sweeps;
+    info->phase = phase;
+    info->next_phase = c->next_phase;
+    info->core_change = F;
+    info->core_norm = std::sqrt(g2);
+    info->residual = std::sqrt(std::max(0.0, c->normX_sq - g2)) / std::sqrt(c->normX_sq);
+    info->max_rel_dA = maxrel;
+    info->converged = F <= eps;
+  }
+  return CPPP_OK;
+}
+
+cppp_status tk_get_factors(tk_ctx* c, double* const* A) {
+  if (!c) return CPPP_EINVAL;
+  if (!A) return tfail(c, CPPP_EINVAL, "null output list");
+  for (int n = 0; n < c->N; ++n)
+    if (A[n]) TKST(copy_out(c, A[n], c->A[n], c->s[n] * c->R[n]));
+  TKCU(c, cudaStreamSynchronize(c->st));
+  return CPPP_OK;
+}
+
+cppp_status tk_get_core(tk_ctx* c, double* G) {
+  if (!c) return CPPP_EINVAL;
+  if (!G) return tfail(c, CPPP_EINVAL, "null output");
+  TKST(copy_out(c, G, c->Gp, canon_elems(c, 0u)));
+  TKCU(c, cudaStreamSynchronize(c->st));
+  return CPPP_OK;
 }
 
 }  // extern "C"

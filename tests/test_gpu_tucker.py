@@ -85,3 +85,61 @@ def test_tucker_errors_and_device_tensor():
     Y = cp.tk_ttmc(ctx)
     assert rel(Y[1], T.ttmc(X, A, 1)) < TOL
     cp.tk_destroy(ctx)
+
+
+# ---------------------------------------------------------------- the HOOI / PP-Tucker driver
+def tucker_tensor(dims, ranks, seed, noise):
+    r = np.random.default_rng(seed)
+    X = r.standard_normal(ranks)
+    for m, (s, R) in enumerate(zip(dims, ranks)):
+        a = np.linalg.qr(r.standard_normal((s, R)))[0]
+        X = np.moveaxis(np.tensordot(X, a, axes=([m], [1])), -1, m)
+    Z = r.standard_normal(dims)
+    return X + noise * np.linalg.norm(X) / np.linalg.norm(Z) * Z
+
+
+def check_trace(ctx, X, tr, A_ref):
+    for t in tr:
+        cp.tk_set_phase_override(ctx, t["phase"])
+        g = cp.tk_sweep(ctx, 0.0, 0.2)
+        assert g["phase"] == t["phase"]
+        assert abs(g["core_norm"] - t["core_norm"]) <= 1e-10 * t["core_norm"], (g, t)
+        assert abs(g["core_change"] - t["core_change"]) <= 1e-8 * t["core_norm"], (g, t)
+        assert abs(g["residual"] - t["residual"]) <= 1e-8, (g, t)
+        assert abs(g["max_rel_dA"] - t["max_rel_dA"]) <= 1e-8, (g, t)
+    A = cp.tk_get_factors(ctx)
+    for a, b in zip(A, A_ref):
+        assert np.linalg.norm(a - b) <= 1e-8 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("dims,ranks", [((40, 36, 34), (5, 4, 3)), ((20, 18, 16, 14), (3, 3, 2, 2))])
+def test_hosvd_and_pp_tucker_trace_match_oracle(dims, ranks):
+    """tk_hosvd = oracle HOSVD (factors, core); then 12 sweeps of Alg. 4 (ε_pp = 0.2, the oracle's
+    phase schedule replayed) match per sweep: core norm, core change, residual, max ||dA||/||A||;
+    final factors within 1e-8 (eigenvectors of well-separated Gram spectra)."""
+    X = tucker_tensor(dims, ranks, 5, 0.1)
+    G0, A0 = T.hosvd(X, ranks)
+    ctx = cp.tk_init(X, dims, ranks)
+    cp.tk_hosvd(ctx)
+    for a, b in zip(cp.tk_get_factors(ctx), A0):
+        assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)
+    assert rel(cp.tk_get_core(ctx), G0) < 1e-10
+    st, tr = T.pp_tucker_als(X, ranks, 0.0, 0.2, 12)
+    assert any(t["phase"] != "dt" for t in tr)
+    check_trace(ctx, X, tr, st.A)
+    cp.tk_destroy(ctx)
+
+
+def test_pp_tucker_large_mode_uses_the_rank_side_gram():
+    """s_0 = 200 > 128: the factor update takes the Gram of Y_(n)^T (R^(N-1) = 20 <= 128) and maps
+    the eigenvectors back (Y v / sqrt(λ)); factors given (the oracle's HOSVD)."""
+    dims, ranks = (200, 40, 36), (5, 5, 4)
+    X = tucker_tensor(dims, ranks, 6, 0.1)
+    _, A0 = T.hosvd(X, ranks)
+    ctx = cp.tk_init(X, dims, ranks)
+    with pytest.raises(cp.CpppError):
+        cp.tk_hosvd(ctx)
+    cp.tk_set_factors(ctx, A0)
+    st, tr = T.pp_tucker_als(X, ranks, 0.0, 0.2, 8, A0=A0)
+    check_trace(ctx, X, tr, st.A)
+    cp.tk_destroy(ctx)
