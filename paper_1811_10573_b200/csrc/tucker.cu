@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -109,24 +110,108 @@ __global__ void tk_gram_kernel(const double* __restrict__ Y, int64_t P, int64_t 
   }
 }
 
+// rows = true for large reductions (HOSVD: Y = X, P*Q = s^(N-1)): CTA c sums the (p, q) range
+// [c0, c1) for every entry of W (S <= 128) into part[c]; batches of 16 (p, q) columns of Y_(n)
+// are staged in shared memory; tk_gram_combine adds the parts in CTA order.
+constexpr int GB = 16;
+__global__ void __launch_bounds__(256)
+    tk_gram_rows_partial(const double* __restrict__ Y, int64_t P, int S, int64_t Q, int64_t per,
+                         double* __restrict__ part) {
+  __shared__ double v[GB][EIG_MAX + 1];
+  const int64_t L = P * Q;
+  const int64_t c0 = blockIdx.x * per, c1 = c0 + per < L ? c0 + per : L;
+  const int ne = S * S;
+  double acc[EIG_MAX * EIG_MAX / 256];
+  constexpr int KMAX = EIG_MAX * EIG_MAX / 256;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) acc[k] = 0.0;
+  for (int64_t c = c0; c < c1; c += GB) {
+    const int nb = static_cast<int>(c1 - c < GB ? c1 - c : GB);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb * S; e += blockDim.x) {
+      int j, a;
+      if (Q > 1) {   // consecutive q are contiguous: j fastest
+        a = e / nb;
+        j = e - a * nb;
+      } else {       // Q == 1: consecutive a are contiguous
+        j = e / S;
+        a = e - j * S;
+      }
+      const int64_t pq = c + j, p = pq / Q, q = pq - p * Q;
+      v[j][a] = Y[(p * S + a) * Q + q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      const int e = threadIdx.x + 256 * k;
+      if (e >= ne) break;
+      const int a = e / S, b = e - a * S;
+      double t = acc[k];
+      for (int j = 0; j < nb; ++j) t = fma(v[j][a], v[j][b], t);
+      acc[k] = t;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const int e = threadIdx.x + 256 * k;
+    if (e < ne) part[blockIdx.x * (int64_t)ne + e] = acc[k];
+  }
+}
+__global__ void tk_gram_combine(const double* __restrict__ part, int nparts, int ne, double* __restrict__ W) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (int c = 0; c < nparts; ++c) t += part[(int64_t)c * ne + e];
+    W[e] = t;
+  }
+}
+
 // Symmetric eigendecomposition of W (n x n, n <= 128): two-sided cyclic Jacobi with the
-// Brent-Luk parallel ordering until the off-diagonal mass is below 1e-30 of the diagonal's
-// (accuracy ~ machine precision relative to ||W||).  lam = diag, V = accumulated rotations.
+// Brent-Luk parallel ordering; a rotation is skipped when |w_pq| <= 1e-15 ||diag W||_2 (the
+// rounding level of a two-sided sweep, which leaves absolute errors ~eps ||W||) and the sweeps
+// end when one applies none.  lam = diag, V (global, n x n) = accumulated rotations.  V is kept in shared
+// memory beside W when both fit (vsm, n <= 118), else updated in place in global memory.
+// warm: V holds this mode's previous eigenvectors; the sweeps start from V^T W V (diagonal up to
+// the change of W since then), so they converge in a few passes.  T: n x n global scratch.
 __global__ void __launch_bounds__(EIG_THREADS, 1)
-    tk_eig_kernel(const double* __restrict__ Win, int n, double* __restrict__ V, double* __restrict__ lam) {
-  extern __shared__ double Wm[];   // n x (n + 1)
+    tk_eig_kernel(const double* __restrict__ Win, int n, double* __restrict__ V, double* __restrict__ T,
+                  int warm, int vsm, double* __restrict__ lam, int debug) {
+  extern __shared__ double smem[];
   __shared__ double sh[32];
   __shared__ double cs[64], sn[64];
   __shared__ int pp_[64], qq_[64];
+  __shared__ int rotated;
   const int tid = threadIdx.x, nt = blockDim.x, P = n + 1, nn = n * n;
+  double* Wm = smem;                        // n x (n + 1)
+  double* Vw = vsm ? smem + n * P : V;      // rotations accumulate here
+  const int Pv = vsm ? P : n;
   for (int e = tid; e < nn; e += nt) {
     const int i = e / n, j = e - i * n;
     Wm[i * P + j] = Win[e];
-    V[e] = i == j ? 1.0 : 0.0;
+    Vw[i * Pv + j] = warm ? V[e] : (i == j ? 1.0 : 0.0);
   }
   __syncthreads();
+  if (warm) {
+    for (int e = tid; e < nn; e += nt) {   // T = W V
+      const int i = e / n, j = e - i * n;
+      double t = 0.0;
+      for (int l = 0; l < n; ++l) t = fma(Wm[i * P + l], Vw[l * Pv + j], t);
+      T[e] = t;
+    }
+    __syncthreads();
+    for (int e = tid; e < nn; e += nt) {   // W' = V^T T (upper triangle, mirrored: exact symmetry)
+      const int i = e / n, j = e - i * n;
+      if (j < i) continue;
+      double t = 0.0;
+      for (int l = 0; l < n; ++l) t = fma(Vw[l * Pv + i], T[l * n + j], t);
+      Wm[i * P + j] = t;
+      Wm[j * P + i] = t;
+    }
+    __syncthreads();
+  }
   const int ne = (n + 1) & ~1;
-  for (int sweep = 0; sweep < 60; ++sweep) {
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    if (tid == 0) rotated = 0;
     double off = 0.0, dia = 0.0;
     for (int e = tid; e < nn; e += nt) {
       const int i = e / n, j = e - i * n;
@@ -136,7 +221,8 @@ __global__ void __launch_bounds__(EIG_THREADS, 1)
     }
     off = tk_block_sum(off, sh);
     dia = tk_block_sum(dia, sh);
-    if (off <= 1e-30 * dia || dia == 0.0) break;
+    if (off == 0.0 || dia == 0.0) break;
+    const double floor_pq = 1e-15 * sqrt(dia);
     for (int r = 0; r < ne - 1; ++r) {
       if (tid < ne / 2) {
         int p = tid == 0 ? ne - 1 : (r + tid) % (ne - 1);
@@ -149,7 +235,8 @@ __global__ void __launch_bounds__(EIG_THREADS, 1)
         double c = 1.0, sv = 0.0;
         if (q < n) {
           const double apq = Wm[p * P + q];
-          if (apq != 0.0) {
+          if (fabs(apq) > floor_pq) {
+            rotated = 1;
             const double tau = (Wm[q * P + q] - Wm[p * P + p]) / (2.0 * apq);
             const double t = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + t * t);
@@ -162,32 +249,46 @@ __global__ void __launch_bounds__(EIG_THREADS, 1)
         qq_[tid] = q;
       }
       __syncthreads();
-      for (int e = tid; e < (ne / 2) * n; e += nt) {   // rows: W <- J^T W
-        const int pr = e / n, l = e - pr * n;
+      const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
+      for (int pr = warp; pr < ne / 2; pr += nwarp) {   // rows: W <- J^T W (warp per pair)
         const int p = pp_[pr], q = qq_[pr];
-        if (q >= n) continue;
-        const double c = cs[pr], sv = sn[pr];
-        const double wp = Wm[p * P + l], wq = Wm[q * P + l];
-        Wm[p * P + l] = c * wp - sv * wq;
-        Wm[q * P + l] = sv * wp + c * wq;
+        const double sv = sn[pr];
+        if (q >= n || sv == 0.0) continue;
+        const double c = cs[pr];
+        for (int l = lane; l < n; l += 32) {
+          const double wp = Wm[p * P + l], wq = Wm[q * P + l];
+          Wm[p * P + l] = c * wp - sv * wq;
+          Wm[q * P + l] = sv * wp + c * wq;
+        }
       }
       __syncthreads();
-      for (int e = tid; e < (ne / 2) * n; e += nt) {   // columns: W <- W J, V <- V J
-        const int pr = e / n, l = e - pr * n;
+      for (int pr = warp; pr < ne / 2; pr += nwarp) {   // columns: W <- W J, V <- V J
         const int p = pp_[pr], q = qq_[pr];
-        if (q >= n) continue;
-        const double c = cs[pr], sv = sn[pr];
-        const double wp = Wm[l * P + p], wq = Wm[l * P + q];
-        Wm[l * P + p] = c * wp - sv * wq;
-        Wm[l * P + q] = sv * wp + c * wq;
-        const double vp = V[l * n + p], vq = V[l * n + q];
-        V[l * n + p] = c * vp - sv * vq;
-        V[l * n + q] = sv * vp + c * vq;
+        const double sv = sn[pr];
+        if (q >= n || sv == 0.0) continue;
+        const double c = cs[pr];
+        for (int l = lane; l < n; l += 32) {
+          const double wp = Wm[l * P + p], wq = Wm[l * P + q];
+          Wm[l * P + p] = c * wp - sv * wq;
+          Wm[l * P + q] = sv * wp + c * wq;
+          const double vp = Vw[l * Pv + p], vq = Vw[l * Pv + q];
+          Vw[l * Pv + p] = c * vp - sv * vq;
+          Vw[l * Pv + q] = sv * vp + c * vq;
+        }
       }
       __syncthreads();
     }
+    const bool any = rotated != 0;
+    __syncthreads();   // everyone has read the flag before thread 0 clears it
+    if (!any) break;
   }
+  if (debug && tid == 0) printf("tk_eig n %d warm %d sweeps %d\n", n, warm, sweep);
   for (int i = tid; i < n; i += nt) lam[i] = Wm[i * P + i];
+  if (vsm)
+    for (int e = tid; e < nn; e += nt) {
+      const int i = e / n, j = e - i * n;
+      V[e] = Vw[i * Pv + j];
+    }
 }
 
 // A (S x R) = the R leading eigenvectors (eigenvalue descending, lower index first on a tie):
@@ -311,7 +412,9 @@ struct tk_ctx {
   bool factors_set = false, ops_valid = false;
   // HOOI driver (tk_hosvd / tk_sweep)
   double* W = nullptr;      // Gram matrix (<= 128 x 128)
-  double* V = nullptr;      // its eigenvectors
+  double* V = nullptr;      // scratch (n x n)
+  double* Vm[CPPP_MAX_ORDER] = {};   // per mode: eigenvectors of the last update (warm start)
+  bool vm_valid[CPPP_MAX_ORDER] = {};
   double* lam = nullptr;    // its eigenvalues
   double* G = nullptr;      // core (canonical R_0 x .. x R_{N-1})
   double* Gp = nullptr;     // previous core
@@ -567,7 +670,13 @@ void unfold_dims(const tk_ctx* c, int n, int64_t* P, int64_t* Q, bool x_everywhe
 
 // A^(n) <- the R_n leading left singular vectors of Y_(n) from the smaller Gram
 // matrix; dA^(n) = A_new - A_old (regular) or A_new - A_p (PP); per-mode norms into stats.
-cppp_status leading_vectors(tk_ctx* c, int n, const double* Y, int64_t P, int64_t Q) {
+bool tk_debug() {
+  static const bool d = getenv("CPPP_DEBUG_TK") != nullptr;
+  return d;
+}
+
+// warm: start the eigensolver from this mode's previous eigenvectors (Vm[n])
+cppp_status leading_vectors(tk_ctx* c, int n, const double* Y, int64_t P, int64_t Q, bool warm) {
   const int64_t S = c->s[n];
   bool rows;
   if (S <= cppp::EIG_MAX) rows = true;
@@ -578,16 +687,34 @@ cppp_status leading_vectors(tk_ctx* c, int n, const double* Y, int64_t P, int64_
   static bool attr = false;
   if (!attr) {
     TKCU(c, cudaFuncSetAttribute(cppp::tk_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 cppp::EIG_MAX * (cppp::EIG_MAX + 1) * 8));
+                                 220 * 1024));
     attr = true;
   }
   const int64_t tot = (int64_t)ne * ne;
-  const int64_t blocks = std::min<int64_t>((tot + 255) / 256, 148 * 8);
-  cppp::tk_gram_kernel<<<(unsigned)blocks, 256, 0, c->st>>>(Y, P, S, Q, rows, c->W);
-  cppp::tk_eig_kernel<<<1, cppp::EIG_THREADS, (size_t)ne * (ne + 1) * 8, c->st>>>(c->W, ne, c->V, c->lam);
-  cppp::tk_select_kernel<<<1, cppp::EIG_THREADS, 0, c->st>>>(c->V, c->lam, ne, c->R[n], Y, P, S, Q,
+  if (rows && P * Q > 4096) {   // long reduction: split it over CTAs, combine in order
+    const int64_t L = P * Q;
+    int64_t nparts = std::min<int64_t>(296, (L + 4095) / 4096);
+    const int64_t per = (L + nparts - 1) / nparts;
+    nparts = (L + per - 1) / per;
+    double* part = nullptr;
+    TKST(talloc(c, &part, nparts * tot));
+    cppp::tk_gram_rows_partial<<<(unsigned)nparts, 256, 0, c->st>>>(Y, P, (int)S, Q, per, part);
+    cppp::tk_gram_combine<<<(unsigned)((tot + 255) / 256), 256, 0, c->st>>>(part, (int)nparts, (int)tot, c->W);
+    cppp::note_launches(2);
+    TKST(tfree(c, part));
+  } else {
+    const int64_t blocks = std::min<int64_t>((tot + 255) / 256, 148 * 8);
+    cppp::tk_gram_kernel<<<(unsigned)blocks, 256, 0, c->st>>>(Y, P, S, Q, rows, c->W);
+    cppp::note_launch();
+  }
+  double* Vn = c->Vm[n];
+  const size_t wbytes = (size_t)ne * (ne + 1) * 8;
+  const bool vsm = 2 * wbytes <= 220 * 1024;
+  cppp::tk_eig_kernel<<<1, cppp::EIG_THREADS, vsm ? 2 * wbytes : wbytes, c->st>>>(
+      c->W, ne, Vn, c->V, warm ? 1 : 0, vsm ? 1 : 0, c->lam, tk_debug() ? 1 : 0);
+  cppp::tk_select_kernel<<<1, cppp::EIG_THREADS, 0, c->st>>>(Vn, c->lam, ne, c->R[n], Y, P, S, Q,
                                                             rows, c->A[n]);
-  cppp::note_launches(3);
+  cppp::note_launches(2);
   TKCU(c, cudaGetLastError());
   return CPPP_OK;
 }
@@ -597,7 +724,8 @@ cppp_status factor_update(tk_ctx* c, int n, const double* Yc, bool pp) {
   if (!pp) TKCU(c, cudaMemcpyAsync(c->Aold, c->A[n], sizeof(double) * na, cudaMemcpyDeviceToDevice, c->st));
   int64_t P, Q;
   unfold_dims(c, n, &P, &Q);
-  TKST(leading_vectors(c, n, Yc, P, Q));
+  TKST(leading_vectors(c, n, Yc, P, Q, c->vm_valid[n]));
+  c->vm_valid[n] = true;
   TKCU(c, cppp::launch_sub(c->A[n], pp ? c->Ap[n] : c->Aold, c->dA[n], na, c->st));
   cppp::tk_sumsq_kernel<<<1, 256, 0, c->st>>>(c->dA[n], c->A[n], na, c->stats + 3 * n);
   cppp::note_launch();
@@ -654,6 +782,15 @@ cppp_status tk_init(tk_ctx** out, const double* X, int N, const int64_t* s, cons
     cudaGetLastError();
     return CPPP_ENODEV;
   }
+  {   // tree intermediates come from the stream-ordered pool: keep freed blocks cached across
+      // synchronizations instead of returning them to the driver after every sweep
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   tk_ctx* c = new tk_ctx;
   c->N = N;
   c->flags = flags;
@@ -701,6 +838,8 @@ cppp_status tk_init(tk_ctx** out, const double* X, int N, const int64_t* s, cons
       dalloc(c, &c->Gp, canon_elems(c, 0u)) != CPPP_OK || dalloc(c, &c->Aold, amax) != CPPP_OK ||
       dalloc(c, &c->stats, 3 * N + 3) != CPPP_OK)
     return bail(CPPP_ENOMEM);
+  for (int n = 0; n < N; ++n)
+    if (dalloc(c, &c->Vm[n], cppp::EIG_MAX * cppp::EIG_MAX) != CPPP_OK) return bail(CPPP_ENOMEM);
   if (cudaMallocHost(&c->hstats, sizeof(double) * (3 * N + 3)) != cudaSuccess) return bail(CPPP_ENOMEM);
   cppp::tk_sumsq_kernel<<<1, 1024, 0, c->st>>>(c->X, nullptr, numel, c->stats);
   cppp::note_launch();
@@ -720,6 +859,7 @@ cppp_status tk_init(tk_ctx** out, const double* X, int N, const int64_t* s, cons
 cppp_status tk_set_factors(tk_ctx* c, const double* const* A) {
   if (!c) return CPPP_EINVAL;
   TKST(load_factors(c, A));
+  for (int n = 0; n < c->N; ++n) c->vm_valid[n] = false;
   TKST(full_core(c));
   TKCU(c, cudaStreamSynchronize(c->st));
   c->factors_set = true;
@@ -851,7 +991,8 @@ cppp_status tk_hosvd(tk_ctx* c) {
                    (long long)c->s[n], cppp::EIG_MAX);
     int64_t P, Q;
     unfold_dims(c, n, &P, &Q, true);
-    TKST(leading_vectors(c, n, c->X, P, Q));
+    TKST(leading_vectors(c, n, c->X, P, Q, false));
+    c->vm_valid[n] = false;   // X's Gram basis: not a useful start for Y^(n)
   }
   TKST(full_core(c));
   TKCU(c, cudaStreamSynchronize(c->st));
