@@ -422,3 +422,46 @@ def test_order3_operator_reuse_is_bit_identical(name):
     assert [r["phase"] for r in ra] == [t["phase"] for t in tr]
     cp.cp_destroy(a)
     cp.cp_destroy(b)
+
+
+@pytest.mark.parametrize("dims,K", [((6, 5, 7), 1),                      # rank 1
+                                    ((2, 3, 2, 2, 3, 2, 2, 3), 3),       # maximum order N = 8
+                                    ((5, 1, 4), 2), ((1, 6, 1, 5), 2)])  # unit extents
+def test_edge_shapes(dims, K):
+    """Degenerate and extreme shapes: MTTKRP, every PP operator and update, and 6 replayed sweeps
+    against the oracle."""
+    X, A = random_problem(dims, K, 11)
+    A = [np.abs(a) + 0.1 for a in A]
+    N = len(dims)
+    ctx = cp.cp_init(X, N, dims, K)
+    cp.cp_set_factors(ctx, A)
+    M = cp.mttkrp_dt(ctx)
+    for n in range(N):
+        assert rel(M[n], O.mttkrp(X, A, n)) < TOL, n
+    cp.pp_build_operators(ctx)
+    ops = O.pp_operators(X, A)
+    for (i, j), ref in ops.items():
+        assert rel(cp.pp_get_operator(ctx, i, j), ref) < TOL, (i, j)
+    r = np.random.default_rng(2)
+    dA = [0.01 * r.standard_normal(a.shape) for a in A]
+    cp.cp_update_factors(ctx, [a + d for a, d in zip(A, dA)])
+    Mp = [O.pp_single(ops, A, n, N) for n in range(N)]
+    for n in range(N):
+        assert rel(cp.pp_update(ctx, n), O.pp_update(Mp[n], ops, dA, n)) < TOL, n
+    _, tr = O.pp_cp_als(X, A, 0.0, 0.1, 6)
+    cp.cp_set_factors(ctx, A)
+    for t in tr:
+        cp.cp_set_phase_override(ctx, t["phase"])
+        info = cp.als_sweep(ctx, 0.0, 0.1)
+        if 1.0 - t["fitness"] >= 1e-6:
+            assert abs(info["fitness"] - t["fitness"]) < 1e-8, (t, info)
+    cp.cp_destroy(ctx)
+
+
+def test_empty_and_oversized_inputs_rejected():
+    X = np.zeros((4, 0, 3))
+    with pytest.raises(cp.CpppError):
+        cp.cp_init(X, 3, (4, 0, 3), 2)
+    X = np.zeros((2,) * 9)
+    with pytest.raises(cp.CpppError):
+        cp.cp_init(X, 9, (2,) * 9, 2)
