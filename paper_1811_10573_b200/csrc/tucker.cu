@@ -14,6 +14,8 @@
 // most), so the permutation costs one pass over them.
 #include <cuda_runtime.h>
 
+#include <cfloat>
+
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
@@ -59,6 +61,7 @@ __global__ void permute_kernel(const double* __restrict__ in, double* __restrict
 // (A^(n) = the R_n leading left singular vectors of Y_(n), from a Gram matrix)
 constexpr int EIG_MAX = 128;      // Gram matrices up to 128 x 128 (one CTA, shared memory)
 constexpr int EIG_THREADS = 512;
+constexpr int EIG_IB = 12;        // inverse-iteration vectors per batch (shared-memory work arrays)
 
 __device__ double tk_warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -291,18 +294,263 @@ __global__ void __launch_bounds__(EIG_THREADS, 1)
     }
 }
 
+// The R largest eigenpairs of a symmetric W (n x n, n <= 128) the LAPACK way, one CTA:
+//   1. Householder tridiagonalization T = Q^T W Q (dsytd2-style, lower; reflector k stored in
+//      column k below the subdiagonal, beta_k beside it),
+//   2. the R largest eigenvalues of T by bisection on the Sturm count (thread per eigenvalue,
+//      to the last bit of the bracket),
+//   3. their eigenvectors of T by inverse iteration (thread per vector: tridiagonal LU with
+//      partial pivoting, 3 solves), then modified Gram-Schmidt inside clusters of close
+//      eigenvalues (gap < 1e-3 ||T||, LAPACK's dstein rule),
+//   4. back-transformation u = H_0 H_1 .. H_{n-3} y (warp per vector).
+// Output: V column j (j < R) = eigenvector of the j-th largest eigenvalue lam[j]; lam[j >= R] =
+// -inf (so tk_select_kernel keeps columns 0..R-1 in order).  S5: 6 x 128 x R doubles of scratch.
+constexpr int TOPR_THREADS = 512;   // 1024 measured no faster (barrier-latency bound) and spills
+__global__ void __launch_bounds__(TOPR_THREADS, 1)
+    tk_eig_topr_kernel(const double* __restrict__ Win, int n, int R, double* __restrict__ V,
+                       double* __restrict__ lam, double* __restrict__ S5, int debug) {
+  extern __shared__ double A[];              // n x (n + 1): W, then the reflectors
+  long long t_[5];
+  t_[0] = clock64();
+  __shared__ double d[EIG_MAX], e[EIG_MAX], beta[EIG_MAX], pv[EIG_MAX], ev[EIG_MAX];
+  __shared__ double sh[32];
+  const int tid = threadIdx.x, nt = blockDim.x, P = n + 1;
+  for (int x = tid; x < n * n; x += nt) A[(x / n) * P + (x % n)] = Win[x];
+  __syncthreads();
+  // ---- 1. tridiagonalization, three barriers per column: warp 0 forms the reflector; all warps
+  //         form p = b A22 v (warp per row); every warp re-derives K = b/2 p.v itself and the
+  //         rank-2 update uses w = p - K v inline
+  __shared__ double bk;
+  const int wq = tid >> 5, lq = tid & 31, nwq = nt >> 5;
+  for (int k = 0; k + 2 < n; ++k) {
+    if (wq == 0) {
+      double t = 0.0;
+      for (int i = k + 2 + lq; i < n; i += 32) t = fma(A[i * P + k], A[i * P + k], t);
+      const double xn2 = tk_warp_sum(t);
+      const double a0 = A[(k + 1) * P + k];
+      double bb = 0.0, alpha = a0;
+      if (xn2 > 0.0) {
+        const double nrm = sqrt(a0 * a0 + xn2);
+        alpha = a0 >= 0.0 ? -nrm : nrm;
+        const double v0 = a0 - alpha;
+        bb = 2.0 / (v0 * v0 + xn2);
+        __syncwarp();
+        if (lq == 0) A[(k + 1) * P + k] = v0;   // v = (v0, x_2..) in column k
+      }
+      if (lq == 0) {
+        d[k] = A[k * P + k];
+        e[k] = alpha;
+        beta[k] = bb;
+        bk = bb;
+      }
+    }
+    __syncthreads();
+    const double b = bk;
+    if (b == 0.0) continue;   // uniform: nothing to reflect
+    for (int i = k + 1 + wq; i < n; i += nwq) {   // p = b A22 v
+      double s2 = 0.0;
+      for (int j = k + 1 + lq; j < n; j += 32) s2 = fma(A[i * P + j], A[j * P + k], s2);
+      s2 = tk_warp_sum(s2);
+      if (lq == 0) pv[i] = b * s2;
+    }
+    __syncthreads();
+    double pt = 0.0;
+    for (int i = k + 1 + lq; i < n; i += 32) pt = fma(pv[i], A[i * P + k], pt);
+    const double K = 0.5 * b * tk_warp_sum(pt);
+    for (int i = k + 1 + wq; i < n; i += nwq) {   // A22 -= v w^T + w v^T, w = p - K v
+      const double vi = A[i * P + k], wi = pv[i] - K * vi;
+      for (int j = k + 1 + lq; j < n; j += 32) {
+        const double vj = A[j * P + k];
+        A[i * P + j] -= vi * (pv[j] - K * vj) + wi * vj;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (n >= 2) {
+      d[n - 2] = A[(n - 2) * P + n - 2];
+      e[n - 2] = A[(n - 1) * P + n - 2];
+      beta[n - 2] = 0.0;
+    }
+    d[n - 1] = A[(n - 1) * P + n - 1];
+    e[n - 1] = 0.0;
+  }
+  __syncthreads();
+  t_[1] = clock64();
+  // ---- 2. multisection: warp per eigenvalue (the j-th largest = index n-1-j ascending); each
+  //         step the 32 lanes evaluate the Sturm count at 32 interior points of the bracket
+  double glo = 0.0, ghi = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+    glo = i == 0 ? d[i] - r : fmin(glo, d[i] - r);
+    ghi = i == 0 ? d[i] + r : fmax(ghi, d[i] + r);
+  }
+  const double tn = fmax(fabs(glo), fabs(ghi));
+  const double pivmin = fmax(tn * 1e-300, 1e-300);
+  for (int i = tid; i + 1 < n; i += nt) pv[i] = e[i] * e[i];   // p is free now: Sturm needs e^2
+  __syncthreads();
+  {
+    const int wp = tid >> 5, ln = tid & 31, nwp = nt >> 5;
+    for (int j = wp; j < R; j += nwp) {
+      const int t = n - 1 - j;
+      double lo = glo - 2.0 * DBL_EPSILON * tn - pivmin, hi = ghi + 2.0 * DBL_EPSILON * tn + pivmin;
+      for (int it = 0; it < 64; ++it) {
+        const double x = lo + (hi - lo) * (ln + 1) / 33.0;
+        int cnt = 0;
+        if (x > lo && x < hi) {
+          double q = d[0] - x;
+          if (fabs(q) < pivmin) q = -pivmin;
+          cnt += q < 0.0;
+          for (int i = 1; i < n; ++i) {
+            q = d[i] - x - pv[i - 1] / q;   // pv = e^2 here
+            if (fabs(q) < pivmin) q = -pivmin;
+            cnt += q < 0.0;
+          }
+        }
+        // lanes with count <= t keep the eigenvalue above their point: the last such point is lo
+        const bool below = (x > lo && x < hi) && cnt <= t;
+        const bool above = (x > lo && x < hi) && cnt > t;
+        const unsigned mb = __ballot_sync(0xffffffffu, below);
+        const unsigned ma = __ballot_sync(0xffffffffu, above);
+        if (mb == 0u && ma == 0u) break;   // no representable interior point left
+        const double nlo = mb ? __shfl_sync(0xffffffffu, x, 31 - __clz(mb)) : lo;
+        const double nhi = ma ? __shfl_sync(0xffffffffu, x, __ffs(ma) - 1) : hi;
+        lo = nlo;
+        hi = nhi;
+      }
+      if (ln == 0) ev[j] = 0.5 * (lo + hi);
+    }
+  }
+  __syncthreads();
+  t_[2] = clock64();
+  // ---- 3. inverse iteration, one thread (lane 0 of a warp) per vector, IB vectors at a time
+  //         with their work arrays in shared memory: (T - lam I) y = b, LU with partial pivoting
+  for (int j0 = 0; j0 < R; j0 += EIG_IB) {
+  const int jb = tid >> 5, jv = j0 + jb;
+  if ((tid & 31) == 0 && jb < EIG_IB && jv < R) {
+    const double lmb = ev[jv];
+    double* dd = A + n * P + jb * 6 * n;   // diag, sup1, sup2, sub multipliers, y, pivots
+    double* u1 = dd + n;
+    double* u2 = u1 + n;
+    double* ml = u2 + n;
+    double* y = ml + n;
+    double* pvt = y + n;
+    const double eps_piv = DBL_EPSILON * fmax(tn, 1e-300);
+    // factor: rows i, i+1 swap when |sub| > |diag|
+    for (int i = 0; i < n; ++i) {
+      dd[i] = d[i] - lmb;
+      u1[i] = i + 1 < n ? e[i] : 0.0;
+      u2[i] = 0.0;
+    }
+    for (int i = 0; i + 1 < n; ++i) {
+      const double sub = e[i];
+      if (fabs(dd[i]) >= fabs(sub)) {
+        pvt[i] = 0.0;
+        if (dd[i] == 0.0) dd[i] = eps_piv;
+        const double mlt = sub / dd[i];
+        ml[i] = mlt;
+        dd[i + 1] -= mlt * u1[i];
+      } else {   // swap rows i and i+1
+        pvt[i] = 1.0;
+        const double mlt = dd[i] / sub;
+        ml[i] = mlt;
+        const double a = dd[i + 1], bb = i + 2 < n ? u1[i + 1] : 0.0;
+        dd[i] = sub;
+        const double old_u1 = u1[i];
+        u1[i] = a;
+        u2[i] = bb;
+        dd[i + 1] = old_u1 - mlt * a;
+        if (i + 2 < n) u1[i + 1] = -mlt * bb;
+      }
+    }
+    if (dd[n - 1] == 0.0) dd[n - 1] = eps_piv;
+    for (int i = 0; i < n; ++i) y[i] = 1.0;
+    for (int iter = 0; iter < 3; ++iter) {
+      for (int i = 0; i + 1 < n; ++i) {   // apply L^-1 (with the row swaps)
+        if (pvt[i] != 0.0) {
+          const double t2 = y[i];
+          y[i] = y[i + 1];
+          y[i + 1] = t2 - ml[i] * y[i];
+        } else {
+          y[i + 1] -= ml[i] * y[i];
+        }
+      }
+      for (int i = n - 1; i >= 0; --i) {   // U^-1
+        double t2 = y[i];
+        if (i + 1 < n) t2 -= u1[i] * y[i + 1];
+        if (i + 2 < n) t2 -= u2[i] * y[i + 2];
+        double dv = dd[i];
+        if (fabs(dv) < eps_piv) dv = dv < 0.0 ? -eps_piv : eps_piv;
+        y[i] = t2 / dv;
+      }
+      double nr = 0.0;
+      for (int i = 0; i < n; ++i) nr = fma(y[i], y[i], nr);
+      nr = 1.0 / sqrt(nr);
+      for (int i = 0; i < n; ++i) y[i] *= nr;
+    }
+    double* yg = S5 + (int64_t)jv * 6 * EIG_MAX + 4 * EIG_MAX;
+    for (int i = 0; i < n; ++i) yg[i] = y[i];
+  }
+  __syncthreads();
+  }
+  // clusters: MGS against the earlier members (eigenvalues descending), warp 0, in order
+  if (tid < 32) {
+    const int ln = tid;
+    const double ortol = 1e-3 * tn;
+    int c0 = 0;
+    for (int j = 1; j < R; ++j) {
+      if (ev[j - 1] - ev[j] >= ortol) {
+        c0 = j;
+        continue;
+      }
+      double* yj = S5 + (int64_t)j * 6 * EIG_MAX + 4 * EIG_MAX;
+      for (int i = c0; i < j; ++i) {
+        const double* yi = S5 + (int64_t)i * 6 * EIG_MAX + 4 * EIG_MAX;
+        double dp = 0.0;
+        for (int x = ln; x < n; x += 32) dp = fma(yi[x], yj[x], dp);
+        dp = tk_warp_sum(dp);
+        for (int x = ln; x < n; x += 32) yj[x] -= dp * yi[x];
+        __syncwarp();
+      }
+      double nr = 0.0;
+      for (int x = ln; x < n; x += 32) nr = fma(yj[x], yj[x], nr);
+      nr = 1.0 / sqrt(tk_warp_sum(nr));
+      for (int x = ln; x < n; x += 32) yj[x] *= nr;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  t_[3] = clock64();
+  // ---- 4. back-transformation, warp per vector: u = H_0 .. H_{n-3} y
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (int j = warp; j < R; j += nw) {
+    double* u = S5 + (int64_t)j * 6 * EIG_MAX + 4 * EIG_MAX;
+    for (int k = n - 3; k >= 0; --k) {
+      if (beta[k] == 0.0) continue;
+      double dp = 0.0;
+      for (int i = k + 1 + lane; i < n; i += 32) dp = fma(A[i * P + k], u[i], dp);
+      dp = tk_warp_sum(dp);
+      const double f = beta[k] * dp;
+      for (int i = k + 1 + lane; i < n; i += 32) u[i] -= f * A[i * P + k];
+      __syncwarp();
+    }
+    for (int i = lane; i < n; i += 32) V[i * n + j] = u[i];
+  }
+  for (int j = tid; j < n; j += nt) lam[j] = j < R ? ev[j] : -INFINITY;
+  t_[4] = clock64();
+  if (debug && tid == 0)
+    printf("tk_eig_topr n %d R %d cycles: tridiag %lld bisect %lld invit %lld back %lld\n", n, R,
+           t_[1] - t_[0], t_[2] - t_[1], t_[3] - t_[2], t_[4] - t_[3]);
+}
+
 // A (S x R) = the R leading eigenvectors (eigenvalue descending, lower index first on a tie):
 // rows = true: columns of V; rows = false: Y_(n) v / sqrt(λ) (the left singular vector from the
-// right one).  Then each column's sign makes its largest-magnitude entry (first on a tie)
-// positive (reading T2).  One CTA.
-__global__ void __launch_bounds__(EIG_THREADS, 1)
-    tk_select_kernel(const double* __restrict__ V, const double* __restrict__ lam, int n, int R,
-                     const double* __restrict__ Y, int64_t P, int64_t S, int64_t Q, bool rows,
-                     double* __restrict__ A) {
+// right one).  Grid over the entries; every CTA repeats the (tiny) selection.
+__global__ void tk_select_kernel(const double* __restrict__ V, const double* __restrict__ lam, int n,
+                                 int R, const double* __restrict__ Y, int64_t P, int64_t S, int64_t Q,
+                                 bool rows, double* __restrict__ A) {
   __shared__ int idx[EIG_MAX];
-  __shared__ double sgn[EIG_MAX];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     bool used[EIG_MAX];
     for (int i = 0; i < n; ++i) used[i] = false;
     for (int j = 0; j < R; ++j) {
@@ -314,7 +562,8 @@ __global__ void __launch_bounds__(EIG_THREADS, 1)
     }
   }
   __syncthreads();
-  for (int64_t e = tid; e < S * R; e += nt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < S * R;
+       e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t y = e / R;
     const int j = static_cast<int>(e - y * R);
     double v;
@@ -330,7 +579,13 @@ __global__ void __launch_bounds__(EIG_THREADS, 1)
     }
     A[e] = v;
   }
-  __syncthreads();
+}
+
+// Sign rule (reading T2): each column's largest-magnitude entry (first on a tie) made positive.
+// One CTA, warp per column.
+__global__ void tk_sign_kernel(double* __restrict__ A, int64_t S, int R) {
+  __shared__ double sgn[EIG_MAX];
+  const int tid = threadIdx.x, nt = blockDim.x;
   const int w = tid >> 5, lane = tid & 31, nw = nt >> 5;
   for (int j = w; j < R; j += nw) {
     double best = -1.0, val = 0.0;
@@ -357,6 +612,45 @@ __global__ void __launch_bounds__(EIG_THREADS, 1)
   }
   __syncthreads();
   for (int64_t e = tid; e < S * R; e += nt) A[e] *= sgn[e % R];
+}
+
+// rows = false with a long reduction: W[a][b] = Σ_y Y[p_a][y][q_a] Y[p_b][y][q_b] over the y range
+// of CTA c (batches of 16 y staged in shared memory) into part[c]; combined in order.
+__global__ void __launch_bounds__(256)
+    tk_gram_cols_partial(const double* __restrict__ Y, int64_t Pd, int64_t S, int64_t Q, int64_t per,
+                         double* __restrict__ part) {
+  __shared__ double v[GB][EIG_MAX + 1];
+  const int n = static_cast<int>(Pd * Q);
+  const int64_t c0 = blockIdx.x * per, c1 = c0 + per < S ? c0 + per : S;
+  const int ne = n * n;
+  constexpr int KMAX = EIG_MAX * EIG_MAX / 256;
+  double acc[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) acc[k] = 0.0;
+  for (int64_t c = c0; c < c1; c += GB) {
+    const int nb = static_cast<int>(c1 - c < GB ? c1 - c : GB);
+    __syncthreads();
+    for (int x = threadIdx.x; x < nb * n; x += blockDim.x) {
+      const int j = x / n, a = x - j * n;
+      const int64_t p = a / Q, q = a - p * Q;
+      v[j][a] = Y[(p * S + c + j) * Q + q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      const int e = threadIdx.x + 256 * k;
+      if (e >= ne) break;
+      const int a = e / n, b = e - a * n;
+      double t = acc[k];
+      for (int j = 0; j < nb; ++j) t = fma(v[j][a], v[j][b], t);
+      acc[k] = t;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const int e = threadIdx.x + 256 * k;
+    if (e < ne) part[blockIdx.x * (int64_t)ne + e] = acc[k];
+  }
 }
 
 // out[0] = Σ (a - b)², out[1] = Σ a², out[2] = Σ b²  (one CTA, fixed order)
@@ -413,6 +707,7 @@ struct tk_ctx {
   // HOOI driver (tk_hosvd / tk_sweep)
   double* W = nullptr;      // Gram matrix (<= 128 x 128)
   double* V = nullptr;      // scratch (n x n)
+  double* S5 = nullptr;     // tridiagonal eigensolver scratch (6 x 128 x 128)
   double* Vm[CPPP_MAX_ORDER] = {};   // per mode: eigenvectors of the last update (warm start)
   bool vm_valid[CPPP_MAX_ORDER] = {};
   double* lam = nullptr;    // its eigenvalues
@@ -688,6 +983,8 @@ cppp_status leading_vectors(tk_ctx* c, int n, const double* Y, int64_t P, int64_
   if (!attr) {
     TKCU(c, cudaFuncSetAttribute(cppp::tk_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  220 * 1024));
+    TKCU(c, cudaFuncSetAttribute(cppp::tk_eig_topr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (cppp::EIG_MAX * (cppp::EIG_MAX + 1) + cppp::EIG_IB * 6 * cppp::EIG_MAX) * 8));
     attr = true;
   }
   const int64_t tot = (int64_t)ne * ne;
@@ -702,6 +999,16 @@ cppp_status leading_vectors(tk_ctx* c, int n, const double* Y, int64_t P, int64_
     cppp::tk_gram_combine<<<(unsigned)((tot + 255) / 256), 256, 0, c->st>>>(part, (int)nparts, (int)tot, c->W);
     cppp::note_launches(2);
     TKST(tfree(c, part));
+  } else if (!rows && S > 64) {   // rank side, long y range: split it over CTAs
+    int64_t nparts = std::min<int64_t>(148, (S + 31) / 32);
+    const int64_t per = (S + nparts - 1) / nparts;
+    nparts = (S + per - 1) / per;
+    double* part = nullptr;
+    TKST(talloc(c, &part, nparts * tot));
+    cppp::tk_gram_cols_partial<<<(unsigned)nparts, 256, 0, c->st>>>(Y, P, S, Q, per, part);
+    cppp::tk_gram_combine<<<(unsigned)((tot + 255) / 256), 256, 0, c->st>>>(part, (int)nparts, (int)tot, c->W);
+    cppp::note_launches(2);
+    TKST(tfree(c, part));
   } else {
     const int64_t blocks = std::min<int64_t>((tot + 255) / 256, 148 * 8);
     cppp::tk_gram_kernel<<<(unsigned)blocks, 256, 0, c->st>>>(Y, P, S, Q, rows, c->W);
@@ -709,12 +1016,23 @@ cppp_status leading_vectors(tk_ctx* c, int n, const double* Y, int64_t P, int64_
   }
   double* Vn = c->Vm[n];
   const size_t wbytes = (size_t)ne * (ne + 1) * 8;
-  const bool vsm = 2 * wbytes <= 220 * 1024;
-  cppp::tk_eig_kernel<<<1, cppp::EIG_THREADS, vsm ? 2 * wbytes : wbytes, c->st>>>(
-      c->W, ne, Vn, c->V, warm ? 1 : 0, vsm ? 1 : 0, c->lam, tk_debug() ? 1 : 0);
-  cppp::tk_select_kernel<<<1, cppp::EIG_THREADS, 0, c->st>>>(Vn, c->lam, ne, c->R[n], Y, P, S, Q,
-                                                            rows, c->A[n]);
-  cppp::note_launches(2);
+  static const bool jacobi = getenv("CPPP_TK_JACOBI") != nullptr;   // A/B: the Jacobi solver
+  if (jacobi) {
+    const bool vsm = 2 * wbytes <= 220 * 1024;
+    cppp::tk_eig_kernel<<<1, cppp::EIG_THREADS, vsm ? 2 * wbytes : wbytes, c->st>>>(
+        c->W, ne, Vn, c->V, warm ? 1 : 0, vsm ? 1 : 0, c->lam, tk_debug() ? 1 : 0);
+  } else {
+    cppp::tk_eig_topr_kernel<<<1, cppp::TOPR_THREADS, wbytes + (size_t)cppp::EIG_IB * 6 * ne * 8, c->st>>>(
+        c->W, ne, c->R[n], Vn, c->lam,
+                                                                       c->S5, tk_debug() ? 1 : 0);
+  }
+  {
+    const int64_t ent = S * c->R[n];
+    const unsigned g = (unsigned)std::min<int64_t>((ent + 127) / 128, 148 * 4);
+    cppp::tk_select_kernel<<<g, 128, 0, c->st>>>(Vn, c->lam, ne, c->R[n], Y, P, S, Q, rows, c->A[n]);
+    cppp::tk_sign_kernel<<<1, cppp::EIG_THREADS, 0, c->st>>>(c->A[n], S, c->R[n]);
+  }
+  cppp::note_launches(3);
   TKCU(c, cudaGetLastError());
   return CPPP_OK;
 }
@@ -836,17 +1154,22 @@ cppp_status tk_init(tk_ctx** out, const double* X, int N, const int64_t* s, cons
       dalloc(c, &c->V, cppp::EIG_MAX * cppp::EIG_MAX) != CPPP_OK ||
       dalloc(c, &c->lam, cppp::EIG_MAX) != CPPP_OK || dalloc(c, &c->G, canon_elems(c, 0u)) != CPPP_OK ||
       dalloc(c, &c->Gp, canon_elems(c, 0u)) != CPPP_OK || dalloc(c, &c->Aold, amax) != CPPP_OK ||
-      dalloc(c, &c->stats, 3 * N + 3) != CPPP_OK)
+      dalloc(c, &c->stats, 3 * N + 3) != CPPP_OK ||
+      dalloc(c, &c->S5, 6 * cppp::EIG_MAX * cppp::EIG_MAX) != CPPP_OK)
     return bail(CPPP_ENOMEM);
   for (int n = 0; n < N; ++n)
     if (dalloc(c, &c->Vm[n], cppp::EIG_MAX * cppp::EIG_MAX) != CPPP_OK) return bail(CPPP_ENOMEM);
   if (cudaMallocHost(&c->hstats, sizeof(double) * (3 * N + 3)) != cudaSuccess) return bail(CPPP_ENOMEM);
-  cppp::tk_sumsq_kernel<<<1, 1024, 0, c->st>>>(c->X, nullptr, numel, c->stats);
-  cppp::note_launch();
-  if (cudaMemcpyAsync(c->hstats, c->stats, sizeof(double) * 3, cudaMemcpyDeviceToHost, c->st) != cudaSuccess ||
-      cudaStreamSynchronize(c->st) != cudaSuccess)
-    return bail(CPPP_ECUDA);
-  c->normX_sq = c->hstats[1];
+  {
+    const int nb = cppp::sqnorm_blocks(numel);
+    double* part = nullptr;
+    if (dalloc(c, &part, nb) != CPPP_OK) return bail(CPPP_ENOMEM);
+    if (cppp::launch_sqnorm(c->X, numel, part, nb, c->stats, c->st) != cudaSuccess ||
+        cudaMemcpyAsync(c->hstats, c->stats, sizeof(double), cudaMemcpyDeviceToHost, c->st) != cudaSuccess ||
+        cudaStreamSynchronize(c->st) != cudaSuccess)
+      return bail(CPPP_ECUDA);
+    c->normX_sq = c->hstats[0];
+  }
   const size_t nscr = cppp::ttm_scratch_doubles(smax);
   if (dalloc(c, &c->Fpad, (int64_t)nscr) != CPPP_OK) return bail(CPPP_ENOMEM);
   if (cudaMemsetAsync(c->Fpad, 0, sizeof(double) * nscr, c->st) != cudaSuccess ||
