@@ -637,8 +637,21 @@ struct PPTree {
     int k = 0;
     for (int v = 0; v < N; ++v)
       if (v != c->q) tau[k++] = v;
-    // largest dimensions contracted first: stable sort by decreasing global size
-    std::stable_sort(tau, tau + k, [&](int a, int b) { return c->s[a] > c->s[b]; });
+    // largest dimensions contracted first: stable sort by decreasing global size; among
+    // equal sizes, modes whose level-1 TTM tiles cleanly come first (the first and last modes,
+    // and middle modes whose trailing extent R is a multiple of 16, which the GEMM tiles over
+    // the flattened (b, r) rows) — only tau[0..2] are contracted from X, so a middle mode with a
+    // ragged R (C3's mode 2: R = 100, 28 of every 128 tile rows idle) moves out of level 1
+    auto ragged = [&](int m) {
+      if (m == 0 || m == c->N - 1) return 0;
+      int64_t R = 1;
+      for (int v = m + 1; v < c->N; ++v) R *= c->dl[v];
+      return R % 16 != 0 ? 1 : 0;
+    };
+    std::stable_sort(tau, tau + k, [&](int a, int b) {
+      if (c->s[a] != c->s[b]) return c->s[a] > c->s[b];
+      return ragged(a) < ragged(b);
+    });
     if (c->q >= 0) tau[k++] = c->q;
   }
 

@@ -56,7 +56,10 @@ def test_plan_describe_lists_def_pptree():
     assert per_level == [3, 6, 10, 15]          # C(l+2, 2), Lemma cost
     assert sum("leaf" in l for l in lines) == 15
     sh = cp.cppp_plan_describe(4, 0)
-    assert sh.splitlines()[0] == "pptree tau: 1 2 3 0"   # sharded mode contracted only at leaves
+    tau = [int(x) for x in sh.splitlines()[0].split(":")[1].split()]
+    assert tau[-1] == 0 and sorted(tau) == [0, 1, 2, 3]   # sharded mode contracted only at leaves
+    # ties in size: the middle mode with a ragged trailing extent (R = 4) leaves level 1
+    assert cp.cppp_plan_describe(4).splitlines()[0] == "pptree tau: 0 1 3 2"
 
 
 @pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="CPU-only behaviour")
