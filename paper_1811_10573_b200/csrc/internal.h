@@ -97,18 +97,6 @@ size_t ttv_scratch_doubles();
 cudaError_t launch_ttv_cfg(const double* P, int64_t B, int64_t S, int64_t R, int K,
                            const double* F, double* out, int V, int U, int xs, cudaStream_t st);
 
-// Fused multi-output TTV: up to 3 children of one parent in one pass.  The parent is viewed
-// as [B][S0]...[S_{m-1}][T][K] where the children contract axis c of the m middle axes.
-struct TtvMulti {
-  const double* P;
-  int64_t B, T;             // outer block count, tail size
-  int m;                    // number of middle axes (1..3), each contracted by one child
-  int64_t S[3];
-  const double* F[3];       // factor for the contracted axis (S[c] x K)
-  double* out[3];           // child outputs: parent layout with axis c removed
-  int K;
-};
-cudaError_t launch_ttv_multi(const TtvMulti& p, cudaStream_t st);
 
 // PP update (Alg. 3): Mt[y][k] = Mp[y][k] + extra[y][k]
 //   + Σ_t Σ_x Op_t(x, y, k) * dA_t[x][k], Op_t(x,y,k) at Op_t + x*sx_t + y*sy_t + k.

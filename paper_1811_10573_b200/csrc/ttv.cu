@@ -8,9 +8,9 @@
 // which walks its x range in ascending order (deterministic, no atomics); consecutive threads own
 // consecutive (r, k) so every x step is a coalesced row read of the parent.
 //
-// The fused variant emits all children of one parent in ONE pass over the parent (the
-// per-parent fan-out of Def. pptree is 3/2/1 at level 2): a CTA owns a [S0 x ... x S_{m-1}]
-// block of one (b, tail, k) fibre set in shared memory and reduces it along each axis.
+// Every child of a tree node is its own pass over the parent (a one-pass variant for all the
+// children of a parent was analysed and not built: the children reduce along different axes, so
+// a one-pass kernel needs partial outputs per block along each axis — DESIGN.md §11).
 #include "internal.h"
 
 #include <cstdio>
@@ -179,19 +179,6 @@ cudaError_t launch_ttv(const double* P, int64_t B, int64_t S, int64_t R, int K, 
     fprintf(stderr, "ttv B %lld S %lld R %lld K %d: V %d xs %d\n", (long long)B, (long long)S,
             (long long)R, K, V, xs);
   return launch_ttv_cfg(P, B, S, R, K, F, out, V, 4, xs, st);
-}
-
-cudaError_t launch_ttv_multi(const TtvMulti& p, cudaStream_t st) {
-  // Generic path: one pass per child.  Child c contracts middle axis c of
-  // [B][S0]..[S_{m-1}][T][K]: view as [B*prod(S_<c)][S_c][prod(S_>c)*T][K].
-  for (int c = 0; c < p.m; ++c) {
-    int64_t Bc = p.B, Rc = p.T;
-    for (int a = 0; a < c; ++a) Bc *= p.S[a];
-    for (int a = c + 1; a < p.m; ++a) Rc *= p.S[a];
-    cudaError_t e = launch_ttv(p.P, Bc, p.S[c], Rc, p.K, p.F[c], p.out[c], nullptr, st);
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
 }
 
 }  // namespace cppp
