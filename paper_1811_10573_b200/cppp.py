@@ -19,7 +19,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcppp.so")
+LIB_PATH = os.environ.get("CPPP_LIB") or os.path.join(_HERE, "libcppp.so")   # CPPP_LIB: A/B builds
 
 PHASE_AUTO, PHASE_DT, PHASE_PP_BUILD, PHASE_PP = -1, 0, 1, 2
 PHASE_NAMES = {PHASE_DT: "dt", PHASE_PP_BUILD: "pp-build", PHASE_PP: "pp-approx"}

@@ -152,7 +152,7 @@ __device__ __forceinline__ Unit decode_unit(long long u, long long nfull, int nk
   return Unit{nfull + v / ks, nk * c / ks, nk * (c + 1) / ks, c};
 }
 
-template <int NT, bool MC>
+template <int NT, bool MC, bool BATCH = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
     ttm_dmma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
                     double* __restrict__ out, int64_t Mrows, int64_t mtiles, int64_t nfull,
@@ -186,18 +186,63 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmF)) : "memory");
-      int64_t it = 0;
-      while (true) {
-        // dynamic tile scheduler: robust to SMs that are busy with other streams' work
-        const long long unit = static_cast<long long>(atomicAdd(tile_counter, 1ull));
-        if (unit >= nunits) {
-          const int st = static_cast<int>(it % stages);
-          const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
-          if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
-          stage_tile[st] = -1;
-          mbar_arrive(smem_u32(&full[st]));   // wake the consumers with the sentinel
-          break;
+      if constexpr (!BATCH) {
+        int64_t it = 0;
+        while (true) {
+          // dynamic tile scheduler: robust to SMs that are busy with other streams' work
+          const long long unit = static_cast<long long>(atomicAdd(tile_counter, 1ull));
+          if (unit >= nunits) {
+            const int st = static_cast<int>(it % stages);
+            const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+            if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+            stage_tile[st] = -1;
+            mbar_arrive(smem_u32(&full[st]));   // wake the consumers with the sentinel
+            break;
+          }
+          const Unit un = decode_unit(unit, nfull, nk, ks);
+          const int64_t b = MC ? un.tile / mtiles : 0;
+          const int64_t m0 = (un.tile - b * mtiles) * BM;
+          // flattened rows: (batch, row) of the tile's first row, one division per unit
+          const int64_t b_first = Rflat ? m0 / Rflat : 0;
+          const int64_t r_first = Rflat ? m0 - b_first * Rflat : 0;
+          for (int kt = un.k0; kt < un.k1; ++kt, ++it) {
+            const int st = static_cast<int>(it % stages);
+            const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+            if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+            if (kt == un.k0) stage_tile[st] = unit;
+            const uint32_t fb = smem_u32(&full[st]);
+            mbar_expect_tx(fb, C::STAGE);
+            const uint32_t sx = smem_u32(base + st * C::STAGE);
+            const uint32_t sf = sx + C::XBYTES;
+            if (!MC) {
+              tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb);
+            } else if (Rflat == 0) {
+#pragma unroll
+              for (int c = 0; c < BM / 16; ++c)
+                tma_3d(sx + c * 2048, &tmX, static_cast<int>(m0 + 16 * c), kt * BK,
+                       static_cast<int>(b), fb);
+            } else {   // rows flattened over (b, r): each 16-row box has its own (b, r)
+              int rc = static_cast<int>(r_first), bc = static_cast<int>(b_first);
+#pragma unroll
+              for (int c = 0; c < BM / 16; ++c) {
+                tma_3d(sx + c * 2048, &tmX, rc, kt * BK, bc, fb);
+                rc += 16;
+                if (rc >= Rflat) {   // R % 16 == 0: a box never straddles two batches
+                  rc -= static_cast<int>(Rflat);
+                  ++bc;
+                }
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < C::BNP / 16; ++c) tma_2d(sf + c * 2048, &tmF, 16 * c, kt * BK, fb);
+          }
         }
+      } else {
+        // units with few k stages (short reductions): claimed UB = 4 at a time, the next batch
+        // before this one's loads are issued, so the atomic's round trip is not paid per unit
+        constexpr long long UB = 4;
+        int64_t it = 0;
+        auto issue = [&](long long unit) {
         const Unit un = decode_unit(unit, nfull, nk, ks);
         const int64_t b = MC ? un.tile / mtiles : 0;
         const int64_t m0 = (un.tile - b * mtiles) * BM;
@@ -235,6 +280,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int c = 0; c < C::BNP / 16; ++c) tma_2d(sf + c * 2048, &tmF, 16 * c, kt * BK, fb);
         }
+        };
+        long long next = static_cast<long long>(atomicAdd(tile_counter, (unsigned long long)UB));
+        while (next < nunits) {
+          const long long u0 = next, u1 = u0 + UB < nunits ? u0 + UB : nunits;
+          next = static_cast<long long>(atomicAdd(tile_counter, (unsigned long long)UB));
+          for (long long unit = u0; unit < u1; ++unit) issue(unit);
+        }
+        const int st = static_cast<int>(it % stages);
+        const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+        if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+        stage_tile[st] = -1;
+        mbar_arrive(smem_u32(&full[st]));   // wake the consumers with the sentinel
       }
     }
     return;
@@ -443,14 +500,14 @@ bool make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims,
   return r == CUDA_SUCCESS;
 }
 
-template <int NT, bool MC>
-cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
+template <int NT, bool MC, bool BATCH>
+cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
                      double* out, unsigned long long* counter, unsigned int* tickets, double* part,
                      cudaStream_t st, int reserve) {
   using C = Cfg<NT>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(ttm_dmma_kernel<NT, MC>,
+    cudaError_t e = cudaFuncSetAttribute(ttm_dmma_kernel<NT, MC, BATCH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::smem(C::MAX_STAGES));
     if (e != cudaSuccess) return e;
@@ -486,7 +543,7 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
   const int64_t mtiles = (Mrows + BM - 1) / BM;
   const int64_t ntiles = mtiles * ((MC && !Rflat) ? B : 1);
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ttm_dmma_kernel<NT, MC>, NTHREADS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ttm_dmma_kernel<NT, MC, BATCH>, NTHREADS, smem);
   if (occ < 1) occ = 1;
   int sms = 148;
   {
@@ -544,11 +601,21 @@ cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const dou
     fprintf(stderr, "ttm B %lld S %lld R %lld K %d: tiles %lld grid %lld split %lld x %d\n",
             (long long)B, (long long)S, (long long)R, K, (long long)ntiles, (long long)grid,
             (long long)nsplit, ks);
-  cudaError_t e = launch_pdl(ttm_dmma_kernel<NT, MC>, dim3((unsigned)grid), dim3(NTHREADS), smem, st,
+  cudaError_t e = launch_pdl(ttm_dmma_kernel<NT, MC, BATCH>, dim3((unsigned)grid), dim3(NTHREADS), smem, st,
                              tmX, tmF, out, Mrows, mtiles, nfull, nsplit, ks, (int)S, K, stages,
                              Rflat, counter, tickets, part);
   note_launch();
   return e;
+}
+
+// units of fewer than 8 k stages (S <= 112, whole tiles) take the batched scheduler
+template <int NT, bool MC>
+cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
+                     double* out, unsigned long long* counter, unsigned int* tickets, double* part,
+                     cudaStream_t st, int reserve) {
+  if ((S + BK - 1) / BK < 8)
+    return run_dmma_b<NT, MC, true>(X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve);
+  return run_dmma_b<NT, MC, false>(X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve);
 }
 
 template <bool MC, int NT = 1>
