@@ -416,8 +416,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const double v0 = acc[2 * c][0], v1 = acc[2 * c + 1][0];
           const double v2 = acc[2 * c][1], v3 = acc[2 * c + 1][1];
           if (pairs && n0 + 3 < K) {
-            *reinterpret_cast<double2*>(orow + n0) = make_double2(v0, v1);
-            *reinterpret_cast<double2*>(orow + n0 + 2) = make_double2(v2, v3);
+            double* p = orow + n0;
+            if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {   // one full 32-byte sector
+              asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v0), "d"(v1),
+                           "d"(v2), "d"(v3)
+                           : "memory");
+            } else {
+              *reinterpret_cast<double2*>(p) = make_double2(v0, v1);
+              *reinterpret_cast<double2*>(p + 2) = make_double2(v2, v3);
+            }
           } else {
             if (n0 < K) orow[n0] = v0;
             if (n0 + 1 < K) orow[n0 + 1] = v1;
