@@ -615,12 +615,14 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
   return e;
 }
 
-// units of fewer than 8 k stages (S <= 112, whole tiles) take the batched scheduler
+// units of fewer than 8 k stages (S <= 112, whole tiles) take the batched scheduler when there
+// are many of them (>= 8 per SM; a small GEMM would leave CTAs idle: C1's 13 tiles)
 template <int NT, bool MC>
 cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
                      double* out, unsigned long long* counter, unsigned int* tickets, double* part,
                      cudaStream_t st, int reserve) {
-  if ((S + BK - 1) / BK < 8)
+  const int64_t tiles_est = MC ? B * ((R + BM - 1) / BM) : (B + BM - 1) / BM;
+  if ((S + BK - 1) / BK < 8 && tiles_est >= 148 * 8)
     return run_dmma_b<NT, MC, true>(X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve);
   return run_dmma_b<NT, MC, false>(X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve);
 }
