@@ -988,9 +988,9 @@ cppp_status leading_vectors(tk_ctx* c, int n, const double* Y, int64_t P, int64_
     attr = true;
   }
   const int64_t tot = (int64_t)ne * ne;
-  if (rows && P * Q > 4096) {   // long reduction: split it over CTAs, combine in order
+  if (rows && P * Q > 256) {   // long reduction: split it over CTAs, combine in order
     const int64_t L = P * Q;
-    int64_t nparts = std::min<int64_t>(296, (L + 4095) / 4096);
+    int64_t nparts = std::min<int64_t>(296, (L + 63) / 64);
     const int64_t per = (L + nparts - 1) / nparts;
     nparts = (L + per - 1) / per;
     double* part = nullptr;
