@@ -111,6 +111,14 @@ __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                       int c2, int c3, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void lds2(double& x, double& y, uint32_t addr) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(addr));
 }
@@ -155,10 +163,11 @@ __device__ __forceinline__ Unit decode_unit(long long u, long long nfull, int nk
 template <int NT, bool MC, bool BATCH = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
     ttm_dmma_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmF,
+                    const __grid_constant__ CUtensorMap tmX4,
                     double* __restrict__ out, int64_t Mrows, int64_t mtiles, int64_t nfull,
                     int64_t nsplit, int ks, int S, int K, int stages, int64_t Rflat,
                     unsigned long long* __restrict__ tile_counter, unsigned int* __restrict__ tickets,
-                    double* __restrict__ part) {
+                    double* __restrict__ part, int box8, int64_t Rm) {
   using C = Cfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -186,6 +195,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmF)) : "memory");
+      if (box8) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX4)) : "memory");
       if constexpr (!BATCH) {
         int64_t it = 0;
         while (true) {
@@ -216,6 +226,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint32_t sf = sx + C::XBYTES;
             if (!MC) {
               tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb);
+            } else if (box8 && (Rflat ? r_first : m0) + BM <= Rm) {
+              // R % 16 == 0 and the tile inside one batch: its eight 16-row boxes in one 4-D load
+              tma_4d(sx, &tmX4, 0, kt * BK, static_cast<int>((Rflat ? r_first : m0) / 16),
+                     static_cast<int>(Rflat ? b_first : b), fb);
             } else if (Rflat == 0) {
 #pragma unroll
               for (int c = 0; c < BM / 16; ++c)
@@ -260,6 +274,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint32_t sf = sx + C::XBYTES;
           if (!MC) {
             tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb);
+          } else if (box8 && (Rflat ? r_first : m0) + BM <= Rm) {
+            // R % 16 == 0 and the tile inside one batch: its eight 16-row boxes in one 4-D load
+            tma_4d(sx, &tmX4, 0, kt * BK, static_cast<int>((Rflat ? r_first : m0) / 16),
+                   static_cast<int>(Rflat ? b_first : b), fb);
           } else if (Rflat == 0) {
 #pragma unroll
             for (int c = 0; c < BM / 16; ++c)
@@ -499,12 +517,17 @@ bool make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims,
               const cuuint64_t* strides_bytes, const cuuint32_t* box) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return false;
-  cuuint32_t es[3] = {1, 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(ptr), dims,
                    strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+bool getenv_no_box8() {   // CPPP_NO_BOX8: the per-16-row boxes (A/B)
+  static const bool v = getenv("CPPP_NO_BOX8") != nullptr;
+  return v;
 }
 
 template <int NT, bool MC, bool BATCH>
@@ -525,6 +548,7 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
   // (16-row boxes never straddle a batch), so no batch leaves a partial tile (C2's middle mode:
   // R = 400 = 3 x 128 + 16 wasted 22% of the tiles' rows)
   const int64_t Rflat = (MC && B > 1 && R % 16 == 0) ? R : 0;
+  const int box8 = (MC && R % 16 == 0 && R >= BM && !getenv_no_box8()) ? 1 : 0;
   const int64_t Mrows = MC ? (Rflat ? B * R : R) : B;
   if (!MC) {
     cuuint64_t dims[2] = {(cuuint64_t)S, (cuuint64_t)B};
@@ -536,6 +560,15 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
     cuuint64_t str[2] = {(cuuint64_t)R * 8, (cuuint64_t)(S * R) * 8};
     cuuint32_t box[3] = {16, 16, 1};
     if (!make_map(&tmX, X, 3, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  CUtensorMap tmX4 = tmX;
+  if (box8) {
+    // [B][S][R] viewed as [B][R/16][S][16] (r = 16 r_hi + r_lo): one box = 8 r_hi x 16 x x 16 r_lo,
+    // landing in shared memory exactly as the eight 16 x 16 boxes of the 3-D map
+    cuuint64_t dims[4] = {16, (cuuint64_t)S, (cuuint64_t)(R / 16), (cuuint64_t)B};
+    cuuint64_t str[3] = {(cuuint64_t)R * 8, 128, (cuuint64_t)(S * R) * 8};
+    cuuint32_t box[4] = {16, 16, 8, 1};
+    if (!make_map(&tmX4, X, 4, dims, str, box)) return cudaErrorInvalidValue;
   }
   {
     cuuint64_t dims[2] = {(cuuint64_t)C::BNP, (cuuint64_t)S};
@@ -609,8 +642,8 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
             (long long)B, (long long)S, (long long)R, K, (long long)ntiles, (long long)grid,
             (long long)nsplit, ks);
   cudaError_t e = launch_pdl(ttm_dmma_kernel<NT, MC, BATCH>, dim3((unsigned)grid), dim3(NTHREADS), smem, st,
-                             tmX, tmF, out, Mrows, mtiles, nfull, nsplit, ks, (int)S, K, stages,
-                             Rflat, counter, tickets, part);
+                             tmX, tmF, tmX4, out, Mrows, mtiles, nfull, nsplit, ks, (int)S, K, stages,
+                             Rflat, counter, tickets, part, box8, R);
   note_launch();
   return e;
 }

@@ -41,7 +41,12 @@ def random_problem(dims, K, seed):
 
 SMALL = ["C1", "C2mini", "C3mini", "C4mini", "C5mini"]
 RAGGED = [((7, 9, 5), 3), ((6, 10, 12), 17), ((130, 4, 6), 5), ((8, 6, 4, 10), 7),
-          ((3, 4, 2, 3, 2), 2), ((40, 36, 34), 128), ((34, 18, 10, 6), 100)]
+          ((3, 4, 2, 3, 2), 2), ((40, 36, 34), 128), ((34, 18, 10, 6), 100),
+          # trailing extents that are multiples of 128: the one-load 4-D TMA path of the
+          # m-contiguous GEMM (B = 1 and flattened B > 1)
+          ((20, 16, 8), 12), ((6, 10, 256), 24), ((4, 128, 130), 20),
+          # multiples of 16 only: the 4-D load for tiles inside one batch, 16-row boxes for the rest
+          ((6, 10, 400), 16), ((3, 20, 48, 16), 8)]
 
 
 @pytest.mark.parametrize("name", SMALL)
