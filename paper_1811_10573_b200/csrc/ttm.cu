@@ -247,8 +247,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
               }
             }
-#pragma unroll
-            for (int c = 0; c < C::BNP / 16; ++c) tma_2d(sf + c * 2048, &tmF, 16 * c, kt * BK, fb);
+            tma_3d(sf, &tmF, 0, kt * BK, 0, fb);   // all BNP/16 column boxes in one load
           }
         }
       } else {
@@ -295,8 +294,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
           }
-#pragma unroll
-          for (int c = 0; c < C::BNP / 16; ++c) tma_2d(sf + c * 2048, &tmF, 16 * c, kt * BK, fb);
+          tma_3d(sf, &tmF, 0, kt * BK, 0, fb);   // all BNP/16 column boxes in one load
         }
         };
         long long next = static_cast<long long>(atomicAdd(tile_counter, (unsigned long long)UB));
@@ -571,10 +569,12 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
     if (!make_map(&tmX4, X, 4, dims, str, box)) return cudaErrorInvalidValue;
   }
   {
-    cuuint64_t dims[2] = {(cuuint64_t)C::BNP, (cuuint64_t)S};
-    cuuint64_t str[1] = {(cuuint64_t)C::BNP * 8};
-    cuuint32_t box[2] = {16, 16};
-    if (!make_map(&tmF, Fp, 2, dims, str, box)) return cudaErrorInvalidValue;
+    // the padded factor [S][BNP] viewed as [BNP/16][S][16]: one box = every 16-column strip of
+    // a 16-deep k slice, landing as the strips' 16 x 16 boxes one after another
+    cuuint64_t dims[3] = {16, (cuuint64_t)S, (cuuint64_t)(C::BNP / 16)};
+    cuuint64_t str[2] = {(cuuint64_t)C::BNP * 8, 128};
+    cuuint32_t box[3] = {16, 16, (cuuint32_t)(C::BNP / 16)};
+    if (!make_map(&tmF, Fp, 3, dims, str, box)) return cudaErrorInvalidValue;
   }
   // the ring spans several tiles when S is short (C4: s = 20 -> 2 slices per tile), so the
   // producer keeps loading the next tiles while the consumers finish this one
