@@ -336,6 +336,24 @@ const double* fac_local(cppp_ctx* c, double* const* F, int u) {
 // regular sweep (Alg. 3: always, unless a phase is forced) has A_p = A, so that TTM IS its
 // M_p^(1,2) = X ×_0 A_p^(0) — one of the build's three full-tensor TTMs is skipped.  Same kernel,
 // same shape: the operator is bit-identical to a recomputed one (tested).
+// The order-3 GEMM that runs beside latency-bound work: two SMs without a persistent CTA (the
+// factorization's 640-thread CTA cannot share an SM with a GEMM CTA).  A shallower ring (so a
+// row-solve CTA could share an SM with a GEMM CTA) costs the GEMM < 1% (CPPP_TTM_STAGES in
+// tools/probe_ttm) but buys nothing: the row solve stages Γ and its factor in ~207 KB of shared
+// memory, and the Gram kernel's registers do not fit beside a GEMM CTA either.
+// CPPP_TTM_RESERVE / CPPP_SIDE_STAGES: A/B.
+TtmOpts side_gemm_opts() {
+  static const TtmOpts o = [] {
+    TtmOpts t;
+    const char* r = getenv("CPPP_TTM_RESERVE");
+    const char* st = getenv("CPPP_SIDE_STAGES");
+    t.reserve_sms = r ? atoi(r) : 2;
+    t.max_stages = st ? atoi(st) : 0;
+    return t;
+  }();
+  return o;
+}
+
 bool reuse12(const cppp_ctx* c) {
   return c->N == 3 && c->q < 0 && !(c->flags & CPPP_FLAG_NO_OP_REUSE);
 }
@@ -348,7 +366,7 @@ int64_t node_elems(cppp_ctx* c, uint32_t mask) {
 
 // out = contraction of `src` along mode u with factor F (local rows)
 cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, double* out,
-                     cudaStream_t st = nullptr, int reserve_sms = 0) {
+                     cudaStream_t st = nullptr, TtmOpts topt = TtmOpts{}) {
   if (!st) st = c->st;
   int64_t B = 1, R = 1;
   for (int v = 0; v < c->N; ++v) {
@@ -365,7 +383,7 @@ cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, doubl
     const bool simt = (c->flags & CPPP_FLAG_SIMT_TTM) != 0;
     if (ttm_uses_dmma(B, S, R, K, simt)) CUCHK(c, ttm_prepare(S, F, K, c->Fpad, st));
     Prof p(c, CPPP_K_TTM, flops, bytes, st);
-    CUCHK(c, launch_ttm_core(src.data, B, S, R, F, K, out, c->Fpad, simt, st, reserve_sms));
+    CUCHK(c, launch_ttm_core(src.data, B, S, R, F, K, out, c->Fpad, simt, st, topt));
   } else {
     const double flops = 2.0 * B * S * R * K;
     const double bytes = 8.0 * (B * S * R * K + B * R * K);
@@ -563,11 +581,7 @@ struct DT {
     // two SMs stay free of the GEMM's persistent CTAs: mode 1's factorization, row solves and
     // Gram and mode 2's factorization (latency-bound, one CTA or a few rows at a time) run there
     // meanwhile instead of waiting for the GEMM to end
-    static const int reserve = [] {
-      const char* e = getenv("CPPP_TTM_RESERVE");
-      return e ? atoi(e) : 2;
-    }();
-    STCHK(contract(c, nd, 0, fac_local(c, c->A, 0), T12, c->st3, reserve));
+    STCHK(contract(c, nd, 0, fac_local(c, c->A, 0), T12, c->st3, side_gemm_opts()));
     if (!c->dry) CUCHK(c, cudaEventRecord(c->ev_T, c->st3));
     STCHK(contract(c, L, 0, fac_local(c, c->A, 0), c->M[1]));
     STCHK(leaf(1, c->M[1]));

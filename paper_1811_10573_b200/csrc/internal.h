@@ -80,10 +80,15 @@ struct KrpArgs {
 cudaError_t ttm_prepare_krp(const KrpArgs& a, double* Fpad, cudaStream_t st);
 cudaError_t launch_ttm_padded(const double* X, int64_t B, int64_t S, int64_t R, int K, double* out,
                               const double* Fpad, cudaStream_t st);
-// reserve_sms: leave that many SMs without a (persistent) GEMM CTA for other streams' kernels
+// Scheduling of one GEMM beside other streams' work: reserve_sms SMs get no (persistent) CTA;
+// max_stages (>= 2) caps the shared-memory ring so small kernels can share the SMs.
+struct TtmOpts {
+  int reserve_sms = 0;
+  int max_stages = 0;
+};
 cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
                             int K, double* out, const double* Fpad, bool force_simt,
-                            cudaStream_t st, int reserve_sms = 0);
+                            cudaStream_t st, TtmOpts topt = TtmOpts{});
 cudaError_t launch_ttm_simt(const double* X, int64_t B, int64_t S, int64_t R,
                             const double* F, int K, double* out, cudaStream_t st);
 bool ttm_dmma_supported(int64_t B, int64_t S, int64_t R, int K);

@@ -531,7 +531,7 @@ bool getenv_no_box8() {   // CPPP_NO_BOX8: the per-16-row boxes (A/B)
 template <int NT, bool MC, bool BATCH>
 cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
                      double* out, unsigned long long* counter, unsigned int* tickets, double* part,
-                     cudaStream_t st, int reserve) {
+                     cudaStream_t st, TtmOpts topt) {
   using C = Cfg<NT>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -578,7 +578,12 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
   }
   // the ring spans several tiles when S is short (C4: s = 20 -> 2 slices per tile), so the
   // producer keeps loading the next tiles while the consumers finish this one
-  const int stages = C::MAX_STAGES;
+  static const int stages_env = [] {   // CPPP_TTM_STAGES: ring depth override (A/B)
+    const char* e = getenv("CPPP_TTM_STAGES");
+    return e ? atoi(e) : 0;
+  }();
+  int stages = stages_env >= 2 && stages_env <= C::MAX_STAGES ? stages_env : C::MAX_STAGES;
+  if (topt.max_stages >= 2 && topt.max_stages < stages) stages = topt.max_stages;
   const int smem = C::smem(stages);
   const int64_t mtiles = (Mrows + BM - 1) / BM;
   const int64_t ntiles = mtiles * ((MC && !Rflat) ? B : 1);
@@ -593,7 +598,7 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
   }
   // `reserve` SMs get no CTA: the latency-bound kernels of other streams run there meanwhile
   // (a persistent CTA holds its SM until the GEMM ends)
-  const int64_t full_grid = std::max<int64_t>(1, static_cast<int64_t>(sms) * occ - reserve);
+  const int64_t full_grid = std::max<int64_t>(1, static_cast<int64_t>(sms) * occ - topt.reserve_sms);
   int64_t grid = full_grid;
   if (grid > ntiles) grid = ntiles;
   const int nk = static_cast<int>((S + BK - 1) / BK);
@@ -653,22 +658,22 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
 template <int NT, bool MC>
 cudaError_t run_dmma(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
                      double* out, unsigned long long* counter, unsigned int* tickets, double* part,
-                     cudaStream_t st, int reserve) {
+                     cudaStream_t st, TtmOpts topt) {
   const int64_t tiles_est = MC ? B * ((R + BM - 1) / BM) : (B + BM - 1) / BM;
   if ((S + BK - 1) / BK < 8 && tiles_est >= 148 * 8)
-    return run_dmma_b<NT, MC, true>(X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve);
-  return run_dmma_b<NT, MC, false>(X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve);
+    return run_dmma_b<NT, MC, true>(X, B, S, R, Fp, K, out, counter, tickets, part, st, topt);
+  return run_dmma_b<NT, MC, false>(X, B, S, R, Fp, K, out, counter, tickets, part, st, topt);
 }
 
 template <bool MC, int NT = 1>
 cudaError_t dispatch_nt(int nt, const double* X, int64_t B, int64_t S, int64_t R, const double* Fp,
                         int K, double* out, unsigned long long* counter, unsigned int* tickets,
-                        double* part, cudaStream_t st, int reserve) {
+                        double* part, cudaStream_t st, TtmOpts topt) {
   if constexpr (NT > 16) {
     return cudaErrorInvalidValue;
   } else {
-    if (nt == NT) return run_dmma<NT, MC>(X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve);
-    return dispatch_nt<MC, NT + 1>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve);
+    if (nt == NT) return run_dmma<NT, MC>(X, B, S, R, Fp, K, out, counter, tickets, part, st, topt);
+    return dispatch_nt<MC, NT + 1>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st, topt);
   }
 }
 
@@ -758,7 +763,7 @@ cudaError_t launch_ttm_padded(const double* X, int64_t B, int64_t S, int64_t R, 
 
 cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
                             int K, double* out, const double* Fpad, bool force_simt,
-                            cudaStream_t st, int reserve_sms) {
+                            cudaStream_t st, TtmOpts topt) {
   if (B * R * K == 0) return cudaSuccess;
   if (!ttm_uses_dmma(B, S, R, K, force_simt)) return launch_ttm_simt(X, B, S, R, F, K, out, st);
   double* ctl = const_cast<double*>(Fpad);
@@ -768,8 +773,8 @@ cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, co
   const double* Fp = ctl + TTM_CTL + TTM_PART;
   const int nt = (K + 7) / 8;
   if (R == 1)
-    return dispatch_nt<false>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve_sms);
-  return dispatch_nt<true>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st, reserve_sms);
+    return dispatch_nt<false>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st, topt);
+  return dispatch_nt<true>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st, topt);
 }
 
 cudaError_t launch_ttm(const double* X, int64_t B, int64_t S, int64_t R, const double* F, int K,
