@@ -831,6 +831,15 @@ cppp_status pp_update_mode(cppp_ctx* c, int n, double* out, const double* extra,
 // after_build: the sweep that follows a PP build starts from A = A_p, so dA^(i) = 0 for every
 // mode not yet updated in this sweep (i > n); those terms are left out, and the first mode's
 // M~ is M_p itself (no launch).
+// A PP sweep starts with mode 0's factorization (side stream) and its PP update (main stream)
+// at the same instant; when the update's CTAs reach the SMs first, the factorization's one CTA
+// finds no room until they drain.  A ~3 µs one-thread kernel ahead of the update lets the
+// factorization land first (CPPP_NO_STAGGER: off, for A/B).
+bool pp_stagger() {
+  static const bool off = getenv("CPPP_NO_STAGGER") != nullptr;
+  return !off;
+}
+
 cppp_status run_pp_sweep(cppp_ctx* c, bool after_build) {
   const int N = c->N;
   const bool sh = c->q >= 0 && comm_on(c);
@@ -843,6 +852,7 @@ cppp_status run_pp_sweep(cppp_ctx* c, bool after_build) {
     if (after_build && n == 0 && extra == nullptr) {   // every term is zero: M~^(0) = M_p^(0)
       STCHK(finish_mode(c, n, c->Mp[n], true));
     } else {
+      if (n == 0 && !c->dry && pp_stagger()) CUCHK(c, launch_stagger(c->st));
       STCHK(pp_update_mode(c, n, c->M[n], extra, sh && n != c->q, c->Mp[n], zero));
       STCHK(finish_mode(c, n, c->M[n], true));
     }

@@ -153,6 +153,8 @@ cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, const d
 cudaError_t launch_sqnorm(const double* x, int64_t n, double* partial, int nblk, double* out,
                           cudaStream_t st);
 int sqnorm_blocks(int64_t n);
+// a one-thread ~3 µs kernel (stream-order spacer)
+cudaError_t launch_stagger(cudaStream_t st);
 // y = a - b (elementwise)
 cudaError_t launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st);
 

@@ -868,6 +868,20 @@ cudaError_t launch_sqnorm(const double* x, int64_t n, double* partial, int nblk,
   return cudaGetLastError();
 }
 
+__global__ void stagger_kernel(unsigned ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+cudaError_t launch_stagger(cudaStream_t st) {
+  stagger_kernel<<<1, 32, 0, st>>>(3000u);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   sub_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(a, b, y, n);
