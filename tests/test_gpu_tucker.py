@@ -143,3 +143,41 @@ def test_pp_tucker_large_mode_uses_the_rank_side_gram():
     st, tr = T.pp_tucker_als(X, ranks, 0.0, 0.2, 8, A0=A0)
     check_trace(ctx, X, tr, st.A)
     cp.tk_destroy(ctx)
+
+
+@pytest.mark.parametrize("dims,ranks", [((5, 4, 6), (1, 1, 1)),                 # rank 1
+                                        ((4, 3, 5), (4, 3, 5)),                 # full ranks
+                                        ((3, 2, 2, 3, 2, 2, 3, 2), (2, 1, 2, 2, 1, 2, 2, 1))])  # N = 8
+def test_tucker_edge_shapes(dims, ranks):
+    """Degenerate ranks and the maximum order: contractions, operators, updates and 4 sweeps of
+    Alg. 4 from HOSVD against the oracle."""
+    X, Ap = problem(dims, ranks, 12)
+    N = len(dims)
+    ctx = cp.tk_init(X, dims, ranks)
+    cp.tk_set_factors(ctx, Ap)
+    Y = cp.tk_ttmc(ctx)
+    for n in range(N):
+        assert rel(Y[n], T.ttmc(X, Ap, n)) < TOL, n
+    cp.tk_pp_build(ctx)
+    ops = T.pp_operators(X, Ap)
+    for (i, j), ref in ops.items():
+        assert rel(cp.tk_pp_get_operator(ctx, i, j), ref) < TOL, (i, j)
+    st, tr = T.pp_tucker_als(X, ranks, 0.0, 0.2, 4)
+    cp.tk_hosvd(ctx)
+    for t in tr:
+        cp.tk_set_phase_override(ctx, t["phase"])
+        g = cp.tk_sweep(ctx, 0.0, 0.2)
+        assert abs(g["core_norm"] - t["core_norm"]) <= 1e-9 * t["core_norm"], (g, t)
+    cp.tk_destroy(ctx)
+
+
+def test_tucker_gram_too_large_rejected():
+    """Both sides of Y_(n) above 128 (s_0 = 200, prod of the other ranks = 11 x 13 = 143): the
+    factor update is refused with CPPP_EINVAL instead of running out of the one-CTA solver."""
+    dims, ranks = (200, 12, 14), (3, 11, 13)
+    X, A = problem(dims, ranks, 13)
+    ctx = cp.tk_init(X, dims, ranks)
+    cp.tk_set_factors(ctx, A)
+    with pytest.raises(cp.CpppError):
+        cp.tk_sweep(ctx, 0.0, 0.0)
+    cp.tk_destroy(ctx)
