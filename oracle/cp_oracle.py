@@ -35,6 +35,7 @@ building blocks and exact recovery).
 from __future__ import annotations
 
 import math
+import time
 from itertools import combinations
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -348,7 +349,7 @@ def cp_als(X, A0, sweeps: int):
 
 
 def pp_cp_als(X, A0, eps: float, eps_pp: float, max_sweeps: int,
-              phase_override: Optional[Sequence[str]] = None):
+              phase_override: Optional[Sequence[str]] = None, deadline: Optional[float] = None):
     """PP-CP-ALS, Alg. 3 with readings L7-L12:
       * the first sweep is regular (L9);
       * after each complete regular sweep, if max_i ‖dA^(i)‖/‖A^(i)‖ < ε_pp the next sweep
@@ -357,6 +358,8 @@ def pp_cp_als(X, A0, eps: float, eps_pp: float, max_sweeps: int,
         sweep ('pp-approx'), otherwise exactly one regular sweep follows (P:598, L10);
       * stop when Σ‖G^(i)‖_F <= ε or after max_sweeps sweeps (L11).
     ``phase_override`` (L12) forces the phase of each sweep (used to replay a schedule).
+    ``deadline`` (a time.perf_counter() value; bench.py's bounded CPU sample only) stops after
+    the sweep during which it passed — control flow only, the arithmetic is unchanged.
     Returns (factors, trace) with one dict per sweep."""
     st = State(X, A0)
     trace = []
@@ -382,6 +385,8 @@ def pp_cp_als(X, A0, eps: float, eps_pp: float, max_sweeps: int,
         trace.append(dict(sweep=sw + 1, phase=phase, fitness=st.fitness(), grad_norm_sum=gsum,
                           max_rel_dA=max(rel), margin=abs(max(rel) - eps_pp)))
         if gsum <= eps:
+            break
+        if deadline is not None and time.perf_counter() >= deadline:
             break
     return st.A, trace
 
