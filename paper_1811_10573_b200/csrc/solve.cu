@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
     }
     if (tid == 0) *mode = 0;
   } else if (tid == 0) {
-    *mode = 1;   // gamma_pinv_kernel takes over
+    *mode = 1;   // gamma_post_kernel runs the pseudo-inverse fallback
   }
   PROBE_T(1);
 }
@@ -220,10 +220,7 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
 // lane c computes column c of inv(L_bb) right-looking with compile-time indices; Q[b][c][j] =
 // inv(L_bb)[j][c] with row pitch 33.  Rows past ld are the identity.  Exits unless the Cholesky
 // path was taken.
-__global__ void __launch_bounds__(128)
-    block_inverse_kernel(double* Tp, int ldt, const int* mode) {
-  pdl_wait();
-  if (*mode != 0) return;
+__device__ __forceinline__ void block_inverse_dev(double* Tp, int ldt) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nblk = (ldt + 31) >> 5;
   if (wid >= nblk) return;
@@ -253,11 +250,8 @@ __global__ void __launch_bounds__(128)
 // Eigen pseudo-inverse fallback (L13): runs after gamma_chol_kernel and exits at once unless
 // the pivot test failed.  Two-sided cyclic Jacobi, Brent-Luk parallel ordering; the
 // pseudo-inverse P goes to Tp (pitch ldt).
-__global__ void __launch_bounds__(GP_THREADS, 1)
-    gamma_pinv_kernel(int K, const double* __restrict__ Gamma, double* Pout, int ldt,
-                      const int* mode, double* Vscratch) {
-  pdl_wait();
-  if (*mode == 0) return;
+__device__ __forceinline__ void gamma_pinv_dev(int K, const double* __restrict__ Gamma,
+                                               double* Pout, int ldt, double* Vscratch) {
   extern __shared__ double W[];  // K x (K+1)
   __shared__ double sh[32];
   const int tid = threadIdx.x, KK = K * K;
@@ -359,6 +353,20 @@ __global__ void __launch_bounds__(GP_THREADS, 1)
     double v = 0.0;
     for (int l = 0; l < K; ++l) v += Vscratch[i * K + l] * lam[l] * Vscratch[j * K + l];
     Pout[i * ldt + j] = v;
+  }
+}
+
+// After the factorization: the Cholesky path inverts the diagonal 32 x 32 blocks of L (warps
+// 0-3), the pseudo-inverse path (failed pivot test) runs the Jacobi fallback — one launch
+// either way (the two separate kernels cost a launch on the factorization chain per mode).
+__global__ void __launch_bounds__(GP_THREADS, 1)
+    gamma_post_kernel(int K, const double* __restrict__ Gamma, double* Tp, int ldt,
+                      const int* mode, double* Vscratch) {
+  pdl_wait();
+  if (*mode == 0) {
+    if (threadIdx.x < 128) block_inverse_dev(Tp, ldt);
+  } else {
+    gamma_pinv_dev(K, Gamma, Tp, ldt, Vscratch);
   }
 }
 
@@ -782,7 +790,7 @@ cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double
   const size_t smem = static_cast<size_t>(K) * (K + 1) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gamma_pinv_kernel,
+    cudaError_t e = cudaFuncSetAttribute(gamma_post_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 129 * 8);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -791,11 +799,7 @@ cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double
                              Gamma, Tp, ldt, mode);
   note_launch();
   if (e != cudaSuccess) return e;
-  e = launch_pdl(block_inverse_kernel, dim3(1), dim3(128), 0, st, Tp, ldt,
-                 static_cast<const int*>(mode));
-  note_launch();
-  if (e != cudaSuccess) return e;
-  e = launch_pdl(gamma_pinv_kernel, dim3(1), dim3(GP_THREADS), smem, st, K,
+  e = launch_pdl(gamma_post_kernel, dim3(1), dim3(GP_THREADS), smem, st, K,
                  static_cast<const double*>(Gamma), Tp, ldt, static_cast<const int*>(mode), Vscratch);
   note_launch();
   return e;
