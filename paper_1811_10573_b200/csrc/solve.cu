@@ -97,6 +97,7 @@ __constant__ unsigned char kCholBlock[20] = {
     4 | 1 << 4, 5 | 1 << 4, 6 | 1 << 4, 7 | 1 << 4, 2 | 1 << 4, 1,          2,
     3,          4,          5,          6,          7,          0};
 
+template <bool transpose>
 __global__ void __launch_bounds__(GF_THREADS, 1)
     gamma_chol_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
                       double* Tp, int ldt, int* mode) {
@@ -134,8 +135,26 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
     if (!(col_ok && v < rows_here)) {
       w[v] = 0.0;
     } else {
-      Gamma[i * ldt + l] = w[v];   // Γ is exactly symmetric (Grams are written mirrored):
-      Gamma[l * ldt + i] = w[v];   // the lower blocks also fill the upper triangle
+      Gamma[i * ldt + l] = w[v];   // row i: 32 consecutive columns per store
+      if constexpr (!transpose) Gamma[l * ldt + i] = w[v];   // small K: the mirror directly
+    }
+  }
+  if constexpr (transpose) {
+    // Γ is exactly symmetric (Grams are written mirrored): the lower blocks also fill the upper
+    // triangle, transposed through shared memory so every store is a 128-byte row segment
+    // (column-wise stores of the mirror cost ~10 k cycles of LSU issue at K = 100)
+    extern __shared__ double gf_dyn[];   // [GF_THREADS / 32][16][33]
+    double(*tb)[16][33] = reinterpret_cast<double(*)[16][33]>(gf_dyn);
+#pragma unroll
+    for (int v = 0; v < 16; ++v) tb[wid][v][lane] = w[v];
+    __syncwarp();
+    const int vi = lane & 15, half = lane >> 4;
+    const int i = r0 + vi;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int lc = 2 * q + half;                 // column of the block = row of the mirror
+      const int lm = 32 * cg + lc;
+      if (lowerw && lm < K && vi < rows_here) Gamma[lm * ldt + i] = tb[wid][vi][lc];
     }
   }
   double dmax = has_diag ? diag : 0.0;
@@ -193,6 +212,8 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
     __syncthreads();
   }
   if (!bad_s) {
+    extern __shared__ double gf_dyn[];   // the mirror transposes again: column l of L as rows
+    double(*tb)[16][33] = reinterpret_cast<double(*)[16][33]>(gf_dyn);
     if (col_ok) {
       const double d = dpiv[l];
       const double r = sqrt(d);
@@ -203,10 +224,21 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
         if (i < K && i > l) {
           const double x = w[v] * ri;
           Tp[i * ldt + l] = x;   // row i of L
-          Tp[l * ldt + i] = x;   // column l of L
+          if constexpr (transpose) tb[wid][v][lane] = x;
+          else Tp[l * ldt + i] = x;
         } else if (i == l) {
           Tp[l * ldt + l] = 1.0 / r;
         }
+      }
+    }
+    __syncwarp();
+    if constexpr (transpose) {   // column l of L below the diagonal into row l of Tp, 128-byte rows
+      const int vi = lane & 15, half = lane >> 4;
+      const int i = r0 + vi;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int lm = 32 * cg + 2 * q + half;
+        if (lowerw && lm < K && i < K && i > lm) Tp[lm * ldt + i] = tb[wid][vi][2 * q + half];
       }
     }
     if (tid == 0) *mode = 0;
@@ -795,8 +827,23 @@ cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  cudaError_t e = launch_pdl(gamma_chol_kernel, dim3(1), dim3(GF_THREADS), 0, st, S_all, N, n, K,
-                             Gamma, Tp, ldt, mode);
+  // K > 48: the mirrored halves of Γ and of the factor go out through shared-memory transposes
+  // (coalesced rows); for small K the direct column stores are cheaper than the extra shared
+  // memory (C1's K = 10 lost 3% to it; the opt-in attribute is only set once a large K needs it)
+  constexpr size_t chol_smem = sizeof(double) * (GF_THREADS / 32) * 16 * 33;   // mirror transposes
+  const bool transpose = K > 48;
+  static bool chol_attr = false;
+  if (transpose && !chol_attr) {
+    cudaError_t e = cudaFuncSetAttribute(gamma_chol_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem);
+    if (e != cudaSuccess) return e;
+    chol_attr = true;
+  }
+  cudaError_t e = transpose
+                      ? launch_pdl(gamma_chol_kernel<true>, dim3(1), dim3(GF_THREADS), chol_smem, st,
+                                   S_all, N, n, K, Gamma, Tp, ldt, mode)
+                      : launch_pdl(gamma_chol_kernel<false>, dim3(1), dim3(GF_THREADS), 0, st, S_all,
+                                   N, n, K, Gamma, Tp, ldt, mode);
   note_launch();
   if (e != cudaSuccess) return e;
   e = launch_pdl(gamma_post_kernel, dim3(1), dim3(GP_THREADS), smem, st, K,
