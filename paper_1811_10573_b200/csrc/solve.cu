@@ -274,9 +274,15 @@ __device__ __forceinline__ void block_inverse_dev(double* Tp, int ldt) {
 #pragma unroll
     for (int j = i + 1; j < 32; ++j) y[j] = fma(Ls[wid][j][i], y[i], y[j]);   // L[j][i]
   }
-  double* Q = Tp + ldt * ldt + wid * 32 * 33;
+  // Q[c][j] = y_c[j]: staged row-wise in shared memory (the block is no longer needed), then
+  // written as 33-double rows by the whole warp (coalesced; lane-c row stores hit 32 sectors)
+  __syncwarp();
 #pragma unroll
-  for (int j = 0; j < 32; ++j) Q[c * 33 + j] = y[j];
+  for (int j = 0; j < 32; ++j) Ls[wid][c][j] = y[j];
+  __syncwarp();
+  double* Q = Tp + ldt * ldt + wid * 32 * 33;
+#pragma unroll 4
+  for (int r = 0; r < 32; ++r) Q[r * 33 + lane] = Ls[wid][r][lane];
 }
 
 // Eigen pseudo-inverse fallback (L13): runs after gamma_chol_kernel and exits at once unless
