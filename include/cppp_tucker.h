@@ -4,7 +4,8 @@
  * (Def. 3.2, Alg. 4), on the same FP64 tensor-core GEMM as the CP path.
  *
  * A full HOOI / PP-Tucker run (tk_hosvd, tk_sweep) runs on the device as well: the factor
- * update is a Gram matrix, a Jacobi eigensolver and a sign fix.
+ * update is a Gram matrix, a top-R symmetric eigensolver (Householder tridiagonalization,
+ * bisection, inverse iteration) and a sign fix.
  *
  * Conventions (in addition to cppp.h's: FP64, row-major, 0-based modes, host or device pointers,
  * stream ordering, status codes):
@@ -63,14 +64,14 @@ cppp_status tk_pp_get_single(tk_ctx *ctx, int n, double *out);
 cppp_status tk_pp_update(tk_ctx *ctx, int n, double *Y_tilde);
 /* HOSVD initialization: A^(n) = the R_n leading left singular vectors of X_(n) from
  * the Gram matrix X_(n) X_(n)^T (sign: largest-magnitude entry positive, T2), core
- * G = X x_1 A^(1)T .. x_N A^(N)T.  Needs every s_n <= 128 (one-CTA Jacobi eigensolver); else
+ * G = X x_1 A^(1)T .. x_N A^(N)T.  Needs every s_n <= 128 (one-CTA eigensolver); else
  * CPPP_EINVAL (set the factors instead). */
 cppp_status tk_hosvd(tk_ctx *ctx);
 /* One sweep of PP-Tucker-ALS (Alg. 4; plain Alg. 2 when eps_pp = 0): regular sweeps
  * update A^(n) from the exact Y^(n) through the dimension tree (Gauss-Seidel order), PP sweeps
  * from Y~^(n) of the operators (built first in a pp-build sweep); the core G = Y^(N) x_N A^(N)T
  * from the last mode's Y (T1).  Every step on the device: TTMc GEMMs, the smaller Gram of Y_(n)
- * (s_n or prod of the other ranks; must be <= 128, else CPPP_EINVAL), Jacobi eigensolver,
+ * (s_n or prod of the other ranks; must be <= 128, else CPPP_EINVAL), top-R eigensolver,
  * selection and sign fix.  info may be NULL. */
 cppp_status tk_sweep(tk_ctx *ctx, double eps, double eps_pp, tk_sweep_info *info);
 /* Force the next sweeps' phase (CPPP_PHASE_AUTO to release), as cp_set_phase_override. */

@@ -381,7 +381,16 @@ cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, doubl
     const double flops = 2.0 * B * S * R * K;
     const double bytes = 8.0 * (B * S * R + B * R * K);
     const bool simt = (c->flags & CPPP_FLAG_SIMT_TTM) != 0;
-    if (ttm_uses_dmma(B, S, R, K, simt)) CUCHK(c, ttm_prepare(S, F, K, c->Fpad, st));
+    // factors live in the workspace (more buffers follow each), so the GEMM can read them in
+    // place; CPPP_PAD_FACTOR keeps the padded copy (A/B)
+    static const bool pad_env = getenv("CPPP_PAD_FACTOR") != nullptr;
+    if (ttm_uses_dmma(B, S, R, K, simt)) {
+      // (the side-stream GEMM keeps its pad kernel: it delays the GEMM's CTAs by a launch, and
+      // without it C2 ran 2% slower -- mode 1's factorization chain then dispatches later; a
+      // 3 us spacer kernel in its place measured the same as the pad)
+      if (!pad_env && topt.reserve_sms == 0 && ttm_direct_ok(F, K)) topt.direct_factor = true;
+      else CUCHK(c, ttm_prepare(S, F, K, c->Fpad, st));
+    }
     Prof p(c, CPPP_K_TTM, flops, bytes, st);
     CUCHK(c, launch_ttm_core(src.data, B, S, R, F, K, out, c->Fpad, simt, st, topt));
   } else {

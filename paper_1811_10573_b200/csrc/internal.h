@@ -85,7 +85,13 @@ cudaError_t launch_ttm_padded(const double* X, int64_t B, int64_t S, int64_t R, 
 struct TtmOpts {
   int reserve_sms = 0;
   int max_stages = 0;
+  // DMMA path: read the factor F (S x K, K even, 16-byte aligned) in place instead of the padded
+  // copy ttm_prepare makes; the last row's last box reads up to ttm_ld(K) - K doubles past
+  // F + S*K (only into discarded columns), so F must sit inside a larger allocation
+  bool direct_factor = false;
 };
+// whether launch_ttm_core can take F in place (TtmOpts::direct_factor)
+bool ttm_direct_ok(const double* F, int K);
 cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
                             int K, double* out, const double* Fpad, bool force_simt,
                             cudaStream_t st, TtmOpts topt = TtmOpts{});

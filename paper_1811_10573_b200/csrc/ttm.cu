@@ -570,9 +570,12 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
   }
   {
     // the padded factor [S][BNP] viewed as [BNP/16][S][16]: one box = every 16-column strip of
-    // a 16-deep k slice, landing as the strips' 16 x 16 boxes one after another
+    // a 16-deep k slice, landing as the strips' 16 x 16 boxes one after another.  In place
+    // (direct_factor) the row stride is K: columns >= K of a strip hold the next row's head,
+    // which only feeds output columns the epilogue drops
+    const int64_t ld = topt.direct_factor ? K : C::BNP;
     cuuint64_t dims[3] = {16, (cuuint64_t)S, (cuuint64_t)(C::BNP / 16)};
-    cuuint64_t str[2] = {(cuuint64_t)C::BNP * 8, 128};
+    cuuint64_t str[2] = {(cuuint64_t)ld * 8, 128};
     cuuint32_t box[3] = {16, 16, (cuuint32_t)(C::BNP / 16)};
     if (!make_map(&tmF, Fp, 3, dims, str, box)) return cudaErrorInvalidValue;
   }
@@ -704,6 +707,10 @@ bool ttm_uses_dmma(int64_t B, int64_t S, int64_t R, int K, bool force_simt) {
 }
 
 
+bool ttm_direct_ok(const double* F, int K) {
+  return F != nullptr && K % 2 == 0 && (reinterpret_cast<uintptr_t>(F) & 15) == 0;
+}
+
 // padded factor width for K: 16-column TMA boxes
 int ttm_ld(int K) { return ((((K + 7) / 8) * 8 + 15) / 16) * 16; }
 
@@ -770,7 +777,7 @@ cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, co
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(ctl);
   unsigned int* tickets = reinterpret_cast<unsigned int*>(ctl + 8);
   double* part = ctl + TTM_CTL;
-  const double* Fp = ctl + TTM_CTL + TTM_PART;
+  const double* Fp = topt.direct_factor ? F : ctl + TTM_CTL + TTM_PART;
   const int nt = (K + 7) / 8;
   if (R == 1)
     return dispatch_nt<false>(nt, X, B, S, R, Fp, K, out, counter, tickets, part, st, topt);

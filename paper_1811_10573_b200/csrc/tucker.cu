@@ -313,7 +313,6 @@ __global__ void __launch_bounds__(TOPR_THREADS, 1)
   long long t_[5];
   t_[0] = clock64();
   __shared__ double d[EIG_MAX], e[EIG_MAX], beta[EIG_MAX], pv[EIG_MAX], ev[EIG_MAX];
-  __shared__ double sh[32];
   const int tid = threadIdx.x, nt = blockDim.x, P = n + 1;
   for (int x = tid; x < n * n; x += nt) A[(x / n) * P + (x % n)] = Win[x];
   __syncthreads();
