@@ -152,12 +152,28 @@ struct Cfg {
 struct Unit {
   long long tile;
   int k0, k1, chunk;   // chunk = -1 for a whole tile
+  int nch;             // chunks of this tile
 };
 __device__ __forceinline__ Unit decode_unit(long long u, long long nfull, int nk, int ks) {
-  if (u < nfull) return Unit{u, 0, nk, -1};
+  if (u < nfull) return Unit{u, 0, nk, -1, 1};
   const long long v = u - nfull;
   const int c = static_cast<int>(v % ks);
-  return Unit{nfull + v / ks, nk * c / ks, nk * (c + 1) / ks, c};
+  return Unit{nfull + v / ks, nk * c / ks, nk * (c + 1) / ks, c, ks};
+}
+// Stream-K split (skG > 0 CTAs): the ntiles x nk k slices, in (tile, k) order, are cut into skG
+// equal ranges and CTA b runs range b, its pieces cut at tile boundaries; unit id = tile x skG +
+// b.  Chunk c of tile t is the c-th range touching it (ranges are non-empty: T >= skG).
+__device__ __forceinline__ long long sk_range_of(long long x, long long T, long long G) {
+  return ((x + 1) * G + T - 1) / T - 1;   // the last range starting at or before slice x
+}
+__device__ __forceinline__ Unit decode_sk(long long u, int nk, long long T, long long G) {
+  const long long t = u / G, b = u - t * G;
+  const long long lo = b * T / G, hi = (b + 1) * T / G, t0 = t * nk;
+  const long long fb = sk_range_of(t0, T, G), lb = sk_range_of(t0 + nk - 1, T, G);
+  const int nch = static_cast<int>(lb - fb + 1);
+  return Unit{t, static_cast<int>((lo > t0 ? lo : t0) - t0),
+              static_cast<int>((hi < t0 + nk ? hi : t0 + nk) - t0),
+              nch > 1 ? static_cast<int>(b - fb) : -1, nch};
 }
 
 template <int NT, bool MC, bool BATCH = false>
@@ -167,7 +183,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     double* __restrict__ out, int64_t Mrows, int64_t mtiles, int64_t nfull,
                     int64_t nsplit, int ks, int S, int K, int stages, int64_t Rflat,
                     unsigned long long* __restrict__ tile_counter, unsigned int* __restrict__ tickets,
-                    double* __restrict__ part, int box8, int64_t Rm) {
+                    double* __restrict__ part, int box8, int64_t Rm, int64_t skG) {
   using C = Cfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -189,7 +205,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   pdl_wait();   // X, the padded factor and the scheduler words come from earlier kernels
   const int nk = (S + BK - 1) / BK;
-  const long long nunits = nfull + static_cast<long long>(ks) * nsplit;
+  const long long nunits = skG ? nsplit * skG : nfull + static_cast<long long>(ks) * nsplit;
+  const long long skT = nsplit * nk;   // stream-K: slices in all
 
   if (warp == NWARP) {  // ---------------- TMA producer
     if (lane == 0) {
@@ -198,9 +215,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (box8) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX4)) : "memory");
       if constexpr (!BATCH) {
         int64_t it = 0;
+        long long sk_t = skG ? (blockIdx.x * skT / skG) / nk : 0;
+        const long long sk_hi = skG ? (blockIdx.x + 1) * skT / skG : 0;
         while (true) {
           // dynamic tile scheduler: robust to SMs that are busy with other streams' work
-          const long long unit = static_cast<long long>(atomicAdd(tile_counter, 1ull));
+          // (stream-K: this CTA's own pieces, in order)
+          long long unit;
+          if (skG) {
+            unit = sk_t * nk < sk_hi ? sk_t * skG + blockIdx.x : nunits;
+            ++sk_t;
+          } else {
+            unit = static_cast<long long>(atomicAdd(tile_counter, 1ull));
+          }
           if (unit >= nunits) {
             const int st = static_cast<int>(it % stages);
             const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
@@ -209,7 +235,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_arrive(smem_u32(&full[st]));   // wake the consumers with the sentinel
             break;
           }
-          const Unit un = decode_unit(unit, nfull, nk, ks);
+          const Unit un = skG ? decode_sk(unit, nk, skT, skG) : decode_unit(unit, nfull, nk, ks);
           const int64_t b = MC ? un.tile / mtiles : 0;
           const int64_t m0 = (un.tile - b * mtiles) * BM;
           // flattened rows: (batch, row) of the tile's first row, one division per unit
@@ -328,7 +354,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     const long long unit = stage_tile[static_cast<int>(it % stages)];
     if (unit < 0) break;
-    const Unit un = decode_unit(unit, nfull, nk, ks);
+    const Unit un = skG ? decode_sk(unit, nk, skT, skG) : decode_unit(unit, nfull, nk, ks);
     TTM_STAMP_START(unit);
     const int64_t b = MC ? un.tile / mtiles : 0;
     const int64_t m0 = (un.tile - b * mtiles) * BM;
@@ -399,7 +425,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       asm volatile("bar.sync 1, %0;" ::"r"(NWARP * 32) : "memory");   // consumer warps only
       if (threadIdx.x == 0) ticket_s = atomicAdd(tickets + v, 1u);
       asm volatile("bar.sync 1, %0;" ::"r"(NWARP * 32) : "memory");
-      if (ticket_s != ks - 1) {   // another chunk finishes the tile
+      if (ticket_s != un.nch - 1) {   // another chunk finishes the tile
         TTM_STAMP_END(unit);
         continue;
       }
@@ -410,7 +436,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         acc[j][0] = __ldcg(p0 + (2 * j) * (NWARP * 32));
         acc[j][1] = __ldcg(p0 + (2 * j + 1) * (NWARP * 32));
       }
-      for (int c = 1; c < ks; ++c) {
+      for (int c = 1; c < un.nch; ++c) {
         const double* pc = p0 + c * (NT * 2) * (NWARP * 32);
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
@@ -606,7 +632,7 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
   if (grid > ntiles) grid = ntiles;
   const int nk = static_cast<int>((S + BK - 1) / BK);
   const int64_t slot = static_cast<int64_t>(NT) * 2 * NWARP * 32;   // doubles per parked chunk
-  int64_t nsplit = 0;
+  int64_t nsplit = 0, skG = 0;
   int ks = 1;
   const double eff1 = [&] {
     const double w = static_cast<double>(ntiles) / full_grid;
@@ -628,7 +654,19 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
       if (eff >= 0.9) break;
     }
     ks = best;
-    if (ks > 1) {
+    // stream-K instead when the uniform split still leaves its last wave < 95% full: every
+    // CTA gets the same number of k slices (C3: ks = 7 left 553 units 3.7 waves deep, SMs
+    // ending between 279 and 380 us; stream-K 343-349 us).  C4's ks = 7 fills 99.3% and
+    // stays (stream-K measured 2.6% slower there)
+    static const bool no_sk = getenv("CPPP_NO_STREAMK") != nullptr;   // A/B
+    const int64_t T = ntiles * nk, per = T / full_grid;
+    const int ksmax = per > 0 ? static_cast<int>((nk + per - 1) / per) + 1 : 0;
+    if (!no_sk && ks > 1 && best_eff < 0.95 && per >= 8 && ntiles * ksmax * slot <= TTM_PART) {
+      skG = full_grid;
+      ks = ksmax;
+      nsplit = ntiles;
+      grid = full_grid;
+    } else if (ks > 1) {
       nsplit = ntiles;
       grid = full_grid < ntiles * ks ? full_grid : ntiles * ks;
     } else {
@@ -643,15 +681,15 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
       ks = 2;
     }
   }
-  const int64_t nfull = ntiles - nsplit;
+  const int64_t nfull = skG ? 0 : ntiles - nsplit;
   static const bool dbg = getenv("CPPP_DEBUG_TTM") != nullptr;
   if (dbg)
-    fprintf(stderr, "ttm B %lld S %lld R %lld K %d: tiles %lld grid %lld split %lld x %d\n",
+    fprintf(stderr, "ttm B %lld S %lld R %lld K %d: tiles %lld grid %lld split %lld x %d%s\n",
             (long long)B, (long long)S, (long long)R, K, (long long)ntiles, (long long)grid,
-            (long long)nsplit, ks);
+            (long long)nsplit, ks, skG ? " (stream-K)" : "");
   cudaError_t e = launch_pdl(ttm_dmma_kernel<NT, MC, BATCH>, dim3((unsigned)grid), dim3(NTHREADS), smem, st,
                              tmX, tmF, tmX4, out, Mrows, mtiles, nfull, nsplit, ks, (int)S, K, stages,
-                             Rflat, counter, tickets, part, box8, R);
+                             Rflat, counter, tickets, part, box8, R, skG);
   note_launch();
   return e;
 }

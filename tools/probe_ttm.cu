@@ -23,7 +23,6 @@ int main(int argc, char** argv) {
   const int64_t R = argc > 3 ? atoll(argv[3]) : 1;
   const int K = argc > 4 ? atoi(argv[4]) : 100;
   const int mc = R > 1;
-  const int64_t s = S;
   double *X, *F, *out, *scr, *o;
   cudaMalloc(&X, 8 * B * S * R);
   cudaMalloc(&F, 8 * S * K);
@@ -51,13 +50,14 @@ int main(int argc, char** argv) {
   unsigned long long t0 = ~0ull, t1 = 0;
   int nunits = 0;
   for (int u = 0; u < (1 << 16); ++u) {
-    if (tr[u][1] == 0) break;
+    if (tr[u][1] == 0) continue;   // stream-K unit ids are sparse
     t0 = std::min(t0, tr[u][1]);
     t1 = std::max(t1, tr[u][2]);
     ++nunits;
   }
   std::vector<double> per_sm_end(160, 0), per_sm_busy(160, 0), dur;
-  for (int u = 0; u < nunits; ++u) {
+  for (int u = 0; u < (1 << 16); ++u) {
+    if (tr[u][1] == 0) continue;
     const int sm = (int)tr[u][0];
     per_sm_end[sm] = std::max(per_sm_end[sm], (tr[u][2] - t0) * 1e-3);
     per_sm_busy[sm] += (tr[u][2] - tr[u][1]) * 1e-3;
