@@ -252,6 +252,32 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
 // lane c computes column c of inv(L_bb) right-looking with compile-time indices; Q[b][c][j] =
 // inv(L_bb)[j][c] with row pitch 33.  Rows past ld are the identity.  Exits unless the Cholesky
 // path was taken.
+// Ls = the block (1 / L[i][i] on the diagonal, L below it; pitch 33), Q = its output rows.
+// NB < 32: rows and columns >= NB of the block are the identity, so the substitution stops at
+// NB and column c >= NB of the inverse is e_c.
+template <int NB = 32>
+__device__ __forceinline__ void block_inverse_smem(double (*Ls)[33], double* Q) {
+  const int lane = threadIdx.x & 31, c = lane;
+  double y[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) y[j] = (j >= NB && j == c) ? 1.0 : 0.0;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) {
+    const double dinv = Ls[i][i];   // 1 / L[i][i]
+    y[i] = i == c ? dinv : (i > c ? -y[i] * dinv : 0.0);
+#pragma unroll
+    for (int j = i + 1; j < NB; ++j) y[j] = fma(Ls[j][i], y[i], y[j]);   // L[j][i]
+  }
+  // Q[c][j] = y_c[j]: staged row-wise in shared memory (the block is no longer needed), then
+  // written as 33-double rows by the whole warp (coalesced; lane-c row stores hit 32 sectors)
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) Ls[c][j] = y[j];
+  __syncwarp();
+#pragma unroll 4
+  for (int r = 0; r < 32; ++r) Q[r * 33 + lane] = Ls[r][lane];
+}
+
 __device__ __forceinline__ void block_inverse_dev(double* Tp, int ldt) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nblk = (ldt + 31) >> 5;
@@ -264,25 +290,7 @@ __device__ __forceinline__ void block_inverse_dev(double* Tp, int ldt) {
     Ls[wid][j][c] = (gj < ldt && gc < ldt) ? Tp[gj * ldt + gc] : (j == c ? 1.0 : 0.0);
   }
   __syncwarp();
-  double y[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) y[j] = 0.0;
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const double dinv = Ls[wid][i][i];   // 1 / L[i][i]
-    y[i] = i == c ? dinv : (i > c ? -y[i] * dinv : 0.0);
-#pragma unroll
-    for (int j = i + 1; j < 32; ++j) y[j] = fma(Ls[wid][j][i], y[i], y[j]);   // L[j][i]
-  }
-  // Q[c][j] = y_c[j]: staged row-wise in shared memory (the block is no longer needed), then
-  // written as 33-double rows by the whole warp (coalesced; lane-c row stores hit 32 sectors)
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 32; ++j) Ls[wid][c][j] = y[j];
-  __syncwarp();
-  double* Q = Tp + ldt * ldt + wid * 32 * 33;
-#pragma unroll 4
-  for (int r = 0; r < 32; ++r) Q[r * 33 + lane] = Ls[wid][r][lane];
+  block_inverse_smem(Ls[wid], Tp + ldt * ldt + wid * 32 * 33);
 }
 
 // Eigen pseudo-inverse fallback (L13): runs after gamma_chol_kernel and exits at once unless
@@ -294,7 +302,7 @@ __device__ __forceinline__ void gamma_pinv_dev(int K, const double* __restrict__
   __shared__ double sh[32];
   const int tid = threadIdx.x, KK = K * K;
   const int P = K + 1;
-  const int nt = GP_THREADS;
+  const int nt = blockDim.x;
   for (int e = tid; e < KK; e += nt) {
     const int i = e / K, j = e - i * K;
     W[i * P + j] = Gamma[i * ldt + j];
@@ -406,6 +414,115 @@ __global__ void __launch_bounds__(GP_THREADS, 1)
   } else {
     gamma_pinv_dev(K, Gamma, Tp, ldt, Vscratch);
   }
+}
+
+// K <= 32: the whole factorization in ONE warp, one launch (the chain above costs two launches
+// and ~570 cycles of barrier + shared-memory round trip per pivot: C4's K = 30 took 21 us).
+// Lane i keeps row i of W in registers; step j broadcasts row j by shuffles (W stays symmetric
+// in exact arithmetic, so row j stands in for column j) and lane i > j updates
+// W[i][k] -= (W[i][j] / d_j) W[j][k], k > j -- the same L13 pivot rule and output layout as
+// gamma_chol_kernel, then the inverse of the single diagonal block (block_inverse_dev).  A
+// failed pivot test runs the Jacobi pseudo-inverse, as gamma_post_kernel.
+// one warp: a shuffle inside a warp-uniform branch of a larger CTA still compiles to the
+// divergent-collective path (WARPSYNC/ENDCOLLECTIVE around every SHFL: 2x slower than the
+// two-kernel chain); the rare pseudo-inverse fallback then runs on 32 threads
+constexpr int GS_THREADS = 32;
+template <int KP>   // K <= KP (8, 16 or 32): every loop is unrolled to KP
+__global__ void __launch_bounds__(GS_THREADS, 1)
+    gamma_small_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
+                       double* Tp, int ldt, int* mode, double* Vscratch) {
+  PROBE_T0();
+  pdl_wait();
+  __shared__ int bad_s;
+  {
+    const int i = threadIdx.x;
+    const bool row_ok = i < K;
+    double w[KP];
+#pragma unroll
+    for (int k = 0; k < KP; ++k) w[k] = 1.0;   // 1.0 * S^(first) is exactly S^(first)
+    // two Grams per round, both rows loaded before either product (ascending m as before)
+    for (int m = 0; m < N; ++m) {
+      if (m == n) continue;
+      int m2 = m + 1;
+      if (m2 == n) ++m2;
+      const double* Sa = S_all + (int64_t)m * K * K + (int64_t)(row_ok ? i : 0) * K;
+      const double* Sb = S_all + (int64_t)(m2 < N ? m2 : m) * K * K + (int64_t)(row_ok ? i : 0) * K;
+      double a[KP], b[KP];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        a[k] = k < K ? __ldg(Sa + k) : 1.0;
+        b[k] = k < K && m2 < N ? __ldg(Sb + k) : 1.0;
+      }
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        w[k] *= a[k];
+        if (m2 < N) w[k] *= b[k];
+      }
+      m = m2;
+    }
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      if (!row_ok || k >= K) w[k] = 0.0;
+      else Gamma[i * ldt + k] = w[k];
+    }
+    double dmax = 0.0;
+#pragma unroll
+    for (int k = 0; k < KP; ++k)
+      if (k == i && row_ok) dmax = w[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    const double thresh = PIVOT_TAU * dmax;
+    PROBE_T(6);
+    // every shuffle unconditional (a shuffle under a runtime condition compiles to the
+    // divergent-collective path); steps j >= K only touch padding lanes and columns (their
+    // zero pivots turn them into inf/NaN there), rows and columns < K are exact
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < KP; ++j) {
+      const double d = __shfl_sync(0xffffffffu, w[j], j);
+      if (j < K && !(d > thresh)) bad = true;
+      const double cl = w[j] * pivot_rcp(d);
+#pragma unroll
+      for (int k = j + 1; k < KP; ++k) {
+        const double rjk = __shfl_sync(0xffffffffu, w[k], j);
+        if (i > j) w[k] = fma(-cl, rjk, w[k]);
+      }
+    }
+    PROBE_T(7);
+    if (!bad) {
+      // L[i][j] = W[i][j] / sqrt(d_j): row i of L into row i of Tp and column i (the mirror);
+      // d_j is lane j's W[j][j], untouched after step j: lane j forms 1 / sqrt(d_j) once
+      __shared__ double Ls[32][33];   // the block for the inverse, straight from registers
+      double own = 1.0;
+#pragma unroll
+      for (int k = 0; k < KP; ++k)
+        if (k == i) own = w[k];
+      const double rinv_own = row_ok ? 1.0 / sqrt(own) : 1.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {   // Ls is the full 32 x 32 block (identity past KP)
+        const double rinv = j < KP ? __shfl_sync(0xffffffffu, rinv_own, j) : 1.0;
+        double x = 0.0;
+        if (j < KP && j < K && row_ok && j < i) {
+          x = w[j] * rinv;
+          Tp[i * ldt + j] = x;
+          Tp[j * ldt + i] = x;
+        }
+        Ls[i][j] = j == i ? rinv_own : x;
+      }
+      if (row_ok) Tp[i * ldt + i] = rinv_own;
+      else if (i < ldt) Tp[i * ldt + i] = 1.0;   // unit diagonal of the padding
+      PROBE_T(8);
+      __syncwarp();
+      block_inverse_smem<KP>(Ls, Tp + ldt * ldt);
+      PROBE_T(9);
+    }
+    if (i == 0) {
+      bad_s = bad ? 1 : 0;
+      *mode = bad ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  if (bad_s) gamma_pinv_dev(K, Gamma, Tp, ldt, Vscratch);
 }
 
 // ---------------------------------------------------------------- row solves
@@ -832,6 +949,22 @@ cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 129 * 8);
     if (e != cudaSuccess) return e;
     attr = true;
+  }
+  static const bool no_small = getenv("CPPP_NO_SMALL_FACTOR") != nullptr;   // A/B
+  if (K <= 32 && !no_small) {
+    static bool small_attr = false;
+    if (!small_attr) {
+      for (auto f : {gamma_small_kernel<8>, gamma_small_kernel<16>, gamma_small_kernel<32>}) {
+        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 33 * 8);
+        if (e != cudaSuccess) return e;
+      }
+      small_attr = true;
+    }
+    auto f = K <= 8 ? gamma_small_kernel<8> : K <= 16 ? gamma_small_kernel<16> : gamma_small_kernel<32>;
+    cudaError_t e = launch_pdl(f, dim3(1), dim3(GS_THREADS), smem, st, S_all, N, n, K, Gamma, Tp, ldt,
+                               mode, Vscratch);
+    note_launch();
+    return e;
   }
   // K > 48: the mirrored halves of Γ and of the factor go out through shared-memory transposes
   // (coalesced rows); for small K the direct column stores are cheaper than the extra shared

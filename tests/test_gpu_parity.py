@@ -189,6 +189,30 @@ def test_singular_gamma_uses_pseudo_inverse():
         assert rel(got[n], st.A[n]) < 1e-8, n
 
 
+@pytest.mark.parametrize("K", [5, 16, 30, 40])
+def test_singular_gamma_each_factorization_kernel(K):
+    """The same L13 branch on every factorization kernel: the one-warp kernel at K <= 8, 16
+    and 32 (K = 5, 16, 30) and the CTA-wide Cholesky chain (K = 40); duplicate columns make Γ
+    singular, distinct ones keep it regular -- both sweeps against the oracle."""
+    dims = (48, 46, 44)
+    X, _ = random_problem(dims, K, 21)
+    r = np.random.default_rng(22)
+    for dup in (False, True):
+        A = [r.standard_normal((d, K)) for d in dims]
+        if dup:
+            for a in A:
+                a[:, 1] = a[:, 0]
+        st = O.State(X, [a.copy() for a in A])
+        st.dt_sweep()
+        ctx = cp.cp_init(X, 3, dims, K)
+        cp.cp_set_factors(ctx, A)
+        cp.cp_set_phase_override(ctx, "dt")
+        cp.als_sweep(ctx, 0.0, 0.1)
+        got = cp.cp_get_factors(ctx)
+        for n in range(3):
+            assert rel(got[n], st.A[n]) < 1e-8, (dup, n)
+
+
 @pytest.mark.parametrize("dims,K", [((160, 150, 140), 128), ((30, 28, 26, 24), 64)])
 def test_sweeps_large_rank(dims, K):
     X, _ = random_problem(dims, K, 5)

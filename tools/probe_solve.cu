@@ -90,6 +90,7 @@ int main(int argc, char** argv) {
         lerr = fmax(lerr, fabs(acc - Gh[i * ldt + j]) / Gh[i * ldt + i]);
         if (j < i) terr = fmax(terr, fabs(Tp[j * ldt + i] - Tp[i * ldt + j]));
       }
+    printf("small-factor cycles: hadamard %lld loop %lld tp %lld inverse %lld\n", cyc[6], cyc[7], cyc[8], cyc[9]);
     printf("K %d: LLt err %.3e, upper-vs-lower %.3e; cycles chol setup %lld total %lld; rows staged %lld subst %lld total %lld; gram loop %lld\n",
            K, lerr, terr, cyc[0], cyc[1], cyc[2], cyc[3], cyc[4], cyc[5]);
     std::vector<double> G(K * ldt);
