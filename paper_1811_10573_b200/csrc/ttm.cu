@@ -658,14 +658,18 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
     // CTA gets the same number of k slices (C3: ks = 7 left 553 units 3.7 waves deep, SMs
     // ending between 279 and 380 us; stream-K 343-349 us).  C4's ks = 7 fills 99.3% and
     // stays (stream-K measured 2.6% slower there)
+    // A static partition cannot absorb a CTA that waits for an SM (the side-stream Γ
+    // factorization is resident on some SM when the GEMM starts), so stream-K leaves two SMs
+    // free unless the caller already reserved some (C3 1029 -> 1048 sweeps/s)
     static const bool no_sk = getenv("CPPP_NO_STREAMK") != nullptr;   // A/B
-    const int64_t T = ntiles * nk, per = T / full_grid;
+    const int64_t G = std::max<int64_t>(1, full_grid - (topt.reserve_sms > 0 ? 0 : 2));
+    const int64_t T = ntiles * nk, per = T / G;
     const int ksmax = per > 0 ? static_cast<int>((nk + per - 1) / per) + 1 : 0;
     if (!no_sk && ks > 1 && best_eff < 0.95 && per >= 8 && ntiles * ksmax * slot <= TTM_PART) {
-      skG = full_grid;
+      skG = G;
       ks = ksmax;
       nsplit = ntiles;
-      grid = full_grid;
+      grid = G;
     } else if (ks > 1) {
       nsplit = ntiles;
       grid = full_grid < ntiles * ks ? full_grid : ntiles * ks;
