@@ -248,6 +248,7 @@ def test_multimode_first_level_matches_single_mode_chain(dims, K, krp):
     ((100, 190, 64), 8),       # 148 tiles + 1 -> tail split with NT = 1
     ((4, 4, 60, 64), 16),      # multi-mode GEMM, 1 tile, S = 3840: every tile in k chunks
     ((6, 6, 50, 50), 100),     # 1 tile of 36 rows, S = 2500, NT = 13
+    ((44, 44, 40, 30), 20),    # X_(01) GEMM: 10 tiles (ragged), 121 k slices -> stream-K ranges
 ])
 def test_ttm_split_units_match_oracle(dims, K):
     X, A = random_problem(dims, K, 12)
