@@ -52,6 +52,31 @@ __device__ double block_sum(double v, double* sh) {
   return r;
 }
 
+// NV block sums at once, each with block_sum's tree (same arithmetic, three barriers in all)
+template <int NV>
+__device__ void block_sum_n(double (&v)[NV], double* sh /* 32 NV */) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int c = 0; c < NV; ++c) v[c] = warp_sum(v[c]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < NV; ++c) sh[32 * c + w] = v[c];
+  }
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+      double r = lane < nw ? sh[32 * c + lane] : 0.0;
+      r = warp_sum(r);
+      if (lane == 0) sh[32 * c] = r;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < NV; ++c) v[c] = sh[32 * c];
+}
+
 constexpr double PIVOT_TAU = 1e-12;  // L13 / S:201
 
 // 1/d for the factorization's pivots: the hardware approximation (MUFU.RCP64H) refined by two
@@ -834,6 +859,28 @@ __global__ void __launch_bounds__(GR_THREADS)
     S[gj * K + gi] = s;
   }
   if (nrm == nullptr) return;
+  if (gridDim.x == 1) {
+    // one CTA (K <= 16, rows <= GR_ROWS: C1): no tickets, and the row statistics and the Σ Γ∘S
+    // term in one five-value block sum (the same per-value trees as below)
+    __shared__ double sh5[5 * 32];
+    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t y = tid; y < rows; y += GR_THREADS) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] += __ldcg(rowstat + y * 4 + c);
+    }
+    if (Gm != nullptr && ok) v[4] = Gm[gi * ldt + gj] * s;
+    block_sum_n<5>(v, sh5);
+    if (tid == 0) {
+      nrm[0] = v[0];
+      nrm[1] = v[1];
+      nrm[2] = v[2];
+      if (Gm != nullptr) {
+        fit[0] = v[3];
+        fit[1] = 0.0 + v[4];   // the tile-order sum over one tile
+      }
+    }
+    return;
+  }
   double* tilepart = scratch + (int64_t)GR_MAX_CTAS * GR_THREADS;
   if (Gm != nullptr) {
     double v = ok ? Gm[gi * ldt + gj] * s : 0.0;
@@ -850,14 +897,19 @@ __global__ void __launch_bounds__(GR_THREADS)
   __syncthreads();
   if (!last_s) return;
   __threadfence();
-  const int nst = Gm != nullptr ? 4 : 3;
-  for (int c = 0; c < nst; ++c) {
-    double v = 0.0;
-    for (int64_t y = tid; y < rows; y += GR_THREADS) v += __ldcg(rowstat + y * 4 + c);
-    v = block_sum(v, sh);
+  {   // the four row-statistic sums in one block reduction (block_sum's tree for each)
+    __shared__ double sh4[4 * 32];
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t y = tid; y < rows; y += GR_THREADS) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] += __ldcg(rowstat + y * 4 + c);
+    }
+    block_sum_n<4>(v, sh4);
     if (tid == 0) {
-      if (c < 3) nrm[c] = v;
-      else fit[0] = v;
+      nrm[0] = v[0];
+      nrm[1] = v[1];
+      nrm[2] = v[2];
+      if (Gm != nullptr) fit[0] = v[3];
     }
   }
   if (tid == 0) {
