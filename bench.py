@@ -112,6 +112,32 @@ def dist_env():
     return world, rank, local
 
 
+def config_dict(cfg, sweeps, world):
+    """The workload description both arms print (identical keys and values)."""
+    return {"workload": cfg.name, "N": cfg.N, "s": cfg.s, "K": cfg.K, "sweeps_per_step": sweeps,
+            "eps_pp": cfg.eps_pp, "family": cfg.family, "noise": [cfg.noise_kind, cfg.noise],
+            "parallelism": f"mode-0 slabs x{world}" if world > 1 else "single GPU",
+            "l2": l2_note(cfg)}
+
+
+L2_BYTES = 126 << 20   # B200 L2 (both dies)
+
+
+def l2_note(cfg):
+    mib = cfg.numel * 8 / 2**20
+    if cfg.numel * 8 > L2_BYTES:
+        return "inputs larger than L2 (X = %.0f MiB)" % mib
+    return "L2 flushed before every timed step (X = %.2f MiB < 126 MiB L2)" % mib
+
+
+def host_cores():
+    """Host cores this process may run on (what the oracle's BLAS and numpy can use)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def oracle_run(cfg, X, A0, sweeps):
     import oracle.cp_oracle as O
     t = time.perf_counter()
@@ -140,6 +166,72 @@ def oracle_sample(cfg, X, A0, sweeps, lo=10.0, hi=30.0):
     return el, done, phases, what + " (oracle/cp_oracle.py, numpy FP64 + BLAS)"
 
 
+def oracle_sample_slab(cfg, slabs, A0, phases):
+    """The bounded CPU sample for a tensor too large for the oracle's full run (C5, 32 GiB): the
+    oracle's own functions, as they stand, timed once per phase on slabs of r rows of one mode
+    (slabs[m]: rows [0, r) of mode m) and scaled by s/r where their work is proportional to the
+    tensor.  Each MTTKRP M^(n) and each PP operator M_p^(i,j) takes a slab of a mode it contracts
+    (so its Khatri-Rao factor, unfolding copy and product all shrink by r/s); the PP update and the
+    K x K solves run at full size.  sweeps/s = sweeps / Σ_phase count x time, with the GPU run's
+    phase mix."""
+    import oracle.cp_oracle as O
+    N, s = cfg.N, cfg.s
+    r = next(iter(slabs.values())).shape[min(slabs)]
+    scale = s / r
+    A = [a.copy() for a in A0]
+    S = [O.gram(a) for a in A]
+
+    def sl(m):
+        Am = list(A)
+        Am[m] = A[m][:r]
+        return slabs[m], Am
+
+    def solves():
+        t = time.perf_counter()
+        for n in range(N):
+            Gm = O.gamma(S, n)
+            An = O.solve_normal(np.ones((s, cfg.K)), Gm)
+            O.gradient(A[n], An, Gm)
+            O.gram(An)
+        return time.perf_counter() - t
+
+    t_mt = 0.0
+    for n in range(N):
+        X_m, A_m = sl(0 if n != 0 else 1)
+        t = time.perf_counter()
+        O.mttkrp(X_m, A_m, n)
+        t_mt += time.perf_counter() - t
+    t_dt = t_mt * scale + solves()
+    t_ops = 0.0
+    for i in range(N):
+        for j in range(i + 1, N):
+            m = min(x for x in range(N) if x not in (i, j))
+            X_m, A_m = sl(m)
+            t = time.perf_counter()
+            O.pp_operator(X_m, A_m, i, j)
+            t_ops += time.perf_counter() - t
+    t_ops *= scale
+    # full-size operators for the update (values irrelevant for the timing: same shapes)
+    full = {(i, j): np.ones((s, s, cfg.K)) for i in range(N) for j in range(i + 1, N)}
+    t = time.perf_counter()
+    Mp = [O.pp_single(full, A, n, N) for n in range(N)]
+    t_single = time.perf_counter() - t
+    dA = [0.01 * a for a in A]
+    t = time.perf_counter()
+    for n in range(N):
+        O.pp_update(Mp[n], full, dA, n)
+    t_pp = time.perf_counter() - t + solves()
+    del full
+    t_build = t_ops + t_single + t_pp
+    cnt = {ph: phases.count(ph) for ph in ("dt", "pp-build", "pp-approx")}
+    total = cnt["dt"] * t_dt + cnt["pp-build"] * t_build + cnt["pp-approx"] * t_pp
+    what = (f"oracle/cp_oracle.py functions timed once per phase on {r}-row slabs of the {cfg.name} tensor "
+            f"(each MTTKRP / PP operator on a slab of a mode it contracts, time x{scale:g}), PP update and "
+            f"solves at full size; per-sweep seconds dt {t_dt:.2f}, pp-build {t_build:.2f}, pp-approx "
+            f"{t_pp:.3f}; the GPU run's phase mix {cnt}")
+    return len(phases) / total, what, {"dt": t_dt, "pp-build": t_build, "pp-approx": t_pp}
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -164,19 +256,22 @@ def run_reference(args):
     for _ in range(args.warmup):
         oracle_run(cfg, X, A0, sweeps)
     total = 0.0
+    done = 0
     for _ in range(args.steps):
         dt, tr = oracle_run(cfg, X, A0, sweeps)
         total += dt
-    value = sweeps * args.steps / total
-    cores = blas_threads()
+        done += len(tr)
+    value = done / total
+    cores = host_cores()
     line = {
         "impl": "reference", "metric": "CP-ALS-PP sweeps/s", "value": value, "unit": "sweeps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded synthgen, host)",
-        "config": {"workload": cfg.name, "N": cfg.N, "s": cfg.s, "K": cfg.K, "sweeps": sweeps,
-                   "eps_pp": cfg.eps_pp},
-        "cpu_baseline": {"value": value, "unit": "sweeps/s", "cores": cores, "kind": "oracle",
+        "config": config_dict(cfg, sweeps, world),
+        "cpu_baseline": {"value": value, "unit": "sweeps/s", "cores": cores, "blas_threads": blas_threads(),
+                         "kind": "oracle",
                          "sample": f"the full {sweeps}-sweep {cfg.name} run per step (oracle/cp_oracle.py, numpy FP64)"},
         "e2e": {"value": value, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "phases": [t["phase"] for t in tr],
@@ -233,10 +328,22 @@ def main():
         obj = [cp.cppp_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+    # the bounded oracle sample of a tensor too large for a full oracle run (C5): a mode-0 slab
+    X_slab = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.numel > 2e8:
+        rows = 16
+        X_slab = {}
+        for m in range(3):   # rows [0, 16) of modes 0, 1, 2 (2 GiB each for C5)
+            shp = list(dims)
+            shp[m] = rows
+            v = X_dev.view(cfg.s ** m, cfg.s, -1)[:, :rows, :]
+            X_slab[m] = v.contiguous().cpu().numpy().reshape(shp)
     # timed pass: no profiling events inside the sweeps (they perturb a C2 step by ~8%)
     ctx = cp.cp_init(X_dev, cfg.N, dims, cfg.K, stream=stream, device=local, flags=cp.FLAG_BORROW_TENSOR,
                      nccl_unique_id=nccl_id, rank=rank, world=world, **shard)
     A0_dev = [torch.from_numpy(a).cuda() for a in A0]
+
+    l2_flush = cfg.numel * 8 <= L2_BYTES
 
     def step():   # one CP-ALS-PP run: als_run = every sweep in one device launch (Alg. 3 on device)
         cp.cp_set_factors(ctx, A0_dev)
@@ -251,24 +358,37 @@ def main():
     torch.cuda.synchronize()
     clk = Clocks(local)
     clk.start()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
+    # inputs smaller than L2 (C1): every timed step is preceded by an untimed L2 flush (a
+    # 512 MiB write); larger inputs stream through L2 anyway and the steps are timed back to back
+    flush = torch.empty(64 << 20, dtype=torch.float64, device="cuda") if l2_flush else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps if l2_flush else 1)]
+    sweeps_done = 0
+    if not l2_flush:
+        ev[0][0].record(stream)
+    for i in range(args.steps):
+        if l2_flush:
+            flush.zero_()
+            ev[i][0].record(stream)
         infos = step()
-    e1.record(stream)
+        sweeps_done += len(infos)
+        if l2_flush:
+            ev[i][1].record(stream)
+    if not l2_flush:
+        ev[0][1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clocks = clk.stop()
-    ms = e0.elapsed_time(e1)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    del flush
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     launches = (cp.cppp_launch_count() - launches0) / max(args.steps, 1)
-    value = sweeps * args.steps / (ms * 1e-3)
-    phases = [i["phase"] for i in infos]
+    value = sweeps_done / (ms * 1e-3)   # the sweeps als_run actually ran (it may stop early)
+    gpu_phases = [i["phase"] for i in infos]
 
     # profiled pass: the same K steps again on a context with per-kernel-class CUDA events on the
     # launching streams (the library's own stream, which is torch's current stream, and the
@@ -369,12 +489,18 @@ def main():
         from concurrent.futures import ThreadPoolExecutor
         pool = ThreadPoolExecutor(max_workers=1)
         pair = []
+        cp.cp_destroy(ctx)   # the profiled context is not used for the end-to-end timing
         if world == 1:
-            cp.cp_destroy(ctx)   # two contexts (C5: 2 x 49 GB) need the room
-            del X_dev
+            del X_dev   # two contexts (C5: 2 x 49 GB) need the room
             torch.cuda.empty_cache()
             pair = [cp.cp_init(Xh, cfg.N, dims, cfg.K, stream=torch.cuda.Stream(), device=local)
                     for _ in range(2)]
+        else:
+            obj = [cp.cppp_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            ctx = cp.cp_init(X_dev, cfg.N, dims, cfg.K, stream=stream, device=local,
+                             flags=cp.FLAG_BORROW_TENSOR, nccl_unique_id=obj[0], rank=rank,
+                             world=world, **shard)
 
         def load(i):   # the step's inputs: tensor + initial factors, from pinned host memory
             torch.cuda.set_device(local)
@@ -382,10 +508,12 @@ def main():
             cp.cp_set_factors(pair[i % 2], A0h)
             return pair[i % 2]
 
+        e2e_sweeps = [0]
+
         def run(c2, set_factors=False):
             if set_factors:
                 cp.cp_set_factors(c2, A0h)
-            cp.als_run(c2, 0.0, cfg.eps_pp, sweeps)
+            e2e_sweeps[0] += len(cp.als_run(c2, 0.0, cfg.eps_pp, sweeps))
             cp.cp_get_factors(c2, out=outh)
             return cp.fitness(c2)
 
@@ -409,6 +537,7 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        e2e_sweeps[0] = 0
         t0 = time.perf_counter()
         e2e_run(args.steps)
         torch.cuda.synchronize()
@@ -421,16 +550,23 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         h2d = local_numel * 8 + sum(a.nbytes for a in A0)
-        e2e = {"value": sweeps * args.steps / dt, "unit": "sweeps/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": e2e_sweeps[0] / dt, "unit": "sweeps/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(sum(a.nbytes for a in A0) + 8)}
 
     # ---- CPU baseline: the oracle on the same workload (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg.numel <= 2e8:
         Xo = G.make_tensor(cfg)
-        dt, done, phases, what = oracle_sample(cfg, Xo, A0, sweeps)
-        cpu = {"value": done / dt, "unit": "sweeps/s", "cores": blas_threads(), "kind": "oracle",
-               "sample": what, "seconds": dt, "phases": phases}
+        dt, done, or_phases, what = oracle_sample(cfg, Xo, A0, sweeps)
+        cpu = {"value": done / dt, "unit": "sweeps/s", "cores": host_cores(), "blas_threads": blas_threads(),
+               "kind": "oracle", "sample": what, "seconds": dt, "phases": or_phases}
+    elif X_slab is not None:
+        t0 = time.perf_counter()
+        v, what, per = oracle_sample_slab(cfg, X_slab, A0, gpu_phases)
+        cpu = {"value": v, "unit": "sweeps/s", "cores": host_cores(), "blas_threads": blas_threads(),
+               "kind": "oracle", "sample": what, "seconds": time.perf_counter() - t0,
+               "seconds_per_sweep": per}
+        del X_slab
 
     if rank == 0:
         line = {
@@ -438,11 +574,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded on-device generator, twin of synthgen)",
-            "config": {"workload": cfg.name, "N": cfg.N, "s": cfg.s, "K": cfg.K, "sweeps_per_step": sweeps,
-                       "eps_pp": cfg.eps_pp, "family": cfg.family, "noise": [cfg.noise_kind, cfg.noise],
-                       "parallelism": f"mode-0 slabs x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (X = %.0f MiB)" % (cfg.numel * 8 / 2**20)},
-            "phases": phases, "final_fitness": infos[-1]["fitness"],
+            "config": config_dict(cfg, sweeps, world),
+            "phases": gpu_phases, "sweeps_per_step": sweeps_done / max(args.steps, 1),
+            "final_fitness": infos[-1]["fitness"], "final_fitness_approximate": infos[-1]["approximate"],
             "roofline": roofline, "roofline_all": roof_all, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
             "profiled_ms_per_step": prof_ms / args.steps,

@@ -104,6 +104,10 @@ typedef struct {
   int restarts;              /* number of PP operator builds so far */
   int converged;             /* grad_norm_sum <= eps */
   double seconds;            /* device time of this sweep (CUDA events) */
+  int approximate;           /* 1 when fitness/residual_sq come from the PP-approximated M~^(N)
+                                (a PP sweep): then r² is only O(ε²)-accurate and may be
+                                negative (clamped in fitness, L17/L27); fitness_exact() gives the
+                                exact value.  0 after a regular sweep (exact M^(N)). */
 } cppp_sweep_info;
 
 /* Kernel classes for cppp_kernel_stats. */
@@ -203,8 +207,15 @@ cppp_status als_run(cppp_ctx *ctx, double eps, double eps_pp, int max_sweeps,
  * oracle's phase schedule in parity runs (L12). */
 cppp_status cp_set_phase_override(cppp_ctx *ctx, int phase);
 
-/* Fitness of the last sweep (L17): 1 - sqrt(max(0, r²))/||X||, r² by the S:177 expansion. */
+/* Fitness of the last sweep (L17): 1 - sqrt(max(0, r²))/||X||, r² by the S:177 expansion with
+ * that sweep's last M^(N) (approximate after a PP sweep: see cppp_sweep_info.approximate). */
 cppp_status fitness(cppp_ctx *ctx, double *f);
+/* Exact fitness at the CURRENT factors (L17): one exact MTTKRP pass through the dimension
+ * tree (the cost of a regular sweep without the solves; M^(n) buffers are overwritten, factors,
+ * operators and the phase state are not), then r² = ||X||² - 2<M^(N), A^(N)> + 1ᵀ(Γ^(N)∗S^(N))1
+ * on the device.  f (may be NULL) = 1 - sqrt(max(0, r²))/||X||; residual_sq (may be NULL) = r²
+ * unclamped.  Host outputs; synchronizes.  CPPP_ESTATE before cp_set_factors. */
+cppp_status fitness_exact(cppp_ctx *ctx, double *f, double *residual_sq);
 
 /* Per-kernel-class statistics since the last reset (CPPP_FLAG_PROFILE only). */
 cppp_status cppp_kernel_stats(cppp_ctx *ctx, int kclass, cppp_kernel_stat *out);

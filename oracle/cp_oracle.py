@@ -334,6 +334,11 @@ class State:
         """‖dA^(i)‖_F / ‖A^(i)‖_F with the current A (L7)."""
         return [float(np.linalg.norm(d) / np.linalg.norm(a)) for d, a in zip(self.dA, self.A)]
 
+    def residual_sq(self) -> float:
+        """The unclamped radicand r² of the S:177 expansion with the last computed M^(N) (L17,
+        L27): exact ‖X − [[A]]‖² after a regular sweep, O(ε²)-approximate after a PP sweep."""
+        return residual_sq_expansion(self.normX_sq, self.M_last, self.A[-1], self.Gamma_last, self.S[-1])
+
     def fitness(self) -> float:
         return fitness_from(self.normX_sq, self.M_last, self.A[-1], self.Gamma_last, self.S[-1])
 
@@ -382,8 +387,9 @@ def pp_cp_als(X, A0, eps: float, eps_pp: float, max_sweeps: int,
         else:
             next_phase = "pp-approx" if small else "dt"
         gsum = float(sum(st.G_norms))
-        trace.append(dict(sweep=sw + 1, phase=phase, fitness=st.fitness(), grad_norm_sum=gsum,
-                          max_rel_dA=max(rel), margin=abs(max(rel) - eps_pp)))
+        trace.append(dict(sweep=sw + 1, phase=phase, fitness=st.fitness(), residual_sq=st.residual_sq(),
+                          grad_norm_sum=gsum, max_rel_dA=max(rel), margin=abs(max(rel) - eps_pp),
+                          normX_sq=st.normX_sq))
         if gsum <= eps:
             break
         if deadline is not None and time.perf_counter() >= deadline:

@@ -11,9 +11,10 @@ SOURCES = ["engine.cu", "ttm.cu", "ttv.cu", "ppupdate.cu", "solve.cu", "gen.cu",
 HEADERS = ["internal.h", os.path.join("..", "..", "include", "cppp.h"),
            os.path.join("..", "..", "include", "cppp_tucker.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-gencode", "arch=compute_100a,code=sm_100a", "-I", os.path.join(ROOT, "include"),
          "-Xptxas", "-warn-spills"]
+OBJDIR = os.path.join(HERE, "build_obj")
 
 
 def _stale() -> bool:
@@ -27,8 +28,22 @@ def _stale() -> bool:
 def build_library(force: bool = False, verbose: bool = True) -> str:
     if not force and not _stale():
         return LIB
+    # one nvcc per translation unit, in parallel (no relocatable device code: the units call
+    # each other only through host-side launchers), then one shared-library link
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJDIR, exist_ok=True)
+    objs = [os.path.join(OBJDIR, os.path.splitext(s)[0] + ".o") for s in SOURCES]
+
+    def compile_one(i):
+        cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, SOURCES[i]), "-o", objs[i]]
+        if verbose:
+            print("[cppp build]", " ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True, cwd=CSRC)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        list(ex.map(compile_one, range(len(SOURCES))))
     tmp = LIB + ".tmp"
-    cmd = [NVCC] + FLAGS + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", tmp, "-ldl"]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a"] + objs + ["-o", tmp, "-ldl"]
     if verbose:
         print("[cppp build]", " ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)

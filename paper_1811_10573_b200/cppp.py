@@ -65,10 +65,11 @@ class SweepInfo(C.Structure):
     _fields_ = [("sweep", C.c_int), ("phase", C.c_int), ("fitness", C.c_double),
                 ("residual_sq", C.c_double), ("grad_norm_sum", C.c_double),
                 ("max_rel_dA", C.c_double), ("next_phase", C.c_int), ("restarts", C.c_int),
-                ("converged", C.c_int), ("seconds", C.c_double)]
+                ("converged", C.c_int), ("seconds", C.c_double), ("approximate", C.c_int)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["approximate"] = bool(self.approximate)
         d["phase"] = PHASE_NAMES.get(self.phase, str(self.phase))
         d["next_phase"] = PHASE_NAMES.get(self.next_phase, str(self.next_phase))
         return d
@@ -109,6 +110,7 @@ def lib():
         "als_run": (I, [P, D, D, I, C.POINTER(SweepInfo), C.POINTER(I)]),
         "cp_set_phase_override": (I, [P, I]),
         "fitness": (I, [P, C.POINTER(D)]),
+        "fitness_exact": (I, [P, C.POINTER(D), C.POINTER(D)]),
         "cppp_kernel_stats": (I, [P, I, C.POINTER(KernelStat)]),
         "cppp_reset_kernel_stats": (I, [P]),
         "cppp_generate": (I, [P, P, I, C.POINTER(C.c_int64), I, C.POINTER(P), I, D, C.c_uint64,
@@ -148,7 +150,7 @@ EXPORTED = ["cppp_default_opts", "cppp_workspace_bytes", "cp_init", "cp_load_ten
             "cp_update_factors",
             "cp_get_factors", "mttkrp_dt", "pp_build_operators", "pp_get_operator",
             "pp_get_single", "pp_update", "pp_error", "als_sweep", "als_run", "cp_set_phase_override", "fitness",
-            "cppp_kernel_stats", "cppp_reset_kernel_stats", "cppp_generate",
+            "fitness_exact", "cppp_kernel_stats", "cppp_reset_kernel_stats", "cppp_generate",
             "cppp_nccl_unique_id", "cppp_plan_describe", "cp_destroy", "cp_last_error",
             "cppp_status_string", "cppp_version", "cppp_launch_count",
             "tk_init", "tk_set_factors", "tk_update_factors", "tk_ttmc", "tk_pp_build",
@@ -344,6 +346,14 @@ def fitness(ctx: Ctx) -> float:
     f = C.c_double()
     _check(ctx, lib().fitness(ctx.h, C.byref(f)))
     return f.value
+
+
+def fitness_exact(ctx: Ctx):
+    """fitness_exact (include/cppp.h): (fitness, unclamped r²) at the current factors from one
+    exact MTTKRP pass."""
+    f, r2 = C.c_double(), C.c_double()
+    _check(ctx, lib().fitness_exact(ctx.h, C.byref(f), C.byref(r2)))
+    return f.value, r2.value
 
 
 def kernel_stats(ctx: Ctx) -> dict:

@@ -83,7 +83,57 @@ __global__ void pp_error_final_kernel(const double* __restrict__ msum, const dou
   bound[idx] = tot == 0.0 ? 0.0 : (mn > 0.0 ? normX * tot / mn : CUDART_INF);
 }
 
+// The two data terms of the S:177 expansion for mode n (one CTA, fixed order):
+//   fit[0] = Σ_y Σ_k M[y][k] A[y][k]                (rows in thread-strided order, k ascending)
+//   fit[1] = Σ_{i,j} Γ^(n)[i][j] S^(n)[i][j],  Γ^(n) = Hadamard of S^(m), m != n ascending
+// Per-thread partials are added by a fixed binary tree.
+constexpr int FT_THREADS = 256;
+__global__ void __launch_bounds__(FT_THREADS)
+    fit_terms_kernel(const double* __restrict__ M, const double* __restrict__ A, int64_t rows, int K,
+                     const double* __restrict__ S_all, int N, int n, double* __restrict__ fit) {
+  __shared__ double red[2][FT_THREADS];
+  double inner = 0.0, model = 0.0;
+  for (int64_t y = threadIdx.x; y < rows; y += FT_THREADS) {
+    double r = 0.0;
+    for (int k = 0; k < K; ++k) r = fma(M[y * K + k], A[y * K + k], r);
+    inner += r;
+  }
+  const int KK = K * K;
+  for (int e = threadIdx.x; e < KK; e += FT_THREADS) {
+    double g = 1.0;
+    bool first = true;
+    for (int m = 0; m < N; ++m) {
+      if (m == n) continue;
+      const double v = S_all[static_cast<int64_t>(m) * KK + e];
+      g = first ? v : g * v;
+      first = false;
+    }
+    model = fma(g, S_all[static_cast<int64_t>(n) * KK + e], model);
+  }
+  red[0][threadIdx.x] = inner;
+  red[1][threadIdx.x] = model;
+  __syncthreads();
+  for (int w = FT_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + w];
+      red[1][threadIdx.x] += red[1][threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    fit[0] = red[0][0];
+    fit[1] = red[1][0];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_fit_terms(const double* M, const double* A, int64_t rows, int K,
+                             const double* S_all, int N, int n, double* fit, cudaStream_t st) {
+  fit_terms_kernel<<<1, FT_THREADS, 0, st>>>(M, A, rows, K, S_all, N, n, fit);
+  note_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_colsq(const double* a, const double* b, int64_t rows, int K, double* sums,
                          cudaStream_t st) {

@@ -1149,9 +1149,13 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   size_t oX = borrow ? 0 : take(sizeof(double) * c->numel_local);
   size_t oA[CPPP_MAX_ORDER], oAp[CPPP_MAX_ORDER], odA[CPPP_MAX_ORDER], oM[CPPP_MAX_ORDER],
       oMp[CPPP_MAX_ORDER], oT[CPPP_MAX_ORDER];
+  // A and A_p feed the first-level GEMM in place (TtmOpts::direct_factor): its TMA view of the
+  // last row reads up to ttm_ld(K) - K doubles past the factor (into columns the epilogue drops),
+  // so each of them owns that much slack
+  const size_t fac_slack = sizeof(double) * (size_t)ttm_ld(K);
   for (int n = 0; n < N; ++n) {
-    oA[n] = take(sizeof(double) * c->s[n] * K);
-    oAp[n] = take(sizeof(double) * c->s[n] * K);
+    oA[n] = take(sizeof(double) * c->s[n] * K + fac_slack);
+    oAp[n] = take(sizeof(double) * c->s[n] * K + fac_slack);
     odA[n] = take(sizeof(double) * c->s[n] * K);
     oM[n] = take(sizeof(double) * c->dl[n] * K);
     oMp[n] = take(sizeof(double) * c->dl[n] * K);
@@ -1511,6 +1515,11 @@ cppp_status cp_update_factors(cppp_ctx* c, const double* const* A) {
                          c->st));
     if (n == c->q) STCHK(allreduce(c, c->S_all + (int64_t)n * c->K * c->K, (size_t)c->K * c->K));
   }
+  // with operators in place the PP state moves with the factors: dA = A - A_p, so a
+  // following PP sweep (which reads dA^(i) of the modes it has not updated yet) sees the new A
+  if (c->ops_valid)
+    for (int n = 0; n < c->N; ++n)
+      CUCHK(c, launch_sub(c->A[n], c->Ap[n], c->dA[n], c->s[n] * c->K, c->st));
   CUCHK(c, cudaEventRecord(c->ev_S, c->st));
   CUCHK(c, cudaStreamSynchronize(c->st));
   c->op12_fresh = false;
@@ -1696,6 +1705,7 @@ cppp_status als_sweep(cppp_ctx* c, double eps, double eps_pp, cppp_sweep_info* i
     info->restarts = c->restarts;
     info->converged = gsum <= eps;
     info->seconds = ms * 1e-3;
+    info->approximate = phase != CPPP_PHASE_DT;
   }
   return CPPP_OK;
 }
@@ -1778,6 +1788,7 @@ cppp_status als_run(cppp_ctx* c, double eps, double eps_pp, int max_sweeps, cppp
       o.restarts = r.restarts;
       o.converged = r.converged;
       o.seconds = ms * 1e-3 / n;   // the run is one launch: its device time, shared evenly
+      o.approximate = r.phase != CPPP_PHASE_DT;
     }
   }
   note_launches(1);   // the prologue
@@ -1793,6 +1804,24 @@ cppp_status fitness(cppp_ctx* c, double* f) {
   if (!f) return fail(c, CPPP_EINVAL, "null output");
   if (c->sweep == 0) return fail(c, CPPP_ESTATE, "fitness before any sweep");
   *f = c->last_fitness;
+  return CPPP_OK;
+}
+
+cppp_status fitness_exact(cppp_ctx* c, double* f, double* residual_sq) {
+  if (!c) return CPPP_EINVAL;
+  if (!c->factors_set) return fail(c, CPPP_ESTATE, "fitness_exact before cp_set_factors");
+  const int N = c->N, K = c->K, n = N - 1;
+  STCHK(run_dt(c, false, c->M));   // exact M^(n) at the current factors (no factor update)
+  double* fit = c->stats + 3 * N + 4;
+  const int64_t off = (n == c->q) ? c->qoff : 0;
+  CUCHK(c, launch_fit_terms(c->M[n], c->A[n] + off * K, c->dl[n], K, c->S_all, N, n, fit, c->st));
+  if (n == c->q) STCHK(allreduce(c, fit, 1));   // the slab mode's rows are local
+  CUCHK(c, cudaMemcpyAsync(c->host_stats, fit, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  prof_collect(c);
+  const double r2 = c->normX_sq - 2.0 * c->host_stats[0] + c->host_stats[1];
+  if (residual_sq) *residual_sq = r2;
+  if (f) *f = 1.0 - std::sqrt(std::max(0.0, r2)) / std::sqrt(c->normX_sq);
   return CPPP_OK;
 }
 

@@ -92,6 +92,8 @@ struct TtmOpts {
 };
 // whether launch_ttm_core can take F in place (TtmOpts::direct_factor)
 bool ttm_direct_ok(const double* F, int K);
+// padded column count of the GEMM's factor tiles (a multiple of 16 >= K)
+int ttm_ld(int K);
 cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
                             int K, double* out, const double* Fpad, bool force_simt,
                             cudaStream_t st, TtmOpts topt = TtmOpts{});
@@ -172,6 +174,9 @@ cudaError_t launch_colsq(const double* a, const double* b, int64_t rows, int K, 
 cudaError_t launch_pp_error_final(const double* msum, const double* asum, int N, int K,
                                   double normX, double* err, double* eps, double* bound,
                                   cudaStream_t st);
+// fit[0] = Σ M∘A over rows x K, fit[1] = Σ (Hadamard_{m≠n} S^(m)) ∘ S^(n) (S:177 terms; one CTA)
+cudaError_t launch_fit_terms(const double* M, const double* A, int64_t rows, int K,
+                             const double* S_all, int N, int n, double* fit, cudaStream_t st);
 // Fp[x][n] = F[x][n] for n < K, 0 for K <= n < ld (TMA-aligned copy of a factor)
 cudaError_t launch_pad_rows(const double* F, int64_t S, int K, double* Fp, int ld, cudaStream_t st);
 

@@ -9,6 +9,7 @@ import pytest
 
 import oracle.cp_oracle as O
 import synthgen as G
+from trace_check import check, conditioning, golden
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -115,20 +116,47 @@ def test_pp_update_matches_oracle(name):
 @pytest.mark.parametrize("name,sweeps", [("C1", 20), ("C2mini", 20), ("C3mini", 20), ("C4mini", 20),
                                          ("C5mini", 20), ("LAPmini", 20)])
 def test_sweep_trace_matches_oracle(name, sweeps):
+    """Every sweep of the replayed 20-sweep trace (tests/trace_check.py): fitness (north_star
+    1e-8), the unclamped r², Σ‖G‖, max ‖dA‖/‖A‖ and the final factors -- including the PP sweeps
+    whose radicand is negative (fitness clamped)."""
     cfg, X, A0 = problem(name)
-    _, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, sweeps)
+    A_or, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, sweeps)
+    cond = golden(name, X, A0, cfg.eps_pp, tr, A_or)
     ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
     cp.cp_set_factors(ctx, A0)
-    phases = []
+    infos = []
+    for t in tr:
+        cp.cp_set_phase_override(ctx, t["phase"])
+        infos.append(cp.als_sweep(ctx, 0.0, cfg.eps_pp))
+    check(tr, infos, cond, A_or, cp.cp_get_factors(ctx), tag=name)
+    assert any(i["phase"] != "dt" for i in infos) or cfg.name in ("C4mini", "LAPmini")
+    cp.cp_destroy(ctx)
+
+
+def test_fitness_exact_matches_explicit_residual():
+    """fitness_exact: one exact MTTKRP at the current factors (L17); after a PP sweep it differs
+    from the sweep's approximate value and equals the oracle's explicit ‖X − [[A]]‖."""
+    cfg, X, A0 = problem("C2mini")
+    _, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, 20)
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    cp.cp_set_factors(ctx, A0)
+    nx2 = float(np.sum(X * X))
+    seen_pp = False
     for t in tr:
         cp.cp_set_phase_override(ctx, t["phase"])
         info = cp.als_sweep(ctx, 0.0, cfg.eps_pp)
-        phases.append(info["phase"])
-        rho = 1.0 - t["fitness"]
-        if rho >= 1e-6:
-            assert abs(info["fitness"] - t["fitness"]) < 1e-8, (name, t, info)
-        assert info["phase"] == t["phase"]
-    assert any(p != "dt" for p in phases) or cfg.name in ("C4mini", "LAPmini")
+        f, r2 = cp.fitness_exact(ctx)
+        A = cp.cp_get_factors(ctx)
+        explicit = float(np.sum((X - O.kruskal_full(A)) ** 2))
+        assert abs(r2 - explicit) <= 1e-11 * nx2, (t["sweep"], r2, explicit)
+        assert abs(f - (1 - np.sqrt(max(explicit, 0.0) / nx2))) < 1e-9
+        if t["phase"] == "dt":
+            assert info["approximate"] is False and abs(info["residual_sq"] - r2) <= 1e-11 * nx2
+        else:
+            assert info["approximate"] is True
+            seen_pp = True
+    assert seen_pp
+    cp.cp_destroy(ctx)
 
 
 def test_free_running_phase_machine_matches_oracle_schedule():
@@ -218,13 +246,15 @@ def test_sweeps_large_rank(dims, K):
     X, _ = random_problem(dims, K, 5)
     r = np.random.default_rng(6)
     A0 = [r.random((d, K)) for d in dims]
-    _, tr = O.pp_cp_als(X, A0, 0.0, 0.5, 6)
+    A_or, tr = O.pp_cp_als(X, A0, 0.0, 0.5, 6)
+    cond = conditioning(X, A0, 0.5, 6, tr, A_or)
     ctx = cp.cp_init(X, len(dims), dims, K)
     cp.cp_set_factors(ctx, A0)
+    infos = []
     for t in tr:
         cp.cp_set_phase_override(ctx, t["phase"])
-        info = cp.als_sweep(ctx, 0.0, 0.5)
-        assert abs(info["fitness"] - t["fitness"]) < 1e-8, (t, info)
+        infos.append(cp.als_sweep(ctx, 0.0, 0.5))
+    check(tr, infos, cond, A_or, cp.cp_get_factors(ctx), tag=str(dims))
 
 
 # ---- scheduling paths of the GEMM / TTV kernels: each shape is chosen to hit one
@@ -293,11 +323,13 @@ def test_load_tensor_replaces_the_tensor():
         for n in range(cfg.N):
             assert rel(M[n], O.mttkrp(X2, A0, n)) < TOL, n
         cp.cp_set_factors(ctx, A0)
-        _, tr = O.pp_cp_als(X2, A0, 0.0, cfg.eps_pp, 8)
+        A_or, tr = O.pp_cp_als(X2, A0, 0.0, cfg.eps_pp, 8)
+        cond = conditioning(X2, A0, cfg.eps_pp, 8, tr, A_or)
+        infos = []
         for t in tr:
             cp.cp_set_phase_override(ctx, t["phase"])
-            info = cp.als_sweep(ctx, 0.0, cfg.eps_pp)
-            assert abs(info["fitness"] - t["fitness"]) < 1e-8, (t, info)
+            infos.append(cp.als_sweep(ctx, 0.0, cfg.eps_pp))
+        check(tr, infos, cond, A_or, cp.cp_get_factors(ctx), tag="load_tensor")
     b = cp.cp_init(torch.from_numpy(X1.ravel().copy()).cuda(), cfg.N, cfg.dims, cfg.K,
                    flags=cp.FLAG_BORROW_TENSOR)
     with pytest.raises(cp.CpppError):
@@ -478,13 +510,14 @@ def test_edge_shapes(dims, K):
     Mp = [O.pp_single(ops, A, n, N) for n in range(N)]
     for n in range(N):
         assert rel(cp.pp_update(ctx, n), O.pp_update(Mp[n], ops, dA, n)) < TOL, n
-    _, tr = O.pp_cp_als(X, A, 0.0, 0.1, 6)
+    A_or, tr = O.pp_cp_als(X, A, 0.0, 0.1, 6)
+    cond = conditioning(X, A, 0.1, 6, tr, A_or)
     cp.cp_set_factors(ctx, A)
+    infos = []
     for t in tr:
         cp.cp_set_phase_override(ctx, t["phase"])
-        info = cp.als_sweep(ctx, 0.0, 0.1)
-        if 1.0 - t["fitness"] >= 1e-6:
-            assert abs(info["fitness"] - t["fitness"]) < 1e-8, (t, info)
+        infos.append(cp.als_sweep(ctx, 0.0, 0.1))
+    check(tr, infos, cond, A_or, cp.cp_get_factors(ctx), tag=str(dims))
     cp.cp_destroy(ctx)
 
 
@@ -495,3 +528,25 @@ def test_empty_and_oversized_inputs_rejected():
     X = np.zeros((2,) * 9)
     with pytest.raises(cp.CpppError):
         cp.cp_init(X, 9, (2,) * 9, 2)
+
+
+@pytest.mark.parametrize("name", ["C2mini", "C3mini", "C5mini"])
+def test_dataflow_factorization_bit_identical(name):
+    """The dataflow Γ factorization (32 < K <= 128, default) applies the same operations to every
+    element in the same order as the barrier-per-pivot kernel it replaced (CPPP_OLD_CHOL=1): the
+    sweeps and the factors must agree bit for bit (separate processes: the switch is read once)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for old in (False, True):
+        env = dict(os.environ)
+        env.pop("CPPP_OLD_CHOL", None)
+        if old:
+            env["CPPP_OLD_CHOL"] = "1"
+        r = subprocess.run([sys.executable, os.path.join(root, "tools", "trace_bits.py"), name, "12"],
+                           env=env, capture_output=True, text=True, timeout=600, check=True)
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]

@@ -10,6 +10,7 @@ import pytest
 
 import oracle.cp_oracle as O
 import synthgen as G
+from trace_check import check, golden
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -138,14 +139,9 @@ def test_sharded_trace_matches_oracle(P, name):
         return infos, cp.cp_get_factors(ctx)
 
     res = run_sharded(P, X, cfg.dims, cfg.K, body)
+    cond = golden(name, X, A0, cfg.eps_pp, tr, A_fin)
     for rank, (infos, A) in enumerate(res):
-        for t, info in zip(tr, infos):
-            assert info["phase"] == t["phase"]
-            if 1.0 - t["fitness"] >= 1e-6:
-                assert abs(info["fitness"] - t["fitness"]) < 1e-8, (rank, t, info)
-        if 1.0 - tr[-1]["fitness"] >= 1e-6:
-            for n in range(cfg.N):
-                assert rel(A[n], A_fin[n]) < 1e-6, (rank, n)
+        check(tr, infos, cond, A_fin, A, tag=(name, P, rank))
     # replicas agree bit for bit on the replicated factors (deterministic reductions)
     for n in range(1, cfg.N):
         for rank in range(1, P):
@@ -169,13 +165,15 @@ def test_nccl_transport_single_rank(name):
     plain = cp.cp_init(X, cfg.N, cfg.dims, cfg.K, flags=cp.FLAG_NO_OVERLAP)
     for c in (nc, plain):
         cp.cp_set_factors(c, A0)
+    cond = golden(name, X, A0, cfg.eps_pp, tr)
+    infos = []
     for t in tr:
         for c in (nc, plain):
             cp.cp_set_phase_override(c, t["phase"])
         a, b = cp.als_sweep(nc, 0.0, cfg.eps_pp), cp.als_sweep(plain, 0.0, cfg.eps_pp)
-        if 1.0 - t["fitness"] >= 1e-6:
-            assert abs(a["fitness"] - t["fitness"]) < 1e-8, (t, a)
+        infos.append(a)
         assert abs(a["fitness"] - b["fitness"]) < 1e-9, (a, b)
+    check(tr, infos, cond, tag=(name, "nccl1"))
     M = cp.mttkrp_dt(nc)
     A = cp.cp_get_factors(nc)
     for n in range(cfg.N):

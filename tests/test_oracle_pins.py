@@ -454,3 +454,56 @@ def test_phase_override_replays_schedule():
     sched = [t["phase"] for t in tr]
     _, tr2 = O.pp_cp_als(X, A0, 0.0, 0.2, 25, phase_override=sched)
     assert [t["fitness"] for t in tr2] == [t["fitness"] for t in tr]
+
+
+# ---------------------------------------------------------------- the ε_pp metric (L7) and r² (L17)
+@pytest.mark.parametrize("t", [0.05, 0.5])
+@pytest.mark.parametrize("phase", ["dt", "pp-build"])
+def test_rel_dA_closed_form_scaled_update(t, phase):
+    """X = (1+t)[[A]]: one sweep from A moves A^(1) to (1+t)A^(1) and leaves the others (mode 0's
+    least-squares solution absorbs the scale; with dA^(2..N) = 0 the PP update is exact too,
+    P:553-557).  So dA^(1) = t A^(1) (L8) and the relative metric of L7, ‖dA‖/‖A‖ with the
+    CURRENT A, is exactly t/(1+t) -- an absolute norm would give t‖A‖, a metric normalised by
+    A_prev or A_p would give t."""
+    r = rng(40)
+    dims = (7, 6, 8, 5)
+    A = [r.random((d, 3)) + 0.1 for d in dims]
+    X = (1.0 + t) * O.kruskal_full(A)
+    _, tr = O.pp_cp_als(X, A, 0.0, 0.1, 1, phase_override=[phase])
+    assert abs(tr[0]["max_rel_dA"] - t / (1.0 + t)) < 1e-10
+    st = O.State(X, A)
+    st.pp_build() if phase != "dt" else None
+    st.pp_sweep() if phase != "dt" else st.dt_sweep()
+    rels = st.rel_dA()
+    assert abs(rels[0] - t / (1.0 + t)) < 1e-10 and max(rels[1:]) < 1e-10
+    # the new factor itself: exactly (1+t) A^(1) up to rounding
+    assert rel(st.A[0], (1.0 + t) * A[0]) < 1e-10
+
+
+def test_phase_sequence_invariant_under_tensor_scaling():
+    """Scaling X and A^(1) by c = 1e6 scales every later A^(1) by c and leaves A^(2..N) unchanged
+    (the normal equations are homogeneous), so a RELATIVE ε_pp metric (L7) sees the same numbers
+    and Alg. 3 takes the same phases; an absolute ‖dA‖ test would not."""
+    X, _, A0 = small_problem(noise=1e-2, seed=24)
+    c = 1e6
+    A1 = [a.copy() for a in A0]
+    A1[0] = c * A1[0]
+    _, tr = O.pp_cp_als(X, A0, 0.0, 0.2, 30)
+    _, tr_c = O.pp_cp_als(c * X, A1, 0.0, 0.2, 30)
+    assert any(t["phase"] != "dt" for t in tr)
+    assert [t["phase"] for t in tr] == [t["phase"] for t in tr_c]
+    for a, b in zip(tr, tr_c):
+        assert abs(a["max_rel_dA"] - b["max_rel_dA"]) <= 1e-9 * a["max_rel_dA"]
+        assert abs(a["fitness"] - b["fitness"]) <= 1e-9
+
+
+def test_trace_residual_sq_is_explicit_residual_after_regular_sweeps():
+    """The trace's unclamped r² (S:177 with the sweep's last M^(N)) equals ‖X - [[A]]‖² computed
+    by explicit reconstruction after every regular sweep (L17)."""
+    X, _, A0 = small_problem(noise=1e-2, seed=26)
+    nx2 = float(np.sum(X * X))
+    st = O.State(X, A0)
+    for _ in range(5):
+        st.dt_sweep()
+        explicit = float(np.sum((X - O.kruskal_full(st.A)) ** 2))
+        assert abs(st.residual_sq() - explicit) <= 1e-12 * nx2
