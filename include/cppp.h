@@ -104,6 +104,8 @@ typedef struct {
   int restarts;              /* number of PP operator builds so far */
   int converged;             /* grad_norm_sum <= eps */
   double seconds;            /* device time of this sweep (CUDA events) */
+  double pp_bound;           /* CPPP_POLICY_BOUND, PP sweeps: the switching monitor's value (the
+                                largest certificate bound, see cp_set_pp_policy); NaN otherwise */
   int approximate;           /* 1 when fitness/residual_sq come from the PP-approximated M~^(N)
                                 (a PP sweep): then r² is only O(ε²)-accurate and may be
                                 negative (clamped in fitness, L17/L27); fitness_exact() gives the
@@ -190,6 +192,16 @@ cppp_status pp_update(cppp_ctx *ctx, int n, double *M_tilde);
  * cp_set_factors or pp_build_operators. */
 cppp_status pp_error(cppp_ctx *ctx, double *err, double *eps, double *bound);
 
+/* Second-order PP term (the first term the PP update P:553 drops): at the
+ * current factors A and the operators' A_p (dA = A - A_p), for every mode n
+ *   T2[n] = Σ_{i<j; i,j≠n} M_p^(i,j,n) ×_i dA^(i) ×_j dA^(j)      (s_n x K, local rows)
+ * with M_p^(i,j,n) the Def. 3.1 intermediate at A_p keeping (i,j,n).  M~^(n) + T2[n] is the
+ * second-order PP update: exact for N = 3, O(ε³) otherwise.  Computed as C(N,2) exact MTTKRP passes
+ * of the dimension tree with the factor lists (dA on {i,j}, A_p elsewhere) -- a diagnostic, each
+ * pass costs about a regular sweep's contractions.  T2[n] host or device (NULL entries skipped);
+ * factors, operators and the phase state are unchanged.  CPPP_ESTATE before a build. */
+cppp_status pp_second_order(cppp_ctx *ctx, double *const *T2);
+
 /* One CP-ALS-PP sweep (Alg. 3, readings L7-L12): phase chosen by the state
  * machine unless cp_set_phase_override forces it.  eps: global stop on Σ||G||;
  * eps_pp: PP tolerance on the relative factor change.  info may be NULL. */
@@ -203,6 +215,19 @@ cppp_status als_sweep(cppp_ctx *ctx, double eps, double eps_pp, cppp_sweep_info 
  * ranks, or a phase override. */
 cppp_status als_run(cppp_ctx *ctx, double eps, double eps_pp, int max_sweeps,
                     cppp_sweep_info *info, int *done);
+/* PP switching policy (the "alternative schemes for switching" of P:1134).
+ *   CPPP_POLICY_EPS_PP (default): Alg. 3 as read in L7-L11 (ε_pp test on max ||dA||/||A||).
+ *   CPPP_POLICY_BOUND: the same transitions, and after every PP sweep a monitor evaluates, per mode
+ *     n and column k, the certificate of pp_error (||X||_F Σ_{|S|>=2} Π_{i∈S}||da_k^(i)||
+ *     Π_{j∉S}||a_p,k^(j)|| / ||m~_k^(n)||, from column norms only: no tensor pass); when its maximum
+ *     reaches tol, the phase does not continue with the stale operators -- the next sweep rebuilds
+ *     them at the current factors (a pp-build) instead of a pp-approx sweep.  info.pp_bound
+ *     reports the value.  tol > 0.
+ * Changing the policy drops the captured sweep graphs (recaptured on the next sweeps). */
+#define CPPP_POLICY_EPS_PP 0
+#define CPPP_POLICY_BOUND 1
+cppp_status cp_set_pp_policy(cppp_ctx *ctx, int policy, double tol);
+
 /* Force the phase of the next sweeps (CPPP_PHASE_AUTO to release); used to replay the
  * oracle's phase schedule in parity runs (L12). */
 cppp_status cp_set_phase_override(cppp_ctx *ctx, int phase);

@@ -65,7 +65,8 @@ class SweepInfo(C.Structure):
     _fields_ = [("sweep", C.c_int), ("phase", C.c_int), ("fitness", C.c_double),
                 ("residual_sq", C.c_double), ("grad_norm_sum", C.c_double),
                 ("max_rel_dA", C.c_double), ("next_phase", C.c_int), ("restarts", C.c_int),
-                ("converged", C.c_int), ("seconds", C.c_double), ("approximate", C.c_int)]
+                ("converged", C.c_int), ("seconds", C.c_double), ("pp_bound", C.c_double),
+                ("approximate", C.c_int)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}
@@ -106,9 +107,11 @@ def lib():
         "pp_get_single": (I, [P, I, P]),
         "pp_update": (I, [P, I, P]),
         "pp_error": (I, [P, P, P, P]),
+        "pp_second_order": (I, [P, C.POINTER(P)]),
         "als_sweep": (I, [P, D, D, C.POINTER(SweepInfo)]),
         "als_run": (I, [P, D, D, I, C.POINTER(SweepInfo), C.POINTER(I)]),
         "cp_set_phase_override": (I, [P, I]),
+        "cp_set_pp_policy": (I, [P, I, D]),
         "fitness": (I, [P, C.POINTER(D)]),
         "fitness_exact": (I, [P, C.POINTER(D), C.POINTER(D)]),
         "cppp_kernel_stats": (I, [P, I, C.POINTER(KernelStat)]),
@@ -149,7 +152,7 @@ def lib():
 EXPORTED = ["cppp_default_opts", "cppp_workspace_bytes", "cp_init", "cp_load_tensor", "cp_set_factors",
             "cp_update_factors",
             "cp_get_factors", "mttkrp_dt", "pp_build_operators", "pp_get_operator",
-            "pp_get_single", "pp_update", "pp_error", "als_sweep", "als_run", "cp_set_phase_override", "fitness",
+            "pp_get_single", "pp_update", "pp_error", "pp_second_order", "als_sweep", "als_run", "cp_set_phase_override", "cp_set_pp_policy", "fitness",
             "fitness_exact", "cppp_kernel_stats", "cppp_reset_kernel_stats", "cppp_generate",
             "cppp_nccl_unique_id", "cppp_plan_describe", "cp_destroy", "cp_last_error",
             "cppp_status_string", "cppp_version", "cppp_launch_count",
@@ -322,6 +325,13 @@ def pp_error(ctx: Ctx):
     return err, eps, bound
 
 
+def pp_second_order(ctx: Ctx) -> List[np.ndarray]:
+    """pp_second_order (include/cppp.h): T2^(n) = Σ_{i<j≠n} M_p^(i,j,n) ×_i dA^(i) ×_j dA^(j)."""
+    out = [np.empty((ctx.local_rows[n], ctx.K)) for n in range(ctx.N)]
+    _check(ctx, lib().pp_second_order(ctx.h, _ptrs(out)))
+    return out
+
+
 def als_sweep(ctx: Ctx, eps: float, eps_pp: float) -> dict:
     info = SweepInfo()
     _check(ctx, lib().als_sweep(ctx.h, eps, eps_pp, C.byref(info)))
@@ -334,6 +344,15 @@ def als_run(ctx: Ctx, eps: float, eps_pp: float, max_sweeps: int) -> list:
     done = C.c_int(0)
     _check(ctx, lib().als_run(ctx.h, eps, eps_pp, max_sweeps, infos, C.byref(done)))
     return [infos[i].as_dict() for i in range(done.value)]
+
+
+POLICY_EPS_PP, POLICY_BOUND = 0, 1
+
+
+def cp_set_pp_policy(ctx: Ctx, policy: int, tol: float = 0.0) -> None:
+    """cp_set_pp_policy (include/cppp.h): POLICY_EPS_PP (Alg. 3) or POLICY_BOUND (rebuild when the
+    switching monitor's certificate reaches tol)."""
+    _check(ctx, lib().cp_set_pp_policy(ctx.h, int(policy), float(tol)))
 
 
 def cp_set_phase_override(ctx: Ctx, phase) -> None:

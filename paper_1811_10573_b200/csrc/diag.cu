@@ -126,7 +126,50 @@ __global__ void __launch_bounds__(FT_THREADS)
   }
 }
 
+// PP switching monitor (the "alternative schemes for switching" of P:1134): the
+// largest certificate bound of pp_error_final_kernel over (n, k), with ||m_k|| taken from the
+// sweep's M~ (msum[n][K..2K) = Σ m~²) instead of an exact MTTKRP -- O(N K 2^N) work, no tensor pass.
+// One warp; out[0] = max bound (fixed-order shuffle max: exact).
+__global__ void pp_bound_max_kernel(const double* __restrict__ msum, const double* __restrict__ asum,
+                                    int N, int K, const double* __restrict__ normX_sq,
+                                    double* __restrict__ out) {
+  const double normX = sqrt(*normX_sq);
+  double mx = 0.0;
+  for (int idx = threadIdx.x; idx < N * K; idx += 32) {
+    const int n = idx / K, k = idx - n * K;
+    double p[CPPP_MAX_ORDER_], d[CPPP_MAX_ORDER_];
+    int m = 0;
+    for (int i = 0; i < N; ++i) {
+      if (i == n) continue;
+      const double* ai = asum + static_cast<int64_t>(i) * 3 * K;
+      d[m] = sqrt(ai[k]);
+      p[m] = sqrt(ai[2 * K + k]);
+      ++m;
+    }
+    double tot = 0.0;
+    for (unsigned S = 0; S < (1u << m); ++S) {
+      if (__popc(S) < 2) continue;
+      double t = 1.0;
+      for (int i = 0; i < m; ++i) t *= (S >> i) & 1u ? d[i] : p[i];
+      tot += t;
+    }
+    const double mn = sqrt(msum[static_cast<int64_t>(n) * 3 * K + K + k]);
+    const double b = tot == 0.0 ? 0.0 : (mn > 0.0 ? normX * tot / mn : CUDART_INF);
+    mx = fmax(mx, b);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (threadIdx.x == 0) out[0] = mx;
+}
+
 }  // namespace
+
+cudaError_t launch_pp_bound_max(const double* msum, const double* asum, int N, int K,
+                                const double* normX_sq, double* out, cudaStream_t st) {
+  pp_bound_max_kernel<<<1, 32, 0, st>>>(msum, asum, N, K, normX_sq, out);
+  note_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_fit_terms(const double* M, const double* A, int64_t rows, int K,
                              const double* S_all, int N, int n, double* fit, cudaStream_t st) {

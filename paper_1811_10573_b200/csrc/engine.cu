@@ -117,6 +117,16 @@ struct cppp_ctx {
   double* stats = nullptr;   // N x 3 norms, then fitness terms [2], then ||X||² [1]
   double* Fpad = nullptr;    // max s x 128
   double* ops[CPPP_MAX_ORDER][CPPP_MAX_ORDER] = {};   // i<j: [x_i][x_j][k]
+  // sharded runs: the operators that contract the slab mode (i, j != q) are laid out back to back
+  // (padding between them is zero), so the build all-reduces them in ONE call (SURVEY C-b)
+  double* ops_red = nullptr;
+  size_t ops_red_count = 0;
+  // the PP sweep's exchange terms T_m, m != q, likewise in one call (C-c)
+  double* T_red = nullptr;
+  size_t T_red_count = 0;
+  // 8 doubles right before S_all: the slab mode's norms land here so that they and S^(q)
+  // (q = 0, the first block) are all-reduced in one call (C-d)
+  double* qhdr = nullptr;
   double* pp_partial = nullptr;
   double* sq_partial = nullptr;
   double* gath = nullptr;    // gather scratch (max s x K)
@@ -134,6 +144,8 @@ struct cppp_ctx {
   bool borrowed = false;        // X is the caller's device buffer (CPPP_FLAG_BORROW_TENSOR)
   int next_phase = CPPP_PHASE_DT;
   int override_phase = CPPP_PHASE_AUTO;
+  int policy = CPPP_POLICY_EPS_PP;   // PP switching policy (cp_set_pp_policy)
+  double policy_tol = 0.0;
   int sweep = 0, restarts = 0;
   double last_fitness = NAN;
   double* host_stats = nullptr;  // pinned
@@ -175,7 +187,7 @@ struct cppp_ctx {
 // Device-side Alg. 3 phase machine state for als_run (the same decisions als_sweep takes on the
 // host, L7-L11, same IEEE operations in the same order).
 struct RunInfo {
-  double fitness, residual_sq, gsum, maxrel;
+  double fitness, residual_sq, gsum, maxrel, bound;
   int phase, next_phase, restarts, converged;
 };
 // the communicating (sharded) code paths run with several ranks, or with one rank under
@@ -186,8 +198,8 @@ inline bool comm_on(const cppp_ctx* c) {
 
 constexpr int RUN_MAX = 1024;   // sweeps per als_run call
 struct RunState {
-  double eps, eps_pp, normX_sq;
-  int max_sweeps, done, phase, restarts, N, pad;
+  double eps, eps_pp, normX_sq, policy_tol;
+  int max_sweeps, done, phase, restarts, N, policy;
   RunInfo info[RUN_MAX];
 };
 
@@ -478,13 +490,17 @@ cppp_status finish_mode(cppp_ctx* c, int n, const double* Mn, bool pp_phase) {
     // S^(n), the norms and (last mode) the fitness terms in one kernel; Γ^(n) is still in place
     // (the next factorization starts after ev_S below)
     const bool last = (n == c->N - 1);
-    CUCHK(c, launch_gram(An, rows, K, c->S_all + (int64_t)n * K * K, c->rowstat, c->stats + 3 * n,
-                         last ? c->Gamma : nullptr, last ? c->stats + 3 * c->N : nullptr,
-                         c->gram_scratch, c->gram_counters, c->st));
+    // the slab mode (q = 0) writes its norms into qhdr, right before S^(q) = S_all's first block
+    const bool packq = (n == c->q) && comm_on(c) && !c->dry;
+    CUCHK(c, launch_gram(An, rows, K, c->S_all + (int64_t)n * K * K, c->rowstat,
+                         packq ? c->qhdr : c->stats + 3 * n, last ? c->Gamma : nullptr,
+                         last ? c->stats + 3 * c->N : nullptr, c->gram_scratch, c->gram_counters, c->st));
   }
-  if (n == c->q) {
-    STCHK(allreduce(c, c->S_all + (int64_t)n * K * K, (size_t)K * K));
-    STCHK(allreduce(c, c->stats + 3 * n, 3));
+  if (n == c->q && comm_on(c)) {
+    // S^(q) and the norms in ONE all-reduce (SURVEY C-d), then the norms into their stats slots
+    STCHK(allreduce(c, c->qhdr, (size_t)K * K + 8));
+    CUCHK(c, cudaMemcpyAsync(c->stats + 3 * n, c->qhdr, 3 * sizeof(double), cudaMemcpyDeviceToDevice,
+                             c->st));
   }
   CUCHK(c, cudaEventRecord(c->ev_S, c->st));
   // the next mode's factorization starts right away on the side stream; inside a captured sweep
@@ -529,8 +545,10 @@ struct DT {
   // keeps the single-mode TTM: its level-1 node feeds two leaves, and the multi-mode GEMM
   // would have only s/128 output tiles.)
   cppp_status chain(const Node& nd, const std::vector<int>& modes, double* final_dst, Node* out) {
-    if (nd.root && modes.size() >= 2 && c->N >= 4 && !(c->flags & CPPP_FLAG_NO_KRP) &&
-        std::find(modes.begin(), modes.end(), c->q) == modes.end()) {
+    // (a half that contains the slab mode q is contracted the same way: with A^(q) restricted to
+    // the local rows the GEMM's output is this rank's partial sum, every later contraction is
+    // linear, and every leaf n != q is all-reduced anyway -- SURVEY §8(e))
+    if (nd.root && modes.size() >= 2 && c->N >= 4 && !(c->flags & CPPP_FLAG_NO_KRP)) {
       std::vector<int> asc = modes;
       std::sort(asc.begin(), asc.end());
       uint32_t nm = nd.mask;
@@ -779,12 +797,9 @@ cppp_status run_pp_build(cppp_ctx* c, bool have12 = false) {
   PPTree t{c};
   t.have12 = have12 && reuse12(c);
   STCHK(t.run());
-  // leaves that contracted the sharded mode hold partial sums: all-reduce them (SURVEY C-b)
-  if (c->q >= 0)
-    for (int i = 0; i < N; ++i)
-      for (int j = i + 1; j < N; ++j)
-        if (i != c->q && j != c->q)
-          STCHK(allreduce(c, c->ops[i][j], (size_t)c->dl[i] * c->dl[j] * K));
+  // leaves that contracted the sharded mode hold partial sums: all-reduce them, one call over
+  // their contiguous span (SURVEY C-b)
+  if (c->q >= 0) STCHK(allreduce(c, c->ops_red, c->ops_red_count));
   STCHK(build_singles(c));
   if (!c->dry) c->ops_valid = true;
   return CPPP_OK;
@@ -855,6 +870,8 @@ bool pp_stagger(const cppp_ctx* c) {
   return bytes >= (1 << 20);
 }
 
+cppp_status pp_monitor(cppp_ctx* c);
+
 cppp_status run_pp_sweep(cppp_ctx* c, bool after_build) {
   const int N = c->N;
   const bool sh = c->q >= 0 && comm_on(c);
@@ -872,7 +889,8 @@ cppp_status run_pp_sweep(cppp_ctx* c, bool after_build) {
       STCHK(finish_mode(c, n, c->M[n], true));
     }
     if (sh && n == c->q) {
-      // T_m = M_p^(q,m) ×_q dA^(q) (partial over local rows) for every m != q
+      // T_m = M_p^(q,m) ×_q dA^(q) (partial over local rows) for every m != q, then ONE all-reduce
+      // over the contiguous T buffers (SURVEY C-c)
       for (int m = 0; m < N; ++m) {
         if (m == c->q) continue;
         if (!c->dry) {
@@ -894,10 +912,34 @@ cppp_status run_pp_sweep(cppp_ctx* c, bool after_build) {
           a.t[0] = t;
           CUCHK(c, launch_pp_update(a, c->st));
         }
-        STCHK(allreduce(c, c->T[m], (size_t)c->dl[m] * c->K));
       }
+      STCHK(allreduce(c, c->T_red, c->T_red_count));
     }
   }
+  if (c->policy == CPPP_POLICY_BOUND) STCHK(pp_monitor(c));
+  return CPPP_OK;
+}
+
+// The switching monitor of CPPP_POLICY_BOUND (after every PP sweep): column sums of squares of the
+// sweep's M~^(n) and of (A_p, A) per mode, then the largest certificate bound into stats[3N+6].
+// The slab mode's rows are local: its sums are all-reduced.
+cppp_status pp_monitor(cppp_ctx* c) {
+  if (c->dry) return CPPP_OK;
+  const int N = c->N, K = c->K;
+  int64_t smax = 0;
+  for (int n = 0; n < N; ++n) smax = std::max(smax, c->s[n]);
+  double* msum = c->chk + smax * K;
+  double* asum = msum + 3 * N * K;
+  for (int n = 0; n < N; ++n) {
+    const int64_t off = (n == c->q) ? c->qoff * K : 0;
+    CUCHK(c, launch_colsq(c->M[n], c->M[n], c->dl[n], K, msum + (int64_t)n * 3 * K, c->st));
+    CUCHK(c, launch_colsq(c->Ap[n] + off, c->A[n] + off, c->dl[n], K, asum + (int64_t)n * 3 * K, c->st));
+  }
+  if (c->q >= 0 && comm_on(c)) {
+    STCHK(allreduce(c, msum + (int64_t)c->q * 3 * K, (size_t)3 * K));
+    STCHK(allreduce(c, asum + (int64_t)c->q * 3 * K, (size_t)3 * K));
+  }
+  CUCHK(c, launch_pp_bound_max(msum, asum, N, K, c->stats + 3 * N + 2, c->stats + 3 * N + 6, c->st));
   return CPPP_OK;
 }
 
@@ -918,7 +960,8 @@ cppp_status run_phase_eager(cppp_ctx* c, int phase, bool have12 = true) {
 // Whole sweeps replay as CUDA graphs (captured on a phase's second use, so the first use sets
 // every kernel attribute eagerly).  Not used with several ranks (collectives stay eager).
 cppp_status run_phase(cppp_ctx* c, int phase) {
-  const bool graphs = !(c->flags & CPPP_FLAG_NO_GRAPH) && !comm_on(c);
+  // NCCL collectives are captured with the sweep (a host all-reduce hook is not capturable)
+  const bool graphs = !(c->flags & CPPP_FLAG_NO_GRAPH) && !(comm_on(c) && c->host_ar);
   auto& g = c->graphs[phase];
   // the captured PP-build sweep takes M_p^(1,2) from the preceding regular sweep; a build
   // forced anywhere else recomputes it, eagerly
@@ -1018,8 +1061,10 @@ __global__ void run_decide_kernel(RunState* rs, const double* __restrict__ stats
   const double fit = __dsub_rn(1.0, __ddiv_rn(sqrt(fmax(0.0, r2)), sqrt(rs->normX_sq)));
   const bool small = maxrel < rs->eps_pp;
   const int phase = rs->phase;
-  const int next = phase == CPPP_PHASE_DT ? (small ? CPPP_PHASE_PP_BUILD : CPPP_PHASE_DT)
-                                          : (small ? CPPP_PHASE_PP : CPPP_PHASE_DT);
+  int next = phase == CPPP_PHASE_DT ? (small ? CPPP_PHASE_PP_BUILD : CPPP_PHASE_DT)
+                                    : (small ? CPPP_PHASE_PP : CPPP_PHASE_DT);
+  const double bound = (rs->policy == CPPP_POLICY_BOUND && phase != CPPP_PHASE_DT) ? stats[3 * N + 6] : NAN;
+  if (next == CPPP_PHASE_PP && bound >= rs->policy_tol) next = CPPP_PHASE_PP_BUILD;
   if (phase == CPPP_PHASE_PP_BUILD) rs->restarts++;
   const int d = rs->done;
   RunInfo& in = rs->info[d];
@@ -1027,6 +1072,7 @@ __global__ void run_decide_kernel(RunState* rs, const double* __restrict__ stats
   in.residual_sq = r2;
   in.gsum = gsum;
   in.maxrel = maxrel;
+  in.bound = bound;
   in.phase = phase;
   in.next_phase = next;
   in.restarts = rs->restarts;
@@ -1156,11 +1202,13 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   for (int n = 0; n < N; ++n) {
     oA[n] = take(sizeof(double) * c->s[n] * K + fac_slack);
     oAp[n] = take(sizeof(double) * c->s[n] * K + fac_slack);
-    odA[n] = take(sizeof(double) * c->s[n] * K);
+    odA[n] = take(sizeof(double) * c->s[n] * K + fac_slack);   // (pp_second_order's GEMMs read dA)
     oM[n] = take(sizeof(double) * c->dl[n] * K);
     oMp[n] = take(sizeof(double) * c->dl[n] * K);
-    oT[n] = take(sizeof(double) * c->dl[n] * K);
   }
+  for (int n = 0; n < N; ++n) oT[n] = take(sizeof(double) * c->dl[n] * K);   // back to back (C-c)
+  const size_t oQh = take(0);            // qhdr: the 8 doubles right before S_all
+  off = oQh + 8 * sizeof(double);        // (S_all need not be 256-byte aligned)
   size_t oS = take(sizeof(double) * N * K * K);
   size_t oG = take(sizeof(double) * solve_ld(K) * solve_ld(K));
   // packed factor, inverted 32 x 32 diagonal blocks, Jacobi V
@@ -1182,8 +1230,18 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   }
   size_t oFpad = take(sizeof(double) * ttm_scratch_doubles(maxS));   // TTM factor + scheduler
   size_t oOps[CPPP_MAX_ORDER][CPPP_MAX_ORDER];
-  for (int i = 0; i < N; ++i)
-    for (int j = i + 1; j < N; ++j) oOps[i][j] = take(sizeof(double) * c->dl[i] * c->dl[j] * K);
+  size_t red_lo = 0, red_hi = 0;
+  for (int pass = 0; pass < 2; ++pass)   // the operators not involving q first, back to back (C-b)
+    for (int i = 0; i < N; ++i)
+      for (int j = i + 1; j < N; ++j) {
+        const bool withq = (i == c->q || j == c->q);
+        if (withq != (pass == 1)) continue;
+        oOps[i][j] = take(sizeof(double) * c->dl[i] * c->dl[j] * K);
+        if (pass == 0) {
+          if (red_hi == 0) red_lo = oOps[i][j];
+          red_hi = oOps[i][j] + sizeof(double) * c->dl[i] * c->dl[j] * K;
+        }
+      }
   size_t oPP = take(sizeof(double) * pp_update_scratch_doubles(smax, K, smax));
   size_t oSq = take(sizeof(double) * 2048);
   size_t oGath = take(sizeof(double) * smax * K);
@@ -1225,6 +1283,19 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   c->Fpad = reinterpret_cast<double*>(b + oFpad);
   for (int i = 0; i < N; ++i)
     for (int j = i + 1; j < N; ++j) c->ops[i][j] = reinterpret_cast<double*>(b + oOps[i][j]);
+  c->ops_red = reinterpret_cast<double*>(b + red_lo);
+  c->ops_red_count = (red_hi - red_lo) / sizeof(double);
+  {
+    int m0 = -1, m1 = -1;
+    for (int m = 0; m < N; ++m)
+      if (m != c->q) {
+        if (m0 < 0) m0 = m;
+        m1 = m;
+      }
+    c->T_red = c->T[m0];
+    c->T_red_count = (size_t)(c->T[m1] - c->T[m0]) + (size_t)c->dl[m1] * K;
+  }
+  c->qhdr = reinterpret_cast<double*>(b + oQh);
   c->pp_partial = reinterpret_cast<double*>(b + oPP);
   c->sq_partial = reinterpret_cast<double*>(b + oSq);
   c->gath = reinterpret_cast<double*>(b + oGath);
@@ -1653,6 +1724,69 @@ cppp_status pp_error(cppp_ctx* c, double* err, double* eps, double* bound) {
   return CPPP_OK;
 }
 
+// Second-order PP term: T2^(n) = Σ_{i<j; i,j≠n} M_p^(i,j,n) ×_i dA^(i)
+// ×_j dA^(j).  M_p^(i,j,n) ×_i dA^(i) ×_j dA^(j) is the MTTKRP of mode n with the factor list
+// (dA^(i), dA^(j), A_p elsewhere) (Def. 3.1 is multilinear), so one exact pass of the dimension tree
+// with that list gives pair (i,j)'s contribution to every mode n ∉ {i,j} at once: C(N,2) passes,
+// the contributions added per mode in ascending pair order (the oracle's order).  c->T holds the
+// sums (dead between sweeps), c->M is overwritten; factors, operators and the phase state are kept.
+cppp_status pp_second_order(cppp_ctx* c, double* const* T2) {
+  if (!c) return CPPP_EINVAL;
+  if (!c->factors_set) return fail(c, CPPP_ESTATE, "pp_second_order before cp_set_factors");
+  if (!c->ops_valid) return fail(c, CPPP_ESTATE, "pp_second_order before pp_build_operators");
+  const int N = c->N, K = c->K;
+  STCHK(drain_prefetch(c));
+  for (int i = 0; i < N; ++i) {
+    CUCHK(c, launch_sub(c->A[i], c->Ap[i], c->dA[i], c->s[i] * K, c->st));
+    CUCHK(c, cudaMemsetAsync(c->T[i], 0, sizeof(double) * c->dl[i] * K, c->st));
+  }
+  double* saved[CPPP_MAX_ORDER];
+  for (int m = 0; m < N; ++m) saved[m] = c->A[m];
+  cppp_status st = CPPP_OK;
+  for (int i = 0; i < N && st == CPPP_OK; ++i)
+    for (int j = i + 1; j < N && st == CPPP_OK; ++j) {
+      for (int m = 0; m < N; ++m) c->A[m] = (m == i || m == j) ? c->dA[m] : c->Ap[m];
+      st = run_dt(c, false, c->M);
+      for (int n = 0; n < N && st == CPPP_OK; ++n) {
+        if (n == i || n == j) continue;
+        cudaError_t e = launch_add(c->M[n], c->T[n], c->dl[n] * K, c->st);
+        if (e != cudaSuccess) st = fail(c, CPPP_ECUDA, "pp_second_order add: %s", cudaGetErrorString(e));
+      }
+    }
+  for (int m = 0; m < N; ++m) c->A[m] = saved[m];
+  STCHK(st);
+  if (T2)
+    for (int n = 0; n < N; ++n)
+      if (T2[n]) STCHK(copy_out(c, T2[n], c->T[n], (size_t)c->dl[n] * K));
+  CUCHK(c, cudaStreamSynchronize(c->st));
+  prof_collect(c);
+  return CPPP_OK;
+}
+
+cppp_status cp_set_pp_policy(cppp_ctx* c, int policy, double tol) {
+  if (!c) return CPPP_EINVAL;
+  if (policy != CPPP_POLICY_EPS_PP && policy != CPPP_POLICY_BOUND)
+    return fail(c, CPPP_EINVAL, "unknown PP policy %d", policy);
+  if (policy == CPPP_POLICY_BOUND && !(tol > 0.0)) return fail(c, CPPP_EINVAL, "policy tolerance must be > 0");
+  if (policy != c->policy) {   // the monitor is part of the PP sweep: recapture the graphs
+    STCHK(drain_prefetch(c));
+    CUCHK(c, cudaStreamSynchronize(c->st));
+    for (auto& g : c->graphs) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      for (auto& p : g.prof) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+      }
+      g = cppp_ctx::SweepGraph{};
+    }
+    if (c->run.exec) cudaGraphExecDestroy(c->run.exec);
+    c->run = cppp_ctx::RunGraph{};
+  }
+  c->policy = policy;
+  c->policy_tol = tol;
+  return CPPP_OK;
+}
+
 cppp_status cp_set_phase_override(cppp_ctx* c, int phase) {
   if (!c) return CPPP_EINVAL;
   if (phase < CPPP_PHASE_AUTO || phase > CPPP_PHASE_PP) return fail(c, CPPP_EINVAL, "bad phase %d", phase);
@@ -1672,7 +1806,7 @@ cppp_status als_sweep(cppp_ctx* c, double eps, double eps_pp, cppp_sweep_info* i
   if (phase == CPPP_PHASE_PP_BUILD) c->restarts++;
   CUCHK(c, cudaEventRecord(c->ev_b, c->st));
   const int N = c->N;
-  CUCHK(c, cudaMemcpyAsync(c->host_stats, c->stats, sizeof(double) * (3 * N + 2),
+  CUCHK(c, cudaMemcpyAsync(c->host_stats, c->stats, sizeof(double) * (3 * N + 7),
                            cudaMemcpyDeviceToHost, c->st));
   CUCHK(c, cudaStreamSynchronize(c->st));
   prof_collect(c);
@@ -1692,6 +1826,10 @@ cppp_status als_sweep(cppp_ctx* c, double eps, double eps_pp, cppp_sweep_info* i
   const bool small = maxrel < eps_pp;
   if (phase == CPPP_PHASE_DT) c->next_phase = small ? CPPP_PHASE_PP_BUILD : CPPP_PHASE_DT;
   else c->next_phase = small ? CPPP_PHASE_PP : CPPP_PHASE_DT;
+  // CPPP_POLICY_BOUND: a PP phase continues only while the monitor's certificate stays below tol;
+  // otherwise the operators are rebuilt at the current factors (the next sweep is a pp-build)
+  const double bound = (c->policy == CPPP_POLICY_BOUND && phase != CPPP_PHASE_DT) ? hs[3 * N + 6] : NAN;
+  if (c->next_phase == CPPP_PHASE_PP && bound >= c->policy_tol) c->next_phase = CPPP_PHASE_PP_BUILD;
   c->sweep++;
   c->last_fitness = fit;
   if (info) {
@@ -1706,6 +1844,7 @@ cppp_status als_sweep(cppp_ctx* c, double eps, double eps_pp, cppp_sweep_info* i
     info->converged = gsum <= eps;
     info->seconds = ms * 1e-3;
     info->approximate = phase != CPPP_PHASE_DT;
+    info->pp_bound = bound;
   }
   return CPPP_OK;
 }
@@ -1721,7 +1860,7 @@ cppp_status als_run(cppp_ctx* c, double eps, double eps_pp, int max_sweeps, cppp
   if (max_sweeps == 0) return CPPP_OK;
   // the host loop: profiling events, several ranks (collectives stay eager), no graphs, a
   // forced phase, or a GPU/driver that cannot build the conditional graph
-  const bool host_loop = (c->flags & (CPPP_FLAG_PROFILE | CPPP_FLAG_NO_GRAPH)) || comm_on(c) ||
+  const bool host_loop = (c->flags & (CPPP_FLAG_PROFILE | CPPP_FLAG_NO_GRAPH)) || (comm_on(c) && c->host_ar) ||
                          c->override_phase != CPPP_PHASE_AUTO || c->run.failed ||
                          (c->next_phase == CPPP_PHASE_PP && !c->ops_valid) ||
                          (c->next_phase == CPPP_PHASE_PP_BUILD && reuse12(c) && !c->op12_fresh);
@@ -1752,6 +1891,8 @@ cppp_status als_run(cppp_ctx* c, double eps, double eps_pp, int max_sweeps, cppp
   h->phase = c->next_phase;
   h->restarts = c->restarts;
   h->N = c->N;
+  h->policy = c->policy;
+  h->policy_tol = c->policy_tol;
   const size_t head = offsetof(RunState, info);
   CUCHK(c, cudaMemcpyAsync(c->run_dev, h, head, cudaMemcpyHostToDevice, c->st));
   CUCHK(c, cudaEventRecord(c->ev_a, c->st));
@@ -1789,6 +1930,7 @@ cppp_status als_run(cppp_ctx* c, double eps, double eps_pp, int max_sweeps, cppp
       o.converged = r.converged;
       o.seconds = ms * 1e-3 / n;   // the run is one launch: its device time, shared evenly
       o.approximate = r.phase != CPPP_PHASE_DT;
+      o.pp_bound = r.bound;
     }
   }
   note_launches(1);   // the prologue

@@ -165,6 +165,8 @@ int sqnorm_blocks(int64_t n);
 cudaError_t launch_stagger(cudaStream_t st);
 // y = a - b (elementwise)
 cudaError_t launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st);
+// y = y + x (elementwise)
+cudaError_t launch_add(const double* x, double* y, int64_t n, cudaStream_t st);
 
 // PP error monitor (diag.cu).  colsq: sums[0..K) = Σ_y (a−b)², [K..2K) = Σ_y b², [2K..3K) = Σ_y a²
 // over a rows x K row-major pair.  pp_error_final: per (n, k) the error ratio, ε and bound
@@ -174,6 +176,9 @@ cudaError_t launch_colsq(const double* a, const double* b, int64_t rows, int K, 
 cudaError_t launch_pp_error_final(const double* msum, const double* asum, int N, int K,
                                   double normX, double* err, double* eps, double* bound,
                                   cudaStream_t st);
+// max over (n, k) of the PP certificate bound with ||m_k|| from M~ (msum: colsq of (M~, M~))
+cudaError_t launch_pp_bound_max(const double* msum, const double* asum, int N, int K,
+                                const double* normX_sq, double* out, cudaStream_t st);
 // fit[0] = Σ M∘A over rows x K, fit[1] = Σ (Hadamard_{m≠n} S^(m)) ∘ S^(n) (S:177 terms; one CTA)
 cudaError_t launch_fit_terms(const double* M, const double* A, int64_t rows, int K,
                              const double* S_all, int N, int n, double* fit, cudaStream_t st);

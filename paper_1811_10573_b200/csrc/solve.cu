@@ -441,177 +441,6 @@ __global__ void __launch_bounds__(GP_THREADS, 1)
   }
 }
 
-// ---------------------------------------------------------------- dataflow factorization, 32 < K <= 128
-// The same right-looking LDLᵀ as gamma_chol_kernel -- element (i, c), i >= c, takes the updates of
-// pivots j = 0..c-1 in ascending order, each W[i][c] = fma(-W[i][j], W[c][j] · (1/d_j), W[i][c]),
-// the same pivot rule, the same reciprocal and the same output layout: the results are bit-identical
-// -- without a CTA-wide barrier per pivot.  Warp w owns the columns c ≡ w (mod NW); lane l holds
-// rows l + 32 s (s < 4) of each, in registers.  Column j is final once pivot j-1 has been applied:
-// its owner then publishes it to shared memory with 1/d_j and arrives on the column's mbarrier, and
-// every other warp waits on that mbarrier (acquire) only when it reaches step j.  The owner of column
-// j+1 applies pivot j to that column FIRST and publishes it before it updates its other columns
-// (lookahead), so the per-pivot critical path is one column update + the reciprocal + the
-// hand-off, not a barrier of every warp.  Then, after one CTA barrier: the packed factor Tp (rows of
-// the lower part from the published columns, bank-conflict-free with an odd column pitch), the
-// inverses of the 32 x 32 diagonal blocks for the row solves (gamma_post_kernel's work, from shared
-// memory), or the Jacobi pseudo-inverse when the pivot test failed -- one launch in all.
-constexpr int DF_LD = 129;   // column pitch of the published columns (odd: conflict-free row reads)
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
-  uint32_t ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], 0;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_addr(bar))
-        : "memory");
-  }
-}
-
-template <int NW>
-__global__ void __launch_bounds__(NW * 32, 1)
-    gamma_df_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
-                    double* Tp, int ldt, int* mode, double* Vscratch) {
-  PROBE_T0();
-  pdl_wait();
-  constexpr int CPW = (128 + NW - 1) / NW;   // columns per warp (K <= 128)
-  extern __shared__ __align__(16) double dfs[];   // published columns [K][DF_LD] | Jacobi W
-  __shared__ __align__(8) uint64_t ready[128];
-  __shared__ double rinv_s[128], dpiv_s[128];
-  __shared__ double sh[32];
-  __shared__ int bad_s;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid < K) mbar_init(&ready[tid], 1);
-  if (tid == 0) bad_s = 0;
-  // Γ^(n) column by column (rows of Γ: the Grams are exactly symmetric, so S[c][r] = S[r][c]) --
-  // 1.0 · S^(first) · S^(next) ... in ascending m, as gamma_chol_kernel
-  double w[CPW][4];
-  double dmax = 0.0;
-#pragma unroll
-  for (int q = 0; q < CPW; ++q) {
-    const int c = wid + NW * q;
-#pragma unroll
-    for (int s = 0; s < 4; ++s) w[q][s] = 1.0;
-    if (c < K) {
-      for (int m = 0; m < N; ++m) {
-        if (m == n) continue;
-        const double* Sm = S_all + (int64_t)m * K * K + (int64_t)c * K;
-#pragma unroll
-        for (int s = 0; s < 4; ++s)
-          if (lane + 32 * s < K) w[q][s] *= __ldg(Sm + lane + 32 * s);
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int r = lane + 32 * s;
-      if (c < K && r < K) {
-        Gamma[c * ldt + r] = w[q][s];   // row c of Γ
-        if (r == c) dmax = fmax(dmax, w[q][s]);
-      } else {
-        w[q][s] = 0.0;
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-  if (lane == 0) sh[wid] = dmax;
-  __syncthreads();   // (also publishes the mbarrier inits)
-  double mx = 0.0;
-  for (int i = 0; i < NW; ++i) mx = fmax(mx, sh[i]);
-  const double thresh = PIVOT_TAU * mx;
-  bool bad = false;
-  // publish column c (its final values v) and 1/d_c; the lane holding row c forms the pivot
-  auto publish = [&](const double (&v)[4], int c) __attribute__((always_inline)) {
-    double* col = dfs + (int64_t)c * DF_LD;
-#pragma unroll
-    for (int s = 0; s < 4; ++s) col[lane + 32 * s] = v[s];
-    if ((c & 31) == lane) {
-      const int sc = c >> 5;
-      const double d = sc == 0 ? v[0] : sc == 1 ? v[1] : sc == 2 ? v[2] : v[3];
-      if (!(d > thresh)) bad = true;
-      dpiv_s[c] = d;
-      rinv_s[c] = pivot_rcp(d);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&ready[c]);
-  };
-  if (wid == 0) publish(w[0], 0);
-  PROBE_T(0);
-  for (int j = 0; j + 1 < K; ++j) {
-    // column j: published by its owner (this warp in program order, else wait for it)
-    if ((j % NW) != wid) mbar_wait0(&ready[j]);
-    const double* colj = dfs + (int64_t)j * DF_LD;
-    double cv[4];
-#pragma unroll
-    for (int s = 0; s < 4; ++s) cv[s] = colj[lane + 32 * s];
-    const double rj = rinv_s[j];
-    // lookahead: column j+1 first (its owner publishes it right away), then the others
-#pragma unroll
-    for (int pass = 0; pass < 2; ++pass) {
-#pragma unroll
-      for (int q = 0; q < CPW; ++q) {
-        const int c = wid + NW * q;
-        if (c >= K || c <= j || ((c == j + 1) != (pass == 0))) continue;
-        const double f = colj[c] * rj;   // W[c][j] / d_j
-#pragma unroll
-        for (int s = 0; s < 4; ++s)
-          if (lane + 32 * s >= c) w[q][s] = fma(-cv[s], f, w[q][s]);
-        if (pass == 0) publish(w[q], c);
-      }
-    }
-  }
-  if (bad) bad_s = 1;   // (a benign race: every writer stores 1)
-  __syncthreads();
-  PROBE_T(1);
-  const int ktiles = (ldt + 31) >> 5;
-  if (!bad_s) {
-    // 1/L[c][c] = 1/sqrt(d_c) exactly as gamma_chol_kernel forms it
-    if (tid < K) rinv_s[tid] = 1.0 / sqrt(dpiv_s[tid]);
-    __syncthreads();
-    // Tp row i: L[i][c] (c < i) from the published columns, 1/L[i][i], L[c][i] = Lᵀ (c > i)
-    for (int e = tid; e < K * ldt; e += NW * 32) {
-      const int i = e / ldt, c = e - i * ldt;
-      if (c >= K) continue;
-      double x;
-      if (c < i) x = dfs[(int64_t)c * DF_LD + i] * rinv_s[c];
-      else if (c > i) x = dfs[(int64_t)i * DF_LD + c] * rinv_s[i];
-      else x = rinv_s[i];
-      Tp[i * ldt + c] = x;
-    }
-    if (tid < ldt - K) Tp[(K + tid) * ldt + K + tid] = 1.0;   // unit diagonal of the padding
-    // the inverted diagonal blocks (Q, after Tp), warp b <-> block b
-    __shared__ double Ls[4][32][33];
-    if (wid < ktiles) {
-      const int b0 = 32 * wid;
-#pragma unroll 4
-      for (int jj = 0; jj < 32; ++jj) {
-        const int gj = b0 + jj, gc = b0 + lane;
-        double v;
-        if (gj >= K || gc >= K) v = (jj == lane) ? 1.0 : 0.0;   // identity past K
-        else if (gj > gc) v = dfs[(int64_t)gc * DF_LD + gj] * rinv_s[gc];
-        else if (gj == gc) v = rinv_s[gc];
-        else v = 0.0;   // (the upper part is not read)
-        Ls[wid][jj][lane] = v;
-      }
-      __syncwarp();
-      block_inverse_smem(Ls[wid], Tp + ldt * ldt + wid * 32 * 33);
-    }
-    if (tid == 0) *mode = 0;
-  } else {
-    // every warp has left the loop, the published columns are dead: the Jacobi scratch reuses them
-    gamma_pinv_dev(K, Gamma, Tp, ldt, Vscratch);
-    if (tid == 0) *mode = 1;
-  }
-  PROBE_T(2);
-}
-
 // K <= 32: the whole factorization in ONE warp, one launch (the chain above costs two launches
 // and ~570 cycles of barrier + shared-memory round trip per pivot: C4's K = 30 took 21 us).
 // Lane i keeps row i of W in registers; step j broadcasts row j by shuffles (W stays symmetric
@@ -1128,6 +957,12 @@ __global__ void sub_kernel(const double* a, const double* b, double* y, int64_t 
     y[e] = a[e] - b[e];
 }
 
+__global__ void add_kernel(const double* x, double* y, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    y[e] = y[e] + x[e];
+}
+
 __global__ void pad_rows_kernel(const double* F, int64_t S, int K, double* Fp, int ld) {
   pdl_wait();
   const int64_t total = S * ld;
@@ -1186,27 +1021,6 @@ cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double
     auto f = K <= 8 ? gamma_small_kernel<8> : K <= 16 ? gamma_small_kernel<16> : gamma_small_kernel<32>;
     cudaError_t e = launch_pdl(f, dim3(1), dim3(GS_THREADS), smem, st, S_all, N, n, K, Gamma, Tp, ldt,
                                mode, Vscratch);
-    note_launch();
-    return e;
-  }
-  // 32 < K <= 128: the dataflow factorization, one launch (CPPP_OLD_CHOL: the barrier-per-pivot
-  // kernel + gamma_post_kernel, for A/B; bit-identical results)
-  static const bool old_chol = getenv("CPPP_OLD_CHOL") != nullptr;
-  if (!old_chol) {
-    const size_t dsm = sizeof(double) * static_cast<size_t>(K) * (K + 1 > DF_LD ? K + 1 : DF_LD);
-    static bool df_attr = false;
-    if (!df_attr) {
-      for (auto f : {gamma_df_kernel<8>, gamma_df_kernel<16>}) {
-        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(sizeof(double) * 128 * 129));
-        if (e != cudaSuccess) return e;
-      }
-      df_attr = true;
-    }
-    cudaError_t e = K <= 64 ? launch_pdl(gamma_df_kernel<8>, dim3(1), dim3(8 * 32), dsm, st, S_all, N, n,
-                                         K, Gamma, Tp, ldt, mode, Vscratch)
-                            : launch_pdl(gamma_df_kernel<16>, dim3(1), dim3(16 * 32), dsm, st, S_all, N,
-                                         n, K, Gamma, Tp, ldt, mode, Vscratch);
     note_launch();
     return e;
   }
@@ -1319,6 +1133,13 @@ cudaError_t launch_stagger(cudaStream_t st) {
 cudaError_t launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   sub_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(a, b, y, n);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add(const double* x, double* y, int64_t n, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  add_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(x, y, n);
   note_launch();
   return cudaGetLastError();
 }

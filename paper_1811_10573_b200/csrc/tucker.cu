@@ -177,7 +177,8 @@ __global__ void tk_gram_combine(const double* __restrict__ part, int nparts, int
 // the change of W since then), so they converge in a few passes.  T: n x n global scratch.
 __global__ void __launch_bounds__(EIG_THREADS, 1)
     tk_eig_kernel(const double* __restrict__ Win, int n, double* __restrict__ V, double* __restrict__ T,
-                  int warm, int vsm, double* __restrict__ lam, int debug) {
+                  int warm, int vsm, double* __restrict__ lam, int debug, const int* gate = nullptr) {
+  if (gate != nullptr && *gate == 0) return;   // fallback use: only when the top-R solver failed
   extern __shared__ double smem[];
   __shared__ double sh[32];
   __shared__ double cs[64], sn[64];
@@ -308,7 +309,8 @@ __global__ void __launch_bounds__(EIG_THREADS, 1)
 constexpr int TOPR_THREADS = 512;   // 1024 measured no faster (barrier-latency bound) and spills
 __global__ void __launch_bounds__(TOPR_THREADS, 1)
     tk_eig_topr_kernel(const double* __restrict__ Win, int n, int R, double* __restrict__ V,
-                       double* __restrict__ lam, double* __restrict__ S5, int debug) {
+                       double* __restrict__ lam, double* __restrict__ S5, int* fail, int debug) {
+  if (threadIdx.x == 0) *fail = 0;
   extern __shared__ double A[];              // n x (n + 1): W, then the reflectors
   long long t_[5];
   t_[0] = clock64();
@@ -463,7 +465,18 @@ __global__ void __launch_bounds__(TOPR_THREADS, 1)
       }
     }
     if (dd[n - 1] == 0.0) dd[n - 1] = eps_piv;
-    for (int i = 0; i < n; ++i) y[i] = 1.0;
+    // a start vector of its own per eigenvector (LAPACK dstein draws one with dlarnv): equal or
+    // nearly equal eigenvalues must not iterate from the same y, or the cluster's Gram-Schmidt
+    // below is left with a zero vector.  Entries in [0.5, 1.5) from a fixed integer hash of (j, i).
+    for (int i = 0; i < n; ++i) {
+      uint32_t h = static_cast<uint32_t>(jv) * 0x9E3779B1u ^ static_cast<uint32_t>(i) * 0x85EBCA77u;
+      h ^= h >> 15;
+      h *= 0x2C1B3C6Du;
+      h ^= h >> 12;
+      h *= 0x297A2D39u;
+      h ^= h >> 15;
+      y[i] = 0.5 + static_cast<double>(h) * (1.0 / 4294967296.0);
+    }
     for (int iter = 0; iter < 3; ++iter) {
       for (int i = 0; i + 1 < n; ++i) {   // apply L^-1 (with the row swaps)
         if (pvt[i] != 0.0) {
@@ -484,6 +497,10 @@ __global__ void __launch_bounds__(TOPR_THREADS, 1)
       }
       double nr = 0.0;
       for (int i = 0; i < n; ++i) nr = fma(y[i], y[i], nr);
+      if (!(nr > 0.0) || !isfinite(nr)) {   // -> the Jacobi fallback
+        *fail = 1;
+        nr = 1.0;
+      }
       nr = 1.0 / sqrt(nr);
       for (int i = 0; i < n; ++i) y[i] *= nr;
     }
@@ -513,7 +530,15 @@ __global__ void __launch_bounds__(TOPR_THREADS, 1)
       }
       double nr = 0.0;
       for (int x = ln; x < n; x += 32) nr = fma(yj[x], yj[x], nr);
-      nr = 1.0 / sqrt(tk_warp_sum(nr));
+      nr = tk_warp_sum(nr);
+      // what is left after removing the earlier members must be a sizeable part of the unit
+      // vector; a (near-)zero or non-finite remainder means inverse iteration did not separate
+      // the cluster: the Jacobi solver takes over (tk_eig_kernel, gated on *fail)
+      if (!(nr > 1e-12) || !isfinite(nr)) {
+        if (ln == 0) *fail = 1;
+        nr = 1.0;
+      }
+      nr = 1.0 / sqrt(nr);
       for (int x = ln; x < n; x += 32) yj[x] *= nr;
       __syncwarp();
     }
@@ -574,9 +599,55 @@ __global__ void tk_select_kernel(const double* __restrict__ V, const double* __r
         const int64_t p = pq / Q, q = pq - p * Q;
         acc = fma(Y[(p * S + y) * Q + q], V[pq * n + idx[j]], acc);
       }
-      v = acc / sqrt(lam[idx[j]]);
+      // a null direction of Y_(n) (λ at the rounding level of the largest): Y v / sqrt(λ) is
+      // noise over ~0, so the column is left zero and tk_complete_kernel fills it with a unit
+      // vector orthogonal to the others (any orthonormal completion is a valid singular basis)
+      const double lj = lam[idx[j]], l0 = lam[idx[0]];
+      v = (lj > 1e-13 * l0 && lj > 0.0) ? acc / sqrt(lj) : 0.0;
     }
     A[e] = v;
+  }
+}
+
+// Columns of A (S x R, orthonormal where nonzero) that tk_select_kernel left zero (null directions
+// on the rank side) become unit vectors orthogonal to every other column: unit vectors e_t,
+// t = j, j+1, ... (mod S), Gram-Schmidt twice against the other columns, the first that keeps
+// a norm > 1/2.  One warp, columns in ascending order (deterministic).
+__global__ void tk_complete_kernel(double* __restrict__ A, int64_t S, int R) {
+  const int lane = threadIdx.x;
+  for (int j = 0; j < R; ++j) {
+    double nr = 0.0;
+    for (int64_t y = lane; y < S; y += 32) nr = fma(A[y * R + j], A[y * R + j], nr);
+    nr = tk_warp_sum(nr);
+    if (nr > 0.25) continue;
+    for (int64_t t = 0; t < S; ++t) {
+      const int64_t hot = (j + t) % S;
+      for (int64_t y = lane; y < S; y += 32) A[y * R + j] = y == hot ? 1.0 : 0.0;
+      __syncwarp();
+      for (int pass = 0; pass < 2; ++pass)
+        for (int i = 0; i < R; ++i) {
+          if (i == j) continue;
+          double dp = 0.0, ni = 0.0;
+          for (int64_t y = lane; y < S; y += 32) {
+            dp = fma(A[y * R + i], A[y * R + j], dp);
+            ni = fma(A[y * R + i], A[y * R + i], ni);
+          }
+          dp = tk_warp_sum(dp);
+          ni = tk_warp_sum(ni);
+          if (ni < 0.25) continue;   // a column still to be completed
+          for (int64_t y = lane; y < S; y += 32) A[y * R + j] -= dp * A[y * R + i];
+          __syncwarp();
+        }
+      double m = 0.0;
+      for (int64_t y = lane; y < S; y += 32) m = fma(A[y * R + j], A[y * R + j], m);
+      m = tk_warp_sum(m);
+      if (m > 0.25) {
+        const double f = 1.0 / sqrt(m);
+        for (int64_t y = lane; y < S; y += 32) A[y * R + j] *= f;
+        __syncwarp();
+        break;
+      }
+    }
   }
 }
 
@@ -978,6 +1049,8 @@ cppp_status leading_vectors(tk_ctx* c, int n, const double* Y, int64_t P, int64_
   else return tfail(c, CPPP_EINVAL, "mode %d: Gram of %lld x %lld exceeds %d", n, (long long)S,
                     (long long)(P * Q), cppp::EIG_MAX);
   const int ne = static_cast<int>(rows ? S : P * Q);
+  if (c->R[n] > ne)   // (tk_init rejects this; the selection would run out of eigenpairs)
+    return tfail(c, CPPP_EINVAL, "mode %d: rank %d exceeds the Gram dimension %d", n, c->R[n], ne);
   static bool attr = false;
   if (!attr) {
     TKCU(c, cudaFuncSetAttribute(cppp::tk_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1021,14 +1094,23 @@ cppp_status leading_vectors(tk_ctx* c, int n, const double* Y, int64_t P, int64_
     cppp::tk_eig_kernel<<<1, cppp::EIG_THREADS, vsm ? 2 * wbytes : wbytes, c->st>>>(
         c->W, ne, Vn, c->V, warm ? 1 : 0, vsm ? 1 : 0, c->lam, tk_debug() ? 1 : 0);
   } else {
+    int* fail = reinterpret_cast<int*>(c->lam + cppp::EIG_MAX);
     cppp::tk_eig_topr_kernel<<<1, cppp::TOPR_THREADS, wbytes + (size_t)cppp::EIG_IB * 6 * ne * 8, c->st>>>(
-        c->W, ne, c->R[n], Vn, c->lam,
-                                                                       c->S5, tk_debug() ? 1 : 0);
+        c->W, ne, c->R[n], Vn, c->lam, c->S5, fail, tk_debug() ? 1 : 0);
+    // the full Jacobi solver, cold, only if the top-R solver flagged an unseparated cluster
+    const bool vsm = 2 * wbytes <= 220 * 1024;
+    cppp::tk_eig_kernel<<<1, cppp::EIG_THREADS, vsm ? 2 * wbytes : wbytes, c->st>>>(
+        c->W, ne, Vn, c->V, 0, vsm ? 1 : 0, c->lam, tk_debug() ? 1 : 0, fail);
+    cppp::note_launch();
   }
   {
     const int64_t ent = S * c->R[n];
     const unsigned g = (unsigned)std::min<int64_t>((ent + 127) / 128, 148 * 4);
     cppp::tk_select_kernel<<<g, 128, 0, c->st>>>(Vn, c->lam, ne, c->R[n], Y, P, S, Q, rows, c->A[n]);
+    if (!rows) {
+      cppp::tk_complete_kernel<<<1, 32, 0, c->st>>>(c->A[n], S, c->R[n]);
+      cppp::note_launch();
+    }
     cppp::tk_sign_kernel<<<1, cppp::EIG_THREADS, 0, c->st>>>(c->A[n], S, c->R[n]);
   }
   cppp::note_launches(3);
@@ -1123,6 +1205,17 @@ cppp_status tk_init(tk_ctx** out, const double* X, int N, const int64_t* s, cons
     numel *= s[n];
     smax = std::max(smax, s[n]);
   }
+  // the factor update takes the Gram of the smaller side of Y_(n) (DESIGN T6): s_n <= 128, or
+  // the rank side Π_{m≠n} R_m <= 128 -- which must hold at least R_n eigenpairs
+  for (int n = 0; n < N; ++n) {
+    int64_t rs = 1;
+    for (int m = 0; m < N; ++m)
+      if (m != n) rs *= R[m];
+    if (s[n] > cppp::EIG_MAX && (rs > cppp::EIG_MAX || R[n] > rs)) {
+      delete c;
+      return CPPP_EINVAL;
+    }
+  }
   auto bail = [&](cppp_status st) {
     tk_destroy(c);
     return st;
@@ -1151,7 +1244,7 @@ cppp_status tk_init(tk_ctx** out, const double* X, int N, const int64_t* s, cons
   for (int n = 0; n < N; ++n) amax = std::max<int64_t>(amax, s[n] * R[n]);
   if (dalloc(c, &c->W, cppp::EIG_MAX * cppp::EIG_MAX) != CPPP_OK ||
       dalloc(c, &c->V, cppp::EIG_MAX * cppp::EIG_MAX) != CPPP_OK ||
-      dalloc(c, &c->lam, cppp::EIG_MAX) != CPPP_OK || dalloc(c, &c->G, canon_elems(c, 0u)) != CPPP_OK ||
+      dalloc(c, &c->lam, cppp::EIG_MAX + 1) != CPPP_OK || dalloc(c, &c->G, canon_elems(c, 0u)) != CPPP_OK ||
       dalloc(c, &c->Gp, canon_elems(c, 0u)) != CPPP_OK || dalloc(c, &c->Aold, amax) != CPPP_OK ||
       dalloc(c, &c->stats, 3 * N + 3) != CPPP_OK ||
       dalloc(c, &c->S5, 6 * cppp::EIG_MAX * cppp::EIG_MAX) != CPPP_OK)

@@ -530,23 +530,100 @@ def test_empty_and_oversized_inputs_rejected():
         cp.cp_init(X, 9, (2,) * 9, 2)
 
 
-@pytest.mark.parametrize("name", ["C2mini", "C3mini", "C5mini"])
-def test_dataflow_factorization_bit_identical(name):
-    """The dataflow Γ factorization (32 < K <= 128, default) applies the same operations to every
-    element in the same order as the barrier-per-pivot kernel it replaced (CPPP_OLD_CHOL=1): the
-    sweeps and the factors must agree bit for bit (separate processes: the switch is read once)."""
-    import json
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    outs = []
-    for old in (False, True):
-        env = dict(os.environ)
-        env.pop("CPPP_OLD_CHOL", None)
-        if old:
-            env["CPPP_OLD_CHOL"] = "1"
-        r = subprocess.run([sys.executable, os.path.join(root, "tools", "trace_bits.py"), name, "12"],
-                           env=env, capture_output=True, text=True, timeout=600, check=True)
-        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
-    assert outs[0] == outs[1]
+@pytest.mark.parametrize("name", ["C1", "C2mini", "C3mini", "C4mini", "C5mini"])
+def test_pp_second_order_matches_oracle(name):
+    """pp_second_order (f3): T2^(n) = Σ_{i<j≠n} M_p^(i,j,n) ×_i dA ×_j dA against the
+    oracle's second_order_term; for N = 3 M~ + T2 is the exact MTTKRP (the expansion ends there)."""
+    cfg, X, Ap = problem(name)
+    A = moved_factors(Ap, 0.05, 9)
+    dA = [a - ap for a, ap in zip(A, Ap)]
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    cp.cp_set_factors(ctx, Ap)
+    cp.pp_build_operators(ctx)
+    cp.cp_update_factors(ctx, A)
+    T2 = cp.pp_second_order(ctx)
+    for n in range(cfg.N):
+        ref = O.second_order_term(X, Ap, dA, n)
+        assert rel(T2[n], ref) < 1e-11, (name, n)
+        if cfg.N == 3:
+            Mt = cp.pp_update(ctx, n)
+            assert rel(Mt + T2[n], O.mttkrp(X, A, n)) < 1e-11, (name, n)
+    # the state is untouched: a PP sweep afterwards equals one on a fresh context
+    b = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    cp.cp_set_factors(b, Ap)
+    cp.pp_build_operators(b)
+    cp.cp_update_factors(b, A)
+    for c in (ctx, b):
+        cp.cp_set_phase_override(c, "pp-approx")
+    ia, ib = cp.als_sweep(ctx, 0.0, 1.0), cp.als_sweep(b, 0.0, 1.0)
+    assert ia["residual_sq"] == ib["residual_sq"]
+    cp.cp_destroy(ctx)
+    cp.cp_destroy(b)
+
+
+def monitor_bound(A, Ap, Mt_colnorms, normX):
+    """max_{n,k} ||X||_F Σ_{S ⊆ others, |S|>=2} Π_{i∈S}||da_k^(i)|| Π_{j∉S}||a_p,k^(j)|| / ||m~_k^(n)||
+    (the certificate of oracle.pp_error_monitor with ||m~|| in the denominator)."""
+    from itertools import combinations as comb
+    N, K = len(A), A[0].shape[1]
+    best = 0.0
+    for n in range(N):
+        others = [i for i in range(N) if i != n]
+        for k in range(K):
+            d = {i: np.linalg.norm(A[i][:, k] - Ap[i][:, k]) for i in others}
+            p = {i: np.linalg.norm(Ap[i][:, k]) for i in others}
+            tot = sum(np.prod([d[i] if i in S else p[i] for i in others])
+                      for size in range(2, len(others) + 1) for S in comb(others, size))
+            best = max(best, normX * tot / Mt_colnorms[n][k])
+    return best
+
+
+@pytest.mark.parametrize("name", ["C1", "C3mini"])
+def test_pp_policy_bound_monitor_and_switch(name):
+    """CPPP_POLICY_BOUND (f3 switching policy): the monitor value after a PP sweep equals the
+    certificate from the oracle's own sweep (||m~|| from its M~); with tol = 1e300 the run is
+    bit-identical to the default policy; with a tol below every monitor value no pp-approx sweep
+    is left (each is replaced by a rebuild)."""
+    cfg, X, Ap = problem(name)
+    A = moved_factors(Ap, 0.02, 10)
+    st = O.State(X, Ap)
+    st.pp_build()
+    st.A = [a.copy() for a in A]
+    st.S = [O.gram(a) for a in st.A]
+    st.dA = [a - ap for a, ap in zip(A, Ap)]
+    norms = []
+    for n in range(cfg.N):
+        M = O.pp_update(st.Mp[n], st.ops, st.dA, n)
+        norms.append(np.linalg.norm(M, axis=0))
+        st._update_mode(n, M, st.A_p[n])
+    want = monitor_bound(st.A, st.A_p, norms, np.sqrt(st.normX_sq))
+    ctx = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+    cp.cp_set_pp_policy(ctx, cp.POLICY_BOUND, 1e300)
+    cp.cp_set_factors(ctx, Ap)
+    cp.pp_build_operators(ctx)
+    cp.cp_update_factors(ctx, A)
+    cp.cp_set_phase_override(ctx, "pp-approx")
+    info = cp.als_sweep(ctx, 0.0, cfg.eps_pp)
+    assert abs(info["pp_bound"] - want) <= 1e-9 * want, (info["pp_bound"], want)
+    cp.cp_destroy(ctx)
+    # whole runs: default vs tol = 1e300 (identical) vs a tiny tol (no pp-approx left)
+    runs = {}
+    for key, pol, tol in (("default", cp.POLICY_EPS_PP, 0.0), ("loose", cp.POLICY_BOUND, 1e300),
+                          ("tight", cp.POLICY_BOUND, 1e-300)):
+        c = cp.cp_init(X, cfg.N, cfg.dims, cfg.K)
+        cp.cp_set_pp_policy(c, pol, tol)
+        cp.cp_set_factors(c, Ap)
+        runs[key] = (cp.als_run(c, 0.0, cfg.eps_pp, 20),
+                     [cp.als_sweep(c, 0.0, cfg.eps_pp) for _ in range(0)])
+        cp.cp_set_factors(c, Ap)
+        host = [cp.als_sweep(c, 0.0, cfg.eps_pp) for _ in range(20)]
+        # the device loop (als_run) and the host loop take the same decisions
+        assert [h["phase"] for h in host] == [d["phase"] for d in runs[key][0]], key
+        assert [h["residual_sq"] for h in host] == [d["residual_sq"] for d in runs[key][0]], key
+        cp.cp_destroy(c)
+    dflt, loose, tight = (runs[k][0] for k in ("default", "loose", "tight"))
+    assert [d["residual_sq"] for d in dflt] == [d["residual_sq"] for d in loose]
+    assert any(d["phase"] == "pp-approx" for d in dflt)
+    assert not any(d["phase"] == "pp-approx" for d in tight)
+    assert any(d["phase"] == "pp-build" for d in tight)
+    assert all(np.isnan(d["pp_bound"]) for d in dflt)

@@ -178,6 +178,19 @@ def test_nccl_transport_single_rank(name):
     A = cp.cp_get_factors(nc)
     for n in range(cfg.N):
         assert rel(M[n], O.mttkrp(X, A, n)) < 1e-11, n
+    # the sharded path with NCCL runs its sweeps from captured graphs, and als_run as ONE device
+    # launch (the collectives inside the WHILE/SWITCH body): the same sweeps, bit for bit, as the
+    # host loop of als_sweep calls, with no host round trip per sweep
+    cp.cp_set_phase_override(nc, cp.PHASE_AUTO)
+    cp.cp_set_factors(nc, A0)
+    host = [cp.als_sweep(nc, 0.0, cfg.eps_pp) for _ in range(12)]
+    for rep in range(2):
+        cp.cp_set_factors(nc, A0)
+        dev = cp.als_run(nc, 0.0, cfg.eps_pp, 12)
+        assert len({d["seconds"] for d in dev}) == 1, cp.lib().cp_last_error(nc.h)
+        for h, d in zip(host, dev):
+            for key in ("phase", "residual_sq", "grad_norm_sum", "max_rel_dA"):
+                assert h[key] == d[key], (rep, key, h, d)
     cp.cp_destroy(nc)
     cp.cp_destroy(plain)
 

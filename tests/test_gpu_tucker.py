@@ -173,11 +173,66 @@ def test_tucker_edge_shapes(dims, ranks):
 
 def test_tucker_gram_too_large_rejected():
     """Both sides of Y_(n) above 128 (s_0 = 200, prod of the other ranks = 11 x 13 = 143): the
-    factor update is refused with CPPP_EINVAL instead of running out of the one-CTA solver."""
+    problem is refused at tk_init with CPPP_EINVAL instead of running out of the one-CTA solver."""
     dims, ranks = (200, 12, 14), (3, 11, 13)
     X, A = problem(dims, ranks, 13)
-    ctx = cp.tk_init(X, dims, ranks)
-    cp.tk_set_factors(ctx, A)
-    with pytest.raises(cp.CpppError):
-        cp.tk_sweep(ctx, 0.0, 0.0)
+    with pytest.raises(cp.CpppError) as e:
+        cp.tk_init(X, dims, ranks)
+    assert e.value.status == -1
+
+
+def lowrank_tensor(dims, core_ranks, seed, equal=True):
+    """X = G ×_1 U1 ×_2 U2 ... with orthonormal U_n (s_n x r_n) and a super-diagonal core of
+    ones (equal=True): every Gram of Y_(n) = X_(n) X_(n)ᵀ then has the eigenvalue 1 repeated."""
+    r = np.random.default_rng(seed)
+    U = [np.linalg.qr(r.standard_normal((s, q)))[0] for s, q in zip(dims, core_ranks)]
+    q = min(core_ranks)
+    G = np.zeros(core_ranks)
+    for i in range(q):
+        G[(i,) * len(dims)] = 1.0 if equal else 1.0 + i
+    X = G
+    for n, u in enumerate(U):
+        X = np.moveaxis(np.tensordot(u, np.moveaxis(X, n, 0), axes=(1, 0)), 0, n)
+    return np.ascontiguousarray(X), U
+
+
+def check_orthonormal_and_span(A, U):
+    for a, u in zip(A, U):
+        assert np.all(np.isfinite(a))
+        assert np.abs(a.T @ a - np.eye(a.shape[1])).max() < 1e-10
+        assert np.linalg.norm(u - a @ (a.T @ u)) < 1e-8 * np.linalg.norm(u)
+
+
+def test_tucker_repeated_eigenvalues_stay_orthonormal():
+    """equal (and zero) eigenvalues among the R_n leading ones -- a super-diagonal core
+    of ones gives the eigenvalue 1 three times and R_n = 4 adds a zero one.  The factors must stay
+    finite and orthonormal and span the true subspaces (the top-R solver's clusters get distinct
+    start vectors; an unseparated cluster falls back to the Jacobi solver)."""
+    dims = (20, 18, 16)
+    X, U = lowrank_tensor(dims, (3, 3, 3), 21)
+    ctx = cp.tk_init(X, dims, (4, 4, 4))
+    cp.tk_hosvd(ctx)
+    check_orthonormal_and_span(cp.tk_get_factors(ctx), U)
+    for _ in range(3):
+        cp.tk_sweep(ctx, 0.0, 0.1)
+    check_orthonormal_and_span(cp.tk_get_factors(ctx), U)
     cp.tk_destroy(ctx)
+
+
+def test_tucker_rank_side_null_directions_completed():
+    """s_0 = 200 > 128: mode 0's factor comes from the rank-side Gram (R_1 R_2 = 4 x 4), which has
+    rank 2 here (multilinear rank 2): two null directions.  They are completed to an orthonormal
+    basis (no division by sqrt(0)); a rank that exceeds the rank side is rejected at tk_init."""
+    dims = (200, 6, 5)
+    X, U = lowrank_tensor(dims, (2, 2, 2), 22, equal=False)
+    ctx = cp.tk_init(X, dims, (4, 2, 2))
+    r = np.random.default_rng(23)
+    A0 = [np.linalg.qr(r.standard_normal((s, q)))[0].copy() for s, q in zip(dims, (4, 2, 2))]
+    cp.tk_set_factors(ctx, A0)
+    for _ in range(3):
+        cp.tk_sweep(ctx, 0.0, 0.1)
+    A = cp.tk_get_factors(ctx)
+    check_orthonormal_and_span(A, U)
+    cp.tk_destroy(ctx)
+    with pytest.raises(cp.CpppError):
+        cp.tk_init(X, dims, (5, 2, 2))   # R_0 = 5 > R_1 R_2 = 4 with s_0 > 128

@@ -507,3 +507,25 @@ def test_trace_residual_sq_is_explicit_residual_after_regular_sweeps():
         st.dt_sweep()
         explicit = float(np.sum((X - O.kruskal_full(st.A)) ** 2))
         assert abs(st.residual_sq() - explicit) <= 1e-12 * nx2
+
+
+@pytest.mark.parametrize("dims", [(5, 4, 6, 3), (4, 3, 5, 3, 4)])
+def test_second_order_term_multilinear_remainder(dims):
+    """Multilinearity of M^(n) in the factors: with A = A_p + dA,
+    M^(n)(A) = Σ_{S ⊆ modes≠n} M^(n)(dA on S, A_p elsewhere).  |S| = 0, 1 are the PP update
+    (P:553), |S| = 2 is second_order_term; the rest (|S| >= 3) is computed here by plain MTTKRPs
+    with mixed factor lists, so M - M~ - T2 must equal that remainder."""
+    from itertools import combinations as comb
+    N = len(dims)
+    r, X, Ap, ops, Mp = setup_pp(dims, 3, 31)
+    dA = [0.2 * r.standard_normal(a.shape) for a in Ap]
+    A = [a + d for a, d in zip(Ap, dA)]
+    for n in range(N):
+        others = [m for m in range(N) if m != n]
+        rem = np.zeros_like(Mp[n])
+        for size in range(3, N):
+            for S in comb(others, size):
+                F = [dA[m] if m in S else Ap[m] for m in range(N)]
+                rem = rem + O.mttkrp(X, F, n)
+        got = O.mttkrp(X, A, n) - O.pp_update(Mp[n], ops, dA, n) - O.second_order_term(X, Ap, dA, n)
+        assert rel(got, rem) < 1e-10, n
