@@ -57,7 +57,8 @@ typedef enum {
 #define CPPP_FLAG_BORROW_TENSOR 1u  /* X is a device pointer the caller keeps alive; not copied */
 #define CPPP_FLAG_SIMT_TTM      2u  /* force the SIMT (non-tensor-core) TTM kernel (testing) */
 #define CPPP_FLAG_PROFILE       4u  /* time each kernel class with CUDA events (cppp_kernel_stats) */
-#define CPPP_FLAG_NO_FUSED_TTV  8u  /* reserved: accepted, no effect (every child is its own multi-TTV pass) */
+#define CPPP_FLAG_NO_FUSED_TTV  8u  /* order 4: build the PP operators through Def. pptree's level-1
+                                        nodes instead of the fused level 1 -> level 2 GEMMs (A/B testing) */
 #define CPPP_FLAG_NO_GRAPH     16u  /* run sweeps eagerly instead of replaying captured CUDA graphs */
 #define CPPP_FLAG_NO_KRP       32u  /* regular DT sweep: single-mode first-level TTMs instead of one
                                         multi-mode (Khatri-Rao) GEMM per half (testing) */

@@ -367,7 +367,9 @@ TtmOpts side_gemm_opts() {
 }
 
 bool reuse12(const cppp_ctx* c) {
-  return c->N == 3 && c->q < 0 && !(c->flags & CPPP_FLAG_NO_OP_REUSE);
+  // (CPPP_POLICY_BOUND can rebuild right after a PP sweep, where ops[1][2] is not at A_p: off)
+  return c->N == 3 && c->q < 0 && !(c->flags & CPPP_FLAG_NO_OP_REUSE) &&
+         c->policy == CPPP_POLICY_EPS_PP;
 }
 int64_t node_elems(cppp_ctx* c, uint32_t mask) {
   int64_t e = c->K;
@@ -785,6 +787,82 @@ cppp_status build_singles(cppp_ctx* c) {
   return CPPP_OK;
 }
 
+// Order 4, unsharded, s_3 % 128 == 0 (C5): the construction tree's level 1 -> level 2 fused into
+// three GEMMs.  Level-1 node "contract a" (a = 0, 1, 2; kept modes in physical
+// order, the last one f = 3) feeds two of its leaves from the GEMM epilogue: the FAST leaf
+// (contract f) and the LOOP leaf (contract l); the third kept mode is o.  The choice (a, l, o) =
+// (0, 1, 2), (1, 2, 0), (2, 0, 1) covers the six leaves exactly once:
+//   a=0: (1,2) fast, (2,3) loop;  a=1: (0,2) fast, (0,3) loop;  a=2: (0,1) fast, (1,3) loop.
+// Def. pptree's leaves are the same operators (L24: any tree gives the same values);
+// no s^3 K level-1 node is ever written (C5: 16 GiB).  CPPP_FLAG_NO_FUSED_TTV: the plain tree.
+bool fused_build_ok(const cppp_ctx* c) {
+  if (c->N != 4 || c->q >= 0 || (c->flags & (CPPP_FLAG_NO_FUSED_TTV | CPPP_FLAG_SIMT_TTM))) return false;
+  for (int a = 0; a < 3; ++a) {
+    int64_t B = 1, R = 1;
+    for (int v = 0; v < 4; ++v) {
+      if (v < a) B *= c->dl[v];
+      if (v > a) R *= c->dl[v];
+    }
+    if (!ttm_fused_ok(B, c->dl[a], R, c->K, c->dl[3])) return false;
+  }
+  return true;
+}
+
+cppp_status run_fused_build(cppp_ctx* c) {
+  const int K = c->K;
+  const int64_t* d = c->dl;
+  static const int cover[3][2] = {{1, 2}, {2, 0}, {0, 1}};   // (l, o) per contracted mode a
+  for (int a = 0; a < 3; ++a) {
+    const int l = cover[a][0], o = cover[a][1], f = 3;
+    int64_t B = 1, R = 1;
+    for (int v = 0; v < 4; ++v) {
+      if (v < a) B *= d[v];
+      if (v > a) R *= d[v];
+    }
+    const int64_t S = d[a];
+    auto tile_stride = [&](int v) {   // flattened kept index stride of mode v, in 128-row tiles
+      int64_t st = 1;
+      for (int u = v + 1; u < 4; ++u)
+        if (u != a) st *= d[u];
+      return st / 128;
+    };
+    TtmFused fz;
+    fz.o_str = tile_stride(o);
+    fz.l_str = tile_stride(l);
+    fz.n_o = d[o];
+    fz.n_l = d[l];
+    fz.sf = d[f];
+    const int64_t units0 = d[o] * (d[f] / 128);
+    fz.nP = std::max<int64_t>(1, std::min<int64_t>(d[l], (148 * 7 + units0 - 1) / units0));
+    fz.Af = c->Ap[f];
+    fz.Al = c->Ap[l];
+    fz.fl_o = o < l ? d[l] : 1;
+    fz.fl_l = l < o ? d[o] : 1;
+    const int64_t fast_rows = d[o] * d[l], loop_rows = d[o] * d[f];
+    const size_t mk = c->stack.mark();
+    fz.fast = c->stack.push((size_t)(d[f] / 128) * fast_rows * K);
+    fz.loop = c->stack.push((size_t)fz.nP * loop_rows * K);
+    if (!c->dry) {
+      CUCHK(c, ttm_prepare(S, c->Ap[a], K, c->Fpad, c->st));
+      {
+        Prof p(c, CPPP_K_TTM, 2.0 * B * S * R * K + 4.0 * B * R * K,
+               8.0 * (B * S * R + ((d[f] / 128) * fast_rows + fz.nP * loop_rows) * K));
+        CUCHK(c, launch_ttm_fused(c->X, B, S, R, K, c->Fpad, fz, c->st));
+      }
+      const int lo = std::min(o, l), hi = std::max(o, l);
+      {
+        const double n1 = (double)fast_rows * K, n2 = (double)loop_rows * K;
+        Prof p(c, CPPP_K_TTV, n1 * (d[f] / 128 - 1) + n2 * (fz.nP - 1),
+               8.0 * (n1 * (d[f] / 128 + 1) + n2 * (fz.nP + 1)));
+        CUCHK(c, launch_sum_parts(fz.fast, (int)(d[f] / 128), fast_rows * K, c->ops[lo][hi], c->st));
+        CUCHK(c, launch_sum_parts(fz.loop, (int)fz.nP, loop_rows * K, c->ops[o][f], c->st));
+      }
+    }
+    c->stack.release(mk);
+  }
+  return CPPP_OK;
+}
+
 cppp_status run_pp_build(cppp_ctx* c, bool have12 = false) {
   const int N = c->N, K = c->K;
   if (!c->dry) {
@@ -794,9 +872,13 @@ cppp_status run_pp_build(cppp_ctx* c, bool have12 = false) {
       CUCHK(c, cudaMemsetAsync(c->dA[n], 0, sizeof(double) * c->s[n] * K, c->st));
     }
   }
-  PPTree t{c};
-  t.have12 = have12 && reuse12(c);
-  STCHK(t.run());
+  if (fused_build_ok(c)) {
+    STCHK(run_fused_build(c));
+  } else {
+    PPTree t{c};
+    t.have12 = have12 && reuse12(c);
+    STCHK(t.run());
+  }
   // leaves that contracted the sharded mode hold partial sums: all-reduce them, one call over
   // their contiguous span (SURVEY C-b)
   if (c->q >= 0) STCHK(allreduce(c, c->ops_red, c->ops_red_count));
@@ -1784,6 +1866,7 @@ cppp_status cp_set_pp_policy(cppp_ctx* c, int policy, double tol) {
   }
   c->policy = policy;
   c->policy_tol = tol;
+  c->op12_fresh = false;   // (the order-3 operator reuse depends on the policy: reuse12)
   return CPPP_OK;
 }
 

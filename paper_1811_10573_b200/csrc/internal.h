@@ -97,6 +97,26 @@ int ttm_ld(int K);
 cudaError_t launch_ttm_core(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
                             int K, double* out, const double* Fpad, bool force_simt,
                             cudaStream_t st, TtmOpts topt = TtmOpts{});
+// Fused PP-construction level 1 -> level 2 (order 4): the m-contiguous GEMM
+// T = X ×_a F (F padded in Fpad, as ttm_prepare leaves it) whose epilogue contracts every tile of T
+// into two leaves -- the fast leaf over the last kept mode f (s_f % 128 == 0; nh = s_f / 128
+// block partials) and the loop leaf over mode l (nP x_l-chunk partials); T itself is never
+// written.  Then launch_sum_parts adds the partials in order.
+struct TtmFused {
+  int64_t o_str, l_str;    // tile strides (flattened kept index / 128) of x_o, x_l
+  int64_t n_o, n_l, sf;    // extents of modes o, l, f
+  int64_t nP;              // x_l chunks (loop-leaf partials)
+  const double* Af;        // s_f x K
+  const double* Al;        // s_l x K
+  double* fast;            // [s_f / 128][n_o n_l][K]
+  int64_t fl_o, fl_l;      // fast-leaf row strides of x_o, x_l
+  double* loop;            // [nP][n_o s_f][K]
+};
+bool ttm_fused_ok(int64_t B, int64_t S, int64_t R, int K, int64_t sf);
+cudaError_t launch_ttm_fused(const double* X, int64_t B, int64_t S, int64_t R, int K, const double* Fpad,
+                             const TtmFused& f, cudaStream_t st);
+// out[e] = Σ_{q < np} part[q n + e] (q ascending)
+cudaError_t launch_sum_parts(const double* part, int np, int64_t n, double* out, cudaStream_t st);
 cudaError_t launch_ttm_simt(const double* X, int64_t B, int64_t S, int64_t R,
                             const double* F, int K, double* out, cudaStream_t st);
 bool ttm_dmma_supported(int64_t B, int64_t S, int64_t R, int K);

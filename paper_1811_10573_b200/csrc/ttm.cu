@@ -500,6 +500,251 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------- fused level 1 -> level 2 (f1)
+// The PP construction tree of an order-4 tensor without its s^3 K level-1 nodes in HBM (SURVEY
+// NEXT f1; P:700-719 amortises exactly these contractions).  One GEMM contracts mode a of X
+// (T = X ×_a A_p^(a), the level-1 node) and its epilogue contracts each 128-row tile of T
+// once more, rank-diagonally, into two leaves:
+//   * the FAST leaf contracts the last kept mode f: a tile is 128 consecutive x_f (s_f % 128 ==
+//     0), so the tile's rows weighted by A_p^(f)[x_f][k] and summed give a partial of
+//     M_p(kept \ f) for this x_f block; the nh = s_f / 128 block partials go to separate buffers
+//     and are added in block order afterwards;
+//   * the LOOP leaf contracts a second kept mode l: a unit is a run of tiles that differ only in
+//     x_l (ascending), and each tile's rows, weighted by A_p^(l)[x_l][k], are accumulated into the
+//     unit's slice of a partial of M_p(o, f) (o = the third kept mode) -- read-modify-write of a
+//     128 x K slice that stays in L2; runs over nP x_l chunks leave nP partials added in order.
+// Tile t of the GEMM (m-contiguous, R % 128 == 0: tiles never straddle a batch) covers the
+// flattened kept index [128 t, 128 t + 128): t = x_o lstr_o + x_l lstr_l + h with the strides in
+// tiles (the flattened row-major index of the kept modes / 128).  Deterministic: every sum has a
+// fixed order (rows inside a tile by a fixed shuffle tree then warps in order, x_l ascending inside
+// a run, blocks and runs by the combine kernel).
+struct FusedArgs {
+  int64_t o_str, l_str;          // tile strides of x_o and x_l
+  int64_t n_o, n_l, nh;          // extents: x_o, x_l, fast blocks (s_f / 128)
+  int64_t run;                   // tiles per unit (x_l chunk length)
+  int64_t nP;                    // x_l chunks
+  const double* Af;              // A_p^(f), s_f x K
+  const double* Al;              // A_p^(l), s_l x K
+  double* fast;                  // [nh][leaf rows][K]  (leaf (kept \ f))
+  int64_t fl_o, fl_l;            // fast leaf row strides of x_o, x_l
+  double* loop;                  // [nP][n_o * s_f][K]  (leaf (o, f))
+  int64_t sf;                    // s_f
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    ttm_fused_kernel(const __grid_constant__ CUtensorMap tmF, const __grid_constant__ CUtensorMap tmX4,
+                     int64_t mtiles, int S, int K, int stages, unsigned long long* __restrict__ tile_counter,
+                     const FusedArgs fa) {
+  using C = Cfg<NT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + stages * C::STAGE);
+  uint64_t* empty = full + stages;
+  double* red = reinterpret_cast<double*>(empty + stages);   // [NWARP][BN] fast-leaf partials
+  double* lacc = red + NWARP * C::BN;                           // [BM][BN + 1] loop-leaf slice
+  constexpr int LP = C::BN + 1;
+  __shared__ long long stage_tile[16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < stages; ++st) {
+      mbar_init(smem_u32(&full[st]), 1);
+      mbar_init(smem_u32(&empty[st]), NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  const int nk = (S + BK - 1) / BK;
+  const long long nunits = fa.n_o * fa.nh * fa.nP;
+  // unit u -> (x_o, h, chunk p); tile i of the run -> x_l = p run + i
+  auto tile_of = [&](long long u, int64_t i, int64_t* xl_out, int64_t* xo, int64_t* h, int64_t* p) {
+    *p = u % fa.nP;
+    const long long r = u / fa.nP;
+    *h = r % fa.nh;
+    *xo = r / fa.nh;
+    const int64_t xl = *p * fa.run + i;
+    *xl_out = xl;
+    return *xo * fa.o_str + xl * fa.l_str + *h;
+  };
+  auto run_len = [&](int64_t p) {
+    const int64_t lo = p * fa.run, hi = lo + fa.run < fa.n_l ? lo + fa.run : fa.n_l;
+    return hi - lo;
+  };
+  if (warp == NWARP) {   // ---------------- TMA producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX4)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmF)) : "memory");
+      int64_t it = 0;
+      while (true) {
+        const long long unit = static_cast<long long>(atomicAdd(tile_counter, 1ull));
+        if (unit >= nunits) {
+          const int st = static_cast<int>(it % stages);
+          const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+          if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+          stage_tile[st] = -1;
+          mbar_arrive(smem_u32(&full[st]));
+          break;
+        }
+        int64_t xl, xo, h, p;
+        tile_of(unit, 0, &xl, &xo, &h, &p);
+        const int64_t L = run_len(p);
+        for (int64_t i = 0; i < L; ++i) {
+          const int64_t t = tile_of(unit, i, &xl, &xo, &h, &p);
+          const int64_t b = t / mtiles, m0 = (t - b * mtiles) * BM;
+          for (int kt = 0; kt < nk; ++kt, ++it) {
+            const int st = static_cast<int>(it % stages);
+            const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+            if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
+            if (kt == 0) stage_tile[st] = unit * 65536 + i;
+            const uint32_t fb = smem_u32(&full[st]);
+            mbar_expect_tx(fb, C::STAGE);
+            const uint32_t sx = smem_u32(base + st * C::STAGE);
+            tma_4d(sx, &tmX4, 0, kt * BK, static_cast<int>(m0 / 16), static_cast<int>(b), fb);
+            tma_3d(sx + C::XBYTES, &tmF, 0, kt * BK, 0, fb);
+          }
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumers (the GEMM part is ttm_dmma_kernel's m-contiguous path)
+  const int g = lane >> 2, t4 = lane & 3;
+  const int mbox = warp >> 1, mrow = 8 * (warp & 1) + g;
+  const int mloc = 16 * mbox + mrow;   // this thread's row of the tile
+  int64_t it = 0;
+  while (true) {
+    {
+      const int st = static_cast<int>(it % stages);
+      mbar_wait(smem_u32(&full[st]), static_cast<uint32_t>((it / stages) & 1));
+    }
+    const long long code = stage_tile[static_cast<int>(it % stages)];
+    if (code < 0) break;
+    const long long unit = code / 65536;
+    const int64_t i = code - unit * 65536;
+    int64_t xl, xo, h, p;
+    tile_of(unit, i, &xl, &xo, &h, &p);
+    double acc[NT][2];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
+    for (int kt = 0; kt < nk; ++kt, ++it) {
+      const int st = static_cast<int>(it % stages);
+      const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+      if (kt > 0) mbar_wait(smem_u32(&full[st]), ph);
+      const uint32_t sx = smem_u32(base + st * C::STAGE);
+      const uint32_t sf = sx + C::XBYTES;
+      const int qmax = (S - kt * BK) > 8 ? 2 : 1;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (q >= qmax) break;
+        double a[2];
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int row = 8 * q + 2 * t4 + kk;
+          asm volatile("ld.shared.f64 %0, [%1];"
+                       : "=d"(a[kk])
+                       : "r"(sx + mbox * 2048 + row * 128 + (((mrow >> 1) ^ (row & 7)) << 4) +
+                             ((mrow & 1) << 3)));
+        }
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int row = 8 * q + 2 * t4 + kk;
+          const uint32_t frow = sf + row * 128 + ((g ^ (row & 7)) << 4);
+#pragma unroll
+          for (int c = 0; c < NT / 2; ++c) {
+            double b0, b1;
+            lds2(b0, b1, frow + c * 2048);
+            dmma(acc[2 * c], a[kk], b0);
+            dmma(acc[2 * c + 1], a[kk], b1);
+          }
+          if (NT & 1) {
+            constexpr int c = NT / 2;
+            double b0;
+            asm volatile("ld.shared.f64 %0, [%1];"
+                         : "=d"(b0)
+                         : "r"(sf + c * 2048 + row * 128 + (((g >> 1) ^ (row & 7)) << 4) + ((g & 1) << 3)));
+            dmma(acc[NT - 1], a[kk], b0);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
+    }
+    // ---------------- epilogue: (row mloc) x (columns 16c + 4t4 + {0..3}, and 16(NT/2) + 2t4 + {0,1})
+    const int64_t xf = h * BM + mloc;
+    const double* af = fa.Af + xf * K;
+    const double* al = fa.Al + xl * K;
+    double* lrow = fa.loop + (p * fa.n_o * fa.sf + xo * fa.sf + xf) * static_cast<int64_t>(K);
+    double* lsm = lacc + mloc * LP;   // this thread's row of the run's loop-leaf slice (smem)
+    const bool last = (i + 1 == run_len(p));
+    // value of (tile pair c, element e) -> column and accumulator
+#pragma unroll
+    for (int c = 0; c < (NT + 1) / 2; ++c) {
+      const bool pair = 2 * c + 1 < NT;
+      double v[4];
+      int n[4];
+      if (pair) {
+        v[0] = acc[2 * c][0];
+        v[1] = acc[2 * c + 1][0];
+        v[2] = acc[2 * c][1];
+        v[3] = acc[2 * c + 1][1];
+        for (int e = 0; e < 4; ++e) n[e] = 16 * c + 4 * t4 + e;
+      } else {
+        v[0] = acc[2 * c][0];
+        v[1] = acc[2 * c][1];
+        v[2] = v[3] = 0.0;
+        n[0] = 16 * c + 2 * t4;
+        n[1] = n[0] + 1;
+        n[2] = n[3] = K;   // none
+      }
+      double fsum[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool ok = n[e] < K;
+        // loop leaf: x_l ascending inside the run (the first tile initialises the slice)
+        if (ok) {
+          const double w = __ldg(al + n[e]);
+          const double x = i == 0 ? v[e] * w : fma(v[e], w, lsm[n[e]]);
+          if (last) lrow[n[e]] = x;
+          else lsm[n[e]] = x;
+        }
+        fsum[e] = ok ? v[e] * __ldg(af + n[e]) : 0.0;
+      }
+      // fast leaf: the warp's 8 rows (g) by a fixed xor tree, then the warps in order
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        fsum[e] += __shfl_xor_sync(0xffffffffu, fsum[e], 4);
+        fsum[e] += __shfl_xor_sync(0xffffffffu, fsum[e], 8);
+        fsum[e] += __shfl_xor_sync(0xffffffffu, fsum[e], 16);
+      }
+      if (g == 0) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (n[e] < K) red[warp * C::BN + n[e]] = fsum[e];
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NWARP * 32) : "memory");   // consumer warps only
+    if (threadIdx.x < K) {
+      const int n = threadIdx.x;
+      double s = 0.0;
+      // warps in row order: warp w holds rows 16 (w >> 1) + 8 (w & 1) + g
+      for (int w = 0; w < NWARP; ++w) s += red[w * C::BN + n];
+      fa.fast[(h * (fa.n_o * fa.n_l) + xo * fa.fl_o + xl * fa.fl_l) * static_cast<int64_t>(K) + n] = s;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NWARP * 32) : "memory");
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(tile_counter + 1, 1ull) == gridDim.x - 1) {
+      tile_counter[0] = 0ull;
+      tile_counter[1] = 0ull;
+      __threadfence();
+    }
+  }
+}
+
 // ---------------------------------------------------------------- SIMT fallback
 // One thread per output (b, r, n); X read with r fastest across the warp.
 __global__ void ttm_simt_kernel(const double* __restrict__ X, int64_t B, int64_t S, int64_t R,
@@ -515,6 +760,155 @@ __global__ void ttm_simt_kernel(const double* __restrict__ X, int64_t B, int64_t
     for (int64_t x = 0; x < S; ++x) acc = fma(xp[x * R], F[x * K + n], acc);
     out[br * K + n] = acc;
   }
+}
+
+// ---------------------------------------------------------------- skinny GEMMs (K <= 16)
+// Shapes the TMA GEMM cannot take (an odd row stride: s = 25 for the compact Laplacian)
+// with a small rank: 2 K flops per 8-byte element of X, far below the FP64 ridge (5.7 flop/B), so
+// the bound is HBM and the tensor core has nothing to win -- what matters is streaming X once,
+// coalesced.  KB >= K accumulators per thread, x in ascending order (as the GEMM).
+//   m-contiguous (R > 1): thread per (b, r); a warp reads 32 consecutive r of one x row (a
+//     coalesced 256-byte run), the factor row F[x][0..K) is a broadcast load.
+template <int KB>
+__global__ void __launch_bounds__(256)
+    ttm_skinny_mc_kernel(const double* __restrict__ X, int64_t B, int64_t S, int64_t R,
+                         const double* __restrict__ F, int K, double* __restrict__ out) {
+  pdl_wait();
+  const int64_t total = B * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / R, r = e - b * R;
+    const double* xp = X + b * S * R + r;
+    double acc[KB];
+#pragma unroll
+    for (int n = 0; n < KB; ++n) acc[n] = 0.0;
+    int64_t x = 0;
+    for (; x + 4 <= S; x += 4) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(xp + (x + u) * R);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int n = 0; n < KB; ++n)
+          if (n < K) acc[n] = fma(v[u], __ldg(F + (x + u) * K + n), acc[n]);
+    }
+    for (; x < S; ++x) {
+      const double v = __ldcs(xp + x * R);
+#pragma unroll
+      for (int n = 0; n < KB; ++n)
+        if (n < K) acc[n] = fma(v, __ldg(F + x * K + n), acc[n]);
+    }
+    double* o = out + e * K;
+#pragma unroll
+    for (int n = 0; n < KB; ++n)
+      if (n < K) o[n] = acc[n];
+  }
+}
+
+//   k-contiguous (R == 1, rows of S doubles): a CTA stages SK_ROWS consecutive rows -- one
+//     contiguous run of X -- through shared memory with coalesced loads, then thread = row
+//     (odd row pitch S: conflict-free for odd S), the factor in shared memory.
+constexpr int SK_ROWS = 128;
+template <int KB>
+__global__ void __launch_bounds__(SK_ROWS)
+    ttm_skinny_kc_kernel(const double* __restrict__ X, int64_t B, int S, const double* __restrict__ F,
+                         int K, double* __restrict__ out) {
+  pdl_wait();
+  extern __shared__ double sk[];   // [SK_ROWS * S] rows | [S * K] factor
+  double* fs = sk + (int64_t)SK_ROWS * S;
+  for (int e = threadIdx.x; e < S * K; e += SK_ROWS) fs[e] = F[e];
+  for (int64_t b0 = (int64_t)blockIdx.x * SK_ROWS; b0 < B; b0 += (int64_t)gridDim.x * SK_ROWS) {
+    const int nr = static_cast<int>(B - b0 < SK_ROWS ? B - b0 : SK_ROWS);
+    const double* src = X + b0 * S;
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * S; e += SK_ROWS) sk[e] = __ldcs(src + e);
+    __syncthreads();
+    if (threadIdx.x < nr) {
+      const double* row = sk + threadIdx.x * S;
+      double acc[KB];
+#pragma unroll
+      for (int n = 0; n < KB; ++n) acc[n] = 0.0;
+      for (int x = 0; x < S; ++x) {
+        const double v = row[x];
+#pragma unroll
+        for (int n = 0; n < KB; ++n)
+          if (n < K) acc[n] = fma(v, fs[x * K + n], acc[n]);
+      }
+      double* o = out + (b0 + threadIdx.x) * K;
+#pragma unroll
+      for (int n = 0; n < KB; ++n)
+        if (n < K) o[n] = acc[n];
+    }
+  }
+}
+
+//   k-contiguous with long rows (the Khatri-Rao first level: S = s^3 = 15625 for LAP): warp per
+//     row, lanes on consecutive x (coalesced), the lane partials added by a fixed xor tree.
+template <int KB>
+__global__ void __launch_bounds__(256)
+    ttm_skinny_rows_kernel(const double* __restrict__ X, int64_t B, int64_t S, const double* __restrict__ F,
+                           int K, double* __restrict__ out) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b = w0; b < B; b += nw) {
+    const double* row = X + b * S;
+    double acc[KB];
+#pragma unroll
+    for (int n = 0; n < KB; ++n) acc[n] = 0.0;
+    for (int64_t x = lane; x < S; x += 32) {
+      const double v = __ldcs(row + x);
+#pragma unroll
+      for (int n = 0; n < KB; ++n)
+        if (n < K) acc[n] = fma(v, __ldg(F + x * K + n), acc[n]);
+    }
+#pragma unroll
+    for (int n = 0; n < KB; ++n)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[n] += __shfl_xor_sync(0xffffffffu, acc[n], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int n = 0; n < KB; ++n)
+        if (n < K) out[b * K + n] = acc[n];
+    }
+  }
+}
+
+template <int KB>
+cudaError_t run_skinny(const double* X, int64_t B, int64_t S, int64_t R, const double* F, int K,
+                       double* out, cudaStream_t st) {
+  if (R > 1) {
+    int64_t blocks = (B * R + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    cudaError_t e = launch_pdl(ttm_skinny_mc_kernel<KB>, dim3((unsigned)blocks), dim3(256), 0, st, X, B, S, R,
+                               F, K, out);
+    note_launch();
+    return e;
+  }
+  const size_t smem = sizeof(double) * (static_cast<size_t>(SK_ROWS) * S + S * K);
+  if (smem > 200 * 1024) {
+    int64_t blocks = (B * 32 + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    cudaError_t e = launch_pdl(ttm_skinny_rows_kernel<KB>, dim3((unsigned)blocks), dim3(256), 0, st, X, B, S, F,
+                               K, out);
+    note_launch();
+    return e;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(ttm_skinny_kc_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int64_t blocks = (B + SK_ROWS - 1) / SK_ROWS;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  cudaError_t e = launch_pdl(ttm_skinny_kc_kernel<KB>, dim3((unsigned)blocks), dim3(SK_ROWS), smem, st, X, B,
+                             (int)S, F, K, out);
+  note_launch();
+  return e;
 }
 
 // ---------------------------------------------------------------- host side
@@ -722,21 +1116,139 @@ cudaError_t dispatch_nt(int nt, const double* X, int64_t B, int64_t S, int64_t R
   }
 }
 
+template <int NT>
+cudaError_t run_fused(const double* X, int64_t B, int64_t S, int64_t R, const double* Fp, int K,
+                      unsigned long long* counter, const FusedArgs& fa, cudaStream_t st) {
+  using C = Cfg<NT>;
+  // the fast-leaf reduction buffer and the run's loop-leaf slice live beside the stage ring
+  const int red_bytes = NWARP * C::BN * 8 + BM * (C::BN + 1) * 8;
+  int stages = C::MAX_STAGES;
+  while (stages > 2 && C::smem(stages) + red_bytes > 220 * 1024) --stages;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(ttm_fused_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         220 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  CUtensorMap tmX4, tmF;
+  {
+    cuuint64_t dims[4] = {16, (cuuint64_t)S, (cuuint64_t)(R / 16), (cuuint64_t)B};
+    cuuint64_t str[3] = {(cuuint64_t)R * 8, 128, (cuuint64_t)(S * R) * 8};
+    cuuint32_t box[4] = {16, 16, 8, 1};
+    if (!make_map(&tmX4, X, 4, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  {
+    cuuint64_t dims[3] = {16, (cuuint64_t)S, (cuuint64_t)(C::BNP / 16)};
+    cuuint64_t str[2] = {(cuuint64_t)C::BNP * 8, 128};
+    cuuint32_t box[3] = {16, 16, (cuuint32_t)(C::BNP / 16)};
+    if (!make_map(&tmF, Fp, 3, dims, str, box)) return cudaErrorInvalidValue;
+  }
+  const int smem = C::smem(stages) + red_bytes;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long long nunits = fa.n_o * fa.nh * fa.nP;
+  const long long grid = nunits < sms ? nunits : sms;
+  static const bool dbg = getenv("CPPP_DEBUG_TTM") != nullptr;
+  if (dbg)
+    fprintf(stderr, "ttm fused B %lld S %lld R %lld K %d: units %lld (run %lld) grid %lld stages %d\n",
+            (long long)B, (long long)S, (long long)R, K, nunits, (long long)fa.run, grid, stages);
+  cudaError_t e = launch_pdl(ttm_fused_kernel<NT>, dim3((unsigned)grid), dim3(NTHREADS), smem, st, tmF, tmX4,
+                             R / BM, (int)S, K, stages, counter, fa);
+  note_launch();
+  return e;
+}
+
+template <int NT = 1>
+cudaError_t dispatch_fused(int nt, const double* X, int64_t B, int64_t S, int64_t R, const double* Fp,
+                           int K, unsigned long long* counter, const FusedArgs& fa, cudaStream_t st) {
+  if constexpr (NT > 16) {
+    return cudaErrorInvalidValue;
+  } else {
+    if (nt == NT) return run_fused<NT>(X, B, S, R, Fp, K, counter, fa, st);
+    return dispatch_fused<NT + 1>(nt, X, B, S, R, Fp, K, counter, fa, st);
+  }
+}
+
+__global__ void sum_parts_kernel(const double* __restrict__ part, int np, int64_t n, double* __restrict__ out) {
+  pdl_wait();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = __ldcs(part + e);
+    for (int q = 1; q < np; ++q) s += __ldcs(part + q * n + e);
+    out[e] = s;
+  }
+}
+
 }  // namespace
+
+bool ttm_fused_ok(int64_t B, int64_t S, int64_t R, int K, int64_t sf) {
+  return ttm_dmma_supported(B, S, R, K) && sf % BM == 0 && R % BM == 0;
+}
+
+cudaError_t launch_ttm_fused(const double* X, int64_t B, int64_t S, int64_t R, int K, const double* Fpad,
+                             const TtmFused& f, cudaStream_t st) {
+  double* ctl = const_cast<double*>(Fpad);
+  unsigned long long* counter = reinterpret_cast<unsigned long long*>(ctl);
+  FusedArgs fa;
+  fa.o_str = f.o_str;
+  fa.l_str = f.l_str;
+  fa.n_o = f.n_o;
+  fa.n_l = f.n_l;
+  fa.sf = f.sf;
+  fa.nh = f.sf / BM;
+  fa.nP = f.nP;
+  fa.run = (f.n_l + f.nP - 1) / f.nP;
+  fa.Af = f.Af;
+  fa.Al = f.Al;
+  fa.fast = f.fast;
+  fa.fl_o = f.fl_o;
+  fa.fl_l = f.fl_l;
+  fa.loop = f.loop;
+  if (fa.run >= 65536) return cudaErrorInvalidValue;
+  return dispatch_fused(static_cast<int>((K + 7) / 8), X, B, S, R, ctl + TTM_CTL + TTM_PART, K, counter, fa, st);
+}
+
+cudaError_t launch_sum_parts(const double* part, int np, int64_t n, double* out, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  cudaError_t e = launch_pdl(sum_parts_kernel, dim3((unsigned)blocks), dim3(256), 0, st, part, np, n, out);
+  note_launch();
+  return e;
+}
 
 bool ttm_dmma_supported(int64_t B, int64_t S, int64_t R, int K) {
   if (K < 1 || K > 128) return false;
   if (S % 2 != 0) return false;                 // TMA: row strides multiple of 16 bytes
   if (R > 1 && R % 2 != 0) return false;
   if (S >= (1ll << 31) || B >= (1ll << 31) || R >= (1ll << 31)) return false;
-  if (get_encode() == nullptr) return false;
+  // (shape only: the workspace plan must not depend on the machine; a missing tensor-map encoder
+  // makes the launch fail -- make_map -- rather than silently change the plan)
   return true;
+}
+
+bool ttm_skinny_ok(int64_t S, int64_t R, int K) {
+  (void)S;
+  (void)R;
+  return K <= 16;
 }
 
 cudaError_t launch_ttm_simt(const double* X, int64_t B, int64_t S, int64_t R, const double* F,
                             int K, double* out, cudaStream_t st) {
   const int64_t total = B * R * K;
   if (total == 0) return cudaSuccess;
+  static const bool no_skinny = getenv("CPPP_NO_SKINNY") != nullptr;   // A/B: the generic kernel
+  if (!no_skinny && ttm_skinny_ok(S, R, K)) {
+    if (K <= 2) return run_skinny<2>(X, B, S, R, F, K, out, st);
+    if (K <= 4) return run_skinny<4>(X, B, S, R, F, K, out, st);
+    if (K <= 8) return run_skinny<8>(X, B, S, R, F, K, out, st);
+    return run_skinny<16>(X, B, S, R, F, K, out, st);
+  }
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 64) blocks = 148 * 64;
   ttm_simt_kernel<<<(unsigned)blocks, 256, 0, st>>>(X, B, S, R, F, K, out);

@@ -627,3 +627,51 @@ def test_pp_policy_bound_monitor_and_switch(name):
     assert not any(d["phase"] == "pp-approx" for d in tight)
     assert any(d["phase"] == "pp-build" for d in tight)
     assert all(np.isnan(d["pp_bound"]) for d in dflt)
+
+
+@pytest.mark.parametrize("dims,K", [((6, 4, 10, 128), 16), ((4, 6, 8, 256), 40), ((2, 130, 4, 128), 8),
+                                    ((8, 8, 6, 384), 100), ((4, 4, 4, 128), 1)])
+def test_fused_level1_build_matches_oracle(dims, K):
+    """Order 4 with s_4 % 128 == 0: the operators come from three GEMMs whose
+    epilogues contract each level-1 tile into two leaves (no level-1 node in memory).  Every
+    operator and M_p^(n) against the oracle, and the plain Def. pptree build (NO_FUSED_TTV)."""
+    X, A = random_problem(dims, K, 14)
+    ops = O.pp_operators(X, A)
+    res = []
+    for flags in (0, cp.FLAG_NO_FUSED_TTV):
+        ctx = cp.cp_init(X, 4, dims, K, flags=flags)
+        cp.cp_set_factors(ctx, A)
+        cp.pp_build_operators(ctx)
+        got = {(i, j): cp.pp_get_operator(ctx, i, j) for (i, j) in ops}
+        for (i, j), ref in ops.items():
+            assert rel(got[(i, j)], ref) < TOL, (dims, K, flags, i, j)
+        for n in range(4):
+            assert rel(cp.pp_get_single(ctx, n), O.mttkrp(X, A, n)) < TOL, (dims, K, flags, n)
+        res.append(got)
+        cp.cp_destroy(ctx)
+
+
+@pytest.mark.parametrize("dims,K", [((25, 25, 25, 25), 2), ((31, 17, 9), 5), ((5, 3, 7, 9, 11, 3), 16),
+                                    ((9, 9, 9, 9, 9, 9), 1), ((3, 101, 7), 8)])
+def test_skinny_odd_extent_contractions(dims, K):
+    """Odd extents (no 16-byte TMA strides: the compact Laplacian's s = 25) with K <= 16:
+    the bandwidth-shaped kernels (thread per (b, r) for m-contiguous contractions, shared-memory
+    rows or warp per row for the natural unfolding) -- MTTKRP, every operator and a PP update."""
+    X, A = random_problem(dims, K, 15)
+    N = len(dims)
+    ctx = cp.cp_init(X, N, dims, K)
+    cp.cp_set_factors(ctx, A)
+    M = cp.mttkrp_dt(ctx)
+    for n in range(N):
+        assert rel(M[n], O.mttkrp(X, A, n)) < TOL, (dims, K, n)
+    cp.pp_build_operators(ctx)
+    ops = O.pp_operators(X, A)
+    for (i, j), ref in ops.items():
+        assert rel(cp.pp_get_operator(ctx, i, j), ref) < TOL, (dims, K, i, j)
+    r = np.random.default_rng(16)
+    dA = [0.01 * r.standard_normal(a.shape) for a in A]
+    cp.cp_update_factors(ctx, [a + d for a, d in zip(A, dA)])
+    Mp = [O.pp_single(ops, A, n, N) for n in range(N)]
+    for n in range(N):
+        assert rel(cp.pp_update(ctx, n), O.pp_update(Mp[n], ops, dA, n)) < TOL, (dims, K, n)
+    cp.cp_destroy(ctx)
