@@ -91,6 +91,10 @@ typedef struct {
    * several contexts on ONE device (one host thread each) run the sharded algebra in tests. */
   int (*host_allreduce)(double *buf, size_t count, void *user);
   void *host_allreduce_user;
+  /* τ of the normal-equation solve (L13): Cholesky of Γ^(n) is accepted iff every
+   * pivot > τ·max diag Γ; otherwise the eigen pseudo-inverse drops eigenvalues <= τ·λ_max.
+   * 0 = the default 1e-12; must lie in [0, 1). */
+  double pinv_rel_tol;
 } cppp_opts;
 
 /* Per-sweep record (S:505 trace schema). */
@@ -135,10 +139,13 @@ typedef struct {
 void cppp_default_opts(cppp_opts *o);
 
 /* Bytes of device workspace cp_init needs for this problem (includes a copy of X unless
- * CPPP_FLAG_BORROW_TENSOR).  Returns 0 on invalid arguments. */
+ * CPPP_FLAG_BORROW_TENSOR): the problem of P:7 / P:572-573 (X, N, s, R) sizes everything -- the
+ * factors, the N(N-1)/2 operators of Def. pptree and the tree intermediates, planned by
+ * a dry run of one regular sweep and one PP build.  Returns 0 on invalid arguments. */
 size_t cppp_workspace_bytes(int N, const int64_t *s, int K, const cppp_opts *o);
 
-/* Create a context for tensor X (order N, GLOBAL sizes s[0..N-1], rank K).
+/* Create a context for tensor X (order N, GLOBAL sizes s[0..N-1], rank K): the input of CP-ALS
+ * with pairwise perturbation, "Input: tensor X, rank R, tolerance" (P:7, Alg. 3).
  *   X: host or device pointer to this rank's slab (whole tensor when unsharded), row-major.
  *   Computes ||X||_F^2 (all-reduced when sharded).  Factors start at zero: call
  *   cp_set_factors before any sweep.  3 <= N <= CPPP_MAX_ORDER, 1 <= K <= CPPP_MAX_RANK. */
@@ -153,7 +160,8 @@ cppp_status cp_init(cppp_ctx **ctx, const double *X, int N, const int64_t *s, in
  * borrowed pointer (after the caller rewrote that buffer); any other pointer -> CPPP_ESTATE. */
 cppp_status cp_load_tensor(cppp_ctx *ctx, const double *X);
 
-/* Set A^(n) for n = 0..N-1 (A[n] is s_n x K, GLOBAL rows even when sharded), reset the PP
+/* Set A^(n) for n = 0..N-1 (A[n] is s_n x K, GLOBAL rows even when sharded): the initial
+ * factors of Alg. 3 ("initialize A^(1..N)"; L15 for the seeded recipe), and reset the PP
  * state (no operators), the sweep counter and the phase machine (next sweep is DT, L9). */
 cppp_status cp_set_factors(cppp_ctx *ctx, const double *const *A);
 /* Overwrite the current factors A (and their Grams) WITHOUT resetting the PP snapshot, the

@@ -214,12 +214,12 @@ def gamma(S: Sequence[np.ndarray], n: int) -> np.ndarray:
     return out
 
 
-def cholesky_pivots(G: np.ndarray):
+def cholesky_pivots(G: np.ndarray, tau: float = PIVOT_TAU):
     """Textbook column Cholesky Γ = L L^T.  Returns (L, ok) where ok is False as soon as a
-    pivot d_j = Γ_jj - Σ_{p<j} L_jp^2 is <= PIVOT_TAU * max diag(Γ) (L13)."""
+    pivot d_j = Γ_jj - Σ_{p<j} L_jp^2 is <= tau * max diag(Γ) (L13, default τ = PIVOT_TAU)."""
     K = G.shape[0]
     L = np.zeros_like(G)
-    thresh = PIVOT_TAU * max(float(np.max(np.diag(G))), 0.0)
+    thresh = tau * max(float(np.max(np.diag(G))), 0.0)
     for j in range(K):
         d = G[j, j] - float(np.dot(L[j, :j], L[j, :j]))
         if not d > thresh:
@@ -229,10 +229,12 @@ def cholesky_pivots(G: np.ndarray):
     return L, True
 
 
-def solve_normal(M: np.ndarray, G: np.ndarray) -> np.ndarray:
+def solve_normal(M: np.ndarray, G: np.ndarray, tau: Optional[float] = None) -> np.ndarray:
     """A_new = M Γ^†.  Cholesky path when Γ is numerically PD (L13); otherwise the
-    eigen pseudo-inverse with cutoff PINV_TAU * λ_max.  Γ = 0 gives 0."""
-    L, ok = cholesky_pivots(G)
+    eigen pseudo-inverse with cutoff τ * λ_max.  Γ = 0 gives 0.
+    τ defaults to PIVOT_TAU for the pivot rule and PINV_TAU for the cutoff (both 1e-12); a given
+    τ is used for both (the library's cppp_opts.pinv_rel_tol)."""
+    L, ok = cholesky_pivots(G, PIVOT_TAU if tau is None else tau)
     if ok:
         # Γ a^T = m^T per row:  L z = m^T (forward), L^T a^T = z (back)
         Z = np.zeros_like(M.T)
@@ -246,7 +248,8 @@ def solve_normal(M: np.ndarray, G: np.ndarray) -> np.ndarray:
         return At.T.copy()
     lam, V = np.linalg.eigh(G)
     lmax = float(np.max(lam)) if lam.size else 0.0
-    inv = np.where(lam > PINV_TAU * lmax, 1.0 / np.where(lam > 0, lam, 1.0), 0.0) if lmax > 0 else np.zeros_like(lam)
+    cut = PINV_TAU if tau is None else tau
+    inv = np.where(lam > cut * lmax, 1.0 / np.where(lam > 0, lam, 1.0), 0.0) if lmax > 0 else np.zeros_like(lam)
     Gp = (V * inv) @ V.T
     return M @ Gp
 
@@ -286,7 +289,8 @@ def kruskal_full(A: Sequence[np.ndarray]) -> np.ndarray:
 class State:
     """CP-ALS(-PP) state: factors, Grams, perturbations, PP snapshot and operators."""
 
-    def __init__(self, X: np.ndarray, A0: Sequence[np.ndarray]):
+    def __init__(self, X: np.ndarray, A0: Sequence[np.ndarray], tau: Optional[float] = None):
+        self.tau = tau   # L13's τ (None: the defaults)
         self.X = np.asarray(X, dtype=np.float64)
         self.N = self.X.ndim
         self.A = [np.array(a, dtype=np.float64, copy=True) for a in A0]
@@ -302,7 +306,7 @@ class State:
 
     def _update_mode(self, n: int, M: np.ndarray, dA_ref: np.ndarray):
         Gm = gamma(self.S, n)
-        A_new = solve_normal(M, Gm)
+        A_new = solve_normal(M, Gm, self.tau)
         Gr = gradient(self.A[n], A_new, Gm)
         self.G_norms[n] = float(np.linalg.norm(Gr))
         self.A[n] = A_new
@@ -354,7 +358,8 @@ def cp_als(X, A0, sweeps: int):
 
 
 def pp_cp_als(X, A0, eps: float, eps_pp: float, max_sweeps: int,
-              phase_override: Optional[Sequence[str]] = None, deadline: Optional[float] = None):
+              phase_override: Optional[Sequence[str]] = None, deadline: Optional[float] = None,
+              tau: Optional[float] = None):
     """PP-CP-ALS, Alg. 3 with readings L7-L12:
       * the first sweep is regular (L9);
       * after each complete regular sweep, if max_i ‖dA^(i)‖/‖A^(i)‖ < ε_pp the next sweep
@@ -365,8 +370,9 @@ def pp_cp_als(X, A0, eps: float, eps_pp: float, max_sweeps: int,
     ``phase_override`` (L12) forces the phase of each sweep (used to replay a schedule).
     ``deadline`` (a time.perf_counter() value; bench.py's bounded CPU sample only) stops after
     the sweep during which it passed — control flow only, the arithmetic is unchanged.
+    ``tau`` is L13's τ (None: the defaults).
     Returns (factors, trace) with one dict per sweep."""
-    st = State(X, A0)
+    st = State(X, A0, tau)
     trace = []
     next_phase = "dt"
     for sw in range(max_sweeps):

@@ -47,7 +47,8 @@ class Opts(C.Structure):
                 ("workspace_bytes", C.c_size_t), ("flags", C.c_uint), ("shard_mode", C.c_int),
                 ("shard_offset", C.c_int64), ("shard_extent", C.c_int64),
                 ("nccl_unique_id", C.c_void_p), ("rank", C.c_int), ("world", C.c_int),
-                ("host_allreduce", HOST_ALLREDUCE), ("host_allreduce_user", C.c_void_p)]
+                ("host_allreduce", HOST_ALLREDUCE), ("host_allreduce_user", C.c_void_p),
+                ("pinv_rel_tol", C.c_double)]
 
 
 class TkSweepInfo(C.Structure):
@@ -209,7 +210,7 @@ def _torch_workspace(nbytes: int, device: int):
 def cp_init(X, N: int, s: Sequence[int], K: int, *, device: int = 0, stream=None,
             flags: int = 0, shard_offset: Optional[int] = None, shard_extent: Optional[int] = None,
             nccl_unique_id: Optional[bytes] = None, rank: int = 0, world: int = 1,
-            torch_workspace: bool = True, host_allreduce=None) -> Ctx:
+            torch_workspace: bool = True, host_allreduce=None, pinv_rel_tol: float = 0.0) -> Ctx:
     """cp_init (include/cppp.h).  X: numpy array (host) or torch CUDA tensor (device; borrowed
     with FLAG_BORROW_TENSOR).  The device workspace is a torch uint8 tensor unless
     torch_workspace=False (then the library cudaMallocs it).  stream: a torch.cuda.Stream or
@@ -228,6 +229,7 @@ def cp_init(X, N: int, s: Sequence[int], K: int, *, device: int = 0, stream=None
         o.shard_offset = int(shard_offset)
         o.shard_extent = int(shard_extent)
     o.rank, o.world = rank, world
+    o.pinv_rel_tol = pinv_rel_tol
     if host_allreduce is not None:
         # host_allreduce(np.ndarray view of the staged buffer) -> None, sums in place
         def _cb(buf, count, _user, _fn=host_allreduce):

@@ -145,6 +145,7 @@ struct cppp_ctx {
   int next_phase = CPPP_PHASE_DT;
   int override_phase = CPPP_PHASE_AUTO;
   int policy = CPPP_POLICY_EPS_PP;   // PP switching policy (cp_set_pp_policy)
+  double pinv_tol = 1e-12;           // τ of L13 (cppp_opts.pinv_rel_tol)
   double policy_tol = 0.0;
   int sweep = 0, restarts = 0;
   double last_fitness = NAN;
@@ -460,7 +461,7 @@ cppp_status prefetch_inverse(cppp_ctx* c, int n) {
     Prof p(c, CPPP_K_FACTOR, (double)c->K * c->K * c->K / 3.0, 8.0 * c->K * c->K * c->N, c->st2);
     CUCHK(c, launch_gamma_factor(c->S_all, c->N, n, c->K, c->Gamma, c->L, c->lmode,
                                  c->L + (int64_t)solve_ld(c->K) * solve_ld(c->K) + 4 * 32 * 33,
-                                 c->st2));
+                                 c->st2, c->pinv_tol));
   }
   CUCHK(c, cudaEventRecord(c->ev_P, c->st2));
   c->prefetched = n;
@@ -1537,6 +1538,9 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
   c->device = o.device;
   CUCHK(c, cudaSetDevice(c->device));
   c->flags = o.flags;
+  if (o.pinv_rel_tol < 0.0 || !(o.pinv_rel_tol < 1.0))
+    return fail(c, CPPP_EINVAL, "pinv_rel_tol %g outside [0, 1)", o.pinv_rel_tol);
+  c->pinv_tol = o.pinv_rel_tol > 0.0 ? o.pinv_rel_tol : 1e-12;
   setup_dims(c, N, s, K, &o);
   if (o.stream) c->st = static_cast<cudaStream_t>(o.stream);
   else {

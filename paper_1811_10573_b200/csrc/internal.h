@@ -162,7 +162,7 @@ size_t pp_update_scratch_doubles(int64_t ny, int K, int64_t max_nx);
 int solve_ld(int K);
 cudaError_t launch_gamma_factor(const double* S_all /* N x K x K */, int N, int n, int K,
                                 double* Gamma, double* Tp, int* mode, double* Vscratch,
-                                cudaStream_t st);
+                                cudaStream_t st, double tau = 1e-12);
 // Row solves: A_new = M Γ^† (substitution with the packed factor, or M P) ; G = (A_old - A_new) Γ ;
 // dA = A_new - ref ; per-row statistics -> rowstat (rows x 4: ‖a_new‖², ‖dA‖², ‖g‖², Σ m∘a_new).
 // A is updated in place; ref may alias A.

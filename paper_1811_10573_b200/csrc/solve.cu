@@ -77,7 +77,8 @@ __device__ void block_sum_n(double (&v)[NV], double* sh /* 32 NV */) {
   for (int c = 0; c < NV; ++c) v[c] = sh[32 * c];
 }
 
-constexpr double PIVOT_TAU = 1e-12;  // L13 / S:201
+// L13 / S:201: the pivot rule and the pseudo-inverse cutoff take τ (cppp_opts.pinv_rel_tol,
+// default 1e-12) as a kernel argument
 
 // 1/d for the factorization's pivots: the hardware approximation (MUFU.RCP64H) refined by two
 // Newton steps -- within an ulp of the correctly rounded value, and off the slow path that
@@ -90,7 +91,6 @@ __device__ __forceinline__ double pivot_rcp(double d) {
   e = fma(-d, y, 1.0);
   return fma(y, e, y);
 }
-constexpr double PINV_TAU = 1e-12;
 constexpr int GF_THREADS = 640;      // factorization: 20 warps = the lower-triangle 16x32 blocks
 constexpr int GP_THREADS = 512;      // Jacobi fallback
 
@@ -125,7 +125,7 @@ __constant__ unsigned char kCholBlock[20] = {
 template <bool transpose>
 __global__ void __launch_bounds__(GF_THREADS, 1)
     gamma_chol_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
-                      double* Tp, int ldt, int* mode) {
+                      double* Tp, int ldt, int* mode, double tau) {
   PROBE_T0();
   pdl_wait();
   __shared__ __align__(16) double colb[2][128];
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
     sh[0] = mx;
   }
   __syncthreads();
-  const double thresh = PIVOT_TAU * sh[0];
+  const double thresh = tau * sh[0];
   if (tid < ldt - K) Tp[(K + tid) * ldt + K + tid] = 1.0;   // unit diagonal of the padding
   if (l == 0) {   // publish column 0 and its pivot
 #pragma unroll
@@ -322,7 +322,7 @@ __device__ __forceinline__ void block_inverse_dev(double* Tp, int ldt) {
 // the pivot test failed.  Two-sided cyclic Jacobi, Brent-Luk parallel ordering; the
 // pseudo-inverse P goes to Tp (pitch ldt).
 __device__ __forceinline__ void gamma_pinv_dev(int K, const double* __restrict__ Gamma,
-                                               double* Pout, int ldt, double* Vscratch) {
+                                               double* Pout, int ldt, double* Vscratch, double tau) {
   extern __shared__ double W[];  // K x (K+1)
   __shared__ double sh[32];
   const int tid = threadIdx.x, KK = K * K;
@@ -416,7 +416,7 @@ __device__ __forceinline__ void gamma_pinv_dev(int K, const double* __restrict__
   const double lmax = sh[0];
   for (int i = tid; i < K; i += nt) {
     const double l = lam[i];
-    lam[i] = (lmax > 0.0 && l > PINV_TAU * lmax) ? 1.0 / l : 0.0;
+    lam[i] = (lmax > 0.0 && l > tau * lmax) ? 1.0 / l : 0.0;
   }
   __syncthreads();
   for (int e = tid; e < KK; e += nt) {
@@ -432,12 +432,12 @@ __device__ __forceinline__ void gamma_pinv_dev(int K, const double* __restrict__
 // either way (the two separate kernels cost a launch on the factorization chain per mode).
 __global__ void __launch_bounds__(GP_THREADS, 1)
     gamma_post_kernel(int K, const double* __restrict__ Gamma, double* Tp, int ldt,
-                      const int* mode, double* Vscratch) {
+                      const int* mode, double* Vscratch, double tau) {
   pdl_wait();
   if (*mode == 0) {
     if (threadIdx.x < 128) block_inverse_dev(Tp, ldt);
   } else {
-    gamma_pinv_dev(K, Gamma, Tp, ldt, Vscratch);
+    gamma_pinv_dev(K, Gamma, Tp, ldt, Vscratch, tau);
   }
 }
 
@@ -455,7 +455,7 @@ constexpr int GS_THREADS = 32;
 template <int KP>   // K <= KP (8, 16 or 32): every loop is unrolled to KP
 __global__ void __launch_bounds__(GS_THREADS, 1)
     gamma_small_kernel(const double* __restrict__ S_all, int N, int n, int K, double* Gamma,
-                       double* Tp, int ldt, int* mode, double* Vscratch) {
+                       double* Tp, int ldt, int* mode, double* Vscratch, double tau) {
   PROBE_T0();
   pdl_wait();
   __shared__ int bad_s;
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1)
       if (k == i && row_ok) dmax = w[k];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-    const double thresh = PIVOT_TAU * dmax;
+    const double thresh = tau * dmax;
     PROBE_T(6);
     // every shuffle unconditional (a shuffle under a runtime condition compiles to the
     // divergent-collective path); steps j >= K only touch padding lanes and columns (their
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(GS_THREADS, 1)
     }
   }
   __syncthreads();
-  if (bad_s) gamma_pinv_dev(K, Gamma, Tp, ldt, Vscratch);
+  if (bad_s) gamma_pinv_dev(K, Gamma, Tp, ldt, Vscratch, tau);
 }
 
 // ---------------------------------------------------------------- row solves
@@ -998,7 +998,7 @@ uint64_t launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED);
 int solve_ld(int K) { return (K + 7) & ~7; }
 
 cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double* Gamma, double* Tp,
-                                int* mode, double* Vscratch, cudaStream_t st) {
+                                int* mode, double* Vscratch, cudaStream_t st, double tau) {
   const int ldt = solve_ld(K);
   const size_t smem = static_cast<size_t>(K) * (K + 1) * sizeof(double);
   static bool attr = false;
@@ -1020,7 +1020,7 @@ cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double
     }
     auto f = K <= 8 ? gamma_small_kernel<8> : K <= 16 ? gamma_small_kernel<16> : gamma_small_kernel<32>;
     cudaError_t e = launch_pdl(f, dim3(1), dim3(GS_THREADS), smem, st, S_all, N, n, K, Gamma, Tp, ldt,
-                               mode, Vscratch);
+                               mode, Vscratch, tau);
     note_launch();
     return e;
   }
@@ -1038,13 +1038,13 @@ cudaError_t launch_gamma_factor(const double* S_all, int N, int n, int K, double
   }
   cudaError_t e = transpose
                       ? launch_pdl(gamma_chol_kernel<true>, dim3(1), dim3(GF_THREADS), chol_smem, st,
-                                   S_all, N, n, K, Gamma, Tp, ldt, mode)
+                                   S_all, N, n, K, Gamma, Tp, ldt, mode, tau)
                       : launch_pdl(gamma_chol_kernel<false>, dim3(1), dim3(GF_THREADS), 0, st, S_all,
-                                   N, n, K, Gamma, Tp, ldt, mode);
+                                   N, n, K, Gamma, Tp, ldt, mode, tau);
   note_launch();
   if (e != cudaSuccess) return e;
   e = launch_pdl(gamma_post_kernel, dim3(1), dim3(GP_THREADS), smem, st, K,
-                 static_cast<const double*>(Gamma), Tp, ldt, static_cast<const int*>(mode), Vscratch);
+                 static_cast<const double*>(Gamma), Tp, ldt, static_cast<const int*>(mode), Vscratch, tau);
   note_launch();
   return e;
 }

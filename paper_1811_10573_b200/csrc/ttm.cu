@@ -546,6 +546,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   double* lacc = red + NWARP * C::BN;                           // [BM][BN + 1] loop-leaf slice
   constexpr int LP = C::BN + 1;
   __shared__ long long stage_tile[16];
+  __shared__ long long stage_meta[16][4];   // per unit's first stage of a tile: x_o, x_l, h, chunk
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int st = 0; st < stages; ++st) {
@@ -598,7 +599,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int st = static_cast<int>(it % stages);
             const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
             if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
-            if (kt == 0) stage_tile[st] = unit * 65536 + i;
+            if (kt == 0) {   // the consumers read the tile's coordinates (no 64-bit divisions)
+              stage_tile[st] = i + (i + 1 == L ? 65536 : 0);
+              stage_meta[st][0] = xo;
+              stage_meta[st][1] = xl;
+              stage_meta[st][2] = h;
+              stage_meta[st][3] = p;
+            }
             const uint32_t fb = smem_u32(&full[st]);
             mbar_expect_tx(fb, C::STAGE);
             const uint32_t sx = smem_u32(base + st * C::STAGE);
@@ -620,12 +627,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int st = static_cast<int>(it % stages);
       mbar_wait(smem_u32(&full[st]), static_cast<uint32_t>((it / stages) & 1));
     }
-    const long long code = stage_tile[static_cast<int>(it % stages)];
+    const int st0 = static_cast<int>(it % stages);
+    const long long code = stage_tile[st0];
     if (code < 0) break;
-    const long long unit = code / 65536;
-    const int64_t i = code - unit * 65536;
-    int64_t xl, xo, h, p;
-    tile_of(unit, i, &xl, &xo, &h, &p);
+    const int64_t i = code & 65535;
+    const bool last = code >= 65536;   // the run's last tile: its loop-leaf slice goes out
+    const int64_t xo = stage_meta[st0][0], xl = stage_meta[st0][1], h = stage_meta[st0][2],
+                  p = stage_meta[st0][3];
     double acc[NT][2];
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
@@ -678,7 +686,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const double* al = fa.Al + xl * K;
     double* lrow = fa.loop + (p * fa.n_o * fa.sf + xo * fa.sf + xf) * static_cast<int64_t>(K);
     double* lsm = lacc + mloc * LP;   // this thread's row of the run's loop-leaf slice (smem)
-    const bool last = (i + 1 == run_len(p));
     // value of (tile pair c, element e) -> column and accumulator
 #pragma unroll
     for (int c = 0; c < (NT + 1) / 2; ++c) {

@@ -675,3 +675,29 @@ def test_skinny_odd_extent_contractions(dims, K):
     for n in range(N):
         assert rel(cp.pp_update(ctx, n), O.pp_update(Mp[n], ops, dA, n)) < TOL, (dims, K, n)
     cp.cp_destroy(ctx)
+
+
+@pytest.mark.parametrize("K", [10, 40])
+def test_pinv_rel_tol_option(K):
+    """cppp_opts.pinv_rel_tol (L13's τ): τ = 0.05 sends ill-conditioned Γ down the
+    eigen pseudo-inverse branch on both sides (one-warp kernel at K = 10, the CTA kernel at 40);
+    three replayed sweeps against the oracle run with the same τ."""
+    dims = (30, 28, 26)
+    X, _ = random_problem(dims, K, 31)
+    r = np.random.default_rng(32)
+    A0 = [r.random((d, K)) for d in dims]
+    tau = 0.05
+    A_or, tr = O.pp_cp_als(X, A0, 0.0, 0.1, 3, phase_override=["dt"] * 3, tau=tau)
+    st = O.State(X, A0, tau)
+    assert not all(O.cholesky_pivots(O.gamma(st.S, n), tau)[1] for n in range(3))
+    ctx = cp.cp_init(X, 3, dims, K, pinv_rel_tol=tau)
+    cp.cp_set_factors(ctx, A0)
+    for t in tr:
+        cp.cp_set_phase_override(ctx, "dt")
+        info = cp.als_sweep(ctx, 0.0, 0.1)
+        assert abs(info["residual_sq"] - t["residual_sq"]) <= 1e-9 * t["normX_sq"], (t, info)
+    for a, b in zip(cp.cp_get_factors(ctx), A_or):
+        assert rel(a, b) < 1e-8
+    with pytest.raises(cp.CpppError):
+        cp.cp_init(X, 3, dims, K, pinv_rel_tol=1.5)
+    cp.cp_destroy(ctx)

@@ -122,7 +122,7 @@ def test_sharded_kernels_match_oracle(P, name):
             assert rel(ops[(i, j)], ref) < 1e-11, (rank, i, j)
 
 
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [2, 4, 8])
 @pytest.mark.parametrize("name", ["C1", "C3mini", "C5mini", "C4mini"])
 def test_sharded_trace_matches_oracle(P, name):
     cfg = G.CONFIGS[name]
@@ -216,3 +216,31 @@ def test_pp_error_sharded_single_rank():
     assert np.allclose(bound, b_ref, rtol=1e-12, atol=0)
     assert np.all(np.abs(err - e_ref) <= 1e-8 * e_ref + 1e-13)
     cp.cp_destroy(nc)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_sharded_als_run_free_running(P):
+    """A whole free-running run through als_run on P slab contexts (C5mini): the phase decisions
+    are taken from the all-reduced statistics, so every replica follows the oracle's schedule
+    (where its ε_pp margins are clear) and ends with bit-identical replicated factors."""
+    cfg = G.CONFIGS["C5mini"]
+    X = G.make_tensor(cfg)
+    A0 = G.initial_factors(cfg)
+    A_fin, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, 20)
+
+    def body(rank, ctx, lo, hi):
+        cp.cp_set_factors(ctx, A0)
+        return cp.als_run(ctx, 0.0, cfg.eps_pp, 20), cp.cp_get_factors(ctx)
+
+    res = run_sharded(P, X, cfg.dims, cfg.K, body)
+    if all(t["margin"] > 1e-6 for t in tr):
+        for infos, _ in res:
+            assert [i["phase"] for i in infos] == [t["phase"] for t in tr]
+    for infos, _ in res[1:]:
+        assert [i["residual_sq"] for i in infos] == [i["residual_sq"] for i in res[0][0]]
+    for n in range(cfg.N):
+        for rank in range(1, P):
+            assert np.array_equal(res[rank][1][n], res[0][1][n])
+    cond = golden("C5mini", X, A0, cfg.eps_pp, tr, A_fin)
+    if [i["phase"] for i in res[0][0]] == [t["phase"] for t in tr]:
+        check(tr, res[0][0], cond, A_fin, res[0][1], tag=("als_run", P))

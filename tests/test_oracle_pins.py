@@ -529,3 +529,19 @@ def test_second_order_term_multilinear_remainder(dims):
                 rem = rem + O.mttkrp(X, F, n)
         got = O.mttkrp(X, A, n) - O.pp_update(Mp[n], ops, dA, n) - O.second_order_term(X, Ap, dA, n)
         assert rel(got, rem) < 1e-10, n
+
+
+def test_solve_tau_selects_the_branch():
+    """L13's τ: a Γ with a pivot ratio of ~1e-3 is solved by Cholesky at τ = 1e-12 and by the
+    eigen pseudo-inverse at τ = 1e-2, which then drops the eigenvalues below τ λ_max -- the
+    minimum-norm solution on the remaining eigenspace, built here from numpy's eigh."""
+    r = rng(41)
+    Q = np.linalg.qr(r.standard_normal((5, 5)))[0]
+    lam = np.array([1.0, 0.5, 0.2, 4e-3, 1e-3])
+    G = (Q * lam) @ Q.T
+    M = r.standard_normal((7, 5))
+    assert O.cholesky_pivots(G)[1] and not O.cholesky_pivots(G, 1e-2)[1]
+    assert rel(O.solve_normal(M, G), M @ np.linalg.inv(G)) < 1e-10
+    keep = lam > 1e-2 * lam.max()
+    want = M @ ((Q[:, keep] / lam[keep]) @ Q[:, keep].T)
+    assert rel(O.solve_normal(M, G, 1e-2), want) < 1e-10

@@ -51,10 +51,10 @@ int main(int argc, char** argv) {
     cudaMemcpy(dA, A.data(), 8 * s * K, cudaMemcpyHostToDevice);
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
-    launch_gamma_factor(dS, N, 0, K, dG, dP, dmode, dV, 0);
+    launch_gamma_factor(dS, N, 0, K, dG, dP, dmode, dV, 0, 1e-12);
     cudaDeviceSynchronize();
     cudaEventRecord(a);
-    for (int r = 0; r < 20; ++r) launch_gamma_factor(dS, N, 0, K, dG, dP, dmode, dV, 0);
+    for (int r = 0; r < 20; ++r) launch_gamma_factor(dS, N, 0, K, dG, dP, dmode, dV, 0, 1e-12);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms_inv; cudaEventElapsedTime(&ms_inv, a, b);
     cudaEventRecord(a);
@@ -70,7 +70,7 @@ int main(int argc, char** argv) {
     launch_solve_rows(dM, dA, dA, dD, s, K, dG, dP, dmode, drs, 0);
     std::vector<double> An(s * K);
     cudaMemcpy(An.data(), dA, 8 * s * K, cudaMemcpyDeviceToHost);
-    launch_gamma_factor(dS, N, 0, K, dG, dP, dmode, dV, 0);
+    launch_gamma_factor(dS, N, 0, K, dG, dP, dmode, dV, 0, 1e-12);
     cudaDeviceSynchronize();
     long long cyc[16];
     cudaMemcpyFromSymbol(cyc, g_probe_cycles, sizeof(cyc));
