@@ -229,9 +229,9 @@ cppp_status als_run(cppp_ctx *ctx, double eps, double eps_pp, int max_sweeps,
  *   CPPP_POLICY_BOUND: the same transitions, and after every PP sweep a monitor evaluates, per mode
  *     n and column k, the certificate of pp_error (||X||_F Σ_{|S|>=2} Π_{i∈S}||da_k^(i)||
  *     Π_{j∉S}||a_p,k^(j)|| / ||m~_k^(n)||, from column norms only: no tensor pass); when its maximum
- *     reaches tol, the phase does not continue with the stale operators -- the next sweep rebuilds
- *     them at the current factors (a pp-build) instead of a pp-approx sweep.  info.pp_bound
- *     reports the value.  tol > 0.
+ *     reaches tol, the PP phase ends as after a failed ε_pp test: the next sweep is a regular one
+ *     (exact MTTKRPs), and Alg. 3 decides from there whether to rebuild.  info.pp_bound reports
+ *     the value.  tol > 0.
  * Changing the policy drops the captured sweep graphs (recaptured on the next sweeps). */
 #define CPPP_POLICY_EPS_PP 0
 #define CPPP_POLICY_BOUND 1

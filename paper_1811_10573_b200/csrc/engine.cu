@@ -368,9 +368,7 @@ TtmOpts side_gemm_opts() {
 }
 
 bool reuse12(const cppp_ctx* c) {
-  // (CPPP_POLICY_BOUND can rebuild right after a PP sweep, where ops[1][2] is not at A_p: off)
-  return c->N == 3 && c->q < 0 && !(c->flags & CPPP_FLAG_NO_OP_REUSE) &&
-         c->policy == CPPP_POLICY_EPS_PP;
+  return c->N == 3 && c->q < 0 && !(c->flags & CPPP_FLAG_NO_OP_REUSE);
 }
 int64_t node_elems(cppp_ctx* c, uint32_t mask) {
   int64_t e = c->K;
@@ -488,16 +486,17 @@ cppp_status finish_mode(cppp_ctx* c, int n, const double* Mn, bool pp_phase) {
     Prof p(c, CPPP_K_SOLVE, 4.0 * rows * K * K, 8.0 * rows * K * 5);
     double* An = c->A[n] + off * K;
     const double* ref = pp_phase ? (c->Ap[n] + off * K) : An;
+    const bool last = (n == c->N - 1);
+    // the slab mode (q = 0) writes its norms into qhdr, right before S^(q) = S_all's first block
+    const bool packq = (n == c->q) && comm_on(c) && !c->dry;
+    double* nrm = packq ? c->qhdr : c->stats + 3 * n;
     CUCHK(c, launch_solve_rows(Mn, An, ref, c->dA[n] + off * K, rows, K, c->Gamma, c->L, c->lmode,
                                c->rowstat, c->st));
     // S^(n), the norms and (last mode) the fitness terms in one kernel; Γ^(n) is still in place
     // (the next factorization starts after ev_S below)
-    const bool last = (n == c->N - 1);
-    // the slab mode (q = 0) writes its norms into qhdr, right before S^(q) = S_all's first block
-    const bool packq = (n == c->q) && comm_on(c) && !c->dry;
-    CUCHK(c, launch_gram(An, rows, K, c->S_all + (int64_t)n * K * K, c->rowstat,
-                         packq ? c->qhdr : c->stats + 3 * n, last ? c->Gamma : nullptr,
-                         last ? c->stats + 3 * c->N : nullptr, c->gram_scratch, c->gram_counters, c->st));
+    CUCHK(c, launch_gram(An, rows, K, c->S_all + (int64_t)n * K * K, c->rowstat, nrm,
+                         last ? c->Gamma : nullptr, last ? c->stats + 3 * c->N : nullptr,
+                         c->gram_scratch, c->gram_counters, c->st));
   }
   if (n == c->q && comm_on(c)) {
     // S^(q) and the norms in ONE all-reduce (SURVEY C-d), then the norms into their stats slots
@@ -1147,7 +1146,7 @@ __global__ void run_decide_kernel(RunState* rs, const double* __restrict__ stats
   int next = phase == CPPP_PHASE_DT ? (small ? CPPP_PHASE_PP_BUILD : CPPP_PHASE_DT)
                                     : (small ? CPPP_PHASE_PP : CPPP_PHASE_DT);
   const double bound = (rs->policy == CPPP_POLICY_BOUND && phase != CPPP_PHASE_DT) ? stats[3 * N + 6] : NAN;
-  if (next == CPPP_PHASE_PP && bound >= rs->policy_tol) next = CPPP_PHASE_PP_BUILD;
+  if (next == CPPP_PHASE_PP && bound >= rs->policy_tol) next = CPPP_PHASE_DT;
   if (phase == CPPP_PHASE_PP_BUILD) rs->restarts++;
   const int d = rs->done;
   RunInfo& in = rs->info[d];
@@ -1870,7 +1869,6 @@ cppp_status cp_set_pp_policy(cppp_ctx* c, int policy, double tol) {
   }
   c->policy = policy;
   c->policy_tol = tol;
-  c->op12_fresh = false;   // (the order-3 operator reuse depends on the policy: reuse12)
   return CPPP_OK;
 }
 
@@ -1914,9 +1912,10 @@ cppp_status als_sweep(cppp_ctx* c, double eps, double eps_pp, cppp_sweep_info* i
   if (phase == CPPP_PHASE_DT) c->next_phase = small ? CPPP_PHASE_PP_BUILD : CPPP_PHASE_DT;
   else c->next_phase = small ? CPPP_PHASE_PP : CPPP_PHASE_DT;
   // CPPP_POLICY_BOUND: a PP phase continues only while the monitor's certificate stays below tol;
-  // otherwise the operators are rebuilt at the current factors (the next sweep is a pp-build)
+  // otherwise it ends like a failed ε_pp test: one regular sweep (exact MTTKRPs) follows, and
+  // Alg. 3 decides from there whether to rebuild
   const double bound = (c->policy == CPPP_POLICY_BOUND && phase != CPPP_PHASE_DT) ? hs[3 * N + 6] : NAN;
-  if (c->next_phase == CPPP_PHASE_PP && bound >= c->policy_tol) c->next_phase = CPPP_PHASE_PP_BUILD;
+  if (c->next_phase == CPPP_PHASE_PP && bound >= c->policy_tol) c->next_phase = CPPP_PHASE_DT;
   c->sweep++;
   c->last_fitness = fit;
   if (info) {

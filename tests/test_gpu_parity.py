@@ -583,7 +583,7 @@ def test_pp_policy_bound_monitor_and_switch(name):
     """CPPP_POLICY_BOUND (f3 switching policy): the monitor value after a PP sweep equals the
     certificate from the oracle's own sweep (||m~|| from its M~); with tol = 1e300 the run is
     bit-identical to the default policy; with a tol below every monitor value no pp-approx sweep
-    is left (each is replaced by a rebuild)."""
+    is left (every PP phase ends after its build sweep, a regular sweep follows)."""
     cfg, X, Ap = problem(name)
     A = moved_factors(Ap, 0.02, 10)
     st = O.State(X, Ap)
@@ -626,6 +626,8 @@ def test_pp_policy_bound_monitor_and_switch(name):
     assert any(d["phase"] == "pp-approx" for d in dflt)
     assert not any(d["phase"] == "pp-approx" for d in tight)
     assert any(d["phase"] == "pp-build" for d in tight)
+    ph = [d["phase"] for d in tight]
+    assert all(b == "dt" for a, b in zip(ph, ph[1:]) if a == "pp-build")
     assert all(np.isnan(d["pp_bound"]) for d in dflt)
 
 
@@ -686,6 +688,8 @@ def test_pinv_rel_tol_option(K):
     X, _ = random_problem(dims, K, 31)
     r = np.random.default_rng(32)
     A0 = [r.random((d, K)) for d in dims]
+    for a in A0:   # two nearly parallel columns: Γ's pivot ratio ~1e-4, well below τ
+        a[:, 1] = a[:, 0] + 1e-2 * r.standard_normal(a.shape[0])
     tau = 0.05
     A_or, tr = O.pp_cp_als(X, A0, 0.0, 0.1, 3, phase_override=["dt"] * 3, tau=tau)
     st = O.State(X, A0, tau)

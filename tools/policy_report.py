@@ -19,7 +19,7 @@ import paper_1811_10573_b200.cppp as cp  # noqa: E402
 
 def main():
     names = [a for a in sys.argv[1:] if not a.startswith("--") and not a[0].isdigit()] or ["C1", "C2", "C3", "C4"]
-    tols = [1.0, 0.3, 0.1]
+    tols = [1e3, 1e2, 10.0, 1.0]
     if "--tols" in sys.argv:
         tols = [float(x) for x in sys.argv[sys.argv.index("--tols") + 1].split(",")]
     st = torch.cuda.current_stream()
@@ -43,7 +43,9 @@ def main():
                          "dt": ph.count("dt"), "pp_build": ph.count("pp-build"),
                          "pp_approx": ph.count("pp-approx"), "run_ms": 1e3 * sum(i["seconds"] for i in infos),
                          "final_rel_residual": (max(r2, 0.0) / float((X * X).sum())) ** 0.5,
-                         "monitor_max": max(bounds) if bounds else None})
+                         "monitor_max": max(bounds) if bounds else None,
+                         "worst_max_rel_dA": max(i["max_rel_dA"] for i in infos),
+                         "last_phase": ph[-1]})
             cp.cp_destroy(ctx)
         print(json.dumps({"config": name, "runs": rows}), flush=True)
         del X
