@@ -74,3 +74,19 @@ def test_device_calls_fail_loudly_without_gpu():
     with pytest.raises(cp.CpppError) as e:
         cp.cp_init(X, 3, (4, 4, 4), 2, torch_workspace=False)
     assert e.value.status == -6   # CPPP_ENODEV
+
+
+def test_bench_arms_print_the_same_config():
+    """bench.py: the reference arm (the oracle) and ours describe the workload with the same dict
+    (the driver compares them), and the L2 note tells inputs larger than L2 from flushed ones."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    import synthgen as G
+    for name in ("C1", "C2", "C5"):
+        cfg = G.CONFIGS[name]
+        a, b = bench.config_dict(cfg, 20, 1), bench.config_dict(cfg, 20, 1)
+        assert a == b and a["workload"] == name and a["parallelism"] == "single GPU"
+    assert "larger than L2" in bench.l2_note(G.CONFIGS["C2"])
+    assert "flushed" in bench.l2_note(G.CONFIGS["C1"])
+    assert bench.host_cores() >= 1
