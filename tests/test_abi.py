@@ -83,10 +83,14 @@ def test_bench_arms_print_the_same_config():
     sys.path.insert(0, ROOT)
     import bench
     import synthgen as G
-    for name in ("C1", "C2", "C5"):
-        cfg = G.CONFIGS[name]
-        a, b = bench.config_dict(cfg, 20, 1), bench.config_dict(cfg, 20, 1)
-        assert a == b and a["workload"] == name and a["parallelism"] == "single GPU"
+    import json
+    import subprocess
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "C1",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300, check=True)
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    assert line["config"] == bench.config_dict(G.CONFIGS["C1"], 20, 1)
+    assert line["cpu_baseline"]["cores"] == bench.host_cores()
     assert "larger than L2" in bench.l2_note(G.CONFIGS["C2"])
     assert "flushed" in bench.l2_note(G.CONFIGS["C1"])
     assert bench.host_cores() >= 1
