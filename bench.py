@@ -294,6 +294,8 @@ def main():
         args.gpus = world if world > 1 else args.gpus
     torch.cuda.set_device(local)
     if world > 1:
+        # the library captures its collectives into CUDA graphs: connect everything at init
+        os.environ.setdefault("NCCL_RUNTIME_CONNECT", "0")
         dist.init_process_group("nccl", init_method="env://")
     cfg = G.CONFIGS[args.config]
     sweeps = args.sweeps or cfg.sweeps

@@ -1554,6 +1554,9 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
   if (comm_on(c) && !c->host_ar) {
     if (!o.nccl_unique_id)
       return fail(c, CPPP_EINVAL, "a communicating context needs nccl_unique_id or host_allreduce");
+    // the sweeps' collectives are captured into CUDA graphs: every connection is set up when the
+    // communicator is created, not lazily inside a capture (a caller's setting wins)
+    setenv("NCCL_RUNTIME_CONNECT", "0", 0);
     if (!g_nccl.load()) return fail(c, CPPP_ENCCL, "cannot dlopen libnccl.so.2");
     ncclUniqueId id;
     std::memcpy(&id, o.nccl_unique_id, sizeof(id));
