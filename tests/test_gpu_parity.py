@@ -705,3 +705,39 @@ def test_pinv_rel_tol_option(K):
     with pytest.raises(cp.CpppError):
         cp.cp_init(X, 3, dims, K, pinv_rel_tol=1.5)
     cp.cp_destroy(ctx)
+
+
+def test_fused_build_inside_sweeps_and_graphs():
+    """An order-4 problem whose PP builds take the fused level-1 GEMMs (s_4 = 128): the 20-sweep
+    trace replayed through als_sweep (eager first uses, then captured phase graphs) against the
+    oracle, and als_run (one device launch, the fused build inside the SWITCH body) bit-identical
+    to the host loop and following the oracle's free-running schedule."""
+    import synthgen as Gs
+    r = np.random.default_rng(41)
+    dims, K = (6, 8, 6, 128), 16
+    B = [r.random((d, K)) for d in dims]
+    X = np.ascontiguousarray(Gs.kruskal_slab(B) + 0.01 * r.standard_normal(dims))
+    A0 = [r.random((d, K)) for d in dims]
+    A_or, tr = O.pp_cp_als(X, A0, 0.0, 0.1, 20)
+    assert sum(t["phase"] == "pp-build" for t in tr) >= 2
+    cond = conditioning(X, A0, 0.1, 20, tr, A_or)
+    ctx = cp.cp_init(X, 4, dims, K)
+    cp.cp_set_factors(ctx, A0)
+    infos = []
+    for t in tr:
+        cp.cp_set_phase_override(ctx, t["phase"])
+        infos.append(cp.als_sweep(ctx, 0.0, 0.1))
+    check(tr, infos, cond, A_or, cp.cp_get_factors(ctx), tag="fused-build trace")
+    cp.cp_set_phase_override(ctx, cp.PHASE_AUTO)
+    b = cp.cp_init(X, 4, dims, K)
+    for rep in range(2):
+        cp.cp_set_factors(ctx, A0)
+        cp.cp_set_factors(b, A0)
+        host = [cp.als_sweep(ctx, 0.0, 0.1) for _ in range(20)]
+        dev = cp.als_run(b, 0.0, 0.1, 20)
+        assert len({d["seconds"] for d in dev}) == 1
+        assert [h["residual_sq"] for h in host] == [d["residual_sq"] for d in dev], rep
+    if all(t["margin"] > 1e-6 for t in tr):
+        assert [d["phase"] for d in dev] == [t["phase"] for t in tr]
+    cp.cp_destroy(ctx)
+    cp.cp_destroy(b)
