@@ -834,6 +834,10 @@ cppp_status run_fused_build(cppp_ctx* c) {
     fz.sf = d[f];
     const int64_t units0 = d[o] * (d[f] / 128);
     fz.nP = std::max<int64_t>(1, std::min<int64_t>(d[l], (148 * 7 + units0 - 1) / units0));
+    {   // equal chunks of the x_l range, none empty (an empty chunk would leave its partial unwritten)
+      const int64_t run = (d[l] + fz.nP - 1) / fz.nP;
+      fz.nP = (d[l] + run - 1) / run;
+    }
     fz.Af = c->Ap[f];
     fz.Al = c->Ap[l];
     fz.fl_o = o < l ? d[l] : 1;

@@ -131,3 +131,29 @@ def test_fullsize_C5_kernels_kruskal_closed_form():
     cp.cp_destroy(ctx)
     del Xd
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_fullsize_als_run_free_running_matches_oracle(name):
+    """The benchmarked call itself: one als_run (20 sweeps, device-side Alg. 3 decisions, one graph
+    launch) on the full-size tensor, free-running, against the oracle's free-running run: the same
+    phase schedule wherever the oracle's ε_pp margins are clear of rounding, and then every sweep
+    within the trace tolerances (tests/trace_check.py)."""
+    cfg = G.CONFIGS[name]
+    X = G.make_tensor(cfg)
+    A0 = G.initial_factors(cfg)
+    A_or, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, cfg.sweeps)
+    ctx, _ = device_ctx(cfg, X=X)
+    # (device_ctx profiles every kernel class, which sends als_run to the host loop: use a plain one)
+    cp.cp_destroy(ctx)
+    Xd = torch.from_numpy(np.ascontiguousarray(X).reshape(-1)).cuda()
+    ctx = cp.cp_init(Xd, cfg.N, cfg.dims, cfg.K, stream=torch.cuda.current_stream(), flags=cp.FLAG_BORROW_TENSOR)
+    cp.cp_set_factors(ctx, A0)
+    cp.als_run(ctx, 0.0, cfg.eps_pp, cfg.sweeps)          # first run: captures the graphs
+    cp.cp_set_factors(ctx, A0)
+    infos = cp.als_run(ctx, 0.0, cfg.eps_pp, cfg.sweeps)
+    assert len({i["seconds"] for i in infos}) == 1          # one device launch
+    if all(t["margin"] > 1e-6 for t in tr):
+        assert [i["phase"] for i in infos] == [t["phase"] for t in tr]
+        check(tr, infos, golden(name, X, A0, cfg.eps_pp, tr, A_or), A_or, cp.cp_get_factors(ctx), tag=name)
+    cp.cp_destroy(ctx)

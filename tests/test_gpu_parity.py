@@ -741,3 +741,17 @@ def test_fused_build_inside_sweeps_and_graphs():
         assert [d["phase"] for d in dev] == [t["phase"] for t in tr]
     cp.cp_destroy(ctx)
     cp.cp_destroy(b)
+
+
+def test_fused_build_uneven_x_l_chunks():
+    """The fused build cuts the loop mode's range into chunks (one partial each); with 6 values and
+    a wish for 4 chunks (300 units of the other modes) the chunks are 2, 2, 2 -- none empty (a
+    fourth, empty chunk would leave its partial unwritten)."""
+    dims, K = (2, 6, 300, 128), 4
+    X, A = random_problem(dims, K, 17)
+    ctx = cp.cp_init(X, 4, dims, K)
+    cp.cp_set_factors(ctx, A)
+    cp.pp_build_operators(ctx)
+    for (i, j), ref in O.pp_operators(X, A).items():
+        assert rel(cp.pp_get_operator(ctx, i, j), ref) < TOL, (i, j)
+    cp.cp_destroy(ctx)
