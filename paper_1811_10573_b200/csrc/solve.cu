@@ -210,28 +210,39 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
   // One pivot per step.  The diagonal owner of column j+1 updates its copy of W[j+1][j+1]
   // first, so the reciprocal overlaps the rest of the update.  A failed pivot test is recorded
   // (sticky) and acted on after the loop.
+  // shared-window addresses computed once (the generic-pointer form re-derived the window base
+  // with an S2R on every pivot, on the chain in front of the column load)
+  const uint32_t colb0 = smem_addr(&colb[0][0]), rdv0 = smem_addr(&rdv[0]);
+  const uint32_t my_l = colb0 + 8u * static_cast<uint32_t>(l), my_rows = colb0 + 8u * static_cast<uint32_t>(r0);
   for (int j = 0; j < K; ++j) {
-    const int b = j & 1;
+    const uint32_t bo = (j & 1) ? 128u * 8u : 0u;   // colb[b] / colb[b ^ 1]
     if (lowerw && r0 + 15 > j && 32 * cg + 31 > j && l > j) {
-      const double cl = colb[b][l] * rdv[b];
+      double cjl, rj;
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cjl) : "r"(my_l + bo) : "memory");
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(rj) : "r"(rdv0 + ((j & 1) ? 8u : 0u)) : "memory");
+      const double cl = cjl * rj;
       if (has_diag) {
-        diag = fma(-colb[b][l], cl, diag);
+        diag = fma(-cjl, cl, diag);
         if (l == j + 1) {
           if (!(diag > thresh)) bad_s = 1;
           dpiv[j + 1] = diag;
-          rdv[b ^ 1] = pivot_rcp(diag);
+          const double rn = pivot_rcp(diag);
+          asm volatile("st.shared.f64 [%0], %1;" ::"r"(rdv0 + ((j & 1) ? 0u : 8u)), "d"(rn) : "memory");
         }
       }
 #pragma unroll
       for (int v = 0; v < 16; v += 2) {
-        const double2 cc = *reinterpret_cast<const double2*>(&colb[b][r0 + v]);
-        w[v] = fma(-cc.x, cl, w[v]);
-        w[v + 1] = fma(-cc.y, cl, w[v + 1]);
+        double cx, cy;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(cx), "=d"(cy) : "r"(my_rows + bo + 8u * v) : "memory");
+        w[v] = fma(-cx, cl, w[v]);
+        w[v + 1] = fma(-cy, cl, w[v + 1]);
       }
       if (l == j + 1) {   // publish column j+1
 #pragma unroll
         for (int v = 0; v < 16; v += 2)
-          *reinterpret_cast<double2*>(&colb[b ^ 1][r0 + v]) = make_double2(w[v], w[v + 1]);
+          asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(my_rows + (1024u - bo) + 8u * v), "d"(w[v]),
+                       "d"(w[v + 1])
+                       : "memory");
       }
     }
     __syncthreads();
