@@ -77,7 +77,8 @@ typedef struct {
   size_t workspace_bytes;
   unsigned flags;           /* CPPP_FLAG_* */
   /* slab sharding of X along one mode (multi-GPU):
-   * this process holds rows [shard_offset, shard_offset+shard_extent) of mode shard_mode.
+   * this process holds rows [shard_offset, shard_offset+shard_extent) of mode shard_mode (any
+   * mode 0..N-1; X is then the dense local slab, extent shard_extent in that mode).
    * shard_mode = -1: X is whole.  s[] passed to cp_init are the GLOBAL sizes. */
   int shard_mode;
   int64_t shard_offset, shard_extent;

@@ -210,9 +210,10 @@ def _torch_workspace(nbytes: int, device: int):
 def cp_init(X, N: int, s: Sequence[int], K: int, *, device: int = 0, stream=None,
             flags: int = 0, shard_offset: Optional[int] = None, shard_extent: Optional[int] = None,
             nccl_unique_id: Optional[bytes] = None, rank: int = 0, world: int = 1,
-            torch_workspace: bool = True, host_allreduce=None, pinv_rel_tol: float = 0.0) -> Ctx:
+            torch_workspace: bool = True, host_allreduce=None, pinv_rel_tol: float = 0.0,
+            shard_mode: int = 0) -> Ctx:
     """cp_init (include/cppp.h).  X: numpy array (host) or torch CUDA tensor (device; borrowed
-    with FLAG_BORROW_TENSOR).  The device workspace is a torch uint8 tensor unless
+    with FLAG_BORROW_TENSOR); sharded (shard_extent given): this rank's slab of mode shard_mode.  The device workspace is a torch uint8 tensor unless
     torch_workspace=False (then the library cudaMallocs it).  stream: a torch.cuda.Stream or
     None (library-owned stream)."""
     L = lib()
@@ -225,7 +226,7 @@ def cp_init(X, N: int, s: Sequence[int], K: int, *, device: int = 0, stream=None
     if stream is not None:
         o.stream = stream.cuda_stream
     if shard_extent is not None:
-        o.shard_mode = 0
+        o.shard_mode = int(shard_mode)
         o.shard_offset = int(shard_offset)
         o.shard_extent = int(shard_extent)
     o.rank, o.world = rank, world
@@ -260,7 +261,7 @@ def cp_init(X, N: int, s: Sequence[int], K: int, *, device: int = 0, stream=None
     _check(ctx, st)
     ctx.local_rows = list(s)
     if shard_extent is not None:
-        ctx.local_rows[0] = int(shard_extent)
+        ctx.local_rows[int(shard_mode)] = int(shard_extent)
     return ctx
 
 

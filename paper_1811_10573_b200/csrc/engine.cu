@@ -122,10 +122,8 @@ struct cppp_ctx {
   double* ops_red = nullptr;
   size_t ops_red_count = 0;
   // the PP sweep's exchange terms T_m, m != q, likewise in one call (C-c)
-  double* T_red = nullptr;
-  size_t T_red_count = 0;
-  // 8 doubles right before S_all: the slab mode's norms land here so that they and S^(q)
-  // (q = 0, the first block) are all-reduced in one call (C-d)
+  // the slab mode's staging block [8 norms | K x K Gram]: its Gram kernel writes both here so
+  // that they are all-reduced in one call (C-d), then they are copied to S_all[q] / stats
   double* qhdr = nullptr;
   double* pp_partial = nullptr;
   double* sq_partial = nullptr;
@@ -490,19 +488,26 @@ cppp_status finish_mode(cppp_ctx* c, int n, const double* Mn, bool pp_phase) {
     // the slab mode (q = 0) writes its norms into qhdr, right before S^(q) = S_all's first block
     const bool packq = (n == c->q) && comm_on(c) && !c->dry;
     double* nrm = packq ? c->qhdr : c->stats + 3 * n;
+    double* Sn = packq ? c->qhdr + 8 : c->S_all + (int64_t)n * K * K;
     CUCHK(c, launch_solve_rows(Mn, An, ref, c->dA[n] + off * K, rows, K, c->Gamma, c->L, c->lmode,
                                c->rowstat, c->st));
     // S^(n), the norms and (last mode) the fitness terms in one kernel; Γ^(n) is still in place
     // (the next factorization starts after ev_S below)
-    CUCHK(c, launch_gram(An, rows, K, c->S_all + (int64_t)n * K * K, c->rowstat, nrm,
-                         last ? c->Gamma : nullptr, last ? c->stats + 3 * c->N : nullptr,
-                         c->gram_scratch, c->gram_counters, c->st));
+    // (the slab mode's fitness terms, when it is the last mode, are partial sums too: qhdr[3..4])
+    CUCHK(c, launch_gram(An, rows, K, Sn, c->rowstat, nrm, last ? c->Gamma : nullptr,
+                         last ? (packq ? c->qhdr + 3 : c->stats + 3 * c->N) : nullptr, c->gram_scratch,
+                         c->gram_counters, c->st));
   }
-  if (n == c->q && comm_on(c)) {
-    // S^(q) and the norms in ONE all-reduce (SURVEY C-d), then the norms into their stats slots
+  if (n == c->q && comm_on(c) && !c->dry) {
+    // S^(q), its norms (and fitness terms) in ONE all-reduce (SURVEY C-d), then into their slots
     STCHK(allreduce(c, c->qhdr, (size_t)K * K + 8));
+    CUCHK(c, cudaMemcpyAsync(c->S_all + (int64_t)n * K * K, c->qhdr + 8, sizeof(double) * K * K,
+                             cudaMemcpyDeviceToDevice, c->st));
     CUCHK(c, cudaMemcpyAsync(c->stats + 3 * n, c->qhdr, 3 * sizeof(double), cudaMemcpyDeviceToDevice,
                              c->st));
+    if (n == c->N - 1)
+      CUCHK(c, cudaMemcpyAsync(c->stats + 3 * c->N, c->qhdr + 3, 2 * sizeof(double), cudaMemcpyDeviceToDevice,
+                               c->st));
   }
   CUCHK(c, cudaEventRecord(c->ev_S, c->st));
   // the next mode's factorization starts right away on the side stream; inside a captured sweep
@@ -958,49 +963,61 @@ bool pp_stagger(const cppp_ctx* c) {
 
 cppp_status pp_monitor(cppp_ctx* c);
 
+// The slab mode's exchange terms T_m = M_p^(q,m) ×_q dA^(q) (partial over the local rows of mode q)
+// for m0 <= m < m1, m != q, then ONE all-reduce over their contiguous buffers (SURVEY C-c).
+cppp_status pp_exchange_terms(cppp_ctx* c, int m0, int m1) {
+  const int q = c->q;
+  int f = -1, l = -1;
+  for (int m = m0; m < m1; ++m) {
+    if (m == q) continue;
+    if (f < 0) f = m;
+    l = m;
+    if (c->dry) continue;
+    PPUpdateArgs a;
+    a.Mp = nullptr;
+    a.extra = nullptr;
+    a.ny = c->dl[m];
+    a.K = c->K;
+    a.out = c->T[m];
+    a.partial = c->pp_partial;
+    a.nterms = 1;
+    const int lo = std::min(q, m), hi = std::max(q, m);
+    PPTerm t;
+    t.op = c->ops[lo][hi];
+    t.dA = fac_local(c, c->dA, q);
+    t.nx = c->dl[q];
+    if (q < m) { t.sx = c->dl[m] * c->K; t.sy = c->K; }
+    else { t.sx = c->K; t.sy = c->dl[q] * c->K; }
+    a.t[0] = t;
+    CUCHK(c, launch_pp_update(a, c->st));
+  }
+  if (f < 0) return CPPP_OK;
+  return allreduce(c, c->T[f], (size_t)(c->T[l] - c->T[f]) + (size_t)c->dl[l] * c->K);
+}
+
 cppp_status run_pp_sweep(cppp_ctx* c, bool after_build) {
-  const int N = c->N;
-  const bool sh = c->q >= 0 && comm_on(c);
+  const int N = c->N, q = c->q;
+  const bool sh = q >= 0 && comm_on(c);
+  // Modes n < q see the current dA^(q) (the previous PP sweep's): form their exchange terms here,
+  // from the live dA^(q), so nothing written to T between sweeps (pp_update, pp_second_order) can
+  // leak in.  After a build dA^(q) = 0 and those terms vanish.
+  if (sh && q > 0 && !after_build) STCHK(pp_exchange_terms(c, 0, q));
   for (int n = 0; n < N; ++n) {
     const double* extra = nullptr;
-    if (sh && n != c->q) extra = c->T[n];
+    if (sh && n != q && !(after_build && n < q)) extra = c->T[n];
     uint32_t zero = 0u;
     if (after_build)
       for (int i = n + 1; i < N; ++i) zero |= 1u << i;
-    if (after_build && n == 0 && extra == nullptr) {   // every term is zero: M~^(0) = M_p^(0)
+    if (after_build && n == 0 && extra == nullptr) {
+      // every term is zero (dA^(i) = 0 for i > 0): M~^(0) = M_p^(0)
       STCHK(finish_mode(c, n, c->Mp[n], true));
     } else {
       if (n == 0 && !c->dry && pp_stagger(c)) CUCHK(c, launch_stagger(c->st));
-      STCHK(pp_update_mode(c, n, c->M[n], extra, sh && n != c->q, c->Mp[n], zero));
+      STCHK(pp_update_mode(c, n, c->M[n], extra, sh && n != q, c->Mp[n], zero));
       STCHK(finish_mode(c, n, c->M[n], true));
     }
-    if (sh && n == c->q) {
-      // T_m = M_p^(q,m) ×_q dA^(q) (partial over local rows) for every m != q, then ONE all-reduce
-      // over the contiguous T buffers (SURVEY C-c)
-      for (int m = 0; m < N; ++m) {
-        if (m == c->q) continue;
-        if (!c->dry) {
-          PPUpdateArgs a;
-          a.Mp = nullptr;
-          a.extra = nullptr;
-          a.ny = c->dl[m];
-          a.K = c->K;
-          a.out = c->T[m];
-          a.partial = c->pp_partial;
-          a.nterms = 1;
-          const int lo = std::min(c->q, m), hi = std::max(c->q, m);
-          PPTerm t;
-          t.op = c->ops[lo][hi];
-          t.dA = fac_local(c, c->dA, c->q);
-          t.nx = c->dl[c->q];
-          if (c->q < m) { t.sx = c->dl[m] * c->K; t.sy = c->K; }
-          else { t.sx = c->K; t.sy = c->dl[c->q] * c->K; }
-          a.t[0] = t;
-          CUCHK(c, launch_pp_update(a, c->st));
-        }
-      }
-      STCHK(allreduce(c, c->T_red, c->T_red_count));
-    }
+    // modes n > q see the dA^(q) just formed
+    if (sh && n == q) STCHK(pp_exchange_terms(c, q + 1, N));
   }
   if (c->policy == CPPP_POLICY_BOUND) STCHK(pp_monitor(c));
   return CPPP_OK;
@@ -1293,8 +1310,7 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
     oMp[n] = take(sizeof(double) * c->dl[n] * K);
   }
   for (int n = 0; n < N; ++n) oT[n] = take(sizeof(double) * c->dl[n] * K);   // back to back (C-c)
-  const size_t oQh = take(0);            // qhdr: the 8 doubles right before S_all
-  off = oQh + 8 * sizeof(double);        // (S_all need not be 256-byte aligned)
+  const size_t oQh = take(sizeof(double) * (8 + (size_t)K * K));   // qhdr staging
   size_t oS = take(sizeof(double) * N * K * K);
   size_t oG = take(sizeof(double) * solve_ld(K) * solve_ld(K));
   // packed factor, inverted 32 x 32 diagonal blocks, Jacobi V
@@ -1371,16 +1387,6 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
     for (int j = i + 1; j < N; ++j) c->ops[i][j] = reinterpret_cast<double*>(b + oOps[i][j]);
   c->ops_red = reinterpret_cast<double*>(b + red_lo);
   c->ops_red_count = (red_hi - red_lo) / sizeof(double);
-  {
-    int m0 = -1, m1 = -1;
-    for (int m = 0; m < N; ++m)
-      if (m != c->q) {
-        if (m0 < 0) m0 = m;
-        m1 = m;
-      }
-    c->T_red = c->T[m0];
-    c->T_red_count = (size_t)(c->T[m1] - c->T[m0]) + (size_t)c->dl[m1] * K;
-  }
   c->qhdr = reinterpret_cast<double*>(b + oQh);
   c->pp_partial = reinterpret_cast<double*>(b + oPP);
   c->sq_partial = reinterpret_cast<double*>(b + oSq);
@@ -1403,11 +1409,11 @@ cppp_status validate(cppp_ctx* c, int N, const int64_t* s, int K, const cppp_opt
   for (int n = 0; n < N; ++n)
     if (s[n] < 1) return fail(c, CPPP_EINVAL, "dimension mismatch: s[%d]=%lld < 1", n, (long long)s[n]);
   if (o && o->shard_mode != -1) {
-    if (o->shard_mode != 0)
-      return fail(c, CPPP_EINVAL, "slab sharding is along mode 0 only (got mode %d)", o->shard_mode);
-    if (o->shard_offset < 0 || o->shard_extent < 1 || o->shard_offset + o->shard_extent > s[0])
-      return fail(c, CPPP_EINVAL, "shard [%lld, +%lld) outside mode 0 of size %lld",
-                  (long long)o->shard_offset, (long long)o->shard_extent, (long long)s[0]);
+    const int q = o->shard_mode;
+    if (q < 0 || q >= N) return fail(c, CPPP_EINVAL, "shard mode %d outside [0, %d)", q, N);
+    if (o->shard_offset < 0 || o->shard_extent < 1 || o->shard_offset + o->shard_extent > s[q])
+      return fail(c, CPPP_EINVAL, "shard [%lld, +%lld) outside mode %d of size %lld",
+                  (long long)o->shard_offset, (long long)o->shard_extent, q, (long long)s[q]);
   }
   return CPPP_OK;
 }
@@ -1418,11 +1424,11 @@ void setup_dims(cppp_ctx* c, int N, const int64_t* s, int K, const cppp_opts* o)
   c->flags = o ? o->flags : 0u;   // the plan (tree shapes) depends on the flags
   for (int n = 0; n < N; ++n) c->s[n] = c->dl[n] = s[n];
   c->q = -1;
-  if (o && o->shard_mode == 0) {
-    c->q = 0;
+  if (o && o->shard_mode >= 0 && o->shard_mode < N) {
+    c->q = o->shard_mode;
     c->qoff = o->shard_offset;
     c->qext = o->shard_extent;
-    c->dl[0] = o->shard_extent;
+    c->dl[c->q] = o->shard_extent;
   }
   c->numel_local = 1;
   for (int n = 0; n < N; ++n) c->numel_local *= c->dl[n];
@@ -2141,8 +2147,8 @@ size_t cppp_plan_describe(int N, int shard_mode, char* buf, size_t buflen) {
   for (int n = 0; n < N; ++n) s[n] = 4;
   cppp_opts o;
   cppp_default_opts(&o);
-  if (shard_mode == 0) {
-    o.shard_mode = 0;
+  if (shard_mode >= 0 && shard_mode < N) {
+    o.shard_mode = shard_mode;
     o.shard_offset = 0;
     o.shard_extent = 2;
   }

@@ -48,18 +48,19 @@ def slab(s0, rank, world):
     return rank * s0 // world, (rank + 1) * s0 // world
 
 
-def run_sharded(P, X, dims, K, body):
-    """Run body(rank, ctx, lo, hi) on P threads with sharded contexts; returns per-rank results."""
+def run_sharded(P, X, dims, K, body, q=0):
+    """Run body(rank, ctx, lo, hi) on P threads with contexts sharded along mode q; returns
+    per-rank results."""
     red = HostReducer(P)
     out = [None] * P
     err = [None] * P
 
     def work(rank):
         try:
-            lo, hi = slab(dims[0], rank, P)
-            Xs = np.ascontiguousarray(X[lo:hi])
+            lo, hi = slab(dims[q], rank, P)
+            Xs = np.ascontiguousarray(np.take(X, np.arange(lo, hi), axis=q))
             ctx = cp.cp_init(Xs, len(dims), dims, K, shard_offset=lo, shard_extent=hi - lo, rank=rank,
-                             world=P, torch_workspace=False, host_allreduce=red.fn(rank))
+                             world=P, torch_workspace=False, host_allreduce=red.fn(rank), shard_mode=q)
             out[rank] = body(rank, ctx, lo, hi)
             cp.cp_destroy(ctx)
         except Exception as e:  # noqa: BLE001
@@ -244,3 +245,48 @@ def test_sharded_als_run_free_running(P):
     cond = golden("C5mini", X, A0, cfg.eps_pp, tr, A_fin)
     if [i["phase"] for i in res[0][0]] == [t["phase"] for t in tr]:
         check(tr, res[0][0], cond, A_fin, res[0][1], tag=("als_run", P))
+
+
+@pytest.mark.parametrize("q", [1, "last"])
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("name", ["C1", "C3mini", "C4mini"])
+def test_sharded_along_other_modes(q, P, name):
+    """Slabs of a middle or of the LAST mode (BASELINE C5 names mode-4 slabs): MTTKRP, every
+    operator and a replayed 12-sweep trace against the unsharded oracle, replicas bit-identical."""
+    cfg = G.CONFIGS[name]
+    q = cfg.N - 1 if q == "last" else q
+    X = G.make_tensor(cfg)
+    A0 = G.initial_factors(cfg)
+    A_fin, tr = O.pp_cp_als(X, A0, 0.0, cfg.eps_pp, 12)
+
+    def body(rank, ctx, lo, hi):
+        cp.cp_set_factors(ctx, A0)
+        M = cp.mttkrp_dt(ctx)
+        cp.pp_build_operators(ctx)
+        ops = {(i, j): cp.pp_get_operator(ctx, i, j) for i in range(cfg.N) for j in range(i + 1, cfg.N)}
+        cp.cp_set_factors(ctx, A0)
+        infos = []
+        for t in tr:
+            cp.cp_set_phase_override(ctx, t["phase"])
+            infos.append(cp.als_sweep(ctx, 0.0, cfg.eps_pp))
+        return M, ops, infos, cp.cp_get_factors(ctx)
+
+    res = run_sharded(P, X, cfg.dims, cfg.K, body, q=q)
+    ops_ref = O.pp_operators(X, A0)
+    cond = golden(name, X, A0, cfg.eps_pp, tr, A_fin)
+    for rank, (M, ops, infos, A) in enumerate(res):
+        lo, hi = slab(cfg.s, rank, P)
+        for n in range(cfg.N):
+            ref = O.mttkrp(X, A0, n)
+            assert rel(M[n], ref[lo:hi] if n == q else ref) < 1e-11, (rank, n)
+        for (i, j), ref in ops_ref.items():
+            if i == q:
+                ref = ref[lo:hi]
+            elif j == q:
+                ref = ref[:, lo:hi]
+            assert rel(ops[(i, j)], ref) < 1e-11, (rank, i, j)
+        check(tr, infos, cond, A_fin, A, tag=(name, q, P, rank))
+    for n in range(cfg.N):
+        if n != q:
+            for rank in range(1, P):
+                assert np.array_equal(res[rank][3][n], res[0][3][n])
