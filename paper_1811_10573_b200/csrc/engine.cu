@@ -413,6 +413,64 @@ cppp_status contract(cppp_ctx* c, const Node& src, int u, const double* F, doubl
   return CPPP_OK;
 }
 
+// Batched multi-TTV jobs (ttv.cu launch_ttv_batch): the contraction of a non-root node `src`
+// along mode u into `out` (same geometry as contract()), and the one-pass pair of two children
+// contracting modes u1 < u2 that are adjacent among src's kept modes.
+TtvJob single_job(cppp_ctx* c, const Node& src, int u, const double* F, double* out) {
+  TtvJob j;
+  int64_t B = 1, R = 1;
+  for (int v = 0; v < c->N; ++v) {
+    if (!(src.mask & (1u << v)) || v == u) continue;
+    if (v < u) B *= c->dl[v];
+    else R *= c->dl[v];
+  }
+  j.P = src.data;
+  j.Fb = F;
+  j.outB = out;
+  j.Bo = B;
+  j.Sa = 1;
+  j.Sb = (int)c->dl[u];
+  j.IN = R * c->K;
+  return j;
+}
+TtvJob pair_job(cppp_ctx* c, const Node& src, int u1, const double* F1, double* out1, int u2,
+                const double* F2, double* out2) {
+  TtvJob j;
+  int64_t B = 1, R = 1;
+  for (int v = 0; v < c->N; ++v) {
+    if (!(src.mask & (1u << v)) || v == u1 || v == u2) continue;
+    if (v < u1) B *= c->dl[v];
+    else R *= c->dl[v];
+  }
+  j.P = src.data;
+  j.Fa = F1;     // child a contracts u1 (the outer of the two)
+  j.outA = out1;
+  j.Fb = F2;     // child b contracts u2
+  j.outB = out2;
+  j.Bo = B;
+  j.Sa = (int)c->dl[u1];
+  j.Sb = (int)c->dl[u2];
+  j.IN = R * c->K;
+  return j;
+}
+bool ttv_batch_on(const cppp_ctx* c) {
+  static const bool off = getenv("CPPP_NO_TTV_BATCH") != nullptr;   // A/B: one launch per child
+  return !off && !(c->flags & CPPP_FLAG_NO_FUSED_TTV);
+}
+cppp_status run_ttv_jobs(cppp_ctx* c, const std::vector<TtvJob>& jobs) {
+  if (c->dry || jobs.empty()) return CPPP_OK;
+  double flops = 0.0, bytes = 0.0;
+  for (const TtvJob& j : jobs) {
+    const double pe = (double)j.Bo * j.Sa * j.Sb * j.IN;
+    const int nch = j.Fa ? 2 : 1;
+    flops += 2.0 * pe * nch;
+    bytes += 8.0 * (pe + (double)j.Bo * j.Sa * j.IN + (j.Fa ? (double)j.Bo * j.Sb * j.IN : 0.0));
+  }
+  Prof p(c, CPPP_K_TTV, flops, bytes, c->st);
+  CUCHK(c, launch_ttv_batch(jobs.data(), (int)jobs.size(), c->K, c->st));
+  return CPPP_OK;
+}
+
 // Multi-mode first level: contract the consecutive modes `modes` (ascending) of X in ONE GEMM
 // with their Khatri-Rao product (P:78-80 applied to a whole half of the tree at once; same
 // 2 s^N R flops as a single-mode TTM, but no s^(N-1) R intermediate and no multi-TTV pass over
@@ -736,7 +794,8 @@ struct PPTree {
         double* dst = child_leaf ? op_ptr(kept) : c->stack.push(node_elems(c, kept));
         if (!(have12 && child_leaf && kept == 0x6u))
           STCHK(contract(c, nd, tau[w], fac_local(c, c->Ap, tau[w]), dst));
-        STCHK(visit(Node{kept, dst, false}, cmu, level + 1));
+        if (!child_leaf && ttv_batch_on(c)) STCHK(subtree_batched(Node{kept, dst, false}, cmu));
+        else STCHK(visit(Node{kept, dst, false}, cmu, level + 1));
         c->stack.release(mk);
       }
       return CPPP_OK;
@@ -758,6 +817,87 @@ struct PPTree {
     return CPPP_OK;
   }
 
+  // Below a level-1 node, level by level (SURVEY a2 "batched multi-TTV"): every contraction of a
+  // level in one batched launch (two when a parent feeds a one-pass pair), instead of one launch
+  // per child depth first.  Same nodes and values as Def. pptree's traversal (L24); the nodes of
+  // the subtree stay on the stack until its leaves are written.
+  cppp_status subtree_batched(const Node& l1, uint32_t mu1) {
+    const int N = c->N;
+    struct Item {
+      Node nd;
+      uint32_t mu;
+    };
+    std::vector<Item> cur{{l1, mu1}};
+    for (int level = 1; level < N - 2; ++level) {
+      const bool child_leaf = (level + 1 == N - 2);
+      std::vector<Item> next;
+      std::vector<TtvJob> jobs;
+      for (const Item& it : cur) {
+        int maxmu = -1;
+        for (int t = 0; t < N; ++t)
+          if (it.mu & (1u << t)) maxmu = t;
+        struct Kid {
+          int u;
+          double* dst;
+        };
+        std::vector<Kid> kid;
+        for (int w = maxmu + 1; w <= level + 2; ++w) {
+          const uint32_t cmu = it.mu | (1u << w);
+          const uint32_t kept = kept_of(cmu);
+          double* dst = child_leaf ? op_ptr(kept) : c->stack.push(node_elems(c, kept));
+          next.push_back(Item{Node{kept, dst, false}, cmu});
+          kid.push_back(Kid{tau[w], dst});
+        }
+        // one pair per parent: two children contracting kept modes adjacent in the parent (no
+        // kept mode between them), the inner one with extent <= TTV_PAIR_MAXSB; the innermost such pair
+        std::vector<bool> used(kid.size(), false);
+        int best_a = -1, best_b = -1;
+        for (size_t x = 0; x < kid.size(); ++x)
+          for (size_t y = 0; y < kid.size(); ++y) {
+            const int u1 = kid[x].u, u2 = kid[y].u;
+            if (u1 >= u2 || c->dl[u2] > TTV_PAIR_MAXSB) continue;
+            bool adjacent = true;
+            for (int v = u1 + 1; v < u2; ++v)
+              if (it.nd.mask & (1u << v)) adjacent = false;
+            if (!adjacent) continue;
+            if (best_a < 0 || u2 > kid[best_b].u) {
+              best_a = (int)x;
+              best_b = (int)y;
+            }
+          }
+        const bool big = (double)node_elems(c, it.nd.mask) * 8.0 > 64.0 * (1 << 20);
+        // pairs only for parents beyond L2 with enough columns to fill the GPU: on L2-resident
+        // parents the batched singles share the parent through L2 anyway, and a pair job's few
+        // long threads lost there (C4 level 4: 49 vs 12 us); C4 level 2 (768 MB parents):
+        // node {1} 243 -> 186 us, node {0} 356 -> 317 us
+        const bool pair_ok = big && best_a >= 0 &&
+                             node_elems(c, it.nd.mask) / (c->dl[kid[best_a].u] * c->dl[kid[best_b].u]) >= 65536;
+        if (pair_ok && !pair_off()) {
+          const int u1 = kid[best_a].u, u2 = kid[best_b].u;
+          TtvJob j = pair_job(c, it.nd, u1, fac_local(c, c->Ap, u1), kid[best_a].dst, u2,
+                              fac_local(c, c->Ap, u2), kid[best_b].dst);
+          j.stream = big;
+          jobs.push_back(j);
+          used[best_a] = used[best_b] = true;
+        }
+        for (size_t x = 0; x < kid.size(); ++x) {
+          if (used[x]) continue;
+          TtvJob j = single_job(c, it.nd, kid[x].u, fac_local(c, c->Ap, kid[x].u), kid[x].dst);
+          j.stream = big;
+          jobs.push_back(j);
+        }
+      }
+      STCHK(run_ttv_jobs(c, jobs));
+      cur.swap(next);
+    }
+    return CPPP_OK;
+  }
+
+  static bool pair_off() {
+    static const bool off = getenv("CPPP_NO_TTV_PAIR") != nullptr;   // A/B
+    return off;
+  }
+
   cppp_status emit_children(const Node& nd, uint32_t mu, int maxmu, int level,
                             const std::vector<Node>& kids) {
     size_t i = 0;
@@ -777,6 +917,7 @@ struct PPTree {
 // M_p^(n) = M_p^(j,n) ×_j A_p^(j), j = min{j ∉ {n, q}}
 cppp_status build_singles(cppp_ctx* c) {
   const int N = c->N, K = c->K;
+  std::vector<TtvJob> jobs;
   for (int n = 0; n < N; ++n) {
     int j = -1;
     for (int v = 0; v < N; ++v)
@@ -786,8 +927,15 @@ cppp_status build_singles(cppp_ctx* c) {
       }
     const int a = std::min(j, n), b = std::max(j, n);
     Node op{(1u << a) | (1u << b), c->ops[a][b], false};
-    STCHK(contract(c, op, j, fac_local(c, c->Ap, j), c->Mp[n]));
+    if (ttv_batch_on(c)) {
+      TtvJob jb = single_job(c, op, j, fac_local(c, c->Ap, j), c->Mp[n]);
+      jb.stream = (double)node_elems(c, op.mask) * 8.0 > 64.0 * (1 << 20);
+      jobs.push_back(jb);
+    } else {
+      STCHK(contract(c, op, j, fac_local(c, c->Ap, j), c->Mp[n]));
+    }
   }
+  STCHK(run_ttv_jobs(c, jobs));   // the N single-mode operators in one batched launch
   (void)K;
   return CPPP_OK;
 }

@@ -130,6 +130,31 @@ size_t ttv_scratch_doubles();
 cudaError_t launch_ttv_cfg(const double* P, int64_t B, int64_t S, int64_t R, int K,
                            const double* F, double* out, int V, int U, int xs, cudaStream_t st);
 
+// Batched multi-TTV (ttv.cu): job j views its parent as [Bo][Sa][Sb][IN] (IN includes K) and
+// writes outB[bo][xa][t] = Σ_xb P·Fb[xb][k]; a PAIR job (Fa != null, Sb <= TTV_PAIR_MAXSB) also writes
+// outA[bo][xb][t] = Σ_xa P·Fa[xa][k] from the same pass over the parent (Sb <= TTV_PAIR_MAXSB).
+// Single jobs: Sa = 1.
+struct TtvJob {
+  const double* P = nullptr;
+  const double* Fa = nullptr;
+  const double* Fb = nullptr;
+  double* outA = nullptr;
+  double* outB = nullptr;
+  int64_t Bo = 1, IN = 1;
+  int Sa = 1, Sb = 1;
+  int64_t nvec = 0;   // set by the launcher
+  int cta0 = 0;       // set by the launcher
+  int stream = 0;     // parent read with evict-first loads (large parents)
+};
+constexpr int TTV_MAX_JOBS = 24;
+constexpr int TTV_PAIR_MAXSB = 24;   // inner extent of a one-pass pair (register-resident sums)
+struct TtvBatch {
+  TtvJob j[TTV_MAX_JOBS];
+  int njobs;
+  int K;
+};
+cudaError_t launch_ttv_batch(const TtvJob* jobs, int n, int K, cudaStream_t st);
+
 
 // PP update (Alg. 3): Mt[y][k] = Mp[y][k] + extra[y][k]
 //   + Σ_t Σ_x Op_t(x, y, k) * dA_t[x][k], Op_t(x,y,k) at Op_t + x*sx_t + y*sy_t + k.

@@ -15,6 +15,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 namespace cppp {
 namespace {
@@ -145,6 +146,161 @@ cudaError_t launch_v(const double* P, int64_t S, int64_t RK, int K, int64_t tota
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- batched multi-TTV
+// ONE launch for a list of jobs (all the contractions of one construction-tree level, or the N
+// single-mode operators; SURVEY a2 "batched multi-TTV").  Job j views its parent as
+// [Bo][Sa][Sb][IN] (IN = the kept extents after the contracted ones, times K) and computes
+//   child b: outB[bo][xa][t] = Σ_xb P[bo][xa][xb][t] · Fb[xb][k]        (always)
+//   child a: outA[bo][xb][t] = Σ_xa P[bo][xa][xb][t] · Fa[xa][k]        (pair jobs, Fa != null)
+// A pair job reads its parent ONCE for two children contracting adjacent kept modes (Sb <= 32:
+// child a's Sb partial sums stay in registers across the xa loop).  A single job has Sa = 1.
+// Each output is owned by one thread and summed in ascending x (with the x split of
+// launch_ttv: cluster partials added in rank order) -- the same fma chain as ttv_kernel.
+// single jobs (Sa = 1): ttv_kernel's arithmetic per job, the x split over a (1, xs, 1) cluster
+template <int V>
+__global__ void __launch_bounds__(TTV_THREADS)
+    ttv_batch_kernel(const __grid_constant__ TtvBatch bt) {
+  using T = typename Vec<V>::T;
+  pdl_wait();
+  __shared__ T red[TTV_THREADS];
+  int ji = 0;
+  while (ji + 1 < bt.njobs && (int)blockIdx.x >= bt.j[ji + 1].cta0) ++ji;
+  const double* __restrict__ P = bt.j[ji].P;
+  const double* __restrict__ F = bt.j[ji].Fb;
+  double* out = bt.j[ji].outB;
+  const int64_t IN = bt.j[ji].IN, S = bt.j[ji].Sb, nvec = bt.j[ji].nvec;
+  const bool stream = bt.j[ji].stream != 0;
+  const int K = bt.K;
+  const int64_t e = ((int64_t)blockIdx.x - bt.j[ji].cta0) * TTV_THREADS + threadIdx.x;
+  const int p = blockIdx.y, xs = gridDim.y;
+  T acc;
+  if constexpr (V == 1) acc = 0.0;
+  else acc = make_double2(0.0, 0.0);
+  if (e < nvec) {
+    const int64_t o = e * V;
+    const int64_t b = o / IN;
+    const int64_t t = o - b * IN;
+    const int k = static_cast<int>(t % K);
+    const int64_t x0 = S * p / xs, x1 = S * (p + 1) / xs;
+    const double* pp = P + b * S * IN + t;
+    const double* f = F + k;
+    int64_t x = x0;
+    for (; x + 4 <= x1; x += 4) {
+      T pv[4], fv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        pv[u] = stream ? Vec<V>::ld_stream(pp + (x + u) * IN) : Vec<V>::ld(pp + (x + u) * IN);
+        fv[u] = Vec<V>::ld(f + (x + u) * K);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) vfma(acc, pv[u], fv[u]);
+    }
+    for (; x < x1; ++x) vfma(acc, Vec<V>::ld(pp + x * IN), Vec<V>::ld(f + x * K));
+  }
+  if (xs == 1) {
+    if (e < nvec) *reinterpret_cast<T*>(out + e * V) = acc;
+    return;
+  }
+  red[threadIdx.x] = acc;
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (p == 0 && e < nvec) {
+    T s = acc;
+    const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&red[threadIdx.x]));
+    for (int r = 1; r < xs; ++r) {
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+      T v;
+      if constexpr (V == 1) {
+        asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote));
+      } else {
+        asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(remote));
+      }
+      vadd(s, v);
+    }
+    *reinterpret_cast<T*>(out + e * V) = s;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// pair jobs: one pass over the parent for two children contracting adjacent kept modes
+template <int MAXSB>
+__global__ void __launch_bounds__(TTV_THREADS, 2)
+    ttv_pair_kernel(const __grid_constant__ TtvBatch bt) {
+  pdl_wait();
+  int ji = 0;
+  while (ji + 1 < bt.njobs && (int)blockIdx.x >= bt.j[ji + 1].cta0) ++ji;
+  const double* __restrict__ P = bt.j[ji].P;
+  const double* __restrict__ Fa = bt.j[ji].Fa;
+  const double* __restrict__ Fb = bt.j[ji].Fb;
+  double* outA = bt.j[ji].outA;
+  double* outB = bt.j[ji].outB;
+  const int64_t IN = bt.j[ji].IN, nvec = bt.j[ji].nvec;
+  const int Sa = bt.j[ji].Sa, Sb = bt.j[ji].Sb;
+  const bool stream = bt.j[ji].stream != 0;
+  const int K = bt.K;
+  const int64_t e = ((int64_t)blockIdx.x - bt.j[ji].cta0) * TTV_THREADS + threadIdx.x;
+  if (e >= nvec) return;
+  const int64_t bo = e / IN, t = e - bo * IN;
+  const int k = static_cast<int>(t % K);
+  double accA[MAXSB];
+#pragma unroll
+  for (int u = 0; u < MAXSB; ++u) accA[u] = 0.0;
+  const double* pp = P + bo * (int64_t)Sa * Sb * IN + t;
+  for (int xa = 0; xa < Sa; ++xa) {
+    const double fa = __ldg(Fa + (int64_t)xa * K + k);
+    const double* px = pp + (int64_t)xa * Sb * IN;
+    const double* fb = Fb + k;
+    double accB = 0.0;
+    // every xb load of this xa in flight at once (registers: MAXSB accumulators + MAXSB loads);
+    // running pointers (hoisted per-xb offsets would take 2 MAXSB more registers)
+    double pv[MAXSB];
+#pragma unroll
+    for (int u = 0; u < MAXSB; ++u) {
+      if (u < Sb) pv[u] = stream ? __ldcs(px) : __ldg(px);
+      px += IN;
+    }
+#pragma unroll
+    for (int u = 0; u < MAXSB; ++u) {
+      if (u < Sb) {
+        accB = fma(pv[u], __ldg(fb), accB);
+        accA[u] = fma(pv[u], fa, accA[u]);
+      }
+      fb += K;
+    }
+    outB[(bo * Sa + xa) * IN + t] = accB;
+  }
+#pragma unroll
+  for (int u = 0; u < MAXSB; ++u)
+    if (u < Sb) outA[(bo * Sb + u) * IN + t] = accA[u];
+}
+
+template <typename Kern>
+cudaError_t launch_batch_k(Kern kern, const TtvBatch& bt, int ctas, int xs, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ctas, (unsigned)xs, 1);
+  cfg.blockDim = dim3(TTV_THREADS, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (xs > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 1;
+    attr[na].val.clusterDim.y = (unsigned)xs;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, bt);
+  note_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 }  // namespace
 
 size_t ttv_scratch_doubles() { return 0; }
@@ -179,6 +335,67 @@ cudaError_t launch_ttv(const double* P, int64_t B, int64_t S, int64_t R, int K, 
     fprintf(stderr, "ttv B %lld S %lld R %lld K %d: V %d xs %d\n", (long long)B, (long long)S,
             (long long)R, K, V, xs);
   return launch_ttv_cfg(P, B, S, R, K, F, out, V, 4, xs, st);
+}
+
+}  // namespace cppp
+
+namespace cppp {
+
+// Batched multi-TTV: the pair jobs of jobs[0..n) in one launch and the single jobs in another
+// (per TTV_MAX_JOBS).  Pair jobs need Sb <= 32 and use 8-byte loads; single jobs take 16-byte
+// loads when K is even and every operand 16-byte aligned, and launch_ttv's x-split rule over
+// the batch's total CTA count.
+cudaError_t launch_ttv_batch(const TtvJob* jobs, int n, int K, cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(ttv_batch_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ttv_batch_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  for (int pass = 0; pass < 2; ++pass) {   // 0: pairs, 1: singles
+    std::vector<TtvJob> sel;
+    for (int i = 0; i < n; ++i)
+      if ((jobs[i].Fa != nullptr) == (pass == 0)) sel.push_back(jobs[i]);
+    for (size_t b0 = 0; b0 < sel.size(); b0 += TTV_MAX_JOBS) {
+      const int nb = (int)std::min(sel.size() - b0, (size_t)TTV_MAX_JOBS);
+      bool v2 = pass == 1 && K % 2 == 0;
+      int64_t minS = INT64_MAX;
+      for (int i = 0; i < nb; ++i) {
+        const TtvJob& J = sel[b0 + i];
+        if (pass == 0 && (J.Sb > TTV_PAIR_MAXSB || J.Sb < 1)) return cudaErrorInvalidValue;
+        if (pass == 1 && J.Sa != 1) return cudaErrorInvalidValue;
+        const uintptr_t al = reinterpret_cast<uintptr_t>(J.P) | reinterpret_cast<uintptr_t>(J.Fb) |
+                             reinterpret_cast<uintptr_t>(J.outB);
+        if (al % 16) v2 = false;
+        minS = std::min<int64_t>(minS, J.Sb);
+      }
+      const int V = v2 ? 2 : 1;
+      TtvBatch bt;
+      bt.njobs = nb;
+      bt.K = K;
+      int ctas = 0;
+      for (int i = 0; i < nb; ++i) {
+        bt.j[i] = sel[b0 + i];
+        bt.j[i].nvec = bt.j[i].Bo * bt.j[i].IN / (pass == 0 ? 1 : V);
+        bt.j[i].cta0 = ctas;
+        ctas += (int)((bt.j[i].nvec + TTV_THREADS - 1) / TTV_THREADS);
+      }
+      if (ctas == 0) continue;
+      cudaError_t e;
+      if (pass == 0) {
+        e = launch_batch_k(ttv_pair_kernel<TTV_PAIR_MAXSB>, bt, ctas, 1, st);
+      } else {
+        int xs = 1;
+        while (xs < 8 && (int64_t)ctas * xs < 148LL * 2 && minS / (2 * xs) >= 16) xs *= 2;
+        e = V == 2 ? launch_batch_k(ttv_batch_kernel<2>, bt, ctas, xs, st)
+                   : launch_batch_k(ttv_batch_kernel<1>, bt, ctas, xs, st);
+      }
+      if (e != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
 }
 
 }  // namespace cppp
