@@ -69,6 +69,9 @@ typedef enum {
                                         all-reduce transport on a single GPU (testing) */
 #define CPPP_FLAG_NO_OP_REUSE 256u /* order 3: PP builds recompute M_p^(1,2) instead of taking the
                                       preceding regular sweep's X x_0 A^(0) (A/B testing) */
+#define CPPP_FLAG_NO_FUSED_SOLVE 512u /* K <= 32, modes <= 64 rows: solve each mode through the
+                                      factorization + row-solve + Gram kernels instead of the one
+                                      fused launch (A/B testing; the two are bit-identical) */
 
 typedef struct {
   int device;               /* CUDA ordinal (default 0) */

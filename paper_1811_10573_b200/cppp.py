@@ -29,6 +29,7 @@ FLAG_NO_KRP = 32
 FLAG_NO_OVERLAP = 64
 FLAG_FORCE_COMM = 128
 FLAG_NO_OP_REUSE = 256
+FLAG_NO_FUSED_SOLVE = 512
 K_TTM, K_TTV, K_PPUPDATE, K_SOLVE, K_OTHER = range(5)
 KCLASS_NAMES = ["ttm", "ttv", "pp_update", "solve", "other", "factor"]
 

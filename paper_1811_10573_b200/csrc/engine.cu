@@ -508,8 +508,22 @@ bool contract_multi(cppp_ctx* c, const Node& src, const std::vector<int>& modes,
 // ---------------------------------------------------------------- small solve of one mode
 // A_new = M Γ^†, G, dA = A_new - ref, S^(n), norms (Alg. 1 P:393-399 / Alg. 3).
 // Issue Γ^(n) and its inverse on the side stream once every S^(m), m != n, is final (ev_S).
+// K <= 32 with every (local) mode <= 64 rows, order >= 4: each mode's solve is ONE launch on the
+// main stream (launch_mode_small: Γ, factorization, rows, Gram, statistics; bit-identical to the
+// chain of gamma factorization on the side stream + row solves + Gram), so nothing is prefetched.
+// Measured (20-sweep runs, A/B with CPPP_NO_FUSED_SOLVE): C4 1784 -> 1850 sweeps/s, the LAP / P6W
+// PP-approximated sweeps 208 -> 182 us; order 3 keeps the chain (C1 15.4 k -> 14.3 k sweeps/s
+// fused: there the side-stream factorization hides under each mode's TTV or GEMM).
+bool small_modes(const cppp_ctx* c) {
+  static const bool off = getenv("CPPP_NO_FUSED_SOLVE") != nullptr;   // A/B
+  if (off || (c->flags & CPPP_FLAG_NO_FUSED_SOLVE) || c->N < 4) return false;
+  for (int n = 0; n < c->N; ++n)
+    if (!mode_small_ok(c->K, c->dl[n])) return false;
+  return true;
+}
+
 cppp_status prefetch_inverse(cppp_ctx* c, int n) {
-  if (c->dry || c->prefetched == n) return CPPP_OK;
+  if (c->dry || c->prefetched == n || small_modes(c)) return CPPP_OK;
   CUCHK(c, cudaStreamWaitEvent(c->st2, c->ev_S, 0));
   {   // (the scope closes before ev_P: every side-stream node must be joined)
     Prof p(c, CPPP_K_FACTOR, (double)c->K * c->K * c->K / 3.0, 8.0 * c->K * c->K * c->N, c->st2);
@@ -535,8 +549,11 @@ cppp_status finish_mode(cppp_ctx* c, int n, const double* Mn, bool pp_phase) {
   const int K = c->K;
   const int64_t rows = c->dl[n];
   const int64_t off = (n == c->q) ? c->qoff : 0;
-  STCHK(prefetch_inverse(c, n));
-  CUCHK(c, cudaStreamWaitEvent(c->st, c->ev_P, 0));
+  const bool fused = small_modes(c);
+  if (!fused) {
+    STCHK(prefetch_inverse(c, n));
+    CUCHK(c, cudaStreamWaitEvent(c->st, c->ev_P, 0));
+  }
   c->prefetched = -1;
   {
     Prof p(c, CPPP_K_SOLVE, 4.0 * rows * K * K, 8.0 * rows * K * 5);
@@ -547,14 +564,21 @@ cppp_status finish_mode(cppp_ctx* c, int n, const double* Mn, bool pp_phase) {
     const bool packq = (n == c->q) && comm_on(c) && !c->dry;
     double* nrm = packq ? c->qhdr : c->stats + 3 * n;
     double* Sn = packq ? c->qhdr + 8 : c->S_all + (int64_t)n * K * K;
-    CUCHK(c, launch_solve_rows(Mn, An, ref, c->dA[n] + off * K, rows, K, c->Gamma, c->L, c->lmode,
-                               c->rowstat, c->st));
-    // S^(n), the norms and (last mode) the fitness terms in one kernel; Γ^(n) is still in place
-    // (the next factorization starts after ev_S below)
-    // (the slab mode's fitness terms, when it is the last mode, are partial sums too: qhdr[3..4])
-    CUCHK(c, launch_gram(An, rows, K, Sn, c->rowstat, nrm, last ? c->Gamma : nullptr,
-                         last ? (packq ? c->qhdr + 3 : c->stats + 3 * c->N) : nullptr, c->gram_scratch,
-                         c->gram_counters, c->st));
+    if (fused) {
+      const int ld = solve_ld(K);
+      CUCHK(c, launch_mode_small(c->S_all, c->N, n, K, Mn, An, ref, c->dA[n] + off * K, rows, Sn, nrm,
+                                 last ? (packq ? c->qhdr + 3 : c->stats + 3 * c->N) : nullptr, c->Gamma,
+                                 c->L, c->L + (int64_t)ld * ld + 4 * 32 * 33, c->st, c->pinv_tol));
+    } else {
+      CUCHK(c, launch_solve_rows(Mn, An, ref, c->dA[n] + off * K, rows, K, c->Gamma, c->L, c->lmode,
+                                 c->rowstat, c->st));
+      // S^(n), the norms and (last mode) the fitness terms in one kernel; Γ^(n) is still in place
+      // (the next factorization starts after ev_S below)
+      // (the slab mode's fitness terms, when it is the last mode, are partial sums too: qhdr[3..4])
+      CUCHK(c, launch_gram(An, rows, K, Sn, c->rowstat, nrm, last ? c->Gamma : nullptr,
+                           last ? (packq ? c->qhdr + 3 : c->stats + 3 * c->N) : nullptr, c->gram_scratch,
+                           c->gram_counters, c->st));
+    }
   }
   if (n == c->q && comm_on(c) && !c->dry) {
     // S^(q), its norms (and fitness terms) in ONE all-reduce (SURVEY C-d), then into their slots

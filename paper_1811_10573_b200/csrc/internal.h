@@ -202,6 +202,15 @@ size_t gram_scratch_doubles();
 cudaError_t launch_gram(const double* A, int64_t rows, int K, double* S, const double* rowstat,
                         double* nrm, const double* Gamma_model, double* fit, double* scratch,
                         unsigned int* counters, cudaStream_t st);
+// One small mode (K <= 32, rows <= 64) in ONE CTA: Γ^(n) from S_all, its factorization (L13;
+// the pseudo-inverse fallback through Gamma / Tp / Vscratch), A_new, G, dA, S^(n) -> Sn, and the
+// statistics gram_kernel leaves (nrm[0..2]; fit[0..1] when fit != null, Γ^(n)'s S:177 terms) —
+// bit-identical to launch_gamma_factor + launch_solve_rows + launch_gram.
+bool mode_small_ok(int K, int64_t rows);
+cudaError_t launch_mode_small(const double* S_all, int N, int n, int K, const double* M, double* A,
+                              const double* ref, double* dA, int64_t rows, double* Sn, double* nrm,
+                              double* fit, double* Gamma, double* Tp, double* Vscratch,
+                              cudaStream_t st, double tau);
 // ||x||² with a fixed reduction tree: partial[nblk] then out[0]
 cudaError_t launch_sqnorm(const double* x, int64_t n, double* partial, int nblk, double* out,
                           cudaStream_t st);

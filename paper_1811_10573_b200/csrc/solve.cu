@@ -933,6 +933,391 @@ __global__ void __launch_bounds__(GR_THREADS)
   }
 }
 
+// ---------------------------------------------------------------- one small mode, one launch
+// K <= 32 and rows <= MS_MAX_ROWS (C1, C4, the paper's P6W / LAP shapes): the whole mode — Γ^(n)
+// (P:364), its LDLᵀ factorization with the L13 pivot rule, the inverse of L, the row solves
+// A_new = M Γ^†, G = (A_old − A_new) Γ, dA, S^(n) = A_newᵀ A_new, the
+// norms and the S:177 fitness terms — in ONE CTA.  The three-kernel chain above spends most of a
+// small mode's time in launch gaps and cross-stream hops (C4: a 30 µs factorization on the side
+// stream, 2.6 µs event hops, 6 + 7 µs row / Gram kernels per mode).
+//
+// Every value is formed by the same IEEE operations in the same order as that chain
+// (gamma_small_kernel -> solve_rows_kernel -> gram_kernel with one row split), so the two paths
+// are bit-identical (tested); only the work is spread differently:
+//   * factorization: warp i keeps row i of W, lane k column k (the one-warp kernel kept row i in
+//     lane i).  Step j: row j (final after step j−1) is read from a double-buffered shared row,
+//     W[i][j] by a shuffle inside warp i, and W[i][k] −= (W[i][j]·(1/d_j))·W[j][k] for i, k > j;
+//     warp j+1 then publishes its row: one barrier per pivot, no per-pivot register sweep.
+//   * inverse of L (block_inverse_smem's column recurrences): warp c runs column c, lane j keeps
+//     y_j, so a step is one shuffle, one multiply and one fma instead of a 32-entry sweep.
+//   * rows: warp w takes rows w, w + NW, …; the Gram and the statistics reductions replay
+//     gram_kernel's 256-thread trees on warps 0-7.
+// The pseudo-inverse fallback (failed pivot test) runs gamma_pinv_dev on the whole CTA; its
+// Jacobi stopping test sums over the CTA's threads, so only that path may differ in rounding.
+constexpr int MS_MAX_ROWS = 64;
+
+template <int KP>
+struct MsCfg {
+  // warps: >= 8 (gram_kernel's 256-thread trees); K <= 32 keeps two rows of Γ per warp so the
+  // CTA stays at 512 threads (128 registers a thread)
+  static constexpr int NW = KP <= 8 ? 8 : 16;
+  static constexpr int RW = KP / NW > 1 ? KP / NW : 1;       // rows of Γ per warp
+};
+
+// gram_kernel's block_sum over 256 threads (8 warps) replayed on warps 0-7 of a larger CTA;
+// every thread must call it (barriers).  Result in all threads.
+template <int NV>
+__device__ __forceinline__ void sum256_n(double (&v)[NV], double* sh /* 32 NV */) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < NV; ++c) v[c] = warp_sum(v[c]);
+  __syncthreads();
+  if (lane == 0 && w < 8) {
+#pragma unroll
+    for (int c = 0; c < NV; ++c) sh[32 * c + w] = v[c];
+  }
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+      double r = lane < 8 ? sh[32 * c + lane] : 0.0;
+      r = warp_sum(r);
+      if (lane == 0) sh[32 * c] = r;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < NV; ++c) v[c] = sh[32 * c];
+  __syncthreads();
+}
+
+// warp_sum's xor butterfly for lane 0, replayed from the 32 lane values in shared memory:
+// ((v_l + v_{l+16}) level by level down to one value (fadd commutes, so each level is exact)
+__device__ __forceinline__ double butterfly32(const double* v) {
+  double x[16];
+#pragma unroll
+  for (int l = 0; l < 16; ++l) x[l] = v[l] + v[l + 16];
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+    for (int l = 0; l < o; ++l) x[l] = x[l] + x[l + o];
+  return x[0];
+}
+
+template <int KP>
+__global__ void __launch_bounds__(MsCfg<KP>::NW * 32, 1)
+    mode_small_kernel(const double* __restrict__ S_all, int N, int n, int K,
+                      const double* __restrict__ M, double* A, const double* ref, double* dA,
+                      int rows, double* Sn, double* nrm, double* fit, double* Gamma_g, double* P_g,
+                      double* Vscratch, double tau) {
+  constexpr int NW = MsCfg<KP>::NW, NT = NW * 32, RW = MsCfg<KP>::RW;
+  PROBE_T0();
+  // dynamic shared memory: [pinv overlay: K (K+1)] | M | A (old, then A_new in place) | ref
+  // (unless ref == A) | z, then d | per-lane statistic terms [rows][4][32] | row statistics
+  // [rows][4].  Row blocks are MS_MAX_ROWS x KP, zero past (rows, K): every loop below runs to
+  // compile-time bounds without predicates (the zero terms are the ones solve_rows_kernel and
+  // gram_kernel add too), and the rows are staged once (all loads in flight together).
+  extern __shared__ __align__(16) double ms_dyn[];
+  constexpr int RB = MS_MAX_ROWS * KP;
+  double* Ms = ms_dyn + ((K * (K + 1) + 1) & ~1);
+  double* Ao = Ms + RB;
+  const bool ref_is_A = ref == A;
+  double* Rf = ref_is_A ? Ao : Ao + RB;
+  double* Zs = Ao + 2 * RB;
+  double* Ps = Zs + RB;                     // [rows][4][32]
+  double* rs = Ps + MS_MAX_ROWS * 128;      // [rows][4]
+  __shared__ double Gs[32][33];   // Γ (zero past K)
+  __shared__ double Ls[32][33];   // 1 / L[i][i] on the diagonal, L below it; identity past K
+  __shared__ double Qs[32][33];   // Qs[c][j] = inv(L)[j][c] (pinv path: the pseudo-inverse)
+  __shared__ double Ss[32][33];   // S^(n)
+  __shared__ __align__(16) double Rb[2][32];
+  __shared__ double rinv_s[32];
+  __shared__ double red[7 * 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int ldt = (K + 7) & ~7;
+  pdl_wait();
+
+  // every load in flight at once: the N-1 Gram rows of Γ and the staged rows
+  double sv[RW][CPPP_MAX_ORDER_ - 1];
+#pragma unroll
+  for (int t = 0; t < RW; ++t) {
+    const int i = w * RW + t;
+#pragma unroll
+    for (int q = 0; q < CPPP_MAX_ORDER_ - 1; ++q) {
+      const int m = q < n ? q : q + 1;   // ascending m != n
+      sv[t][q] = (q < N - 1 && i < K && lane < K) ? __ldg(S_all + (int64_t)m * K * K + i * K + lane) : 1.0;
+    }
+  }
+  constexpr int LQ = RB / NT;
+  double lm[LQ], la[LQ], lr[LQ];
+#pragma unroll
+  for (int q = 0; q < LQ; ++q) {
+    const int f = tid + q * NT, y = f / KP, c = f % KP;
+    const bool in = y < rows && c < K;
+    const int e = y * K + c;
+    lm[q] = in ? __ldg(M + e) : 0.0;
+    la[q] = in ? A[e] : 0.0;
+    lr[q] = (in && !ref_is_A) ? ref[e] : 0.0;
+  }
+  // Γ^(n) = 1.0 · S^(m_0) · S^(m_1) · … (ascending m, as gamma_small_kernel); warp w keeps rows
+  // w RW + t, lane k column k
+  double g[RW];
+  double dmax = 0.0;
+#pragma unroll
+  for (int t = 0; t < RW; ++t) {
+    const int i = w * RW + t;
+    g[t] = 0.0;
+    if (i < K && lane < K) {
+      double x = 1.0;
+#pragma unroll
+      for (int q = 0; q < CPPP_MAX_ORDER_ - 1; ++q)
+        if (q < N - 1) x *= sv[t][q];
+      g[t] = x;
+    }
+    Gs[i][lane] = g[t];
+    if (i == lane && i < K) dmax = g[t];
+  }
+  for (int r = NW * RW + w; r < 32; r += NW) Gs[r][lane] = 0.0;
+#pragma unroll
+  for (int q = 0; q < LQ; ++q) {
+    const int f = tid + q * NT;
+    Ms[f] = lm[q];
+    Ao[f] = la[q];
+    if (!ref_is_A) Rf[f] = lr[q];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  if (lane == 0) red[w] = dmax;
+  if (w == 0) Rb[0][lane] = g[0];
+  __syncthreads();
+  double mx = 0.0;
+  for (int q = 0; q < NW; ++q) mx = fmax(mx, red[q]);
+  const double thresh = tau * mx;
+  PROBE_T(10);
+
+  // LDLᵀ, right-looking, one pivot per barrier (the one-warp kernel's operations element by
+  // element: cl = W[i][j]·(1/d_j), W[i][k] = fma(−cl, W[j][k], W[i][k]) for i, k > j)
+  bool bad = false;
+  for (int j = 0; j < K; ++j) {
+    const double d = Rb[j & 1][j];
+    const double rjk = Rb[j & 1][lane];
+    if (!(d > thresh)) bad = true;
+    const double rd = pivot_rcp(d);
+#pragma unroll
+    for (int t = 0; t < RW; ++t) {
+      const int i = w * RW + t;
+      const double wij = __shfl_sync(0xffffffffu, g[t], j);
+      const double cl = wij * rd;
+      if (i < K && lane < K && i > j && lane > j) g[t] = fma(-cl, rjk, g[t]);
+      if (i == j + 1) Rb[(j + 1) & 1][lane] = g[t];
+    }
+    __syncthreads();
+  }
+  PROBE_T(11);
+
+  // L[i][j] = W[i][j] / sqrt(d_j) (d_j = W[j][j], untouched after step j); formed and inverted
+  // whether or not the pivot test passed (a failed test replaces the result below)
+#pragma unroll
+  for (int t = 0; t < RW; ++t) {
+    const int i = w * RW + t;
+    if (i == lane && i < K) rinv_s[i] = 1.0 / sqrt(g[t]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < RW; ++t) {
+    const int r = w * RW + t;
+    double v;
+    if (r == lane) v = r < K ? rinv_s[r] : 1.0;
+    else v = (r < K && lane < K && lane < r) ? g[t] * rinv_s[lane] : 0.0;
+    Ls[r][lane] = v;
+  }
+  for (int r = NW * RW + w; r < 32; r += NW) Ls[r][lane] = r == lane ? 1.0 : 0.0;
+  __syncthreads();
+  if (w == 0) {   // inv(L): block_inverse_smem<KP>'s recurrences, lane c = column c (no shuffles)
+    const int c = lane;
+    double y[KP];
+#pragma unroll
+    for (int j = 0; j < KP; ++j) y[j] = 0.0;
+#pragma unroll
+    for (int i = 0; i < KP; ++i) {
+      const double dinv = Ls[i][i];
+      y[i] = i == c ? dinv : (i > c ? -y[i] * dinv : 0.0);
+#pragma unroll
+      for (int j = i + 1; j < KP; ++j) y[j] = fma(Ls[j][i], y[i], y[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < KP; ++j) Qs[c][j] = y[j];
+  }
+  if (bad) {   // CTA-uniform (every thread tested the same pivots)
+    // pseudo-inverse fallback (L13): Γ to global, gamma_pinv_dev on the whole CTA, P into Qs
+    __syncthreads();
+    for (int e = tid; e < K * ldt; e += NT) {
+      const int i = e / ldt, j = e - i * ldt;
+      Gamma_g[e] = j < K ? Gs[i][j] : 0.0;
+    }
+    __syncthreads();
+    gamma_pinv_dev(K, Gamma_g, P_g, ldt, Vscratch, tau);
+    __syncthreads();
+    for (int r = w; r < 32; r += NW) Qs[r][lane] = (r < K && lane < K) ? P_g[r * ldt + lane] : 0.0;
+  }
+  __syncthreads();
+  PROBE_T(12);
+
+  // rows: warp w takes rows w, w + NW, …, lane c = column c (solve_rows_kernel's arithmetic).
+  // The vector operand comes from shared memory (broadcast), the matrix operand from registers.
+  // No shuffles (the sums are replayed below).
+  //   pass 1: z = inv(L) m (even / odd accumulators)      [pinv: a = P m, one accumulator]
+  //   pass 2: a = inv(L)ᵀ z; d = a_old − a, dA, A; the lane terms of ‖a‖², ‖dA‖², Σ m∘a
+  //   pass 3: g = d Γ; the lane terms of ‖g‖²
+  const int c = lane < KP ? lane : 0;
+  {
+    double qv[KP];
+#pragma unroll
+    for (int jj = 0; jj < KP; ++jj) qv[jj] = Qs[jj][lane];
+    for (int y = w; y < MS_MAX_ROWS; y += NW) {
+      const double* mrow = Ms + y * KP;
+      double z;
+      if (!bad) {
+        double z0 = 0.0, z1 = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < KP; jj += 2) {
+          z0 = fma(qv[jj], mrow[jj], z0);
+          z1 = fma(qv[jj + 1], mrow[jj + 1], z1);
+        }
+        z = z0 + z1;
+      } else {
+        double a = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < KP; ++jj) a = fma(mrow[jj], qv[jj], a);
+        z = a;
+      }
+      if (lane < KP) Zs[y * KP + lane] = lane < K ? z : 0.0;
+      if (y + NW >= rows) break;
+    }
+  }
+  __syncwarp();
+  PROBE_T(1);
+  {
+    double qv[KP];
+#pragma unroll
+    for (int jj = 0; jj < KP; ++jj) qv[jj] = Qs[lane][jj];
+    for (int y = w; y < MS_MAX_ROWS; y += NW) {
+      const double* zrow = Zs + y * KP;
+      double m;
+      if (!bad) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < KP; jj += 2) {
+          a0 = fma(qv[jj], zrow[jj], a0);
+          a1 = fma(qv[jj + 1], zrow[jj + 1], a1);
+        }
+        m = a0 + a1;
+      } else {
+        m = zrow[c];
+      }
+      const int f = y * KP + c;
+      const bool in = y < rows && lane < K;
+      const double aold = Ao[f], rf = Rf[f], m0 = Ms[f];
+      __syncwarp();   // every lane has read row y of z before it is overwritten with d
+      const double ev = m - rf;
+      double na = 0.0, nd = 0.0, ip = 0.0;
+      if (in) {
+        const int e = y * K + lane;
+        A[e] = m;
+        dA[e] = ev;
+        na = fma(m, m, na);
+        nd = fma(ev, ev, nd);
+        ip = fma(m0, m, ip);
+      }
+      if (lane < KP) {
+        Ao[f] = in ? m : 0.0;            // A_new for the Gram (ref, when it aliases A, was read above)
+        Zs[f] = in ? aold - m : 0.0;     // d for pass 3
+      }
+      Ps[y * 128 + 0 * 32 + lane] = na;
+      Ps[y * 128 + 1 * 32 + lane] = nd;
+      Ps[y * 128 + 3 * 32 + lane] = ip;
+      if (y + NW >= rows) break;
+    }
+  }
+  __syncwarp();
+  PROBE_T(2);
+  {
+    double gv[KP];
+#pragma unroll
+    for (int p = 0; p < KP; ++p) gv[p] = Gs[p][lane];
+    for (int y = w; y < MS_MAX_ROWS; y += NW) {
+      const double* drow = Zs + y * KP;
+      double gg = 0.0;
+#pragma unroll
+      for (int p = 0; p < KP; ++p) gg = fma(drow[p], gv[p], gg);
+      Ps[y * 128 + 2 * 32 + lane] = lane < K ? fma(gg, gg, 0.0) : 0.0;
+      if (y + NW >= rows) break;
+    }
+  }
+  __syncthreads();
+  // the per-row sums, warp_sum's tree (thread = (row, statistic))
+  for (int e = tid; e < rows * 4; e += NT) rs[e] = butterfly32(Ps + e * 32);
+  __syncthreads();
+  PROBE_T(13);
+
+  // S^(n) = A_newᵀ A_new (gram_kernel: 4 accumulators by row mod 4, rows in ascending order,
+  // zero rows up to the row-pair loop's multiple of 4, (acc0 + acc1) + (acc2 + acc3))
+  const int r4 = 4 * (((rows + 1) / 2 + 1) / 2);
+  for (int e = tid; e < KP * KP; e += NT) {
+    const int a = e / KP, b = e - a * KP;
+    if (a > b || b >= K) continue;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int r = 0; r < r4; r += 4) {   // rows past `rows` are zero in Ao
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[t] = fma(Ao[(r + t) * KP + a], Ao[(r + t) * KP + b], acc[t]);
+    }
+    const double s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    Ss[a][b] = s;
+    Ss[b][a] = s;
+    Sn[a * K + b] = s;
+    Sn[b * K + a] = s;
+  }
+  if (nrm == nullptr) return;
+  __syncthreads();
+  PROBE_T(14);
+  // gram_kernel's statistics, every sum with its 256-thread tree: the row sums (0.0 + one row per
+  // virtual thread t < 256, rows <= 64) and, for the last mode, Σ Γ∘S by 16 x 16 tiles (thread
+  // t = (i, j) = (t >> 4, t & 15); the mirrored tile counted twice), all in one reduction
+  const int T = (K + 15) >> 4;
+  double v[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  if (tid < 256) {
+    if (tid < rows) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[c] += rs[4 * tid + c];
+    }
+    if (fit != nullptr) {
+#pragma unroll
+      for (int tile = 0; tile < 3; ++tile) {   // T <= 2: tile pairs (0,0), (0,1), (1,1)
+        const int ti = tile == 2 ? 1 : 0, tj = tile == 0 ? 0 : 1;
+        if (tj < T) {
+          const int gi = 16 * ti + (tid >> 4), gj = 16 * tj + (tid & 15);
+          double x = (gi < K && gj < K) ? Gs[gi][gj] * Ss[gi][gj] : 0.0;
+          if (ti != tj) x *= 2.0;
+          v[4 + tile] = x;
+        }
+      }
+    }
+  }
+  sum256_n<7>(v, red);
+  if (tid == 0) {
+    nrm[0] = v[0];
+    nrm[1] = v[1];
+    nrm[2] = v[2];
+    if (fit != nullptr) {
+      fit[0] = v[3];
+      double f = 0.0 + v[4];   // T == 1: 0.0 + the one tile, as gram_kernel's single-CTA path
+      if (T == 2) f = (f + v[5]) + v[6];
+      fit[1] = f;
+    }
+  }
+  PROBE_T(15);
+}
+
 __global__ void sqnorm_partial(const double* __restrict__ x, int64_t n, double* partial) {
   __shared__ double sh[32];
   double v = 0.0;
@@ -1081,6 +1466,39 @@ cudaError_t launch_solve_rows(const double* M, double* A, const double* ref, dou
   const int64_t blocks = (rows + SR_WARPS - 1) / SR_WARPS;
   cudaError_t e = launch_pdl(solve_rows_kernel, dim3((unsigned)blocks), dim3(SR_WARPS * 32), smem,
                              st, M, A, ref, dA, rows, K, Gamma, Tp, ldt, both ? 1 : 0, mode, rowstat);
+  note_launch();
+  return e;
+}
+
+bool mode_small_ok(int K, int64_t rows) { return K >= 1 && K <= 32 && rows >= 1 && rows <= MS_MAX_ROWS; }
+
+cudaError_t launch_mode_small(const double* S_all, int N, int n, int K, const double* M, double* A,
+                              const double* ref, double* dA, int64_t rows, double* Sn, double* nrm,
+                              double* fit, double* Gamma, double* Tp, double* Vscratch,
+                              cudaStream_t st, double tau) {
+  if (!mode_small_ok(K, rows)) return cudaErrorInvalidValue;
+  // [pinv overlay | M | A | ref | z/d | lane terms | row statistics] (mode_small_kernel)
+  const int KP = K <= 8 ? 8 : K <= 16 ? 16 : 32;
+  const size_t smem = sizeof(double) * ((((int64_t)K * (K + 1) + 1) & ~1) + 4 * MS_MAX_ROWS * KP + 132 * MS_MAX_ROWS);
+  const size_t smem_max = sizeof(double) * (32 * 33 + 4 * MS_MAX_ROWS * 32 + 132 * MS_MAX_ROWS);
+  static bool attr = false;
+  if (!attr) {
+    for (auto f : {mode_small_kernel<8>, mode_small_kernel<16>, mode_small_kernel<32>}) {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+      if (e != cudaSuccess) return e;
+    }
+    attr = true;
+  }
+  cudaError_t e;
+  if (K <= 8)
+    e = launch_pdl(mode_small_kernel<8>, dim3(1), dim3(MsCfg<8>::NW * 32), smem, st, S_all, N, n, K, M, A,
+                   ref, dA, (int)rows, Sn, nrm, fit, Gamma, Tp, Vscratch, tau);
+  else if (K <= 16)
+    e = launch_pdl(mode_small_kernel<16>, dim3(1), dim3(MsCfg<16>::NW * 32), smem, st, S_all, N, n, K, M,
+                   A, ref, dA, (int)rows, Sn, nrm, fit, Gamma, Tp, Vscratch, tau);
+  else
+    e = launch_pdl(mode_small_kernel<32>, dim3(1), dim3(MsCfg<32>::NW * 32), smem, st, S_all, N, n, K, M,
+                   A, ref, dA, (int)rows, Sn, nrm, fit, Gamma, Tp, Vscratch, tau);
   note_launch();
   return e;
 }

@@ -217,12 +217,16 @@ def test_singular_gamma_uses_pseudo_inverse():
         assert rel(got[n], st.A[n]) < 1e-8, n
 
 
+@pytest.mark.parametrize("unfused", [False, True])
 @pytest.mark.parametrize("K", [5, 16, 30, 40])
-def test_singular_gamma_each_factorization_kernel(K):
-    """The same L13 branch on every factorization kernel: the one-warp kernel at K <= 8, 16
-    and 32 (K = 5, 16, 30) and the CTA-wide Cholesky chain (K = 40); duplicate columns make Γ
-    singular, distinct ones keep it regular -- both sweeps against the oracle."""
-    dims = (48, 46, 44)
+def test_singular_gamma_each_factorization_kernel(K, unfused):
+    """The same L13 branch on every factorization kernel: the fused small-mode kernel and (with
+    FLAG_NO_FUSED_SOLVE) the one-warp kernel at K <= 8, 16 and 32 (K = 5, 16, 30), and the
+    CTA-wide Cholesky chain (K = 40); duplicate columns make Γ singular, distinct ones keep it
+    regular -- both sweeps against the oracle."""
+    if unfused and K > 32:
+        pytest.skip("K > 32 always takes the factorization chain")
+    dims = (30, 28, 26, 24)   # order 4: the fused small-mode kernel runs for K <= 32
     X, _ = random_problem(dims, K, 21)
     r = np.random.default_rng(22)
     for dup in (False, True):
@@ -232,13 +236,51 @@ def test_singular_gamma_each_factorization_kernel(K):
                 a[:, 1] = a[:, 0]
         st = O.State(X, [a.copy() for a in A])
         st.dt_sweep()
-        ctx = cp.cp_init(X, 3, dims, K)
+        ctx = cp.cp_init(X, 4, dims, K, flags=cp.FLAG_NO_FUSED_SOLVE if unfused else 0)
         cp.cp_set_factors(ctx, A)
         cp.cp_set_phase_override(ctx, "dt")
         cp.als_sweep(ctx, 0.0, 0.1)
         got = cp.cp_get_factors(ctx)
-        for n in range(3):
+        for n in range(4):
             assert rel(got[n], st.A[n]) < 1e-8, (dup, n)
+
+
+# fused small-mode solve (K <= 32, modes <= 64 rows): one launch per mode, the same IEEE
+# operations in the same order as the factorization + row-solve + Gram chain
+FUSED_CASES = [("C3mini", None), ("C4mini", None), ("C5mini", None), ("LAPmini", None),
+               (None, ((7, 9, 5, 4), 3)), (None, ((40, 36, 34, 2), 32)), (None, ((64, 6, 9, 5), 17)),
+               (None, ((60, 62, 64, 3), 32)), (None, ((12, 3, 10, 4, 2), 8)), (None, ((20, 21, 22, 23), 16))]
+
+
+@pytest.mark.parametrize("name,shape", FUSED_CASES)
+def test_fused_small_mode_is_bit_identical(name, shape):
+    """20 free-running sweeps (every phase: DT, PP build, PP) through the fused small-mode kernel
+    and through the three-kernel chain give bit-identical sweep records and factors; the same
+    run through als_run (the graph device loop) too."""
+    if name is not None:
+        cfg, X, A0 = problem(name)
+        N, dims, K, epp = cfg.N, cfg.dims, cfg.K, cfg.eps_pp
+    else:
+        dims, K = shape
+        X, _ = random_problem(dims, K, 31)
+        r = np.random.default_rng(32)
+        A0 = [r.random((d, K)) for d in dims]
+        N, epp = len(dims), 0.5
+    a = cp.cp_init(X, N, dims, K)
+    b = cp.cp_init(X, N, dims, K, flags=cp.FLAG_NO_FUSED_SOLVE)
+    c = cp.cp_init(X, N, dims, K)
+    cp.cp_set_factors(a, A0)
+    cp.cp_set_factors(b, A0)
+    cp.cp_set_factors(c, A0)
+    fa = [cp.als_sweep(a, 0.0, epp) for _ in range(20)]
+    fb = [cp.als_sweep(b, 0.0, epp) for _ in range(20)]
+    fc = cp.als_run(c, 0.0, epp, 20)
+    assert {x["phase"] for x in fa} >= {"dt"}
+    for x, y, z in zip(fa, fb, fc):
+        for key in ("phase", "fitness", "residual_sq", "grad_norm_sum", "max_rel_dA"):
+            assert x[key] == y[key] == z[key], (key, x, y, z)
+    for x, y, z in zip(cp.cp_get_factors(a), cp.cp_get_factors(b), cp.cp_get_factors(c)):
+        assert np.array_equal(x, y) and np.array_equal(x, z)
 
 
 @pytest.mark.parametrize("dims,K", [((160, 150, 140), 128), ((30, 28, 26, 24), 64)])
