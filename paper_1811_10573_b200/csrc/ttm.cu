@@ -95,28 +95,45 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Every TMA load carries an L2 cache policy: X streams through once (evict_first, so the GEMM's
+// output -- which the next tree level reads right away -- stays in L2 instead of X's dead lines),
+// the factor tiles are read by every CTA (evict_last).
+__device__ __forceinline__ uint64_t l2_policy_x() {
+  uint64_t pol;
+#ifdef CPPP_X_EVICT_NORMAL   // A/B builds
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#else
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_f() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
-                                       uint32_t bar) {
+                                       uint32_t bar, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
-                                       int c2, uint32_t bar) {
+                                       int c2, uint32_t bar, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
-                                       int c2, int c3, uint32_t bar) {
+                                       int c2, int c3, uint32_t bar, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void lds2(double& x, double& y, uint32_t addr) {
@@ -210,6 +227,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (warp == NWARP) {  // ---------------- TMA producer
     if (lane == 0) {
+      const uint64_t polX = l2_policy_x(), polF = l2_policy_f();
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmF)) : "memory");
       if (box8) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX4)) : "memory");
@@ -251,21 +269,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint32_t sx = smem_u32(base + st * C::STAGE);
             const uint32_t sf = sx + C::XBYTES;
             if (!MC) {
-              tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb);
+              tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb, polX);
             } else if (box8 && (Rflat ? r_first : m0) + BM <= Rm) {
               // R % 16 == 0 and the tile inside one batch: its eight 16-row boxes in one 4-D load
               tma_4d(sx, &tmX4, 0, kt * BK, static_cast<int>((Rflat ? r_first : m0) / 16),
-                     static_cast<int>(Rflat ? b_first : b), fb);
+                     static_cast<int>(Rflat ? b_first : b), fb, polX);
             } else if (Rflat == 0) {
 #pragma unroll
               for (int c = 0; c < BM / 16; ++c)
                 tma_3d(sx + c * 2048, &tmX, static_cast<int>(m0 + 16 * c), kt * BK,
-                       static_cast<int>(b), fb);
+                       static_cast<int>(b), fb, polX);
             } else {   // rows flattened over (b, r): each 16-row box has its own (b, r)
               int rc = static_cast<int>(r_first), bc = static_cast<int>(b_first);
 #pragma unroll
               for (int c = 0; c < BM / 16; ++c) {
-                tma_3d(sx + c * 2048, &tmX, rc, kt * BK, bc, fb);
+                tma_3d(sx + c * 2048, &tmX, rc, kt * BK, bc, fb, polX);
                 rc += 16;
                 if (rc >= Rflat) {   // R % 16 == 0: a box never straddles two batches
                   rc -= static_cast<int>(Rflat);
@@ -273,7 +291,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
               }
             }
-            tma_3d(sf, &tmF, 0, kt * BK, 0, fb);   // all BNP/16 column boxes in one load
+            tma_3d(sf, &tmF, 0, kt * BK, 0, fb, polF);   // all BNP/16 column boxes in one load
           }
         }
       } else {
@@ -298,21 +316,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint32_t sx = smem_u32(base + st * C::STAGE);
           const uint32_t sf = sx + C::XBYTES;
           if (!MC) {
-            tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb);
+            tma_2d(sx, &tmX, kt * BK, static_cast<int>(m0), fb, polX);
           } else if (box8 && (Rflat ? r_first : m0) + BM <= Rm) {
             // R % 16 == 0 and the tile inside one batch: its eight 16-row boxes in one 4-D load
             tma_4d(sx, &tmX4, 0, kt * BK, static_cast<int>((Rflat ? r_first : m0) / 16),
-                   static_cast<int>(Rflat ? b_first : b), fb);
+                   static_cast<int>(Rflat ? b_first : b), fb, polX);
           } else if (Rflat == 0) {
 #pragma unroll
             for (int c = 0; c < BM / 16; ++c)
               tma_3d(sx + c * 2048, &tmX, static_cast<int>(m0 + 16 * c), kt * BK,
-                     static_cast<int>(b), fb);
+                     static_cast<int>(b), fb, polX);
           } else {   // rows flattened over (b, r): each 16-row box has its own (b, r)
             int rc = static_cast<int>(r_first), bc = static_cast<int>(b_first);
 #pragma unroll
             for (int c = 0; c < BM / 16; ++c) {
-              tma_3d(sx + c * 2048, &tmX, rc, kt * BK, bc, fb);
+              tma_3d(sx + c * 2048, &tmX, rc, kt * BK, bc, fb, polX);
               rc += 16;
               if (rc >= Rflat) {   // R % 16 == 0: a box never straddles two batches
                 rc -= static_cast<int>(Rflat);
@@ -320,7 +338,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
           }
-          tma_3d(sf, &tmF, 0, kt * BK, 0, fb);   // all BNP/16 column boxes in one load
+          tma_3d(sf, &tmF, 0, kt * BK, 0, fb, polF);   // all BNP/16 column boxes in one load
         }
         };
         long long next = static_cast<long long>(atomicAdd(tile_counter, (unsigned long long)UB));
@@ -576,6 +594,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   };
   if (warp == NWARP) {   // ---------------- TMA producer
     if (lane == 0) {
+      const uint64_t polX = l2_policy_x(), polF = l2_policy_f();
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX4)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmF)) : "memory");
       int64_t it = 0;
@@ -609,8 +628,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint32_t fb = smem_u32(&full[st]);
             mbar_expect_tx(fb, C::STAGE);
             const uint32_t sx = smem_u32(base + st * C::STAGE);
-            tma_4d(sx, &tmX4, 0, kt * BK, static_cast<int>(m0 / 16), static_cast<int>(b), fb);
-            tma_3d(sx + C::XBYTES, &tmF, 0, kt * BK, 0, fb);
+            tma_4d(sx, &tmX4, 0, kt * BK, static_cast<int>(m0 / 16), static_cast<int>(b), fb, polX);
+            tma_3d(sx + C::XBYTES, &tmF, 0, kt * BK, 0, fb, polF);
           }
         }
       }
