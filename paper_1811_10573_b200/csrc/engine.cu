@@ -476,7 +476,7 @@ cppp_status run_ttv_jobs(cppp_ctx* c, const std::vector<TtvJob>& jobs) {
 // 2 s^N R flops as a single-mode TTM, but no s^(N-1) R intermediate and no multi-TTV pass over
 // it).  Returns false (nothing done) when the DMMA GEMM cannot take the shape.
 bool contract_multi(cppp_ctx* c, const Node& src, const std::vector<int>& modes, double* out,
-                    cppp_status* st) {
+                    cppp_status* st, double* const* F = nullptr) {
   *st = CPPP_OK;
   int64_t B = 1, S = 1, R = 1;
   for (int v = 0; v < c->N; ++v) {
@@ -491,7 +491,7 @@ bool contract_multi(cppp_ctx* c, const Node& src, const std::vector<int>& modes,
   a.nm = static_cast<int>(modes.size());
   a.K = K;
   for (int j = 0; j < a.nm; ++j) {
-    a.F[j] = fac_local(c, c->A, modes[j]);
+    a.F[j] = fac_local(c, F ? F : c->A, modes[j]);
     a.dims[j] = c->dl[modes[j]];
   }
   cudaError_t e = ttm_prepare_krp(a, c->Fpad, c->st);
@@ -814,6 +814,13 @@ struct PPTree {
       for (int w = maxmu + 1; w <= level + 2; ++w) {
         const uint32_t cmu = mu | (1u << w);
         const uint32_t kept = kept_of(cmu);
+        if (w == 2 && !child_leaf && ttv_batch_on(c)) {
+          cppp_status st = CPPP_OK;
+          if (level2_from_x(nd, cmu | (1u << 3), &st)) {
+            STCHK(st);
+            continue;
+          }
+        }
         const size_t mk = c->stack.mark();
         double* dst = child_leaf ? op_ptr(kept) : c->stack.push(node_elems(c, kept));
         if (!(have12 && child_leaf && kept == 0x6u))
@@ -841,18 +848,45 @@ struct PPTree {
     return CPPP_OK;
   }
 
+  // The last level-1 node of Def. pptree, {2}, has ONE child, {2, 3}.  When the two modes it
+  // contracts are neighbours in X's layout, that level-2 node comes straight from X in one
+  // multi-mode (Khatri-Rao) GEMM -- the same contraction of X with A_p^(tau 2) and A_p^(tau 3)
+  // (L24: any tree gives the same values) -- and the s^(N-1) K level-1 node is
+  // neither written nor read back (C4: a 768 MB node, its 307 us TTM and a 130 us multi-TTV pass,
+  // against one GEMM whose output is 38 MB).  Unsharded, order >= 4, not with CPPP_FLAG_NO_KRP.
+  bool level2_from_x(const Node& root, uint32_t mu2, cppp_status* st) {
+    const int N = c->N;
+    if (N < 4 || c->q >= 0 || (c->flags & CPPP_FLAG_NO_KRP)) return false;
+    static const bool off = getenv("CPPP_NO_L2_FROM_X") != nullptr;   // A/B
+    if (off) return false;
+    const int u = std::min(tau[2], tau[3]), v = std::max(tau[2], tau[3]);
+    if (v != u + 1) return false;
+    const uint32_t kept = kept_of(mu2);
+    const bool leaf = (N == 4);
+    const size_t mk = c->stack.mark();
+    double* dst = leaf ? op_ptr(kept) : c->stack.push(node_elems(c, kept));
+    if (!contract_multi(c, root, std::vector<int>{u, v}, dst, st, c->Ap)) {
+      c->stack.release(mk);
+      return false;
+    }
+    if (*st == CPPP_OK && !leaf) *st = subtree_batched(Node{kept, dst, false}, mu2, 2);
+    c->stack.release(mk);
+    return true;
+  }
+
   // Below a level-1 node, level by level (SURVEY a2 "batched multi-TTV"): every contraction of a
   // level in one batched launch (two when a parent feeds a one-pass pair), instead of one launch
   // per child depth first.  Same nodes and values as Def. pptree's traversal (L24); the nodes of
-  // the subtree stay on the stack until its leaves are written.
-  cppp_status subtree_batched(const Node& l1, uint32_t mu1) {
+  // the subtree stay on the stack until its leaves are written.  (level0: the level of the node
+  // the subtree hangs from -- 1, or 2 for a level-2 node contracted straight from X.)
+  cppp_status subtree_batched(const Node& l1, uint32_t mu1, int level0 = 1) {
     const int N = c->N;
     struct Item {
       Node nd;
       uint32_t mu;
     };
     std::vector<Item> cur{{l1, mu1}};
-    for (int level = 1; level < N - 2; ++level) {
+    for (int level = level0; level < N - 2; ++level) {
       const bool child_leaf = (level + 1 == N - 2);
       std::vector<Item> next;
       std::vector<TtvJob> jobs;
@@ -1044,6 +1078,86 @@ cppp_status run_fused_build(cppp_ctx* c) {
   return CPPP_OK;
 }
 
+// Order >= 6, unsharded: a construction tree whose level-2 nodes are the neighbour pairs of modes
+// (0,1), (2,3), (4,5), ... each contracted straight from X in ONE Khatri-Rao GEMM (P:78-80 over two
+// modes at once), with no s^(N-1) K level-1 node.  Every leaf M_p^(a,b) keeps two modes, so it
+// contracts N-2 >= 4 of them, and those always include one whole pair of the matching ({a, b}
+// meets at most two of the >= 3 pairs): the leaf hangs below the first pair disjoint from {a, b},
+// from which its remaining N-4 modes are contracted in ascending order by batched multi-TTVs
+// over the s^(N-2) K pair node (intermediate nodes shared between leaves, one launch per level).
+// Def. pptree and this tree compute the same operators (L24: any tree gives the same values).
+// C4: three GEMMs with 38 MB outputs instead of Def. pptree's three 768 MB level-1 nodes and
+// their level-2 passes.  CPPP_NO_PAIR_BUILD (A/B) and the flags below select Def. pptree.
+bool pair_build_ok(const cppp_ctx* c) {
+  static const bool off = getenv("CPPP_NO_PAIR_BUILD") != nullptr;
+  if (off || c->N < 6 || c->q >= 0 ||
+      (c->flags & (CPPP_FLAG_NO_KRP | CPPP_FLAG_NO_FUSED_TTV | CPPP_FLAG_SIMT_TTM)))
+    return false;
+  for (int u = 0; u + 1 < c->N; u += 2) {
+    int64_t B = 1, R = 1;
+    for (int v = 0; v < c->N; ++v) {
+      if (v < u) B *= c->dl[v];
+      if (v > u + 1) R *= c->dl[v];
+    }
+    if (!ttm_uses_dmma(B, c->dl[u] * c->dl[u + 1], R, c->K, false)) return false;
+  }
+  return true;
+}
+
+cppp_status run_pair_build(cppp_ctx* c) {
+  const int N = c->N;
+  const uint32_t full = (1u << N) - 1;
+  auto owner = [&](int a, int b) {   // the first pair (2p, 2p+1) disjoint from {a, b}
+    for (int u = 0; u + 1 < N; u += 2)
+      if (a != u && a != u + 1 && b != u && b != u + 1) return u;
+    return -1;
+  };
+  for (int u = 0; u + 1 < N; u += 2) {
+    std::vector<std::pair<int, int>> leaves;
+    for (int a = 0; a < N; ++a)
+      for (int b = a + 1; b < N; ++b)
+        if (owner(a, b) == u) leaves.emplace_back(a, b);
+    if (leaves.empty()) continue;
+    const uint32_t kept2 = full & ~(3u << u);
+    const size_t mk = c->stack.mark();
+    double* P2 = c->stack.push(node_elems(c, kept2));
+    cppp_status st = CPPP_OK;
+    if (!contract_multi(c, Node{full, c->X, true}, std::vector<int>{u, u + 1}, P2, &st, c->Ap))
+      return fail(c, CPPP_EINVAL, "pair build: GEMM shape");   // pair_build_ok checked the shapes
+    STCHK(st);
+    std::vector<std::pair<uint32_t, double*>> nodes{{kept2, P2}};
+    auto find = [&](uint32_t m) -> double* {
+      for (auto& x : nodes)
+        if (x.first == m) return x.second;
+      return nullptr;
+    };
+    for (int step = 0; step < N - 4; ++step) {
+      std::vector<TtvJob> jobs;
+      std::vector<std::pair<uint32_t, double*>> made;
+      for (const auto& lf : leaves) {
+        std::vector<int> seq;   // the modes this leaf contracts below the pair node, ascending
+        for (int v = 0; v < N; ++v)
+          if ((kept2 & (1u << v)) && v != lf.first && v != lf.second) seq.push_back(v);
+        uint32_t parent = kept2;
+        for (int t = 0; t < step; ++t) parent &= ~(1u << seq[t]);
+        const uint32_t child = parent & ~(1u << seq[step]);
+        bool dup = false;
+        for (auto& x : made) dup |= (x.first == child);
+        if (dup) continue;
+        double* dst = (step == N - 5) ? c->ops[lf.first][lf.second] : c->stack.push(node_elems(c, child));
+        TtvJob j = single_job(c, Node{parent, find(parent), false}, seq[step], fac_local(c, c->Ap, seq[step]), dst);
+        j.stream = (double)node_elems(c, parent) * 8.0 > 64.0 * (1 << 20);
+        jobs.push_back(j);
+        made.emplace_back(child, dst);
+      }
+      STCHK(run_ttv_jobs(c, jobs));
+      for (auto& x : made) nodes.push_back(x);
+    }
+    c->stack.release(mk);
+  }
+  return CPPP_OK;
+}
+
 cppp_status run_pp_build(cppp_ctx* c, bool have12 = false) {
   const int N = c->N, K = c->K;
   if (!c->dry) {
@@ -1055,6 +1169,8 @@ cppp_status run_pp_build(cppp_ctx* c, bool have12 = false) {
   }
   if (fused_build_ok(c)) {
     STCHK(run_fused_build(c));
+  } else if (pair_build_ok(c)) {
+    STCHK(run_pair_build(c));
   } else {
     PPTree t{c};
     t.have12 = have12 && reuse12(c);
@@ -1501,6 +1617,9 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
     for (int v = 0; v <= mid; ++v) sl *= c->dl[v];
     for (int v = mid + 1; v < c->N; ++v) sr *= c->dl[v];
     maxS = std::max(maxS, std::max(sl, sr));
+    // the PP build's level-2 node straight from X (PPTree::level2_from_x): two neighbour modes
+    if (c->N >= 4)
+      for (int v = 0; v + 1 < c->N; ++v) maxS = std::max(maxS, c->dl[v] * c->dl[v + 1]);
   }
   size_t oFpad = take(sizeof(double) * ttm_scratch_doubles(maxS));   // TTM factor + scheduler
   size_t oOps[CPPP_MAX_ORDER][CPPP_MAX_ORDER];

@@ -96,6 +96,26 @@ def test_pp_operators_ragged(dims, K):
         assert rel(cp.pp_get_operator(ctx, i, j), ref) < TOL, (dims, K, i, j)
 
 
+@pytest.mark.parametrize("flags", [0, cp.FLAG_NO_KRP])
+@pytest.mark.parametrize("dims,K", [((6, 7, 8, 9), 12), ((5, 6, 4, 7, 3), 9), ((4, 5, 3, 4, 3, 4), 10),
+                                    ((12, 10, 11, 9, 8), 33), ((4, 6, 4, 2, 6, 4), 10),
+                                    ((6, 4, 2, 4, 6, 2, 4), 7), ((4, 4, 6, 4, 4, 6), 40)])
+def test_pp_level2_from_x(dims, K, flags):
+    """Order >= 4: the last level-1 node's only child {2, 3} comes straight from X in one
+    Khatri-Rao GEMM when its two modes are neighbours; order >= 6 (even extents): the whole tree
+    hangs from the neighbour pairs (0,1), (2,3), ... contracted from X (default) -- or Def. pptree
+    with its level-1 nodes (FLAG_NO_KRP); both against the oracle's operators and single-mode
+    MTTKRPs."""
+    X, A = random_problem(dims, K, 41)
+    ctx = cp.cp_init(X, len(dims), dims, K, flags=flags)
+    cp.cp_set_factors(ctx, A)
+    cp.pp_build_operators(ctx)
+    for (i, j), ref in O.pp_operators(X, A).items():
+        assert rel(cp.pp_get_operator(ctx, i, j), ref) < TOL, (dims, K, i, j)
+    for n in range(len(dims)):
+        assert rel(cp.pp_get_single(ctx, n), O.mttkrp(X, A, n)) < TOL, (dims, n)
+
+
 @pytest.mark.parametrize("name", SMALL)
 def test_pp_update_matches_oracle(name):
     cfg, X, Ap = problem(name)
