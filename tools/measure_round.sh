@@ -10,6 +10,8 @@ for c in C2 C1 C3 C4 LAP P6W; do
   python bench.py --config $c --steps 5 --warmup 3 > "$O/bench_$c.json" 2> "$O/bench_$c.err"
 done
 python bench.py --config C5 --steps 2 --warmup 3 > "$O/bench_C5.json" 2> "$O/bench_C5.err"
+# the paper's strong-scaling tensor (125 GB): device-resident only (its upload alone is ~2.3 s)
+python bench.py --config P6S --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > "$O/bench_P6S.json" 2> "$O/bench_P6S.err"
 python bench.py --impl reference --steps 2 --warmup 1 > "$O/bench_ref_C2.json" 2> "$O/bench_ref_C2.err"
 for c in C2 C4; do
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$O/launches_$c.csv" \
