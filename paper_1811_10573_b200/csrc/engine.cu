@@ -508,15 +508,17 @@ bool contract_multi(cppp_ctx* c, const Node& src, const std::vector<int>& modes,
 // ---------------------------------------------------------------- small solve of one mode
 // A_new = M Γ^†, G, dA = A_new - ref, S^(n), norms (Alg. 1 P:393-399 / Alg. 3).
 // Issue Γ^(n) and its inverse on the side stream once every S^(m), m != n, is final (ev_S).
-// K <= 32 with every (local) mode <= 64 rows, order >= 4: each mode's solve is ONE launch on the
-// main stream (launch_mode_small: Γ, factorization, rows, Gram, statistics; bit-identical to the
-// chain of gamma factorization on the side stream + row solves + Gram), so nothing is prefetched.
-// Measured (20-sweep runs, A/B with CPPP_NO_FUSED_SOLVE): C4 1784 -> 1850 sweeps/s, the LAP / P6W
-// PP-approximated sweeps 208 -> 182 us; order 3 keeps the chain (C1 15.4 k -> 14.3 k sweeps/s
-// fused: there the side-stream factorization hides under each mode's TTV or GEMM).
+// K <= 32 with every (local) mode <= 64 rows: each mode's solve is ONE launch on the main stream
+// (launch_mode_small: Γ, factorization, rows, Gram, statistics; bit-identical to the chain of
+// gamma factorization on the side stream + row solves + Gram), so nothing is prefetched.  The
+// kernels that produce M^(n) trigger it early (pdl_trigger), so its Γ / factorization part runs
+// beside them, as the side-stream factorization did.  Measured (20-sweep runs, A/B with
+// CPPP_NO_FUSED_SOLVE and a build without the early trigger): C4 1784 -> 1848 sweeps/s fused,
+// 2107 -> 2189 with the trigger (after the pair tree); C1 14.9 k (chain) -> 13.7 k fused without
+// the trigger, 15.4 k with it; the LAP / P6W PP-approximated sweeps 208 -> 182 us.
 bool small_modes(const cppp_ctx* c) {
   static const bool off = getenv("CPPP_NO_FUSED_SOLVE") != nullptr;   // A/B
-  if (off || (c->flags & CPPP_FLAG_NO_FUSED_SOLVE) || c->N < 4) return false;
+  if (off || (c->flags & CPPP_FLAG_NO_FUSED_SOLVE)) return false;
   for (int n = 0; n < c->N; ++n)
     if (!mode_small_ok(c->K, c->dl[n])) return false;
   return true;

@@ -14,6 +14,14 @@
 // of them calls pdl_wait() before touching anything an earlier kernel wrote.
 #ifdef __CUDACC__
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the next kernel on the stream launch before this one ends (its CTAs run up to their own
+// pdl_wait).  Called after pdl_wait by the kernels that feed the fused small-mode solve, whose
+// pre-wait part (Γ and its factorization) reads only data of kernels two or more launches back.
+#ifndef CPPP_NO_TRIGGER   // A/B builds
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#else
+__device__ __forceinline__ void pdl_trigger() {}
+#endif
 #endif
 namespace cppp {
 bool pdl_enabled();   // false when CPPP_NO_PDL is set (A/B measurements) or suppressed

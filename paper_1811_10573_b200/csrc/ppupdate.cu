@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(256, (YG * U > 8) ? 2 : 3)
 
 __global__ void pp_update_combine(PPUpdateArgs a, int xsplit) {
   pdl_wait();
+  pdl_trigger();
   const int64_t total = a.ny * a.K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {

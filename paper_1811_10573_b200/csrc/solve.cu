@@ -1035,7 +1035,10 @@ __global__ void __launch_bounds__(MsCfg<KP>::NW * 32, 1)
   __shared__ double red[7 * 32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int ldt = (K + 7) & ~7;
-  pdl_wait();
+  // Everything up to the factor's inverse reads only data of kernels two or more launches back
+  // (the Grams, A^(n), the reference factor), so it runs BEFORE the programmatic wait: the
+  // kernels that produce M^(n) trigger their dependents early (pdl_trigger) and this part
+  // overlaps them.  Those reads go through L2 (ld.global.cg), M after the wait.
 
   // every load in flight at once: the N-1 Gram rows of Γ and the staged rows
   double sv[RW][CPPP_MAX_ORDER_ - 1];
@@ -1045,19 +1048,18 @@ __global__ void __launch_bounds__(MsCfg<KP>::NW * 32, 1)
 #pragma unroll
     for (int q = 0; q < CPPP_MAX_ORDER_ - 1; ++q) {
       const int m = q < n ? q : q + 1;   // ascending m != n
-      sv[t][q] = (q < N - 1 && i < K && lane < K) ? __ldg(S_all + (int64_t)m * K * K + i * K + lane) : 1.0;
+      sv[t][q] = (q < N - 1 && i < K && lane < K) ? __ldcg(S_all + (int64_t)m * K * K + i * K + lane) : 1.0;
     }
   }
   constexpr int LQ = RB / NT;
-  double lm[LQ], la[LQ], lr[LQ];
+  double la[LQ], lr[LQ];
 #pragma unroll
   for (int q = 0; q < LQ; ++q) {
     const int f = tid + q * NT, y = f / KP, c = f % KP;
     const bool in = y < rows && c < K;
     const int e = y * K + c;
-    lm[q] = in ? __ldg(M + e) : 0.0;
-    la[q] = in ? A[e] : 0.0;
-    lr[q] = (in && !ref_is_A) ? ref[e] : 0.0;
+    la[q] = in ? __ldcg(A + e) : 0.0;
+    lr[q] = (in && !ref_is_A) ? __ldcg(ref + e) : 0.0;
   }
   // Γ^(n) = 1.0 · S^(m_0) · S^(m_1) · … (ascending m, as gamma_small_kernel); warp w keeps rows
   // w RW + t, lane k column k
@@ -1081,7 +1083,6 @@ __global__ void __launch_bounds__(MsCfg<KP>::NW * 32, 1)
 #pragma unroll
   for (int q = 0; q < LQ; ++q) {
     const int f = tid + q * NT;
-    Ms[f] = lm[q];
     Ao[f] = la[q];
     if (!ref_is_A) Rf[f] = lr[q];
   }
@@ -1159,6 +1160,12 @@ __global__ void __launch_bounds__(MsCfg<KP>::NW * 32, 1)
     gamma_pinv_dev(K, Gamma_g, P_g, ldt, Vscratch, tau);
     __syncthreads();
     for (int r = w; r < 32; r += NW) Qs[r][lane] = (r < K && lane < K) ? P_g[r * ldt + lane] : 0.0;
+  }
+  pdl_wait();   // M^(n) comes from the kernel right before this one
+#pragma unroll
+  for (int q = 0; q < LQ; ++q) {
+    const int f = tid + q * NT, y = f / KP, c = f % KP;
+    Ms[f] = (y < rows && c < K) ? __ldcg(M + y * K + c) : 0.0;
   }
   __syncthreads();
   PROBE_T(12);

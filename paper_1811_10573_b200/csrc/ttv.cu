@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(TTV_THREADS)
                const double* __restrict__ F, double* __restrict__ out) {
   using T = typename Vec<V>::T;
   pdl_wait();
+  pdl_trigger();
   __shared__ T red[TTV_THREADS];
   const int64_t e = blockIdx.x * (int64_t)TTV_THREADS + threadIdx.x;   // vector index
   const int p = blockIdx.y, xs = gridDim.y;
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(TTV_THREADS)
     ttv_batch_kernel(const __grid_constant__ TtvBatch bt) {
   using T = typename Vec<V>::T;
   pdl_wait();
+  pdl_trigger();
   __shared__ T red[TTV_THREADS];
   int ji = 0;
   while (ji + 1 < bt.njobs && (int)blockIdx.x >= bt.j[ji + 1].cta0) ++ji;
@@ -227,6 +229,7 @@ template <int MAXSB>
 __global__ void __launch_bounds__(TTV_THREADS, 2)
     ttv_pair_kernel(const __grid_constant__ TtvBatch bt) {
   pdl_wait();
+  pdl_trigger();
   int ji = 0;
   while (ji + 1 < bt.njobs && (int)blockIdx.x >= bt.j[ji + 1].cta0) ++ji;
   const double* __restrict__ P = bt.j[ji].P;

@@ -246,7 +246,7 @@ def test_singular_gamma_each_factorization_kernel(K, unfused):
     regular -- both sweeps against the oracle."""
     if unfused and K > 32:
         pytest.skip("K > 32 always takes the factorization chain")
-    dims = (30, 28, 26, 24)   # order 4: the fused small-mode kernel runs for K <= 32
+    dims = (30, 28, 26, 24)   # the fused small-mode kernel runs for K <= 32
     X, _ = random_problem(dims, K, 21)
     r = np.random.default_rng(22)
     for dup in (False, True):
@@ -267,7 +267,8 @@ def test_singular_gamma_each_factorization_kernel(K, unfused):
 
 # fused small-mode solve (K <= 32, modes <= 64 rows): one launch per mode, the same IEEE
 # operations in the same order as the factorization + row-solve + Gram chain
-FUSED_CASES = [("C3mini", None), ("C4mini", None), ("C5mini", None), ("LAPmini", None),
+FUSED_CASES = [("C1", None), ("C3mini", None), ("C4mini", None), ("C5mini", None), ("LAPmini", None),
+               (None, ((7, 9, 5), 3)), (None, ((40, 36, 34), 32)),
                (None, ((7, 9, 5, 4), 3)), (None, ((40, 36, 34, 2), 32)), (None, ((64, 6, 9, 5), 17)),
                (None, ((60, 62, 64, 3), 32)), (None, ((12, 3, 10, 4, 2), 8)), (None, ((20, 21, 22, 23), 16))]
 
