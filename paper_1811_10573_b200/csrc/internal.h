@@ -86,6 +86,19 @@ struct KrpArgs {
   int64_t rows;    // set by ttm_prepare_krp
 };
 cudaError_t ttm_prepare_krp(const KrpArgs& a, double* Fpad, cudaStream_t st);
+// Tucker's multi-mode contraction: the Kronecker product F_0 ⊗ ... ⊗ F_{h-1} (F_j: dims[j] x
+// ranks[j]; rows (x_0..x_{h-1}) and columns (z_0..z_{h-1}) row-major, Π ranks <= 128) into the
+// padded-factor area of Fpad, for launch_ttm_padded with K = Π ranks.
+struct KronArgs {
+  const double* F[CPPP_MAX_ORDER_];
+  int64_t dims[CPPP_MAX_ORDER_];
+  int ranks[CPPP_MAX_ORDER_];
+  int nm;
+  int cols;        // set by ttm_prepare_kron
+  int ld;          // set by ttm_prepare_kron
+  int64_t rows;    // set by ttm_prepare_kron
+};
+cudaError_t ttm_prepare_kron(const KronArgs& a, double* Fpad, cudaStream_t st);
 cudaError_t launch_ttm_padded(const double* X, int64_t B, int64_t S, int64_t R, int K, double* out,
                               const double* Fpad, cudaStream_t st);
 // Scheduling of one GEMM beside other streams' work: reserve_sms SMs get no (persistent) CTA;

@@ -1341,6 +1341,52 @@ cudaError_t ttm_prepare_krp(const KrpArgs& args, double* Fpad, cudaStream_t st) 
   return e;
 }
 
+// Kronecker product of factor matrices (Tucker's multi-mode contraction):
+// out[(x_0 .. x_{h-1})][(z_0 .. z_{h-1})] = Π_j F_j[x_j][z_j], both multi-indices row-major
+__global__ void kron_kernel(KronArgs a, double* __restrict__ out) {
+  pdl_wait();
+  const int64_t total = a.rows * a.ld;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / a.ld;
+    int col = static_cast<int>(e - row * a.ld);
+    if (col >= a.cols) {
+      out[e] = 0.0;
+      continue;
+    }
+    int64_t x[CPPP_MAX_ORDER_];
+    int z[CPPP_MAX_ORDER_];
+    int64_t r = row;
+    for (int j = a.nm - 1; j >= 0; --j) {
+      x[j] = r % a.dims[j];
+      r /= a.dims[j];
+      z[j] = col % a.ranks[j];
+      col /= a.ranks[j];
+    }
+    double v = 1.0;
+    for (int j = 0; j < a.nm; ++j) v *= __ldg(a.F[j] + x[j] * a.ranks[j] + z[j]);
+    out[e] = v;
+  }
+}
+
+cudaError_t ttm_prepare_kron(const KronArgs& args, double* Fpad, cudaStream_t st) {
+  KronArgs a = args;
+  a.rows = 1;
+  a.cols = 1;
+  for (int j = 0; j < a.nm; ++j) {
+    a.rows *= a.dims[j];
+    a.cols *= a.ranks[j];
+  }
+  a.ld = ttm_ld(a.cols);
+  const int64_t total = a.rows * a.ld;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  cudaError_t e = launch_pdl(kron_kernel, dim3((unsigned)blocks), dim3(256), 0, st, a,
+                             Fpad + TTM_CTL + TTM_PART);
+  note_launch();
+  return e;
+}
+
 size_t ttm_scratch_doubles(int64_t S) { return TTM_CTL + TTM_PART + static_cast<size_t>(S) * 128; }
 
 cudaError_t launch_ttm_padded(const double* X, int64_t B, int64_t S, int64_t R, int K, double* out,

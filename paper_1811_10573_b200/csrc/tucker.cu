@@ -884,6 +884,66 @@ cppp_status contract(tk_ctx* c, const double* in, const Lay& l, int u, const dou
   return CPPP_OK;
 }
 
+// Several consecutive modes [a, b] of X (the root layout) in ONE GEMM against the Kronecker
+// product of their factors (Y = X ×_a A^(a)T ... ×_b A^(b)T is one contraction of X's
+// natural unfolding with A^(a) ⊗ ... ⊗ A^(b)): the s^(N-1) R-sized intermediates of the
+// one-mode-at-a-time chain are never written.  The new rank axes z_a .. z_b are appended in
+// order, as the chain would append them.  Returns false (nothing done) when Π R > 128 or the
+// DMMA GEMM cannot take the shape.
+bool kron_ok(const tk_ctx* c, int a, int b) {
+  static const bool off = getenv("CPPP_TK_NO_KRON") != nullptr;   // A/B: one mode at a time
+  if (off || (c->flags & (CPPP_FLAG_SIMT_TTM | CPPP_FLAG_NO_KRP)) || b <= a) return false;
+  int64_t B = 1, S = 1, R = 1, KC = 1;
+  for (int v = 0; v < c->N; ++v) {
+    if (v < a) B *= c->s[v];
+    else if (v > b) R *= c->s[v];
+    else {
+      S *= c->s[v];
+      KC *= c->R[v];
+    }
+  }
+  // the GEMM does 2 s^N Π R flops against the chain's 2 s^N R for its first (largest) step: only
+  // while Π R <= 16 does it stay HBM-bound (2 Π R flop per 8-byte element, below the 5.7 flop/B
+  // ridge) and so cost one pass over X.  Measured: T6W's halves (Π R = 64) 6.6 -> 9.5 ms a regular
+  // sweep, T4 / T3 (Π R = 100) 4.2 -> 4.5 / 2.7 -> 3.4 ms; the PP build's pairs (Π R = 16 on T6W):
+  // 11.3 -> 6.9 ms.
+  return KC <= 16 && cppp::ttm_uses_dmma(B, S, R, static_cast<int>(KC), false);
+}
+
+cppp_status contract_kron(tk_ctx* c, int a, int b, double* const* F, double* out, Lay* lo) {
+  int64_t B = 1, S = 1, R = 1;
+  cppp::KronArgs k{};
+  k.nm = b - a + 1;
+  int KC = 1;
+  for (int v = 0; v < c->N; ++v) {
+    if (v < a) B *= c->s[v];
+    else if (v > b) R *= c->s[v];
+    else {
+      S *= c->s[v];
+      k.F[v - a] = F[v];
+      k.dims[v - a] = c->s[v];
+      k.ranks[v - a] = c->R[v];
+      KC *= c->R[v];
+    }
+  }
+  TKCU(c, cppp::ttm_prepare_kron(k, c->Fpad, c->st));
+  TKCU(c, cppp::launch_ttm_padded(c->X, B, S, R, KC, out, c->Fpad, c->st));
+  Lay o;
+  for (int v = 0; v < c->N; ++v) {
+    if (v >= a && v <= b) continue;
+    o.mode[o.n] = v;
+    o.z[o.n] = false;
+    ++o.n;
+  }
+  for (int v = a; v <= b; ++v) {
+    o.mode[o.n] = v;
+    o.z[o.n] = true;
+    ++o.n;
+  }
+  *lo = o;
+  return CPPP_OK;
+}
+
 // canonical out [+]= in (layout l, one axis per mode)
 cppp_status to_canonical(tk_ctx* c, const double* in, const Lay& l, double* out, bool accumulate) {
   cppp::PermArgs p{};
@@ -943,7 +1003,17 @@ struct TDT {
   cppp_status half(const double* d, const Lay& l, int a, int b, int lo, int hi) {
     const double* cur = d;
     Lay cl = l;
-    std::vector<double*> tmp;
+    if (d == c->X && kron_ok(c, a, b)) {   // the whole half from X in one GEMM
+      int64_t e = 1;
+      for (int v = 0; v < c->N; ++v) e *= (v >= a && v <= b) ? c->R[v] : c->s[v];
+      double* o = nullptr;
+      TKST(talloc(c, &o, e));
+      Lay nl;
+      TKST(contract_kron(c, a, b, c->A, o, &nl));
+      cppp_status s = range(o, nl, lo, hi);
+      TKST(tfree(c, o));
+      return s;
+    }
     for (int u = a; u <= b; ++u) {
       Lay nl;
       Lay probe = cl;
@@ -1003,6 +1073,79 @@ struct TTree {
     return CPPP_OK;
   }
 };
+
+// Order >= 6: the construction tree hangs from the neighbour pairs (0,1), (2,3), ... contracted
+// straight from X (one Kronecker GEMM each); every leaf Y_p^(a,b) sits below the first pair
+// disjoint from {a, b} (its N-2 >= 4 contracted modes always hold one whole pair), and its other
+// modes are contracted from the pair node in ascending order, intermediates shared (the CP
+// path's run_pair_build; L24: any tree gives the same operators).
+bool tk_pair_ok(const tk_ctx* c) {
+  static const bool off = getenv("CPPP_NO_PAIR_BUILD") != nullptr;
+  if (off || c->N < 6) return false;
+  for (int u = 0; u + 1 < c->N; u += 2)
+    if (!kron_ok(c, u, u + 1)) return false;
+  return true;
+}
+
+cppp_status tk_pair_build(tk_ctx* c) {
+  const int N = c->N;
+  auto owner = [&](int a, int b) {
+    for (int u = 0; u + 1 < N; u += 2)
+      if (a != u && a != u + 1 && b != u && b != u + 1) return u;
+    return -1;
+  };
+  for (int u = 0; u + 1 < N; u += 2) {
+    std::vector<std::pair<int, int>> leaves;
+    for (int a = 0; a < N; ++a)
+      for (int b = a + 1; b < N; ++b)
+        if (owner(a, b) == u) leaves.emplace_back(a, b);
+    if (leaves.empty()) continue;
+    int64_t e = 1;
+    for (int v = 0; v < N; ++v) e *= (v == u || v == u + 1) ? c->R[v] : c->s[v];
+    double* P2 = nullptr;
+    TKST(talloc(c, &P2, e));
+    Lay l2;
+    TKST(contract_kron(c, u, u + 1, c->Ap, P2, &l2));
+    struct Nd {
+      uint32_t done;   // modes contracted below the pair node
+      double* d;
+      Lay l;
+    };
+    std::vector<Nd> nodes;
+    nodes.reserve(64);   // (pointers into it are held across push_back)
+    nodes.push_back(Nd{0u, P2, l2});
+    cppp_status st = CPPP_OK;
+    for (const auto& lf : leaves) {
+      const Nd* cur = &nodes[0];
+      uint32_t done = 0;
+      for (int v = 0; v < N && st == CPPP_OK; ++v) {
+        if (v == u || v == u + 1 || v == lf.first || v == lf.second) continue;
+        done |= 1u << v;
+        const Nd* hit = nullptr;
+        for (const Nd& x : nodes)
+          if (x.done == done) hit = &x;
+        if (hit == nullptr) {
+          double* o = nullptr;
+          st = talloc(c, &o, lay_elems(c, cur->l) / c->s[v] * c->R[v]);
+          if (st != CPPP_OK) break;
+          Lay nl;
+          st = contract(c, cur->d, cur->l, v, c->Ap[v], o, &nl);
+          nodes.push_back(Nd{done, o, nl});
+          hit = &nodes.back();
+        }
+        cur = hit;
+      }
+      if (st == CPPP_OK) st = to_canonical(c, cur->d, cur->l, c->ops[lf.first][lf.second], false);
+      if (st != CPPP_OK) break;
+    }
+    for (const Nd& x : nodes) {
+      cppp_status f = tfree(c, x.d);
+      if (st == CPPP_OK) st = f;
+    }
+    TKST(st);
+  }
+  return CPPP_OK;
+}
 
 Lay canon_lay(const tk_ctx* c, uint32_t kept) {
   Lay l;
@@ -1262,7 +1405,18 @@ cppp_status tk_init(tk_ctx** out, const double* X, int N, const int64_t* s, cons
       return bail(CPPP_ECUDA);
     c->normX_sq = c->hstats[0];
   }
-  const size_t nscr = cppp::ttm_scratch_doubles(smax);
+  // the padded factor of the widest GEMM: one mode, a half of the regular tree, or a neighbour
+  // pair of the PP build, contracted through their Kronecker product
+  int64_t kmax = smax;
+  {
+    const int mid = (N - 1 + 2) / 2 - 1;   // TDT::range's split of [0, N-1]
+    int64_t sl = 1, sr = 1;
+    for (int v = 0; v <= mid; ++v) sl *= c->s[v];
+    for (int v = mid + 1; v < N; ++v) sr *= c->s[v];
+    kmax = std::max(kmax, std::max(sl, sr));
+    for (int v = 0; v + 1 < N; ++v) kmax = std::max(kmax, c->s[v] * c->s[v + 1]);
+  }
+  const size_t nscr = cppp::ttm_scratch_doubles(kmax);
   if (dalloc(c, &c->Fpad, (int64_t)nscr) != CPPP_OK) return bail(CPPP_ENOMEM);
   if (cudaMemsetAsync(c->Fpad, 0, sizeof(double) * nscr, c->st) != cudaSuccess ||
       cudaStreamSynchronize(c->st) != cudaSuccess)
@@ -1357,10 +1511,14 @@ cppp_status pp_build_ops(tk_ctx* c) {
                             cudaMemcpyDeviceToDevice, c->st));
     TKCU(c, cudaMemsetAsync(c->dA[n], 0, sizeof(double) * c->s[n] * c->R[n], c->st));
   }
-  TTree t{c, {}};
-  for (int n = 0; n < N; ++n) t.tau[n] = n;
-  std::stable_sort(t.tau, t.tau + N, [&](int a, int b) { return c->s[a] > c->s[b]; });
-  TKST(t.visit(c->X, root_lay(c), 0u, 0));
+  if (tk_pair_ok(c)) {
+    TKST(tk_pair_build(c));
+  } else {
+    TTree t{c, {}};
+    for (int n = 0; n < N; ++n) t.tau[n] = n;
+    std::stable_sort(t.tau, t.tau + N, [&](int a, int b) { return c->s[a] > c->s[b]; });
+    TKST(t.visit(c->X, root_lay(c), 0u, 0));
+  }
   // Y_p^(n) = Y_p^(j,n) ×_j A_p^(j)T, j = min{j != n}
   for (int n = 0; n < N; ++n) {
     const int j = n == 0 ? 1 : 0;

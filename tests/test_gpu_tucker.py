@@ -47,6 +47,27 @@ def test_ttmc_matches_oracle(dims, ranks, simt):
     cp.tk_destroy(ctx)
 
 
+@pytest.mark.parametrize("flags", [0, cp.FLAG_NO_KRP])
+@pytest.mark.parametrize("dims,ranks", [((20, 18, 16, 14), (4, 4, 3, 3)), ((40, 36, 34), (4, 2, 6)),
+                                        ((12, 12, 12, 12, 12, 12), (3, 3, 3, 3, 3, 3)),
+                                        ((8, 6, 10, 6, 8, 4, 6), (2, 3, 2, 2, 3, 2, 2))])
+def test_kronecker_first_level_and_pair_tree(dims, ranks, flags):
+    """Halves of the regular tree with Π R <= 16 contracted from X in one Kronecker GEMM each, and
+    (order >= 6) the PP operators built below the neighbour pairs (0,1), (2,3), ... (default) --
+    or one mode at a time through Def. pptree (FLAG_NO_KRP): TTMc and operators against the
+    oracle."""
+    X, A = problem(dims, ranks, 7)
+    ctx = cp.tk_init(X, dims, ranks, flags=flags)
+    cp.tk_set_factors(ctx, A)
+    Y = cp.tk_ttmc(ctx)
+    for n in range(len(dims)):
+        assert rel(Y[n], T.ttmc(X, A, n)) < TOL, n
+    cp.tk_pp_build(ctx)
+    for (i, j), ref in T.pp_operators(X, A).items():
+        assert rel(cp.tk_pp_get_operator(ctx, i, j), ref) < TOL, (i, j)
+    cp.tk_destroy(ctx)
+
+
 @pytest.mark.parametrize("dims,ranks", SHAPES)
 def test_pp_operators_and_update_match_oracle(dims, ranks):
     X, Ap = problem(dims, ranks, 2)
