@@ -1,0 +1,304 @@
+// probe_ttv2.cu — multi-TTV with several output rows per thread (the factor row F[x][k] loaded
+// once for NR parent rows) against the library's ttv_kernel, on the workload shapes.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/probe_ttv2 \
+//        tools/probe_ttv2.cu paper_1811_10573_b200/csrc/ttv.cu
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+#include <vector>
+#include <string>
+#include <cuda_runtime.h>
+#include "../paper_1811_10573_b200/csrc/internal.h"
+
+namespace cppp {
+bool pdl_enabled() { return false; }
+void note_launch() {}
+cudaError_t launch_ttv_cfg(const double* P, int64_t B, int64_t S, int64_t R, int K,
+                           const double* F, double* out, int V, int U, int xs, cudaStream_t st);
+}  // namespace cppp
+
+constexpr int TH = 256;
+
+// out[rho][k] = sum_x P[b][x][r][k] F[x][k], rho = b R + r; thread = NR rows x 2 columns
+template <int NR, int U>
+__global__ void __launch_bounds__(TH) ttv_rows(const double* __restrict__ P, int64_t S, int64_t R,
+                                              int K, int64_t rows, const double* __restrict__ F,
+                                              double* __restrict__ out) {
+  __shared__ double2 red[NR][TH];
+  const int KH = K / 2;
+  const int64_t e = blockIdx.x * (int64_t)TH + threadIdx.x;
+  const int64_t ngrp = (rows + NR - 1) / NR;
+  const int p = blockIdx.y, xs = gridDim.y;
+  const int64_t RK = R * K;
+  double2 acc[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) acc[j] = make_double2(0.0, 0.0);
+  const bool live = e < ngrp * KH;
+  if (live) {
+    const int64_t g = e / KH;
+    const int c = static_cast<int>(e - g * KH);
+    const double* base[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      int64_t rho = g * NR + j;
+      if (rho >= rows) rho = rows - 1;
+      const int64_t b = rho / R, r = rho - b * R;
+      base[j] = P + b * S * RK + r * K + 2 * c;
+    }
+    const double* f = F + 2 * c;
+    const int64_t x0 = S * p / xs, x1 = S * (p + 1) / xs;
+    int64_t x = x0;
+    for (; x + U <= x1; x += U) {
+      double2 pv[U][NR], fv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int j = 0; j < NR; ++j)
+          pv[u][j] = __ldcs(reinterpret_cast<const double2*>(base[j] + (x + u) * RK));
+        fv[u] = __ldg(reinterpret_cast<const double2*>(f + (x + u) * K));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          acc[j].x = fma(pv[u][j].x, fv[u].x, acc[j].x);
+          acc[j].y = fma(pv[u][j].y, fv[u].y, acc[j].y);
+        }
+    }
+    for (; x < x1; ++x) {
+      const double2 fv = __ldg(reinterpret_cast<const double2*>(f + x * K));
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const double2 pv = __ldcs(reinterpret_cast<const double2*>(base[j] + x * RK));
+        acc[j].x = fma(pv.x, fv.x, acc[j].x);
+        acc[j].y = fma(pv.y, fv.y, acc[j].y);
+      }
+    }
+  }
+  if (xs == 1) {
+    if (live) {
+      const int64_t g = e / KH;
+      const int c = static_cast<int>(e - g * KH);
+#pragma unroll
+      for (int j = 0; j < NR; ++j)
+        if (g * NR + j < rows)
+          *reinterpret_cast<double2*>(out + (g * NR + j) * K + 2 * c) = acc[j];
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < NR; ++j) red[j][threadIdx.x] = acc[j];
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  // rank p adds entries [p E / xs, (p+1) E / xs) of all ranks in rank order
+  constexpr int E = NR * TH;
+  const int i0 = p * E / xs, i1 = (p + 1) * E / xs;
+  for (int i = i0 + threadIdx.x; i < i1; i += TH) {
+    const int j = i / TH, t = i - j * TH;
+    const int64_t et = blockIdx.x * (int64_t)TH + t;
+    if (et >= ngrp * KH) continue;
+    const int64_t g = et / KH;
+    const int c = static_cast<int>(et - g * KH);
+    if (g * NR + j >= rows) continue;
+    const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&red[j][t]));
+    double2 s = make_double2(0.0, 0.0);
+    for (int r = 0; r < xs; ++r) {
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+      double2 v;
+      asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(remote));
+      if (r == 0) s = v;
+      else { s.x += v.x; s.y += v.y; }
+    }
+    *reinterpret_cast<double2*>(out + (g * NR + j) * K + 2 * c) = s;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int NR, int U>
+cudaError_t launch_rows(const double* P, int64_t B, int64_t S, int64_t R, int K, const double* F,
+                        double* out, int xs) {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(ttv_rows<NR, U>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    done = true;
+  }
+  const int64_t rows = B * R, ngrp = (rows + NR - 1) / NR;
+  const int64_t th = ngrp * (K / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((th + TH - 1) / TH), (unsigned)xs, 1);
+  cfg.blockDim = dim3(TH, 1, 1);
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = 1;
+  a[0].val.clusterDim.y = (unsigned)xs;
+  a[0].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ttv_rows<NR, U>, P, S, R, K, rows, F, out);
+}
+
+// software-pipelined: round i+1's loads are issued before round i is consumed; predicated tail
+template <int U, int THR, int MINB>
+__global__ void __launch_bounds__(THR, MINB) ttv_pipe(const double* __restrict__ P, int64_t S, int64_t RK,
+                                               int K, int64_t nvec, const double* __restrict__ F,
+                                               double* __restrict__ out) {
+  __shared__ double2 red[THR];
+  const int64_t e = blockIdx.x * (int64_t)THR + threadIdx.x;
+  const int p = blockIdx.y, xs = gridDim.y;
+  double2 acc = make_double2(0.0, 0.0);
+  if (e < nvec) {
+    const int64_t o = e * 2;
+    const int64_t b = o / RK;
+    const int64_t rk = o - b * RK;
+    const int k = static_cast<int>(rk % K);
+    const int64_t x0 = S * p / xs, x1 = S * (p + 1) / xs;
+    const double* pp = P + b * S * RK + rk;
+    const double* f = F + k;
+    double2 pa[U], fa[U], pb[U], fb[U];
+#define LOADB(PV, FV, X)                                                                     \
+  _Pragma("unroll") for (int u = 0; u < U; ++u) {                                             \
+    const bool ok = (X) + u < x1;                                                             \
+    const int64_t xx = ok ? (X) + u : x0;                                                     \
+    PV[u] = __ldcs(reinterpret_cast<const double2*>(pp + xx * RK));                           \
+    FV[u] = ok ? __ldg(reinterpret_cast<const double2*>(f + xx * K)) : make_double2(0.0, 0.0); \
+  }
+#define CONS(PV, FV)                                   \
+  _Pragma("unroll") for (int u = 0; u < U; ++u) {      \
+    acc.x = fma(PV[u].x, FV[u].x, acc.x);              \
+    acc.y = fma(PV[u].y, FV[u].y, acc.y);              \
+  }
+    LOADB(pa, fa, x0);
+    int64_t x = x0;
+    while (true) {
+      if (x + U < x1) { LOADB(pb, fb, x + U); }
+      CONS(pa, fa);
+      x += U;
+      if (x >= x1) break;
+      if (x + U < x1) { LOADB(pa, fa, x + U); }
+      CONS(pb, fb);
+      x += U;
+      if (x >= x1) break;
+    }
+  }
+  if (xs == 1) {
+    if (e < nvec) *reinterpret_cast<double2*>(out + e * 2) = acc;
+    return;
+  }
+  red[threadIdx.x] = acc;
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (p == 0 && e < nvec) {
+    double2 s = acc;
+    const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&red[threadIdx.x]));
+    for (int r = 1; r < xs; ++r) {
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+      double2 v;
+      asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(remote));
+      s.x += v.x; s.y += v.y;
+    }
+    *reinterpret_cast<double2*>(out + e * 2) = s;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <int U, int THR, int MINB>
+cudaError_t launch_pipe(const double* P, int64_t B, int64_t S, int64_t R, int K, const double* F,
+                        double* out, int xs) {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(ttv_pipe<U, THR, MINB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    done = true;
+  }
+  const int64_t nvec = B * R * K / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((nvec + THR - 1) / THR), (unsigned)xs, 1);
+  cfg.blockDim = dim3(THR, 1, 1);
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = 1;
+  a[0].val.clusterDim.y = (unsigned)xs;
+  a[0].val.clusterDim.z = 1;
+  cfg.attrs = a;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ttv_pipe<U, THR, MINB>, P, S, R * K, K, nvec, F, out);
+}
+
+__global__ void fill(double* p, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    z = (z ^ (z >> 31)) * 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 29;
+    p[i] = (double)(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+  }
+}
+
+int main() {
+  struct Shape { const char* name; int64_t B, S, R; int K; };
+  Shape shapes[] = {{"C4 T012 contract last", 400, 20, 1, 30},
+                    {"C4 T012 contract mid", 20, 20, 20, 30},
+                    {"C4 T012 contract first", 1, 20, 400, 30},
+                    {"C4 20x20 contract last", 20, 20, 1, 30},
+                    {"C4 20x20 contract first", 1, 20, 20, 30},
+                    {"C2 M0 (contract middle)", 400, 400, 1, 100}};
+  const int64_t PN = 256ll * 256 * 256 * 128;
+  double *P, *F, *out, *ref, *flush;
+  cudaMalloc(&P, 8 * PN);
+  cudaMalloc(&F, 8 * 400 * 128);
+  cudaMalloc(&out, 8ll * 256 * 256 * 128);
+  cudaMalloc(&ref, 8ll * 256 * 256 * 128);
+  const int64_t FL = 300ll << 20;
+  cudaMalloc(&flush, FL);
+  fill<<<4096, 256>>>(P, PN, 1);
+  fill<<<64, 256>>>(F, 400 * 128, 2);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (const Shape& s : shapes) {
+    const double bytes = 8.0 * (s.B * s.S * s.R * s.K + s.B * s.R * s.K);
+    if (s.B * s.S * s.R * s.K > PN) continue;
+    printf("%s  (%.1f MB)\n", s.name, bytes / 1e6);
+    cppp::launch_ttv_cfg(P, s.B, s.S, s.R, s.K, F, ref, 2, 4, 1, 0);   // unsplit reference
+    cudaDeviceSynchronize();
+    std::vector<double> hr(s.B * s.R * s.K), ho(hr.size());
+    cudaMemcpy(hr.data(), ref, 8 * hr.size(), cudaMemcpyDeviceToHost);
+    auto run = [&](const char* nm, auto&& f) {
+      for (int cold = 0; cold < 2; ++cold) {
+        float tot = 0;
+        const int reps = 10;
+        for (int i = 0; i < reps + 2; ++i) {
+          if (cold) cudaMemsetAsync(flush, i & 0xff, FL);
+          cudaEventRecord(a);
+          f();
+          cudaEventRecord(b);
+          cudaEventSynchronize(b);
+          float ms;
+          cudaEventElapsedTime(&ms, a, b);
+          if (i >= 2) tot += ms;
+        }
+        cudaError_t e = cudaGetLastError();
+        cudaMemcpy(ho.data(), out, 8 * ho.size(), cudaMemcpyDeviceToHost);
+        double md = 0, mr = 0;
+        for (size_t i = 0; i < ho.size(); ++i) {
+          md = fmax(md, fabs(ho[i] - hr[i]));
+          mr = fmax(mr, fabs(hr[i]));
+        }
+        const double us = 1e3 * tot / reps;
+        printf("  %-22s %s %7.1f us %6.2f TB/s  err %.1e %s\n", nm, cold ? "cold" : "warm", us,
+               bytes / us / 1e6, md / mr, e == cudaSuccess ? "" : cudaGetErrorString(e));
+      }
+    };
+    for (int xs : {1, 2, 4, 5}) {
+      char nm[64];
+      snprintf(nm, 64, "lib U4 xs=%d", xs);
+      run(nm, [&] { cppp::launch_ttv_cfg(P, s.B, s.S, s.R, s.K, F, out, 2, 4, xs, 0); });
+      snprintf(nm, 64, "pipe U4 T128 m5 xs=%d", xs);
+      run(nm, [&] { launch_pipe<4, 128, 5>(P, s.B, s.S, s.R, s.K, F, out, xs); });
+      snprintf(nm, 64, "pipe U2 T64 m16 xs=%d", xs);
+      run(nm, [&] { launch_pipe<2, 64, 16>(P, s.B, s.S, s.R, s.K, F, out, xs); });
+    }
+    {
+      // launch-only floor: empty-ish kernel of the same grid
+      run("lib xs=1 (again)", [&] { cppp::launch_ttv_cfg(P, s.B, s.S, s.R, s.K, F, out, 2, 4, 1, 0); });
+    }
+  }
+  return 0;
+}
