@@ -902,9 +902,214 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Bulk-copy versions of the two skinny kernels above (same per-output fma chains in ascending x,
+// so bit-identical): X reaches shared memory by 1-D bulk async copies (cp.async.bulk, SASS
+// UBLKCP) completing on an mbarrier, instead of per-thread loads -- every CTA keeps one or two
+// whole chunks of X in flight with one issuing thread.  tools/probe_skinny.cu on the compact
+// Laplacian's 1.95 GB first-level shapes (L2 flushed): k-contiguous 428 -> 329 us (4.9 -> 6.4
+// TB/s), m-contiguous 531 -> 336 us (4.0 -> 6.3 TB/s).  Per-CTA multi-stage rings measured
+// slower for the m-contiguous shape (NS = 2..4 with 1-2 CTAs per SM: 3.1-5.5 TB/s); four CTAs
+// per SM with one chunk each are the fastest.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+//   k-contiguous (R == 1): a chunk = SKB_CH consecutive rows of S doubles, one contiguous run
+//     (SKB_CH even and X 16-byte aligned, so every full chunk is a legal bulk copy); an
+//     SKB_NS-deep ring per CTA; thread = row; a ragged last chunk by plain loads.
+constexpr int SKB_CH = 256, SKB_NS = 2;
+template <int KB>
+__global__ void __launch_bounds__(SKB_CH)
+    ttm_skinny_kc_bulk_kernel(const double* __restrict__ X, int64_t B, int S, const double* __restrict__ F,
+                              int K, double* __restrict__ out) {
+  extern __shared__ __align__(16) double skb[];   // [SKB_NS][SKB_CH * S] | factor [S * K] | barriers
+  double* fs = skb + (int64_t)SKB_NS * SKB_CH * S;
+  uint64_t* full = reinterpret_cast<uint64_t*>(fs + ((S * K + 1) & ~1));
+  const int tid = threadIdx.x;
+  const int64_t nch = (B + SKB_CH - 1) / SKB_CH, nfull = B / SKB_CH;
+  const uint32_t bytes = static_cast<uint32_t>(SKB_CH) * S * 8;
+  if (tid == 0) {
+    for (int s = 0; s < SKB_NS; ++s) mbar_init(smem_u32(&full[s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  pdl_wait();
+  uint64_t pol = 0;
+  if (tid == 0) {
+    pol = l2_policy_x();
+    for (int s = 0; s < SKB_NS; ++s) {
+      const int64_t c = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
+      if (c < nfull) {
+        mbar_expect_tx(smem_u32(&full[s]), bytes);
+        bulk_g2s(smem_u32(skb + static_cast<int64_t>(s) * SKB_CH * S), X + c * SKB_CH * S, bytes,
+                 smem_u32(&full[s]), pol);
+      }
+    }
+  }
+  for (int e = tid; e < S * K; e += SKB_CH) fs[e] = F[e];
+  __syncthreads();
+  uint32_t phase = 0;   // per-stage parity (a plain-load chunk leaves its stage's barrier as it is)
+  int it = 0;
+  for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, ++it) {
+    const int st = it % SKB_NS;
+    double* stage = skb + static_cast<int64_t>(st) * SKB_CH * S;
+    const int nr = static_cast<int>(B - c * SKB_CH < SKB_CH ? B - c * SKB_CH : SKB_CH);
+    if (c < nfull) {
+      mbar_wait(smem_u32(&full[st]), (phase >> st) & 1u);
+      phase ^= 1u << st;
+    } else {
+      for (int e = tid; e < nr * S; e += SKB_CH) stage[e] = __ldcs(X + c * SKB_CH * S + e);
+      __syncthreads();
+    }
+    if (tid < nr) {
+      const double* row = stage + tid * S;   // odd S: conflict-free 8-byte reads across the warp
+      double acc[KB];
+#pragma unroll
+      for (int n = 0; n < KB; ++n) acc[n] = 0.0;
+      for (int x = 0; x < S; ++x) {
+        const double v = row[x];
+#pragma unroll
+        for (int n = 0; n < KB; ++n)
+          if (n < K) acc[n] = fma(v, fs[x * K + n], acc[n]);
+      }
+      double* o = out + (c * SKB_CH + tid) * K;
+#pragma unroll
+      for (int n = 0; n < KB; ++n)
+        if (n < K) o[n] = acc[n];
+    }
+    __syncthreads();   // every thread is done with the stage before it is refilled
+    if (tid == 0) {
+      const int64_t cn = c + static_cast<int64_t>(SKB_NS) * gridDim.x;
+      if (cn < nfull) {
+        mbar_expect_tx(smem_u32(&full[st]), bytes);
+        bulk_g2s(smem_u32(stage), X + cn * SKB_CH * S, bytes, smem_u32(&full[st]), pol);
+      }
+    }
+  }
+}
+
+//   m-contiguous (R >= SMB_CR): a unit = (b, SMB_CR consecutive r, SMB_XG consecutive x): SMB_XG
+//     row segments X[b][x][r0 .. r0 + SMB_CR), each copied from the 16-byte boundary at or below
+//     its start (odd R: every other x row is 8 bytes off), pitch SMB_CR + 2; a CTA runs the x
+//     groups of its r block in order, so each thread's SMB_CR / 256 accumulator sets persist
+//     across units; blocks whose rounded copies would leave X (the ragged last r block of a
+//     batch, the very end of X) go by plain loads.
+constexpr int SMB_CR = 1024, SMB_XG = 5, SMB_THREADS = 256;
+template <int KB>
+__global__ void __launch_bounds__(SMB_THREADS)
+    ttm_skinny_mc_bulk_kernel(const double* __restrict__ X, int64_t B, int S, int64_t R,
+                              const double* __restrict__ F, int K, double* __restrict__ out) {
+  extern __shared__ __align__(16) double smb[];   // [SMB_XG][SMB_CR + 2] | factor [S * K] | barrier
+  constexpr int P = SMB_CR + 2, RT = SMB_CR / SMB_THREADS;
+  double* fs = smb + SMB_XG * P;
+  uint64_t* full = reinterpret_cast<uint64_t*>(fs + ((S * K + 1) & ~1));
+  const int tid = threadIdx.x;
+  const int ng = (S + SMB_XG - 1) / SMB_XG;
+  const int64_t nrb = (R + SMB_CR - 1) / SMB_CR, nch = B * nrb;
+  const double* Xend = X + B * S * R;
+  auto bulk_ok = [&](int64_t b, int64_t r0) {
+    return r0 + SMB_CR <= R && X + ((b * S + S - 1) * R + r0 + SMB_CR + 2) <= Xend;
+  };
+  auto seg_off = [](const double* p) { return static_cast<int>((reinterpret_cast<uintptr_t>(p) >> 3) & 1); };
+  if (tid == 0) {
+    mbar_init(smem_u32(&full[0]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  pdl_wait();
+  for (int e = tid; e < S * K; e += SMB_THREADS) fs[e] = F[e];
+  const uint64_t pol = l2_policy_x();
+  uint32_t phase = 0;
+  double acc[RT][KB];
+  for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const int64_t b = c / nrb, r0 = (c - b * nrb) * SMB_CR;
+    const int nr = static_cast<int>(R - r0 < SMB_CR ? R - r0 : SMB_CR);
+    const bool bulk = bulk_ok(b, r0);
+#pragma unroll
+    for (int j = 0; j < RT; ++j)
+#pragma unroll
+      for (int n = 0; n < KB; ++n) acc[j][n] = 0.0;
+    for (int g = 0; g < ng; ++g) {
+      const int xa = g * SMB_XG, xb = xa + SMB_XG < S ? xa + SMB_XG : S;
+      const double* row0 = X + (b * S + xa) * R + r0;
+      __syncthreads();   // the previous unit's readers are done (and the factor is staged)
+      if (bulk) {
+        if (tid == 0) {
+          uint32_t tot = 0;
+          for (int x = xa; x < xb; ++x)
+            tot += static_cast<uint32_t>(((SMB_CR + seg_off(row0 + (x - xa) * R)) * 8 + 15) & ~15);
+          mbar_expect_tx(smem_u32(&full[0]), tot);
+          for (int x = xa; x < xb; ++x) {
+            const double* src = row0 + (x - xa) * R;
+            const int off = seg_off(src);
+            bulk_g2s(smem_u32(smb + (x - xa) * P), src - off,
+                     static_cast<uint32_t>(((SMB_CR + off) * 8 + 15) & ~15), smem_u32(&full[0]), pol);
+          }
+        }
+        mbar_wait(smem_u32(&full[0]), phase);
+        phase ^= 1u;
+      } else {
+        for (int x = xa; x < xb; ++x) {
+          const double* src = row0 + (x - xa) * R;
+          const int off = seg_off(src);
+          for (int t = tid; t < nr; t += SMB_THREADS) smb[(x - xa) * P + off + t] = __ldcs(src + t);
+        }
+        __syncthreads();
+      }
+      for (int x = xa; x < xb; ++x) {
+        const double* srow = smb + (x - xa) * P + seg_off(row0 + (x - xa) * R);
+        double f[KB];
+#pragma unroll
+        for (int n = 0; n < KB; ++n) f[n] = n < K ? fs[x * K + n] : 0.0;
+#pragma unroll
+        for (int j = 0; j < RT; ++j) {
+          const double v = srow[tid + SMB_THREADS * j];
+#pragma unroll
+          for (int n = 0; n < KB; ++n)
+            if (n < K) acc[j][n] = fma(v, f[n], acc[j][n]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < RT; ++j) {
+      const int r = tid + SMB_THREADS * j;
+      if (r < nr) {
+        double* o = out + (b * R + r0 + r) * K;
+#pragma unroll
+        for (int n = 0; n < KB; ++n)
+          if (n < K) o[n] = acc[j][n];
+      }
+    }
+  }
+}
+
+bool skinny_bulk_on() {
+  static const bool off = getenv("CPPP_NO_SKINNY_BULK") != nullptr;   // A/B: the register-load kernels
+  return !off;
+}
+
 template <int KB>
 cudaError_t run_skinny(const double* X, int64_t B, int64_t S, int64_t R, const double* F, int K,
                        double* out, cudaStream_t st) {
+  const bool al16 = (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  if (R > 1 && al16 && skinny_bulk_on() && R >= SMB_CR && S * K <= 1024 && S < (1 << 30)) {
+    const size_t smem = sizeof(double) * (SMB_XG * (SMB_CR + 2) + ((S * K + 1) & ~1)) + 16;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(ttm_skinny_mc_bulk_kernel<KB>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 56 * 1024);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    int64_t blocks = B * ((R + SMB_CR - 1) / SMB_CR);
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    cudaError_t e = launch_pdl(ttm_skinny_mc_bulk_kernel<KB>, dim3((unsigned)blocks), dim3(SMB_THREADS), smem,
+                               st, X, B, (int)S, R, F, K, out);
+    note_launch();
+    return e;
+  }
   if (R > 1) {
     int64_t blocks = (B * R + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
@@ -919,6 +1124,22 @@ cudaError_t run_skinny(const double* X, int64_t B, int64_t S, int64_t R, const d
     if (blocks > 148 * 16) blocks = 148 * 16;
     cudaError_t e = launch_pdl(ttm_skinny_rows_kernel<KB>, dim3((unsigned)blocks), dim3(256), 0, st, X, B, S, F,
                                K, out);
+    note_launch();
+    return e;
+  }
+  const size_t smem_b = sizeof(double) * (static_cast<size_t>(SKB_NS) * SKB_CH * S + ((S * K + 1) & ~1)) + 16 * SKB_NS;
+  if (al16 && skinny_bulk_on() && smem_b <= 110 * 1024) {   // two CTAs per SM
+    static bool attr_b = false;
+    if (!attr_b) {
+      cudaError_t e = cudaFuncSetAttribute(ttm_skinny_kc_bulk_kernel<KB>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+      if (e != cudaSuccess) return e;
+      attr_b = true;
+    }
+    int64_t blocks = (B + SKB_CH - 1) / SKB_CH;
+    if (blocks > 148 * 2) blocks = 148 * 2;
+    cudaError_t e = launch_pdl(ttm_skinny_kc_bulk_kernel<KB>, dim3((unsigned)blocks), dim3(SKB_CH), smem_b, st, X,
+                               B, (int)S, F, K, out);
     note_launch();
     return e;
   }

@@ -717,11 +717,13 @@ def test_fused_level1_build_matches_oracle(dims, K):
 
 
 @pytest.mark.parametrize("dims,K", [((25, 25, 25, 25), 2), ((31, 17, 9), 5), ((5, 3, 7, 9, 11, 3), 16),
-                                    ((9, 9, 9, 9, 9, 9), 1), ((3, 101, 7), 8)])
+                                    ((9, 9, 9, 9, 9, 9), 1), ((3, 101, 7), 8),
+                                    ((13, 97, 23), 4), ((7, 1031, 3), 2), ((3, 5, 2053), 3)])
 def test_skinny_odd_extent_contractions(dims, K):
     """Odd extents (no 16-byte TMA strides: the compact Laplacian's s = 25) with K <= 16:
-    the bandwidth-shaped kernels (thread per (b, r) for m-contiguous contractions, shared-memory
-    rows or warp per row for the natural unfolding) -- MTTKRP, every operator and a PP update."""
+    the bandwidth-shaped kernels (bulk-copied chunks of rows or of r blocks, ragged last chunks by
+    plain loads; thread per (b, r) for short m-contiguous rows, shared-memory rows or warp per row
+    for the natural unfolding) -- MTTKRP, every operator and a PP update."""
     X, A = random_problem(dims, K, 15)
     N = len(dims)
     ctx = cp.cp_init(X, N, dims, K)
