@@ -222,6 +222,165 @@ cudaError_t launch_pipe(const double* P, int64_t B, int64_t S, int64_t R, int K,
   return cudaLaunchKernelEx(&cfg, ttv_pipe<U, THR, MINB>, P, S, R * K, K, nvec, F, out);
 }
 
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint32_t b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mb_expect(uint32_t b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint32_t b, uint32_t ph) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok) : "r"(b), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// bulk-staged multi-TTV: CTA = (item = (b, column block cb of W), x part p of a (1, xs, 1) cluster);
+// units of XG x rows: W == RK -> one contiguous bulk copy per unit; else per-x segments from
+// the 16-byte boundary (pitch W + 2).  Thread = (column pair c, x phase j of TPC).
+struct TB { const double* P; const double* F; double* out; int64_t B, S, RK; int K, W, XG, ncb, NS; };
+__global__ void __launch_bounds__(256) ttv_bulk(const TB a) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(16) double2 red[256];
+  __shared__ uint64_t full[4];
+  const int tid = threadIdx.x;
+  const int P2 = a.W == a.RK ? a.W : a.W + 2;   // stage pitch
+  const int64_t item = blockIdx.x;
+  const int64_t b = item / a.ncb;
+  const int64_t c0 = (item - b * a.ncb) * a.W;
+  const int wv = (int)(a.RK - c0 < a.W ? a.RK - c0 : a.W);
+  const int np = a.W / 2, tpc = 256 / np;
+  const int cp = tid % np, j = tid / np;
+  const bool act = j < tpc && 2 * cp < wv;
+  const int p = blockIdx.y, xs = gridDim.y;
+  const int64_t x0 = a.S * p / xs, x1 = a.S * (p + 1) / xs;
+  const int nu = (int)((x1 - x0 + a.XG - 1) / a.XG);
+  const double* base = a.P + b * a.S * a.RK + c0;
+  const bool whole = a.W == a.RK;
+  const int k = (int)((c0 + 2 * cp) % a.K);
+  auto issue = [&](int u, int st, uint64_t pol) {
+    const int64_t xa = x0 + (int64_t)u * a.XG, xb = xa + a.XG < x1 ? xa + a.XG : x1;
+    double* dst = sm + (int64_t)st * a.XG * P2;
+    if (whole) {
+      const uint32_t bytes = (uint32_t)((xb - xa) * a.RK * 8);
+      mb_expect(su32(&full[st]), bytes);
+      bulk(su32(dst), base + xa * a.RK, bytes, su32(&full[st]), pol);
+    } else {
+      uint32_t tot = 0;
+      for (int64_t x = xa; x < xb; ++x) {
+        const double* src = base + x * a.RK;
+        const int off = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+        tot += (uint32_t)(((wv + off) * 8 + 15) & ~15);
+      }
+      mb_expect(su32(&full[st]), tot);
+      for (int64_t x = xa; x < xb; ++x) {
+        const double* src = base + x * a.RK;
+        const int off = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+        bulk(su32(dst + (x - xa) * P2), src - off, (uint32_t)(((wv + off) * 8 + 15) & ~15), su32(&full[st]), pol);
+      }
+    }
+  };
+  uint64_t pol = 0;
+  if (tid == 0) {
+    pol = pol_first();
+    for (int s = 0; s < a.NS; ++s) mb_init(su32(&full[s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < a.NS && s < nu; ++s) issue(s, s, pol);
+  }
+  __syncthreads();
+  double2 acc = make_double2(0.0, 0.0);
+  uint32_t phase = 0;
+  for (int u = 0; u < nu; ++u) {
+    const int st = u % a.NS;
+    const int64_t xa = x0 + (int64_t)u * a.XG, xb = xa + a.XG < x1 ? xa + a.XG : x1;
+    mb_wait(su32(&full[st]), (phase >> st) & 1);
+    phase ^= 1u << st;
+    if (act) {
+      const double* stg = sm + (int64_t)st * a.XG * P2;
+      for (int64_t x = xa + j; x < xb; x += tpc) {
+        const double* row = stg + (x - xa) * P2;
+        const int off = whole ? 0 : (int)((reinterpret_cast<uintptr_t>(base + x * a.RK) >> 3) & 1);
+        double v0, v1;
+        if (whole || off == 0) {
+          const double2 v = *reinterpret_cast<const double2*>(row + 2 * cp);
+          v0 = v.x; v1 = v.y;
+        } else {
+          v0 = row[off + 2 * cp]; v1 = row[off + 2 * cp + 1];
+        }
+        const double2 f = __ldg(reinterpret_cast<const double2*>(a.F + x * a.K + k));
+        acc.x = fma(v0, f.x, acc.x);
+        acc.y = fma(v1, f.y, acc.y);
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && u + a.NS < nu) issue(u + a.NS, st, pol);
+  }
+  red[tid] = acc;
+  __syncthreads();
+  double2 s = make_double2(0.0, 0.0);
+  if (j == 0 && act) {
+    s = red[cp];
+    for (int jj = 1; jj < tpc; ++jj) { s.x += red[jj * np + cp].x; s.y += red[jj * np + cp].y; }
+  }
+  if (xs == 1) {
+    if (j == 0 && act) *reinterpret_cast<double2*>(a.out + b * a.RK + c0 + 2 * cp) = s;
+    return;
+  }
+  __syncthreads();
+  if (j == 0) red[cp] = s;
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (p == 0 && j == 0 && act) {
+    const uint32_t local = su32(&red[cp]);
+    for (int r = 1; r < xs; ++r) {
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+      double2 v;
+      asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(remote));
+      s.x += v.x; s.y += v.y;
+    }
+    *reinterpret_cast<double2*>(a.out + b * a.RK + c0 + 2 * cp) = s;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+void run_bulk(const double* P, int64_t B, int64_t S, int64_t R, int K, const double* F, double* out,
+              int W, int XG, int NS, int xs) {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(ttv_bulk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(ttv_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    done = true;
+  }
+  TB a;
+  a.P = P; a.F = F; a.out = out; a.B = B; a.S = S; a.RK = R * K; a.K = K;
+  a.W = W > a.RK ? (int)a.RK : W;
+  a.XG = XG; a.NS = NS;
+  a.ncb = (int)((a.RK + a.W - 1) / a.W);
+  const int P2 = a.W == a.RK ? a.W : a.W + 2;
+  const size_t smem = 8ull * NS * XG * P2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(B * a.ncb), (unsigned)xs, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = (unsigned)xs;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, ttv_bulk, a);
+}
+
 __global__ void fill(double* p, int64_t n, uint64_t seed) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t z = (i + 1) * 0x9E3779B97F4A7C15ull ^ seed;
@@ -232,13 +391,13 @@ __global__ void fill(double* p, int64_t n, uint64_t seed) {
 }
 
 int main() {
+  setvbuf(stdout, nullptr, _IONBF, 0);
   struct Shape { const char* name; int64_t B, S, R; int K; };
-  Shape shapes[] = {{"C4 T012 contract last", 400, 20, 1, 30},
-                    {"C4 T012 contract mid", 20, 20, 20, 30},
-                    {"C4 T012 contract first", 1, 20, 400, 30},
-                    {"C4 20x20 contract last", 20, 20, 1, 30},
-                    {"C4 20x20 contract first", 1, 20, 20, 30},
-                    {"C2 M0 (contract middle)", 400, 400, 1, 100}};
+  Shape shapes[] = {{"C2 M0 (contract middle)", 400, 400, 1, 100},
+                    {"C2 M1 (contract first)", 1, 400, 400, 100},
+                    {"C3 lvl2 (100^3 x50 mid)", 100, 100, 100, 50},
+                    {"C3 lvl2 last", 10000, 100, 1, 50},
+                    {"C3 lvl2 first", 1, 100, 10000, 50}};
   const int64_t PN = 256ll * 256 * 256 * 128;
   double *P, *F, *out, *ref, *flush;
   cudaMalloc(&P, 8 * PN);
@@ -261,7 +420,7 @@ int main() {
     std::vector<double> hr(s.B * s.R * s.K), ho(hr.size());
     cudaMemcpy(hr.data(), ref, 8 * hr.size(), cudaMemcpyDeviceToHost);
     auto run = [&](const char* nm, auto&& f) {
-      for (int cold = 0; cold < 2; ++cold) {
+      for (int cold = 1; cold < 2; ++cold) {
         float tot = 0;
         const int reps = 10;
         for (int i = 0; i < reps + 2; ++i) {
@@ -286,18 +445,16 @@ int main() {
                bytes / us / 1e6, md / mr, e == cudaSuccess ? "" : cudaGetErrorString(e));
       }
     };
-    for (int xs : {1, 2, 4, 5}) {
+    run("lib (launch_ttv rule)", [&] { cppp::launch_ttv_cfg(P, s.B, s.S, s.R, s.K, F, out, 2, 4,
+        s.B * s.R * s.K / 2 / 256 < 148 ? 4 : 1, 0); });
+    struct V { int W, XG, NS, xs; };
+    V vs[] = {{100, 40, 2, 1}, {100, 20, 2, 1}, {100, 40, 2, 2}, {100, 20, 3, 2}, {256, 16, 2, 2}, {256, 16, 2, 4},
+              {512, 8, 2, 4}, {512, 16, 2, 2}, {256, 32, 2, 2}, {128, 32, 2, 4}, {256, 16, 1, 4}, {512, 16, 1, 2}};
+    for (const V& v : vs) {
+      if ((v.W == 100) != (s.R * s.K == 100)) continue;
       char nm[64];
-      snprintf(nm, 64, "lib U4 xs=%d", xs);
-      run(nm, [&] { cppp::launch_ttv_cfg(P, s.B, s.S, s.R, s.K, F, out, 2, 4, xs, 0); });
-      snprintf(nm, 64, "pipe U4 T128 m5 xs=%d", xs);
-      run(nm, [&] { launch_pipe<4, 128, 5>(P, s.B, s.S, s.R, s.K, F, out, xs); });
-      snprintf(nm, 64, "pipe U2 T64 m16 xs=%d", xs);
-      run(nm, [&] { launch_pipe<2, 64, 16>(P, s.B, s.S, s.R, s.K, F, out, xs); });
-    }
-    {
-      // launch-only floor: empty-ish kernel of the same grid
-      run("lib xs=1 (again)", [&] { cppp::launch_ttv_cfg(P, s.B, s.S, s.R, s.K, F, out, 2, 4, 1, 0); });
+      snprintf(nm, 64, "bulk W%d XG%d NS%d xs%d", v.W, v.XG, v.NS, v.xs);
+      run(nm, [&] { run_bulk(P, s.B, s.S, s.R, s.K, F, out, v.W, v.XG, v.NS, v.xs); });
     }
   }
   return 0;
