@@ -233,6 +233,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (box8) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX4)) : "memory");
       if constexpr (!BATCH) {
         int64_t it = 0;
+        int pst = 0;          // it % stages and (it / stages) & 1, kept incrementally (a runtime
+        uint32_t pph = 0;     // divisor costs a division sequence per stage)
         long long sk_t = skG ? (blockIdx.x * skT / skG) / nk : 0;
         const long long sk_hi = skG ? (blockIdx.x + 1) * skT / skG : 0;
         while (true) {
@@ -246,11 +248,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             unit = static_cast<long long>(atomicAdd(tile_counter, 1ull));
           }
           if (unit >= nunits) {
-            const int st = static_cast<int>(it % stages);
-            const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
-            if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
-            stage_tile[st] = -1;
-            mbar_arrive(smem_u32(&full[st]));   // wake the consumers with the sentinel
+            if (it >= stages) mbar_wait(smem_u32(&empty[pst]), pph ^ 1);
+            stage_tile[pst] = -1;
+            mbar_arrive(smem_u32(&full[pst]));   // wake the consumers with the sentinel
             break;
           }
           const Unit un = skG ? decode_sk(unit, nk, skT, skG) : decode_unit(unit, nfull, nk, ks);
@@ -260,8 +260,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int64_t b_first = Rflat ? m0 / Rflat : 0;
           const int64_t r_first = Rflat ? m0 - b_first * Rflat : 0;
           for (int kt = un.k0; kt < un.k1; ++kt, ++it) {
-            const int st = static_cast<int>(it % stages);
-            const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+            const int st = pst;
+            const uint32_t ph = pph;
+            if (++pst == stages) {
+              pst = 0;
+              pph ^= 1u;
+            }
             if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
             if (kt == un.k0) stage_tile[st] = unit;
             const uint32_t fb = smem_u32(&full[st]);
@@ -299,6 +303,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // before this one's loads are issued, so the atomic's round trip is not paid per unit
         constexpr long long UB = 4;
         int64_t it = 0;
+        int pst = 0;
+        uint32_t pph = 0;
         auto issue = [&](long long unit) {
         const Unit un = decode_unit(unit, nfull, nk, ks);
         const int64_t b = MC ? un.tile / mtiles : 0;
@@ -307,8 +313,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int64_t b_first = Rflat ? m0 / Rflat : 0;
         const int64_t r_first = Rflat ? m0 - b_first * Rflat : 0;
         for (int kt = un.k0; kt < un.k1; ++kt, ++it) {
-          const int st = static_cast<int>(it % stages);
-          const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+          const int st = pst;
+          const uint32_t ph = pph;
+          if (++pst == stages) {
+            pst = 0;
+            pph ^= 1u;
+          }
           if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
           if (kt == un.k0) stage_tile[st] = unit;
           const uint32_t fb = smem_u32(&full[st]);
@@ -347,11 +357,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           next = static_cast<long long>(atomicAdd(tile_counter, (unsigned long long)UB));
           for (long long unit = u0; unit < u1; ++unit) issue(unit);
         }
-        const int st = static_cast<int>(it % stages);
-        const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
-        if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
-        stage_tile[st] = -1;
-        mbar_arrive(smem_u32(&full[st]));   // wake the consumers with the sentinel
+        if (it >= stages) mbar_wait(smem_u32(&empty[pst]), pph ^ 1);
+        stage_tile[pst] = -1;
+        mbar_arrive(smem_u32(&full[pst]));   // wake the consumers with the sentinel
       }
     }
     return;
@@ -364,13 +372,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // m-contiguous A: 16-row box (warp >> 1), rows 8 (warp & 1) + g within it
   const int mbox = warp >> 1, mrow = 8 * (warp & 1) + g;
   const bool pairs = (K % 2) == 0;
-  int64_t it = 0;
+  int cst = 0;        // stage index and parity of the next k stage, kept incrementally
+  uint32_t cph = 0;
   while (true) {
-    {
-      const int st = static_cast<int>(it % stages);
-      mbar_wait(smem_u32(&full[st]), static_cast<uint32_t>((it / stages) & 1));
-    }
-    const long long unit = stage_tile[static_cast<int>(it % stages)];
+    mbar_wait(smem_u32(&full[cst]), cph);
+    const long long unit = stage_tile[cst];
     if (unit < 0) break;
     const Unit un = skG ? decode_sk(unit, nk, skT, skG) : decode_unit(unit, nfull, nk, ks);
     TTM_STAMP_START(unit);
@@ -380,10 +386,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
 
-    for (int kt = un.k0; kt < un.k1; ++kt, ++it) {
-      const int st = static_cast<int>(it % stages);
-      const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
-      if (kt > un.k0) mbar_wait(smem_u32(&full[st]), ph);
+    for (int kt = un.k0; kt < un.k1; ++kt) {
+      const int st = cst;
+      if (kt > un.k0) mbar_wait(smem_u32(&full[st]), cph);
+      if (++cst == stages) {
+        cst = 0;
+        cph ^= 1u;
+      }
       const uint32_t sx = smem_u32(base + st * C::STAGE);
       const uint32_t sf = sx + C::XBYTES;
       const int qmax = (S - kt * BK) > 8 ? 2 : 1;   // skip an all-zero k tail
@@ -598,14 +607,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX4)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmF)) : "memory");
       int64_t it = 0;
+      int pst = 0;   // it % stages, (it / stages) & 1 kept incrementally
+      uint32_t pph = 0;
       while (true) {
         const long long unit = static_cast<long long>(atomicAdd(tile_counter, 1ull));
         if (unit >= nunits) {
-          const int st = static_cast<int>(it % stages);
-          const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
-          if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
-          stage_tile[st] = -1;
-          mbar_arrive(smem_u32(&full[st]));
+          if (it >= stages) mbar_wait(smem_u32(&empty[pst]), pph ^ 1);
+          stage_tile[pst] = -1;
+          mbar_arrive(smem_u32(&full[pst]));
           break;
         }
         int64_t xl, xo, h, p;
@@ -615,8 +624,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int64_t t = tile_of(unit, i, &xl, &xo, &h, &p);
           const int64_t b = t / mtiles, m0 = (t - b * mtiles) * BM;
           for (int kt = 0; kt < nk; ++kt, ++it) {
-            const int st = static_cast<int>(it % stages);
-            const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
+            const int st = pst;
+            const uint32_t ph = pph;
+            if (++pst == stages) {
+              pst = 0;
+              pph ^= 1u;
+            }
             if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
             if (kt == 0) {   // the consumers read the tile's coordinates (no 64-bit divisions)
               stage_tile[st] = i + (i + 1 == L ? 65536 : 0);
@@ -640,13 +653,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int g = lane >> 2, t4 = lane & 3;
   const int mbox = warp >> 1, mrow = 8 * (warp & 1) + g;
   const int mloc = 16 * mbox + mrow;   // this thread's row of the tile
-  int64_t it = 0;
+  int cst = 0;   // stage index and parity of the next k stage, kept incrementally
+  uint32_t cph = 0;
   while (true) {
-    {
-      const int st = static_cast<int>(it % stages);
-      mbar_wait(smem_u32(&full[st]), static_cast<uint32_t>((it / stages) & 1));
-    }
-    const int st0 = static_cast<int>(it % stages);
+    mbar_wait(smem_u32(&full[cst]), cph);
+    const int st0 = cst;
     const long long code = stage_tile[st0];
     if (code < 0) break;
     const int64_t i = code & 65535;
@@ -656,10 +667,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     double acc[NT][2];
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
-    for (int kt = 0; kt < nk; ++kt, ++it) {
-      const int st = static_cast<int>(it % stages);
-      const uint32_t ph = static_cast<uint32_t>((it / stages) & 1);
-      if (kt > 0) mbar_wait(smem_u32(&full[st]), ph);
+    for (int kt = 0; kt < nk; ++kt) {
+      const int st = cst;
+      if (kt > 0) mbar_wait(smem_u32(&full[st]), cph);
+      if (++cst == stages) {
+        cst = 0;
+        cph ^= 1u;
+      }
       const uint32_t sx = smem_u32(base + st * C::STAGE);
       const uint32_t sf = sx + C::XBYTES;
       const int qmax = (S - kt * BK) > 8 ? 2 : 1;
