@@ -208,6 +208,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(base + stages * C::STAGE);
   uint64_t* empty = full + stages;
   __shared__ long long stage_tile[16];   // unit id carried by the first k-stage of each unit
+  __shared__ Unit stage_unit[16];        // ... its decoded form and tile origin (the consumers
+  __shared__ long long stage_bm[16][2];  // skip the 64-bit divisions of decode / batch split)
   __shared__ int ticket_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -224,6 +226,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int nk = (S + BK - 1) / BK;
   const long long nunits = skG ? nsplit * skG : nfull + static_cast<long long>(ks) * nsplit;
   const long long skT = nsplit * nk;   // stream-K: slices in all
+  auto decode = [&](long long unit) {
+    return skG ? decode_sk(unit, nk, skT, skG) : decode_unit(unit, nfull, nk, ks);
+  };
 
   if (warp == NWARP) {  // ---------------- TMA producer
     if (lane == 0) {
@@ -253,7 +258,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_arrive(smem_u32(&full[pst]));   // wake the consumers with the sentinel
             break;
           }
-          const Unit un = skG ? decode_sk(unit, nk, skT, skG) : decode_unit(unit, nfull, nk, ks);
+          const Unit un = decode(unit);
           const int64_t b = MC ? un.tile / mtiles : 0;
           const int64_t m0 = (un.tile - b * mtiles) * BM;
           // flattened rows: (batch, row) of the tile's first row, one division per unit
@@ -320,7 +325,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             pph ^= 1u;
           }
           if (it >= stages) mbar_wait(smem_u32(&empty[st]), ph ^ 1);
-          if (kt == un.k0) stage_tile[st] = unit;
+          if (kt == un.k0) {
+            stage_tile[st] = unit;
+            stage_unit[st] = un;
+            stage_bm[st][0] = b;
+            stage_bm[st][1] = m0;
+          }
           const uint32_t fb = smem_u32(&full[st]);
           mbar_expect_tx(fb, C::STAGE);
           const uint32_t sx = smem_u32(base + st * C::STAGE);
@@ -378,10 +388,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_wait(smem_u32(&full[cst]), cph);
     const long long unit = stage_tile[cst];
     if (unit < 0) break;
-    const Unit un = skG ? decode_sk(unit, nk, skT, skG) : decode_unit(unit, nfull, nk, ks);
+    // short units (BATCH): the producer's decoded unit; long ones decode it here (measured: the
+    // shared-memory copy helps the S = 20 GEMM 272 -> 264 us and costs C2's 395 -> 399 us)
+    const Unit un = BATCH ? stage_unit[cst] : decode(unit);
     TTM_STAMP_START(unit);
-    const int64_t b = MC ? un.tile / mtiles : 0;
-    const int64_t m0 = (un.tile - b * mtiles) * BM;
+    const int64_t b = BATCH ? stage_bm[cst][0] : (MC ? un.tile / mtiles : 0);
+    const int64_t m0 = BATCH ? stage_bm[cst][1] : (un.tile - b * mtiles) * BM;
     double acc[NT][2];
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
@@ -1333,7 +1345,9 @@ cudaError_t run_dmma_b(const double* X, int64_t B, int64_t S, int64_t R, const d
     }
   }
   if (ks == 1) {
-    // a last wave at most half full is split into k halves (one wave of half-tiles)
+    // a last wave at most half full is split into k halves (one wave of half-tiles).  (Stream-K
+    // over the last wave's k slices -- every SM ending within a few slices of the others -- was
+    // slower: the partial-tile combines land on the critical path, C2's GEMM 395 -> 404 us.)
     const int64_t tail = ntiles % grid;
     if (ntiles > grid && tail > 0 && 2 * tail <= grid && tail * 2 * slot <= TTM_PART && nk >= 4) {
       nsplit = tail;

@@ -268,21 +268,25 @@ __global__ void __launch_bounds__(256) ttv_bulk(const TB a) {
   const double* base = a.P + b * a.S * a.RK + c0;
   const bool whole = a.W == a.RK;
   const int k = (int)((c0 + 2 * cp) % a.K);
+  double* fsm = sm + (int64_t)a.NS * a.XG * P2;   // [NS][XG][K] factor rows
   auto issue = [&](int u, int st, uint64_t pol) {
     const int64_t xa = x0 + (int64_t)u * a.XG, xb = xa + a.XG < x1 ? xa + a.XG : x1;
     double* dst = sm + (int64_t)st * a.XG * P2;
+    const uint32_t fbytes = (uint32_t)((xb - xa) * a.K * 8);
     if (whole) {
       const uint32_t bytes = (uint32_t)((xb - xa) * a.RK * 8);
-      mb_expect(su32(&full[st]), bytes);
+      mb_expect(su32(&full[st]), bytes + fbytes);
+      bulk(su32(fsm + (int64_t)st * a.XG * a.K), a.F + xa * a.K, fbytes, su32(&full[st]), pol);
       bulk(su32(dst), base + xa * a.RK, bytes, su32(&full[st]), pol);
     } else {
-      uint32_t tot = 0;
+      uint32_t tot = fbytes;
       for (int64_t x = xa; x < xb; ++x) {
         const double* src = base + x * a.RK;
         const int off = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
         tot += (uint32_t)(((wv + off) * 8 + 15) & ~15);
       }
       mb_expect(su32(&full[st]), tot);
+      bulk(su32(fsm + (int64_t)st * a.XG * a.K), a.F + xa * a.K, fbytes, su32(&full[st]), pol);
       for (int64_t x = xa; x < xb; ++x) {
         const double* src = base + x * a.RK;
         const int off = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
@@ -307,20 +311,32 @@ __global__ void __launch_bounds__(256) ttv_bulk(const TB a) {
     phase ^= 1u << st;
     if (act) {
       const double* stg = sm + (int64_t)st * a.XG * P2;
-      for (int64_t x = xa + j; x < xb; x += tpc) {
-        const double* row = stg + (x - xa) * P2;
-        const int off = whole ? 0 : (int)((reinterpret_cast<uintptr_t>(base + x * a.RK) >> 3) & 1);
-        double v0, v1;
-        if (whole || off == 0) {
-          const double2 v = *reinterpret_cast<const double2*>(row + 2 * cp);
-          v0 = v.x; v1 = v.y;
-        } else {
-          v0 = row[off + 2 * cp]; v1 = row[off + 2 * cp + 1];
-        }
-        const double2 f = __ldg(reinterpret_cast<const double2*>(a.F + x * a.K + k));
+      const double* fst = fsm + (int64_t)st * a.XG * a.K;
+      int64_t x = xa + j;
+      double2 acc2 = make_double2(0.0, 0.0);
+      for (; x + tpc < xb; x += 2 * tpc) {
+        const double* r0 = stg + (x - xa) * P2;
+        const double* r1 = r0 + tpc * P2;
+        const int o0 = whole ? 0 : (int)((reinterpret_cast<uintptr_t>(base + x * a.RK) >> 3) & 1);
+        const int o1 = whole ? 0 : (int)((reinterpret_cast<uintptr_t>(base + (x + tpc) * a.RK) >> 3) & 1);
+        const double v0 = r0[o0 + 2 * cp], v1 = r0[o0 + 2 * cp + 1];
+        const double w0 = r1[o1 + 2 * cp], w1 = r1[o1 + 2 * cp + 1];
+        const double2 f = *reinterpret_cast<const double2*>(fst + (x - xa) * a.K + k);
+        const double2 g = *reinterpret_cast<const double2*>(fst + (x + tpc - xa) * a.K + k);
         acc.x = fma(v0, f.x, acc.x);
         acc.y = fma(v1, f.y, acc.y);
+        acc2.x = fma(w0, g.x, acc2.x);
+        acc2.y = fma(w1, g.y, acc2.y);
       }
+      for (; x < xb; x += tpc) {
+        const double* row = stg + (x - xa) * P2;
+        const int off = whole ? 0 : (int)((reinterpret_cast<uintptr_t>(base + x * a.RK) >> 3) & 1);
+        const double2 f = *reinterpret_cast<const double2*>(fst + (x - xa) * a.K + k);
+        acc.x = fma(row[off + 2 * cp], f.x, acc.x);
+        acc.y = fma(row[off + 2 * cp + 1], f.y, acc.y);
+      }
+      acc.x += acc2.x;
+      acc.y += acc2.y;
     }
     __syncthreads();
     if (tid == 0 && u + a.NS < nu) issue(u + a.NS, st, pol);
@@ -366,7 +382,7 @@ void run_bulk(const double* P, int64_t B, int64_t S, int64_t R, int K, const dou
   a.XG = XG; a.NS = NS;
   a.ncb = (int)((a.RK + a.W - 1) / a.W);
   const int P2 = a.W == a.RK ? a.W : a.W + 2;
-  const size_t smem = 8ull * NS * XG * P2;
+  const size_t smem = 8ull * NS * XG * P2 + 8ull * NS * XG * K;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(B * a.ncb), (unsigned)xs, 1);
   cfg.blockDim = dim3(256, 1, 1);
@@ -448,8 +464,8 @@ int main() {
     run("lib (launch_ttv rule)", [&] { cppp::launch_ttv_cfg(P, s.B, s.S, s.R, s.K, F, out, 2, 4,
         s.B * s.R * s.K / 2 / 256 < 148 ? 4 : 1, 0); });
     struct V { int W, XG, NS, xs; };
-    V vs[] = {{100, 40, 2, 1}, {100, 20, 2, 1}, {100, 40, 2, 2}, {100, 20, 3, 2}, {256, 16, 2, 2}, {256, 16, 2, 4},
-              {512, 8, 2, 4}, {512, 16, 2, 2}, {256, 32, 2, 2}, {128, 32, 2, 4}, {256, 16, 1, 4}, {512, 16, 1, 2}};
+    V vs[] = {{100, 40, 2, 1}, {100, 20, 2, 1}, {100, 40, 2, 2}, {100, 20, 3, 2}, {100, 10, 4, 2}, {256, 16, 2, 2}, {256, 16, 2, 4},
+              {512, 8, 2, 4}, {256, 8, 2, 4}, {128, 16, 2, 4}, {256, 16, 1, 4}, {512, 8, 1, 4}, {1024, 4, 2, 4}};
     for (const V& v : vs) {
       if ((v.W == 100) != (s.R * s.K == 100)) continue;
       char nm[64];
