@@ -13,15 +13,19 @@ python bench.py --config C5 --steps 2 --warmup 3 > "$O/bench_C5.json" 2> "$O/ben
 # the paper's strong-scaling tensor (125 GB): device-resident only (its upload alone is ~2.3 s)
 python bench.py --config P6S --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > "$O/bench_P6S.json" 2> "$O/bench_P6S.err"
 python bench.py --impl reference --steps 2 --warmup 1 > "$O/bench_ref_C2.json" 2> "$O/bench_ref_C2.err"
-for c in C2 C4; do
+for c in C2 C4 LAP; do
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$O/launches_$c.csv" \
     python bench.py --config $c --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > "$O/ncu_l_$c.log" 2>&1
   python tools/ncu_summary.py launches "$O/launches_$c.csv" > "$O/launches_$c.md"
 done
-ncu --set full --clock-control none --import-source on -k regex:"ttm_dmma|pp_update_partial|ttv_kernel" -c 4 \
+DM=sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_tensor_subpipe_dmma.sum
+ncu --set full --metrics $DM --clock-control none --import-source on -k regex:"ttm_dmma|pp_update_partial|ttv_kernel" -c 4 \
   -o "$O/full_C2" python tools/ncu_target.py C2 > "$O/ncu_full_C2.log" 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"ttv_pair|ttm_dmma" -c 3 \
+ncu --set full --metrics $DM --clock-control none --import-source on -k regex:"ttv_pair|ttm_dmma" -c 3 \
   -o "$O/full_C4" python tools/ncu_target.py C4 > "$O/ncu_full_C4.log" 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"skinny" -c 2 \
+  -o "$O/full_LAP" python tools/ncu_target.py LAP > "$O/ncu_full_LAP.log" 2>&1
+python tools/ncu_summary.py full "$O/full_LAP.ncu-rep" > "$O/ncu_full_LAP.json" 2>&1
 python tools/ncu_summary.py full "$O/full_C2.ncu-rep" > "$O/ncu_full_C2.json" 2>&1
 python tools/ncu_summary.py full "$O/full_C4.ncu-rep" > "$O/ncu_full_C4.json" 2>&1
 ls -la "$O"
