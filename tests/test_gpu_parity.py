@@ -820,3 +820,42 @@ def test_fused_build_uneven_x_l_chunks():
     for (i, j), ref in O.pp_operators(X, A).items():
         assert rel(cp.pp_get_operator(ctx, i, j), ref) < TOL, (i, j)
     cp.cp_destroy(ctx)
+
+
+_BULK_AB = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1811_10573_b200.cppp as cp
+r = np.random.default_rng(41)
+dims, K = {dims!r}, {K}
+X = r.standard_normal(dims)
+A = [r.standard_normal((d, K)) for d in dims]
+ctx = cp.cp_init(X, len(dims), dims, K)
+cp.cp_set_factors(ctx, A)
+M = cp.mttkrp_dt(ctx)
+np.savez({out!r}, *M)
+"""
+
+
+@pytest.mark.parametrize("dims,K", [((25, 25, 25, 25), 2), ((13, 97, 23), 4), ((7, 1031, 3), 2)])
+def test_skinny_bulk_kernels_bit_identical_to_register_loads(dims, K, tmp_path):
+    """The bulk-copy skinny kernels sum every output in the same ascending-x fma order as the
+    register-load kernels they replace: the MTTKRPs of one process with
+    CPPP_NO_SKINNY_BULK set and of one without are equal bit for bit."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for off in (False, True):
+        out = str(tmp_path / f"m{int(off)}.npz")
+        env = dict(os.environ)
+        env.pop("CPPP_NO_SKINNY_BULK", None)
+        if off:
+            env["CPPP_NO_SKINNY_BULK"] = "1"
+        code = _BULK_AB.format(root=root, dims=tuple(dims), K=K, out=out)
+        subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
+        with np.load(out) as z:
+            outs.append([z[f"arr_{i}"] for i in range(len(dims))])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
