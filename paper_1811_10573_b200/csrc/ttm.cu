@@ -60,11 +60,6 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 16;
 constexpr int NWARP = 16;   // consumer warps, 8 output rows each (4 per SM sub-partition)
-#ifndef CPPP_TTM_ONE_STAGE   // A/B builds: one ring stage per barrier round
-constexpr bool TWO_STAGE = true;
-#else
-constexpr bool TWO_STAGE = false;
-#endif
 constexpr int NTHREADS = (NWARP + 1) * 32;
 // scratch layout (ttm_scratch_doubles): tile counter + split tickets (TTM_CTL doubles) | split
 // partial sums (TTM_PART doubles) | padded factor (S x ttm_ld(K)) -- the control words sit at a
@@ -403,8 +398,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
 
-    // one k stage's DMMAs (stage st holds k slice kt)
-    auto stage_mma = [&](int st, int kt) {
+    for (int kt = un.k0; kt < un.k1; ++kt) {
+      const int st = cst;
+      if (kt > un.k0) mbar_wait(smem_u32(&full[st]), cph);
+      if (++cst == stages) {
+        cst = 0;
+        cph ^= 1u;
+      }
       const uint32_t sx = smem_u32(base + st * C::STAGE);
       const uint32_t sf = sx + C::XBYTES;
       const int qmax = (S - kt * BK) > 8 ? 2 : 1;   // skip an all-zero k tail
@@ -447,35 +447,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       }
-    };
-    // Two ring stages per barrier round: both waits up front, then both stages' DMMAs, then both
-    // releases -- the second stage's fragment loads need no wait in between, so the pipeline
-    // bubble of a stage boundary (all four warps of a sub-partition reach it together) is paid
-    // once per 32 k instead of once per 16.  Same DMMAs in the same order.
-    for (int kt = un.k0; kt < un.k1;) {
-      const int st = cst;
-      if (kt > un.k0) mbar_wait(smem_u32(&full[st]), cph);
-      if (++cst == stages) {
-        cst = 0;
-        cph ^= 1u;
-      }
-      const bool two = TWO_STAGE && kt + 1 < un.k1;
-      const int st2 = cst;
-      if (two) {
-        mbar_wait(smem_u32(&full[st2]), cph);
-        if (++cst == stages) {
-          cst = 0;
-          cph ^= 1u;
-        }
-      }
-      stage_mma(st, kt);
-      if (two) stage_mma(st2, kt + 1);
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(smem_u32(&empty[st]));
-        if (two) mbar_arrive(smem_u32(&empty[st2]));
-      }
-      kt += two ? 2 : 1;
+      if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
     }
 
     // ---------------- split tile: park this chunk; the last chunk to finish combines
