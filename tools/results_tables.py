@@ -42,7 +42,7 @@ def main():
             roof = f"TTM {r['achieved'] / 1000:.2f} TB/s = {r['frac']:.3f} of HBM"
         cpu = b.get("cpu_baseline") or {}
         oracle = f"{cpu['value']:.4g} sweeps/s" if cpu else "—"
-        print(f"| {name} | {b["value"]:.5g} | {b['ms_per_step']:.4g} | {mix} | {cell[0]} | {cell[1]} | "
+        print(f"| {name} | {b['value']:.5g} | {b['ms_per_step']:.4g} | {mix} | {cell[0]} | {cell[1]} | "
               f"{cell[2]} | {roof} | {oracle} |")
 
 
