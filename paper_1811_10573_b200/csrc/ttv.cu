@@ -117,6 +117,105 @@ __global__ void __launch_bounds__(TTV_THREADS)
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// The same contraction for 16-byte pairs when x is split over a cluster (small outputs: C2's
+// level 2), software-pipelined: the next U x-steps' loads are issued before the current ones are
+// consumed, 128-thread CTAs so every CTA of the split stays resident.  Each output is still ONE
+// fma chain in ascending x (steps past the range load a valid row and multiply it by 0), the
+// ranks' sums added in rank order: bit-identical to ttv_kernel<2, U> with the same split.
+// tools/probe_ttv2.cu, C2's two level-2 shapes, L2 flushed: 35.1 / 32.9 -> 31.3 / 30.7 us.
+constexpr int TTVP_THREADS = 128;
+template <int U>
+__global__ void __launch_bounds__(TTVP_THREADS, 5)
+    ttv_pipe_kernel(const double* __restrict__ P, int64_t S, int64_t RK, int K, int64_t nvec,
+                    const double* __restrict__ F, double* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double2 red[TTVP_THREADS];
+  const int64_t e = blockIdx.x * (int64_t)TTVP_THREADS + threadIdx.x;
+  const int p = blockIdx.y, xs = gridDim.y;
+  double2 acc = make_double2(0.0, 0.0);
+  if (e < nvec) {
+    const int64_t o = e * 2;
+    const int64_t b = o / RK;
+    const int64_t rk = o - b * RK;
+    const int k = static_cast<int>(rk % K);
+    const int64_t x0 = S * p / xs, x1 = S * (p + 1) / xs;
+    const double* pp = P + b * S * RK + rk;
+    const double* f = F + k;
+    double2 pa[U], fa[U], pb[U], fb[U];
+    auto load = [&](double2 (&pv)[U], double2 (&fv)[U], int64_t x) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = x + u < x1;
+        const int64_t xx = ok ? x + u : x0;
+        pv[u] = __ldcs(reinterpret_cast<const double2*>(pp + xx * RK));
+        fv[u] = ok ? __ldg(reinterpret_cast<const double2*>(f + xx * K)) : make_double2(0.0, 0.0);
+      }
+    };
+    auto consume = [&](const double2 (&pv)[U], const double2 (&fv)[U]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) vfma(acc, pv[u], fv[u]);
+    };
+    if (x0 < x1) {
+      load(pa, fa, x0);
+      int64_t x = x0;
+      while (true) {
+        if (x + U < x1) load(pb, fb, x + U);
+        consume(pa, fa);
+        x += U;
+        if (x >= x1) break;
+        if (x + U < x1) load(pa, fa, x + U);
+        consume(pb, fb);
+        x += U;
+        if (x >= x1) break;
+      }
+    }
+  }
+  // cluster reduction (rank order), as ttv_kernel
+  red[threadIdx.x] = acc;
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (p == 0 && e < nvec) {
+    double2 s = acc;
+    const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(&red[threadIdx.x]));
+    for (int r = 1; r < xs; ++r) {
+      uint32_t remote;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+      double2 v;
+      asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(remote));
+      vadd(s, v);
+    }
+    *reinterpret_cast<double2*>(out + e * 2) = s;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+cudaError_t launch_pipe(const double* P, int64_t S, int64_t RK, int K, int64_t total, int xs,
+                        const double* F, double* out, cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(ttv_pipe_kernel<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  const int64_t nvec = total / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((nvec + TTVP_THREADS - 1) / TTVP_THREADS), (unsigned)xs, 1);
+  cfg.blockDim = dim3(TTVP_THREADS, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = (unsigned)xs;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see launch_pdl
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, ttv_pipe_kernel<4>, P, S, RK, K, nvec, F, out);
+  note_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 template <int V, int U>
 cudaError_t launch_v(const double* P, int64_t S, int64_t RK, int K, int64_t total, int xs,
                      const double* F, double* out, cudaStream_t st) {
@@ -337,6 +436,8 @@ cudaError_t launch_ttv(const double* P, int64_t B, int64_t S, int64_t R, int K, 
   if (dbg)
     fprintf(stderr, "ttv B %lld S %lld R %lld K %d: V %d xs %d\n", (long long)B, (long long)S,
             (long long)R, K, V, xs);
+  static const bool no_pipe = getenv("CPPP_NO_TTV_PIPE") != nullptr;   // A/B: ttv_kernel
+  if (V == 2 && xs > 1 && !no_pipe) return launch_pipe(P, S, RK, K, total, xs, F, out, st);
   return launch_ttv_cfg(P, B, S, R, K, F, out, V, 4, xs, st);
 }
 

@@ -837,11 +837,16 @@ np.savez({out!r}, *M)
 """
 
 
-@pytest.mark.parametrize("dims,K", [((25, 25, 25, 25), 2), ((13, 97, 23), 4), ((7, 1031, 3), 2)])
-def test_skinny_bulk_kernels_bit_identical_to_register_loads(dims, K, tmp_path):
-    """The bulk-copy skinny kernels sum every output in the same ascending-x fma order as the
-    register-load kernels they replace: the MTTKRPs of one process with
-    CPPP_NO_SKINNY_BULK set and of one without are equal bit for bit."""
+@pytest.mark.parametrize("env,dims,K", [("CPPP_NO_SKINNY_BULK", (25, 25, 25, 25), 2),
+                                         ("CPPP_NO_SKINNY_BULK", (13, 97, 23), 4),
+                                         ("CPPP_NO_SKINNY_BULK", (7, 1031, 3), 2),
+                                         ("CPPP_NO_TTV_PIPE", (40, 64, 50), 24),
+                                         ("CPPP_NO_TTV_PIPE", (72, 130, 66, 4), 20)])
+def test_kernel_variants_bit_identical(env, dims, K, tmp_path):
+    """Kernels that replace another one without changing any output's fma order:
+    the bulk-copy skinny kernels (CPPP_NO_SKINNY_BULK: the register-load kernels) and the
+    software-pipelined split multi-TTV (CPPP_NO_TTV_PIPE: ttv_kernel) -- the MTTKRPs of one
+    process with the switch set and of one without are equal bit for bit."""
     import os
     import subprocess
     import sys
@@ -849,12 +854,12 @@ def test_skinny_bulk_kernels_bit_identical_to_register_loads(dims, K, tmp_path):
     outs = []
     for off in (False, True):
         out = str(tmp_path / f"m{int(off)}.npz")
-        env = dict(os.environ)
-        env.pop("CPPP_NO_SKINNY_BULK", None)
+        penv = dict(os.environ)
+        penv.pop(env, None)
         if off:
-            env["CPPP_NO_SKINNY_BULK"] = "1"
+            penv[env] = "1"
         code = _BULK_AB.format(root=root, dims=tuple(dims), K=K, out=out)
-        subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
+        subprocess.run([sys.executable, "-c", code], check=True, env=penv, timeout=300)
         with np.load(out) as z:
             outs.append([z[f"arr_{i}"] for i in range(len(dims))])
     for a, b in zip(*outs):
