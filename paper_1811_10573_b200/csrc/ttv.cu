@@ -117,12 +117,13 @@ __global__ void __launch_bounds__(TTV_THREADS)
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// The same contraction for 16-byte pairs when x is split over a cluster (small outputs: C2's
-// level 2), software-pipelined: the next U x-steps' loads are issued before the current ones are
-// consumed, 128-thread CTAs so every CTA of the split stays resident.  Each output is still ONE
-// fma chain in ascending x (steps past the range load a valid row and multiply it by 0), the
-// ranks' sums added in rank order: bit-identical to ttv_kernel<2, U> with the same split.
-// tools/probe_ttv2.cu, C2's two level-2 shapes, L2 flushed: 35.1 / 32.9 -> 31.3 / 30.7 us.
+// The same contraction for 16-byte pairs, software-pipelined: the next U x-steps' loads are
+// issued before the current ones are consumed, in 128-thread CTAs (so every CTA of an x split
+// stays resident).  Each output is still ONE fma chain in ascending x (steps past the range load
+// a valid row and multiply it by 0), the ranks' sums added in rank order: bit-identical to
+// ttv_kernel<2, U> with the same split.  tools/probe_ttv2.cu, L2 flushed: C2's two level-2
+// shapes (xs = 4) 35.1 / 32.9 -> 31.3 / 30.7 us; unsplit shapes: C3 73.9 / 75.9 / 71.9 ->
+// 71.8 / 72.3 / 71.8 us, C5 2455 -> 2445 us, LAP's last-mode level 2 65.0 -> 49.1 us.
 constexpr int TTVP_THREADS = 128;
 template <int U>
 __global__ void __launch_bounds__(TTVP_THREADS, 5)
@@ -170,6 +171,10 @@ __global__ void __launch_bounds__(TTVP_THREADS, 5)
         if (x >= x1) break;
       }
     }
+  }
+  if (xs == 1) {
+    if (e < nvec) *reinterpret_cast<double2*>(out + e * 2) = acc;
+    return;
   }
   // cluster reduction (rank order), as ttv_kernel
   red[threadIdx.x] = acc;
@@ -437,7 +442,7 @@ cudaError_t launch_ttv(const double* P, int64_t B, int64_t S, int64_t R, int K, 
     fprintf(stderr, "ttv B %lld S %lld R %lld K %d: V %d xs %d\n", (long long)B, (long long)S,
             (long long)R, K, V, xs);
   static const bool no_pipe = getenv("CPPP_NO_TTV_PIPE") != nullptr;   // A/B: ttv_kernel
-  if (V == 2 && xs > 1 && !no_pipe) return launch_pipe(P, S, RK, K, total, xs, F, out, st);
+  if (V == 2 && !no_pipe) return launch_pipe(P, S, RK, K, total, xs, F, out, st);
   return launch_ttv_cfg(P, B, S, R, K, F, out, V, 4, xs, st);
 }
 

@@ -841,7 +841,8 @@ np.savez({out!r}, *M)
                                          ("CPPP_NO_SKINNY_BULK", (13, 97, 23), 4),
                                          ("CPPP_NO_SKINNY_BULK", (7, 1031, 3), 2),
                                          ("CPPP_NO_TTV_PIPE", (40, 64, 50), 24),
-                                         ("CPPP_NO_TTV_PIPE", (72, 130, 66, 4), 20)])
+                                         ("CPPP_NO_TTV_PIPE", (72, 130, 66, 4), 20),
+                                         ("CPPP_NO_TTV_PIPE", (9, 9, 9, 9, 9, 9), 2)])
 def test_kernel_variants_bit_identical(env, dims, K, tmp_path):
     """Kernels that replace another one without changing any output's fma order:
     the bulk-copy skinny kernels (CPPP_NO_SKINNY_BULK: the register-load kernels) and the

@@ -409,11 +409,12 @@ __global__ void fill(double* p, int64_t n, uint64_t seed) {
 int main() {
   setvbuf(stdout, nullptr, _IONBF, 0);
   struct Shape { const char* name; int64_t B, S, R; int K; };
-  Shape shapes[] = {{"C2 M0 (contract middle)", 400, 400, 1, 100},
-                    {"C2 M1 (contract first)", 1, 400, 400, 100},
-                    {"C3 lvl2 (100^3 x50 mid)", 100, 100, 100, 50},
+  Shape shapes[] = {{"C3 lvl2 (100^3 x50 mid)", 100, 100, 100, 50},
                     {"C3 lvl2 last", 10000, 100, 1, 50},
-                    {"C3 lvl2 first", 1, 100, 10000, 50}};
+                    {"C3 lvl2 first", 1, 100, 10000, 50},
+                    {"C5 lvl2 (256^3 x128 mid)", 256, 256, 256, 128},
+                    {"LAP lvl2 last (25^4 x 25 x 2)", 390625, 25, 1, 2},
+                    {"LAP lvl2 first (25 x 25^4 x 2)", 1, 25, 390625, 2}};
   const int64_t PN = 256ll * 256 * 256 * 128;
   double *P, *F, *out, *ref, *flush;
   cudaMalloc(&P, 8 * PN);
@@ -461,17 +462,11 @@ int main() {
                bytes / us / 1e6, md / mr, e == cudaSuccess ? "" : cudaGetErrorString(e));
       }
     };
-    run("lib (launch_ttv rule)", [&] { cppp::launch_ttv_cfg(P, s.B, s.S, s.R, s.K, F, out, 2, 4,
-        s.B * s.R * s.K / 2 / 256 < 148 ? 4 : 1, 0); });
-    struct V { int W, XG, NS, xs; };
-    V vs[] = {{100, 40, 2, 1}, {100, 20, 2, 1}, {100, 40, 2, 2}, {100, 20, 3, 2}, {100, 10, 4, 2}, {256, 16, 2, 2}, {256, 16, 2, 4},
-              {512, 8, 2, 4}, {256, 8, 2, 4}, {128, 16, 2, 4}, {256, 16, 1, 4}, {512, 8, 1, 4}, {1024, 4, 2, 4}};
-    for (const V& v : vs) {
-      if ((v.W == 100) != (s.R * s.K == 100)) continue;
-      char nm[64];
-      snprintf(nm, 64, "bulk W%d XG%d NS%d xs%d", v.W, v.XG, v.NS, v.xs);
-      run(nm, [&] { run_bulk(P, s.B, s.S, s.R, s.K, F, out, v.W, v.XG, v.NS, v.xs); });
-    }
+    run("lib xs1", [&] { cppp::launch_ttv_cfg(P, s.B, s.S, s.R, s.K, F, out, 2, 4, 1, 0); });
+    run("pipe U4 T128 m5 xs1", [&] { launch_pipe<4, 128, 5>(P, s.B, s.S, s.R, s.K, F, out, 1); });
+    run("pipe U4 T256 m2 xs1", [&] { launch_pipe<4, 256, 2>(P, s.B, s.S, s.R, s.K, F, out, 1); });
+    run("pipe U2 T128 m8 xs1", [&] { launch_pipe<2, 128, 8>(P, s.B, s.S, s.R, s.K, F, out, 1); });
+    run("pipe U8 T128 m2 xs1", [&] { launch_pipe<8, 128, 2>(P, s.B, s.S, s.R, s.K, F, out, 1); });
   }
   return 0;
 }
