@@ -262,13 +262,14 @@ cudaError_t launch_v(const double* P, int64_t S, int64_t RK, int K, int64_t tota
 // Each output is owned by one thread and summed in ascending x (with the x split of
 // launch_ttv: cluster partials added in rank order) -- the same fma chain as ttv_kernel.
 // single jobs (Sa = 1): ttv_kernel's arithmetic per job, the x split over a (1, xs, 1) cluster
-template <int V>
-__global__ void __launch_bounds__(TTV_THREADS)
+// (V = 2: 128-thread CTAs and ttv_pipe_kernel's software-pipelined x loop, the same fma chain)
+template <int V, int THR = TTV_THREADS>
+__global__ void __launch_bounds__(THR, THR == TTV_THREADS ? 1 : 5)
     ttv_batch_kernel(const __grid_constant__ TtvBatch bt) {
   using T = typename Vec<V>::T;
   pdl_wait();
   pdl_trigger();
-  __shared__ T red[TTV_THREADS];
+  __shared__ T red[THR];
   int ji = 0;
   while (ji + 1 < bt.njobs && (int)blockIdx.x >= bt.j[ji + 1].cta0) ++ji;
   const double* __restrict__ P = bt.j[ji].P;
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(TTV_THREADS)
   const int64_t IN = bt.j[ji].IN, S = bt.j[ji].Sb, nvec = bt.j[ji].nvec;
   const bool stream = bt.j[ji].stream != 0;
   const int K = bt.K;
-  const int64_t e = ((int64_t)blockIdx.x - bt.j[ji].cta0) * TTV_THREADS + threadIdx.x;
+  const int64_t e = ((int64_t)blockIdx.x - bt.j[ji].cta0) * THR + threadIdx.x;
   const int p = blockIdx.y, xs = gridDim.y;
   T acc;
   if constexpr (V == 1) acc = 0.0;
@@ -291,6 +292,39 @@ __global__ void __launch_bounds__(TTV_THREADS)
     const double* pp = P + b * S * IN + t;
     const double* f = F + k;
     int64_t x = x0;
+    if constexpr (THR != TTV_THREADS) {
+      constexpr int U = 4;
+      T pa[U], fa[U], pb[U], fb[U];
+      auto load = [&](T (&pv)[U], T (&fv)[U], int64_t xb) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool ok = xb + u < x1;
+          const int64_t xx = ok ? xb + u : x0;
+          pv[u] = stream ? Vec<V>::ld_stream(pp + xx * IN) : Vec<V>::ld(pp + xx * IN);
+          if (ok) fv[u] = Vec<V>::ld(f + xx * K);
+          else if constexpr (V == 1) fv[u] = 0.0;
+          else fv[u] = make_double2(0.0, 0.0);
+        }
+      };
+      auto consume = [&](const T (&pv)[U], const T (&fv)[U]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) vfma(acc, pv[u], fv[u]);
+      };
+      if (x0 < x1) {
+        load(pa, fa, x0);
+        while (true) {
+          if (x + U < x1) load(pb, fb, x + U);
+          consume(pa, fa);
+          x += U;
+          if (x >= x1) break;
+          if (x + U < x1) load(pa, fa, x + U);
+          consume(pb, fb);
+          x += U;
+          if (x >= x1) break;
+        }
+      }
+      x = x1;
+    }
     for (; x + 4 <= x1; x += 4) {
       T pv[4], fv[4];
 #pragma unroll
@@ -382,10 +416,11 @@ __global__ void __launch_bounds__(TTV_THREADS, 2)
 }
 
 template <typename Kern>
-cudaError_t launch_batch_k(Kern kern, const TtvBatch& bt, int ctas, int xs, cudaStream_t st) {
+cudaError_t launch_batch_k(Kern kern, const TtvBatch& bt, int ctas, int xs, cudaStream_t st,
+                           int threads = TTV_THREADS) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)ctas, (unsigned)xs, 1);
-  cfg.blockDim = dim3(TTV_THREADS, 1, 1);
+  cfg.blockDim = dim3((unsigned)threads, 1, 1);
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   int na = 0;
@@ -460,6 +495,8 @@ cudaError_t launch_ttv_batch(const TtvJob* jobs, int n, int K, cudaStream_t st) 
     cudaError_t e = cudaFuncSetAttribute(ttv_batch_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(ttv_batch_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(ttv_batch_kernel<2, TTVP_THREADS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -498,8 +535,18 @@ cudaError_t launch_ttv_batch(const TtvJob* jobs, int n, int K, cudaStream_t st) 
       } else {
         int xs = 1;
         while (xs < 8 && (int64_t)ctas * xs < 148LL * 2 && minS / (2 * xs) >= 16) xs *= 2;
-        e = V == 2 ? launch_batch_k(ttv_batch_kernel<2>, bt, ctas, xs, st)
-                   : launch_batch_k(ttv_batch_kernel<1>, bt, ctas, xs, st);
+        static const bool no_pipe = getenv("CPPP_NO_TTV_PIPE") != nullptr;   // A/B
+        if (V == 2 && !no_pipe) {   // the same split, 128-thread CTAs
+          int c128 = 0;
+          for (int i = 0; i < nb; ++i) {
+            bt.j[i].cta0 = c128;
+            c128 += (int)((bt.j[i].nvec + TTVP_THREADS - 1) / TTVP_THREADS);
+          }
+          e = launch_batch_k(ttv_batch_kernel<2, TTVP_THREADS>, bt, c128, xs, st, TTVP_THREADS);
+        } else {
+          e = V == 2 ? launch_batch_k(ttv_batch_kernel<2>, bt, ctas, xs, st)
+                     : launch_batch_k(ttv_batch_kernel<1>, bt, ctas, xs, st);
+        }
       }
       if (e != cudaSuccess) return e;
     }

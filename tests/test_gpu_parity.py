@@ -832,7 +832,11 @@ X = r.standard_normal(dims)
 A = [r.standard_normal((d, K)) for d in dims]
 ctx = cp.cp_init(X, len(dims), dims, K)
 cp.cp_set_factors(ctx, A)
-M = cp.mttkrp_dt(ctx)
+M = list(cp.mttkrp_dt(ctx))
+cp.pp_build_operators(ctx)
+N = len(dims)
+M += [cp.pp_get_operator(ctx, i, j) for i in range(N) for j in range(i + 1, N)]
+M += [cp.pp_get_single(ctx, n) for n in range(N)]
 np.savez({out!r}, *M)
 """
 
@@ -842,12 +846,14 @@ np.savez({out!r}, *M)
                                          ("CPPP_NO_SKINNY_BULK", (7, 1031, 3), 2),
                                          ("CPPP_NO_TTV_PIPE", (40, 64, 50), 24),
                                          ("CPPP_NO_TTV_PIPE", (72, 130, 66, 4), 20),
-                                         ("CPPP_NO_TTV_PIPE", (9, 9, 9, 9, 9, 9), 2)])
+                                         ("CPPP_NO_TTV_PIPE", (9, 9, 9, 9, 9, 9), 2),
+                                         ("CPPP_NO_TTV_PIPE", (12, 10, 9, 11, 8, 7), 16)])
 def test_kernel_variants_bit_identical(env, dims, K, tmp_path):
     """Kernels that replace another one without changing any output's fma order:
     the bulk-copy skinny kernels (CPPP_NO_SKINNY_BULK: the register-load kernels) and the
-    software-pipelined split multi-TTV (CPPP_NO_TTV_PIPE: ttv_kernel) -- the MTTKRPs of one
-    process with the switch set and of one without are equal bit for bit."""
+    software-pipelined multi-TTVs (CPPP_NO_TTV_PIPE: ttv_kernel and the 256-thread batched
+    kernel) -- the MTTKRPs, PP operators and single-mode operators of one process with the
+    switch set and of one without are equal bit for bit."""
     import os
     import subprocess
     import sys
@@ -862,6 +868,7 @@ def test_kernel_variants_bit_identical(env, dims, K, tmp_path):
         code = _BULK_AB.format(root=root, dims=tuple(dims), K=K, out=out)
         subprocess.run([sys.executable, "-c", code], check=True, env=penv, timeout=300)
         with np.load(out) as z:
-            outs.append([z[f"arr_{i}"] for i in range(len(dims))])
+            outs.append([z[k] for k in sorted(z.files, key=lambda f: int(f.split("_")[1]))])
+    assert len(outs[0]) == len(outs[1]) > len(dims)
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
