@@ -212,8 +212,11 @@ __global__ void __launch_bounds__(GF_THREADS, 1)
   // (sticky) and acted on after the loop.
   // shared-window addresses computed once (the generic-pointer form re-derived the window base
   // with an S2R on every pivot, on the chain in front of the column load)
-  const uint32_t colb0 = smem_addr(&colb[0][0]), rdv0 = smem_addr(&rdv[0]);
-  const uint32_t my_l = colb0 + 8u * static_cast<uint32_t>(l), my_rows = colb0 + 8u * static_cast<uint32_t>(r0);
+  uint32_t colb0 = smem_addr(&colb[0][0]), rdv0 = smem_addr(&rdv[0]);
+  uint32_t my_l = colb0 + 8u * static_cast<uint32_t>(l), my_rows = colb0 + 8u * static_cast<uint32_t>(r0);
+  // opaque to the compiler: otherwise it re-derives them from the shared window base (S2R
+  // SR_CgaCtaId + LEA) inside the pivot loop, on the chain in front of every column load
+  asm volatile("" : "+r"(rdv0), "+r"(my_l), "+r"(my_rows));
   for (int j = 0; j < K; ++j) {
     const uint32_t bo = (j & 1) ? 128u * 8u : 0u;   // colb[b] / colb[b ^ 1]
     if (lowerw && r0 + 15 > j && 32 * cg + 31 > j && l > j) {
