@@ -8,9 +8,10 @@
 // which walks its x range in ascending order (deterministic, no atomics); consecutive threads own
 // consecutive (r, k) so every x step is a coalesced row read of the parent.
 //
-// Every child of a tree node is its own pass over the parent (a one-pass variant for all the
-// children of a parent was analysed and not built: the children reduce along different axes, so
-// a one-pass kernel needs partial outputs per block along each axis — DESIGN.md §11).
+// Kernels: ttv_pipe_kernel (16-byte pairs, software-pipelined x loop) and ttv_kernel (odd K)
+// for single contractions; ttv_batch_kernel (one launch per construction-tree level) and
+// ttv_pair_kernel (two children of one parent that contract adjacent kept modes, one pass over
+// the parent) for the batched jobs below.
 #include "internal.h"
 
 #include <cstdio>
