@@ -19,7 +19,7 @@ for c in C2 C4 LAP; do
   python tools/ncu_summary.py launches "$O/launches_$c.csv" > "$O/launches_$c.md"
 done
 DM=sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_tensor_subpipe_dmma.sum
-ncu --set full --metrics $DM --clock-control none --import-source on -k regex:"ttm_dmma|pp_update_partial|ttv_kernel" -c 4 \
+ncu --set full --metrics $DM --clock-control none --import-source on -k regex:"ttm_dmma|pp_update_partial|ttv_pipe|ttv_kernel" -c 5 \
   -o "$O/full_C2" python tools/ncu_target.py C2 > "$O/ncu_full_C2.log" 2>&1
 ncu --set full --metrics $DM --clock-control none --import-source on -k regex:"ttv_pair|ttm_dmma" -c 3 \
   -o "$O/full_C4" python tools/ncu_target.py C4 > "$O/ncu_full_C4.log" 2>&1
