@@ -111,6 +111,8 @@ struct cppp_ctx {
   cudaStream_t st2 = nullptr;           // side stream: Γ^(n) inverse overlapped with M^(n)
   cudaStream_t st3 = nullptr;           // order-3 DT: the second first-level TTM, overlapped
   cudaEvent_t ev_F = nullptr, ev_T = nullptr;   // st3 fork / join
+  cudaStream_t st4 = nullptr;           // PP sweep: the next mode's early update terms
+  cudaEvent_t ev_pf = nullptr, ev_pe[2] = {nullptr, nullptr};   // st4 fork / joins
   cudaEvent_t ev_S = nullptr, ev_P = nullptr;
   int prefetched = -1;                  // mode whose Γ inverse is issued on st2
   double* rowstat = nullptr; // max local rows x 4
@@ -126,6 +128,7 @@ struct cppp_ctx {
   // that they are all-reduced in one call (C-d), then they are copied to S_all[q] / stats
   double* qhdr = nullptr;
   double* pp_partial = nullptr;
+  double* pp_part_early[2] = {nullptr, nullptr};   // split PP update: early-term partials
   double* sq_partial = nullptr;
   double* gath = nullptr;    // gather scratch (max s x K)
   double* chk = nullptr;     // pp_error: M~ scratch (max s x K), [N][3][K] sums x 2, [3][N][K] out
@@ -1285,9 +1288,116 @@ cppp_status pp_exchange_terms(cppp_ctx* c, int m0, int m1) {
   return allreduce(c, c->T[f], (size_t)(c->T[l] - c->T[f]) + (size_t)c->dl[l] * c->K);
 }
 
+// Split PP update (unsharded, small operators): mode n's terms other than i = n-1 need only
+// factors final before mode n-1's solve, so they are issued on st4 right after mode n-1's own
+// update (capped to one CTA per SM, so that mode n-1's solves still find room); at mode n only
+// the i = n-1 term is on the chain, then a combine of both partial sets.  Measured (A/B with
+// CPPP_NO_PP_SPLIT): PP sweeps LAP 96 -> 78 us, P6W 97 -> 79 us; with large operators the
+// capped early launch is too slow for its window (C2's 128 MB operators: 207 -> 279 us, C3's
+// 4 MB: 164 -> 170 us), so only operators of at most 1 MiB take it.
+bool pp_split_on(const cppp_ctx* c) {
+  static const bool off = getenv("CPPP_NO_PP_SPLIT") != nullptr;
+  if (off || c->q >= 0 || c->N < 3) return false;
+  for (int i = 0; i < c->N; ++i)
+    for (int j = i + 1; j < c->N; ++j)
+      if (8.0 * c->dl[i] * c->dl[j] * c->K > (1 << 20)) return false;
+  return true;
+}
+
+// the terms of mode n in `sel` (bit i: term i) into a
+void pp_terms_sel(cppp_ctx* c, int n, uint32_t sel, PPUpdateArgs* a) {
+  pp_terms(c, n, false, a, ~sel);
+}
+
+cppp_status pp_sweep_split(cppp_ctx* c, bool after_build) {
+  const int N = c->N;
+  const uint32_t all = (1u << N) - 1;
+  int xsE[2] = {0, 0};
+  auto zero_of = [&](int n) {
+    uint32_t z = 0u;
+    if (after_build)
+      for (int i = n + 1; i < N; ++i) z |= 1u << i;
+    return z;
+  };
+  auto early_mask = [&](int n) {   // mode n's terms except i = n-1 (all of them for n = 0)
+    uint32_t m = all & ~(1u << n) & ~zero_of(n);
+    if (n > 0) m &= ~(1u << (n - 1));
+    return m;
+  };
+  auto base_args = [&](int n, PPUpdateArgs* a) {
+    a->Mp = c->Mp[n];
+    a->extra = nullptr;
+    a->ny = c->dl[n];
+    a->K = c->K;
+    a->out = c->M[n];
+    a->partial = c->pp_partial;
+  };
+    // the early terms of mode m, on st4 after everything issued so far on the main stream
+  auto issue_early = [&](int m) -> cppp_status {
+    xsE[m & 1] = 0;
+    if (m >= N) return CPPP_OK;
+    PPUpdateArgs a;
+    base_args(m, &a);
+    pp_terms_sel(c, m, early_mask(m), &a);
+    if (a.nterms == 0 || c->dry) return CPPP_OK;
+    CUCHK(c, cudaEventRecord(c->ev_pf, c->st));
+    CUCHK(c, cudaStreamWaitEvent(c->st4, c->ev_pf, 0));
+    {
+      double bytes = 0.0, flops = 0.0;
+      for (int i = 0; i < a.nterms; ++i) {
+        bytes += 8.0 * (a.t[i].nx * a.ny * a.K + a.t[i].nx * a.K);
+        flops += 2.0 * a.t[i].nx * a.ny * a.K;
+      }
+      Prof p(c, CPPP_K_PPUPDATE, flops, bytes, c->st4);
+      CUCHK(c, launch_pp_partial(a, c->pp_part_early[m & 1], 148, &xsE[m & 1], c->st4));
+    }
+    CUCHK(c, cudaEventRecord(c->ev_pe[m & 1], c->st4));
+    return CPPP_OK;
+  };
+  for (int n = 0; n < N; ++n) {
+    PPUpdateArgs a;
+    base_args(n, &a);
+    if (n == 0) {
+      pp_terms(c, 0, false, &a, zero_of(0));
+      if (a.nterms == 0) {   // after a build: M~^(0) = M_p^(0)
+        STCHK(issue_early(1));
+        STCHK(finish_mode(c, 0, c->Mp[0], true));
+        continue;
+      }
+      if (!c->dry && pp_stagger(c)) CUCHK(c, launch_stagger(c->st));
+      STCHK(pp_update_mode(c, 0, c->M[0], nullptr, false, c->Mp[0], zero_of(0)));
+      STCHK(issue_early(1));
+      STCHK(finish_mode(c, 0, c->M[0], true));
+      continue;
+    }
+    // the late term (i = n-1) on the main stream, then the early ones of mode n+1 beside it
+    uint32_t late = (1u << (n - 1)) & ~zero_of(n);
+    PPUpdateArgs al;
+    base_args(n, &al);
+    pp_terms_sel(c, n, late, &al);
+    int xsL = 0;
+    if (!c->dry) {
+      double bytes = 8.0 * 2.0 * al.ny * al.K, flops = 0.0;
+      for (int i = 0; i < al.nterms; ++i) {
+        bytes += 8.0 * (al.t[i].nx * al.ny * al.K + al.t[i].nx * al.K);
+        flops += 2.0 * al.t[i].nx * al.ny * al.K;
+      }
+      Prof p(c, CPPP_K_PPUPDATE, flops, bytes);
+      CUCHK(c, launch_pp_partial(al, c->pp_partial, 0, &xsL, c->st));
+      if (xsE[n & 1] > 0) CUCHK(c, cudaStreamWaitEvent(c->st, c->ev_pe[n & 1], 0));
+      CUCHK(c, launch_pp_combine2(al, c->pp_part_early[n & 1], xsE[n & 1], c->pp_partial, xsL, c->st));
+    }
+    STCHK(issue_early(n + 1));
+    STCHK(finish_mode(c, n, c->M[n], true));
+  }
+  if (c->policy == CPPP_POLICY_BOUND) STCHK(pp_monitor(c));
+  return CPPP_OK;
+}
+
 cppp_status run_pp_sweep(cppp_ctx* c, bool after_build) {
   const int N = c->N, q = c->q;
   const bool sh = q >= 0 && comm_on(c);
+  if (!sh && pp_split_on(c)) return pp_sweep_split(c, after_build);
   // Modes n < q see the current dA^(q) (the previous PP sweep's): form their exchange terms here,
   // from the live dA^(q), so nothing written to T between sweeps (pp_update, pp_second_order) can
   // leak in.  After a build dA^(q) = 0 and those terms vanish.
@@ -1638,6 +1748,8 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
         }
       }
   size_t oPP = take(sizeof(double) * pp_update_scratch_doubles(smax, K, smax));
+  size_t oPE0 = take(sizeof(double) * pp_update_scratch_doubles(smax, K, smax));
+  size_t oPE1 = take(sizeof(double) * pp_update_scratch_doubles(smax, K, smax));
   size_t oSq = take(sizeof(double) * 2048);
   size_t oGath = take(sizeof(double) * smax * K);
   size_t oChk = take(sizeof(double) * (smax * K + 9 * N * K));
@@ -1682,6 +1794,8 @@ cppp_status assign_buffers(cppp_ctx* c, bool borrow, Plan* plan) {
   c->ops_red_count = (red_hi - red_lo) / sizeof(double);
   c->qhdr = reinterpret_cast<double*>(b + oQh);
   c->pp_partial = reinterpret_cast<double*>(b + oPP);
+  c->pp_part_early[0] = reinterpret_cast<double*>(b + oPE0);
+  c->pp_part_early[1] = reinterpret_cast<double*>(b + oPE1);
   c->sq_partial = reinterpret_cast<double*>(b + oSq);
   c->gath = reinterpret_cast<double*>(b + oGath);
   c->chk = reinterpret_cast<double*>(b + oChk);
@@ -1911,6 +2025,10 @@ cppp_status cp_init(cppp_ctx** out, const double* X, int N, const int64_t* s, in
     CUCHK(c, cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, hi));
   }
   CUCHK(c, cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
+  CUCHK(c, cudaStreamCreateWithFlags(&c->st4, cudaStreamNonBlocking));
+  CUCHK(c, cudaEventCreateWithFlags(&c->ev_pf, cudaEventDisableTiming));
+  CUCHK(c, cudaEventCreateWithFlags(&c->ev_pe[0], cudaEventDisableTiming));
+  CUCHK(c, cudaEventCreateWithFlags(&c->ev_pe[1], cudaEventDisableTiming));
   CUCHK(c, cudaEventCreateWithFlags(&c->ev_F, cudaEventDisableTiming));
   CUCHK(c, cudaEventCreateWithFlags(&c->ev_T, cudaEventDisableTiming));
   CUCHK(c, cudaEventCreateWithFlags(&c->ev_S, cudaEventDisableTiming));
@@ -2487,6 +2605,7 @@ void cp_destroy(cppp_ctx* c) {
   if (!c) return;
   if (c->st) cudaStreamSynchronize(c->st);
   if (c->st3) cudaStreamSynchronize(c->st3);
+  if (c->st4) cudaStreamSynchronize(c->st4);
   if (c->st2) cudaStreamSynchronize(c->st2);
   prof_collect(c);
   for (auto e : c->evpool) cudaEventDestroy(e);
@@ -2509,6 +2628,10 @@ void cp_destroy(cppp_ctx* c) {
   if (c->ev_P) cudaEventDestroy(c->ev_P);
   if (c->st2) cudaStreamDestroy(c->st2);
   if (c->st3) cudaStreamDestroy(c->st3);
+  if (c->st4) cudaStreamDestroy(c->st4);
+  if (c->ev_pf) cudaEventDestroy(c->ev_pf);
+  for (auto& ev : c->ev_pe)
+    if (ev) cudaEventDestroy(ev);
   if (c->ev_F) cudaEventDestroy(c->ev_F);
   if (c->ev_T) cudaEventDestroy(c->ev_T);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);

@@ -196,6 +196,12 @@ struct PPUpdateArgs {
   double* partial;        // scratch for split-x partial sums (>= xsplit * ny * K doubles)
 };
 cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st);
+// the two halves of a split update: partial sums of a term subset into `partial` (*xs_used parts;
+// grid_cap > 0 caps the CTAs), then out = (Mp [+ extra]) + (Σ pE parts + Σ pL parts)
+cudaError_t launch_pp_partial(const PPUpdateArgs& a, double* partial, int grid_cap, int* xs_used,
+                              cudaStream_t st);
+cudaError_t launch_pp_combine2(const PPUpdateArgs& a, const double* pE, int xsE, const double* pL,
+                               int xsL, cudaStream_t st);
 size_t pp_update_scratch_doubles(int64_t ny, int K, int64_t max_nx);
 
 

@@ -168,6 +168,25 @@ __global__ void pp_update_combine(PPUpdateArgs a, int xsplit) {
   }
 }
 
+// The combine of a PP update split in two partial launches (the early terms computed during the
+// previous mode's window, the late term after it): out = (M_p [+ extra]) + (Σ early parts + Σ late
+// parts), every sum in a fixed order.
+__global__ void pp_update_combine2(PPUpdateArgs a, const double* __restrict__ pE, int xsE,
+                                   const double* __restrict__ pL, int xsL) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t total = a.ny * a.K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int p = 0; p < xsE; ++p) v += pE[p * total + e];
+    for (int p = 0; p < xsL; ++p) v += pL[p * total + e];
+    double m = a.Mp ? a.Mp[e] : 0.0;
+    if (a.extra) m += a.extra[e];
+    a.out[e] = m + v;
+  }
+}
+
 int choose_xsplit(int64_t ny, int64_t max_nx) {
   // the aligned kernel walks (y, part) items grid-stride with 4 CTAs/SM: make ~4 items per CTA
   // slot; keep >= 8 x per part
@@ -186,6 +205,9 @@ size_t pp_update_scratch_doubles(int64_t ny, int K, int64_t max_nx) {
   (void)max_nx;
   return static_cast<size_t>(16) * ny * K;
 }
+
+cudaError_t launch_pp_partial(const PPUpdateArgs& a, double* partial, int grid_cap, int* xs_used,
+                              cudaStream_t st);
 
 cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st) {
   if (a.ny == 0) return cudaSuccess;
@@ -226,6 +248,56 @@ cudaError_t launch_pp_update(const PPUpdateArgs& a, cudaStream_t st) {
   int blocks = (int)((total + 255) / 256);
   if (blocks > 1184) blocks = 1184;
   cudaError_t e = launch_pdl(pp_update_combine, dim3(blocks), dim3(256), 0, st, a, xs_used);
+  note_launch();
+  return e;
+}
+
+// The partial kernel alone, into `partial` (>= 16 ny K doubles); *xs_used = its x parts (0 when
+// there are no terms: nothing launched).  grid_cap > 0 caps the CTAs (a side-stream launch that
+// must leave room on every SM).
+cudaError_t launch_pp_partial(const PPUpdateArgs& a, double* partial, int grid_cap, int* xs_used,
+                              cudaStream_t st) {
+  *xs_used = 0;
+  if (a.ny == 0 || a.nterms == 0) return cudaSuccess;
+  if (a.K > NT) return cudaErrorInvalidValue;
+  PPUpdateArgs b = a;
+  b.partial = partial;
+  int64_t max_nx = 1;
+  for (int i = 0; i < b.nterms; ++i) max_nx = b.t[i].nx > max_nx ? b.t[i].nx : max_nx;
+  bool aligned = (b.K % 2) == 0;
+  for (int i = 0; i < b.nterms; ++i)
+    aligned = aligned && (b.t[i].sx % 2 == 0) && (b.t[i].sy % 2 == 0) &&
+              (reinterpret_cast<uintptr_t>(b.t[i].op) % 16 == 0) &&
+              (reinterpret_cast<uintptr_t>(b.t[i].dA) % 16 == 0);
+  if (aligned) {
+    const int64_t ngroups = (b.ny + 1) / 2;
+    int64_t xs = (148 * 3 + ngroups / 2) / ngroups;
+    const int64_t lim = max_nx / 16;
+    if (xs > lim) xs = lim;
+    if (xs > 16) xs = 16;
+    if (xs < 1) xs = 1;
+    const int64_t items = ngroups * xs;
+    int64_t grid = items < 148 * 3 ? items : 148 * 3;
+    if (grid_cap > 0 && grid > grid_cap) grid = grid_cap;
+    pp_update_partial_v4<2, 2><<<(unsigned)grid, 256, 0, st>>>(b, static_cast<int>(xs));
+    *xs_used = static_cast<int>(xs);
+  } else {
+    const int xsplit = choose_xsplit(b.ny, max_nx);
+    dim3 grid((unsigned)b.ny, (unsigned)xsplit);
+    pp_update_partial<<<grid, NT, 0, st>>>(b, xsplit);
+    *xs_used = xsplit;
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pp_combine2(const PPUpdateArgs& a, const double* pE, int xsE, const double* pL,
+                               int xsL, cudaStream_t st) {
+  if (a.ny == 0) return cudaSuccess;
+  const int64_t total = a.ny * a.K;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  cudaError_t e = launch_pdl(pp_update_combine2, dim3(blocks), dim3(256), 0, st, a, pE, xsE, pL, xsL);
   note_launch();
   return e;
 }
